@@ -1,0 +1,273 @@
+#!/usr/bin/env python
+"""Benchmark: ASPOT iterations/s at BASELINE.json configs[2] (n = 16384,
+fp32, squared-Euclidean cost regenerated on the fly), plus time-to-eps, the
+roofline of the hot sweep kernel and the CPU oracle beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one accepted ASPOT iteration (solvers.hpp:323-369) on the
+resident problem. `value` is whole-job iterations/s from CUDA-event device
+time of exactly K steps (max over ranks); `e2e` is the same metric through
+the public API from host buffers (upload + setup + K iterations + rounding +
+download). N > 1: the plan is row-block sharded once
+the sharded path is enabled; until then ranks run independent replicas.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--epsilon", type=float, default=1e-2)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-iters", type=int, default=2, help="oracle iterations in the CPU sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tte", action="store_true", help="skip the time-to-eps solve")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 4 + k and "Active" in s[4 + k]
+                          and "Not" not in s[4 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    return rank, world, local, dist
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(x, dist, local):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference(inst, args, threads):
+    """The reference solver's CPU restatement (oracle, kind "port") timed on a
+    bounded sample of the same workload: `cpu_iters` ASPOT iterations."""
+    from oracle import binding
+    binding.lib().oracle_set_threads(threads)
+    t0 = time.perf_counter()
+    res = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=args.epsilon,
+                        max_iterations=args.cpu_iters, skip_plan=True)
+    wall = time.perf_counter() - t0
+    binding.lib().oracle_set_threads(1)
+    # the sample also pays the initial phi/grad pass: 1 sweep vs 4 per iteration
+    it = max(res.iterations, 1)
+    return {"value": it / wall, "unit": "iterations/s", "cores": threads, "kind": "port",
+            "sample": f"{it} ASPOT iterations of the same n={inst.size()} instance (fp64 oracle on the fp32-rounded "
+                      f"coordinates, {threads} host threads, incl. its initial phi/grad pass), {wall:.1f} s"}
+
+
+def flush_l2(local):
+    import torch
+    if not hasattr(flush_l2, "buf"):
+        flush_l2.buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+    flush_l2.buf.zero_()
+    torch.cuda.synchronize()
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_setup(args)
+    from paper_2601_17196_b200 import pot
+
+    inst = pot.config_instance(3, n=args.n, seed=args.seed + (rank if world > 1 else 0))
+    if inst.cost_scale is None or inst.cost_scale <= 0:
+        inst.cost_scale = pot.points_scale(inst.X, inst.Y)
+    n = inst.size()
+    threads = os.cpu_count() or 1
+    config = {"workload": f"BASELINE configs[2]: registration-shaped POT n={n}, fp32, on-the-fly sq-Euclidean cost, "
+                          f"eps={args.epsilon}, s=0.9, ASPOT",
+              "n": n, "epsilon": args.epsilon, "solver": "aspot", "cost": "on-the-fly",
+              "parallelism": f"replicas{world}" if world > 1 else "single",
+              "l2": "coordinates are L2-resident by design (on-the-fly cost); L2 flushed (256 MB write) between "
+                    "timed steps"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(inst, args, threads)
+        line = {"impl": "reference", "metric": "ASPOT iterations/s", "value": ref["value"], "unit": "iterations/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / ref["value"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config, "cpu_baseline": ref,
+                "e2e": {"value": ref["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    ctx = pot.Context(local)
+    cfg = pot.SolverConfig(epsilon=args.epsilon, log_every=10 ** 9, max_iterations=10 ** 7, record_rounded_cost=False,
+                           materialize_plan=False)
+    sess = pot.Session(pot.SolverKind.Aspot, inst, cfg, ctx=ctx)
+    sess.iterate(args.warmup)
+    k0, a0, s0 = sess.stats()
+    per_step = []
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        done = 0
+        for _ in range(args.steps):
+            flush_l2(local)
+            ms, it, fin = sess.iterate(1)
+            per_step.append(ms)
+            done += it
+            if fin:
+                break
+    torch.cuda.synchronize()
+    barrier(dist)
+    k1, a1, s1 = sess.stats()
+    total_ms = sum(per_step)
+    total_ms = max_over_ranks(total_ms, dist, local)
+    value = world * done / (total_ms / 1000.0) if total_ms > 0 else 0.0
+    sweeps_per_it = (s1 - s0) / max(done, 1)
+    # roofline of the dominant kernel (the on-the-fly sweep): MUFU ex2 bound
+    ms_sweep, elems, _ = sess.time_sweep(20)
+    clocks = clk.summary()
+    sess.close()
+
+    # stored-cost variant of the same shape (C materialised once on the
+    # device, fp32, 1 GiB) for the HBM roofline of the stored sweep
+    stored = None
+    try:
+        st_inst = pot.Instance(r=inst.r, c=inst.c, s=inst.s, X=inst.X, Y=inst.Y, cost_scale=inst.cost_scale,
+                               dtype=pot.DType.F32)
+        st_inst.stored = True
+        ss = pot.Session(pot.SolverKind.Aspot, st_inst, cfg, ctx=ctx)
+        ss.iterate(2)
+        ms_st, el_st, by_st = ss.time_sweep(10)
+        ss.close()
+        peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        stored = {"bound": "hbm", "achieved": by_st / (ms_st * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                  "frac": by_st / (ms_st * 1e-3) / 1e9 / hbm, "traffic": None,
+                  "kernel": "sweep_f32<SrcDenseF32>", "ms_per_launch": ms_st,
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    except Exception as e:  # pragma: no cover
+        stored = {"error": str(e)}
+
+    # time-to-eps (the reference's wall_seconds: solver entry -> rounded plan)
+    tte = None
+    if not args.no_tte:
+        full = pot.aspot_solve(inst, pot.SolverConfig(epsilon=args.epsilon, log_every=10 ** 9, record_rounded_cost=False,
+                                                      materialize_plan=False), ctx=ctx)
+        tte = {"seconds": full.wall_seconds, "loop_seconds": full.loop_seconds, "iterations": full.iterations,
+               "status": full.status.name, "final_error": full.final_error, "tolerance": full.tolerance,
+               "cost": full.cost, "feasibility_gap": full.feasibility_gap}
+
+    # e2e: the public API from host buffers, K iterations per call
+    e2e_cfg = pot.SolverConfig(epsilon=args.epsilon, log_every=10 ** 9, max_iterations=args.steps,
+                               record_rounded_cost=False, materialize_plan=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r2 = pot.aspot_solve(inst, e2e_cfg, ctx=ctx)
+    e2e_wall = time.perf_counter() - t0
+    h2d = 8 * (inst.X.size + inst.Y.size + 2 * n)
+    d2h = 8 * (4 * n + 1)
+    e2e_val = world * r2.iterations / e2e_wall
+
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    mufu_peak = 16 * nsm * sm_mhz * 1e6 / 1e9  # G ex2/s at the measured clock
+    achieved = elems / (ms_sweep * 1e-3) / 1e9
+    roofline = {"bound": "mufu", "achieved": achieved, "peak": mufu_peak, "unit": "Gex2/s", "frac": achieved / mufu_peak,
+                "traffic": None, "kernel": "sweep_f32<SrcPointsF32>", "ms_per_launch": ms_sweep,
+                "per_unit": "1 MUFU.EX2 per plan entry; n^2 entries per launch",
+                "peak_source": f"16 ex2/clk/SM x {nsm} SMs x median SM clock {sm_mhz} MHz under load"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(inst, args, threads)
+    if rank == 0:
+        line = {"metric": "ASPOT iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
+                "steps": len(per_step), "warmup": args.warmup, "ms_per_step": total_ms / max(len(per_step), 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config, "clocks": clocks,
+                "e2e": {"value": e2e_val, "unit": "iterations/s", "h2d_bytes_per_step": h2d / max(r2.iterations, 1),
+                        "d2h_bytes_per_step": d2h / max(r2.iterations, 1),
+                        "note": "one public-API call (aspot_solve, max_iterations=K) from host buffers: upload, setup, "
+                                "K iterations, rounding, download"},
+                "gpu_launches": k1 - k0, "sweeps_per_iteration": sweeps_per_it,
+                "roofline": roofline, "roofline_stored": stored, "time_to_eps": tte, "cpu_baseline": cpu}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

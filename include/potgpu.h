@@ -1,0 +1,238 @@
+/* potgpu.h — C-ABI of the B200-native entropic partial-OT solver.
+ *
+ * Drop-in boundary for the reference's header API (namespace pot in
+ * /root/reference/proj/include/pot/). Plain pointers, sizes and POD structs
+ * only; no C++ or torch types. The C++ mirror in include/pot/ (headers) converts
+ * pot::Instance / SolverConfig <-> these structs and rethrows PotError, so a
+ * reference user keeps calling pot::solve / aspot_solve / ... unchanged.
+ *
+ * Return codes: 0 on success, else 1 + the ordinal of the reference's
+ * pot::ErrorCode (core.hpp:21-39, order preserved), or one of the
+ * POTGPU_ERR_* device codes appended after it. potgpu_last_error() gives the
+ * message (thread-local). No pointer passed in is retained after return.
+ */
+#ifndef POTGPU_H
+#define POTGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POTGPU_ABI_VERSION 1
+
+/* pot::ErrorCode ordinals + 1 (core.hpp:21-39). */
+enum potgpu_status_code {
+  POTGPU_OK = 0,
+  POTGPU_DIMENSION_MISMATCH = 1,
+  POTGPU_NEGATIVE_ENTRY = 2,
+  POTGPU_NON_FINITE_ENTRY = 3,
+  POTGPU_BUDGET_EXCEEDS_MASS = 4,
+  POTGPU_OVERFLOW = 5,
+  POTGPU_NON_POSITIVE_ARGUMENT = 6,
+  POTGPU_DEGENERATE_INSTANCE = 7,
+  POTGPU_PENALTY_TOO_SMALL = 8,
+  POTGPU_UNBALANCED_MARGINALS = 9,
+  POTGPU_ZERO_ENTROPY = 10,
+  POTGPU_INFEASIBLE = 11,
+  POTGPU_SIZE_LIMIT_EXCEEDED = 12,
+  POTGPU_ZERO_MASS_PLAN = 13,
+  POTGPU_DEGENERATE_SVD = 14,
+  POTGPU_EMPTY_INPUT = 15,
+  POTGPU_INVALID_ARGUMENT = 16,
+  POTGPU_IO_FAILURE = 17,
+  /* appended: device-side failures with no reference counterpart */
+  POTGPU_ERR_CUDA = 18,
+  POTGPU_ERR_NCCL = 19,
+  POTGPU_ERR_UNSUPPORTED = 20
+};
+
+/* pot::SolverKind (core.hpp:223). */
+enum potgpu_solver_kind { POTGPU_ASPOT = 0, POTGPU_FEASIBLE_SINKHORN = 1, POTGPU_TUNED_SINKHORN = 2 };
+/* pot::BlockRule (core.hpp:221). */
+enum potgpu_block_rule { POTGPU_GREEDY = 0, POTGPU_ROUND_ROBIN = 1 };
+/* pot::SolveStatus (core.hpp:284). */
+enum potgpu_solve_status { POTGPU_CONVERGED = 0, POTGPU_MAX_ITERATIONS_EXCEEDED = 1, POTGPU_STEP_SIZE_UNDERFLOW = 2 };
+/* Arithmetic of the n^2 sweeps. F64: the reference's IEEE-double semantics.
+ * F32: fp32 cost stream + MUFU ex2 with exact per-tile shifts, fp64
+ * potentials and accumulation across tiles. */
+enum potgpu_dtype { POTGPU_F64 = 0, POTGPU_F32 = 1 };
+/* Cost representation. DENSE: stored n x n matrix streamed from HBM.
+ * SQEUCLIDEAN: C_ij = cost_scale * |x_i - y_j|^2 regenerated per tile from
+ * n x d point coordinates (d <= 4); never materialised. */
+enum potgpu_cost_kind {
+  POTGPU_COST_DENSE = 0,
+  POTGPU_COST_SQEUCLIDEAN = 1,
+  /* points given as for SQEUCLIDEAN, but the cost is built once on the device
+   * and STORED (n x n in the problem dtype), then streamed like DENSE. */
+  POTGPU_COST_SQEUCLIDEAN_STORED = 2
+};
+
+/* pot::Instance (core.hpp:108-118) plus the cost representation. All host
+ * pointers (device pointers when device_ptrs = 1). */
+typedef struct potgpu_problem {
+  int64_t n;
+  int dtype;            /* potgpu_dtype */
+  int cost_kind;        /* potgpu_cost_kind */
+  /* DENSE: element (i, j) at C[i*ldc + j] if row_major, else C[i + j*ldc]
+   * (Eigen's column-major MatrixXd layout, core.hpp:19). */
+  const double* C;
+  int64_t ldc;
+  int row_major;
+  /* SQEUCLIDEAN: X, Y are n x d row-major; cost_scale <= 0 means 1/max C. */
+  const double* X;
+  const double* Y;
+  int d;
+  double cost_scale;
+  const double* r;
+  const double* c;
+  double s;
+  int device_ptrs;
+} potgpu_problem;
+
+/* pot::SolverConfig (core.hpp:241-267) + device options. */
+typedef struct potgpu_config {
+  double epsilon;            /* 0.1 */
+  double gamma_override;     /* <= 0: derived (the reference's std::nullopt) */
+  int64_t max_iterations;    /* 50000 */
+  int block_rule;            /* POTGPU_GREEDY */
+  double tuning_exponent_p;  /* 1.0 */
+  int deterministic;         /* 1 (unused by the reference too, core.hpp:247) */
+  int64_t log_every;         /* 1 */
+  int record_rounded_cost;   /* 1: every trace record carries rounded_cost like the reference */
+  int materialize_plan;      /* 1: write the dense n x n plan to outputs->X */
+  int collect_iter_log;      /* 1: per-iteration decision log (outputs->iter_log) */
+  int use_graphs;            /* 1: replay the per-attempt kernel sequence as a CUDA graph */
+  int sync_every;            /* host polls the device state every k attempts (default 8) */
+} potgpu_config;
+
+typedef struct potgpu_trace_record {  /* pot::TraceRecord (core.hpp:269-275) */
+  int64_t t;
+  double error;
+  double phi;
+  double rounded_cost;  /* NaN when absent (std::nullopt) */
+  double elapsed_s;
+} potgpu_trace_record;
+
+typedef struct potgpu_iter_log {  /* decision log of one accepted ASPOT iteration */
+  int64_t t;
+  int32_t halvings;
+  int32_t block_hat;        /* Greenkhorn block picked at z_grave (solvers.hpp:340) */
+  int32_t zbest_is_check;   /* phi(z_check) <= phi_hat (solvers.hpp:342) */
+  int32_t block_check;      /* Greenkhorn block picked at z_best (solvers.hpp:344) */
+  double error;
+  double phi_check;
+  double phi_hat;
+  double theta;
+} potgpu_iter_log;
+
+/* pot::SolveResult scalars (solvers.hpp:176-186) + plan metrics. */
+typedef struct potgpu_summary {
+  int status;
+  int64_t iterations;
+  double gamma;
+  double tolerance;
+  double final_error;
+  double wall_seconds;       /* the reference's definition (solver entry -> rounded plan) */
+  double loop_seconds;       /* accepted-iteration loop only (iterations/s) */
+  int has_bounds;
+  double bound_R, bound_L, bound_mu_f, iteration_bound;
+  double cost;               /* transport_cost(C, X) of the returned plan (core.hpp:199) */
+  double feasibility_gap;    /* plan_feasibility_gap (core.hpp:207) */
+  double mass;               /* 1^T X 1 */
+  double phi;                /* dual value at the stopping iterate */
+  int64_t trace_len;
+  int64_t iter_log_len;
+  int64_t sweeps;            /* n^2 passes executed on the device */
+  int64_t attempts;          /* step attempts incl. halvings */
+  char stopping_iterate[24]; /* "z_check" | "extended-marginals" | "trivial" */
+} potgpu_summary;
+
+/* Caller-owned optional outputs (NULL / 0 capacity = not wanted). */
+typedef struct potgpu_outputs {
+  double* X;            /* n x n row-major plan, needs config.materialize_plan */
+  double* row_slack;    /* r - X 1 */
+  double* col_slack;    /* c - X^T 1 */
+  potgpu_trace_record* trace;
+  int64_t trace_cap;
+  potgpu_iter_log* iter_log;
+  int64_t iter_log_cap;
+  double* u;            /* final potentials (ASPOT: z_check; Sinkhorn: extended u[0..n], v[0..n]) */
+  double* v;
+  double* w;
+} potgpu_outputs;
+
+typedef struct potgpu_ctx potgpu_ctx;
+
+int potgpu_abi_version(void);
+const char* potgpu_last_error(void);
+void potgpu_config_default(potgpu_config* cfg);
+
+/* Context: owns the device, stream, workspaces and (optionally) the NCCL
+ * communicator of a row-block-sharded multi-GPU solve. */
+int potgpu_create(int device, potgpu_ctx** out);
+int potgpu_destroy(potgpu_ctx* ctx);
+
+/* pot::solve (solvers.hpp:591) / aspot_solve (:265) /
+ * feasible_sinkhorn_solve (:516) / tuned_sinkhorn_solve (:547, :586). */
+int potgpu_solve(potgpu_ctx* ctx, int solver_kind, const potgpu_problem* problem, const potgpu_config* config,
+                 potgpu_summary* summary, potgpu_outputs* outputs);
+
+/* Step-wise form of potgpu_solve (no reference counterpart; used to time a
+ * fixed number of iterations and to drive the loop from a host runtime):
+ * begin = validation + setup + the first evaluation (+ record(0));
+ * iterate = run until k more iterations are accepted or the solve stops
+ * (k < 0: until it stops), device time of that loop in *device_ms;
+ * finish = final rounding + outputs (the solve must have stopped).
+ * potgpu_solve == begin; iterate(-1); finish. */
+typedef struct potgpu_session potgpu_session;
+int potgpu_session_begin(potgpu_ctx* ctx, int solver_kind, const potgpu_problem* problem, const potgpu_config* config,
+                         int64_t trace_cap, int64_t iter_log_cap, potgpu_session** out);
+int potgpu_session_iterate(potgpu_session* s, int64_t k, double* device_ms, int64_t* iterations, int* finished);
+int potgpu_session_finish(potgpu_session* s, potgpu_summary* summary, potgpu_outputs* outputs);
+int potgpu_session_destroy(potgpu_session* s);
+/* Roofline probe: average device time of one hot-path sweep launch at the
+ * session's current iterate (reps back-to-back launches between CUDA events
+ * on the session stream), with the algorithmic elements (n^2 exponentials)
+ * and HBM bytes (stored cost only) of one launch. */
+int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep, double* elements, double* bytes);
+/* Counters of the session so far: kernels launched by iterate(), step
+ * attempts (incl. halvings) and n^2 sweeps executed. */
+int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* attempts, int64_t* sweeps);
+/* The context's CUDA stream (cudaStream_t), for callers that time with events. */
+void* potgpu_ctx_stream(potgpu_ctx* ctx);
+
+/* B(z) reductions at a dual point for logK = -C/gamma with marginals
+ * (r, c, s) taken from `problem` as given (no mixing): the helpers
+ * b_matrix / dual_objective / dual_gradient / feasibility_error
+ * (dual.hpp:104-141) and greenkhorn_step's sums (solvers.hpp:46-52).
+ * row/col: n doubles (B 1, B^T 1). scalars[6] = {total, max_exponent, phi,
+ * feasibility_error, grad_w, overflow(0/1)}. Returns POTGPU_OVERFLOW exactly
+ * when the reference's range checks would throw (scalars still filled). */
+int potgpu_dual_eval(potgpu_ctx* ctx, const potgpu_problem* problem, double gamma, const double* u, const double* v,
+                     double w, double* row, double* col, double* scalars);
+
+/* round_pot (rounding.hpp:46-77) on the device for a dense row-major X. */
+int potgpu_round_pot(potgpu_ctx* ctx, int64_t n, const double* X, const double* r, const double* c, double s,
+                     double* X_out);
+
+/* Multi-GPU row-block sharding (one process per GPU). rank 0 creates the id,
+ * the caller broadcasts its 128 bytes (e.g. torch.distributed), then every
+ * rank calls potgpu_comm_init before potgpu_solve. */
+int potgpu_comm_unique_id(unsigned char id_out[128]);
+int potgpu_comm_init(potgpu_ctx* ctx, int rank, int world_size, const unsigned char id[128]);
+
+/* Synthetic fixtures: make_synthetic_instance (synthetic.hpp:15-54) and the
+ * BASELINE.json config recipes. Host buffers:
+ * r, c: n; C: n*n row-major (may be NULL for point configs); X, Y: n*3. */
+int potgpu_make_synthetic(int64_t n, uint64_t seed, double mass_r, double mass_c, double s_frac, double* r, double* c,
+                          double* C, double* s);
+int potgpu_make_config(int config_id, int64_t n, uint64_t seed, double* r, double* c, double* X, double* Y, int* d,
+                       double* s, double* cost_scale);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POTGPU_H */

@@ -1,0 +1,386 @@
+// aspot_kernels.cuh — device-resident control of the accelerated solver
+// (reference: aspot_solve, solvers.hpp:265-385; Alg. 2 of PAPER.md:108-134).
+//
+// One step attempt is a fixed sequence of kernels; every decision the
+// reference takes on the host (overflow -> halve the step, Greenkhorn block
+// choice, z_best selection, stopping) is taken on the device by single-thread
+// "scalar" kernels that write gate flags. Later kernels read the gates and
+// become no-ops, so the whole attempt is replayable as one CUDA graph with no
+// host round trip; the host only polls the state every few attempts.
+#pragma once
+
+#include "common.cuh"
+
+namespace potgpu {
+
+enum PointRole { R_BAR = 0, R_GRAVE = 1, R_HAT = 2, R_CHECK = 3, R_NEW = 4, R_EVAL = 5, kRoles = 6 };
+
+enum CtlStatus { ST_RUNNING = -1 };
+
+struct TraceDev {  // mirrors potgpu_trace_record
+  int64_t t;
+  double error, phi, rounded_cost, elapsed_s;
+};
+struct IterLogDev {  // mirrors potgpu_iter_log
+  int64_t t;
+  int32_t halvings, block_hat, zbest_is_check, block_check;
+  double error, phi_check, phi_hat, theta;
+};
+
+struct RoundOut {
+  double alpha, mass3, na, nb, f, mass, cost, row_gap, col_gap, gap;
+  int infeasible, pad;
+};
+
+struct AspotCtl {
+  // gates (read by kernels)
+  int g_active;   // solve not finished
+  int g_new;      // this attempt starts a new iteration (z_bar, grad recomputed)
+  int g_alive;    // no range failure so far in this attempt
+  int g_record;   // trace record rounding pending
+  int g_round;    // rounding pipeline gate (set by the caller of the pipeline)
+  int attempt_ok;
+  int zbar_failed;
+  int keep_check;
+  int block_hat, block_check;
+  int block_rule;
+  int status;
+  int halvings;
+  int fatal;      // potgpu error code raised on the device (0 = none)
+  int record_rounded_cost;
+  int paused;     // loop stopped at pause_at (session API), not finished
+  int64_t pause_at;
+  int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
+  int64_t trace_len, trace_cap, log_len, log_cap;
+  double theta, step, gamma, eps_tilde, step_denom, s;
+  double error, phi_check, phi_hat, phi_best;
+  uint64_t t0_ns, loop_end_ns;
+  PointScalars ps[kRoles];
+  RoundOut ro;
+};
+
+__device__ __forceinline__ double theta_next_d(double th) {  // solvers.hpp:32-37
+  return th * (sqrt(th * th + 4.0) - th) / 2.0;
+}
+
+// z_bar = (1 - theta) z_check + theta z   (solvers.hpp:336, DualPoint ops dual.hpp:33-43)
+__global__ void k_zbar(AspotCtl* ctl, Slot zc, Slot z, Slot zb) {
+  if (!ctl->g_new) return;
+  const double th = ctl->theta, om = 1.0 - th;
+  const int64_t n = zb.n;
+  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+    const double a = om * zc.base[k];
+    const double b = th * z.base[k];
+    zb.base[k] = a + b;
+  }
+}
+
+// Per-point reduction of the sweep partials into B 1, B^T 1 and the scalar
+// partials of every functional the reference evaluates at that point.
+// Partials per block (fixed grid, fixed order) -> k_point_scalars.
+struct ReduceArgs {
+  Slot z;
+  const double* rowp; int64_t nstrips;
+  const double* colp; int64_t nrowblocks;
+  const double* maxp; int64_t nmax;
+  double* row_out; double* col_out;
+  const double* rt; const double* ct;  // marginals the dual targets (mixed r~, c~)
+  double* scratch;                      // [gridDim.x][kNumPartials + 1]
+  const int* gate;
+};
+
+__global__ void __launch_bounds__(kVecThreads) k_point_reduce(ReduceArgs a) {
+  if (a.gate && *a.gate == 0) return;
+  const int64_t n = a.z.n;
+  double acc[kNumPartials + 1];
+  // 0 total, 1 maxu, 2 maxv, 3 seu, 4 sev, 5 ur, 6 vc, 7 score_u, 8 score_v, 9 gl1u, 10 gl1v, 11 maxe
+#pragma unroll
+  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = 0.0;
+  acc[1] = acc[2] = acc[11] = -INFINITY;
+  const double* u = a.z.u();
+  const double* v = a.z.v();
+  for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double rb = 0.0;
+    for (int64_t s = 0; s < a.nstrips; ++s) rb += a.rowp[s * n + i];
+    double cb = 0.0;
+    for (int64_t s = 0; s < a.nrowblocks; ++s) cb += a.colp[s * n + i];
+    a.row_out[i] = rb;
+    a.col_out[i] = cb;
+    const double ui = u[i], vi = v[i];
+    const double eu = eexp(ui), ev = eexp(vi);
+    acc[0] += rb;
+    acc[1] = nan_max(acc[1], ui);
+    acc[2] = nan_max(acc[2], vi);
+    acc[3] += eu;
+    acc[4] += ev;
+    acc[5] += ui * a.rt[i];
+    acc[6] += vi * a.ct[i];
+    const double rowf = rb + eu, colf = cb + ev;
+    acc[7] += rho_limit(a.rt[i], rowf);
+    acc[8] += rho_limit(a.ct[i], colf);
+    acc[9] += fabs(rowf - a.rt[i]);
+    acc[10] += fabs(colf - a.ct[i]);
+  }
+  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
+    acc[11] = nan_max(acc[11], a.maxp[k]);
+  // fixed-order block reduction through shared memory
+  __shared__ double sh[kNumPartials + 1][kVecThreads];
+#pragma unroll
+  for (int k = 0; k < kNumPartials + 1; ++k) sh[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int stride = kVecThreads / 2; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) {
+#pragma unroll
+      for (int k = 0; k < kNumPartials + 1; ++k) {
+        const double o = sh[k][threadIdx.x + stride];
+        if (k == 1 || k == 2 || k == 11) sh[k][threadIdx.x] = nan_max(sh[k][threadIdx.x], o);
+        else sh[k][threadIdx.x] += o;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < kNumPartials + 1) a.scratch[blockIdx.x * (kNumPartials + 1) + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__device__ void reduce_scratch(const double* scratch, int nblk, PointScalars& ps) {
+  double acc[kNumPartials + 1];
+  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = (k == 1 || k == 2 || k == 11) ? -INFINITY : 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    for (int k = 0; k < kNumPartials + 1; ++k) {
+      const double x = scratch[b * (kNumPartials + 1) + k];
+      if (k == 1 || k == 2 || k == 11) acc[k] = nan_max(acc[k], x);
+      else acc[k] += x;
+    }
+  }
+  ps.total = acc[0]; ps.maxu = acc[1]; ps.maxv = acc[2]; ps.seu = acc[3]; ps.sev = acc[4];
+  ps.ur = acc[5]; ps.vc = acc[6]; ps.score_u = acc[7]; ps.score_v = acc[8]; ps.gl1u = acc[9]; ps.gl1v = acc[10];
+  ps.maxe = acc[11];
+}
+
+__device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) {  // solvers.hpp:58-68
+  const double su = ps.score_u, sv = ps.score_v, sw = rho_limit(s, ps.total);
+  int block = 0;
+  double best = su;
+  if (sv > best) { block = 1; best = sv; }
+  if (sw > best) block = 2;
+  return block;
+}
+
+// Scalar finalisation + the decision the reference takes at that point.
+__global__ void k_point_scalars(AspotCtl* ctl, int role, const double* scratch, int nblk, Slot z, const int* gate) {
+  if (gate && *gate == 0) return;
+  if (threadIdx.x != 0) return;
+  PointScalars ps;
+  reduce_scratch(scratch, nblk, ps);
+  const double w = *z.w();
+  // phi (dual.hpp:117-118): B.sum() + eu.sum() + ev.sum() - u.r - v.c - w s
+  ps.phi = ((((ps.total + ps.seu) + ps.sev) - ps.ur) - ps.vc) - w * ctl->s;
+  ps.err = (ps.gl1u + ps.gl1v) + fabs(ps.total - ctl->s);  // dual.hpp:138-141
+  ps.overflow = !(ps.maxe <= kMaxExponent) || !(ps.maxu <= kMaxExponent) || !(ps.maxv <= kMaxExponent) || (w != w);
+  ctl->ps[role] = ps;
+  ctl->sweeps += 1;
+  switch (role) {
+    case R_BAR:
+      if (ps.overflow) { ctl->zbar_failed = 1; ctl->g_alive = 0; }
+      break;
+    case R_GRAVE:
+      if (ps.overflow) { ctl->g_alive = 0; break; }
+      ctl->block_hat = ctl->block_rule == POTGPU_ROUND_ROBIN ? int(ctl->gk_calls % 3) : greedy_block(ps, ctl->s);
+      break;
+    case R_HAT: {
+      if (ps.overflow) { ctl->g_alive = 0; break; }
+      ctl->phi_hat = ps.phi;
+      const int keep = ctl->phi_check <= ps.phi;  // solvers.hpp:342
+      ctl->keep_check = keep;
+      ctl->phi_best = fmin(ctl->phi_check, ps.phi);
+      const PointScalars& pb = keep ? ctl->ps[R_CHECK] : ps;
+      ctl->block_check = ctl->block_rule == POTGPU_ROUND_ROBIN ? int((ctl->gk_calls + 1) % 3) : greedy_block(pb, ctl->s);
+      break;
+    }
+    case R_NEW:
+      if (ps.overflow) { ctl->g_alive = 0; break; }
+      ctl->attempt_ok = 1;
+      break;
+    case R_CHECK:  // initial evaluation at z_check = 0 (solvers.hpp:305)
+      if (ps.overflow) { ctl->fatal = POTGPU_OVERFLOW; ctl->g_active = 0; ctl->g_new = 0; ctl->g_alive = 0; }
+      break;
+    default:
+      break;
+  }
+}
+
+// z_next = z_bar - step grad ; z_grave = z_bar + theta (z_next - z)
+// (solvers.hpp:337-339). On a new iteration the gradient of z_bar is formed
+// first (dual.hpp:129-131) and kept for the retries (halving keeps z_bar).
+__global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const double* rowb, const double* colb,
+                         const double* rt, const double* ct) {
+  if (!ctl->g_alive) return;
+  const int64_t n = zb.n;
+  const int fresh = ctl->g_new;
+  const double step = ctl->step, th = ctl->theta;
+  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+    double gk;
+    if (fresh) {
+      if (k < n) gk = (rowb[k] + eexp(zb.base[k])) - rt[k];
+      else if (k < 2 * n) gk = (colb[k - n] + eexp(zb.base[k])) - ct[k - n];
+      else gk = ctl->ps[R_BAR].total - ctl->s;
+      g.base[k] = gk;
+    } else {
+      gk = g.base[k];
+    }
+    const double zn = zb.base[k] - step * gk;
+    zg.base[k] = zb.base[k] + th * (zn - z.base[k]);
+  }
+}
+
+// Exact block minimisation (solvers.hpp:71-88) of src with the B sums of
+// src; dst = src with the chosen block replaced. `which` selects the source:
+// 0 = (src_a, rows_a, ps_a) [z_grave], 1 = z_best (z_check if keep_check
+// else z_hat).
+__global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* row_a, const double* col_a, int role_a,
+                            Slot src_b, const double* row_b, const double* col_b, int role_b, Slot dst,
+                            const double* rt, const double* ct) {
+  if (!ctl->g_alive) return;
+  int block;
+  Slot src;
+  const double *rowb, *colb;
+  int role;
+  if (which == 0) {
+    block = ctl->block_hat; src = src_a; rowb = row_a; colb = col_a; role = role_a;
+  } else {
+    block = ctl->block_check;
+    const bool keep = ctl->keep_check;
+    src = keep ? src_b : src_a; rowb = keep ? row_b : row_a; colb = keep ? col_b : col_a; role = keep ? role_b : role_a;
+  }
+  const int64_t n = src.n;
+  bool finite = true;
+  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+    double x = src.base[k];
+    if (k < n) {
+      if (block == 0) x = x + (log(rt[k]) - log(rowb[k] + eexp(x)));
+    } else if (k < 2 * n) {
+      if (block == 1) x = x + (log(ct[k - n]) - log(colb[k - n] + eexp(x)));
+    } else {
+      if (block == 2) x = x + (log(ctl->s) - log(ctl->ps[role].total));
+    }
+    dst.base[k] = x;
+    finite = finite && isfinite(x);
+  }
+  if (!finite) ctl->g_alive = 0;  // solvers.hpp:83-87: non-finite update -> Overflow
+}
+
+// Commit of an accepted attempt: z <- z_best, z_check <- z_check', sums of
+// z_check <- sums of z_check' (solvers.hpp:357-360). Element-parallel.
+__global__ void k_commit_copy(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, double* rowc, double* colc,
+                              const double* rown, const double* coln) {
+  if (!ctl->g_active || !ctl->attempt_ok) return;
+  const bool keep = ctl->keep_check;
+  const int64_t n = z.n;
+  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+    const double zbst = keep ? zc.base[k] : zh.base[k];
+    z.base[k] = zbst;
+    zc.base[k] = zn.base[k];
+    if (k < n) {
+      rowc[k] = rown[k];
+      colc[k] = coln[k];
+    }
+  }
+}
+
+__device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double err, double phi) {
+  if (ctl->trace_len < ctl->trace_cap) {
+    TraceDev& r = trace[ctl->trace_len];
+    r.t = t; r.error = err; r.phi = phi;
+    r.rounded_cost = __longlong_as_double(0x7ff8000000000000ULL);
+    r.elapsed_s = double(globaltimer_ns() - ctl->t0_ns) * 1e-9;
+  }
+  ctl->trace_len += 1;
+  ctl->g_record = ctl->record_rounded_cost;
+}
+
+__device__ void begin_iteration(AspotCtl* ctl) {
+  ctl->halvings = 0;
+  ctl->step = ctl->gamma / (ctl->step_denom * ctl->theta);  // solvers.hpp:328
+  ctl->g_new = 1;
+  ctl->g_alive = 1;
+  ctl->attempt_ok = 0;
+  ctl->zbar_failed = 0;
+}
+
+__device__ void finish(AspotCtl* ctl, int status) {
+  ctl->status = status;
+  ctl->g_active = 0;
+  ctl->g_new = 0;
+  ctl->g_alive = 0;
+  ctl->loop_end_ns = globaltimer_ns();
+}
+
+// Loop-head test of the reference (solvers.hpp:323-327), plus the session
+// pause point (no reference counterpart: lets a caller run k iterations).
+__device__ void loop_head(AspotCtl* ctl) {
+  if (!(ctl->error > ctl->eps_tilde)) { finish(ctl, POTGPU_CONVERGED); return; }
+  if (ctl->t >= ctl->max_iterations) { finish(ctl, POTGPU_MAX_ITERATIONS_EXCEEDED); return; }
+  if (ctl->t >= ctl->pause_at) {
+    ctl->paused = 1;
+    ctl->g_active = 0;
+    ctl->g_new = 0;
+    ctl->g_alive = 0;
+    ctl->loop_end_ns = globaltimer_ns();
+    return;
+  }
+  begin_iteration(ctl);
+}
+
+__global__ void k_resume(AspotCtl* ctl, int64_t pause_at) {
+  ctl->pause_at = pause_at;
+  if (!ctl->paused) return;
+  ctl->paused = 0;
+  ctl->g_active = 1;
+  loop_head(ctl);
+}
+
+__global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
+  if (!ctl->g_active) return;
+  ctl->attempts += 1;
+  if (!ctl->attempt_ok) {
+    // halving loop (solvers.hpp:334-356): z_bar/grad failures repeat on every
+    // retry, so they exhaust the 61 tries immediately.
+    if (ctl->zbar_failed || ctl->halvings >= 60) { finish(ctl, POTGPU_STEP_SIZE_UNDERFLOW); return; }
+    ctl->halvings += 1;
+    ctl->step *= 0.5;
+    ctl->g_new = 0;
+    ctl->g_alive = 1;
+    ctl->attempt_ok = 0;
+    return;
+  }
+  ctl->ps[R_CHECK] = ctl->ps[R_NEW];
+  ctl->gk_calls += 2;
+  ctl->error = ctl->ps[R_NEW].err;
+  ctl->phi_check = ctl->ps[R_NEW].phi;
+  ctl->theta = theta_next_d(ctl->theta);
+  ctl->t += 1;
+  if (lg && ctl->log_len < ctl->log_cap) {
+    IterLogDev& e = lg[ctl->log_len];
+    e.t = ctl->t; e.halvings = ctl->halvings; e.block_hat = ctl->block_hat; e.zbest_is_check = ctl->keep_check;
+    e.block_check = ctl->block_check; e.error = ctl->error; e.phi_check = ctl->phi_check; e.phi_hat = ctl->phi_hat;
+    e.theta = ctl->theta;
+  }
+  ctl->log_len += 1;
+  if (ctl->t % ctl->log_every == 0 || !(ctl->error > ctl->eps_tilde))  // solvers.hpp:309
+    append_trace(ctl, trace, ctl->t, ctl->error, ctl->phi_check);
+  loop_head(ctl);
+}
+
+// Initial state after the first phi/grad evaluation at z_check = 0.
+__global__ void k_init_state(AspotCtl* ctl, TraceDev* trace) {
+  if (ctl->fatal) return;
+  ctl->error = ctl->ps[R_CHECK].err;
+  ctl->phi_check = ctl->ps[R_CHECK].phi;
+  ctl->g_active = 1;
+  append_trace(ctl, trace, 0, ctl->error, ctl->phi_check);  // record(0) (solvers.hpp:320)
+  loop_head(ctl);
+}
+
+__global__ void k_stamp_t0(AspotCtl* ctl) { ctl->t0_ns = globaltimer_ns(); }
+
+}  // namespace potgpu

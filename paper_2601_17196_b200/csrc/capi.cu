@@ -1,0 +1,802 @@
+// capi.cu — the C-ABI (include/potgpu.h): context, problem upload and
+// validation, the accelerated solver driver, dual evaluation.
+#include <chrono>
+#include <cstring>
+#include <mutex>
+
+#include "engine.cuh"
+
+namespace potgpu {
+
+thread_local std::string g_last_error;
+
+// ------------------------------------------------------------------ setup --
+__global__ void k_dense_prepare(const double* __restrict__ src, int64_t n, int64_t ldc, int row_major, int64_t ld,
+                                double* C64, float* C32, unsigned long long* flags) {
+  // flags[0]: non-finite, flags[1]: negative, flags[2]: max (bit pattern, >= 0 values)
+  const int64_t total = n * ld;
+  unsigned long long nf = 0, neg = 0, mx = 0;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = k / ld, j = k % ld;
+    double x = 0.0;
+    if (j < n) {
+      if (!src) x = double(C32[k]);  // rescan of an already stored fp32 matrix
+      else x = row_major ? src[i * ldc + j] : src[i + j * ldc];
+      if (C32) x = double(float(x));  // fp32 instances: every semantic on the rounded value
+      if (!isfinite(x)) nf = 1;
+      else if (x < 0) neg = 1;
+      else mx = max(mx, (unsigned long long)__double_as_longlong(x));
+    }
+    if (C64) C64[k] = x;
+    if (C32) C32[k] = float(x);
+  }
+  if (nf) atomicOr(&flags[0], 1ULL);
+  if (neg) atomicOr(&flags[1], 1ULL);
+  if (mx) atomicMax(&flags[2], mx);
+}
+
+// logK = -C / gamma (dual.hpp:67, IEEE division); padding columns -inf.
+__global__ void k_build_logk(const double* __restrict__ C64, int64_t n, int64_t ld, double gamma, double* L) {
+  const int64_t total = n * ld;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = k % ld;
+    L[k] = j < n ? (-C64[k]) / gamma : -INFINITY;
+  }
+}
+
+__global__ void k_points_max(const float4* X, const float4* Y, int64_t n, double scale, unsigned long long* out) {
+  unsigned long long mx = 0;
+  ElemPointsF32 el{X, Y, scale, 1.0};
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const double c = el.cost(i, j);
+      mx = max(mx, (unsigned long long)__double_as_longlong(c));
+    }
+  atomicMax(out, mx);
+}
+
+__global__ void k_points_store(const float4* X, const float4* Y, int64_t n, int64_t ld, double scale, double* C64,
+                               float* C32) {
+  ElemPointsF32 el{X, Y, scale, 1.0};
+  const int64_t total = n * ld;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = k / ld, j = k % ld;
+    const double c = j < n ? el.cost(i, j) : 0.0;
+    if (C64) C64[k] = c;
+    if (C32) C32[k] = float(c);
+  }
+}
+
+static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P) {
+  if (!pr) throw Error(POTGPU_INVALID_ARGUMENT, "null problem");
+  if (pr->device_ptrs) throw Error(POTGPU_ERR_UNSUPPORTED, "device_ptrs=1 is not supported yet; pass host buffers");
+  const int64_t n = pr->n;
+  // validation_report (core.hpp:131-169): report the FIRST violation's code.
+  if (n <= 0) throw Error(POTGPU_EMPTY_INPUT, "invalid instance: marginals are empty");
+  if (!pr->r || !pr->c) throw Error(POTGPU_INVALID_ARGUMENT, "null marginals");
+  if (pr->dtype != POTGPU_F64 && pr->dtype != POTGPU_F32) throw Error(POTGPU_INVALID_ARGUMENT, "unknown dtype");
+  P.n = n;
+  P.dtype = pr->dtype;
+  P.kind = pr->cost_kind;
+  P.ld = round_up(n, kStripCols);
+  P.r.assign(pr->r, pr->r + n);
+  P.c.assign(pr->c, pr->c + n);
+  P.s = pr->s;
+  bool finite = std::isfinite(pr->s);
+  for (int64_t i = 0; i < n; ++i) finite = finite && std::isfinite(P.r[i]) && std::isfinite(P.c[i]);
+  bool cnf = false, cneg = false;
+  if (pr->cost_kind == POTGPU_COST_DENSE) {
+    if (!pr->C) throw Error(POTGPU_DIMENSION_MISMATCH, "invalid instance: cost matrix missing");
+    const int64_t ldc = pr->ldc > 0 ? pr->ldc : n;
+    DevBuf<double> raw;
+    raw.alloc(size_t(n * ldc));
+    PG_CK(cudaMemcpyAsync(raw.p, pr->C, size_t(n * ldc) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    DevBuf<unsigned long long> flags;
+    flags.alloc(3);
+    flags.zero(cx.stream);
+    if (pr->dtype == POTGPU_F64) P.C64.alloc(size_t(n * P.ld)); else P.C32.alloc(size_t(n * P.ld));
+    k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw.p, n, ldc, pr->row_major, P.ld,
+                                                          pr->dtype == POTGPU_F64 ? P.C64.p : nullptr,
+                                                          pr->dtype == POTGPU_F32 ? P.C32.p : nullptr, flags.p);
+    PG_CK(cudaGetLastError());
+    unsigned long long hf[3];
+    PG_CK(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    cnf = hf[0] != 0;
+    cneg = hf[1] != 0;
+    double mx;
+    std::memcpy(&mx, &hf[2], sizeof(double));
+    P.cmax = mx;
+  } else if (pr->cost_kind == POTGPU_COST_SQEUCLIDEAN || pr->cost_kind == POTGPU_COST_SQEUCLIDEAN_STORED) {
+    if (pr->cost_kind == POTGPU_COST_SQEUCLIDEAN && pr->dtype != POTGPU_F32)
+      throw Error(POTGPU_ERR_UNSUPPORTED, "on-the-fly costs run in fp32 (dtype=F32)");
+    if (!pr->X || !pr->Y || pr->d < 1 || pr->d > 3) throw Error(POTGPU_INVALID_ARGUMENT, "points need X, Y and 1 <= d <= 3");
+    std::vector<float4> hx(static_cast<size_t>(n)), hy(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      float a[3] = {0, 0, 0}, b[3] = {0, 0, 0};
+      for (int k = 0; k < pr->d; ++k) {
+        a[k] = float(pr->X[i * pr->d + k]);
+        b[k] = float(pr->Y[i * pr->d + k]);
+        finite = finite && std::isfinite(a[k]) && std::isfinite(b[k]);
+      }
+      hx[size_t(i)] = make_float4(a[0], a[1], a[2], 0.f);
+      hy[size_t(i)] = make_float4(b[0], b[1], b[2], 0.f);
+    }
+    P.X4.alloc(size_t(n));
+    P.Y4.alloc(size_t(n));
+    PG_CK(cudaMemcpyAsync(P.X4.p, hx.data(), size_t(n) * sizeof(float4), cudaMemcpyHostToDevice, cx.stream));
+    PG_CK(cudaMemcpyAsync(P.Y4.p, hy.data(), size_t(n) * sizeof(float4), cudaMemcpyHostToDevice, cx.stream));
+    DevBuf<unsigned long long> mx;
+    mx.alloc(1);
+    mx.zero(cx.stream);
+    k_points_max<<<int(std::min<int64_t>(n, 4096)), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, 1.0, mx.p);
+    unsigned long long hm = 0;
+    PG_CK(cudaMemcpyAsync(&hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    double maxd2;
+    std::memcpy(&maxd2, &hm, sizeof(double));
+    P.cost_scale = pr->cost_scale > 0 ? pr->cost_scale : (maxd2 > 0 ? 1.0 / maxd2 : 1.0);
+    // max C under the same fp64 formula as the cost views
+    mx.zero(cx.stream);
+    k_points_max<<<int(std::min<int64_t>(n, 4096)), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, P.cost_scale, mx.p);
+    PG_CK(cudaMemcpyAsync(&hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    std::memcpy(&P.cmax, &hm, sizeof(double));
+    if (pr->cost_kind == POTGPU_COST_SQEUCLIDEAN_STORED) {
+      // materialise C = scale |x - y|^2 once (fp64 formula of the cost views)
+      if (P.dtype == POTGPU_F64) P.C64.alloc(size_t(n * P.ld)); else P.C32.alloc(size_t(n * P.ld));
+      k_points_store<<<cx.num_sms * 8, 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, P.ld, P.cost_scale,
+                                                            P.dtype == POTGPU_F64 ? P.C64.p : nullptr,
+                                                            P.dtype == POTGPU_F32 ? P.C32.p : nullptr);
+      PG_CK(cudaGetLastError());
+      P.kind = POTGPU_COST_DENSE;
+      if (P.dtype == POTGPU_F32) {  // every semantic on the stored (rounded) value
+        DevBuf<unsigned long long> m2;
+        m2.alloc(3);
+        m2.zero(cx.stream);
+        k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(nullptr, n, P.ld, 2, P.ld, nullptr, P.C32.p, m2.p);
+        unsigned long long hf[3];
+        PG_CK(cudaMemcpyAsync(hf, m2.p, sizeof(hf), cudaMemcpyDeviceToHost, cx.stream));
+        PG_CK(cudaStreamSynchronize(cx.stream));
+        std::memcpy(&P.cmax, &hf[2], sizeof(double));
+      }
+    }
+  } else {
+    throw Error(POTGPU_INVALID_ARGUMENT, "unknown cost kind");
+  }
+  if (!finite || cnf) throw Error(POTGPU_NON_FINITE_ENTRY, "invalid instance: non-finite entry in r, c, C or s");
+  bool neg = false;
+  for (int64_t i = 0; i < n; ++i) neg = neg || P.r[i] < 0 || P.c[i] < 0;
+  if (neg) throw Error(POTGPU_NEGATIVE_ENTRY, "invalid instance: negative marginal entry");
+  if (cneg) throw Error(POTGPU_NEGATIVE_ENTRY, "invalid instance: negative cost entry");
+  if (P.s < 0) throw Error(POTGPU_NEGATIVE_ENTRY, "invalid instance: negative budget");
+  if (P.s > std::min(ksum(P.r.data(), n), ksum(P.c.data(), n)) + 1e-12)
+    throw Error(POTGPU_BUDGET_EXCEEDS_MASS, "invalid instance: budget exceeds min marginal mass");
+}
+
+void build_logk(Context& cx, DevProblem& P, double gamma) {
+  if (P.dtype != POTGPU_F64 || P.kind != POTGPU_COST_DENSE) return;
+  if (P.L_gamma == gamma && P.L64.p) return;
+  P.L64.alloc(size_t(P.n * P.ld));
+  k_build_logk<<<cx.num_sms * 8, 256, 0, cx.stream>>>(P.C64.p, P.n, P.ld, gamma, P.L64.p);
+  PG_CK(cudaGetLastError());
+  P.L_gamma = gamma;
+}
+
+// ------------------------------------------------------- aspot_setup etc. --
+struct Setup {
+  double gamma = 0, eps_tilde = 0;
+  std::vector<double> mr, mc;
+};
+
+// solvers.hpp:100-133
+Setup aspot_setup(const DevProblem& P, double epsilon) {
+  if (!(epsilon > 0) || !std::isfinite(epsilon)) throw Error(POTGPU_INVALID_ARGUMENT, "epsilon must be positive");
+  const int64_t n = P.n;
+  if (n < 2) throw Error(POTGPU_DEGENERATE_INSTANCE, "accelerated setup needs n >= 2 (log n vanishes)");
+  Setup st;
+  st.gamma = epsilon / (4.0 * std::log(double(n)));
+  const double cmax = P.cmax;
+  st.eps_tilde = cmax > 0 ? epsilon / (8.0 * cmax) : std::numeric_limits<double>::infinity();
+  const double sr = ksum(P.r.data(), n), sc = ksum(P.c.data(), n);
+  if (sr > 1) st.eps_tilde = std::min(st.eps_tilde, 8.0 * (sr - P.s) / (sr - 1.0));
+  if (sc > 1) st.eps_tilde = std::min(st.eps_tilde, 8.0 * (sc - P.s) / (sc - 1.0));
+  if (!(st.gamma > 0) || !std::isfinite(st.gamma)) throw Error(POTGPU_DEGENERATE_INSTANCE, "derived gamma is not positive");
+  if (!(st.eps_tilde > 0))
+    throw Error(POTGPU_DEGENERATE_INSTANCE, "stopping tolerance collapsed to zero (budget equals mass)");
+  const double lambda = std::min(st.eps_tilde / 8.0, 0.5);
+  const double nd = double(n);
+  st.mr.resize(size_t(n));
+  st.mc.resize(size_t(n));
+  for (int64_t i = 0; i < n; ++i) {
+    st.mr[size_t(i)] = (1.0 - lambda) * P.r[size_t(i)] + lambda / nd;
+    st.mc[size_t(i)] = (1.0 - lambda) * P.c[size_t(i)] + lambda / nd;
+  }
+  return st;
+}
+
+// solvers.hpp:146-174 on the mixed marginals; returns false when undefined.
+bool theory_bounds(const std::vector<double>& r, const std::vector<double>& c, double s, double cmax, double gamma,
+                   double eps_prime, double* out4) {
+  if (!(gamma > 0) || !std::isfinite(gamma) || !(eps_prime > 0) || !std::isfinite(eps_prime)) return false;
+  const int64_t n = int64_t(r.size());
+  const double sr = ksum(r.data(), n), sc = ksum(c.data(), n);
+  const double M = std::max(sr, sc);
+  if (!(M > s)) return false;
+  double me = std::numeric_limits<double>::infinity();
+  for (int64_t i = 0; i < n; ++i) me = std::min(me, std::min(r[size_t(i)], c[size_t(i)]));
+  if (!(me > 0)) return false;
+  const double R = cmax * M / (gamma * (M - s)) - std::log(me);
+  const double mu = gamma / (sr + sc - s);
+  const double L = 3.0 / mu;
+  out4[0] = R; out4[1] = L; out4[2] = mu;
+  out4[3] = 1.0 + std::pow(12.0 * std::sqrt(14.0 * double(n) * L) * R / eps_prime, 2.0 / 3.0);
+  return true;
+}
+
+using HostClock = std::chrono::steady_clock;
+inline double secs(HostClock::time_point a) { return std::chrono::duration<double>(HostClock::now() - a).count(); }
+
+void fill_trivial(const DevProblem& P, double gamma, double plan_value, potgpu_summary* sm, potgpu_outputs* out,
+                  const potgpu_config& cfg) {
+  // trivial_result (solvers.hpp:240-255): plan 0 (s == 0) or [[s]] (n == 1)
+  const int64_t n = P.n;
+  sm->status = POTGPU_CONVERGED;
+  sm->iterations = 0;
+  sm->gamma = gamma;
+  sm->tolerance = 0.0;
+  sm->final_error = 0.0;
+  sm->wall_seconds = 0.0;
+  sm->loop_seconds = 0.0;
+  sm->has_bounds = 0;
+  sm->mass = plan_value;  // n == 1 plan [[s]] or zero plan
+  double cost = 0.0;
+  if (n == 1 && plan_value != 0.0) {
+    // cost = C_00 * s; C_00 from the device copy
+    double c00 = 0.0;
+    if (P.kind == POTGPU_COST_DENSE) {
+      if (P.dtype == POTGPU_F64) PG_CK(cudaMemcpy(&c00, P.C64.p, sizeof(double), cudaMemcpyDeviceToHost));
+      else { float f; PG_CK(cudaMemcpy(&f, P.C32.p, sizeof(float), cudaMemcpyDeviceToHost)); c00 = f; }
+    }
+    cost = c00 * plan_value;
+  }
+  sm->cost = cost;
+  sm->phi = 0.0;
+  double gap = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double rowx = n == 1 ? plan_value : 0.0;
+    gap = std::max(gap, std::max(rowx - P.r[size_t(i)], 0.0));
+    gap = std::max(gap, std::max(rowx - P.c[size_t(i)], 0.0));
+    if (out && out->row_slack) out->row_slack[i] = P.r[size_t(i)] - rowx;
+    if (out && out->col_slack) out->col_slack[i] = P.c[size_t(i)] - rowx;
+  }
+  sm->feasibility_gap = std::max(gap, std::fabs(plan_value - P.s));
+  sm->trace_len = 1;
+  sm->iter_log_len = 0;
+  sm->sweeps = 0;
+  sm->attempts = 0;
+  std::strncpy(sm->stopping_iterate, "trivial", sizeof(sm->stopping_iterate));
+  if (out && out->X && cfg.materialize_plan)
+    for (int64_t k = 0; k < n * n; ++k) out->X[k] = (n == 1) ? plan_value : 0.0;
+  if (out && out->trace && out->trace_cap > 0) {
+    out->trace[0] = potgpu_trace_record{0, 0.0, 0.0, cost, 0.0};
+  }
+}
+
+void copy_trace_and_log(Workspace& ws, const AspotCtl& hc, potgpu_outputs* out) {
+  if (!out) return;
+  if (out->trace && out->trace_cap > 0) {
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(hc.trace_len, hc.trace_cap), out->trace_cap);
+    std::vector<TraceDev> tr(size_t(std::max<int64_t>(k, 1)));
+    if (k > 0) PG_CK(cudaMemcpy(tr.data(), ws.trace.p, size_t(k) * sizeof(TraceDev), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < k; ++i)
+      out->trace[i] = potgpu_trace_record{tr[size_t(i)].t, tr[size_t(i)].error, tr[size_t(i)].phi, tr[size_t(i)].rounded_cost,
+                                          tr[size_t(i)].elapsed_s};
+  }
+  if (out->iter_log && out->iter_log_cap > 0) {
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(hc.log_len, hc.log_cap), out->iter_log_cap);
+    std::vector<IterLogDev> lg(size_t(std::max<int64_t>(k, 1)));
+    if (k > 0) PG_CK(cudaMemcpy(lg.data(), ws.iterlog.p, size_t(k) * sizeof(IterLogDev), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < k; ++i) {
+      const IterLogDev& e = lg[size_t(i)];
+      out->iter_log[i] = potgpu_iter_log{e.t, e.halvings, e.block_hat, e.zbest_is_check, e.block_check, e.error,
+                                         e.phi_check, e.phi_hat, e.theta};
+    }
+  }
+}
+
+// ------------------------------------------------------------ sessions --
+// A solve = begin (validate, setup, first evaluation, record(0)) ->
+// iterate(k) any number of times (device-resident loop, CUDA-graph replay)
+// -> finish (final rounding, outputs). potgpu_solve runs all three.
+struct Session {
+  Context& cx;
+  DevProblem P;
+  potgpu_config cfg{};
+  HostClock::time_point t_start;
+  bool trivial = false;
+  double trivial_plan = 0.0, trivial_gamma = 0.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  explicit Session(Context& c) : cx(c) {
+    PG_CK(cudaEventCreate(&ev0));
+    PG_CK(cudaEventCreate(&ev1));
+  }
+  virtual ~Session() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+  virtual void begin() = 0;
+  virtual void iterate(int64_t k, double* ms, int64_t* iters, int* finished) = 0;
+  virtual void finish(potgpu_summary* sm, potgpu_outputs* out) = 0;
+  // average device time (ms) of one hot-path sweep launch; algorithmic
+  // elements and HBM bytes that launch must touch
+  virtual double time_sweep(int reps, double* elems, double* bytes) = 0;
+  virtual void stats(int64_t* attempts, int64_t* sweeps) = 0;
+  int64_t launches = 0;  // kernels this session launched inside iterate()
+};
+
+inline double stream_bytes_per_elem(const DevProblem& P) {
+  if (P.kind != POTGPU_COST_DENSE) return 0.0;
+  return P.dtype == POTGPU_F64 ? 8.0 : 4.0;
+}
+
+// aspot_solve (solvers.hpp:265-385).
+struct AspotSession : Session {
+  Workspace ws;
+  double gamma = 0;
+  Setup st;
+  cudaGraphExec_t exec = nullptr;
+  int64_t trace_cap = 1, log_cap = 0;
+  explicit AspotSession(Context& c) : Session(c) {}
+  ~AspotSession() override {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+
+  void enqueue_attempt() {
+    AspotCtl* ctl = ws.ctl.p;
+    const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
+               ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
+    const int gv = ws.nblk;
+    k_zbar<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZC, Z, ZB);
+    launch_sweep(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma);
+    launch_reduce(cx, ws, ZB, R_BAR, &ctl->g_new);
+    launch_scalars(cx, ws, R_BAR, ZB, &ctl->g_new);
+    k_zgrave<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
+    launch_sweep(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma);
+    launch_reduce(cx, ws, ZG, R_GRAVE, &ctl->g_alive);
+    launch_scalars(cx, ws, R_GRAVE, ZG, &ctl->g_alive);
+    k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
+                                                   ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
+    launch_sweep(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_alive, true, gamma);
+    launch_reduce(cx, ws, ZH, R_HAT, &ctl->g_alive);
+    launch_scalars(cx, ws, R_HAT, ZH, &ctl->g_alive);
+    k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
+                                                   ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
+    launch_sweep(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_alive, true, gamma);
+    launch_reduce(cx, ws, ZN, R_NEW, &ctl->g_alive);
+    launch_scalars(cx, ws, R_NEW, ZN, &ctl->g_alive);
+    k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
+                                                     ws.col(R_NEW));
+    k_commit_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p, ws.iterlog.p);
+    enqueue_rounding(cx, P, ws, ZC, R_CHECK, &ctl->g_record, true, gamma, true, nullptr, false);
+    PG_CK(cudaGetLastError());
+  }
+
+  void sync_ctl() {
+    PG_CK(cudaMemcpyAsync(ws.host_ctl, ws.ctl.p, sizeof(AspotCtl), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+  }
+
+  void begin() override {
+    const int64_t n = P.n;
+    if (n < 2) throw Error(POTGPU_DEGENERATE_INSTANCE, "accelerated solver needs n >= 2");
+    if (P.s == 0) {  // solvers.hpp:274-276
+      trivial = true;
+      return;
+    }
+    st = aspot_setup(P, cfg.epsilon);
+    gamma = cfg.gamma_override > 0 ? cfg.gamma_override : st.gamma;
+    if (!(gamma > 0) || !std::isfinite(gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
+    const double step_denom = 3.0 * (ksum(st.mr.data(), n) + ksum(st.mc.data(), n) - P.s);
+    build_logk(cx, P, gamma);
+    prepare_workspace(cx, P, ws, trace_cap, log_cap);
+    PG_CK(cudaMemcpyAsync(ws.rt.p, st.mr.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    PG_CK(cudaMemcpyAsync(ws.ct.p, st.mc.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    PG_CK(cudaMemcpyAsync(ws.ro_r.p, P.r.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    PG_CK(cudaMemcpyAsync(ws.ro_c.p, P.c.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    ws.slots.zero(cx.stream);
+    AspotCtl& h = *ws.host_ctl;
+    std::memset(&h, 0, sizeof(AspotCtl));
+    h.n = n;
+    h.max_iterations = cfg.max_iterations;
+    h.pause_at = INT64_MAX;
+    h.log_every = cfg.log_every;
+    h.block_rule = cfg.block_rule;
+    h.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
+    h.trace_cap = trace_cap;
+    h.log_cap = log_cap;
+    h.theta = 1.0;
+    h.gamma = gamma;
+    h.eps_tilde = st.eps_tilde;
+    h.step_denom = step_denom;
+    h.s = P.s;
+    h.status = ST_RUNNING;
+    PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(AspotCtl), cudaMemcpyHostToDevice, cx.stream));
+    AspotCtl* ctl = ws.ctl.p;
+    k_stamp_t0<<<1, 1, 0, cx.stream>>>(ctl);
+    // phi_and_gradient(z_check = 0) (solvers.hpp:305) and record(0) (:320)
+    const Slot ZC = ws.slot(S_ZC);
+    launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);
+    launch_reduce(cx, ws, ZC, R_CHECK, nullptr);
+    launch_scalars(cx, ws, R_CHECK, ZC, nullptr);
+    k_init_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p);
+    enqueue_rounding(cx, P, ws, ZC, R_CHECK, &ctl->g_record, true, gamma, true, nullptr, false);
+    sync_ctl();
+    if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
+    if (cfg.use_graphs) {
+      cudaGraph_t graph;
+      PG_CK(cudaStreamBeginCapture(cx.stream, cudaStreamCaptureModeThreadLocal));
+      enqueue_attempt();
+      PG_CK(cudaStreamEndCapture(cx.stream, &graph));
+      size_t nodes = 0;
+      PG_CK(cudaGraphGetNodes(graph, nullptr, &nodes));
+      graph_nodes = int64_t(nodes);
+      PG_CK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+    } else {
+      graph_nodes = kKernelsPerAttempt;
+    }
+  }
+
+  static constexpr int64_t kKernelsPerAttempt = 27;
+  int64_t graph_nodes = kKernelsPerAttempt;
+
+  void launch_attempts(int64_t k) {
+    for (int64_t i = 0; i < k; ++i) {
+      if (exec) PG_CK(cudaGraphLaunch(exec, cx.stream));
+      else enqueue_attempt();
+      launches += graph_nodes;
+    }
+  }
+
+  // Runs until k more iterations are accepted, the solve stops, or forever
+  // when k < 0. Device time of the loop between events -> *ms.
+  void iterate(int64_t k, double* ms, int64_t* iters, int* finished) override {
+    AspotCtl& h = *ws.host_ctl;
+    if (trivial || (!h.g_active && !h.paused)) {
+      if (ms) *ms = 0.0;
+      if (iters) *iters = trivial ? 0 : h.t;
+      if (finished) *finished = 1;
+      return;
+    }
+    const int64_t t0 = h.t;
+    const int64_t target = k < 0 ? INT64_MAX : t0 + k;
+    PG_CK(cudaEventRecord(ev0, cx.stream));
+    k_resume<<<1, 1, 0, cx.stream>>>(ws.ctl.p, target);
+    launches += 1;
+    // first burst: exactly the iterations asked for (1 attempt each unless a
+    // step is halved), then poll every sync_every attempts
+    int64_t burst = k < 0 ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, k);
+    while (true) {
+      launch_attempts(burst);
+      PG_CK(cudaEventRecord(ev1, cx.stream));
+      sync_ctl();
+      if (!h.g_active || h.fatal) break;
+      burst = std::max(1, cfg.sync_every);
+      if (k >= 0) burst = std::max<int64_t>(1, std::min<int64_t>(burst, target - h.t));
+    }
+    float f = 0.f;
+    PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
+    if (ms) *ms = double(f);
+    if (iters) *iters = h.t - t0;
+    if (finished) *finished = h.paused ? 0 : 1;
+    if (h.fatal) throw Error(h.fatal, "device reported an error in the solve loop");
+  }
+
+  void stats(int64_t* attempts, int64_t* sweeps) override {
+    if (trivial) { *attempts = 0; *sweeps = 0; return; }
+    sync_ctl();
+    *attempts = ws.host_ctl->attempts;
+    *sweeps = ws.host_ctl->sweeps;
+  }
+
+  double time_sweep(int reps, double* elems, double* bytes) override {
+    if (trivial) throw Error(POTGPU_INVALID_ARGUMENT, "trivial solve has no sweep");
+    const Slot ZC = ws.slot(S_ZC);
+    launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);  // warm
+    PG_CK(cudaEventRecord(ev0, cx.stream));
+    for (int k = 0; k < reps; ++k) launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);
+    PG_CK(cudaEventRecord(ev1, cx.stream));
+    PG_CK(cudaEventSynchronize(ev1));
+    float f = 0.f;
+    PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
+    const double n = double(P.n);
+    if (elems) *elems = n * n;
+    if (bytes) *bytes = n * n * stream_bytes_per_elem(P);
+    return double(f) / reps;
+  }
+
+  void finish(potgpu_summary* sm, potgpu_outputs* out) override {
+    const int64_t n = P.n;
+    if (trivial) {
+      fill_trivial(P, 0.0, 0.0, sm, out, cfg);
+      return;
+    }
+    AspotCtl& h = *ws.host_ctl;
+    if (h.paused) throw Error(POTGPU_INVALID_ARGUMENT, "session finish before the solve stopped");
+    double tb[4];
+    sm->has_bounds = theory_bounds(st.mr, st.mc, P.s, P.cmax, gamma, st.eps_tilde, tb) ? 1 : 0;
+    if (sm->has_bounds) { sm->bound_R = tb[0]; sm->bound_L = tb[1]; sm->bound_mu_f = tb[2]; sm->iteration_bound = tb[3]; }
+    // result.plan = round_pot(b_matrix(ctx, z_check), in)  (solvers.hpp:371)
+    const Slot ZC = ws.slot(S_ZC);
+    DevBuf<double> Xd;
+    const bool mat = cfg.materialize_plan && out && out->X;
+    if (mat) Xd.alloc(size_t(n * n));
+    enqueue_rounding(cx, P, ws, ZC, R_CHECK, nullptr, false, gamma, true, mat ? Xd.p : nullptr, true);
+    sync_ctl();
+    if (h.fatal) throw Error(h.fatal, "Infeasible: deficit fill has no slack mass");
+    const double wall = secs(t_start);
+    sm->status = h.status;
+    sm->iterations = h.t;
+    sm->gamma = gamma;
+    sm->tolerance = st.eps_tilde;
+    sm->final_error = h.error;
+    sm->wall_seconds = wall;
+    sm->loop_seconds = h.loop_end_ns > h.t0_ns ? double(h.loop_end_ns - h.t0_ns) * 1e-9 : 0.0;
+    sm->cost = h.ro.cost;
+    sm->feasibility_gap = h.ro.gap;
+    sm->mass = h.ro.mass;
+    sm->phi = h.phi_check;
+    sm->iter_log_len = h.log_len;
+    sm->sweeps = h.sweeps;
+    sm->attempts = h.attempts;
+    std::strncpy(sm->stopping_iterate, "z_check", sizeof(sm->stopping_iterate));
+    copy_trace_and_log(ws, h, out);
+    int64_t tl = std::min<int64_t>(h.trace_len, h.trace_cap);
+    int64_t last_t = -1;
+    if (tl > 0) {
+      TraceDev last;
+      PG_CK(cudaMemcpy(&last, ws.trace.p + (tl - 1), sizeof(TraceDev), cudaMemcpyDeviceToHost));
+      last_t = last.t;
+    }
+    // final record if the last one is not at t (solvers.hpp:375-383)
+    if (h.trace_len == 0 || last_t != h.t) {
+      if (out && out->trace && tl < out->trace_cap) out->trace[tl] = potgpu_trace_record{h.t, h.error, h.phi_check, h.ro.cost, wall};
+      tl += 1;
+    }
+    sm->trace_len = tl;
+    if (out) {
+      if (out->row_slack) PG_CK(cudaMemcpy(out->row_slack, ws.rv(8), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->col_slack) PG_CK(cudaMemcpy(out->col_slack, ws.rv(9), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->u) PG_CK(cudaMemcpy(out->u, ZC.u(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->v) PG_CK(cudaMemcpy(out->v, ZC.v(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->w) PG_CK(cudaMemcpy(out->w, ZC.w(), sizeof(double), cudaMemcpyDeviceToHost));
+      if (mat) PG_CK(cudaMemcpy(out->X, Xd.p, size_t(n * n) * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+  }
+};
+
+}  // namespace potgpu
+
+#include "sinkhorn.cuh"
+
+namespace potgpu {
+}  // namespace potgpu
+
+using namespace potgpu;
+
+struct potgpu_ctx {
+  Context cx;
+};
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return POTGPU_ERR_CUDA;
+  }
+}
+
+extern "C" {
+
+int potgpu_abi_version(void) { return POTGPU_ABI_VERSION; }
+const char* potgpu_last_error(void) { return g_last_error.c_str(); }
+
+void potgpu_config_default(potgpu_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->epsilon = 0.1;
+  c->gamma_override = 0.0;
+  c->max_iterations = 50000;
+  c->block_rule = POTGPU_GREEDY;
+  c->tuning_exponent_p = 1.0;
+  c->deterministic = 1;
+  c->log_every = 1;
+  c->record_rounded_cost = 1;
+  c->materialize_plan = 1;
+  c->collect_iter_log = 0;
+  c->use_graphs = 1;
+  c->sync_every = 8;
+}
+
+int potgpu_create(int device, potgpu_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Error(POTGPU_INVALID_ARGUMENT, "null out");
+    int count = 0;
+    PG_CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(POTGPU_ERR_CUDA, "no such CUDA device");
+    PG_CK(cudaSetDevice(device));
+    auto* c = new potgpu_ctx();
+    c->cx.device = device;
+    PG_CK(cudaStreamCreateWithFlags(&c->cx.stream, cudaStreamNonBlocking));
+    PG_CK(cudaDeviceGetAttribute(&c->cx.num_sms, cudaDevAttrMultiProcessorCount, device));
+    *out = c;
+  });
+}
+
+int potgpu_destroy(potgpu_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->cx.device);
+    if (c->cx.stream) cudaStreamDestroy(c->cx.stream);
+    delete c;
+  });
+}
+
+static void check_config(const potgpu_config& c) {  // core.hpp:250-266
+  if (!(c.epsilon > 0) || !std::isfinite(c.epsilon)) throw Error(POTGPU_INVALID_ARGUMENT, "epsilon must be positive");
+  if (c.max_iterations < 1) throw Error(POTGPU_INVALID_ARGUMENT, "max_iterations must be >= 1");
+  if (!(c.tuning_exponent_p >= 1)) throw Error(POTGPU_INVALID_ARGUMENT, "tuning exponent p must be >= 1");
+  if (c.log_every < 1) throw Error(POTGPU_INVALID_ARGUMENT, "log_every must be >= 1");
+  if (c.gamma_override != 0 && !(c.gamma_override > 0)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma override must be positive");
+}
+
+static std::unique_ptr<Session> make_session(potgpu_ctx* c, int kind, const potgpu_problem* pr,
+                                             const potgpu_config* cfg_in, int64_t trace_cap, int64_t log_cap) {
+  if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+  PG_CK(cudaSetDevice(c->cx.device));
+  potgpu_config cfg;
+  if (cfg_in) cfg = *cfg_in; else potgpu_config_default(&cfg);
+  const auto t_start = HostClock::now();
+  std::unique_ptr<Session> s;
+  if (kind == POTGPU_ASPOT) {
+    auto a = std::make_unique<AspotSession>(c->cx);
+    a->trace_cap = std::max<int64_t>(trace_cap, 0) + 1;
+    a->log_cap = cfg.collect_iter_log ? std::max<int64_t>(log_cap, 0) : 0;
+    s = std::move(a);
+  } else if (kind == POTGPU_FEASIBLE_SINKHORN || kind == POTGPU_TUNED_SINKHORN) {
+    s = make_sinkhorn_session(c->cx, kind, trace_cap);
+  } else {
+    throw Error(POTGPU_INVALID_ARGUMENT, "unknown solver kind");
+  }
+  s->cfg = cfg;
+  s->t_start = t_start;
+  upload_problem(c->cx, pr, s->P);
+  check_config(cfg);
+  s->begin();
+  return s;
+}
+
+int potgpu_solve(potgpu_ctx* c, int kind, const potgpu_problem* pr, const potgpu_config* cfg_in, potgpu_summary* sm,
+                 potgpu_outputs* out) {
+  return guarded([&] {
+    if (!sm) throw Error(POTGPU_INVALID_ARGUMENT, "null summary");
+    std::memset(sm, 0, sizeof(*sm));
+    auto s = make_session(c, kind, pr, cfg_in, out ? out->trace_cap : 0, out ? out->iter_log_cap : 0);
+    s->iterate(-1, nullptr, nullptr, nullptr);
+    s->finish(sm, out);
+  });
+}
+
+int potgpu_session_begin(potgpu_ctx* c, int kind, const potgpu_problem* pr, const potgpu_config* cfg,
+                         int64_t trace_cap, int64_t iter_log_cap, potgpu_session** out) {
+  return guarded([&] {
+    if (!out) throw Error(POTGPU_INVALID_ARGUMENT, "null out");
+    auto s = make_session(c, kind, pr, cfg, trace_cap, iter_log_cap);
+    *out = reinterpret_cast<potgpu_session*>(s.release());
+  });
+}
+
+int potgpu_session_iterate(potgpu_session* s, int64_t k, double* device_ms, int64_t* iterations, int* finished) {
+  return guarded([&] {
+    if (!s) throw Error(POTGPU_INVALID_ARGUMENT, "null session");
+    reinterpret_cast<Session*>(s)->iterate(k, device_ms, iterations, finished);
+  });
+}
+
+int potgpu_session_finish(potgpu_session* s, potgpu_summary* sm, potgpu_outputs* out) {
+  return guarded([&] {
+    if (!s || !sm) throw Error(POTGPU_INVALID_ARGUMENT, "null session or summary");
+    std::memset(sm, 0, sizeof(*sm));
+    reinterpret_cast<Session*>(s)->finish(sm, out);
+  });
+}
+
+int potgpu_session_destroy(potgpu_session* s) {
+  return guarded([&] { delete reinterpret_cast<Session*>(s); });
+}
+
+int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep, double* elements, double* bytes) {
+  return guarded([&] {
+    if (!s || reps < 1) throw Error(POTGPU_INVALID_ARGUMENT, "null session or reps < 1");
+    const double ms = reinterpret_cast<Session*>(s)->time_sweep(reps, elements, bytes);
+    if (ms_per_sweep) *ms_per_sweep = ms;
+  });
+}
+
+int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* attempts, int64_t* sweeps) {
+  return guarded([&] {
+    if (!s) throw Error(POTGPU_INVALID_ARGUMENT, "null session");
+    Session* se = reinterpret_cast<Session*>(s);
+    int64_t a = 0, w = 0;
+    se->stats(&a, &w);
+    if (kernel_launches) *kernel_launches = se->launches;
+    if (attempts) *attempts = a;
+    if (sweeps) *sweeps = w;
+  });
+}
+
+void* potgpu_ctx_stream(potgpu_ctx* c) { return c ? reinterpret_cast<void*>(c->cx.stream) : nullptr; }
+
+int potgpu_dual_eval(potgpu_ctx* c, const potgpu_problem* pr, double gamma, const double* u, const double* v, double w,
+                     double* row, double* col, double* scalars) {
+  int overflow = 0;
+  const int rc = guarded([&] {
+    if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+    if (!(gamma > 0) || !std::isfinite(gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
+    PG_CK(cudaSetDevice(c->cx.device));
+    DevProblem P;
+    upload_problem(c->cx, pr, P);
+    build_logk(c->cx, P, gamma);
+    Workspace ws;
+    prepare_workspace(c->cx, P, ws, 1, 0);
+    const int64_t n = P.n;
+    const Slot Z = ws.slot(S_ZB);
+    ws.slots.zero(c->cx.stream);
+    PG_CK(cudaMemcpyAsync(Z.u(), u, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(Z.v(), v, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(Z.w(), &w, sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(ws.rt.p, P.r.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(ws.ct.p, P.c.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    AspotCtl& h = *ws.host_ctl;
+    std::memset(&h, 0, sizeof(h));
+    h.n = n;
+    h.s = P.s;
+    PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(h), cudaMemcpyHostToDevice, c->cx.stream));
+    launch_sweep(c->cx, P, ws, Z, nullptr, nullptr, nullptr, true, gamma);
+    launch_reduce(c->cx, ws, Z, R_EVAL, nullptr);
+    launch_scalars(c->cx, ws, R_EVAL, Z, nullptr);
+    PG_CK(cudaMemcpyAsync(&h, ws.ctl.p, sizeof(h), cudaMemcpyDeviceToHost, c->cx.stream));
+    if (row) PG_CK(cudaMemcpyAsync(row, ws.row(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
+    if (col) PG_CK(cudaMemcpyAsync(col, ws.col(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
+    PG_CK(cudaStreamSynchronize(c->cx.stream));
+    const PointScalars& ps = h.ps[R_EVAL];
+    if (scalars) {
+      scalars[0] = ps.total;
+      scalars[1] = ps.maxe;
+      scalars[2] = ps.phi;
+      scalars[3] = ps.err;
+      scalars[4] = ps.total - P.s;
+      scalars[5] = ps.overflow;
+    }
+    overflow = ps.overflow;
+  });
+  if (rc) return rc;
+  if (overflow) {
+    g_last_error = "B(z) exponent exceeds representable range";
+    return POTGPU_OVERFLOW;
+  }
+  return 0;
+}
+
+int potgpu_round_pot(potgpu_ctx*, int64_t, const double*, const double*, const double*, double, double*) {
+  g_last_error = "potgpu_round_pot on a dense user plan is not implemented yet";
+  return POTGPU_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// common.cuh — shared device/host internals of libpotgpu (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/potgpu.h"
+
+namespace potgpu {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PG_CK(x)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::potgpu::Error(POTGPU_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// dual.hpp:47 and the Eigen packet-exp clamp (see oracle/pot_oracle.hpp eexp).
+constexpr double kMaxExponent = 700.0;
+constexpr double kExpLo = -709.784;
+constexpr double kExpHi = 709.784;
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr double kLn2 = 0.69314718055994530942;
+
+// Sweep geometry: a warp owns 256 consecutive columns of a row (8 per lane),
+// a CTA's 8 warps share that column strip and split the CTA's row range.
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kStripCols = 256;
+constexpr int kVecThreads = 256;  // O(n) kernels
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// A dual point z = (u, v, w) lives in one slot: [u (n) | v (n) | w | pad].
+struct Slot {
+  double* base = nullptr;
+  int64_t n = 0;
+  __host__ __device__ double* u() const { return base; }
+  __host__ __device__ double* v() const { return base + n; }
+  __host__ __device__ double* w() const { return base + 2 * n; }
+};
+
+// Reductions of B at a point that every caller needs (dual.hpp:117-131,
+// solvers.hpp:49-69, 224-232), produced by finalize kernels.
+struct PointScalars {
+  double total;    // 1^T B 1
+  double maxe;     // max_ij exponent (NaN-propagating)
+  double maxu, maxv;
+  double seu, sev; // sum exp(u), sum exp(v)
+  double ur, vc;   // <u, r~>, <v, c~>
+  double score_u, score_v;  // sum rho(r~_i, row_i), sum rho(c~_j, col_j)
+  double gl1u, gl1v;        // |grad_u|_1, |grad_v|_1
+  double phi, err;
+  int overflow;
+  int pad;
+};
+constexpr int kNumPartials = 11;  // total, maxu, maxv, seu, sev, ur, vc, score_u, score_v, gl1u, gl1v
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  void alloc(size_t k) {
+    if (k <= count && p) return;
+    release();
+    if (k == 0) return;
+    PG_CK(cudaMalloc(&p, k * sizeof(T)));
+    count = k;
+  }
+  void zero(cudaStream_t st) {
+    if (p) PG_CK(cudaMemsetAsync(p, 0, count * sizeof(T), st));
+  }
+};
+
+// ---------------------------------------------------------------- device --
+__device__ __forceinline__ double nan_max(double a, double b) {
+  // NaN-propagating max, the reference's !(max <= 700) sees NaN as overflow.
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ULL) : (a > b ? a : b);
+}
+
+// Eigen packet exp semantics (pot_oracle.hpp eexp).
+__device__ __forceinline__ double eexp(double x) {
+  if (x != x) return x;
+  if (x == __longlong_as_double(0x7ff0000000000000ULL)) return x;
+  return exp(fmin(fmax(x, kExpLo), kExpHi));
+}
+
+// rho extended by its limits (dual.hpp:144-159).
+__device__ __forceinline__ double rho_limit(double a, double b) {
+  if (!(a > 0)) return b;
+  if (!(b > 0)) return __longlong_as_double(0x7ff0000000000000ULL);
+  return b - a + a * log(a / b);
+}
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ float warp_maxf(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ double warp_nanmax(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = nan_max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+}  // namespace potgpu

@@ -1,0 +1,330 @@
+// sweep.cuh — the n^2 hot path: one pass over B(z) = exp(-C/gamma + u_i + v_j + w)
+// producing per-strip row partials, per-rowblock column partials and the
+// max exponent, without ever transposing or materialising B.
+//
+// Reference counterpart: exponent_matrix + b_matrix + rowwise()/colwise()/
+// sum() reductions (dual.hpp:93-133; solvers.hpp:46-52, 224-232).
+//
+// Tiling (sm_100a, 148 SMs): a warp owns a 256-column strip of one row per
+// step (8 columns per lane, 128-bit coalesced loads), a CTA's 8 warps share
+// the strip and interleave over the CTA's row range. Row sums are warp
+// shuffles; column sums stay in registers across the CTA's rows and are
+// combined across warps in shared memory, so the matrix is read once, in
+// row order, and never transposed. All reductions are fixed-order
+// (deterministic run to run).
+#pragma once
+
+#include "common.cuh"
+
+namespace potgpu {
+
+struct SweepArgs {
+  int64_t n;            // plan side
+  int rows_per_cta;
+  const double* u;      // point (fp64 potentials)
+  const double* v;
+  const double* w;
+  const double* lu;     // optional additive row log-weights (rounding), may be null
+  const double* lv;     // optional additive column log-weights
+  double* rowp;         // [gridDim.x][n]: row partial of strip x
+  double* colp;         // [gridDim.y][n]: column partial of row block y
+  double* maxp;         // [gridDim.y][gridDim.x]: max exponent (natural log units)
+  const int* gate;      // kernel runs iff *gate != 0 (null: always)
+  double gamma;         // for fp32 sources: exponent scale log2(e)/gamma folded in src
+};
+
+// ------------------------------------------------------------------------
+// fp64, stored logK = -C/gamma (the reference's EntropicContext::logK,
+// dual.hpp:67, computed once by IEEE division). Exponent association
+// ((logK + u_i) + v_j) + w exactly as dual.hpp:94-97; exp with the Eigen
+// packet clamp when FLOOR (the reference's B), plain exp for rounding
+// sweeps. Padding columns of L hold -inf.
+template <bool FLOOR>
+__global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __restrict__ L, int64_t ld, SweepArgs a) {
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
+  double vj[8];
+  bool ok[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t j = j0 + 2 * lane + 64 * k + e;
+      ok[2 * k + e] = j < n;
+      double vv = 0.0;
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+      }
+      vj[2 * k + e] = vv;
+    }
+  }
+  const double w = *a.w;
+  double cacc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cacc[k] = 0.0;
+  double mx = -INFINITY;
+  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    double ui = a.u[i];
+    if (a.lu) ui = ui + a.lu[i];
+    const double2* row = reinterpret_cast<const double2*>(L + i * ld + j0) + lane;
+    double2 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldcs(row + 32 * k);
+    double rs = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double e0 = ((x[k].x + ui) + vj[2 * k]) + w;
+      const double e1 = ((x[k].y + ui) + vj[2 * k + 1]) + w;
+      mx = fmax(mx, fmax(e0, e1));
+      double b0 = exp(FLOOR ? fmax(e0, kExpLo) : e0);
+      double b1 = exp(FLOOR ? fmax(e1, kExpLo) : e1);
+      b0 = ok[2 * k] ? b0 : 0.0;
+      b1 = ok[2 * k + 1] ? b1 : 0.0;
+      rs += b0;
+      rs += b1;
+      cacc[2 * k] += b0;
+      cacc[2 * k + 1] += b1;
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) a.rowp[int64_t(blockIdx.x) * n + i] = rs;
+  }
+  __shared__ double cs[kWarps][kStripCols];
+  __shared__ double ms[kWarps];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    cs[warp][2 * lane + 64 * k] = cacc[2 * k];
+    cs[warp][2 * lane + 64 * k + 1] = cacc[2 * k + 1];
+  }
+  mx = warp_nanmax(mx);
+  if (lane == 0) ms[warp] = mx;
+  __syncthreads();
+  const int t = threadIdx.x;
+  double s = 0.0;
+#pragma unroll
+  for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][t];
+  if (j0 + t < n) a.colp[int64_t(blockIdx.y) * n + j0 + t] = s;
+  if (t == 0) {
+    double m = ms[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = nan_max(m, ms[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = m;
+  }
+}
+
+// ------------------------------------------------------------------------
+// fp32 sweeps. The exponent in log2 units t_ij = A_i + B_j - kappa_ij with
+// A_i = (u_i + w) log2 e, B_j = v_j log2 e (fp32, from fp64 potentials) and
+// kappa_ij = g2 * C_ij (stored fp32 C) or g2 * |x_i - y_j|^2 (coordinates).
+// Each row of a warp tile is exponentiated once with MUFU.EX2 at the exact
+// tile-row max m_i (no overflow, no underflow of the row's mass); the column
+// accumulators carry a per-warp running scale sigma and take p_ij 2^(m_i -
+// sigma). Partials leave the kernel as fp64 values sum * 2^scale.
+struct SrcDenseF32 {
+  const float* C;
+  int64_t ld;
+  float g2;  // log2(e) / gamma
+  static constexpr int kColRegs = 0;
+  struct Col {};
+  struct RowCtx { const float4* p; };
+  __device__ __forceinline__ void load_cols(int64_t, Col*) const {}
+  __device__ __forceinline__ RowCtx row(int64_t i, int64_t j0, int lane) const {
+    return RowCtx{reinterpret_cast<const float4*>(C + i * ld + j0) + lane};
+  }
+  // -kappa for the lane's 8 columns: j0 + 4*lane + 128*k + e, k = 0..1, e = 0..3
+  __device__ __forceinline__ void kappa(const RowCtx& r, const Col*, float2 (&kp)[4]) const {
+    const float4 c0 = __ldcs(r.p);
+    const float4 c1 = __ldcs(r.p + 32);
+    const float2 g = make_float2(-g2, -g2);
+    kp[0] = __fmul2_rn(g, make_float2(c0.x, c0.y));
+    kp[1] = __fmul2_rn(g, make_float2(c0.z, c0.w));
+    kp[2] = __fmul2_rn(g, make_float2(c1.x, c1.y));
+    kp[3] = __fmul2_rn(g, make_float2(c1.z, c1.w));
+  }
+};
+
+struct SrcPointsF32 {
+  const float4* X;  // n x (x, y, z, 0)
+  const float4* Y;
+  float g2s;        // log2(e) * cost_scale / gamma
+  struct Col { float2 x, y, z; };  // 2 columns per Col, NEGATED coordinates
+  struct RowCtx { float2 x, y, z; };
+  __device__ __forceinline__ void load_cols(int64_t j_first, Col* c) const {}
+  __device__ __forceinline__ RowCtx row(int64_t i, int64_t, int) const {
+    const float4 p = X[i];
+    return RowCtx{make_float2(p.x, p.x), make_float2(p.y, p.y), make_float2(p.z, p.z)};
+  }
+  // returns -kappa = -g2s |x_i - y_j|^2
+  __device__ __forceinline__ void kappa(const RowCtx& r, const Col* c, float2 (&kp)[4]) const {
+    const float2 g = make_float2(-g2s, -g2s);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 dx = __fadd2_rn(r.x, c[q].x);
+      const float2 dy = __fadd2_rn(r.y, c[q].y);
+      const float2 dz = __fadd2_rn(r.z, c[q].z);
+      float2 d2 = __fmul2_rn(dx, dx);
+      d2 = __ffma2_rn(dy, dy, d2);
+      d2 = __ffma2_rn(dz, dz, d2);
+      kp[q] = __fmul2_rn(g, d2);
+    }
+  }
+};
+
+// Lane column map for fp32 sweeps: j = j0 + 4*lane + 128*k + e (k < 2, e < 4),
+// stored as 4 float2 pairs q = 2k + e/2.
+__device__ __forceinline__ int64_t f32_col(int64_t j0, int lane, int q, int h) {
+  return j0 + 4 * lane + 128 * (q >> 1) + 2 * (q & 1) + h;
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
+  float2 Bj[4];
+  typename Src::Col cols[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float b[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;  // padding column: exp2(-inf) = 0, ignored by max
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+      }
+      b[h] = float(vv);
+    }
+    Bj[q] = make_float2(b[0], b[1]);
+  }
+  if constexpr (sizeof(typename Src::Col) > 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 y0 = make_float4(0, 0, 0, 0), y1 = make_float4(0, 0, 0, 0);
+      const int64_t ja = f32_col(j0, lane, q, 0), jb = f32_col(j0, lane, q, 1);
+      if (ja < n) y0 = src.Y[ja];
+      if (jb < n) y1 = src.Y[jb];
+      cols[q].x = make_float2(-y0.x, -y1.x);
+      cols[q].y = make_float2(-y0.y, -y1.y);
+      cols[q].z = make_float2(-y0.z, -y1.z);
+    }
+  }
+  const double w = *a.w;
+  float2 cacc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY;  // running column scale (log2) of this warp
+  float mmax = -INFINITY;
+  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    const float Ai = float((ud + w) * kLog2e);
+    const auto rc = src.row(i, j0, lane);
+    float2 kp[4];
+    src.kappa(rc, cols, kp);
+    const float2 A2 = make_float2(Ai, Ai);
+    float2 t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = __fadd2_rn(__fadd2_rn(A2, Bj[q]), kp[q]);
+    float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
+    m = warp_maxf(m);
+    // m == -inf only if the whole row segment is padding/-inf potentials.
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    const float2 M2 = make_float2(-ms, -ms);
+    float2 rs = make_float2(0.f, 0.f);
+    float2 p[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 d = __fadd2_rn(t[q], M2);
+      p[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      rs = __fadd2_rn(rs, p[q]);
+    }
+    float r = warp_sum(rs.x + rs.y);
+    if (lane == 0) a.rowp[int64_t(blockIdx.x) * n + i] = double(r) * exp2(double(ms));
+    if (m > sigma) {
+      const float sc = ex2f(sigma - m);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = m;
+    }
+    mmax = fmaxf(mmax, m);
+    const float f = (m == -INFINITY) ? 0.f : ex2f(m - sigma);
+    const float2 F2 = make_float2(f, f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+  }
+  // CTA combine of the 8 warps' column accumulators (each with its sigma).
+  __shared__ float cs[kWarps][kStripCols];
+  __shared__ float ss[kWarps];
+  __shared__ float mm[kWarps];
+  if (lane == 0) {
+    ss[warp] = sigma;
+    mm[warp] = mmax;
+  }
+  __syncthreads();
+  float sig = ss[0];
+  for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+  const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+    cs[warp][c] = cacc[q].x * fw;
+    cs[warp][c + 1] = cacc[q].y * fw;
+  }
+  __syncthreads();
+  const int tt = threadIdx.x;
+  double s = 0.0;
+#pragma unroll
+  for (int ww = 0; ww < kWarps; ++ww) s += double(cs[ww][tt]);
+  if (j0 + tt < n) a.colp[int64_t(blockIdx.y) * n + j0 + tt] = (sig == -INFINITY) ? 0.0 : s * exp2(double(sig));
+  if (tt == 0) {
+    float m = mm[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
+// ------------------------------------------------------------------------
+// Grid shape: a 1-D-equivalent grid of (strips x row blocks) whose CTA count
+// is a multiple of the resident CTA capacity (SMs x occupancy) when that is
+// possible, so no partial last wave.
+struct SweepGrid {
+  dim3 grid;
+  int rows_per_cta;
+};
+
+inline int64_t gcd64(int64_t a, int64_t b) {
+  while (b) { const int64_t t = a % b; a = b; b = t; }
+  return a;
+}
+
+inline SweepGrid choose_grid(int64_t n, int num_sms, int occupancy) {
+  const int64_t strips = ceil_div(n, kStripCols);
+  const int64_t cap = int64_t(num_sms) * occupancy;
+  const int64_t base = cap / gcd64(cap, strips);  // row blocks per quantum
+  const int64_t max_rb = std::max<int64_t>(1, n / 8);
+  int64_t rb;
+  if (base <= max_rb) {
+    // about 8 CTAs per resident slot per SM when n allows, at least 1 quantum
+    int64_t quanta = std::max<int64_t>(1, (8 * cap) / (strips * base));
+    while (quanta > 1 && base * quanta > max_rb) --quanta;
+    rb = base * quanta;
+  } else {
+    rb = std::min<int64_t>(max_rb, std::max<int64_t>(1, ceil_div(2 * cap, strips)));
+  }
+  SweepGrid g;
+  g.rows_per_cta = int(ceil_div(n, rb));
+  rb = ceil_div(n, g.rows_per_cta);
+  g.grid = dim3(unsigned(strips), unsigned(rb), 1);
+  return g;
+}
+
+}  // namespace potgpu

@@ -1,0 +1,608 @@
+"""Python mirror of the reference's ``namespace pot`` solver API over the
+C-ABI in include/potgpu.h (libpotgpu.so, sm_100a).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/pot/{core,solvers}.hpp:
+
+* ``Instance`` (core.hpp:108-118), ``SolverConfig`` (core.hpp:241-267),
+  ``SolveResult`` (solvers.hpp:176-186), ``TraceRecord`` (core.hpp:269-275),
+  ``TheoryBounds`` (solvers.hpp:139-144);
+* ``solve`` (solvers.hpp:591), ``aspot_solve`` (:265),
+  ``feasible_sinkhorn_solve`` (:516), ``tuned_sinkhorn_solve`` (:547/:586);
+* failures raise ``PotError`` carrying the reference's ``ErrorCode``.
+
+There is no CPU fallback: importing works anywhere (the library is
+self-contained), but every solve runs on a CUDA device and raises if none is
+present or the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpotgpu.so")
+
+
+class ErrorCode(enum.IntEnum):  # core.hpp:21-39 (order preserved)
+    DimensionMismatch = 0
+    NegativeEntry = 1
+    NonFiniteEntry = 2
+    BudgetExceedsMass = 3
+    Overflow = 4
+    NonPositiveArgument = 5
+    DegenerateInstance = 6
+    PenaltyTooSmall = 7
+    UnbalancedMarginals = 8
+    ZeroEntropy = 9
+    Infeasible = 10
+    SizeLimitExceeded = 11
+    ZeroMassPlan = 12
+    DegenerateSvd = 13
+    EmptyInput = 14
+    InvalidArgument = 15
+    IoFailure = 16
+    # appended by the device boundary (no reference counterpart)
+    CudaError = 17
+    NcclError = 18
+    Unsupported = 19
+
+
+class PotError(RuntimeError):
+    """core.hpp:64-74."""
+
+    def __init__(self, code: ErrorCode, message: str):
+        super().__init__(f"{code.name}: {message}")
+        self.code = code
+
+
+class SolverKind(enum.IntEnum):  # core.hpp:223
+    Aspot = 0
+    FeasibleSinkhorn = 1
+    TunedSinkhorn = 2
+
+
+class BlockRule(enum.IntEnum):  # core.hpp:221
+    Greedy = 0
+    RoundRobin = 1
+
+
+class SolveStatus(enum.IntEnum):  # core.hpp:284
+    Converged = 0
+    MaxIterationsExceeded = 1
+    StepSizeUnderflow = 2
+
+
+class DType(enum.IntEnum):
+    F64 = 0
+    F32 = 1
+
+
+# --------------------------------------------------------------- C structs --
+class _Problem(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("dtype", ctypes.c_int), ("cost_kind", ctypes.c_int),
+        ("C", ctypes.POINTER(ctypes.c_double)), ("ldc", ctypes.c_int64), ("row_major", ctypes.c_int),
+        ("X", ctypes.POINTER(ctypes.c_double)), ("Y", ctypes.POINTER(ctypes.c_double)), ("d", ctypes.c_int),
+        ("cost_scale", ctypes.c_double),
+        ("r", ctypes.POINTER(ctypes.c_double)), ("c", ctypes.POINTER(ctypes.c_double)), ("s", ctypes.c_double),
+        ("device_ptrs", ctypes.c_int),
+    ]
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [
+        ("epsilon", ctypes.c_double), ("gamma_override", ctypes.c_double), ("max_iterations", ctypes.c_int64),
+        ("block_rule", ctypes.c_int), ("tuning_exponent_p", ctypes.c_double), ("deterministic", ctypes.c_int),
+        ("log_every", ctypes.c_int64), ("record_rounded_cost", ctypes.c_int), ("materialize_plan", ctypes.c_int),
+        ("collect_iter_log", ctypes.c_int), ("use_graphs", ctypes.c_int), ("sync_every", ctypes.c_int),
+    ]
+
+
+class _Trace(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("error", ctypes.c_double), ("phi", ctypes.c_double),
+                ("rounded_cost", ctypes.c_double), ("elapsed_s", ctypes.c_double)]
+
+
+class _IterLog(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("halvings", ctypes.c_int32), ("block_hat", ctypes.c_int32),
+                ("zbest_is_check", ctypes.c_int32), ("block_check", ctypes.c_int32), ("error", ctypes.c_double),
+                ("phi_check", ctypes.c_double), ("phi_hat", ctypes.c_double), ("theta", ctypes.c_double)]
+
+
+class _Summary(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int), ("iterations", ctypes.c_int64), ("gamma", ctypes.c_double),
+        ("tolerance", ctypes.c_double), ("final_error", ctypes.c_double), ("wall_seconds", ctypes.c_double),
+        ("loop_seconds", ctypes.c_double), ("has_bounds", ctypes.c_int), ("bound_R", ctypes.c_double),
+        ("bound_L", ctypes.c_double), ("bound_mu_f", ctypes.c_double), ("iteration_bound", ctypes.c_double),
+        ("cost", ctypes.c_double), ("feasibility_gap", ctypes.c_double), ("mass", ctypes.c_double),
+        ("phi", ctypes.c_double), ("trace_len", ctypes.c_int64), ("iter_log_len", ctypes.c_int64),
+        ("sweeps", ctypes.c_int64), ("attempts", ctypes.c_int64), ("stopping_iterate", ctypes.c_char * 24),
+    ]
+
+
+class _Outputs(ctypes.Structure):
+    _fields_ = [
+        ("X", ctypes.POINTER(ctypes.c_double)), ("row_slack", ctypes.POINTER(ctypes.c_double)),
+        ("col_slack", ctypes.POINTER(ctypes.c_double)), ("trace", ctypes.POINTER(_Trace)), ("trace_cap", ctypes.c_int64),
+        ("iter_log", ctypes.POINTER(_IterLog)), ("iter_log_cap", ctypes.c_int64),
+        ("u", ctypes.POINTER(ctypes.c_double)), ("v", ctypes.POINTER(ctypes.c_double)),
+        ("w", ctypes.POINTER(ctypes.c_double)),
+    ]
+
+
+# Every symbol include/potgpu.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = (
+    "potgpu_abi_version", "potgpu_last_error", "potgpu_config_default", "potgpu_create", "potgpu_destroy",
+    "potgpu_solve", "potgpu_dual_eval", "potgpu_round_pot", "potgpu_comm_unique_id", "potgpu_comm_init",
+    "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
+    "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
+    "potgpu_session_stats",
+)
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libpotgpu.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise PotError(ErrorCode.CudaError, f"{path} is missing: run __graft_entry__.build() (make -C paper_2601_17196_b200)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    dp = P(ctypes.c_double)
+    lib.potgpu_last_error.restype = ctypes.c_char_p
+    lib.potgpu_create.argtypes = [ctypes.c_int, P(ctypes.c_void_p)]
+    lib.potgpu_destroy.argtypes = [ctypes.c_void_p]
+    lib.potgpu_config_default.argtypes = [P(_Config)]
+    lib.potgpu_solve.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), P(_Config), P(_Summary), P(_Outputs)]
+    lib.potgpu_dual_eval.argtypes = [ctypes.c_void_p, P(_Problem), ctypes.c_double, dp, dp, ctypes.c_double, dp, dp, dp]
+    lib.potgpu_session_begin.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), P(_Config), ctypes.c_int64,
+                                         ctypes.c_int64, P(ctypes.c_void_p)]
+    lib.potgpu_session_iterate.argtypes = [ctypes.c_void_p, ctypes.c_int64, dp, P(ctypes.c_int64), P(ctypes.c_int)]
+    lib.potgpu_session_finish.argtypes = [ctypes.c_void_p, P(_Summary), P(_Outputs)]
+    lib.potgpu_session_destroy.argtypes = [ctypes.c_void_p]
+    lib.potgpu_ctx_stream.argtypes = [ctypes.c_void_p]
+    lib.potgpu_ctx_stream.restype = ctypes.c_void_p
+    lib.potgpu_session_time_sweep.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, dp, dp]
+    lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.potgpu_make_synthetic.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, dp, dp, dp, dp]
+    lib.potgpu_make_config.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, dp, dp, dp, dp,
+                                       P(ctypes.c_int), dp, dp]
+    _lib = lib
+    return lib
+
+
+def _dp(a: Optional[np.ndarray]):
+    if a is None:
+        return ctypes.POINTER(ctypes.c_double)()
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = load_library().potgpu_last_error().decode(errors="replace")
+        raise PotError(ErrorCode(rc - 1), msg)
+
+
+# ------------------------------------------------------------ public types --
+@dataclass
+class Instance:
+    """core.hpp:108-118. Either a dense cost C (n x n) or, for the on-the-fly
+    squared-Euclidean kernel, point coordinates X, Y (n x d) with
+    C_ij = cost_scale |x_i - y_j|^2 (cost_scale None -> 1 / max)."""
+    r: np.ndarray
+    c: np.ndarray
+    s: float
+    C: Optional[np.ndarray] = None
+    X: Optional[np.ndarray] = None
+    Y: Optional[np.ndarray] = None
+    cost_scale: Optional[float] = None
+    dtype: DType = DType.F64
+    stored: bool = False  # points given, cost materialised once on the device and streamed
+
+    def size(self) -> int:
+        return int(np.asarray(self.r).shape[0])
+
+    def source_mass(self) -> float:
+        return float(np.sum(self.r))
+
+    def target_mass(self) -> float:
+        return float(np.sum(self.c))
+
+
+@dataclass
+class SolverConfig:  # core.hpp:241-267
+    epsilon: float = 0.1
+    gamma_override: Optional[float] = None
+    max_iterations: int = 50000
+    block_rule: BlockRule = BlockRule.Greedy
+    tuning_exponent_p: float = 1.0
+    deterministic: bool = True
+    log_every: int = 1
+    # device options (no reference counterpart)
+    record_rounded_cost: bool = True
+    materialize_plan: bool = True
+    collect_iter_log: bool = False
+    use_graphs: bool = True
+    sync_every: int = 8
+
+
+@dataclass
+class TraceRecord:  # core.hpp:269-275
+    t: int
+    error: float
+    phi: float
+    rounded_cost: Optional[float]
+    elapsed_s: float
+
+
+@dataclass
+class TheoryBounds:  # solvers.hpp:139-144
+    R: float
+    L: float
+    mu_f: float
+    iteration_bound: float
+
+
+@dataclass
+class TransportPlan:  # core.hpp:179-197 (X is None unless materialised)
+    X: Optional[np.ndarray]
+    row_slack: np.ndarray
+    col_slack: np.ndarray
+    mass: float
+
+
+@dataclass
+class SolveResult:  # solvers.hpp:176-186 (+ plan metrics computed on the device)
+    plan: TransportPlan
+    trace: List[TraceRecord]
+    stopping_iterate: str
+    status: SolveStatus
+    iterations: int
+    gamma: float
+    tolerance: float
+    final_error: float
+    wall_seconds: float
+    bounds: Optional[TheoryBounds]
+    cost: float
+    feasibility_gap: float
+    phi: float
+    loop_seconds: float = 0.0
+    sweeps: int = 0
+    attempts: int = 0
+    iter_log: Optional[np.ndarray] = None
+    u: Optional[np.ndarray] = None
+    v: Optional[np.ndarray] = None
+    w: Optional[float] = None
+
+
+ITER_LOG_FIELDS = ("t", "halvings", "block_hat", "zbest_is_check", "block_check", "error", "phi_check", "phi_hat",
+                   "theta")
+
+
+class Context:
+    """Owns a device, a stream and the workspaces (potgpu_create)."""
+
+    def __init__(self, device: int = 0):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.potgpu_create(int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if self._h:
+            load_library().potgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("POTGPU_USE_LOCAL_RANK") else 0)
+    return _default_ctx
+
+
+def _problem(inst: Instance, keep: list) -> _Problem:
+    n = inst.size()
+    p = _Problem()
+    p.n = n
+    p.dtype = int(inst.dtype)
+    r = np.ascontiguousarray(inst.r, dtype=np.float64)
+    c = np.ascontiguousarray(inst.c, dtype=np.float64)
+    keep += [r, c]
+    p.r, p.c, p.s = _dp(r), _dp(c), float(inst.s)
+    if inst.C is not None:
+        C = np.ascontiguousarray(inst.C, dtype=np.float64)
+        if C.shape != (n, n):
+            raise PotError(ErrorCode.DimensionMismatch, f"cost matrix is {C.shape}, expected {(n, n)}")
+        keep.append(C)
+        p.cost_kind, p.C, p.ldc, p.row_major = 0, _dp(C), n, 1
+    else:
+        X = np.ascontiguousarray(inst.X, dtype=np.float64)
+        Y = np.ascontiguousarray(inst.Y, dtype=np.float64)
+        keep += [X, Y]
+        p.cost_kind, p.X, p.Y, p.d = (2 if inst.stored else 1), _dp(X), _dp(Y), int(X.shape[1])
+        p.cost_scale = float(inst.cost_scale) if inst.cost_scale else 0.0
+    return p
+
+
+def _config(cfg: SolverConfig) -> _Config:
+    c = _Config()
+    c.epsilon = cfg.epsilon
+    c.gamma_override = cfg.gamma_override if cfg.gamma_override is not None else 0.0
+    if cfg.gamma_override is not None and not cfg.gamma_override > 0:
+        raise PotError(ErrorCode.InvalidArgument, "gamma override must be positive")
+    c.max_iterations = int(cfg.max_iterations)
+    c.block_rule = int(cfg.block_rule)
+    c.tuning_exponent_p = cfg.tuning_exponent_p
+    c.deterministic = int(cfg.deterministic)
+    c.log_every = int(cfg.log_every)
+    c.record_rounded_cost = int(cfg.record_rounded_cost)
+    c.materialize_plan = int(cfg.materialize_plan)
+    c.collect_iter_log = int(cfg.collect_iter_log)
+    c.use_graphs = int(cfg.use_graphs)
+    c.sync_every = int(cfg.sync_every)
+    return c
+
+
+class _OutBufs:
+    def __init__(self, kind: SolverKind, n: int, cfg: SolverConfig, trace_cap: int, iter_log_cap: int):
+        self.X = np.empty((n, n), dtype=np.float64) if cfg.materialize_plan else None
+        self.rs = np.empty(n, dtype=np.float64)
+        self.cs = np.empty(n, dtype=np.float64)
+        m = n + 1 if kind != SolverKind.Aspot else n
+        self.u = np.empty(m, dtype=np.float64)
+        self.v = np.empty(m, dtype=np.float64)
+        self.w = np.zeros(1, dtype=np.float64)
+        self.trace_cap = trace_cap
+        self.trace = (_Trace * max(trace_cap, 1))()
+        self.cap = iter_log_cap if cfg.collect_iter_log else 0
+        self.ilog = (_IterLog * max(self.cap, 1))()
+        out = _Outputs()
+        out.X, out.row_slack, out.col_slack = _dp(self.X), _dp(self.rs), _dp(self.cs)
+        out.trace, out.trace_cap = self.trace, trace_cap
+        out.iter_log, out.iter_log_cap = self.ilog, self.cap
+        out.u, out.v, out.w = _dp(self.u), _dp(self.v), _dp(self.w)
+        self.out = out
+
+    def result(self, sm: _Summary) -> SolveResult:
+        tl = min(int(sm.trace_len), self.trace_cap)
+        tr = self.trace
+        recs = [TraceRecord(int(tr[k].t), tr[k].error, tr[k].phi,
+                            None if math.isnan(tr[k].rounded_cost) else tr[k].rounded_cost, tr[k].elapsed_s)
+                for k in range(tl)]
+        il = None
+        if self.cap:
+            k = min(int(sm.iter_log_len), self.cap)
+            il = np.array([[getattr(self.ilog[i], f) for f in ITER_LOG_FIELDS] for i in range(k)],
+                          dtype=np.float64).reshape(k, 9)
+        bounds = TheoryBounds(sm.bound_R, sm.bound_L, sm.bound_mu_f, sm.iteration_bound) if sm.has_bounds else None
+        return SolveResult(
+            plan=TransportPlan(self.X, self.rs, self.cs, sm.mass), trace=recs,
+            stopping_iterate=sm.stopping_iterate.decode(), status=SolveStatus(sm.status),
+            iterations=int(sm.iterations), gamma=sm.gamma, tolerance=sm.tolerance, final_error=sm.final_error,
+            wall_seconds=sm.wall_seconds, bounds=bounds, cost=sm.cost, feasibility_gap=sm.feasibility_gap,
+            phi=sm.phi, loop_seconds=sm.loop_seconds, sweeps=int(sm.sweeps), attempts=int(sm.attempts),
+            iter_log=il, u=self.u, v=self.v, w=float(self.w[0]))
+
+
+def _run(kind: SolverKind, inst: Instance, cfg: SolverConfig, ctx: Optional[Context], trace_cap: int = 4096,
+         iter_log_cap: int = 0) -> SolveResult:
+    lib = load_library()
+    ctx = ctx or default_context()
+    keep: list = []
+    prob = _problem(inst, keep)
+    conf = _config(cfg)
+    bufs = _OutBufs(kind, inst.size(), cfg, trace_cap, iter_log_cap)
+    sm = _Summary()
+    _check(lib.potgpu_solve(ctx._h, int(kind), ctypes.byref(prob), ctypes.byref(conf), ctypes.byref(sm),
+                            ctypes.byref(bufs.out)))
+    return bufs.result(sm)
+
+
+class Session:
+    """potgpu_session_*: begin (setup + first evaluation), iterate(k) with
+    device timing, finish (final rounding + outputs)."""
+
+    def __init__(self, kind: SolverKind, inst: Instance, config: SolverConfig = SolverConfig(),
+                 ctx: Optional[Context] = None, trace_cap: int = 4096, iter_log_cap: int = 0):
+        self.lib = load_library()
+        self.ctx = ctx or default_context()
+        self.kind = SolverKind(kind)
+        self.cfg = config
+        self._keep: list = []
+        prob = _problem(inst, self._keep)
+        conf = _config(config)
+        self.bufs = _OutBufs(self.kind, inst.size(), config, trace_cap, iter_log_cap)
+        h = ctypes.c_void_p()
+        _check(self.lib.potgpu_session_begin(self.ctx._h, int(kind), ctypes.byref(prob), ctypes.byref(conf),
+                                             trace_cap, iter_log_cap if config.collect_iter_log else 0,
+                                             ctypes.byref(h)))
+        self._h = h
+
+    def iterate(self, k: int):
+        """Returns (device_ms, iterations_done, finished)."""
+        ms = np.zeros(1)
+        it = ctypes.c_int64(0)
+        fin = ctypes.c_int(0)
+        _check(self.lib.potgpu_session_iterate(self._h, int(k), _dp(ms), ctypes.byref(it), ctypes.byref(fin)))
+        return float(ms[0]), int(it.value), bool(fin.value)
+
+    def time_sweep(self, reps: int = 10):
+        """(ms per sweep launch, elements per launch, HBM bytes per launch)."""
+        ms, el, by = np.zeros(1), np.zeros(1), np.zeros(1)
+        _check(self.lib.potgpu_session_time_sweep(self._h, int(reps), _dp(ms), _dp(el), _dp(by)))
+        return float(ms[0]), float(el[0]), float(by[0])
+
+    def stats(self):
+        """(kernel launches by iterate(), attempts, sweeps) so far."""
+        k, a, w = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(self.lib.potgpu_session_stats(self._h, ctypes.byref(k), ctypes.byref(a), ctypes.byref(w)))
+        return int(k.value), int(a.value), int(w.value)
+
+    def finish(self) -> SolveResult:
+        sm = _Summary()
+        _check(self.lib.potgpu_session_finish(self._h, ctypes.byref(sm), ctypes.byref(self.bufs.out)))
+        return self.bufs.result(sm)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.potgpu_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def aspot_solve(inst: Instance, config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
+                **kw) -> SolveResult:
+    """solvers.hpp:265-385."""
+    return _run(SolverKind.Aspot, inst, config, ctx, **kw)
+
+
+def feasible_sinkhorn_solve(inst: Instance, config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
+                            **kw) -> SolveResult:
+    """solvers.hpp:516-542."""
+    return _run(SolverKind.FeasibleSinkhorn, inst, config, ctx, **kw)
+
+
+def tuned_sinkhorn_solve(inst: Instance, epsilon_or_config=None, p: Optional[float] = None,
+                         config: Optional[SolverConfig] = None, ctx: Optional[Context] = None, **kw) -> SolveResult:
+    """solvers.hpp:547-589: (inst, epsilon, p, config) or (inst, config)."""
+    if isinstance(epsilon_or_config, SolverConfig) or epsilon_or_config is None:
+        cfg = epsilon_or_config or config or SolverConfig()
+    else:
+        base = config or SolverConfig()
+        cfg = SolverConfig(**{**base.__dict__, "epsilon": float(epsilon_or_config),
+                              "tuning_exponent_p": float(p if p is not None else base.tuning_exponent_p)})
+    return _run(SolverKind.TunedSinkhorn, inst, cfg, ctx, **kw)
+
+
+def solve(inst: Instance, kind: SolverKind, config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
+          **kw) -> SolveResult:
+    """solvers.hpp:591-599."""
+    return _run(SolverKind(kind), inst, config, ctx, **kw)
+
+
+@dataclass
+class DualEval:
+    row: np.ndarray     # B 1
+    col: np.ndarray     # B^T 1
+    total: float
+    max_exponent: float
+    phi: float
+    error: float
+    grad_w: float
+
+
+def dual_eval(inst: Instance, gamma: float, u, v, w: float, ctx: Optional[Context] = None) -> DualEval:
+    """b_matrix / dual_objective / dual_gradient / feasibility_error sums at
+    z = (u, v, w) for logK = -C/gamma with the instance's marginals as given
+    (dual.hpp:104-141). Raises PotError(Overflow) like the reference."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    keep: list = []
+    prob = _problem(inst, keep)
+    n = inst.size()
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    row = np.empty(n)
+    col = np.empty(n)
+    sc = np.empty(6)
+    _check(lib.potgpu_dual_eval(ctx._h, ctypes.byref(prob), float(gamma), _dp(u), _dp(v), float(w), _dp(row),
+                                _dp(col), _dp(sc)))
+    return DualEval(row, col, sc[0], sc[1], sc[2], sc[3], sc[4])
+
+
+def make_synthetic_instance(n: int, seed: int, mass_r: float, mass_c: float, s_frac: float) -> Instance:
+    """synthetic.hpp:15-54 (bit-identical draw order)."""
+    lib = load_library()
+    r, c, C, s = np.empty(n), np.empty(n), np.empty((n, n)), np.empty(1)
+    rc = lib.potgpu_make_synthetic(n, seed, mass_r, mass_c, s_frac, _dp(r), _dp(c), _dp(C), _dp(s))
+    if rc:
+        raise PotError(ErrorCode(rc - 1), "invalid synthetic instance parameters")
+    return Instance(r=r, c=c, s=float(s[0]), C=C)
+
+
+def make_scaling_instance(n: int, seed: int) -> Instance:  # synthetic.hpp:58-60
+    return make_synthetic_instance(n, seed, 5.0, 3.0, 0.2)
+
+
+def make_config_points(config_id: int, n: int, seed: int = 1):
+    """BASELINE.json configs[config_id - 1] as points: returns
+    (r, c, X, Y, s, cost_scale)."""
+    lib = load_library()
+    r, c = np.empty(n), np.empty(n)
+    X, Y = np.empty((n, 3)), np.empty((n, 3))
+    d = ctypes.c_int(0)
+    s, sc = np.empty(1), np.empty(1)
+    rc = lib.potgpu_make_config(config_id, n, seed, _dp(r), _dp(c), _dp(X), _dp(Y), ctypes.byref(d), _dp(s), _dp(sc))
+    if rc:
+        raise PotError(ErrorCode(rc - 1), "invalid config id / size")
+    dd = d.value
+    X = X.reshape(-1)[: n * dd].reshape(n, dd).copy()
+    Y = Y.reshape(-1)[: n * dd].reshape(n, dd).copy()
+    return r, c, X, Y, float(s[0]), float(sc[0])
+
+
+def dense_cost(X: np.ndarray, Y: np.ndarray, cost_scale: float) -> np.ndarray:
+    """C_ij = cost_scale * |x_i - y_j|^2 with the cost views' fp64 association."""
+    C = np.zeros((X.shape[0], Y.shape[0]))
+    for k in range(X.shape[1]):
+        D = X[:, k][:, None] - Y[:, k][None, :]
+        C = C + D * D
+    return C * cost_scale
+
+
+def points_scale(X: np.ndarray, Y: np.ndarray, chunk: int = 1024) -> float:
+    """1 / max_ij |x_i - y_j|^2 (same fp64 association as the device)."""
+    m = 0.0
+    for a in range(0, X.shape[0], chunk):
+        m = max(m, float(dense_cost(X[a:a + chunk], Y, 1.0).max()))
+    return 1.0 / m if m > 0 else 1.0
+
+
+def config_instance(config_id: int, n: Optional[int] = None, seed: int = 1, dense: Optional[bool] = None,
+                    dtype: Optional[DType] = None) -> Instance:
+    """Instance for a BASELINE.json workload."""
+    defaults = {1: (1000, True, DType.F64), 2: (4096, True, DType.F64), 3: (16384, False, DType.F32),
+                4: (65536, False, DType.F32), 5: (2048, True, DType.F32)}
+    n0, dense0, dt0 = defaults[config_id]
+    n = n or n0
+    dense = dense0 if dense is None else dense
+    dtype = dt0 if dtype is None else dtype
+    r, c, X, Y, s, scale = make_config_points(config_id, n, seed)
+    if dtype == DType.F32:  # fp32 instances: coordinates are rounded once, here
+        X = X.astype(np.float32).astype(np.float64)
+        Y = Y.astype(np.float32).astype(np.float64)
+        scale = points_scale(X, Y) if (dense or n <= 8192) else 0.0  # 0: derived on the device
+    if dense:
+        C = dense_cost(X, Y, scale)
+        if dtype == DType.F32:
+            C = C.astype(np.float32).astype(np.float64)
+        return Instance(r=r, c=c, s=s, C=C, dtype=dtype)
+    return Instance(r=r, c=c, s=s, X=X, Y=Y, cost_scale=scale if scale > 0 else None, dtype=dtype)

@@ -1,0 +1,215 @@
+"""GPU parity of the accelerated solver and the B(z) sweep against the CPU
+oracle (oracle/pot_oracle.hpp), through the C-ABI.
+
+Bars (BASELINE.json north_star): fp64 — identical iteration counts, status
+and per-iteration decisions (block choices, z_best choice, halvings),
+objective rel <= 1e-6, violation <= 1e-7; fp32 — objective rel <= 1e-4,
+violation <= 1e-5."""
+import numpy as np
+import pytest
+
+from oracle import binding
+from paper_2601_17196_b200 import pot
+
+pytestmark = pytest.mark.gpu
+
+TOL_F64_OBJ = 1e-6
+TOL_F64_VIOL = 1e-7
+TOL_F32_OBJ = 1e-4
+TOL_F32_VIOL = 1e-5
+
+
+def inst_of(r, c, C, s, dtype=pot.DType.F64):
+    return pot.Instance(r=r, c=c, s=s, C=C, dtype=dtype)
+
+
+# ------------------------------------------------------------- the sweep --
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 255, 256, 257, 1000])
+def test_sweep_sums_match_oracle(ctx, n):
+    rng = np.random.default_rng(n)
+    r, c, C, s = binding.random_instance(100 + n, n)
+    gamma = 0.05
+    for rep in range(3):
+        u = rng.uniform(-3, 1, n)
+        v = rng.uniform(-3, 1, n)
+        w = float(rng.uniform(-1, 1))
+        rc, row, col, tot, mx = binding.sweep(C, gamma, u, v, w)
+        assert rc == 0
+        ev = pot.dual_eval(inst_of(r, c, C, s), gamma, u, v, w, ctx=ctx)
+        np.testing.assert_allclose(ev.row, row, rtol=1e-13, atol=0)
+        np.testing.assert_allclose(ev.col, col, rtol=1e-13, atol=0)
+        assert abs(ev.total - tot) <= 1e-13 * tot
+        assert ev.max_exponent == pytest.approx(mx, rel=0, abs=1e-12)
+
+
+def test_sweep_overflow_is_structured_error(ctx):
+    """test_dual.cpp:54-62: exponent 800 > 700 raises Overflow."""
+    inst = inst_of(np.ones(1), np.ones(1), np.zeros((1, 1)), 0.5)
+    with pytest.raises(pot.PotError) as e:
+        pot.dual_eval(inst, 1.0, np.array([400.0]), np.array([400.0]), 0.0, ctx=ctx)
+    assert e.value.code == pot.ErrorCode.Overflow
+
+
+def test_dual_hand_values(ctx):
+    """test_dual.cpp:73-76, 111-117, 157-160: phi = 3, grad = (1, 1, 0.5), E = 2.5."""
+    inst = inst_of(np.ones(1), np.ones(1), np.zeros((1, 1)), 0.5)
+    ev = pot.dual_eval(inst, 1.0, np.zeros(1), np.zeros(1), 0.0, ctx=ctx)
+    assert ev.phi == 3.0
+    assert ev.row[0] == 1.0 and ev.grad_w == 0.5
+    assert ev.error == 2.5
+
+
+# ---------------------------------------------------------- fp64 solves --
+def compare_fp64(ctx, r, c, C, s, cfg: pot.SolverConfig, exact_decisions=True):
+    cfg.collect_iter_log = True
+    g = pot.aspot_solve(inst_of(r, c, C, s), cfg, ctx=ctx, iter_log_cap=200000)
+    o = binding.solve(0, r, c, s, C=C, epsilon=cfg.epsilon, gamma_override=cfg.gamma_override,
+                      max_iterations=cfg.max_iterations, block_rule=int(cfg.block_rule), log_every=10 ** 9)
+    assert int(g.status) == o.status
+    assert g.iterations == o.iterations
+    assert g.gamma == o.gamma and g.tolerance == o.tolerance
+    if exact_decisions:
+        # decision columns: halvings, block_hat, zbest_is_check, block_check
+        np.testing.assert_array_equal(g.iter_log[:, 1:5], o.log[:, 1:5])
+    np.testing.assert_allclose(g.iter_log[:, 5], o.log[:, 5], rtol=1e-9, atol=1e-14)
+    assert abs(g.final_error - o.final_error) <= 1e-9 * max(o.final_error, 1e-30) + 1e-15
+    assert abs(g.cost - o.cost) <= TOL_F64_OBJ * max(abs(o.cost), 1e-12)
+    assert g.feasibility_gap <= TOL_F64_VIOL
+    assert abs(g.plan.mass - s) <= TOL_F64_VIOL
+    if g.plan.X is not None and o.plan is not None:
+        np.testing.assert_allclose(g.plan.X, o.plan, rtol=1e-6, atol=1e-12)
+    return g, o
+
+
+@pytest.mark.parametrize("seed,n,eps", [(24, 5, 0.1), (25, 6, 0.05), (26, 5, 0.05), (28, 6, 0.1), (13, 4, 0.02)])
+def test_aspot_small_instances_match_oracle(ctx, seed, n, eps):
+    r, c, C, s = binding.random_instance(seed, n)
+    cfg = pot.SolverConfig(epsilon=eps, log_every=10 ** 9)
+    compare_fp64(ctx, r, c, C, s, cfg)
+
+
+def test_aspot_round_robin_matches_oracle(ctx):
+    r, c, C, s = binding.random_instance(77, 9)
+    cfg = pot.SolverConfig(epsilon=0.05, log_every=10 ** 9, block_rule=pot.BlockRule.RoundRobin)
+    compare_fp64(ctx, r, c, C, s, cfg)
+
+
+def test_aspot_overflow_halving(ctx):
+    """test_solvers.cpp:272-290: gamma 1e5 with masses 50 forces halvings."""
+    r = np.full(2, 50.0)
+    C = np.ones((2, 2)) - np.eye(2)
+    cfg = pot.SolverConfig(epsilon=0.1, gamma_override=1e5, max_iterations=20000, log_every=10 ** 9)
+    g, o = compare_fp64(ctx, r, r.copy(), C, 1.0, cfg)
+    assert g.status != pot.SolveStatus.StepSizeUnderflow
+    assert g.iter_log[:, 1].sum() > 0  # halvings happened
+    assert g.feasibility_gap <= 1e-9 * r.sum()
+
+
+def test_aspot_max_iterations(ctx):
+    """test_solvers.cpp:292-303."""
+    r, c, C, s = binding.random_instance(27, 6)
+    cfg = pot.SolverConfig(epsilon=1e-4, max_iterations=2)
+    g, o = compare_fp64(ctx, r, c, C, s, cfg)
+    assert g.status == pot.SolveStatus.MaxIterationsExceeded and g.iterations == 2
+    assert len(g.trace) >= 1
+    assert g.feasibility_gap <= 1e-9
+
+
+def test_aspot_paper_overrides(ctx):
+    """test_solvers.cpp:225-237 (make_scaling_instance(40, 5), gamma 1e-3, tol 1e-7)."""
+    inst = pot.make_scaling_instance(40, 5)
+    cfg = pot.SolverConfig(epsilon=8e-7, gamma_override=1e-3, max_iterations=1500, log_every=10 ** 9)
+    g, o = compare_fp64(ctx, inst.r, inst.c, inst.C, inst.s, cfg)
+    assert g.gamma == 1e-3 and g.status == pot.SolveStatus.Converged
+    assert g.final_error <= g.tolerance
+
+
+def test_aspot_trace_records_match_oracle(ctx):
+    """log_every = 1 (the reference default): every record carries the
+    rounded cost of round_pot(B(z_check)) (solvers.hpp:308-318)."""
+    r, c, C, s = binding.random_instance(25, 6)
+    g = pot.aspot_solve(inst_of(r, c, C, s), pot.SolverConfig(epsilon=0.05), ctx=ctx)
+    o = binding.solve(0, r, c, s, C=C, epsilon=0.05, log_every=1, record_rounded_cost=True)
+    assert len(g.trace) == len(o.trace)
+    for rec, orow in zip(g.trace, o.trace):
+        assert rec.t == int(orow[0])
+        assert rec.error == pytest.approx(orow[1], rel=1e-9)
+        assert rec.phi == pytest.approx(orow[2], rel=1e-12)
+        assert rec.rounded_cost == pytest.approx(orow[3], rel=1e-9)
+    assert g.stopping_iterate == "z_check"
+
+
+def test_zero_budget_and_degenerate(ctx):
+    """test_solvers.cpp:194-207, 480-490."""
+    r, c, C, s = binding.random_instance(34, 4)
+    g = pot.aspot_solve(inst_of(r, c, C, 0.0), pot.SolverConfig(), ctx=ctx)
+    assert g.status == pot.SolveStatus.Converged and np.abs(g.plan.X).max() == 0.0
+    assert g.stopping_iterate == "trivial"
+    with pytest.raises(pot.PotError) as e:
+        pot.aspot_solve(inst_of(np.ones(1), np.ones(1), np.zeros((1, 1)), 0.5), pot.SolverConfig(), ctx=ctx)
+    assert e.value.code == pot.ErrorCode.DegenerateInstance
+    Z = np.ones((2, 2)) - np.eye(2)
+    g = pot.aspot_solve(inst_of(np.full(2, 0.5), np.full(2, 0.5), 0 * Z, 0.5), pot.SolverConfig(epsilon=0.1), ctx=ctx)
+    assert g.status == pot.SolveStatus.Converged and abs(g.cost) <= 1e-15 and g.feasibility_gap <= 1e-9
+
+
+def test_validation_errors(ctx):
+    """test_core.cpp:24-87: first violation's code."""
+    bad = inst_of(np.ones(1), np.ones(1), np.zeros((1, 1)), 2.0)
+    with pytest.raises(pot.PotError) as e:
+        pot.aspot_solve(bad, pot.SolverConfig(), ctx=ctx)
+    assert e.value.code == pot.ErrorCode.BudgetExceedsMass
+    C = np.array([[np.inf]])
+    with pytest.raises(pot.PotError) as e:
+        pot.aspot_solve(inst_of(np.ones(1), np.ones(1), C, 0.5), pot.SolverConfig(), ctx=ctx)
+    assert e.value.code == pot.ErrorCode.NonFiniteEntry
+
+
+def test_aspot_c1_small_matches_oracle(ctx):
+    """configs[0] recipe at n = 300 (the full n = 1000 case is below)."""
+    inst = pot.config_instance(1, n=300)
+    compare_fp64(ctx, inst.r, inst.c, inst.C, inst.s, pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9))
+
+
+@pytest.mark.slow
+def test_aspot_c1_full_matches_oracle(ctx):
+    """configs[0]: n = 1000 fp64, eps = 1e-2, stored C, run to convergence:
+    identical iteration count and decision log."""
+    inst = pot.config_instance(1, n=1000)
+    g, o = compare_fp64(ctx, inst.r, inst.c, inst.C, inst.s, pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9))
+    assert g.status == pot.SolveStatus.Converged
+
+
+def test_aspot_deterministic(ctx):
+    """test_cli.cpp:136-155 analogue: two solves give identical traces."""
+    inst = pot.config_instance(1, n=200)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=5)
+    a = pot.aspot_solve(inst, cfg, ctx=ctx)
+    b = pot.aspot_solve(inst, cfg, ctx=ctx)
+    assert [(t.t, t.error, t.phi, t.rounded_cost) for t in a.trace] == [(t.t, t.error, t.phi, t.rounded_cost) for t in b.trace]
+    assert np.array_equal(a.plan.X, b.plan.X)
+
+
+# ----------------------------------------------------------- fp32 solves --
+def test_aspot_fp32_points_prefix_and_converged(ctx):
+    """configs[2] shape (registration clouds, on-the-fly cost) at n = 1024:
+    fp32 path vs fp64 oracle on the same fp32-rounded coordinates."""
+    inst = pot.config_instance(3, n=1024)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False)
+    g = pot.aspot_solve(inst, cfg, ctx=ctx)
+    C = pot.dense_cost(inst.X, inst.Y, inst.cost_scale)
+    o = binding.solve(0, inst.r, inst.c, inst.s, C=C, epsilon=1e-2, log_every=10 ** 9)
+    assert g.status == pot.SolveStatus.Converged == o.status
+    assert abs(g.cost - o.cost) <= TOL_F32_OBJ * abs(o.cost)
+    assert g.feasibility_gap <= TOL_F32_VIOL
+    assert abs(g.iterations - o.iterations) <= max(3, 0.05 * o.iterations)
+
+
+def test_aspot_fp32_dense_matches_oracle(ctx):
+    inst = pot.config_instance(5, n=512)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9)
+    g = pot.aspot_solve(inst, cfg, ctx=ctx)
+    o = binding.solve(0, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-2, log_every=10 ** 9)
+    assert g.status == o.status
+    assert abs(g.cost - o.cost) <= TOL_F32_OBJ * abs(o.cost)
+    assert g.feasibility_gap <= TOL_F32_VIOL
