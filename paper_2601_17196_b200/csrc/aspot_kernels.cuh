@@ -10,6 +10,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "sweep.cuh"
 
 namespace potgpu {
 
@@ -87,6 +88,7 @@ struct ReduceArgs {
   const double* rt; const double* ct;  // marginals the dual targets (mixed r~, c~)
   double* scratch;                      // [gridDim.x][kNumPartials + 1]
   const int* gate;
+  int pfmt;                             // PartialFormat of rowp/colp
 };
 
 __global__ void __launch_bounds__(kVecThreads) k_point_reduce(ReduceArgs a) {
@@ -99,11 +101,13 @@ __global__ void __launch_bounds__(kVecThreads) k_point_reduce(ReduceArgs a) {
   acc[1] = acc[2] = acc[11] = -INFINITY;
   const double* u = a.z.u();
   const double* v = a.z.v();
+  const double w = *a.z.w();
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double a2 = (u[i] + w) * kLog2e;  // row offset of fp32 row partials
     double rb = 0.0;
-    for (int64_t s = 0; s < a.nstrips; ++s) rb += a.rowp[s * n + i];
+    for (int64_t s = 0; s < a.nstrips; ++s) rb += partial_value(a.rowp, s * n + i, a.pfmt, a2);
     double cb = 0.0;
-    for (int64_t s = 0; s < a.nrowblocks; ++s) cb += a.colp[s * n + i];
+    for (int64_t s = 0; s < a.nrowblocks; ++s) cb += partial_value(a.colp, s * n + i, a.pfmt);
     a.row_out[i] = rb;
     a.col_out[i] = cb;
     const double ui = u[i], vi = v[i];

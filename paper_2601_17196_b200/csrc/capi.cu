@@ -78,7 +78,7 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
   P.n = n;
   P.dtype = pr->dtype;
   P.kind = pr->cost_kind;
-  P.ld = round_up(n, kStripCols);
+  P.ld = round_up(n, kStripCols32);  // covers both strip widths
   P.r.assign(pr->r, pr->r + n);
   P.c.assign(pr->c, pr->c + n);
   P.s = pr->s;
@@ -174,7 +174,28 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     throw Error(POTGPU_BUDGET_EXCEEDS_MASS, "invalid instance: budget exceeds min marginal mass");
 }
 
+__global__ void k_scale_points(const float4* X, int64_t n, float sc, float4* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 p = X[i];
+    out[i] = make_float4(p.x * sc, p.y * sc, p.z * sc, 0.f);
+  }
+}
+
+// Coordinates pre-scaled by sqrt(log2 e * scale / gamma): the fp32 sweep's
+// kappa is then |x' - y'|^2 in log2 units.
+void prepare_points(Context& cx, DevProblem& P, double gamma) {
+  if (P.kind != POTGPU_COST_SQEUCLIDEAN || P.XS_gamma == gamma) return;
+  P.XS4.alloc(size_t(P.n));
+  P.YS4.alloc(size_t(P.n));
+  const float sc = float(std::sqrt(kLog2e * P.cost_scale / gamma));
+  k_scale_points<<<cx.num_sms * 4, 256, 0, cx.stream>>>(P.X4.p, P.n, sc, P.XS4.p);
+  k_scale_points<<<cx.num_sms * 4, 256, 0, cx.stream>>>(P.Y4.p, P.n, sc, P.YS4.p);
+  PG_CK(cudaGetLastError());
+  P.XS_gamma = gamma;
+}
+
 void build_logk(Context& cx, DevProblem& P, double gamma) {
+  prepare_points(cx, P, gamma);
   if (P.dtype != POTGPU_F64 || P.kind != POTGPU_COST_DENSE) return;
   if (P.L_gamma == gamma && P.L64.p) return;
   P.L64.alloc(size_t(P.n * P.ld));

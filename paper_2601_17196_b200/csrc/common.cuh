@@ -130,10 +130,11 @@ __device__ __forceinline__ T warp_sum(T x) {
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
+// sm_100a: one CREDUX.MAX.F32 instead of a 5-step shuffle tree.
 __device__ __forceinline__ float warp_maxf(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
-  return x;
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+  return r;
 }
 __device__ __forceinline__ double warp_nanmax(double x) {
 #pragma unroll

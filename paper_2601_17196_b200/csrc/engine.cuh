@@ -44,6 +44,8 @@ struct DevProblem {
   double L_gamma = -1.0;   // gamma L64 was built for
   DevBuf<float> C32;       // fp32 dense C (n x ld), 0-padded
   DevBuf<float4> X4, Y4;   // fp32 points
+  DevBuf<float4> XS4, YS4; // points pre-scaled by sqrt(log2 e * scale / gamma) for the fp32 sweep
+  double XS_gamma = -1.0;
   double cost_scale = 1.0;
   double cmax = 0.0;
   std::vector<double> r, c;  // host copies (original marginals)
@@ -55,6 +57,9 @@ struct Workspace {
   SweepGrid g{};
   int64_t nstrips = 0, nrb = 0;
   int nblk = 0;  // O(n) kernel grid
+  int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
+  int strip = 256;
+  size_t sweep_smem = 0;
   DevBuf<double> slots;     // 7 dual points
   DevBuf<double> sums;      // 6 x (row, col)
   DevBuf<double> rowp, colp, maxp, scratch, partial;
@@ -93,7 +98,10 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f32<SrcPointsF32>, kThreads, 0));
   }
   occ = std::max(occ, 1);
-  ws.g = choose_grid(n, cx.num_sms, occ);
+  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : kStripCols32;
+  ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
+  ws.g = choose_grid(n, cx.num_sms, occ, ws.strip);
+  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : size_t(ws.g.rows_per_cta) * sizeof(float);
   ws.nstrips = ws.g.grid.x;
   ws.nrb = ws.g.grid.y;
   ws.nblk = int(std::min<int64_t>(cx.num_sms, std::max<int64_t>(1, ceil_div(n, kVecThreads))));
@@ -133,10 +141,11 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
     else sweep_f64_dense<false><<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
   } else if (P.kind == POTGPU_COST_DENSE) {
     SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
-    sweep_f32<SrcDenseF32><<<ws.g.grid, kThreads, 0, cx.stream>>>(s, a);
+    sweep_f32<SrcDenseF32><<<ws.g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   } else {
-    SrcPointsF32 s{P.X4.p, P.Y4.p, float(kLog2e * P.cost_scale / gamma)};
-    sweep_f32<SrcPointsF32><<<ws.g.grid, kThreads, 0, cx.stream>>>(s, a);
+    if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
+    SrcPointsF32 s{P.XS4.p, P.YS4.p};
+    sweep_f32<SrcPointsF32><<<ws.g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   }
   PG_CK(cudaGetLastError());
 }
@@ -151,6 +160,7 @@ inline void launch_reduce(Context& cx, Workspace& ws, Slot z, int sum_slot, cons
   r.rt = ws.rt.p; r.ct = ws.ct.p;
   r.scratch = ws.scratch.p;
   r.gate = gate;
+  r.pfmt = ws.pfmt;
   k_point_reduce<<<ws.nblk, kVecThreads, 0, cx.stream>>>(r);
   PG_CK(cudaGetLastError());
 }
@@ -177,9 +187,9 @@ inline void enqueue_rounding(Context& cx, const DevProblem& P, Workspace& ws, Sl
   AspotCtl* ctl = ws.ctl.p;
   k_round_a<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl, ra);
   launch_sweep(cx, P, ws, z, ra.lu, nullptr, gate, false, gamma);
-  k_round_b<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.colp.p, ws.nrb);
+  k_round_b<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.colp.p, ws.nrb, ws.pfmt);
   launch_sweep(cx, P, ws, z, ra.lu, ra.lv, gate, false, gamma);
-  k_round_c<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb);
+  k_round_c<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.pfmt);
   k_round_d<<<1, 32, 0, cx.stream>>>(ctl, ra, ws.nblk);
   k_round_e<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl, ra);
   const int rows = cost_sweep_rows(n);

@@ -60,12 +60,12 @@ __global__ void k_round_a(AspotCtl* ctl, RoundArgs a) {
 }
 
 // kappa_j = min(1, c_j / col_j) of the row-scaled plan (rounding.hpp:59-62)
-__global__ void k_round_b(RoundArgs a, const double* colp, int64_t nrb) {
+__global__ void k_round_b(RoundArgs a, const double* colp, int64_t nrb, int pfmt) {
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.n;
   for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
     double col = 0.0;
-    for (int64_t s = 0; s < nrb; ++s) col += colp[s * n + j];
+    for (int64_t s = 0; s < nrb; ++s) col += partial_value(colp, s * n + j, pfmt);
     const double k = col > 0 ? fmin(1.0, a.c[j] / col) : 1.0;
     a.kappa[j] = k;
     a.lv[j] = log(k);
@@ -88,14 +88,15 @@ __device__ void block_reduce_store(double (&acc)[K], double* out, const bool* is
 
 // Row/col sums of the scaled plan, slacks a, b (rounding.hpp:63-67)
 __global__ void __launch_bounds__(kVecThreads) k_round_c(RoundArgs a, const double* rowp, int64_t nstrips, const double* colp,
-                                                         int64_t nrb) {
+                                                         int64_t nrb, int pfmt) {
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.n;
   double acc[3] = {0.0, 0.0, 0.0};  // mass3, na, nb
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double row = 0.0, col = 0.0;
-    for (int64_t s = 0; s < nstrips; ++s) row += rowp[s * n + i];
-    for (int64_t s = 0; s < nrb; ++s) col += colp[s * n + i];
+    const double a2 = ((a.z.u()[i] + a.lu[i]) + *a.z.w()) * kLog2e;  // fp32 row-partial offset
+    for (int64_t s = 0; s < nstrips; ++s) row += partial_value(rowp, s * n + i, pfmt, a2);
+    for (int64_t s = 0; s < nrb; ++s) col += partial_value(colp, s * n + i, pfmt);
     a.rowx[i] = row;
     a.colx[i] = col;
     const double ai = fmax(a.r[i] - row, 0.0), bi = fmax(a.c[i] - col, 0.0);

@@ -116,67 +116,81 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __r
 }
 
 // ------------------------------------------------------------------------
-// fp32 sweeps. The exponent in log2 units t_ij = A_i + B_j - kappa_ij with
-// A_i = (u_i + w) log2 e, B_j = v_j log2 e (fp32, from fp64 potentials) and
-// kappa_ij = g2 * C_ij (stored fp32 C) or g2 * |x_i - y_j|^2 (coordinates).
-// Each row of a warp tile is exponentiated once with MUFU.EX2 at the exact
-// tile-row max m_i (no overflow, no underflow of the row's mass); the column
-// accumulators carry a per-warp running scale sigma and take p_ij 2^(m_i -
-// sigma). Partials leave the kernel as fp64 values sum * 2^scale.
+// fp32 sweeps. Exponent in log2 units t_ij = A_i + B_j - kappa_ij with
+// A_i = (u_i + w) log2 e and B_j = v_j log2 e (fp32, from the fp64
+// potentials) and kappa_ij = g2 C_ij (stored fp32 C) or |x'_i - y'_j|^2 with
+// coordinates pre-scaled by sqrt(log2 e * scale / gamma) (on-the-fly).
+//
+// Each row segment of a warp (512 columns, 16 per lane) is exponentiated
+// once with MUFU.EX2 at its exact max m_i, so the row's mass never over- or
+// underflows; column accumulators carry a per-warp running scale sigma and
+// take p_ij 2^(m_i - sigma). Partials leave as fp32 (sum, log2 scale) pairs
+// and are turned into fp64 values by the reduce kernels, so the hot loop has
+// no fp64 work at all.
+constexpr int kStripCols32 = 512;
+constexpr int kPairs = 8;  // 16 columns per lane as 8 float2 pairs
+
+// Lane column map: pair q (0..7), half h: j = j0 + 4*lane + 128*(q>>1) + 2*(q&1) + h.
+__device__ __forceinline__ int64_t f32_col(int64_t j0, int lane, int q, int h) {
+  return j0 + 4 * lane + 128 * (q >> 1) + 2 * (q & 1) + h;
+}
+
 struct SrcDenseF32 {
   const float* C;
   int64_t ld;
   float g2;  // log2(e) / gamma
-  static constexpr int kColRegs = 0;
   struct Col {};
   struct RowCtx { const float4* p; };
-  __device__ __forceinline__ void load_cols(int64_t, Col*) const {}
+  static constexpr bool kHasCols = false;
   __device__ __forceinline__ RowCtx row(int64_t i, int64_t j0, int lane) const {
     return RowCtx{reinterpret_cast<const float4*>(C + i * ld + j0) + lane};
   }
-  // -kappa for the lane's 8 columns: j0 + 4*lane + 128*k + e, k = 0..1, e = 0..3
-  __device__ __forceinline__ void kappa(const RowCtx& r, const Col*, float2 (&kp)[4]) const {
-    const float4 c0 = __ldcs(r.p);
-    const float4 c1 = __ldcs(r.p + 32);
+  // t' = B_j - g2 * C for the lane's 16 columns (the row potential is
+  // added back in fp64 by the reduce kernels)
+  __device__ __forceinline__ void expo(const RowCtx& r, const Col*, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
     const float2 g = make_float2(-g2, -g2);
-    kp[0] = __fmul2_rn(g, make_float2(c0.x, c0.y));
-    kp[1] = __fmul2_rn(g, make_float2(c0.z, c0.w));
-    kp[2] = __fmul2_rn(g, make_float2(c1.x, c1.y));
-    kp[3] = __fmul2_rn(g, make_float2(c1.z, c1.w));
-  }
-};
-
-struct SrcPointsF32 {
-  const float4* X;  // n x (x, y, z, 0)
-  const float4* Y;
-  float g2s;        // log2(e) * cost_scale / gamma
-  struct Col { float2 x, y, z; };  // 2 columns per Col, NEGATED coordinates
-  struct RowCtx { float2 x, y, z; };
-  __device__ __forceinline__ void load_cols(int64_t j_first, Col* c) const {}
-  __device__ __forceinline__ RowCtx row(int64_t i, int64_t, int) const {
-    const float4 p = X[i];
-    return RowCtx{make_float2(p.x, p.x), make_float2(p.y, p.y), make_float2(p.z, p.z)};
-  }
-  // returns -kappa = -g2s |x_i - y_j|^2
-  __device__ __forceinline__ void kappa(const RowCtx& r, const Col* c, float2 (&kp)[4]) const {
-    const float2 g = make_float2(-g2s, -g2s);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 dx = __fadd2_rn(r.x, c[q].x);
-      const float2 dy = __fadd2_rn(r.y, c[q].y);
-      const float2 dz = __fadd2_rn(r.z, c[q].z);
-      float2 d2 = __fmul2_rn(dx, dx);
-      d2 = __ffma2_rn(dy, dy, d2);
-      d2 = __ffma2_rn(dz, dz, d2);
-      kp[q] = __fmul2_rn(g, d2);
+    for (int k = 0; k < 4; ++k) {
+      const float4 c = __ldcs(r.p + 32 * k);
+      t[2 * k] = __ffma2_rn(g, make_float2(c.x, c.y), B[2 * k]);
+      t[2 * k + 1] = __ffma2_rn(g, make_float2(c.z, c.w), B[2 * k + 1]);
     }
   }
 };
 
-// Lane column map for fp32 sweeps: j = j0 + 4*lane + 128*k + e (k < 2, e < 4),
-// stored as 4 float2 pairs q = 2k + e/2.
-__device__ __forceinline__ int64_t f32_col(int64_t j0, int lane, int q, int h) {
-  return j0 + 4 * lane + 128 * (q >> 1) + 2 * (q & 1) + h;
+struct SrcPointsF32 {
+  const float4* Xs;  // pre-scaled coordinates (x, y, z, 0)
+  const float4* Ys;
+  struct Col { float2 x, y, z; };  // 2 columns per pair
+  struct RowCtx { float2 x, y, z; };  // NEGATED row coordinates
+  static constexpr bool kHasCols = true;
+  __device__ __forceinline__ RowCtx row(int64_t i, int64_t, int) const {
+    const float4 p = Xs[i];
+    return RowCtx{make_float2(-p.x, -p.x), make_float2(-p.y, -p.y), make_float2(-p.z, -p.z)};
+  }
+  // t' = B_j - |x'_i - y'_j|^2 as an FFMA2 chain on d = y' - x'
+  __device__ __forceinline__ void expo(const RowCtx& r, const Col* c, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const float2 dx = __fadd2_rn(r.x, c[q].x);
+      const float2 dy = __fadd2_rn(r.y, c[q].y);
+      const float2 dz = __fadd2_rn(r.z, c[q].z);
+      float2 tt = __ffma2_rn(make_float2(-dx.x, -dx.y), dx, B[q]);
+      tt = __ffma2_rn(make_float2(-dy.x, -dy.y), dy, tt);
+      t[q] = __ffma2_rn(make_float2(-dz.x, -dz.y), dz, tt);
+    }
+  }
+};
+
+// Partial formats understood by the reduce kernels: fp64 values, or fp32
+// (sum, log2 scale) pairs whose scale is relative to a per-row fp64 offset
+// (rows: A_i = (u_i + lu_i + w) log2 e; columns: 0).
+enum PartialFormat { PF_F64 = 0, PF_F32_SCALED = 1 };
+
+__device__ __forceinline__ double partial_value(const double* p, int64_t idx, int fmt, double log2_offset = 0.0) {
+  if (fmt == PF_F64) return p[idx];
+  const float2 f = reinterpret_cast<const float2*>(p)[idx];
+  return f.x == 0.f ? 0.0 : double(f.x) * exp2(double(f.y) + log2_offset);
 }
 
 template <class Src>
@@ -184,11 +198,21 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
-  const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
-  float2 Bj[4];
-  typename Src::Col cols[4];
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
+  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  // row potentials of this CTA's rows, once, into shared memory
+  extern __shared__ float s_A[];
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    s_A[i - r0] = float((ud + w) * kLog2e);
+  }
+  float2 Bj[kPairs];  // v_j log2 e (+ lv_j)
+  typename Src::Col cols[kPairs];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < kPairs; ++q) {
     float b[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -203,66 +227,61 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
     }
     Bj[q] = make_float2(b[0], b[1]);
   }
-  if constexpr (sizeof(typename Src::Col) > 1) {
+  if constexpr (Src::kHasCols) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kPairs; ++q) {
       float4 y0 = make_float4(0, 0, 0, 0), y1 = make_float4(0, 0, 0, 0);
       const int64_t ja = f32_col(j0, lane, q, 0), jb = f32_col(j0, lane, q, 1);
-      if (ja < n) y0 = src.Y[ja];
-      if (jb < n) y1 = src.Y[jb];
-      cols[q].x = make_float2(-y0.x, -y1.x);
-      cols[q].y = make_float2(-y0.y, -y1.y);
-      cols[q].z = make_float2(-y0.z, -y1.z);
+      if (ja < n) y0 = src.Ys[ja];
+      if (jb < n) y1 = src.Ys[jb];
+      cols[q].x = make_float2(y0.x, y1.x);
+      cols[q].y = make_float2(y0.y, y1.y);
+      cols[q].z = make_float2(y0.z, y1.z);
     }
   }
-  const double w = *a.w;
-  float2 cacc[4];
+  __syncthreads();
+  float2 cacc[kPairs];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) cacc[q] = make_float2(0.f, 0.f);
+  for (int q = 0; q < kPairs; ++q) cacc[q] = make_float2(0.f, 0.f);
   float sigma = -INFINITY;  // running column scale (log2) of this warp
   float mmax = -INFINITY;
-  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
-  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  float2* rowp = reinterpret_cast<float2*>(a.rowp) + int64_t(blockIdx.x) * n;
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
-    double ud = a.u[i];
-    if (a.lu) ud = ud + a.lu[i];
-    const float Ai = float((ud + w) * kLog2e);
+    const float Ai = s_A[i - r0];
     const auto rc = src.row(i, j0, lane);
-    float2 kp[4];
-    src.kappa(rc, cols, kp);
-    const float2 A2 = make_float2(Ai, Ai);
-    float2 t[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) t[q] = __fadd2_rn(__fadd2_rn(A2, Bj[q]), kp[q]);
+    float2 t[kPairs];
+    src.expo(rc, cols, Bj, t);  // t' = t - A_i
     float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
+    m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[4].x, t[4].y), fmaxf(t[5].x, t[5].y)), fmaxf(fmaxf(t[6].x, t[6].y), fmaxf(t[7].x, t[7].y))));
     m = warp_maxf(m);
-    // m == -inf only if the whole row segment is padding/-inf potentials.
+    // m == -inf only if the whole row segment is padding / -inf potentials
     const float ms = (m == -INFINITY) ? 0.f : m;
     const float2 M2 = make_float2(-ms, -ms);
     float2 rs = make_float2(0.f, 0.f);
-    float2 p[4];
+    float2 p[kPairs];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kPairs; ++q) {
       const float2 d = __fadd2_rn(t[q], M2);
       p[q] = make_float2(ex2f(d.x), ex2f(d.y));
       rs = __fadd2_rn(rs, p[q]);
     }
-    float r = warp_sum(rs.x + rs.y);
-    if (lane == 0) a.rowp[int64_t(blockIdx.x) * n + i] = double(r) * exp2(double(ms));
-    if (m > sigma) {
-      const float sc = ex2f(sigma - m);
+    const float r = warp_sum(rs.x + rs.y);
+    if (lane == 0) rowp[i] = make_float2(r, ms);  // value = r 2^(ms + A_i), A_i added in fp64
+    const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;  // row max of t (log2)
+    if (mA > sigma) {  // warp-uniform
+      const float sc = ex2f(sigma - mA);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
-      sigma = m;
+      for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = mA;
     }
-    mmax = fmaxf(mmax, m);
-    const float f = (m == -INFINITY) ? 0.f : ex2f(m - sigma);
+    mmax = fmaxf(mmax, mA);
+    const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
     const float2 F2 = make_float2(f, f);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+    for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
   }
-  // CTA combine of the 8 warps' column accumulators (each with its sigma).
-  __shared__ float cs[kWarps][kStripCols];
+  // CTA combine of the 8 warps' column accumulators (each with its sigma)
+  __shared__ float cs[kWarps][kStripCols32];
   __shared__ float ss[kWarps];
   __shared__ float mm[kWarps];
   if (lane == 0) {
@@ -274,18 +293,20 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
   const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < kPairs; ++q) {
     const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
     cs[warp][c] = cacc[q].x * fw;
     cs[warp][c + 1] = cacc[q].y * fw;
   }
   __syncthreads();
-  const int tt = threadIdx.x;
-  double s = 0.0;
+  float2* colp = reinterpret_cast<float2*>(a.colp) + int64_t(blockIdx.y) * n;
+  for (int c = threadIdx.x; c < kStripCols32; c += kThreads) {
+    float s = 0.f;
 #pragma unroll
-  for (int ww = 0; ww < kWarps; ++ww) s += double(cs[ww][tt]);
-  if (j0 + tt < n) a.colp[int64_t(blockIdx.y) * n + j0 + tt] = (sig == -INFINITY) ? 0.0 : s * exp2(double(sig));
-  if (tt == 0) {
+    for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
+    if (j0 + c < n) colp[j0 + c] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+  }
+  if (threadIdx.x == 0) {
     float m = mm[0];
     for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
     a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
@@ -306,8 +327,8 @@ inline int64_t gcd64(int64_t a, int64_t b) {
   return a;
 }
 
-inline SweepGrid choose_grid(int64_t n, int num_sms, int occupancy) {
-  const int64_t strips = ceil_div(n, kStripCols);
+inline SweepGrid choose_grid(int64_t n, int num_sms, int occupancy, int strip_cols) {
+  const int64_t strips = ceil_div(n, strip_cols);
   const int64_t cap = int64_t(num_sms) * occupancy;
   const int64_t base = cap / gcd64(cap, strips);  // row blocks per quantum
   const int64_t max_rb = std::max<int64_t>(1, n / 8);
