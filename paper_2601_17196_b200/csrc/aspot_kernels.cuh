@@ -299,7 +299,6 @@ __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double e
     r.elapsed_s = double(globaltimer_ns() - ctl->t0_ns) * 1e-9;
   }
   ctl->trace_len += 1;
-  ctl->g_record = ctl->record_rounded_cost;
 }
 
 __device__ void begin_iteration(AspotCtl* ctl) {

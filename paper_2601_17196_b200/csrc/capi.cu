@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include "engine.cuh"
+#include "plan.cuh"
 
 namespace potgpu {
 
@@ -368,11 +369,14 @@ struct AspotSession : Session {
   Setup st;
   cudaGraphExec_t exec = nullptr;
   int64_t trace_cap = 1, log_cap = 0;
+  static constexpr int64_t kKernelsPerAttempt = 18;
+  int64_t graph_nodes = kKernelsPerAttempt;
   explicit AspotSession(Context& c) : Session(c) {}
   ~AspotSession() override {
     if (exec) cudaGraphExecDestroy(exec);
   }
 
+  // One step attempt of the halving loop (solvers.hpp:334-352) + commit.
   void enqueue_attempt() {
     AspotCtl* ctl = ws.ctl.p;
     const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
@@ -399,13 +403,33 @@ struct AspotSession : Session {
     k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
                                                      ws.col(R_NEW));
     k_commit_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p, ws.iterlog.p);
-    enqueue_rounding(cx, P, ws, ZC, R_CHECK, &ctl->g_record, true, gamma, true, nullptr, false);
     PG_CK(cudaGetLastError());
   }
 
   void sync_ctl() {
     PG_CK(cudaMemcpyAsync(ws.host_ctl, ws.ctl.p, sizeof(AspotCtl), cudaMemcpyDeviceToHost, cx.stream));
     PG_CK(cudaStreamSynchronize(cx.stream));
+  }
+
+  // round_pot(b_matrix(ctx, z_check), in) (solvers.hpp:315, :371)
+  PlanResult round_now(double* Xdev) {
+    const int64_t n = P.n;
+    PlanEngine pe(cx, P, ws, gamma);
+    HVec row0(static_cast<size_t>(n)), ones(static_cast<size_t>(n), 1.0);
+    PG_CK(cudaMemcpy(row0.data(), ws.row(R_CHECK), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+    return round_pot_implicit(pe, ws.slot(S_ZC), ones, ones, row0, nullptr, nullptr, P.r, P.c, P.s, Xdev);
+  }
+
+  // The record appended at the current t gets its rounded cost (solvers.hpp:314-315).
+  void fill_last_record_cost(double cost) {
+    const AspotCtl& h = *ws.host_ctl;
+    const int64_t k = std::min(h.trace_len, h.trace_cap) - 1;
+    if (k < 0) return;
+    TraceDev last;
+    PG_CK(cudaMemcpy(&last, ws.trace.p + k, sizeof(TraceDev), cudaMemcpyDeviceToHost));
+    if (last.t != h.t || !std::isnan(last.rounded_cost)) return;
+    last.rounded_cost = cost;
+    PG_CK(cudaMemcpy(ws.trace.p + k, &last, sizeof(TraceDev), cudaMemcpyHostToDevice));
   }
 
   void begin() override {
@@ -423,8 +447,6 @@ struct AspotSession : Session {
     prepare_workspace(cx, P, ws, trace_cap, log_cap);
     PG_CK(cudaMemcpyAsync(ws.rt.p, st.mr.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     PG_CK(cudaMemcpyAsync(ws.ct.p, st.mc.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
-    PG_CK(cudaMemcpyAsync(ws.ro_r.p, P.r.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
-    PG_CK(cudaMemcpyAsync(ws.ro_c.p, P.c.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     ws.slots.zero(cx.stream);
     AspotCtl& h = *ws.host_ctl;
     std::memset(&h, 0, sizeof(AspotCtl));
@@ -433,7 +455,6 @@ struct AspotSession : Session {
     h.pause_at = INT64_MAX;
     h.log_every = cfg.log_every;
     h.block_rule = cfg.block_rule;
-    h.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
     h.trace_cap = trace_cap;
     h.log_cap = log_cap;
     h.theta = 1.0;
@@ -451,9 +472,9 @@ struct AspotSession : Session {
     launch_reduce(cx, ws, ZC, R_CHECK, nullptr);
     launch_scalars(cx, ws, R_CHECK, ZC, nullptr);
     k_init_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p);
-    enqueue_rounding(cx, P, ws, ZC, R_CHECK, &ctl->g_record, true, gamma, true, nullptr, false);
     sync_ctl();
     if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
+    if (cfg.record_rounded_cost && h.g_active) fill_last_record_cost(round_now(nullptr).cost);
     if (cfg.use_graphs) {
       cudaGraph_t graph;
       PG_CK(cudaStreamBeginCapture(cx.stream, cudaStreamCaptureModeThreadLocal));
@@ -464,13 +485,8 @@ struct AspotSession : Session {
       graph_nodes = int64_t(nodes);
       PG_CK(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
-    } else {
-      graph_nodes = kKernelsPerAttempt;
     }
   }
-
-  static constexpr int64_t kKernelsPerAttempt = 27;
-  int64_t graph_nodes = kKernelsPerAttempt;
 
   void launch_attempts(int64_t k) {
     for (int64_t i = 0; i < k; ++i) {
@@ -480,32 +496,45 @@ struct AspotSession : Session {
     }
   }
 
-  // Runs until k more iterations are accepted, the solve stops, or forever
-  // when k < 0. Device time of the loop between events -> *ms.
+  // Device loop until it pauses at `stop` or the solve stops.
+  void run_until(int64_t stop) {
+    AspotCtl& h = *ws.host_ctl;
+    k_resume<<<1, 1, 0, cx.stream>>>(ws.ctl.p, stop);
+    launches += 1;
+    // first burst: exactly the iterations asked for (1 attempt each unless a
+    // step is halved), then poll every sync_every attempts
+    int64_t burst = stop == INT64_MAX ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, stop - h.t);
+    burst = std::min<int64_t>(burst, 1 << 16);
+    while (true) {
+      launch_attempts(burst);
+      sync_ctl();
+      if (!h.g_active || h.fatal) break;
+      burst = std::max(1, cfg.sync_every);
+      if (stop != INT64_MAX) burst = std::max<int64_t>(1, std::min<int64_t>(burst, stop - h.t));
+    }
+  }
+
   void iterate(int64_t k, double* ms, int64_t* iters, int* finished) override {
     AspotCtl& h = *ws.host_ctl;
     if (trivial || (!h.g_active && !h.paused)) {
       if (ms) *ms = 0.0;
-      if (iters) *iters = trivial ? 0 : h.t;
+      if (iters) *iters = 0;
       if (finished) *finished = 1;
       return;
     }
     const int64_t t0 = h.t;
     const int64_t target = k < 0 ? INT64_MAX : t0 + k;
     PG_CK(cudaEventRecord(ev0, cx.stream));
-    k_resume<<<1, 1, 0, cx.stream>>>(ws.ctl.p, target);
-    launches += 1;
-    // first burst: exactly the iterations asked for (1 attempt each unless a
-    // step is halved), then poll every sync_every attempts
-    int64_t burst = k < 0 ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, k);
     while (true) {
-      launch_attempts(burst);
-      PG_CK(cudaEventRecord(ev1, cx.stream));
-      sync_ctl();
-      if (!h.g_active || h.fatal) break;
-      burst = std::max(1, cfg.sync_every);
-      if (k >= 0) burst = std::max<int64_t>(1, std::min<int64_t>(burst, target - h.t));
+      int64_t stop = target;
+      if (cfg.record_rounded_cost) stop = std::min(stop, (h.t / cfg.log_every + 1) * cfg.log_every);
+      run_until(stop);
+      if (h.fatal) break;
+      if (cfg.record_rounded_cost && h.paused) fill_last_record_cost(round_now(nullptr).cost);
+      if (!h.paused || h.t >= target) break;
     }
+    PG_CK(cudaEventRecord(ev1, cx.stream));
+    PG_CK(cudaEventSynchronize(ev1));
     float f = 0.f;
     PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
     if (ms) *ms = double(f);
@@ -553,9 +582,8 @@ struct AspotSession : Session {
     DevBuf<double> Xd;
     const bool mat = cfg.materialize_plan && out && out->X;
     if (mat) Xd.alloc(size_t(n * n));
-    enqueue_rounding(cx, P, ws, ZC, R_CHECK, nullptr, false, gamma, true, mat ? Xd.p : nullptr, true);
+    const PlanResult pr = round_now(mat ? Xd.p : nullptr);
     sync_ctl();
-    if (h.fatal) throw Error(h.fatal, "Infeasible: deficit fill has no slack mass");
     const double wall = secs(t_start);
     sm->status = h.status;
     sm->iterations = h.t;
@@ -564,14 +592,15 @@ struct AspotSession : Session {
     sm->final_error = h.error;
     sm->wall_seconds = wall;
     sm->loop_seconds = h.loop_end_ns > h.t0_ns ? double(h.loop_end_ns - h.t0_ns) * 1e-9 : 0.0;
-    sm->cost = h.ro.cost;
-    sm->feasibility_gap = h.ro.gap;
-    sm->mass = h.ro.mass;
+    sm->cost = pr.cost;
+    sm->feasibility_gap = pr.gap;
+    sm->mass = pr.mass;
     sm->phi = h.phi_check;
     sm->iter_log_len = h.log_len;
     sm->sweeps = h.sweeps;
     sm->attempts = h.attempts;
     std::strncpy(sm->stopping_iterate, "z_check", sizeof(sm->stopping_iterate));
+    if (cfg.record_rounded_cost) fill_last_record_cost(pr.cost);  // record at the stopping t
     copy_trace_and_log(ws, h, out);
     int64_t tl = std::min<int64_t>(h.trace_len, h.trace_cap);
     int64_t last_t = -1;
@@ -582,13 +611,13 @@ struct AspotSession : Session {
     }
     // final record if the last one is not at t (solvers.hpp:375-383)
     if (h.trace_len == 0 || last_t != h.t) {
-      if (out && out->trace && tl < out->trace_cap) out->trace[tl] = potgpu_trace_record{h.t, h.error, h.phi_check, h.ro.cost, wall};
+      if (out && out->trace && tl < out->trace_cap) out->trace[tl] = potgpu_trace_record{h.t, h.error, h.phi_check, pr.cost, wall};
       tl += 1;
     }
     sm->trace_len = tl;
     if (out) {
-      if (out->row_slack) PG_CK(cudaMemcpy(out->row_slack, ws.rv(8), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
-      if (out->col_slack) PG_CK(cudaMemcpy(out->col_slack, ws.rv(9), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->row_slack) std::memcpy(out->row_slack, pr.row_slack.data(), size_t(n) * sizeof(double));
+      if (out->col_slack) std::memcpy(out->col_slack, pr.col_slack.data(), size_t(n) * sizeof(double));
       if (out->u) PG_CK(cudaMemcpy(out->u, ZC.u(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
       if (out->v) PG_CK(cudaMemcpy(out->v, ZC.v(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
       if (out->w) PG_CK(cudaMemcpy(out->w, ZC.w(), sizeof(double), cudaMemcpyDeviceToHost));

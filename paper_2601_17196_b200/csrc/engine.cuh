@@ -108,8 +108,8 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.slot_stride = round_up(2 * n + 1, 32);
   ws.slots.alloc(size_t(kSlots * ws.slot_stride));
   ws.sums.alloc(size_t(2 * kRoles * n));
-  ws.rowp.alloc(size_t(ws.nstrips * n));
-  ws.colp.alloc(size_t(ws.nrb * n));
+  ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
+  ws.colp.alloc(size_t(2 * ws.nrb * n));
   ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
   ws.scratch.alloc(8192);
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n))));
@@ -167,49 +167,6 @@ inline void launch_reduce(Context& cx, Workspace& ws, Slot z, int sum_slot, cons
 
 inline void launch_scalars(Context& cx, Workspace& ws, int role, Slot z, const int* gate) {
   k_point_scalars<<<1, 32, 0, cx.stream>>>(ws.ctl.p, role, ws.scratch.p, ws.nblk, z, gate);
-  PG_CK(cudaGetLastError());
-}
-
-// The implicit round_pot pipeline on point z with B sums at sum slot `ss`.
-inline void enqueue_rounding(Context& cx, const DevProblem& P, Workspace& ws, Slot z, int ss, const int* gate,
-                             bool is_record, double gamma, bool floor_exp, double* Xdev, bool want_slacks) {
-  const int64_t n = P.n;
-  RoundArgs ra;
-  ra.n = n; ra.z = z; ra.rowb = ws.row(ss);
-  ra.r = ws.ro_r.p; ra.c = ws.ro_c.p; ra.s = P.s;
-  ra.rho = ws.rv(0); ra.kappa = ws.rv(1); ra.lu = ws.rv(2); ra.lv = ws.rv(3);
-  ra.rowx = ws.rv(4); ra.colx = ws.rv(5); ra.a = ws.rv(6); ra.b = ws.rv(7);
-  ra.row_slack = want_slacks ? ws.rv(8) : nullptr;
-  ra.col_slack = want_slacks ? ws.rv(9) : nullptr;
-  ra.scratch = ws.scratch.p;
-  ra.gate = gate;
-  ra.total_ptr = &ws.ctl.p->ps[ss].total;  // sum slots are indexed by PointRole
-  AspotCtl* ctl = ws.ctl.p;
-  k_round_a<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl, ra);
-  launch_sweep(cx, P, ws, z, ra.lu, nullptr, gate, false, gamma);
-  k_round_b<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.colp.p, ws.nrb, ws.pfmt);
-  launch_sweep(cx, P, ws, z, ra.lu, ra.lv, gate, false, gamma);
-  k_round_c<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ra, ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.pfmt);
-  k_round_d<<<1, 32, 0, cx.stream>>>(ctl, ra, ws.nblk);
-  k_round_e<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl, ra);
-  const int rows = cost_sweep_rows(n);
-  dim3 cg(unsigned(ceil_div(n, kThreads)), unsigned(ceil_div(n, rows)));
-  const int64_t npart = int64_t(cg.x) * cg.y;
-  const bool mat = Xdev != nullptr;
-  if (P.dtype == POTGPU_F64) {
-    ElemDenseF64 el{P.L64.p, P.ld, gamma};
-    if (mat) k_cost_sweep<ElemDenseF64, true><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-    else k_cost_sweep<ElemDenseF64, false><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-  } else if (P.kind == POTGPU_COST_DENSE) {
-    ElemDenseF32 el{P.C32.p, P.ld, gamma};
-    if (mat) k_cost_sweep<ElemDenseF32, true><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-    else k_cost_sweep<ElemDenseF32, false><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-  } else {
-    ElemPointsF32 el{P.X4.p, P.Y4.p, P.cost_scale, gamma};
-    if (mat) k_cost_sweep<ElemPointsF32, true><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-    else k_cost_sweep<ElemPointsF32, false><<<cg, kThreads, 0, cx.stream>>>(ctl, el, ra, rows, ws.partial.p, Xdev, floor_exp);
-  }
-  k_round_f<<<1, 32, 0, cx.stream>>>(ctl, ra, ws.partial.p, npart, ws.nblk, ws.trace.p, is_record ? 1 : 0);
   PG_CK(cudaGetLastError());
 }
 

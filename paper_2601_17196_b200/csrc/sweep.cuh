@@ -140,20 +140,23 @@ struct SrcDenseF32 {
   int64_t ld;
   float g2;  // log2(e) / gamma
   struct Col {};
-  struct RowCtx { const float4* p; };
+  struct RowData { float4 c[4]; };  // the lane's 16 entries of one row
   static constexpr bool kHasCols = false;
-  __device__ __forceinline__ RowCtx row(int64_t i, int64_t j0, int lane) const {
-    return RowCtx{reinterpret_cast<const float4*>(C + i * ld + j0) + lane};
+  __device__ __forceinline__ RowData load(int64_t i, int64_t j0, int lane) const {
+    const float4* p = reinterpret_cast<const float4*>(C + i * ld + j0) + lane;
+    RowData d;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d.c[k] = __ldcs(p + 32 * k);
+    return d;
   }
   // t' = B_j - g2 * C for the lane's 16 columns (the row potential is
   // added back in fp64 by the reduce kernels)
-  __device__ __forceinline__ void expo(const RowCtx& r, const Col*, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
+  __device__ __forceinline__ void expo(const RowData& d, const Col*, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
     const float2 g = make_float2(-g2, -g2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float4 c = __ldcs(r.p + 32 * k);
-      t[2 * k] = __ffma2_rn(g, make_float2(c.x, c.y), B[2 * k]);
-      t[2 * k + 1] = __ffma2_rn(g, make_float2(c.z, c.w), B[2 * k + 1]);
+      t[2 * k] = __ffma2_rn(g, make_float2(d.c[k].x, d.c[k].y), B[2 * k]);
+      t[2 * k + 1] = __ffma2_rn(g, make_float2(d.c[k].z, d.c[k].w), B[2 * k + 1]);
     }
   }
 };
@@ -162,19 +165,17 @@ struct SrcPointsF32 {
   const float4* Xs;  // pre-scaled coordinates (x, y, z, 0)
   const float4* Ys;
   struct Col { float2 x, y, z; };  // 2 columns per pair
-  struct RowCtx { float2 x, y, z; };  // NEGATED row coordinates
+  struct RowData { float4 p; };
   static constexpr bool kHasCols = true;
-  __device__ __forceinline__ RowCtx row(int64_t i, int64_t, int) const {
-    const float4 p = Xs[i];
-    return RowCtx{make_float2(-p.x, -p.x), make_float2(-p.y, -p.y), make_float2(-p.z, -p.z)};
-  }
+  __device__ __forceinline__ RowData load(int64_t i, int64_t, int) const { return RowData{Xs[i]}; }
   // t' = B_j - |x'_i - y'_j|^2 as an FFMA2 chain on d = y' - x'
-  __device__ __forceinline__ void expo(const RowCtx& r, const Col* c, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
+  __device__ __forceinline__ void expo(const RowData& d, const Col* c, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
+    const float2 rx = make_float2(-d.p.x, -d.p.x), ry = make_float2(-d.p.y, -d.p.y), rz = make_float2(-d.p.z, -d.p.z);
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) {
-      const float2 dx = __fadd2_rn(r.x, c[q].x);
-      const float2 dy = __fadd2_rn(r.y, c[q].y);
-      const float2 dz = __fadd2_rn(r.z, c[q].z);
+      const float2 dx = __fadd2_rn(rx, c[q].x);
+      const float2 dy = __fadd2_rn(ry, c[q].y);
+      const float2 dz = __fadd2_rn(rz, c[q].z);
       float2 tt = __ffma2_rn(make_float2(-dx.x, -dx.y), dx, B[q]);
       tt = __ffma2_rn(make_float2(-dy.x, -dy.y), dy, tt);
       t[q] = __ffma2_rn(make_float2(-dz.x, -dz.y), dz, tt);
@@ -246,11 +247,16 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   float sigma = -INFINITY;  // running column scale (log2) of this warp
   float mmax = -INFINITY;
   float2* rowp = reinterpret_cast<float2*>(a.rowp) + int64_t(blockIdx.x) * n;
+  // one-row-ahead software pipeline: the next row's data is in flight while
+  // this row is exponentiated
+  typename Src::RowData nxt{};
+  if (r0 + warp < r1) nxt = src.load(r0 + warp, j0, lane);
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    const typename Src::RowData cur = nxt;
+    if (i + kWarps < r1) nxt = src.load(i + kWarps, j0, lane);
     const float Ai = s_A[i - r0];
-    const auto rc = src.row(i, j0, lane);
     float2 t[kPairs];
-    src.expo(rc, cols, Bj, t);  // t' = t - A_i
+    src.expo(cur, cols, Bj, t);  // t' = t - A_i
     float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
     m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[4].x, t[4].y), fmaxf(t[5].x, t[5].y)), fmaxf(fmaxf(t[6].x, t[6].y), fmaxf(t[7].x, t[7].y))));
     m = warp_maxf(m);
