@@ -78,7 +78,7 @@ __global__ void k_zbar(AspotCtl* ctl, Slot zc, Slot z, Slot zb) {
 
 // Per-point reduction of the sweep partials into B 1, B^T 1 and the scalar
 // partials of every functional the reference evaluates at that point.
-// Partials per block (fixed grid, fixed order) -> k_point_scalars.
+// One launch per point (k_point_eval).
 struct ReduceArgs {
   Slot z;
   const double* rowp; int64_t nstrips;
@@ -91,75 +91,7 @@ struct ReduceArgs {
   int pfmt;                             // PartialFormat of rowp/colp
 };
 
-__global__ void __launch_bounds__(kVecThreads) k_point_reduce(ReduceArgs a) {
-  if (a.gate && *a.gate == 0) return;
-  const int64_t n = a.z.n;
-  double acc[kNumPartials + 1];
-  // 0 total, 1 maxu, 2 maxv, 3 seu, 4 sev, 5 ur, 6 vc, 7 score_u, 8 score_v, 9 gl1u, 10 gl1v, 11 maxe
-#pragma unroll
-  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = 0.0;
-  acc[1] = acc[2] = acc[11] = -INFINITY;
-  const double* u = a.z.u();
-  const double* v = a.z.v();
-  const double w = *a.z.w();
-  for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const double a2 = (u[i] + w) * kLog2e;  // row offset of fp32 row partials
-    double rb = 0.0;
-    for (int64_t s = 0; s < a.nstrips; ++s) rb += partial_value(a.rowp, s * n + i, a.pfmt, a2);
-    double cb = 0.0;
-    for (int64_t s = 0; s < a.nrowblocks; ++s) cb += partial_value(a.colp, s * n + i, a.pfmt);
-    a.row_out[i] = rb;
-    a.col_out[i] = cb;
-    const double ui = u[i], vi = v[i];
-    const double eu = eexp(ui), ev = eexp(vi);
-    acc[0] += rb;
-    acc[1] = nan_max(acc[1], ui);
-    acc[2] = nan_max(acc[2], vi);
-    acc[3] += eu;
-    acc[4] += ev;
-    acc[5] += ui * a.rt[i];
-    acc[6] += vi * a.ct[i];
-    const double rowf = rb + eu, colf = cb + ev;
-    acc[7] += rho_limit(a.rt[i], rowf);
-    acc[8] += rho_limit(a.ct[i], colf);
-    acc[9] += fabs(rowf - a.rt[i]);
-    acc[10] += fabs(colf - a.ct[i]);
-  }
-  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
-    acc[11] = nan_max(acc[11], a.maxp[k]);
-  // fixed-order block reduction through shared memory
-  __shared__ double sh[kNumPartials + 1][kVecThreads];
-#pragma unroll
-  for (int k = 0; k < kNumPartials + 1; ++k) sh[k][threadIdx.x] = acc[k];
-  __syncthreads();
-  for (int stride = kVecThreads / 2; stride > 0; stride >>= 1) {
-    if (threadIdx.x < stride) {
-#pragma unroll
-      for (int k = 0; k < kNumPartials + 1; ++k) {
-        const double o = sh[k][threadIdx.x + stride];
-        if (k == 1 || k == 2 || k == 11) sh[k][threadIdx.x] = nan_max(sh[k][threadIdx.x], o);
-        else sh[k][threadIdx.x] += o;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < kNumPartials + 1) a.scratch[blockIdx.x * (kNumPartials + 1) + threadIdx.x] = sh[threadIdx.x][0];
-}
-
-__device__ void reduce_scratch(const double* scratch, int nblk, PointScalars& ps) {
-  double acc[kNumPartials + 1];
-  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = (k == 1 || k == 2 || k == 11) ? -INFINITY : 0.0;
-  for (int b = 0; b < nblk; ++b) {
-    for (int k = 0; k < kNumPartials + 1; ++k) {
-      const double x = scratch[b * (kNumPartials + 1) + k];
-      if (k == 1 || k == 2 || k == 11) acc[k] = nan_max(acc[k], x);
-      else acc[k] += x;
-    }
-  }
-  ps.total = acc[0]; ps.maxu = acc[1]; ps.maxv = acc[2]; ps.seu = acc[3]; ps.sev = acc[4];
-  ps.ur = acc[5]; ps.vc = acc[6]; ps.score_u = acc[7]; ps.score_v = acc[8]; ps.gl1u = acc[9]; ps.gl1v = acc[10];
-  ps.maxe = acc[11];
-}
+__device__ __forceinline__ bool is_max_slot(int k) { return k == 1 || k == 2 || k == 11; }
 
 __device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) {  // solvers.hpp:58-68
   const double su = ps.score_u, sv = ps.score_v, sw = rho_limit(s, ps.total);
@@ -171,16 +103,16 @@ __device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) { 
 }
 
 // Scalar finalisation + the decision the reference takes at that point.
-__global__ void k_point_scalars(AspotCtl* ctl, int role, const double* scratch, int nblk, Slot z, const int* gate) {
-  if (gate && *gate == 0) return;
-  if (threadIdx.x != 0) return;
+__device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPartials + 1], double w) {
   PointScalars ps;
-  reduce_scratch(scratch, nblk, ps);
-  const double w = *z.w();
+  ps.total = acc[0]; ps.maxu = acc[1]; ps.maxv = acc[2]; ps.seu = acc[3]; ps.sev = acc[4];
+  ps.ur = acc[5]; ps.vc = acc[6]; ps.score_u = acc[7]; ps.score_v = acc[8]; ps.gl1u = acc[9]; ps.gl1v = acc[10];
+  ps.maxe = acc[11];
   // phi (dual.hpp:117-118): B.sum() + eu.sum() + ev.sum() - u.r - v.c - w s
   ps.phi = ((((ps.total + ps.seu) + ps.sev) - ps.ur) - ps.vc) - w * ctl->s;
   ps.err = (ps.gl1u + ps.gl1v) + fabs(ps.total - ctl->s);  // dual.hpp:138-141
   ps.overflow = !(ps.maxe <= kMaxExponent) || !(ps.maxu <= kMaxExponent) || !(ps.maxv <= kMaxExponent) || (w != w);
+  ps.pad = 0;
   ctl->ps[role] = ps;
   ctl->sweeps += 1;
   switch (role) {
@@ -210,6 +142,97 @@ __global__ void k_point_scalars(AspotCtl* ctl, int role, const double* scratch, 
       break;
     default:
       break;
+  }
+}
+
+// One kernel per evaluated point: a warp per index i combines the sweep's
+// strip / row-block partials into (B 1)_i and (B^T 1)_i and forms the
+// per-element terms of every functional the reference evaluates there;
+// blocks reduce them to fixed-order partials, and the last block to finish
+// (atomic ticket) reduces all partials in a fixed order and takes the
+// decision (apply_role). Deterministic, one launch.
+constexpr int kEvalWarps = kVecThreads / 32;
+
+__global__ void __launch_bounds__(kVecThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
+  if (a.gate && *a.gate == 0) return;
+  const int64_t n = a.z.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[kNumPartials + 1];
+#pragma unroll
+  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = is_max_slot(k) ? -INFINITY : 0.0;
+  const double* u = a.z.u();
+  const double* v = a.z.v();
+  const double w = *a.z.w();
+  for (int64_t i = int64_t(blockIdx.x) * kEvalWarps + warp; i < n; i += int64_t(gridDim.x) * kEvalWarps) {
+    const double ui = u[i], vi = v[i];
+    const double a2 = (ui + w) * kLog2e;  // row offset of fp32 row partials
+    double rb = 0.0, cb = 0.0;
+    for (int64_t s = lane; s < a.nstrips; s += 32) rb += partial_value(a.rowp, s * n + i, a.pfmt, a2);
+    for (int64_t s = lane; s < a.nrowblocks; s += 32) cb += partial_value(a.colp, s * n + i, a.pfmt);
+    rb = warp_sum(rb);
+    cb = warp_sum(cb);
+    if (lane == 0) {
+      a.row_out[i] = rb;
+      a.col_out[i] = cb;
+      const double eu = eexp(ui), ev = eexp(vi);
+      acc[0] += rb;
+      acc[1] = nan_max(acc[1], ui);
+      acc[2] = nan_max(acc[2], vi);
+      acc[3] += eu;
+      acc[4] += ev;
+      acc[5] += ui * a.rt[i];
+      acc[6] += vi * a.ct[i];
+      const double rowf = rb + eu, colf = cb + ev;
+      acc[7] += rho_limit(a.rt[i], rowf);
+      acc[8] += rho_limit(a.ct[i], colf);
+      acc[9] += fabs(rowf - a.rt[i]);
+      acc[10] += fabs(colf - a.ct[i]);
+    }
+  }
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
+    acc[11] = nan_max(acc[11], a.maxp[k]);
+  __shared__ double sh[kNumPartials + 1][kVecThreads];
+  __shared__ bool last;
+  auto block_reduce = [&]() {
+#pragma unroll
+    for (int k = 0; k < kNumPartials + 1; ++k) sh[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int stride = kVecThreads / 2; stride > 0; stride >>= 1) {
+      if (threadIdx.x < stride) {
+#pragma unroll
+        for (int k = 0; k < kNumPartials + 1; ++k) {
+          const double o = sh[k][threadIdx.x + stride];
+          sh[k][threadIdx.x] = is_max_slot(k) ? nan_max(sh[k][threadIdx.x], o) : sh[k][threadIdx.x] + o;
+        }
+      }
+      __syncthreads();
+    }
+  };
+  block_reduce();
+  if (threadIdx.x < kNumPartials + 1) a.scratch[blockIdx.x * (kNumPartials + 1) + threadIdx.x] = sh[threadIdx.x][0];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const volatile double* sc = a.scratch;
+#pragma unroll
+  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = is_max_slot(k) ? -INFINITY : 0.0;
+  for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < kNumPartials + 1; ++k) {
+      const double x = sc[b * (kNumPartials + 1) + k];
+      acc[k] = is_max_slot(k) ? nan_max(acc[k], x) : acc[k] + x;
+    }
+  __syncthreads();
+  block_reduce();
+  if (threadIdx.x == 0) {
+    double tot[kNumPartials + 1];
+#pragma unroll
+    for (int k = 0; k < kNumPartials + 1; ++k) tot[k] = sh[k][0];
+    *ticket = 0u;  // ready for the next launch
+    apply_role(ctl, role, tot, w);
   }
 }
 

@@ -369,7 +369,7 @@ struct AspotSession : Session {
   Setup st;
   cudaGraphExec_t exec = nullptr;
   int64_t trace_cap = 1, log_cap = 0;
-  static constexpr int64_t kKernelsPerAttempt = 18;
+  static constexpr int64_t kKernelsPerAttempt = 14;
   int64_t graph_nodes = kKernelsPerAttempt;
   explicit AspotSession(Context& c) : Session(c) {}
   ~AspotSession() override {
@@ -384,22 +384,18 @@ struct AspotSession : Session {
     const int gv = ws.nblk;
     k_zbar<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZC, Z, ZB);
     launch_sweep(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma);
-    launch_reduce(cx, ws, ZB, R_BAR, &ctl->g_new);
-    launch_scalars(cx, ws, R_BAR, ZB, &ctl->g_new);
+    launch_eval(cx, ws, ZB, R_BAR, &ctl->g_new);
     k_zgrave<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
     launch_sweep(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_reduce(cx, ws, ZG, R_GRAVE, &ctl->g_alive);
-    launch_scalars(cx, ws, R_GRAVE, ZG, &ctl->g_alive);
+    launch_eval(cx, ws, ZG, R_GRAVE, &ctl->g_alive);
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
                                                    ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
     launch_sweep(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_reduce(cx, ws, ZH, R_HAT, &ctl->g_alive);
-    launch_scalars(cx, ws, R_HAT, ZH, &ctl->g_alive);
+    launch_eval(cx, ws, ZH, R_HAT, &ctl->g_alive);
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
                                                    ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
     launch_sweep(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_reduce(cx, ws, ZN, R_NEW, &ctl->g_alive);
-    launch_scalars(cx, ws, R_NEW, ZN, &ctl->g_alive);
+    launch_eval(cx, ws, ZN, R_NEW, &ctl->g_alive);
     k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
                                                      ws.col(R_NEW));
     k_commit_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p, ws.iterlog.p);
@@ -469,8 +465,7 @@ struct AspotSession : Session {
     // phi_and_gradient(z_check = 0) (solvers.hpp:305) and record(0) (:320)
     const Slot ZC = ws.slot(S_ZC);
     launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);
-    launch_reduce(cx, ws, ZC, R_CHECK, nullptr);
-    launch_scalars(cx, ws, R_CHECK, ZC, nullptr);
+    launch_eval(cx, ws, ZC, R_CHECK, nullptr);
     k_init_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p);
     sync_ctl();
     if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
@@ -819,8 +814,7 @@ int potgpu_dual_eval(potgpu_ctx* c, const potgpu_problem* pr, double gamma, cons
     h.s = P.s;
     PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(h), cudaMemcpyHostToDevice, c->cx.stream));
     launch_sweep(c->cx, P, ws, Z, nullptr, nullptr, nullptr, true, gamma);
-    launch_reduce(c->cx, ws, Z, R_EVAL, nullptr);
-    launch_scalars(c->cx, ws, R_EVAL, Z, nullptr);
+    launch_eval(c->cx, ws, Z, R_EVAL, nullptr);
     PG_CK(cudaMemcpyAsync(&h, ws.ctl.p, sizeof(h), cudaMemcpyDeviceToHost, c->cx.stream));
     if (row) PG_CK(cudaMemcpyAsync(row, ws.row(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
     if (col) PG_CK(cudaMemcpyAsync(col, ws.col(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));

@@ -57,6 +57,7 @@ struct Workspace {
   SweepGrid g{};
   int64_t nstrips = 0, nrb = 0;
   int nblk = 0;  // O(n) kernel grid
+  int eval_blocks = 0;  // k_point_eval grid (8 indices per block)
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
   int strip = 256;
   size_t sweep_smem = 0;
@@ -67,6 +68,7 @@ struct Workspace {
   DevBuf<double> ro_buf;    // rounding vectors: rho, kappa, lu, lv, rowx, colx, a, b, row_slack, col_slack
   DevBuf<double> ro_r, ro_c;  // original marginals for rounding
   DevBuf<AspotCtl> ctl;
+  DevBuf<unsigned> ticket;
   AspotCtl* host_ctl = nullptr;  // pinned mirror
   DevBuf<TraceDev> trace;
   DevBuf<IterLogDev> iterlog;
@@ -111,7 +113,10 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * ws.nrb * n));
   ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
-  ws.scratch.alloc(8192);
+  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n, kEvalWarps), 4096));
+  ws.scratch.alloc(size_t(std::max(8192, (kNumPartials + 1) * ws.eval_blocks)));
+  ws.ticket.alloc(1);
+  ws.ticket.zero(cx.stream);
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n))));
   ws.rt.alloc(size_t(n));
   ws.ct.alloc(size_t(n));
@@ -150,23 +155,19 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
   PG_CK(cudaGetLastError());
 }
 
-inline void launch_reduce(Context& cx, Workspace& ws, Slot z, int sum_slot, const int* gate) {
+// The per-point evaluation (partials -> B 1, B^T 1, scalars, decision).
+inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int* gate) {
   ReduceArgs r;
   r.z = z;
   r.rowp = ws.rowp.p; r.nstrips = ws.nstrips;
   r.colp = ws.colp.p; r.nrowblocks = ws.nrb;
   r.maxp = ws.maxp.p; r.nmax = ws.nstrips * ws.nrb;
-  r.row_out = ws.row(sum_slot); r.col_out = ws.col(sum_slot);
+  r.row_out = ws.row(role); r.col_out = ws.col(role);
   r.rt = ws.rt.p; r.ct = ws.ct.p;
   r.scratch = ws.scratch.p;
   r.gate = gate;
   r.pfmt = ws.pfmt;
-  k_point_reduce<<<ws.nblk, kVecThreads, 0, cx.stream>>>(r);
-  PG_CK(cudaGetLastError());
-}
-
-inline void launch_scalars(Context& cx, Workspace& ws, int role, Slot z, const int* gate) {
-  k_point_scalars<<<1, 32, 0, cx.stream>>>(ws.ctl.p, role, ws.scratch.p, ws.nblk, z, gate);
+  k_point_eval<<<ws.eval_blocks, kVecThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());
 }
 

@@ -43,6 +43,7 @@ struct SinkhornSession : Session {
     if (hctl) cudaFreeHost(hctl);
   }
 
+  int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n, kSkWarps), 2048)); }
   Slot zv_slot() const { return Slot{zv.p, P.n}; }
   Slot zf_slot() const { return Slot{zf.p, P.n}; }
 
@@ -60,7 +61,7 @@ struct SinkhornSession : Session {
       launch_sweep(cx, P, ws, zv_slot(), nullptr, nullptr, gate, false, gamma);  // rows of (0, v, 0)
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.v, 0, gate);
-    k_sk_rows<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.rowp.p, ws.nstrips,
+    k_sk_rows<<<sk_blocks(), kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.rowp.p, ws.nstrips,
                                                       P.dtype == POTGPU_F64 ? LP_F64 : LP_F32, gate);
   }
 
@@ -79,8 +80,8 @@ struct SinkhornSession : Session {
                                                                             reinterpret_cast<float2*>(ws.colp.p), gate);
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
-    k_sk_cols<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.colp.p, ws.nrb, P.dtype == POTGPU_F64 ? LP_F64 : LP_F32,
-                                                      update, ws.nblk, gate);
+    k_sk_cols<<<sk_blocks(), kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.colp.p, ws.nrb, P.dtype == POTGPU_F64 ? LP_F64 : LP_F32,
+                                                      update, sk_blocks(), gate);
   }
 
   // solvers.hpp:463-476: u update, v update, B, E, ++iterations, record
@@ -89,7 +90,7 @@ struct SinkhornSession : Session {
     k_sk_commit_u<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl.p, sv);
     col_lse(1, gate);
     row_lse(gate);
-    k_sk_scalars<<<1, 32, 0, cx.stream>>>(ctl.p, sv, ws.nblk, 0, ws.trace.p, gate);
+    k_sk_scalars<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv, sk_blocks(), 0, ws.trace.p, gate);
     PG_CK(cudaGetLastError());
   }
 
@@ -143,7 +144,7 @@ struct SinkhornSession : Session {
     build_logk(cx, P, gamma);
     prepare_workspace(cx, P, ws, trace_cap, 0);
     const size_t m = size_t(n + 1);
-    vec.alloc(7 * m + 8 * size_t(ws.nblk) + 64);
+    vec.alloc(7 * m + 8 * size_t(sk_blocks()) + 64);
     sv.u = vec.p; sv.u_next = vec.p + m; sv.v = vec.p + 2 * m; sv.log_r = vec.p + 3 * m; sv.log_c = vec.p + 4 * m;
     sv.r = vec.p + 5 * m; sv.c = vec.p + 6 * m; sv.scratch = vec.p + 7 * m;
     zv.alloc(size_t(ws.slot_stride));
@@ -174,7 +175,7 @@ struct SinkhornSession : Session {
     // B at u = v = 0 and E (solvers.hpp:441-442), record(0)
     row_lse(nullptr);
     col_lse(0, nullptr);
-    k_sk_scalars<<<1, 32, 0, cx.stream>>>(ctl.p, sv, ws.nblk, 1, ws.trace.p, nullptr);
+    k_sk_scalars<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv, sk_blocks(), 1, ws.trace.p, nullptr);
     PG_CK(cudaGetLastError());
     sync_ctl();
     if (cfg.record_rounded_cost) fill_last_record_cost(round_now(nullptr).cost);

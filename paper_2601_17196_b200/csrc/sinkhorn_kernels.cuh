@@ -294,59 +294,80 @@ __device__ void sk_block_store(double (&acc)[K], double* out) {
   if (threadIdx.x < K) out[blockIdx.x * K + threadIdx.x] = sh[threadIdx.x][0];
 }
 
-// Rows: LSE_i over strips + the dummy column (logK_in = -0, x = v_n);
-// row sums of B(u, v) = exp(u_i + LSE_i); next u = log r - LSE.
+// warp-wide (m, S) log-sum-exp merge
+__device__ __forceinline__ void warp_lse(double& m, double& S) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const double S2 = __shfl_xor_sync(0xffffffffu, S, o);
+    lse_merge(m, S, m2, S2);
+  }
+}
+
+constexpr int kSkWarps = kVecThreads / 32;
+
+// Rows (a warp per row): LSE_i over strips + the dummy column
+// (logK_in = -0, x = v_n); row sums of B(u, v) = exp(u_i + LSE_i); next
+// u = log r - LSE.
 __global__ void __launch_bounds__(kVecThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
                                                          int fmt, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double vn = sv.v[n];
   double acc[4] = {0, 0, 0, 0};  // |row - r|, sum row, masked u.r
-  for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t i = int64_t(blockIdx.x) * kSkWarps + warp; i < n; i += int64_t(gridDim.x) * kSkWarps) {
     double M = -INFINITY, S = 0.0;
-    for (int64_t s = 0; s < nstrips; ++s) {
+    for (int64_t s = lane; s < nstrips; s += 32) {
       double m2, S2;
       lse_part(rowp, s * n + i, fmt, m2, S2);
       lse_merge(M, S, m2, S2);
     }
-    lse_merge(M, S, -0.0 + vn, 1.0);
-    const double lse = M + log(S);
-    const double row = exp(sv.u[i] + lse);
-    acc[0] += fabs(row - sv.r[i]);
-    acc[1] += row;
-    if (sv.r[i] > 0) acc[2] += sv.u[i] * sv.r[i];  // masked_dot (solvers.hpp:389-395)
-    sv.u_next[i] = sv.log_r[i] - lse;
+    warp_lse(M, S);
+    if (lane == 0) {
+      lse_merge(M, S, -0.0 + vn, 1.0);
+      const double lse = M + log(S);
+      const double row = exp(sv.u[i] + lse);
+      acc[0] += fabs(row - sv.r[i]);
+      acc[1] += row;
+      if (sv.r[i] > 0) acc[2] += sv.u[i] * sv.r[i];  // masked_dot (solvers.hpp:389-395)
+      sv.u_next[i] = sv.log_r[i] - lse;
+    }
   }
   sk_block_store<4>(acc, sv.scratch);
 }
 
-// Columns: LSE_j over row blocks + the dummy row (logK_nj = -0, x = u_n).
-// update: v_j = log c_j - LSE_j; the column sums of B(u, v) are
-// exp(v_j + LSE_j) with the (updated or current) v.
+// Columns (a warp per column): LSE_j over row blocks + the dummy row
+// (logK_nj = -0, x = u_n). update: v_j = log c_j - LSE_j; the column sums
+// of B(u, v) are exp(v_j + LSE_j) with the (updated or current) v.
 __global__ void __launch_bounds__(kVecThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
                                                          int update, int nblk_rows, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double un = sv.u[n];
   double acc[4] = {0, 0, 0, 0};  // |col - c|, masked v.c
-  for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t j = int64_t(blockIdx.x) * kSkWarps + warp; j < n; j += int64_t(gridDim.x) * kSkWarps) {
     double M = -INFINITY, S = 0.0;
-    for (int64_t s = 0; s < nrb; ++s) {
+    for (int64_t s = lane; s < nrb; s += 32) {
       double m2, S2;
       lse_part(colp, s * n + j, fmt, m2, S2);
       lse_merge(M, S, m2, S2);
     }
-    lse_merge(M, S, -0.0 + un, 1.0);
-    const double lse = M + log(S);
-    double vj = sv.v[j];
-    if (update) {
-      vj = sv.log_c[j] - lse;
-      sv.v[j] = vj;
-      sv.zv_v[j] = vj;
+    warp_lse(M, S);
+    if (lane == 0) {
+      lse_merge(M, S, -0.0 + un, 1.0);
+      const double lse = M + log(S);
+      double vj = sv.v[j];
+      if (update) {
+        vj = sv.log_c[j] - lse;
+        sv.v[j] = vj;
+        sv.zv_v[j] = vj;
+      }
+      const double col = exp(vj + lse);
+      acc[0] += fabs(col - sv.c[j]);
+      if (sv.c[j] > 0) acc[1] += vj * sv.c[j];
     }
-    const double col = exp(vj + lse);
-    acc[0] += fabs(col - sv.c[j]);
-    if (sv.c[j] > 0) acc[1] += vj * sv.c[j];
   }
   if (update && blockIdx.x == 0 && threadIdx.x == 0) sv.v[n] = sv.log_c[n] - ctl->col_lse_n;
   sk_block_store<4>(acc, sv.scratch + 4 * nblk_rows);
@@ -369,13 +390,25 @@ __device__ void sk_loop_head(SinkCtl* ctl) {  // solvers.hpp:458-462
 
 // E = |B1 - r|_1 + |B^T 1 - c|_1 (solvers.hpp:432-435), the trace's dual
 // value (:436-438), record rule (:445) and the loop head.
-__global__ void k_sk_scalars(SinkCtl* ctl, SinkVec sv, int nblk, int init, TraceDev* trace, const int* gate) {
+__global__ void __launch_bounds__(kVecThreads) k_sk_scalars(SinkCtl* ctl, SinkVec sv, int nblk, int init, TraceDev* trace,
+                                                            const int* gate) {
   if (gate && *gate == 0) return;
-  if (threadIdx.x || blockIdx.x) return;
+  double part[5] = {0, 0, 0, 0, 0};  // rerr, rsum, ur, cerr, vc
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    part[0] += sv.scratch[4 * b]; part[1] += sv.scratch[4 * b + 1]; part[2] += sv.scratch[4 * b + 2];
+    part[3] += sv.scratch[4 * nblk + 4 * b]; part[4] += sv.scratch[4 * nblk + 4 * b + 1];
+  }
+  __shared__ double sh[5][kVecThreads];
+  for (int q = 0; q < 5; ++q) sh[q][threadIdx.x] = part[q];
+  __syncthreads();
+  for (int s = kVecThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int q = 0; q < 5; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x) return;
   const int64_t n = ctl->n;
-  double rerr = 0, rsum = 0, ur = 0, cerr = 0, vc = 0;
-  for (int b = 0; b < nblk; ++b) { rerr += sv.scratch[4 * b]; rsum += sv.scratch[4 * b + 1]; ur += sv.scratch[4 * b + 2]; }
-  for (int b = 0; b < nblk; ++b) { cerr += sv.scratch[4 * nblk + 4 * b]; vc += sv.scratch[4 * nblk + 4 * b + 1]; }
+  double rerr = sh[0][0], rsum = sh[1][0], ur = sh[2][0], cerr = sh[3][0], vc = sh[4][0];
   // dummy row n and column n
   const double rown = exp(sv.u[n] + ctl->row_lse_n);
   const double coln = exp(sv.v[n] + ctl->col_lse_n);
