@@ -502,6 +502,7 @@ struct AspotSession : Session {
     burst = std::min<int64_t>(burst, 1 << 16);
     while (true) {
       launch_attempts(burst);
+      PG_CK(cudaEventRecord(ev1, cx.stream));  // device end of the loop (before the host poll)
       sync_ctl();
       if (!h.g_active || h.fatal) break;
       burst = std::max(1, cfg.sync_every);
@@ -528,7 +529,6 @@ struct AspotSession : Session {
       if (cfg.record_rounded_cost && h.paused) fill_last_record_cost(round_now(nullptr).cost);
       if (!h.paused || h.t >= target) break;
     }
-    PG_CK(cudaEventRecord(ev1, cx.stream));
     PG_CK(cudaEventSynchronize(ev1));
     float f = 0.f;
     PG_CK(cudaEventElapsedTime(&f, ev0, ev1));

@@ -207,6 +207,7 @@ struct SinkhornSession : Session {
     burst = std::min<int64_t>(burst, 1 << 16);
     while (true) {
       launch_iterations(burst);
+      PG_CK(cudaEventRecord(ev1, cx.stream));
       sync_ctl();
       if (!hctl->g_active || hctl->fatal) break;
       burst = std::max(1, cfg.sync_every);
@@ -242,7 +243,6 @@ struct SinkhornSession : Session {
       if (cfg.record_rounded_cost && hctl->paused) fill_last_record_cost(round_now(nullptr).cost);
       if (!hctl->paused || hctl->it >= target) break;
     }
-    PG_CK(cudaEventRecord(ev1, cx.stream));
     PG_CK(cudaEventSynchronize(ev1));
     float f = 0.f;
     PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
