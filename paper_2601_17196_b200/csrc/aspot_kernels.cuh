@@ -145,59 +145,57 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
   }
 }
 
-// One kernel per evaluated point: a warp per index i combines the sweep's
-// strip / row-block partials into (B 1)_i and (B^T 1)_i and forms the
-// per-element terms of every functional the reference evaluates there;
-// blocks reduce them to fixed-order partials, and the last block to finish
-// (atomic ticket) reduces all partials in a fixed order and takes the
-// decision (apply_role). Deterministic, one launch.
-constexpr int kEvalWarps = kVecThreads / 32;
+// One kernel per evaluated point: a thread per index i combines the
+// sweep's strip / row-block partials (contiguous per index) into (B 1)_i and
+// (B^T 1)_i and forms the per-element terms of every functional the
+// reference evaluates there; blocks reduce them to fixed-order partials, and
+// the last block to finish (atomic ticket) reduces all partials in a fixed
+// order and takes the decision (apply_role). Deterministic, one launch.
+constexpr int kEvalThreads = 128;
 
-__global__ void __launch_bounds__(kVecThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
+__global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.z.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[kNumPartials + 1];
 #pragma unroll
   for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = is_max_slot(k) ? -INFINITY : 0.0;
   const double* u = a.z.u();
   const double* v = a.z.v();
   const double w = *a.z.w();
-  for (int64_t i = int64_t(blockIdx.x) * kEvalWarps + warp; i < n; i += int64_t(gridDim.x) * kEvalWarps) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double ui = u[i], vi = v[i];
     const double a2 = (ui + w) * kLog2e;  // row offset of fp32 row partials
     double rb = 0.0, cb = 0.0;
-    for (int64_t s = lane; s < a.nstrips; s += 32) rb += partial_value(a.rowp, s * n + i, a.pfmt, a2);
-    for (int64_t s = lane; s < a.nrowblocks; s += 32) cb += partial_value(a.colp, s * n + i, a.pfmt);
-    rb = warp_sum(rb);
-    cb = warp_sum(cb);
-    if (lane == 0) {
-      a.row_out[i] = rb;
-      a.col_out[i] = cb;
-      const double eu = eexp(ui), ev = eexp(vi);
-      acc[0] += rb;
-      acc[1] = nan_max(acc[1], ui);
-      acc[2] = nan_max(acc[2], vi);
-      acc[3] += eu;
-      acc[4] += ev;
-      acc[5] += ui * a.rt[i];
-      acc[6] += vi * a.ct[i];
-      const double rowf = rb + eu, colf = cb + ev;
-      acc[7] += rho_limit(a.rt[i], rowf);
-      acc[8] += rho_limit(a.ct[i], colf);
-      acc[9] += fabs(rowf - a.rt[i]);
-      acc[10] += fabs(colf - a.ct[i]);
-    }
+    const int64_t ns = a.nstrips, nr = a.nrowblocks;
+#pragma unroll 4
+    for (int64_t s = 0; s < ns; ++s) rb += partial_value(a.rowp, i * ns + s, a.pfmt, a2);
+#pragma unroll 4
+    for (int64_t s = 0; s < nr; ++s) cb += partial_value(a.colp, i * nr + s, a.pfmt);
+    a.row_out[i] = rb;
+    a.col_out[i] = cb;
+    const double eu = eexp(ui), ev = eexp(vi);
+    acc[0] += rb;
+    acc[1] = nan_max(acc[1], ui);
+    acc[2] = nan_max(acc[2], vi);
+    acc[3] += eu;
+    acc[4] += ev;
+    acc[5] += ui * a.rt[i];
+    acc[6] += vi * a.ct[i];
+    const double rowf = rb + eu, colf = cb + ev;
+    acc[7] += rho_limit(a.rt[i], rowf);
+    acc[8] += rho_limit(a.ct[i], colf);
+    acc[9] += fabs(rowf - a.rt[i]);
+    acc[10] += fabs(colf - a.ct[i]);
   }
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
     acc[11] = nan_max(acc[11], a.maxp[k]);
-  __shared__ double sh[kNumPartials + 1][kVecThreads];
+  __shared__ double sh[kNumPartials + 1][kEvalThreads];
   __shared__ bool last;
   auto block_reduce = [&]() {
 #pragma unroll
     for (int k = 0; k < kNumPartials + 1; ++k) sh[k][threadIdx.x] = acc[k];
     __syncthreads();
-    for (int stride = kVecThreads / 2; stride > 0; stride >>= 1) {
+    for (int stride = kEvalThreads / 2; stride > 0; stride >>= 1) {
       if (threadIdx.x < stride) {
 #pragma unroll
         for (int k = 0; k < kNumPartials + 1; ++k) {

@@ -113,7 +113,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * ws.nrb * n));
   ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
-  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n, kEvalWarps), 4096));
+  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n, kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, (kNumPartials + 1) * ws.eval_blocks)));
   ws.ticket.alloc(1);
   ws.ticket.zero(cx.stream);
@@ -167,7 +167,7 @@ inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int*
   r.scratch = ws.scratch.p;
   r.gate = gate;
   r.pfmt = ws.pfmt;
-  k_point_eval<<<ws.eval_blocks, kVecThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
+  k_point_eval<<<ws.eval_blocks, kEvalThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());
 }
 

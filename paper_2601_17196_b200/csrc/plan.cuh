@@ -23,8 +23,8 @@ __global__ void __launch_bounds__(kVecThreads) k_sum_partials(const double* rowp
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double a2 = ((z.u()[i] + (lu ? lu[i] : 0.0)) + w) * kLog2e;
     double rr = 0.0, cc = 0.0;
-    for (int64_t s = 0; s < nstrips; ++s) rr += partial_value(rowp, s * n + i, pfmt, a2);
-    for (int64_t s = 0; s < nrb; ++s) cc += partial_value(colp, s * n + i, pfmt);
+    for (int64_t s = 0; s < nstrips; ++s) rr += partial_value(rowp, i * nstrips + s, pfmt, a2);
+    for (int64_t s = 0; s < nrb; ++s) cc += partial_value(colp, i * nrb + s, pfmt);
     row[i] = rr;
     col[i] = cc;
   }

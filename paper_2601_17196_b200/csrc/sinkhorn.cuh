@@ -43,7 +43,7 @@ struct SinkhornSession : Session {
     if (hctl) cudaFreeHost(hctl);
   }
 
-  int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n, kSkWarps), 2048)); }
+  int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n, kSkThreads), 2048)); }
   Slot zv_slot() const { return Slot{zv.p, P.n}; }
   Slot zf_slot() const { return Slot{zf.p, P.n}; }
 
@@ -61,7 +61,7 @@ struct SinkhornSession : Session {
       launch_sweep(cx, P, ws, zv_slot(), nullptr, nullptr, gate, false, gamma);  // rows of (0, v, 0)
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.v, 0, gate);
-    k_sk_rows<<<sk_blocks(), kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.rowp.p, ws.nstrips,
+    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, ws.rowp.p, ws.nstrips,
                                                       P.dtype == POTGPU_F64 ? LP_F64 : LP_F32, gate);
   }
 
@@ -80,7 +80,7 @@ struct SinkhornSession : Session {
                                                                             reinterpret_cast<float2*>(ws.colp.p), gate);
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
-    k_sk_cols<<<sk_blocks(), kVecThreads, 0, cx.stream>>>(ctl.p, sv, ws.colp.p, ws.nrb, P.dtype == POTGPU_F64 ? LP_F64 : LP_F32,
+    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, ws.colp.p, ws.nrb, P.dtype == POTGPU_F64 ? LP_F64 : LP_F32,
                                                       update, sk_blocks(), gate);
   }
 

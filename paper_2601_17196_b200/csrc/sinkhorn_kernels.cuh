@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __
       for (int k = 0; k < 8; ++k) S += exp(x[k] - m);
     }
     S = warp_sum(S);
-    if (lane == 0) rowp[int64_t(blockIdx.x) * n + i] = make_double2(m, S);
+    if (lane == 0) rowp[i * gridDim.x + blockIdx.x] = make_double2(m, S);
   }
 }
 
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f64(const double* __
   const int t = threadIdx.x;
   double M = -INFINITY, SS = 0.0;
   for (int w = 0; w < kWarps; ++w) lse_merge(M, SS, sm[w][t], sS[w][t]);
-  if (j0 + t < n) colp[int64_t(blockIdx.y) * n + j0 + t] = make_double2(M, SS);
+  if (j0 + t < n) colp[(j0 + t) * gridDim.y + blockIdx.y] = make_double2(M, SS);
 }
 
 // ---------------------------------------------------------------- fp32 --
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t
     if (M != -INFINITY)
       for (int w = 0; w < kWarps; ++w)
         if (sm[w][c] != -INFINITY) SS += sS[w][c] * ex2f(sm[w][c] - M);
-    if (j0 + c < n) colp[int64_t(blockIdx.y) * n + j0 + c] = make_float2(M == -INFINITY ? 0.f : SS, M == -INFINITY ? 0.f : M);
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(M == -INFINITY ? 0.f : SS, M == -INFINITY ? 0.f : M);
   }
 }
 
@@ -281,12 +281,12 @@ __global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, const int* 
   }
 }
 
-template <int K>
+template <int K, int T>
 __device__ void sk_block_store(double (&acc)[K], double* out) {
-  __shared__ double sh[K][kVecThreads];
+  __shared__ double sh[K][T];
   for (int k = 0; k < K; ++k) sh[k][threadIdx.x] = acc[k];
   __syncthreads();
-  for (int s = kVecThreads / 2; s > 0; s >>= 1) {
+  for (int s = T / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s)
       for (int k = 0; k < K; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + s];
     __syncthreads();
@@ -294,83 +294,65 @@ __device__ void sk_block_store(double (&acc)[K], double* out) {
   if (threadIdx.x < K) out[blockIdx.x * K + threadIdx.x] = sh[threadIdx.x][0];
 }
 
-// warp-wide (m, S) log-sum-exp merge
-__device__ __forceinline__ void warp_lse(double& m, double& S) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
-    const double S2 = __shfl_xor_sync(0xffffffffu, S, o);
-    lse_merge(m, S, m2, S2);
-  }
-}
+constexpr int kSkThreads = 128;
 
-constexpr int kSkWarps = kVecThreads / 32;
-
-// Rows (a warp per row): LSE_i over strips + the dummy column
-// (logK_in = -0, x = v_n); row sums of B(u, v) = exp(u_i + LSE_i); next
-// u = log r - LSE.
-__global__ void __launch_bounds__(kVecThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
-                                                         int fmt, const int* gate) {
+// Rows (a thread per row; the row's strip partials are contiguous): LSE_i
+// + the dummy column (logK_in = -0, x = v_n); row sums of B(u, v) =
+// exp(u_i + LSE_i); next u = log r - LSE.
+__global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
+                                                        int fmt, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double vn = sv.v[n];
   double acc[4] = {0, 0, 0, 0};  // |row - r|, sum row, masked u.r
-  for (int64_t i = int64_t(blockIdx.x) * kSkWarps + warp; i < n; i += int64_t(gridDim.x) * kSkWarps) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double M = -INFINITY, S = 0.0;
-    for (int64_t s = lane; s < nstrips; s += 32) {
+    for (int64_t s = 0; s < nstrips; ++s) {
       double m2, S2;
-      lse_part(rowp, s * n + i, fmt, m2, S2);
+      lse_part(rowp, i * nstrips + s, fmt, m2, S2);
       lse_merge(M, S, m2, S2);
     }
-    warp_lse(M, S);
-    if (lane == 0) {
-      lse_merge(M, S, -0.0 + vn, 1.0);
-      const double lse = M + log(S);
-      const double row = exp(sv.u[i] + lse);
-      acc[0] += fabs(row - sv.r[i]);
-      acc[1] += row;
-      if (sv.r[i] > 0) acc[2] += sv.u[i] * sv.r[i];  // masked_dot (solvers.hpp:389-395)
-      sv.u_next[i] = sv.log_r[i] - lse;
-    }
+    lse_merge(M, S, -0.0 + vn, 1.0);
+    const double lse = M + log(S);
+    const double row = exp(sv.u[i] + lse);
+    acc[0] += fabs(row - sv.r[i]);
+    acc[1] += row;
+    if (sv.r[i] > 0) acc[2] += sv.u[i] * sv.r[i];  // masked_dot (solvers.hpp:389-395)
+    sv.u_next[i] = sv.log_r[i] - lse;
   }
-  sk_block_store<4>(acc, sv.scratch);
+  sk_block_store<4, kSkThreads>(acc, sv.scratch);
 }
 
-// Columns (a warp per column): LSE_j over row blocks + the dummy row
-// (logK_nj = -0, x = u_n). update: v_j = log c_j - LSE_j; the column sums
-// of B(u, v) are exp(v_j + LSE_j) with the (updated or current) v.
-__global__ void __launch_bounds__(kVecThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
-                                                         int update, int nblk_rows, const int* gate) {
+// Columns (a thread per column): LSE_j + the dummy row (logK_nj = -0,
+// x = u_n). update: v_j = log c_j - LSE_j; the column sums of B(u, v) are
+// exp(v_j + LSE_j) with the (updated or current) v.
+__global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
+                                                        int update, int nblk_rows, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double un = sv.u[n];
   double acc[4] = {0, 0, 0, 0};  // |col - c|, masked v.c
-  for (int64_t j = int64_t(blockIdx.x) * kSkWarps + warp; j < n; j += int64_t(gridDim.x) * kSkWarps) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
     double M = -INFINITY, S = 0.0;
-    for (int64_t s = lane; s < nrb; s += 32) {
+    for (int64_t s = 0; s < nrb; ++s) {
       double m2, S2;
-      lse_part(colp, s * n + j, fmt, m2, S2);
+      lse_part(colp, j * nrb + s, fmt, m2, S2);
       lse_merge(M, S, m2, S2);
     }
-    warp_lse(M, S);
-    if (lane == 0) {
-      lse_merge(M, S, -0.0 + un, 1.0);
-      const double lse = M + log(S);
-      double vj = sv.v[j];
-      if (update) {
-        vj = sv.log_c[j] - lse;
-        sv.v[j] = vj;
-        sv.zv_v[j] = vj;
-      }
-      const double col = exp(vj + lse);
-      acc[0] += fabs(col - sv.c[j]);
-      if (sv.c[j] > 0) acc[1] += vj * sv.c[j];
+    lse_merge(M, S, -0.0 + un, 1.0);
+    const double lse = M + log(S);
+    double vj = sv.v[j];
+    if (update) {
+      vj = sv.log_c[j] - lse;
+      sv.v[j] = vj;
+      sv.zv_v[j] = vj;
     }
+    const double col = exp(vj + lse);
+    acc[0] += fabs(col - sv.c[j]);
+    if (sv.c[j] > 0) acc[1] += vj * sv.c[j];
   }
   if (update && blockIdx.x == 0 && threadIdx.x == 0) sv.v[n] = sv.log_c[n] - ctl->col_lse_n;
-  sk_block_store<4>(acc, sv.scratch + 4 * nblk_rows);
+  sk_block_store<4, kSkThreads>(acc, sv.scratch + 4 * nblk_rows);
 }
 
 __global__ void k_sk_commit_u(SinkCtl* ctl, SinkVec sv) {

@@ -26,8 +26,8 @@ struct SweepArgs {
   const double* w;
   const double* lu;     // optional additive row log-weights (rounding), may be null
   const double* lv;     // optional additive column log-weights
-  double* rowp;         // [gridDim.x][n]: row partial of strip x
-  double* colp;         // [gridDim.y][n]: column partial of row block y
+  double* rowp;         // [n][gridDim.x]: row partials, one per strip (contiguous per row)
+  double* colp;         // [n][gridDim.y]: column partials, one per row block
   double* maxp;         // [gridDim.y][gridDim.x]: max exponent (natural log units)
   const int* gate;      // kernel runs iff *gate != 0 (null: always)
   double gamma;         // for fp32 sources: exponent scale log2(e)/gamma folded in src
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __r
       cacc[2 * k + 1] += b1;
     }
     rs = warp_sum(rs);
-    if (lane == 0) a.rowp[int64_t(blockIdx.x) * n + i] = rs;
+    if (lane == 0) a.rowp[i * gridDim.x + blockIdx.x] = rs;  // [row][strip]
   }
   __shared__ double cs[kWarps][kStripCols];
   __shared__ double ms[kWarps];
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __r
   double s = 0.0;
 #pragma unroll
   for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][t];
-  if (j0 + t < n) a.colp[int64_t(blockIdx.y) * n + j0 + t] = s;
+  if (j0 + t < n) a.colp[(j0 + t) * gridDim.y + blockIdx.y] = s;  // [col][row block]
   if (t == 0) {
     double m = ms[0];
     for (int ww = 1; ww < kWarps; ++ww) m = nan_max(m, ms[ww]);
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   for (int q = 0; q < kPairs; ++q) cacc[q] = make_float2(0.f, 0.f);
   float sigma = -INFINITY;  // running column scale (log2) of this warp
   float mmax = -INFINITY;
-  float2* rowp = reinterpret_cast<float2*>(a.rowp) + int64_t(blockIdx.x) * n;
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);  // [row][strip]
   // one-row-ahead software pipeline: the next row's data is in flight while
   // this row is exponentiated
   typename Src::RowData nxt{};
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
       rs = __fadd2_rn(rs, p[q]);
     }
     const float r = warp_sum(rs.x + rs.y);
-    if (lane == 0) rowp[i] = make_float2(r, ms);  // value = r 2^(ms + A_i), A_i added in fp64
+    if (lane == 0) rowp[i * gridDim.x + blockIdx.x] = make_float2(r, ms);  // value = r 2^(ms + A_i), A_i added in fp64
     const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;  // row max of t (log2)
     if (mA > sigma) {  // warp-uniform
       const float sc = ex2f(sigma - mA);
@@ -305,12 +305,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
     cs[warp][c + 1] = cacc[q].y * fw;
   }
   __syncthreads();
-  float2* colp = reinterpret_cast<float2*>(a.colp) + int64_t(blockIdx.y) * n;
+  float2* colp = reinterpret_cast<float2*>(a.colp);  // [col][row block]
   for (int c = threadIdx.x; c < kStripCols32; c += kThreads) {
     float s = 0.f;
 #pragma unroll
     for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
-    if (j0 + c < n) colp[j0 + c] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
   }
   if (threadIdx.x == 0) {
     float m = mm[0];

@@ -72,7 +72,8 @@ def compare_fp64(ctx, r, c, C, s, cfg: pot.SolverConfig, exact_decisions=True, m
         # decision columns: halvings, block_hat, zbest_is_check, block_check
         flips = np.flatnonzero((g.iter_log[:, 1:5] != o.log[:, 1:5]).any(axis=1))
         assert len(flips) <= max_tie_flips, (flips, g.iter_log[flips], o.log[flips])
-    np.testing.assert_allclose(g.iter_log[:, 5], o.log[:, 5], rtol=1e-9, atol=1e-14)
+    if max_tie_flips == 0:  # identical decisions -> identical E trajectory
+        np.testing.assert_allclose(g.iter_log[:, 5], o.log[:, 5], rtol=1e-9, atol=1e-14)
     assert abs(g.final_error - o.final_error) <= 1e-9 * max(o.final_error, 1e-30) + 1e-15
     assert abs(g.cost - o.cost) <= TOL_F64_OBJ * max(abs(o.cost), 1e-12)
     assert g.feasibility_gap <= TOL_F64_VIOL
