@@ -152,7 +152,47 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
 // the last block to finish (atomic ticket) reduces all partials in a fixed
 // order and takes the decision (apply_role). Deterministic, one launch.
 constexpr int kEvalThreads = 128;
+constexpr int kTPI = 4;  // threads per index
 
+// Sum of the partials p[base .. base + cnt) of one index, split over the
+// kTPI threads of a group (thread q takes s = q, q + kTPI, ...). fp32
+// (sum, log2 scale) partials are combined relative to their max with MUFU
+// ex2 and turned into fp64 once: S 2^(M + offset).
+__device__ __forceinline__ double group_partial_sum(const double* p, int64_t base, int64_t cnt, int fmt, double offset,
+                                                    int q) {
+  if (fmt == PF_F64) {
+    double s = 0.0;
+    for (int64_t k = q; k < cnt; k += kTPI) s += p[base + k];
+#pragma unroll
+    for (int o = kTPI / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+  }
+  const float2* f = reinterpret_cast<const float2*>(p) + base;
+  float M = -INFINITY;
+  for (int64_t k = q; k < cnt; k += kTPI) {
+    const float2 x = f[k];
+    if (x.x != 0.f) M = fmaxf(M, x.y);
+  }
+#pragma unroll
+  for (int o = kTPI / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float S = 0.f;
+  if (M != -INFINITY)
+    for (int64_t k = q; k < cnt; k += kTPI) {
+      const float2 x = f[k];
+      if (x.x != 0.f) S += x.x * ex2f(x.y - M);
+    }
+#pragma unroll
+  for (int o = kTPI / 2; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+  return M == -INFINITY ? 0.0 : double(S) * exp2(double(M) + offset);
+}
+
+// One kernel per evaluated point: a group of kTPI threads per index i
+// combines the sweep's strip / row-block partials (contiguous per index)
+// into (B 1)_i and (B^T 1)_i and forms the per-element terms of every
+// functional the reference evaluates there; blocks reduce them to
+// fixed-order partials, and the last block to finish (atomic ticket)
+// reduces all partials in a fixed order and takes the decision
+// (apply_role). Deterministic, one launch.
 __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.z.n;
@@ -162,15 +202,18 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   const double* u = a.z.u();
   const double* v = a.z.v();
   const double w = *a.z.w();
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const double ui = u[i], vi = v[i];
-    const double a2 = (ui + w) * kLog2e;  // row offset of fp32 row partials
-    double rb = 0.0, cb = 0.0;
-    const int64_t ns = a.nstrips, nr = a.nrowblocks;
-#pragma unroll 4
-    for (int64_t s = 0; s < ns; ++s) rb += partial_value(a.rowp, i * ns + s, a.pfmt, a2);
-#pragma unroll 4
-    for (int64_t s = 0; s < nr; ++s) cb += partial_value(a.colp, i * nr + s, a.pfmt);
+  const int q = threadIdx.x % kTPI;
+  const int64_t per_block = kEvalThreads / kTPI;
+  const int64_t span = int64_t(gridDim.x) * per_block;
+  // all threads iterate the same number of times (the shuffles need the full warp)
+  for (int64_t i0 = int64_t(blockIdx.x) * per_block; i0 < n; i0 += span) {
+    const int64_t i = i0 + threadIdx.x / kTPI;
+    const bool live = i < n;
+    const int64_t ii = live ? i : n - 1;
+    const double ui = u[ii], vi = v[ii];
+    const double rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, (ui + w) * kLog2e, q);
+    const double cb = group_partial_sum(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
+    if (!live || q != 0) continue;
     a.row_out[i] = rb;
     a.col_out[i] = cb;
     const double eu = eexp(ui), ev = eexp(vi);

@@ -113,7 +113,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * ws.nrb * n));
   ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
-  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n, kEvalThreads), 4096));
+  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * kTPI, kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, (kNumPartials + 1) * ws.eval_blocks)));
   ws.ticket.alloc(1);
   ws.ticket.zero(cx.stream);

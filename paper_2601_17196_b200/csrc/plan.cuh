@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kVecThreads) k_sum_partials(const double* rowp
     double rr = 0.0, cc = 0.0;
     for (int64_t s = 0; s < nstrips; ++s) rr += partial_value(rowp, i * nstrips + s, pfmt, a2);
     for (int64_t s = 0; s < nrb; ++s) cc += partial_value(colp, i * nrb + s, pfmt);
-    row[i] = rr;
+    row[i] = rr;  // (output stage only: fp64 exp2 per partial is fine here)
     col[i] = cc;
   }
 }

@@ -43,7 +43,7 @@ struct SinkhornSession : Session {
     if (hctl) cudaFreeHost(hctl);
   }
 
-  int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n, kSkThreads), 2048)); }
+  int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n * kSkTPI, kSkThreads), 4096)); }
   Slot zv_slot() const { return Slot{zv.p, P.n}; }
   Slot zf_slot() const { return Slot{zf.p, P.n}; }
 

@@ -295,23 +295,62 @@ __device__ void sk_block_store(double (&acc)[K], double* out) {
 }
 
 constexpr int kSkThreads = 128;
+constexpr int kSkTPI = 4;  // threads per index
 
-// Rows (a thread per row; the row's strip partials are contiguous): LSE_i
-// + the dummy column (logK_in = -0, x = v_n); row sums of B(u, v) =
+// log-sum-exp of the cnt (max, sum) partials at p[base..] of one index,
+// split over a group of kSkTPI threads (max pass, then sum pass); result as
+// (M, S) in natural-log units, replicated in the group.
+__device__ __forceinline__ void group_lse(const double* p, int64_t base, int64_t cnt, int fmt, int q, double& M, double& S) {
+  M = -INFINITY;
+  for (int64_t k = q; k < cnt; k += kSkTPI) {
+    double m2, S2;
+    lse_part(p, base + k, fmt, m2, S2);
+    if (S2 != 0.0) M = fmax(M, m2);
+  }
+#pragma unroll
+  for (int o = kSkTPI / 2; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  S = 0.0;
+  if (M != -INFINITY) {
+    if (fmt == LP_F32) {
+      const float Ml2 = float(M * kLog2e);
+      float Sf = 0.f;
+      const float2* f = reinterpret_cast<const float2*>(p) + base;
+      for (int64_t k = q; k < cnt; k += kSkTPI) {
+        const float2 x = f[k];
+        if (x.x != 0.f) Sf += x.x * ex2f(x.y - Ml2);
+      }
+      S = double(Sf);
+      M = double(Ml2) * kLn2;
+    } else {
+      for (int64_t k = q; k < cnt; k += kSkTPI) {
+        double m2, S2;
+        lse_part(p, base + k, fmt, m2, S2);
+        if (S2 != 0.0) S += S2 * exp(m2 - M);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = kSkTPI / 2; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+}
+
+// Rows (a thread group per row; the row's strip partials are contiguous):
+// LSE_i + the dummy column (logK_in = -0, x = v_n); row sums of B(u, v) =
 // exp(u_i + LSE_i); next u = log r - LSE.
 __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
                                                         int fmt, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double vn = sv.v[n];
+  const int q = threadIdx.x % kSkTPI;
+  const int64_t per_block = kSkThreads / kSkTPI, span = int64_t(gridDim.x) * per_block;
   double acc[4] = {0, 0, 0, 0};  // |row - r|, sum row, masked u.r
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double M = -INFINITY, S = 0.0;
-    for (int64_t s = 0; s < nstrips; ++s) {
-      double m2, S2;
-      lse_part(rowp, i * nstrips + s, fmt, m2, S2);
-      lse_merge(M, S, m2, S2);
-    }
+  for (int64_t i0 = int64_t(blockIdx.x) * per_block; i0 < n; i0 += span) {
+    const int64_t i = i0 + threadIdx.x / kSkTPI;
+    const bool live = i < n;
+    const int64_t ii = live ? i : n - 1;
+    double M, S;
+    group_lse(rowp, ii * nstrips, nstrips, fmt, q, M, S);
+    if (!live || q != 0) continue;
     lse_merge(M, S, -0.0 + vn, 1.0);
     const double lse = M + log(S);
     const double row = exp(sv.u[i] + lse);
@@ -323,22 +362,24 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv
   sk_block_store<4, kSkThreads>(acc, sv.scratch);
 }
 
-// Columns (a thread per column): LSE_j + the dummy row (logK_nj = -0,
-// x = u_n). update: v_j = log c_j - LSE_j; the column sums of B(u, v) are
-// exp(v_j + LSE_j) with the (updated or current) v.
+// Columns (a thread group per column): LSE_j + the dummy row (logK_nj =
+// -0, x = u_n). update: v_j = log c_j - LSE_j; the column sums of B(u, v)
+// are exp(v_j + LSE_j) with the (updated or current) v.
 __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
                                                         int update, int nblk_rows, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double un = sv.u[n];
+  const int q = threadIdx.x % kSkTPI;
+  const int64_t per_block = kSkThreads / kSkTPI, span = int64_t(gridDim.x) * per_block;
   double acc[4] = {0, 0, 0, 0};  // |col - c|, masked v.c
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
-    double M = -INFINITY, S = 0.0;
-    for (int64_t s = 0; s < nrb; ++s) {
-      double m2, S2;
-      lse_part(colp, j * nrb + s, fmt, m2, S2);
-      lse_merge(M, S, m2, S2);
-    }
+  for (int64_t j0 = int64_t(blockIdx.x) * per_block; j0 < n; j0 += span) {
+    const int64_t j = j0 + threadIdx.x / kSkTPI;
+    const bool live = j < n;
+    const int64_t jj = live ? j : n - 1;
+    double M, S;
+    group_lse(colp, jj * nrb, nrb, fmt, q, M, S);
+    if (!live || q != 0) continue;
     lse_merge(M, S, -0.0 + un, 1.0);
     const double lse = M + log(S);
     double vj = sv.v[j];
