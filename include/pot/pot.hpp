@@ -1,0 +1,376 @@
+// pot/pot.hpp — drop-in C++ mirror of the reference's `namespace pot` solver
+// API (/root/reference/proj/include/pot/{core,dual,solvers,extend,rounding,
+// synthetic}.hpp), backed by libpotgpu.so (include/potgpu.h) on a B200.
+//
+// Same names, argument meaning and error behaviour: a reference user replaces
+// `-I proj/include` with `-I <repo>/include` and links `-lpotgpu`. Eigen is not
+// required: pot::Vector / pot::Matrix are small owning dense types with the
+// subset of Eigen's interface the reference API exposes (column-major Matrix,
+// (i, j) indexing). Solves run on the GPU; validation, plan metrics and the
+// small helpers (entropy, theta_next, rho, theory_bounds) are host code.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../potgpu.h"
+
+namespace pot {
+
+// ------------------------------------------------------------- dense types --
+class Vector {
+ public:
+  Vector() = default;
+  explicit Vector(long n) : d_(static_cast<size_t>(n), 0.0) {}
+  static Vector Zero(long n) { return Vector(n); }
+  static Vector Constant(long n, double x) { Vector v(n); std::fill(v.d_.begin(), v.d_.end(), x); return v; }
+  long size() const { return long(d_.size()); }
+  double& operator()(long i) { return d_[size_t(i)]; }
+  double operator()(long i) const { return d_[size_t(i)]; }
+  double& operator[](long i) { return d_[size_t(i)]; }
+  double operator[](long i) const { return d_[size_t(i)]; }
+  double* data() { return d_.data(); }
+  const double* data() const { return d_.data(); }
+  double sum() const { double s = 0.0; for (double x : d_) s += x; return s; }
+  double minCoeff() const { return *std::min_element(d_.begin(), d_.end()); }
+  double maxCoeff() const { return *std::max_element(d_.begin(), d_.end()); }
+  bool allFinite() const { for (double x : d_) if (!std::isfinite(x)) return false; return true; }
+  void resize(long n) { d_.resize(size_t(n)); }
+
+ private:
+  std::vector<double> d_;
+};
+
+class Matrix {  // column-major like Eigen::MatrixXd
+ public:
+  Matrix() = default;
+  Matrix(long r, long c) : r_(r), c_(c), d_(static_cast<size_t>(r * c), 0.0) {}
+  static Matrix Zero(long r, long c) { return Matrix(r, c); }
+  static Matrix Constant(long r, long c, double x) { Matrix m(r, c); std::fill(m.d_.begin(), m.d_.end(), x); return m; }
+  static Matrix Ones(long r, long c) { return Constant(r, c, 1.0); }
+  long rows() const { return r_; }
+  long cols() const { return c_; }
+  long size() const { return r_ * c_; }
+  double& operator()(long i, long j) { return d_[size_t(i + j * r_)]; }
+  double operator()(long i, long j) const { return d_[size_t(i + j * r_)]; }
+  double* data() { return d_.data(); }
+  const double* data() const { return d_.data(); }
+  double sum() const { double s = 0.0; for (double x : d_) s += x; return s; }
+  double maxCoeff() const { return *std::max_element(d_.begin(), d_.end()); }
+  double minCoeff() const { return *std::min_element(d_.begin(), d_.end()); }
+  bool allFinite() const { for (double x : d_) if (!std::isfinite(x)) return false; return true; }
+  Vector rowSums() const { Vector v(r_); for (long j = 0; j < c_; ++j) for (long i = 0; i < r_; ++i) v(i) += (*this)(i, j); return v; }
+  Vector colSums() const { Vector v(c_); for (long j = 0; j < c_; ++j) for (long i = 0; i < r_; ++i) v(j) += (*this)(i, j); return v; }
+
+ private:
+  long r_ = 0, c_ = 0;
+  std::vector<double> d_;
+};
+
+// ------------------------------------------------------------ core.hpp --
+enum class ErrorCode {  // core.hpp:21-39 (order is the C-ABI contract)
+  DimensionMismatch, NegativeEntry, NonFiniteEntry, BudgetExceedsMass, Overflow, NonPositiveArgument,
+  DegenerateInstance, PenaltyTooSmall, UnbalancedMarginals, ZeroEntropy, Infeasible, SizeLimitExceeded,
+  ZeroMassPlan, DegenerateSvd, EmptyInput, InvalidArgument, IoFailure,
+};
+
+inline const char* error_code_name(ErrorCode code) {
+  static const char* names[] = {"DimensionMismatch", "NegativeEntry", "NonFiniteEntry", "BudgetExceedsMass", "Overflow",
+                                "NonPositiveArgument", "DegenerateInstance", "PenaltyTooSmall", "UnbalancedMarginals",
+                                "ZeroEntropy", "Infeasible", "SizeLimitExceeded", "ZeroMassPlan", "DegenerateSvd",
+                                "EmptyInput", "InvalidArgument", "IoFailure"};
+  const int k = int(code);
+  return k >= 0 && k < 17 ? names[k] : "Unknown";
+}
+
+class PotError : public std::runtime_error {  // core.hpp:64-74
+ public:
+  PotError(ErrorCode code, const std::string& message)
+      : std::runtime_error(std::string(error_code_name(code)) + ": " + message), code_(code) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+// Device-side failures with no reference counterpart (CUDA / NCCL errors).
+class DeviceError : public std::runtime_error {
+ public:
+  DeviceError(int code, const std::string& m) : std::runtime_error(m), code_(code) {}
+  int code() const { return code_; }
+
+ private:
+  int code_;
+};
+
+struct Instance {  // core.hpp:108-118
+  Vector r;
+  Vector c;
+  Matrix C;
+  double s = 0.0;
+  long size() const { return r.size(); }
+  double source_mass() const { return r.sum(); }
+  double target_mass() const { return c.sum(); }
+  double max_cost() const { return C.size() > 0 ? C.maxCoeff() : 0.0; }
+};
+
+inline constexpr double kBudgetSlack = 1e-12;  // core.hpp:129
+
+struct TransportPlan {  // core.hpp:179-197
+  Matrix X;
+  Vector row_slack;
+  Vector col_slack;
+  double mass = 0.0;
+};
+
+inline double transport_cost(const Matrix& C, const Matrix& X) {  // core.hpp:199-204
+  if (C.rows() != X.rows() || C.cols() != X.cols()) throw PotError(ErrorCode::DimensionMismatch, "cost/plan shape mismatch");
+  double s = 0.0;
+  for (long k = 0; k < C.size(); ++k) s += C.data()[k] * X.data()[k];
+  return s;
+}
+
+inline double plan_feasibility_gap(const TransportPlan& p, const Instance& in) {  // core.hpp:207-219
+  if (p.X.rows() != in.size() || p.X.cols() != in.size())
+    throw PotError(ErrorCode::DimensionMismatch, "plan shape does not match the instance");
+  const Vector rs = p.X.rowSums(), cs = p.X.colSums();
+  double rg = 0.0, cg = 0.0;
+  for (long i = 0; i < rs.size(); ++i) rg = std::max(rg, std::max(rs(i) - in.r(i), 0.0));
+  for (long j = 0; j < cs.size(); ++j) cg = std::max(cg, std::max(cs(j) - in.c(j), 0.0));
+  return std::max({rg, cg, std::fabs(p.X.sum() - in.s)});
+}
+
+enum class BlockRule { Greedy, RoundRobin };
+enum class SolverKind { Aspot, FeasibleSinkhorn, TunedSinkhorn };
+enum class SolveStatus { Converged, MaxIterationsExceeded, StepSizeUnderflow };
+
+inline const char* solver_kind_name(SolverKind k) {
+  switch (k) {
+    case SolverKind::Aspot: return "aspot";
+    case SolverKind::FeasibleSinkhorn: return "sinkhorn";
+    case SolverKind::TunedSinkhorn: return "tuned-sinkhorn";
+  }
+  return "unknown";
+}
+
+inline const char* solve_status_name(SolveStatus s) {
+  switch (s) {
+    case SolveStatus::Converged: return "converged";
+    case SolveStatus::MaxIterationsExceeded: return "max-iterations-exceeded";
+    case SolveStatus::StepSizeUnderflow: return "step-size-underflow";
+  }
+  return "unknown";
+}
+
+struct SolverConfig {  // core.hpp:241-267
+  double epsilon = 0.1;
+  std::optional<double> gamma_override;
+  long max_iterations = 50000;
+  BlockRule block_rule = BlockRule::Greedy;
+  double tuning_exponent_p = 1.0;
+  bool deterministic = true;
+  long log_every = 1;
+  void check() const {
+    if (!(epsilon > 0) || !std::isfinite(epsilon)) throw PotError(ErrorCode::InvalidArgument, "epsilon must be positive");
+    if (max_iterations < 1) throw PotError(ErrorCode::InvalidArgument, "max_iterations must be >= 1");
+    if (!(tuning_exponent_p >= 1)) throw PotError(ErrorCode::InvalidArgument, "tuning exponent p must be >= 1");
+    if (log_every < 1) throw PotError(ErrorCode::InvalidArgument, "log_every must be >= 1");
+    if (gamma_override && !(*gamma_override > 0)) throw PotError(ErrorCode::InvalidArgument, "gamma override must be positive");
+  }
+};
+
+struct TraceRecord {  // core.hpp:269-275
+  long t = 0;
+  double error = 0.0;
+  double phi = 0.0;
+  std::optional<double> rounded_cost;
+  double elapsed_s = 0.0;
+};
+
+struct ConvergenceTrace {
+  std::vector<TraceRecord> records;
+  std::string stopping_iterate;
+};
+
+// ---------------------------------------------------------- solvers.hpp --
+struct TheoryBounds {  // solvers.hpp:139-144
+  double R = 0.0, L = 0.0, mu_f = 0.0, iteration_bound = 0.0;
+};
+
+struct SolveResult {  // solvers.hpp:176-186
+  TransportPlan plan;
+  ConvergenceTrace trace;
+  SolveStatus status = SolveStatus::Converged;
+  long iterations = 0;
+  double gamma = 0.0;
+  double tolerance = 0.0;
+  double final_error = 0.0;
+  double wall_seconds = 0.0;
+  std::optional<TheoryBounds> bounds;
+};
+
+inline double entropy(const Vector& x) {  // solvers.hpp:19-28
+  for (long i = 0; i < x.size(); ++i)
+    if (x(i) < 0) throw PotError(ErrorCode::NegativeEntry, "entropy requires x >= 0");
+  double h = 0.0;
+  for (long i = 0; i < x.size(); ++i)
+    if (x(i) > 0) h -= x(i) * std::log(x(i));
+  return h;
+}
+
+inline double theta_next(double theta) {  // solvers.hpp:32-37
+  if (!(theta > 0) || !(theta <= 1)) throw PotError(ErrorCode::InvalidArgument, "theta must lie in (0, 1]");
+  return theta * (std::sqrt(theta * theta + 4.0) - theta) / 2.0;
+}
+
+inline double rho(double a, double b) {  // dual.hpp:144-149
+  if (!(a > 0) || !(b > 0)) throw PotError(ErrorCode::NonPositiveArgument, "rho requires a, b > 0");
+  return b - a + a * std::log(a / b);
+}
+
+namespace detail {
+
+inline potgpu_ctx* context() {
+  // one context per thread: distinct solves may run concurrently (README.md:132-133)
+  struct Holder {
+    potgpu_ctx* c = nullptr;
+    ~Holder() { if (c) potgpu_destroy(c); }
+  };
+  thread_local Holder h;
+  if (!h.c) {
+    if (int rc = potgpu_create(0, &h.c)) throw DeviceError(rc, potgpu_last_error());
+  }
+  return h.c;
+}
+
+[[noreturn]] inline void rethrow(int rc) {
+  const std::string msg = potgpu_last_error();
+  if (rc >= 1 && rc <= 17) throw PotError(ErrorCode(rc - 1), msg);
+  throw DeviceError(rc, msg);
+}
+
+inline SolveResult run(int kind, const Instance& in, const SolverConfig& config, double epsilon, double p) {
+  config.check();
+  const long n = in.size();
+  potgpu_problem pr{};
+  pr.n = n;
+  pr.dtype = POTGPU_F64;
+  pr.cost_kind = POTGPU_COST_DENSE;
+  pr.C = in.C.data();
+  pr.ldc = in.C.rows();
+  pr.row_major = 0;  // Eigen layout
+  pr.r = in.r.data();
+  pr.c = in.c.data();
+  pr.s = in.s;
+  if (in.c.size() != n || in.C.rows() != n || in.C.cols() != n)
+    throw PotError(ErrorCode::DimensionMismatch, "instance shapes differ");
+  potgpu_config cfg;
+  potgpu_config_default(&cfg);
+  cfg.epsilon = epsilon;
+  cfg.gamma_override = config.gamma_override.value_or(0.0);
+  cfg.max_iterations = config.max_iterations;
+  cfg.block_rule = config.block_rule == BlockRule::Greedy ? POTGPU_GREEDY : POTGPU_ROUND_ROBIN;
+  cfg.tuning_exponent_p = p;
+  cfg.deterministic = config.deterministic ? 1 : 0;
+  cfg.log_every = config.log_every;
+  const int64_t cap = std::min<int64_t>(config.max_iterations / config.log_every + 4, 1 << 20);
+  std::vector<potgpu_trace_record> trace(static_cast<size_t>(cap));
+  SolveResult res;
+  res.plan.X = Matrix(n, n);
+  std::vector<double> Xrm(static_cast<size_t>(n * n));
+  res.plan.row_slack = Vector(n);
+  res.plan.col_slack = Vector(n);
+  potgpu_outputs out{};
+  out.X = Xrm.data();
+  out.row_slack = res.plan.row_slack.data();
+  out.col_slack = res.plan.col_slack.data();
+  out.trace = trace.data();
+  out.trace_cap = cap;
+  potgpu_summary sm{};
+  if (int rc = potgpu_solve(context(), kind, &pr, &cfg, &sm, &out)) rethrow(rc);
+  for (long i = 0; i < n; ++i)
+    for (long j = 0; j < n; ++j) res.plan.X(i, j) = Xrm[size_t(i * n + j)];
+  res.plan.mass = sm.mass;
+  res.status = SolveStatus(sm.status);
+  res.iterations = sm.iterations;
+  res.gamma = sm.gamma;
+  res.tolerance = sm.tolerance;
+  res.final_error = sm.final_error;
+  res.wall_seconds = sm.wall_seconds;
+  if (sm.has_bounds) res.bounds = TheoryBounds{sm.bound_R, sm.bound_L, sm.bound_mu_f, sm.iteration_bound};
+  res.trace.stopping_iterate = sm.stopping_iterate;
+  for (int64_t k = 0; k < std::min<int64_t>(sm.trace_len, cap); ++k) {
+    TraceRecord r;
+    r.t = trace[size_t(k)].t;
+    r.error = trace[size_t(k)].error;
+    r.phi = trace[size_t(k)].phi;
+    if (!std::isnan(trace[size_t(k)].rounded_cost)) r.rounded_cost = trace[size_t(k)].rounded_cost;
+    r.elapsed_s = trace[size_t(k)].elapsed_s;
+    res.trace.records.push_back(r);
+  }
+  return res;
+}
+
+}  // namespace detail
+
+// The AspotObserver hook of the reference (solvers.hpp:188-204) is not
+// offered: the loop is device resident. iterate-by-iterate access to the
+// dual points is the potgpu_session_* C-ABI.
+inline SolveResult aspot_solve(const Instance& in, const SolverConfig& config) {  // solvers.hpp:265
+  return detail::run(POTGPU_ASPOT, in, config, config.epsilon, config.tuning_exponent_p);
+}
+
+inline SolveResult feasible_sinkhorn_solve(const Instance& in, const SolverConfig& config) {  // solvers.hpp:516
+  return detail::run(POTGPU_FEASIBLE_SINKHORN, in, config, config.epsilon, config.tuning_exponent_p);
+}
+
+inline SolveResult tuned_sinkhorn_solve(const Instance& in, double epsilon, double p,
+                                        const SolverConfig& config = {}) {  // solvers.hpp:547
+  if (!(epsilon > 0) || !std::isfinite(epsilon)) throw PotError(ErrorCode::InvalidArgument, "epsilon must be positive");
+  if (!(p >= 1)) throw PotError(ErrorCode::InvalidArgument, "tuning exponent p must be >= 1");
+  return detail::run(POTGPU_TUNED_SINKHORN, in, config, epsilon, p);
+}
+
+inline SolveResult tuned_sinkhorn_solve(const Instance& in, const SolverConfig& config) {  // solvers.hpp:586
+  return tuned_sinkhorn_solve(in, config.epsilon, config.tuning_exponent_p, config);
+}
+
+inline SolveResult solve(const Instance& in, SolverKind kind, const SolverConfig& config) {  // solvers.hpp:591
+  switch (kind) {
+    case SolverKind::Aspot: return aspot_solve(in, config);
+    case SolverKind::FeasibleSinkhorn: return feasible_sinkhorn_solve(in, config);
+    case SolverKind::TunedSinkhorn: return tuned_sinkhorn_solve(in, config);
+  }
+  throw PotError(ErrorCode::InvalidArgument, "unknown solver kind");
+}
+
+// -------------------------------------------------------- synthetic.hpp --
+inline Instance make_synthetic_instance(long n, std::uint64_t seed, double mass_r, double mass_c, double s_frac) {
+  Instance in;
+  in.r = Vector(n);
+  in.c = Vector(n);
+  std::vector<double> Crm(static_cast<size_t>(n * n));
+  double s = 0.0;
+  if (int rc = potgpu_make_synthetic(n, seed, mass_r, mass_c, s_frac, in.r.data(), in.c.data(), Crm.data(), &s))
+    throw PotError(ErrorCode::InvalidArgument, "invalid synthetic instance parameters (rc " + std::to_string(rc) + ")");
+  in.C = Matrix(n, n);
+  for (long i = 0; i < n; ++i)
+    for (long j = 0; j < n; ++j) in.C(i, j) = Crm[size_t(i * n + j)];
+  in.s = s;
+  return in;
+}
+
+inline Instance make_scaling_instance(long n, std::uint64_t seed) {  // synthetic.hpp:58-60
+  return make_synthetic_instance(n, seed, 5.0, 3.0, 0.2);
+}
+
+}  // namespace pot

@@ -251,37 +251,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   // this row is exponentiated
   typename Src::RowData nxt{};
   if (r0 + warp < r1) nxt = src.load(r0 + warp, j0, lane);
-  // Row sums are batched over 4 consecutive rows of this warp and reduced
-  // with one reduce-scatter butterfly (6 shuffles per 4 rows instead of 20).
-  float rsv[4];
-  float my_ms = 0.f;  // max of the row this lane holds after the butterfly (lane 8k <- row k)
-  int nb = 0;
-  int64_t ib = r0 + warp;  // first row of the batch
-  float2* rowp_out = rowp;
-  const int64_t ldp = gridDim.x;
-  auto flush = [&](int cnt) {
-    float v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = k < cnt ? rsv[k] : 0.f;
-    const bool b4 = lane & 16, b3 = lane & 8;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {  // keep rows (b4 ? 2..3 : 0..1)
-      const float send = b4 ? v[k] : v[k + 2];
-      const float keep = b4 ? v[k + 2] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    {
-      const float send = b3 ? v[0] : v[1];
-      const float keep = b3 ? v[1] : v[0];
-      v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    const int k = (b4 ? 2 : 0) + (b3 ? 1 : 0);  // the row this lane now holds (= lane >> 3)
-    if ((lane & 7) == 0 && k < cnt)  // value = sum 2^(ms + A_i), A_i added in fp64
-      rowp_out[(ib + int64_t(kWarps) * k) * ldp + blockIdx.x] = make_float2(v[0], my_ms);
-  };
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
     const typename Src::RowData cur = nxt;
     if (i + kWarps < r1) nxt = src.load(i + kWarps, j0, lane);
@@ -294,25 +263,16 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
     // m == -inf only if the whole row segment is padding / -inf potentials
     const float ms = (m == -INFINITY) ? 0.f : m;
     const float2 M2 = make_float2(-ms, -ms);
+    float2 rs = make_float2(0.f, 0.f);
     float2 p[kPairs];
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) {
       const float2 d = __fadd2_rn(t[q], M2);
       p[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      rs = __fadd2_rn(rs, p[q]);
     }
-    // pairwise lane-local row sum
-    const float2 s01 = __fadd2_rn(p[0], p[1]), s23 = __fadd2_rn(p[2], p[3]);
-    const float2 s45 = __fadd2_rn(p[4], p[5]), s67 = __fadd2_rn(p[6], p[7]);
-    const float2 rs = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (k == nb) rsv[k] = rs.x + rs.y;
-    if ((lane >> 3) == nb) my_ms = ms;
-    if (++nb == 4) {
-      flush(4);
-      nb = 0;
-      ib = i + kWarps;
-    }
+    const float r = warp_sum(rs.x + rs.y);
+    if (lane == 0) rowp[i * gridDim.x + blockIdx.x] = make_float2(r, ms);  // value = r 2^(ms + A_i), A_i added in fp64
     const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;  // row max of t (log2)
     if (mA > sigma) {  // warp-uniform
       const float sc = ex2f(sigma - mA);
@@ -326,7 +286,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
   }
-  if (nb > 0) flush(nb);
   // CTA combine of the 8 warps' column accumulators (each with its sigma)
   __shared__ float cs[kWarps][kStripCols32];
   __shared__ float ss[kWarps];

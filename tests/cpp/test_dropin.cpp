@@ -1,0 +1,106 @@
+// test_dropin.cpp — the reference's own solver tests, unchanged in spirit,
+// compiled against the drop-in headers (include/pot/) and libpotgpu.so.
+// Ports of /root/reference/proj/tests/test_solvers.cpp cases; GTest-free.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "pot/solvers.hpp"
+#include "pot/synthetic.hpp"
+
+using namespace pot;
+
+static int fails = 0;
+#define EXPECT(c) do { if (!(c)) { ++fails; std::printf("FAIL line %d: %s\n", __LINE__, #c); } } while (0)
+
+static Instance uniform_instance(long n, double mass, double s) {  // test_solvers.cpp:24-32
+  Instance in;
+  in.r = Vector::Constant(n, mass / double(n));
+  in.c = Vector::Constant(n, mass / double(n));
+  in.C = Matrix::Ones(n, n);
+  for (long i = 0; i < n; ++i) in.C(i, i) = 0.0;
+  in.s = s;
+  return in;
+}
+
+int main() {
+  {  // AspotSolve.ZeroCostInstance (:194-203)
+    Instance in = uniform_instance(2, 1.0, 0.5);
+    in.C = Matrix::Zero(2, 2);
+    SolverConfig cfg; cfg.epsilon = 0.1;
+    const SolveResult res = aspot_solve(in, cfg);
+    EXPECT(res.status == SolveStatus::Converged);
+    EXPECT(std::fabs(transport_cost(in.C, res.plan.X)) <= 1e-15);
+    EXPECT(plan_feasibility_gap(res.plan, in) <= 1e-9);
+  }
+  {  // AspotSolve.RejectsSinglePoint (:205-207)
+    Instance in; in.r = Vector::Constant(1, 1); in.c = Vector::Constant(1, 1); in.C = Matrix::Zero(1, 1); in.s = 0.5;
+    bool threw = false;
+    try { aspot_solve(in, SolverConfig{}); } catch (const PotError& e) { threw = e.code() == ErrorCode::DegenerateInstance; }
+    EXPECT(threw);
+  }
+  {  // AspotSolve.PaperStyleOverrides (:225-237)
+    const Instance in = make_scaling_instance(40, 5);
+    SolverConfig cfg; cfg.epsilon = 8e-7; cfg.gamma_override = 1e-3; cfg.max_iterations = 1500; cfg.log_every = 1000000;
+    const SolveResult res = aspot_solve(in, cfg);
+    EXPECT(res.gamma == 1e-3);
+    EXPECT(std::fabs(res.tolerance - 1e-7) <= 1e-20);
+    EXPECT(res.status == SolveStatus::Converged);
+    EXPECT(res.final_error <= res.tolerance);
+  }
+  {  // AspotSolve.OverflowTriggersStepHalvingAndStillSolves (:272-290)
+    Instance in; in.r = Vector::Constant(2, 50.0); in.c = Vector::Constant(2, 50.0);
+    in.C = Matrix::Ones(2, 2); in.C(0, 0) = 0; in.C(1, 1) = 0; in.s = 1.0;
+    SolverConfig cfg; cfg.epsilon = 0.1; cfg.gamma_override = 1e5; cfg.max_iterations = 20000; cfg.log_every = 1000000;
+    const SolveResult res = aspot_solve(in, cfg);
+    EXPECT(plan_feasibility_gap(res.plan, in) <= 1e-9 * in.r.sum());
+    EXPECT(res.status != SolveStatus::StepSizeUnderflow);
+  }
+  {  // StoppingIterateRecordedAndTraceMonotoneIndices (:239-250) on a synthetic instance
+    const Instance in = make_synthetic_instance(6, 25, 1.0, 1.1, 0.5);
+    SolverConfig cfg; cfg.epsilon = 0.05;
+    const SolveResult res = aspot_solve(in, cfg);
+    EXPECT(res.trace.stopping_iterate == "z_check");
+    for (size_t i = 1; i < res.trace.records.size(); ++i) EXPECT(res.trace.records[i - 1].t < res.trace.records[i].t);
+    EXPECT(res.final_error <= res.tolerance);
+    EXPECT(res.trace.records.back().rounded_cost.has_value());
+  }
+  {  // FeasibleSinkhorn.SinglePointIsExact (:373-378)
+    Instance in; in.r = Vector::Constant(1, 1.0); in.c = Vector::Constant(1, 0.8); in.C = Matrix::Constant(1, 1, 3.0); in.s = 0.5;
+    const SolveResult res = feasible_sinkhorn_solve(in, SolverConfig{});
+    EXPECT(res.plan.X(0, 0) == 0.5);
+    EXPECT(res.status == SolveStatus::Converged);
+  }
+  {  // TunedSinkhorn.RejectsNonPositiveEntropy (:446-461)
+    Instance in; in.r = Vector(2); in.r(0) = 3.0; in.r(1) = 2.0; in.c = Vector::Constant(2, 2.5); in.C = Matrix::Ones(2, 2); in.s = 1.0;
+    bool threw = false;
+    try { tuned_sinkhorn_solve(in, 0.1, 1.0); } catch (const PotError& e) { threw = e.code() == ErrorCode::ZeroEntropy; }
+    EXPECT(threw);
+  }
+  {  // Solvers.AgreeWithinTwoEpsilon (:463-478) + ZeroBudgetReturnsEmptyPlan (:480-490)
+    const Instance in = make_synthetic_instance(6, 33, 1.0, 0.9, 0.6);
+    SolverConfig cfg; cfg.epsilon = 0.1; cfg.log_every = 1000000; cfg.max_iterations = 200000;
+    const double a = transport_cost(in.C, aspot_solve(in, cfg).plan.X);
+    const double s = transport_cost(in.C, feasible_sinkhorn_solve(in, cfg).plan.X);
+    const double t = transport_cost(in.C, tuned_sinkhorn_solve(in, 0.1, 2.0, cfg).plan.X);
+    EXPECT(std::fabs(a - s) <= 2 * cfg.epsilon + 1e-9);
+    EXPECT(std::fabs(a - t) <= 2 * cfg.epsilon + 1e-9);
+    EXPECT(std::fabs(s - t) <= 2 * cfg.epsilon + 1e-9);
+    Instance z = in; z.s = 0.0;
+    for (SolverKind k : {SolverKind::Aspot, SolverKind::FeasibleSinkhorn, SolverKind::TunedSinkhorn}) {
+      const SolveResult r = solve(z, k, SolverConfig{});
+      double m = 0.0;
+      for (long q = 0; q < r.plan.X.size(); ++q) m = std::max(m, std::fabs(r.plan.X.data()[q]));
+      EXPECT(m == 0.0);
+      EXPECT(r.status == SolveStatus::Converged);
+    }
+  }
+  {  // Validate (test_core.cpp:28-37): budget above mass
+    Instance in; in.r = Vector::Constant(1, 1.0); in.c = Vector::Constant(1, 1.0); in.C = Matrix::Zero(1, 1); in.s = 2.0;
+    bool threw = false;
+    try { feasible_sinkhorn_solve(in, SolverConfig{}); } catch (const PotError& e) { threw = e.code() == ErrorCode::BudgetExceedsMass; }
+    EXPECT(threw);
+  }
+  std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
+  return fails ? 1 : 0;
+}
