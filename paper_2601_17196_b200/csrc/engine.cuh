@@ -103,7 +103,11 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.strip = P.dtype == POTGPU_F64 ? kStripCols : kStripCols32;
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
   ws.g = choose_grid(n, cx.num_sms, occ, ws.strip);
-  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : size_t(ws.g.rows_per_cta) * sizeof(float);
+  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : sweep_f32_smem(ws.g.rows_per_cta);
+  if (P.dtype != POTGPU_F64) {
+    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcPointsF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+  }
   ws.nstrips = ws.g.grid.x;
   ws.nrb = ws.g.grid.y;
   ws.nblk = int(std::min<int64_t>(cx.num_sms, std::max<int64_t>(1, ceil_div(n, kVecThreads))));

@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __r
 // take p_ij 2^(m_i - sigma). Partials leave as fp32 (sum, log2 scale) pairs
 // and are turned into fp64 values by the reduce kernels, so the hot loop has
 // no fp64 work at all.
-constexpr int kStripCols32 = 512;
-constexpr int kPairs = 8;  // 16 columns per lane as 8 float2 pairs
+constexpr int kPairs = 8;  // columns per lane / 2 (float2 pairs)
+constexpr int kStripCols32 = 64 * kPairs;  // columns per warp strip
 
 // Lane column map: pair q (0..7), half h: j = j0 + 4*lane + 128*(q>>1) + 2*(q&1) + h.
 __device__ __forceinline__ int64_t f32_col(int64_t j0, int lane, int q, int h) {
@@ -140,13 +140,13 @@ struct SrcDenseF32 {
   int64_t ld;
   float g2;  // log2(e) / gamma
   struct Col {};
-  struct RowData { float4 c[4]; };  // the lane's 16 entries of one row
+  struct RowData { float4 c[kPairs / 2]; };  // the lane's 2*kPairs entries of one row
   static constexpr bool kHasCols = false;
   __device__ __forceinline__ RowData load(int64_t i, int64_t j0, int lane) const {
     const float4* p = reinterpret_cast<const float4*>(C + i * ld + j0) + lane;
     RowData d;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) d.c[k] = __ldcs(p + 32 * k);
+    for (int k = 0; k < kPairs / 2; ++k) d.c[k] = __ldcs(p + 32 * k);
     return d;
   }
   // t' = B_j - g2 * C for the lane's 16 columns (the row potential is
@@ -154,7 +154,7 @@ struct SrcDenseF32 {
   __device__ __forceinline__ void expo(const RowData& d, const Col*, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
     const float2 g = make_float2(-g2, -g2);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kPairs / 2; ++k) {
       t[2 * k] = __ffma2_rn(g, make_float2(d.c[k].x, d.c[k].y), B[2 * k]);
       t[2 * k + 1] = __ffma2_rn(g, make_float2(d.c[k].z, d.c[k].w), B[2 * k + 1]);
     }
@@ -182,6 +182,13 @@ struct SrcPointsF32 {
     }
   }
 };
+
+// Dynamic shared memory of the fp32 sweep: row potentials (rows_per_cta
+// floats, padded to 16 B) then 8 per-warp 32x33 row-sum tiles.
+__host__ __device__ constexpr int kRowTileOffset(int rows_per_cta) { return (rows_per_cta + 3) & ~3; }
+__host__ __device__ constexpr size_t sweep_f32_smem(int rows_per_cta) {
+  return size_t(kRowTileOffset(rows_per_cta) + kWarps * 32 * 33) * sizeof(float);
+}
 
 // Partial formats understood by the reduce kernels: fp64 values, or fp32
 // (sum, log2 scale) pairs whose scale is relative to a per-row fp64 offset
@@ -247,10 +254,31 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   float sigma = -INFINITY;  // running column scale (log2) of this warp
   float mmax = -INFINITY;
   float2* rowp = reinterpret_cast<float2*>(a.rowp);  // [row][strip]
+  (void)rowp;
   // one-row-ahead software pipeline: the next row's data is in flight while
   // this row is exponentiated
   typename Src::RowData nxt{};
   if (r0 + warp < r1) nxt = src.load(r0 + warp, j0, lane);
+  // Row sums: each lane parks its lane-local sum of a row in a per-warp
+  // shared tile (32 rows x 33, conflict-free); every 32 rows lane L reduces
+  // row L of the tile. No shuffle chain inside the row loop.
+  float* tile = s_A + kRowTileOffset(a.rows_per_cta) + warp * (32 * 33);
+  float my_ms = 0.f;  // max of tile row `lane`
+  int slot = 0;
+  int64_t ib = r0 + warp;  // first row of the tile
+  const int64_t ldp = gridDim.x;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      // value = sum 2^(ms + A_i); A_i is added in fp64 by the reduce kernels
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+    }
+    __syncwarp();
+  };
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
     const typename Src::RowData cur = nxt;
     if (i + kWarps < r1) nxt = src.load(i + kWarps, j0, lane);
@@ -258,21 +286,29 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
     float2 t[kPairs];
     src.expo(cur, cols, Bj, t);  // t' = t - A_i
     float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
-    m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[4].x, t[4].y), fmaxf(t[5].x, t[5].y)), fmaxf(fmaxf(t[6].x, t[6].y), fmaxf(t[7].x, t[7].y))));
+#pragma unroll
+    for (int q = 4; q < kPairs; q += 4)
+      m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[q].x, t[q].y), fmaxf(t[q + 1].x, t[q + 1].y)), fmaxf(fmaxf(t[q + 2].x, t[q + 2].y), fmaxf(t[q + 3].x, t[q + 3].y))));
     m = warp_maxf(m);
     // m == -inf only if the whole row segment is padding / -inf potentials
     const float ms = (m == -INFINITY) ? 0.f : m;
     const float2 M2 = make_float2(-ms, -ms);
-    float2 rs = make_float2(0.f, 0.f);
     float2 p[kPairs];
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) {
       const float2 d = __fadd2_rn(t[q], M2);
       p[q] = make_float2(ex2f(d.x), ex2f(d.y));
-      rs = __fadd2_rn(rs, p[q]);
     }
-    const float r = warp_sum(rs.x + rs.y);
-    if (lane == 0) rowp[i * gridDim.x + blockIdx.x] = make_float2(r, ms);  // value = r 2^(ms + A_i), A_i added in fp64
+    float2 rs = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
+#pragma unroll
+    for (int q = 4; q < kPairs; q += 4) rs = __fadd2_rn(rs, __fadd2_rn(__fadd2_rn(p[q], p[q + 1]), __fadd2_rn(p[q + 2], p[q + 3])));
+    tile[slot * 33 + lane] = rs.x + rs.y;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      ib = i + kWarps;
+    }
     const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;  // row max of t (log2)
     if (mA > sigma) {  // warp-uniform
       const float sc = ex2f(sigma - mA);
@@ -286,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
   }
+  if (slot > 0) flush(slot);
   // CTA combine of the 8 warps' column accumulators (each with its sigma)
   __shared__ float cs[kWarps][kStripCols32];
   __shared__ float ss[kWarps];
