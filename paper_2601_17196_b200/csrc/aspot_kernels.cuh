@@ -50,6 +50,8 @@ struct AspotCtl {
   int fatal;      // potgpu error code raised on the device (0 = none)
   int record_rounded_cost;
   int paused;     // loop stopped at pause_at (session API), not finished
+  // sweep-vs-scale gates of z_hat and z_check' (block w: B scales by e^dw)
+  int g_hat_sweep, g_hat_scaled, g_new_sweep, g_new_scaled;
   int64_t pause_at;
   int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
   int64_t trace_len, trace_cap, log_len, log_cap;
@@ -89,6 +91,12 @@ struct ReduceArgs {
   double* scratch;                      // [gridDim.x][kNumPartials + 1]
   const int* gate;
   int pfmt;                             // PartialFormat of rowp/colp
+  // mode 1: no sweep; the point differs from a source point only in w, so
+  // B = B(src) e^(w - w_src): sums are scaled (source b when *select_b).
+  int mode;
+  const double* src_row_a; const double* src_col_a; const double* src_w_a; int src_role_a;
+  const double* src_row_b; const double* src_col_b; const double* src_w_b; int src_role_b;
+  const int* select_b;
 };
 
 __device__ __forceinline__ bool is_max_slot(int k) { return k == 1 || k == 2 || k == 11; }
@@ -103,7 +111,7 @@ __device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) { 
 }
 
 // Scalar finalisation + the decision the reference takes at that point.
-__device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPartials + 1], double w) {
+__device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPartials + 1], double w, bool swept) {
   PointScalars ps;
   ps.total = acc[0]; ps.maxu = acc[1]; ps.maxv = acc[2]; ps.seu = acc[3]; ps.sev = acc[4];
   ps.ur = acc[5]; ps.vc = acc[6]; ps.score_u = acc[7]; ps.score_v = acc[8]; ps.gl1u = acc[9]; ps.gl1v = acc[10];
@@ -114,7 +122,7 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
   ps.overflow = !(ps.maxe <= kMaxExponent) || !(ps.maxu <= kMaxExponent) || !(ps.maxv <= kMaxExponent) || (w != w);
   ps.pad = 0;
   ctl->ps[role] = ps;
-  ctl->sweeps += 1;
+  if (swept) ctl->sweeps += 1;
   switch (role) {
     case R_BAR:
       if (ps.overflow) { ctl->zbar_failed = 1; ctl->g_alive = 0; }
@@ -122,6 +130,8 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
     case R_GRAVE:
       if (ps.overflow) { ctl->g_alive = 0; break; }
       ctl->block_hat = ctl->block_rule == POTGPU_ROUND_ROBIN ? int(ctl->gk_calls % 3) : greedy_block(ps, ctl->s);
+      ctl->g_hat_sweep = ctl->block_hat != 2;
+      ctl->g_hat_scaled = ctl->block_hat == 2;
       break;
     case R_HAT: {
       if (ps.overflow) { ctl->g_alive = 0; break; }
@@ -131,6 +141,8 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
       ctl->phi_best = fmin(ctl->phi_check, ps.phi);
       const PointScalars& pb = keep ? ctl->ps[R_CHECK] : ps;
       ctl->block_check = ctl->block_rule == POTGPU_ROUND_ROBIN ? int((ctl->gk_calls + 1) % 3) : greedy_block(pb, ctl->s);
+      ctl->g_new_sweep = ctl->block_check != 2;
+      ctl->g_new_scaled = ctl->block_check == 2;
       break;
     }
     case R_NEW:
@@ -205,14 +217,25 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   const int q = threadIdx.x % kTPI;
   const int64_t per_block = kEvalThreads / kTPI;
   const int64_t span = int64_t(gridDim.x) * per_block;
+  const bool useb = a.mode == 1 && a.select_b && *a.select_b;
+  const double* srow = useb ? a.src_row_b : a.src_row_a;
+  const double* scol = useb ? a.src_col_b : a.src_col_a;
+  const double dw = a.mode == 1 ? w - *(useb ? a.src_w_b : a.src_w_a) : 0.0;
+  const double fs = a.mode == 1 ? exp(dw) : 1.0;
   // all threads iterate the same number of times (the shuffles need the full warp)
   for (int64_t i0 = int64_t(blockIdx.x) * per_block; i0 < n; i0 += span) {
     const int64_t i = i0 + threadIdx.x / kTPI;
     const bool live = i < n;
     const int64_t ii = live ? i : n - 1;
     const double ui = u[ii], vi = v[ii];
-    const double rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, (ui + w) * kLog2e, q);
-    const double cb = group_partial_sum(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
+    double rb, cb;
+    if (a.mode == 0) {
+      rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, (ui + w) * kLog2e, q);
+      cb = group_partial_sum(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
+    } else {
+      rb = srow[ii] * fs;
+      cb = scol[ii] * fs;
+    }
     if (!live || q != 0) continue;
     a.row_out[i] = rb;
     a.col_out[i] = cb;
@@ -230,8 +253,9 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     acc[9] += fabs(rowf - a.rt[i]);
     acc[10] += fabs(colf - a.ct[i]);
   }
-  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
-    acc[11] = nan_max(acc[11], a.maxp[k]);
+  if (a.mode == 0)
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
+      acc[11] = nan_max(acc[11], a.maxp[k]);
   __shared__ double sh[kNumPartials + 1][kEvalThreads];
   __shared__ bool last;
   auto block_reduce = [&]() {
@@ -273,7 +297,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
 #pragma unroll
     for (int k = 0; k < kNumPartials + 1; ++k) tot[k] = sh[k][0];
     *ticket = 0u;  // ready for the next launch
-    apply_role(ctl, role, tot, w);
+    if (a.mode == 1) tot[11] = ctl->ps[useb ? a.src_role_b : a.src_role_a].maxe + dw;  // max exponent shifts by dw
+    apply_role(ctl, role, tot, w, a.mode == 0);
   }
 }
 
@@ -334,7 +359,10 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
     dst.base[k] = x;
     finite = finite && isfinite(x);
   }
-  if (!finite) ctl->g_alive = 0;  // solvers.hpp:83-87: non-finite update -> Overflow
+  if (!finite) {  // solvers.hpp:83-87: non-finite update -> Overflow
+    ctl->g_alive = 0;
+    ctl->g_hat_sweep = ctl->g_hat_scaled = ctl->g_new_sweep = ctl->g_new_scaled = 0;
+  }
 }
 
 // Commit of an accepted attempt: z <- z_best, z_check <- z_check', sums of
@@ -365,7 +393,12 @@ __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double e
   ctl->trace_len += 1;
 }
 
+__device__ void reset_point_gates(AspotCtl* ctl) {
+  ctl->g_hat_sweep = ctl->g_hat_scaled = ctl->g_new_sweep = ctl->g_new_scaled = 0;
+}
+
 __device__ void begin_iteration(AspotCtl* ctl) {
+  reset_point_gates(ctl);
   ctl->halvings = 0;
   ctl->step = ctl->gamma / (ctl->step_denom * ctl->theta);  // solvers.hpp:328
   ctl->g_new = 1;
@@ -413,6 +446,7 @@ __global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
     // halving loop (solvers.hpp:334-356): z_bar/grad failures repeat on every
     // retry, so they exhaust the 61 tries immediately.
     if (ctl->zbar_failed || ctl->halvings >= 60) { finish(ctl, POTGPU_STEP_SIZE_UNDERFLOW); return; }
+    reset_point_gates(ctl);
     ctl->halvings += 1;
     ctl->step *= 0.5;
     ctl->g_new = 0;

@@ -369,7 +369,7 @@ struct AspotSession : Session {
   Setup st;
   cudaGraphExec_t exec = nullptr;
   int64_t trace_cap = 1, log_cap = 0;
-  static constexpr int64_t kKernelsPerAttempt = 14;
+  static constexpr int64_t kKernelsPerAttempt = 16;
   int64_t graph_nodes = kKernelsPerAttempt;
   explicit AspotSession(Context& c) : Session(c) {}
   ~AspotSession() override {
@@ -390,12 +390,26 @@ struct AspotSession : Session {
     launch_eval(cx, ws, ZG, R_GRAVE, &ctl->g_alive);
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
                                                    ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
-    launch_sweep(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_eval(cx, ws, ZH, R_HAT, &ctl->g_alive);
+    // z_hat: a sweep, or (block w, ~all iterations) B(z_grave) scaled by e^dw
+    launch_sweep(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma);
+    launch_eval(cx, ws, ZH, R_HAT, &ctl->g_hat_sweep);
+    {
+      ReduceArgs sc{};
+      sc.src_row_a = ws.row(R_GRAVE); sc.src_col_a = ws.col(R_GRAVE); sc.src_w_a = ZG.w(); sc.src_role_a = R_GRAVE;
+      launch_eval(cx, ws, ZH, R_HAT, &ctl->g_hat_scaled, &sc);
+    }
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
                                                    ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
-    launch_sweep(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_eval(cx, ws, ZN, R_NEW, &ctl->g_alive);
+    // z_check' = GK(z_best): a sweep, or (block w) B(z_best) scaled
+    launch_sweep(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma);
+    launch_eval(cx, ws, ZN, R_NEW, &ctl->g_new_sweep);
+    {
+      ReduceArgs sc{};
+      sc.src_row_a = ws.row(R_HAT); sc.src_col_a = ws.col(R_HAT); sc.src_w_a = ZH.w(); sc.src_role_a = R_HAT;
+      sc.src_row_b = ws.row(R_CHECK); sc.src_col_b = ws.col(R_CHECK); sc.src_w_b = ZC.w(); sc.src_role_b = R_CHECK;
+      sc.select_b = &ctl->keep_check;
+      launch_eval(cx, ws, ZN, R_NEW, &ctl->g_new_scaled, &sc);
+    }
     k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
                                                      ws.col(R_NEW));
     k_commit_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p, ws.iterlog.p);

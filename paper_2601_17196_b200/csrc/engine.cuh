@@ -160,8 +160,9 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
 }
 
 // The per-point evaluation (partials -> B 1, B^T 1, scalars, decision).
-inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int* gate) {
-  ReduceArgs r;
+inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int* gate, const ReduceArgs* scaled = nullptr) {
+  ReduceArgs r{};
+  if (scaled) r = *scaled;
   r.z = z;
   r.rowp = ws.rowp.p; r.nstrips = ws.nstrips;
   r.colp = ws.colp.p; r.nrowblocks = ws.nrb;
@@ -171,6 +172,7 @@ inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int*
   r.scratch = ws.scratch.p;
   r.gate = gate;
   r.pfmt = ws.pfmt;
+  r.mode = scaled ? 1 : 0;
   k_point_eval<<<ws.eval_blocks, kEvalThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());
 }

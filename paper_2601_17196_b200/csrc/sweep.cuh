@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   // shared tile (32 rows x 33, conflict-free); every 32 rows lane L reduces
   // row L of the tile. No shuffle chain inside the row loop.
   float* tile = s_A + kRowTileOffset(a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;  // &tile[slot][lane]
   float my_ms = 0.f;  // max of tile row `lane`
   int slot = 0;
   int64_t ib = r0 + warp;  // first row of the tile
@@ -302,11 +303,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
     float2 rs = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
 #pragma unroll
     for (int q = 4; q < kPairs; q += 4) rs = __fadd2_rn(rs, __fadd2_rn(__fadd2_rn(p[q], p[q + 1]), __fadd2_rn(p[q + 2], p[q + 3])));
-    tile[slot * 33 + lane] = rs.x + rs.y;
+    *tslot = rs.x + rs.y;
+    tslot += 33;
     if (lane == slot) my_ms = ms;
     if (++slot == 32) {
       flush(32);
       slot = 0;
+      tslot = tile + lane;
       ib = i + kWarps;
     }
     const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;  // row max of t (log2)
