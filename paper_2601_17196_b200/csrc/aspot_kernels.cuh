@@ -88,7 +88,7 @@ struct ReduceArgs {
   const double* maxp; int64_t nmax;
   double* row_out; double* col_out;
   const double* rt; const double* ct;  // marginals the dual targets (mixed r~, c~)
-  double* scratch;                      // [gridDim.x][kNumPartials + 1]
+  double* scratch;                      // [gridDim.x][kNumAcc]
   const int* gate;
   int pfmt;                             // PartialFormat of rowp/colp
   // mode 1: no sweep; the point differs from a source point only in w, so
@@ -100,6 +100,20 @@ struct ReduceArgs {
 };
 
 __device__ __forceinline__ bool is_max_slot(int k) { return k == 1 || k == 2 || k == 11; }
+__device__ __forceinline__ bool is_min_slot(int k) { return k == 12 || k == 13; }
+__device__ __forceinline__ double acc_init(int k) { return is_max_slot(k) ? -INFINITY : (is_min_slot(k) ? INFINITY : 0.0); }
+__device__ __forceinline__ double acc_join(int k, double x, double y) {
+  return is_max_slot(k) ? nan_max(x, y) : (is_min_slot(k) ? fmin(x, y) : x + y);
+}
+
+// Scaling shortcut guard: B(z + dw e_w) = B(z) e^dw holds entry-wise only
+// while no exponent meets the Eigen clamp (kExpLo); sums far above the
+// clamp floor on both sides make the clamp's contribution negligible.
+constexpr double kScaleSafeFloor = 1e-250;
+__device__ __forceinline__ bool scale_safe(const PointScalars& src, double s) {
+  const double m = fmin(src.minrow, src.mincol);
+  return m >= kScaleSafeFloor && m * (s / src.total) >= kScaleSafeFloor && src.total > 0;
+}
 
 __device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) {  // solvers.hpp:58-68
   const double su = ps.score_u, sv = ps.score_v, sw = rho_limit(s, ps.total);
@@ -111,11 +125,13 @@ __device__ __forceinline__ int greedy_block(const PointScalars& ps, double s) { 
 }
 
 // Scalar finalisation + the decision the reference takes at that point.
-__device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPartials + 1], double w, bool swept) {
+__device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc], double w, bool swept) {
   PointScalars ps;
   ps.total = acc[0]; ps.maxu = acc[1]; ps.maxv = acc[2]; ps.seu = acc[3]; ps.sev = acc[4];
   ps.ur = acc[5]; ps.vc = acc[6]; ps.score_u = acc[7]; ps.score_v = acc[8]; ps.gl1u = acc[9]; ps.gl1v = acc[10];
   ps.maxe = acc[11];
+  ps.minrow = acc[12];
+  ps.mincol = acc[13];
   // phi (dual.hpp:117-118): B.sum() + eu.sum() + ev.sum() - u.r - v.c - w s
   ps.phi = ((((ps.total + ps.seu) + ps.sev) - ps.ur) - ps.vc) - w * ctl->s;
   ps.err = (ps.gl1u + ps.gl1v) + fabs(ps.total - ctl->s);  // dual.hpp:138-141
@@ -130,8 +146,8 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
     case R_GRAVE:
       if (ps.overflow) { ctl->g_alive = 0; break; }
       ctl->block_hat = ctl->block_rule == POTGPU_ROUND_ROBIN ? int(ctl->gk_calls % 3) : greedy_block(ps, ctl->s);
-      ctl->g_hat_sweep = ctl->block_hat != 2;
-      ctl->g_hat_scaled = ctl->block_hat == 2;
+      ctl->g_hat_scaled = ctl->block_hat == 2 && scale_safe(ps, ctl->s);
+      ctl->g_hat_sweep = !ctl->g_hat_scaled;
       break;
     case R_HAT: {
       if (ps.overflow) { ctl->g_alive = 0; break; }
@@ -141,8 +157,8 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumPart
       ctl->phi_best = fmin(ctl->phi_check, ps.phi);
       const PointScalars& pb = keep ? ctl->ps[R_CHECK] : ps;
       ctl->block_check = ctl->block_rule == POTGPU_ROUND_ROBIN ? int((ctl->gk_calls + 1) % 3) : greedy_block(pb, ctl->s);
-      ctl->g_new_sweep = ctl->block_check != 2;
-      ctl->g_new_scaled = ctl->block_check == 2;
+      ctl->g_new_scaled = ctl->block_check == 2 && scale_safe(pb, ctl->s);
+      ctl->g_new_sweep = !ctl->g_new_scaled;
       break;
     }
     case R_NEW:
@@ -208,9 +224,9 @@ __device__ __forceinline__ double group_partial_sum(const double* p, int64_t bas
 __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.z.n;
-  double acc[kNumPartials + 1];
+  double acc[kNumAcc];
 #pragma unroll
-  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = is_max_slot(k) ? -INFINITY : 0.0;
+  for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_init(k);
   const double* u = a.z.u();
   const double* v = a.z.v();
   const double w = *a.z.w();
@@ -252,29 +268,31 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     acc[8] += rho_limit(a.ct[i], colf);
     acc[9] += fabs(rowf - a.rt[i]);
     acc[10] += fabs(colf - a.ct[i]);
+    acc[12] = fmin(acc[12], rb);
+    acc[13] = fmin(acc[13], cb);
   }
   if (a.mode == 0)
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
       acc[11] = nan_max(acc[11], a.maxp[k]);
-  __shared__ double sh[kNumPartials + 1][kEvalThreads];
+  __shared__ double sh[kNumAcc][kEvalThreads];
   __shared__ bool last;
   auto block_reduce = [&]() {
 #pragma unroll
-    for (int k = 0; k < kNumPartials + 1; ++k) sh[k][threadIdx.x] = acc[k];
+    for (int k = 0; k < kNumAcc; ++k) sh[k][threadIdx.x] = acc[k];
     __syncthreads();
     for (int stride = kEvalThreads / 2; stride > 0; stride >>= 1) {
       if (threadIdx.x < stride) {
 #pragma unroll
-        for (int k = 0; k < kNumPartials + 1; ++k) {
+        for (int k = 0; k < kNumAcc; ++k) {
           const double o = sh[k][threadIdx.x + stride];
-          sh[k][threadIdx.x] = is_max_slot(k) ? nan_max(sh[k][threadIdx.x], o) : sh[k][threadIdx.x] + o;
+          sh[k][threadIdx.x] = acc_join(k, sh[k][threadIdx.x], o);
         }
       }
       __syncthreads();
     }
   };
   block_reduce();
-  if (threadIdx.x < kNumPartials + 1) a.scratch[blockIdx.x * (kNumPartials + 1) + threadIdx.x] = sh[threadIdx.x][0];
+  if (threadIdx.x < kNumAcc) a.scratch[blockIdx.x * (kNumAcc) + threadIdx.x] = sh[threadIdx.x][0];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -283,19 +301,16 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   __threadfence();
   const volatile double* sc = a.scratch;
 #pragma unroll
-  for (int k = 0; k < kNumPartials + 1; ++k) acc[k] = is_max_slot(k) ? -INFINITY : 0.0;
+  for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_init(k);
   for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x)
 #pragma unroll
-    for (int k = 0; k < kNumPartials + 1; ++k) {
-      const double x = sc[b * (kNumPartials + 1) + k];
-      acc[k] = is_max_slot(k) ? nan_max(acc[k], x) : acc[k] + x;
-    }
+    for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_join(k, acc[k], sc[b * (kNumAcc) + k]);
   __syncthreads();
   block_reduce();
   if (threadIdx.x == 0) {
-    double tot[kNumPartials + 1];
+    double tot[kNumAcc];
 #pragma unroll
-    for (int k = 0; k < kNumPartials + 1; ++k) tot[k] = sh[k][0];
+    for (int k = 0; k < kNumAcc; ++k) tot[k] = sh[k][0];
     *ticket = 0u;  // ready for the next launch
     if (a.mode == 1) tot[11] = ctl->ps[useb ? a.src_role_b : a.src_role_a].maxe + dw;  // max exponent shifts by dw
     apply_role(ctl, role, tot, w, a.mode == 0);

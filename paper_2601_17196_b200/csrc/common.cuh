@@ -62,10 +62,12 @@ struct PointScalars {
   double score_u, score_v;  // sum rho(r~_i, row_i), sum rho(c~_j, col_j)
   double gl1u, gl1v;        // |grad_u|_1, |grad_v|_1
   double phi, err;
+  double minrow, mincol;  // smallest entry of B 1 and B^T 1 (scaling shortcut guard)
   int overflow;
   int pad;
 };
 constexpr int kNumPartials = 11;  // total, maxu, maxv, seu, sev, ur, vc, score_u, score_v, gl1u, gl1v
+constexpr int kNumAcc = kNumPartials + 3;  // + maxe (11), minrow (12), mincol (13)
 
 template <class T>
 struct DevBuf {

@@ -118,7 +118,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.colp.alloc(size_t(2 * ws.nrb * n));
   ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
   ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * kTPI, kEvalThreads), 4096));
-  ws.scratch.alloc(size_t(std::max(8192, (kNumPartials + 1) * ws.eval_blocks)));
+  ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
   ws.ticket.alloc(1);
   ws.ticket.zero(cx.stream);
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n))));
