@@ -52,6 +52,7 @@ struct AspotCtl {
   int paused;     // loop stopped at pause_at (session API), not finished
   // sweep-vs-scale gates of z_hat and z_check' (block w: B scales by e^dw)
   int g_hat_sweep, g_hat_scaled, g_new_sweep, g_new_scaled;
+  int clamp_guard;  // fp64 (Eigen-clamped exp) problems: scale only far above the clamp floor
   int64_t pause_at;
   int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
   int64_t trace_len, trace_cap, log_len, log_cap;
@@ -106,9 +107,12 @@ __device__ __forceinline__ double acc_join(int k, double x, double y) {
   return is_max_slot(k) ? nan_max(x, y) : (is_min_slot(k) ? fmin(x, y) : x + y);
 }
 
-// Scaling shortcut guard: B(z + dw e_w) = B(z) e^dw holds entry-wise only
-// while no exponent meets the Eigen clamp (kExpLo); sums far above the
-// clamp floor on both sides make the clamp's contribution negligible.
+// Scaling shortcut guard (fp64 only): B(z + dw e_w) = B(z) e^dw holds
+// entry-wise only while no exponent meets the Eigen clamp (kExpLo); sums far
+// above the clamp floor on both sides make the clamp's contribution
+// negligible. The fp32 sweeps have no clamp: a column flushed to 0 relative
+// to its rows' maxima stays flushed after a shift of w, so scaling matches a
+// fresh sweep.
 constexpr double kScaleSafeFloor = 1e-250;
 __device__ __forceinline__ bool scale_safe(const PointScalars& src, double s) {
   const double m = fmin(src.minrow, src.mincol);
@@ -146,7 +150,7 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
     case R_GRAVE:
       if (ps.overflow) { ctl->g_alive = 0; break; }
       ctl->block_hat = ctl->block_rule == POTGPU_ROUND_ROBIN ? int(ctl->gk_calls % 3) : greedy_block(ps, ctl->s);
-      ctl->g_hat_scaled = ctl->block_hat == 2 && scale_safe(ps, ctl->s);
+      ctl->g_hat_scaled = ctl->block_hat == 2 && (!ctl->clamp_guard || scale_safe(ps, ctl->s));
       ctl->g_hat_sweep = !ctl->g_hat_scaled;
       break;
     case R_HAT: {
@@ -157,7 +161,7 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
       ctl->phi_best = fmin(ctl->phi_check, ps.phi);
       const PointScalars& pb = keep ? ctl->ps[R_CHECK] : ps;
       ctl->block_check = ctl->block_rule == POTGPU_ROUND_ROBIN ? int((ctl->gk_calls + 1) % 3) : greedy_block(pb, ctl->s);
-      ctl->g_new_scaled = ctl->block_check == 2 && scale_safe(pb, ctl->s);
+      ctl->g_new_scaled = ctl->block_check == 2 && (!ctl->clamp_guard || scale_safe(pb, ctl->s));
       ctl->g_new_sweep = !ctl->g_new_scaled;
       break;
     }

@@ -473,6 +473,7 @@ struct AspotSession : Session {
     h.step_denom = step_denom;
     h.s = P.s;
     h.status = ST_RUNNING;
+    h.clamp_guard = P.dtype == POTGPU_F64 ? 1 : 0;
     PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(AspotCtl), cudaMemcpyHostToDevice, cx.stream));
     AspotCtl* ctl = ws.ctl.p;
     k_stamp_t0<<<1, 1, 0, cx.stream>>>(ctl);
