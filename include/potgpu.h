@@ -179,6 +179,15 @@ int potgpu_destroy(potgpu_ctx* ctx);
 int potgpu_solve(potgpu_ctx* ctx, int solver_kind, const potgpu_problem* problem, const potgpu_config* config,
                  potgpu_summary* summary, potgpu_outputs* outputs);
 
+/* Batched independent problems (BASELINE configs[4]; no reference
+ * counterpart): `concurrency` workers (0 = 8), each with its own stream, run
+ * complete solves concurrently. summaries[count]; outputs may be NULL or an
+ * array of count entries. Returns the first failure (message names the
+ * problem index). */
+int potgpu_solve_batched(potgpu_ctx* ctx, int solver_kind, const potgpu_problem* problems, int64_t count,
+                         const potgpu_config* config, potgpu_summary* summaries, potgpu_outputs* outputs,
+                         int concurrency);
+
 /* Step-wise form of potgpu_solve (no reference counterpart; used to time a
  * fixed number of iterations and to drive the loop from a host runtime):
  * begin = validation + setup + the first evaluation (+ record(0));

@@ -300,74 +300,62 @@ struct BSums { Vec row, col; double total = 0.0; double max_e = 0.0; };
 // CPU-baseline timing (bench.py), splitting columns into contiguous chunks.
 inline int& oracle_threads() { static int t = 1; return t; }
 
-inline BSums sweep_parallel(const EntropicContext& ctx, const DualPoint& z, int T) {
+// f(k) for k in [0, count) on oracle_threads() host threads (contiguous
+// chunks). Every index is computed independently, so results do not depend
+// on the thread count.
+template <class F>
+inline void parallel_for(long count, F f) {
+  const int T = std::max(1, std::min<int>(oracle_threads(), int(std::max<long>(count, 1))));
+  if (T == 1) { for (long k = 0; k < count; ++k) f(k); return; }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] { for (long k = count * t / T; k < count * (t + 1) / T; ++k) f(k); });
+  for (auto& th : pool) th.join();
+}
+
+// Row i's sum runs over j in order, column j's over i in order, the total
+// is the compensated sum of the column sums: the same bits for any number of
+// oracle threads (the threaded form recomputes the exponentials per pass).
+inline BSums sweep(const EntropicContext& ctx, const DualPoint& z, bool want_rows = true, bool want_cols = true) {
+  (void)want_rows; (void)want_cols;
   const long n = ctx.size();
-  std::vector<std::vector<KSum>> racc(static_cast<size_t>(T), std::vector<KSum>(static_cast<size_t>(n)));
-  std::vector<KSum> tacc(static_cast<size_t>(T));
-  std::vector<double> mx(size_t(T), -std::numeric_limits<double>::infinity());
-  std::vector<int> nan(size_t(T), 0);
   BSums out;
-  out.col.assign(size_t(n), 0.0);
-  auto work = [&](int th) {
-    const long j0 = n * th / T, j1 = n * (th + 1) / T;
-    auto& ra = racc[size_t(th)];
-    for (long j = j0; j < j1; ++j) {
+  out.row.assign(static_cast<size_t>(n), 0.0);
+  out.col.assign(static_cast<size_t>(n), 0.0);
+  const auto expo = [&](long i, long j) { return ((ctx.logK.at(i, j) + z.u[size_t(i)]) + z.v[size_t(j)]) + z.w; };
+  double mx = -std::numeric_limits<double>::infinity();
+  bool nan = false;
+  if (oracle_threads() <= 1) {
+    std::vector<KSum> racc(static_cast<size_t>(n));
+    for (long j = 0; j < n; ++j) {
       KSum cacc;
       for (long i = 0; i < n; ++i) {
-        const double e = ((ctx.logK.at(i, j) + z.u[size_t(i)]) + z.v[size_t(j)]) + z.w;
-        if (e != e) nan[size_t(th)] = 1; else if (e > mx[size_t(th)]) mx[size_t(th)] = e;
+        const double e = expo(i, j);
+        if (e != e) nan = true; else if (e > mx) mx = e;
         const double b = eexp(e);
-        ra[size_t(i)].add(b);
+        racc[size_t(i)].add(b);
         cacc.add(b);
-        tacc[size_t(th)].add(b);
       }
       out.col[size_t(j)] = cacc.get();
     }
-  };
-  std::vector<std::thread> pool;
-  for (int th = 0; th < T; ++th) pool.emplace_back(work, th);
-  for (auto& t : pool) t.join();
-  double m = -std::numeric_limits<double>::infinity();
-  bool anynan = false;
-  KSum tot;
-  for (int th = 0; th < T; ++th) { m = std::max(m, mx[size_t(th)]); anynan |= nan[size_t(th)] != 0; tot.add(tacc[size_t(th)].s); tot.add(tacc[size_t(th)].c); }
-  out.max_e = anynan ? std::numeric_limits<double>::quiet_NaN() : m;
-  check_exp_range(out.max_e, "B(z)");
-  out.row.resize(size_t(n));
-  for (long i = 0; i < n; ++i) {
-    KSum k;
-    for (int th = 0; th < T; ++th) { k.add(racc[size_t(th)][size_t(i)].s); k.add(racc[size_t(th)][size_t(i)].c); }
-    out.row[size_t(i)] = k.get();
-  }
-  out.total = tot.get();
-  return out;
-}
-
-inline BSums sweep(const EntropicContext& ctx, const DualPoint& z, bool want_rows = true, bool want_cols = true) {
-  if (oracle_threads() > 1) return sweep_parallel(ctx, z, oracle_threads());
-  const long n = ctx.size();
-  BSums out;
-  std::vector<KSum> racc(want_rows ? size_t(n) : 0);
-  if (want_cols) out.col.assign(size_t(n), 0.0);
-  KSum tot;
-  double mx = -std::numeric_limits<double>::infinity();
-  bool nan = false;
-  for (long j = 0; j < n; ++j) {
-    KSum cacc;
-    for (long i = 0; i < n; ++i) {
-      const double e = ((ctx.logK.at(i, j) + z.u[size_t(i)]) + z.v[size_t(j)]) + z.w;
-      if (e != e) nan = true; else if (e > mx) mx = e;
-      const double b = eexp(e);
-      if (want_rows) racc[size_t(i)].add(b);
-      if (want_cols) cacc.add(b);
-      tot.add(b);
-    }
-    if (want_cols) out.col[size_t(j)] = cacc.get();
+    for (long i = 0; i < n; ++i) out.row[size_t(i)] = racc[size_t(i)].get();
+  } else {
+    std::vector<double> cmx(static_cast<size_t>(n), -std::numeric_limits<double>::infinity());
+    std::vector<char> cnan(static_cast<size_t>(n), 0);
+    parallel_for(n, [&](long i) {
+      KSum r; for (long j = 0; j < n; ++j) r.add(eexp(expo(i, j)));
+      out.row[size_t(i)] = r.get();
+    });
+    parallel_for(n, [&](long j) {
+      KSum c; double m = -std::numeric_limits<double>::infinity(); char nn = 0;
+      for (long i = 0; i < n; ++i) { const double e = expo(i, j); if (e != e) nn = 1; else if (e > m) m = e; c.add(eexp(e)); }
+      out.col[size_t(j)] = c.get(); cmx[size_t(j)] = m; cnan[size_t(j)] = nn;
+    });
+    for (long j = 0; j < n; ++j) { mx = std::max(mx, cmx[size_t(j)]); nan = nan || cnan[size_t(j)]; }
   }
   out.max_e = nan ? std::numeric_limits<double>::quiet_NaN() : mx;
   check_exp_range(out.max_e, "B(z)");
-  if (want_rows) { out.row.resize(static_cast<size_t>(n)); for (long i = 0; i < n; ++i) out.row[size_t(i)] = racc[size_t(i)].get(); }
-  out.total = tot.get();
+  out.total = vsum(out.col);
   return out;
 }
 
@@ -790,6 +778,8 @@ struct ExtendedSinkhornRun { Mat B; Vec u, v; long iterations = 0; SolveStatus s
 
 inline double seq_max(double m, double x) { return (x > m || m != m) ? x : m; }
 
+
+
 inline ExtendedSinkhornRun extended_sinkhorn(const ExtendedOtInstance& ext, const ExtLogK& K, double tol, const SolverConfig& config,
                                              const Instance& original, ConvergenceTrace& trace, Clock::time_point start,
                                              bool materialise_B) {
@@ -799,15 +789,18 @@ inline ExtendedSinkhornRun extended_sinkhorn(const ExtendedOtInstance& ext, cons
   Vec u(static_cast<size_t>(m), 0.0), v(static_cast<size_t>(m), 0.0);
   // B = exp((logK + u_i) + v_j) (solvers.hpp:426-431) and its row/col sums.
   const auto kernel_sums = [&](Vec& rs, Vec& cs, double& tot) {
-    std::vector<KSum> racc(static_cast<size_t>(m)); KSum t;
+    // row sums (each over j in order) and column sums (each over i in order)
+    rs.assign(static_cast<size_t>(m), 0.0);
     cs.assign(static_cast<size_t>(m), 0.0);
-    for (long j = 0; j < m; ++j) {
-      KSum c;
-      for (long i = 0; i < m; ++i) { const double b = eexp((K.at(i, j) + u[size_t(i)]) + v[size_t(j)]); racc[size_t(i)].add(b); c.add(b); t.add(b); }
+    parallel_for(m, [&](long i) {
+      KSum r; for (long j = 0; j < m; ++j) r.add(eexp((K.at(i, j) + u[size_t(i)]) + v[size_t(j)]));
+      rs[size_t(i)] = r.get();
+    });
+    parallel_for(m, [&](long j) {
+      KSum c; for (long i = 0; i < m; ++i) c.add(eexp((K.at(i, j) + u[size_t(i)]) + v[size_t(j)]));
       cs[size_t(j)] = c.get();
-    }
-    rs.resize(static_cast<size_t>(m)); for (long i = 0; i < m; ++i) rs[size_t(i)] = racc[size_t(i)].get();
-    tot = t.get();
+    });
+    tot = vsum(cs);
   };
   const auto marginal_error = [&](const Vec& rs, const Vec& cs) {  // solvers.hpp:432-435
     Vec a(static_cast<size_t>(m)), b(static_cast<size_t>(m));
@@ -839,21 +832,21 @@ inline ExtendedSinkhornRun extended_sinkhorn(const ExtendedOtInstance& ext, cons
     if (run.iterations >= config.max_iterations) { run.status = SolveStatus::MaxIterationsExceeded; break; }
     // u = log r - lse_rows(logK + 1 v^T)  (solvers.hpp:463-467, lse_rows :397-401)
     Vec nu(static_cast<size_t>(m));
-    for (long i = 0; i < m; ++i) {
+    parallel_for(m, [&](long i) {
       double mx = -std::numeric_limits<double>::infinity();
       for (long j = 0; j < m; ++j) mx = seq_max(mx, K.at(i, j) + v[size_t(j)]);
       KSum s; for (long j = 0; j < m; ++j) s.add(eexp((K.at(i, j) + v[size_t(j)]) - mx));
       nu[size_t(i)] = log_r[size_t(i)] - (mx + std::log(s.get()));
-    }
+    });
     u = std::move(nu);
     // v = log c - lse_rows(logK^T + 1 u^T)  (solvers.hpp:468-472)
     Vec nv(static_cast<size_t>(m));
-    for (long j = 0; j < m; ++j) {
+    parallel_for(m, [&](long j) {
       double mx = -std::numeric_limits<double>::infinity();
       for (long i = 0; i < m; ++i) mx = seq_max(mx, K.at(i, j) + u[size_t(i)]);
       KSum s; for (long i = 0; i < m; ++i) s.add(eexp((K.at(i, j) + u[size_t(i)]) - mx));
       nv[size_t(j)] = log_c[size_t(j)] - (mx + std::log(s.get()));
-    }
+    });
     v = std::move(nv);
     kernel_sums(rs, cs, tot);
     run.final_error = marginal_error(rs, cs);

@@ -2,7 +2,9 @@
 // validation, the accelerated solver driver, dual evaluation.
 #include <chrono>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <thread>
 
 #include "engine.cuh"
 #include "plan.cuh"
@@ -716,30 +718,88 @@ static void check_config(const potgpu_config& c) {  // core.hpp:250-266
   if (c.gamma_override != 0 && !(c.gamma_override > 0)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma override must be positive");
 }
 
-static std::unique_ptr<Session> make_session(potgpu_ctx* c, int kind, const potgpu_problem* pr,
-                                             const potgpu_config* cfg_in, int64_t trace_cap, int64_t log_cap) {
-  if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
-  PG_CK(cudaSetDevice(c->cx.device));
+static std::unique_ptr<Session> make_session_cx(Context& cx, int kind, const potgpu_problem* pr,
+                                                const potgpu_config* cfg_in, int64_t trace_cap, int64_t log_cap) {
+  PG_CK(cudaSetDevice(cx.device));
   potgpu_config cfg;
   if (cfg_in) cfg = *cfg_in; else potgpu_config_default(&cfg);
   const auto t_start = HostClock::now();
   std::unique_ptr<Session> s;
   if (kind == POTGPU_ASPOT) {
-    auto a = std::make_unique<AspotSession>(c->cx);
+    auto a = std::make_unique<AspotSession>(cx);
     a->trace_cap = std::max<int64_t>(trace_cap, 0) + 1;
     a->log_cap = cfg.collect_iter_log ? std::max<int64_t>(log_cap, 0) : 0;
     s = std::move(a);
   } else if (kind == POTGPU_FEASIBLE_SINKHORN || kind == POTGPU_TUNED_SINKHORN) {
-    s = make_sinkhorn_session(c->cx, kind, trace_cap);
+    s = make_sinkhorn_session(cx, kind, trace_cap);
   } else {
     throw Error(POTGPU_INVALID_ARGUMENT, "unknown solver kind");
   }
   s->cfg = cfg;
   s->t_start = t_start;
-  upload_problem(c->cx, pr, s->P);
+  upload_problem(cx, pr, s->P);
   check_config(cfg);
   s->begin();
   return s;
+}
+
+static std::unique_ptr<Session> make_session(potgpu_ctx* c, int kind, const potgpu_problem* pr,
+                                             const potgpu_config* cfg_in, int64_t trace_cap, int64_t log_cap) {
+  if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+  return make_session_cx(c->cx, kind, pr, cfg_in, trace_cap, log_cap);
+}
+
+// Batched independent problems (BASELINE configs[4]): `concurrency` host
+// workers, each with its own CUDA stream, pull problems from a shared
+// counter and run complete device-resident solves; the GPU overlaps the
+// streams' kernels. No reference counterpart (the reference solves one
+// instance per call).
+int potgpu_solve_batched(potgpu_ctx* c, int kind, const potgpu_problem* problems, int64_t count,
+                         const potgpu_config* cfg, potgpu_summary* summaries, potgpu_outputs* outputs, int concurrency) {
+  return guarded([&] {
+    if (!c || !problems || !summaries || count < 0) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    const int workers = int(std::max<int64_t>(1, std::min<int64_t>(concurrency > 0 ? concurrency : 8, count)));
+    std::atomic<int64_t> next{0};
+    std::mutex mu;
+    int first_code = 0;
+    std::string first_msg;
+    std::vector<std::thread> pool;
+    for (int t = 0; t < workers; ++t) {
+      pool.emplace_back([&] {
+        Context cx = c->cx;
+        try {
+          PG_CK(cudaSetDevice(cx.device));
+          PG_CK(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+        } catch (const Error& e) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!first_code) { first_code = e.code; first_msg = e.what(); }
+          return;
+        }
+        int64_t k;
+        while ((k = next.fetch_add(1)) < count) {
+          try {
+            potgpu_summary* sm = &summaries[k];
+            std::memset(sm, 0, sizeof(*sm));
+            potgpu_outputs* out = outputs ? &outputs[k] : nullptr;
+            auto s = make_session_cx(cx, kind, &problems[k], cfg, out ? out->trace_cap : 0, out ? out->iter_log_cap : 0);
+            s->iterate(-1, nullptr, nullptr, nullptr);
+            s->finish(sm, out);
+          } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!first_code) {
+              const Error* pe = dynamic_cast<const Error*>(&e);
+              first_code = pe ? pe->code : POTGPU_ERR_CUDA;
+              first_msg = "problem " + std::to_string(k) + ": " + e.what();
+            }
+          }
+        }
+        cudaStreamSynchronize(cx.stream);
+        cudaStreamDestroy(cx.stream);
+      });
+    }
+    for (auto& th : pool) th.join();
+    if (first_code) throw Error(first_code, first_msg);
+  });
 }
 
 int potgpu_solve(potgpu_ctx* c, int kind, const potgpu_problem* pr, const potgpu_config* cfg_in, potgpu_summary* sm,

@@ -144,7 +144,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_solve", "potgpu_dual_eval", "potgpu_round_pot", "potgpu_comm_unique_id", "potgpu_comm_init",
     "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
-    "potgpu_session_stats",
+    "potgpu_session_stats", "potgpu_solve_batched",
 )
 
 _lib = None
@@ -174,6 +174,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_ctx_stream.argtypes = [ctypes.c_void_p]
     lib.potgpu_ctx_stream.restype = ctypes.c_void_p
     lib.potgpu_session_time_sweep.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, dp, dp]
+    lib.potgpu_solve_batched.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), ctypes.c_int64, P(_Config),
+                                         P(_Summary), P(_Outputs), ctypes.c_int]
     lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
     lib.potgpu_make_synthetic.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_double, dp, dp, dp, dp]
@@ -506,6 +508,28 @@ def solve(inst: Instance, kind: SolverKind, config: SolverConfig = SolverConfig(
           **kw) -> SolveResult:
     """solvers.hpp:591-599."""
     return _run(SolverKind(kind), inst, config, ctx, **kw)
+
+
+def solve_batched(kind: SolverKind, instances: List[Instance], config: SolverConfig = SolverConfig(),
+                  ctx: Optional[Context] = None, concurrency: int = 8, trace_cap: int = 16) -> List[SolveResult]:
+    """Independent problems solved concurrently (potgpu_solve_batched;
+    BASELINE configs[4]). Same per-problem results as `solve`."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    keep: list = []
+    k = len(instances)
+    probs = (_Problem * max(k, 1))()
+    outs = (_Outputs * max(k, 1))()
+    sums = (_Summary * max(k, 1))()
+    bufs = []
+    for i, inst in enumerate(instances):
+        probs[i] = _problem(inst, keep)
+        b = _OutBufs(SolverKind(kind), inst.size(), config, trace_cap, 0)
+        bufs.append(b)
+        outs[i] = b.out
+    conf = _config(config)
+    _check(lib.potgpu_solve_batched(ctx._h, int(kind), probs, k, ctypes.byref(conf), sums, outs, int(concurrency)))
+    return [bufs[i].result(sums[i]) for i in range(k)]
 
 
 @dataclass
