@@ -103,9 +103,16 @@ def test_c3_aspot_prefix_and_full(ctx):
     o = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=1e-2,
                       max_iterations=3, skip_plan=True)
     assert g.iterations == o.iterations == 3
-    np.testing.assert_array_equal(g.iter_log[:, 2:5], o.log[:, 2:5])   # block choices, z_best
-    np.testing.assert_allclose(g.iter_log[:, 5], o.log[:, 5], rtol=1e-3)  # E_t
-    np.testing.assert_allclose(g.iter_log[:, 6], o.log[:, 6], rtol=1e-5)  # phi(z_check)
+    # fp32 vs fp64: identical decisions until the first near-tie (z_best's
+    # phi(z_check) <= phi_hat can resolve differently at fp32 precision);
+    # E_t and phi agree to fp32 tolerance up to there
+    diff = np.flatnonzero((g.iter_log[:, 2:5] != o.log[:, 2:5]).any(axis=1))
+    k = int(diff[0]) if len(diff) else 3
+    assert k >= 1
+    np.testing.assert_allclose(g.iter_log[:k, 5], o.log[:k, 5], rtol=1e-3)  # E_t
+    np.testing.assert_allclose(g.iter_log[:k, 6], o.log[:k, 6], rtol=1e-5)  # phi(z_check)
+    if k < 3:  # iteration k compares phi(z_check_{k-1}) (col 6, row k-1) with phi_hat_k (col 7)
+        assert abs(o.log[k - 1, 6] - o.log[k, 7]) <= 1e-5 * abs(o.log[k, 7]), (o.log, g.iter_log)
     full = pot.aspot_solve(inst, pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False), ctx=ctx)
     assert full.status == pot.SolveStatus.Converged
     check_properties(full, inst.s, TOL_F32_VIOL)
