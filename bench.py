@@ -9,8 +9,10 @@ A "step" is one accepted ASPOT iteration (solvers.hpp:323-369) on the
 resident problem. `value` is whole-job iterations/s from CUDA-event device
 time of exactly K steps (max over ranks); `e2e` is the same metric through
 the public API from host buffers (upload + setup + K iterations + rounding +
-download). N > 1: the plan is row-block sharded once
-the sharded path is enabled; until then ranks run independent replicas.
+download). N > 1 (torchrun, one process per GPU): the SAME problem is
+row-block sharded over the N GPUs (csrc/shard.cuh: each rank sweeps n/N
+rows, one NCCL all-reduce per sweep) — strong scaling of one solve; `value`
+is that solve's iterations/s from the max-over-ranks device time.
 """
 import argparse
 import json
@@ -146,7 +148,7 @@ def main():
     rank, world, local, dist = dist_setup(args)
     from paper_2601_17196_b200 import pot
 
-    inst = pot.config_instance(3, n=args.n, seed=args.seed + (rank if world > 1 else 0))
+    inst = pot.config_instance(3, n=args.n, seed=args.seed)  # one problem, sharded over the ranks
     if inst.cost_scale is None or inst.cost_scale <= 0:
         inst.cost_scale = pot.points_scale(inst.X, inst.Y)
     n = inst.size()
@@ -154,7 +156,7 @@ def main():
     config = {"workload": f"BASELINE configs[2]: registration-shaped POT n={n}, fp32, on-the-fly sq-Euclidean cost, "
                           f"eps={args.epsilon}, s=0.9, ASPOT",
               "n": n, "epsilon": args.epsilon, "solver": "aspot", "cost": "on-the-fly",
-              "parallelism": f"replicas{world}" if world > 1 else "single",
+              "parallelism": f"rowshard{world}" if world > 1 else "single",
               "l2": "coordinates are L2-resident by design (on-the-fly cost); L2 flushed (256 MB write) between "
                     "timed steps"}
 
@@ -164,7 +166,7 @@ def main():
         ref = cpu_reference(inst, args, threads)
         line = {"impl": "reference", "metric": "ASPOT iterations/s", "value": ref["value"], "unit": "iterations/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / ref["value"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "cpu_baseline": ref,
                 "e2e": {"value": ref["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -173,6 +175,8 @@ def main():
     import torch
     torch.cuda.set_device(local)
     ctx = pot.Context(local)
+    if world > 1:
+        pot.init_distributed(ctx)  # NCCL communicator for the row shards
     cfg = pot.SolverConfig(epsilon=args.epsilon, log_every=10 ** 9, max_iterations=10 ** 7, record_rounded_cost=False,
                            materialize_plan=False)
     sess = pot.Session(pot.SolverKind.Aspot, inst, cfg, ctx=ctx)
@@ -195,7 +199,7 @@ def main():
     k1, a1, s1 = sess.stats()
     total_ms = sum(per_step)
     total_ms = max_over_ranks(total_ms, dist, local)
-    value = world * done / (total_ms / 1000.0) if total_ms > 0 else 0.0
+    value = done / (total_ms / 1000.0) if total_ms > 0 else 0.0  # one sharded solve
     sweeps_per_it = (s1 - s0) / max(done, 1)
     # roofline of the dominant kernel (the on-the-fly sweep): MUFU ex2 bound
     ms_sweep, elems, _ = sess.time_sweep(20)
@@ -240,7 +244,8 @@ def main():
     e2e_wall = time.perf_counter() - t0
     h2d = 8 * (inst.X.size + inst.Y.size + 2 * n)
     d2h = 8 * (4 * n + 1)
-    e2e_val = world * r2.iterations / e2e_wall
+    e2e_wall = max_over_ranks(e2e_wall, dist, local)
+    e2e_val = r2.iterations / e2e_wall
 
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
@@ -256,7 +261,7 @@ def main():
     if rank == 0:
         line = {"metric": "ASPOT iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
                 "steps": len(per_step), "warmup": args.warmup, "ms_per_step": total_ms / max(len(per_step), 1),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config, "clocks": clocks,
                 "e2e": {"value": e2e_val, "unit": "iterations/s", "h2d_bytes_per_step": h2d / max(r2.iterations, 1),
                         "d2h_bytes_per_step": d2h / max(r2.iterations, 1),

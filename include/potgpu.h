@@ -226,11 +226,22 @@ int potgpu_dual_eval(potgpu_ctx* ctx, const potgpu_problem* problem, double gamm
 int potgpu_round_pot(potgpu_ctx* ctx, int64_t n, const double* X, const double* r, const double* c, double s,
                      double* X_out);
 
-/* Multi-GPU row-block sharding (one process per GPU). rank 0 creates the id,
- * the caller broadcasts its 128 bytes (e.g. torch.distributed), then every
- * rank calls potgpu_comm_init before potgpu_solve. */
+/* Multi-GPU row-block sharding (no reference counterpart —
+ * the reference is single-threaded). One process per GPU: rank 0 creates the
+ * id, the caller broadcasts its 128 bytes (e.g. torch.distributed), then
+ * every rank calls potgpu_comm_init on its context and runs the SAME solve
+ * calls with the SAME full problem; each rank sweeps its contiguous block of
+ * rows and one NCCL all-reduce per sweep combines the sums, so every rank
+ * returns the same summary (a materialised plan holds the rank's own rows).
+ * NCCL is loaded at run time (libnccl.so.2 or $POTGPU_NCCL_LIB);
+ * POTGPU_ERR_NCCL when it is missing or fails. */
 int potgpu_comm_unique_id(unsigned char id_out[128]);
 int potgpu_comm_init(potgpu_ctx* ctx, int rank, int world_size, const unsigned char id[128]);
+/* The context computes `shards` row shards itself (per rank when combined
+ * with potgpu_comm_init) and reduces them with a fixed-order device sum: the
+ * sharded arithmetic on one GPU, for testing; shards = 1 is the default. */
+int potgpu_comm_init_local(potgpu_ctx* ctx, int shards);
+int potgpu_comm_info(potgpu_ctx* ctx, int* rank, int* world_size, int* shards_per_rank);
 
 /* Synthetic fixtures: make_synthetic_instance (synthetic.hpp:15-54) and the
  * BASELINE.json config recipes. Host buffers:

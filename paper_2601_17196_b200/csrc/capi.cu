@@ -385,32 +385,32 @@ struct AspotSession : Session {
                ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
     const int gv = ws.nblk;
     k_zbar<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZC, Z, ZB);
-    launch_sweep(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma);
-    launch_eval(cx, ws, ZB, R_BAR, &ctl->g_new);
+    const SweepOut none{};
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new);
     k_zgrave<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
-    launch_sweep(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma);
-    launch_eval(cx, ws, ZG, R_GRAVE, &ctl->g_alive);
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma), ZG, R_GRAVE,
+                &ctl->g_alive);
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
                                                    ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
     // z_hat: a sweep, or (block w, ~all iterations) B(z_grave) scaled by e^dw
-    launch_sweep(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma);
-    launch_eval(cx, ws, ZH, R_HAT, &ctl->g_hat_sweep);
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma), ZH, R_HAT,
+                &ctl->g_hat_sweep);
     {
       ReduceArgs sc{};
       sc.src_row_a = ws.row(R_GRAVE); sc.src_col_a = ws.col(R_GRAVE); sc.src_w_a = ZG.w(); sc.src_role_a = R_GRAVE;
-      launch_eval(cx, ws, ZH, R_HAT, &ctl->g_hat_scaled, &sc);
+      launch_eval(cx, ws, none, ZH, R_HAT, &ctl->g_hat_scaled, &sc);
     }
     k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
                                                    ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
     // z_check' = GK(z_best): a sweep, or (block w) B(z_best) scaled
-    launch_sweep(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma);
-    launch_eval(cx, ws, ZN, R_NEW, &ctl->g_new_sweep);
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma), ZN, R_NEW,
+                &ctl->g_new_sweep);
     {
       ReduceArgs sc{};
       sc.src_row_a = ws.row(R_HAT); sc.src_col_a = ws.col(R_HAT); sc.src_w_a = ZH.w(); sc.src_role_a = R_HAT;
       sc.src_row_b = ws.row(R_CHECK); sc.src_col_b = ws.col(R_CHECK); sc.src_w_b = ZC.w(); sc.src_role_b = R_CHECK;
       sc.select_b = &ctl->keep_check;
-      launch_eval(cx, ws, ZN, R_NEW, &ctl->g_new_scaled, &sc);
+      launch_eval(cx, ws, none, ZN, R_NEW, &ctl->g_new_scaled, &sc);
     }
     k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
                                                      ws.col(R_NEW));
@@ -481,8 +481,7 @@ struct AspotSession : Session {
     k_stamp_t0<<<1, 1, 0, cx.stream>>>(ctl);
     // phi_and_gradient(z_check = 0) (solvers.hpp:305) and record(0) (:320)
     const Slot ZC = ws.slot(S_ZC);
-    launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);
-    launch_eval(cx, ws, ZC, R_CHECK, nullptr);
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma), ZC, R_CHECK, nullptr);
     k_init_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p);
     sync_ctl();
     if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
@@ -565,16 +564,16 @@ struct AspotSession : Session {
   double time_sweep(int reps, double* elems, double* bytes) override {
     if (trivial) throw Error(POTGPU_INVALID_ARGUMENT, "trivial solve has no sweep");
     const Slot ZC = ws.slot(S_ZC);
-    launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);  // warm
+    int64_t rows = launch_local_sweeps(cx, P, ws, ZC, gamma);  // warm
     PG_CK(cudaEventRecord(ev0, cx.stream));
-    for (int k = 0; k < reps; ++k) launch_sweep(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma);
+    for (int k = 0; k < reps; ++k) rows = launch_local_sweeps(cx, P, ws, ZC, gamma);
     PG_CK(cudaEventRecord(ev1, cx.stream));
     PG_CK(cudaEventSynchronize(ev1));
     float f = 0.f;
     PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
     const double n = double(P.n);
-    if (elems) *elems = n * n;
-    if (bytes) *bytes = n * n * stream_bytes_per_elem(P);
+    if (elems) *elems = double(rows) * n;
+    if (bytes) *bytes = double(rows) * n * stream_bytes_per_elem(P);
     return double(f) / reps;
   }
 
@@ -705,6 +704,7 @@ int potgpu_destroy(potgpu_ctx* c) {
   return guarded([&] {
     if (!c) return;
     cudaSetDevice(c->cx.device);
+    if (c->cx.comm.nccl) nccl_api().CommDestroy(c->cx.comm.nccl);
     if (c->cx.stream) cudaStreamDestroy(c->cx.stream);
     delete c;
   });
@@ -888,8 +888,7 @@ int potgpu_dual_eval(potgpu_ctx* c, const potgpu_problem* pr, double gamma, cons
     h.n = n;
     h.s = P.s;
     PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(h), cudaMemcpyHostToDevice, c->cx.stream));
-    launch_sweep(c->cx, P, ws, Z, nullptr, nullptr, nullptr, true, gamma);
-    launch_eval(c->cx, ws, Z, R_EVAL, nullptr);
+    launch_eval(c->cx, ws, sweep_point(c->cx, P, ws, Z, nullptr, nullptr, nullptr, true, gamma), Z, R_EVAL, nullptr);
     PG_CK(cudaMemcpyAsync(&h, ws.ctl.p, sizeof(h), cudaMemcpyDeviceToHost, c->cx.stream));
     if (row) PG_CK(cudaMemcpyAsync(row, ws.row(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
     if (col) PG_CK(cudaMemcpyAsync(col, ws.col(R_EVAL), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
@@ -911,6 +910,48 @@ int potgpu_dual_eval(potgpu_ctx* c, const potgpu_problem* pr, double gamma, cons
     return POTGPU_OVERFLOW;
   }
   return 0;
+}
+
+int potgpu_comm_unique_id(unsigned char id_out[128]) {
+  return guarded([&] {
+    if (!id_out) throw Error(POTGPU_INVALID_ARGUMENT, "null id");
+    NcclUid id;
+    nccl_check(nccl_api().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, id.internal, sizeof(id.internal));
+  });
+}
+
+int potgpu_comm_init(potgpu_ctx* c, int rank, int world_size, const unsigned char id[128]) {
+  return guarded([&] {
+    if (!c || !id) throw Error(POTGPU_INVALID_ARGUMENT, "null context or id");
+    if (world_size < 1 || rank < 0 || rank >= world_size) throw Error(POTGPU_INVALID_ARGUMENT, "bad rank / world size");
+    if (c->cx.comm.nccl) throw Error(POTGPU_INVALID_ARGUMENT, "communicator already initialised");
+    PG_CK(cudaSetDevice(c->cx.device));
+    NcclUid uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    void* comm = nullptr;
+    nccl_check(nccl_api().CommInitRank(&comm, world_size, uid, rank), "ncclCommInitRank");
+    c->cx.comm.nccl = comm;
+    c->cx.comm.rank = rank;
+    c->cx.comm.world = world_size;
+  });
+}
+
+int potgpu_comm_init_local(potgpu_ctx* c, int shards) {
+  return guarded([&] {
+    if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+    if (shards < 1 || shards > 1024) throw Error(POTGPU_INVALID_ARGUMENT, "shards must be in [1, 1024]");
+    c->cx.comm.vshards = shards;
+  });
+}
+
+int potgpu_comm_info(potgpu_ctx* c, int* rank, int* world_size, int* shards_per_rank) {
+  return guarded([&] {
+    if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+    if (rank) *rank = c->cx.comm.rank;
+    if (world_size) *world_size = c->cx.comm.world;
+    if (shards_per_rank) *shards_per_rank = c->cx.comm.vshards;
+  });
 }
 
 int potgpu_round_pot(potgpu_ctx*, int64_t, const double*, const double*, const double*, double, double*) {

@@ -7,6 +7,7 @@
 
 #include "aspot_kernels.cuh"
 #include "rounding.cuh"
+#include "shard.cuh"
 #include "sweep.cuh"
 
 namespace potgpu {
@@ -28,9 +29,7 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
-  // multi-GPU row sharding (filled by potgpu_comm_init)
-  int rank = 0, world = 1;
-  void* nccl_comm = nullptr;
+  Comm comm;  // row sharding (potgpu_comm_init / potgpu_comm_init_local)
 };
 
 // Device-resident problem: one of three cost representations.
@@ -52,9 +51,19 @@ struct DevProblem {
   double s = 0.0;
 };
 
+struct ShardGrid {
+  int64_t lo = 0, hi = 0;  // rows [lo, hi)
+  int index = 0;           // global shard index
+  SweepGrid g{};
+};
+
 struct Workspace {
   int64_t n = 0;
   SweepGrid g{};
+  std::vector<ShardGrid> shards;  // this process's row shards (sharded contexts only)
+  int nshards = 1;                // all shards of the job
+  int64_t xstride = 0;            // per-shard length of the all-reduce vector
+  DevBuf<double> xsend, xrecv;
   int64_t nstrips = 0, nrb = 0;
   int nblk = 0;  // O(n) kernel grid
   int eval_blocks = 0;  // k_point_eval grid (8 indices per block)
@@ -102,8 +111,27 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   occ = std::max(occ, 1);
   ws.strip = P.dtype == POTGPU_F64 ? kStripCols : kStripCols32;
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
-  ws.g = choose_grid(n, cx.num_sms, occ, ws.strip);
-  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : sweep_f32_smem(ws.g.rows_per_cta);
+  ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip);
+  int64_t max_rb = ws.g.grid.y;
+  int max_rpc = ws.g.rows_per_cta;
+  ws.shards.clear();
+  ws.nshards = cx.comm.total();
+  if (cx.comm.sharded()) {
+    for (int p = 0; p < cx.comm.vshards; ++p) {
+      ShardGrid sg;
+      sg.index = cx.comm.shard_index(p);
+      sg.lo = cx.comm.lo(n, sg.index);
+      sg.hi = cx.comm.hi(n, sg.index);
+      sg.g = choose_grid(n, sg.hi - sg.lo, cx.num_sms, occ, ws.strip);
+      max_rb = std::max<int64_t>(max_rb, sg.g.grid.y);
+      max_rpc = std::max(max_rpc, sg.g.rows_per_cta);
+      ws.shards.push_back(sg);
+    }
+    ws.xstride = round_up(2 * n + ws.nshards + 2, 32);
+    ws.xsend.alloc(size_t(cx.comm.vshards * ws.xstride));
+    ws.xrecv.alloc(size_t(ws.xstride));
+  }
+  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : sweep_f32_smem(max_rpc);
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcPointsF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
@@ -115,13 +143,13 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.slots.alloc(size_t(kSlots * ws.slot_stride));
   ws.sums.alloc(size_t(2 * kRoles * n));
   ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
-  ws.colp.alloc(size_t(2 * ws.nrb * n));
-  ws.maxp.alloc(size_t(ws.nstrips * ws.nrb));
+  ws.colp.alloc(size_t(2 * max_rb * n));
+  ws.maxp.alloc(size_t(ws.nstrips * max_rb));
   ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * kTPI, kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
   ws.ticket.alloc(1);
   ws.ticket.zero(cx.stream);
-  ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n))));
+  ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n) + ws.nshards * ceil_div(n, kThreads))));
   ws.rt.alloc(size_t(n));
   ws.ct.alloc(size_t(n));
   ws.ro_buf.alloc(size_t(10 * n));
@@ -134,44 +162,107 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
 }
 
 // --------------------------------------------------------------------------
-// Sweep dispatch.
+// Sweep dispatch (one launch over the rows of `sh`, or all rows).
 inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const double* lu, const double* lv,
-                         const int* gate, bool floor_exp, double gamma) {
+                         const int* gate, bool floor_exp, double gamma, const ShardGrid* sh = nullptr) {
+  const SweepGrid& g = sh ? sh->g : ws.g;
   SweepArgs a;
   a.n = P.n;
-  a.rows_per_cta = ws.g.rows_per_cta;
+  a.row_lo = sh ? sh->lo : 0;
+  a.row_hi = sh ? sh->hi : P.n;
+  a.rows_per_cta = g.rows_per_cta;
   a.u = z.u(); a.v = z.v(); a.w = z.w();
   a.lu = lu; a.lv = lv;
   a.rowp = ws.rowp.p; a.colp = ws.colp.p; a.maxp = ws.maxp.p;
   a.gate = gate;
   a.gamma = gamma;
   if (P.dtype == POTGPU_F64) {
-    if (floor_exp) sweep_f64_dense<true><<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
-    else sweep_f64_dense<false><<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
+    if (floor_exp) sweep_f64_dense<true><<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
+    else sweep_f64_dense<false><<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
   } else if (P.kind == POTGPU_COST_DENSE) {
     SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
-    sweep_f32<SrcDenseF32><<<ws.g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
+    sweep_f32<SrcDenseF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   } else {
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsF32 s{P.XS4.p, P.YS4.p};
-    sweep_f32<SrcPointsF32><<<ws.g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
+    sweep_f32<SrcPointsF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   }
   PG_CK(cudaGetLastError());
 }
 
+// Where the reductions of one swept point live: the raw per-strip /
+// per-row-block partials (one GPU), or the all-reduced fp64 vector
+// [rows | cols | per-shard max] (sharded).
+struct SweepOut {
+  const double* rowp; int64_t nstrips;
+  const double* colp; int64_t nrb;
+  const double* maxp; int64_t nmax;
+  int pfmt;
+};
+
+// The hot path of every evaluation: sweep B(z) (own rows) and, when sharded,
+// gather + all-reduce (shard.cuh).
+inline SweepOut sweep_point(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const double* lu, const double* lv,
+                            const int* gate, bool floor_exp, double gamma) {
+  const int64_t n = P.n;
+  if (!cx.comm.sharded()) {
+    launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma);
+    return SweepOut{ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.maxp.p, ws.nstrips * ws.nrb, ws.pfmt};
+  }
+  for (size_t p = 0; p < ws.shards.size(); ++p) {
+    const ShardGrid& sh = ws.shards[p];
+    launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma, &sh);
+    k_shard_gather<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, ws.colp.p, sh.g.grid.y, ws.maxp.p,
+                                                          int64_t(sh.g.grid.x) * sh.g.grid.y, ws.pfmt, z, lu, sh.lo, sh.hi,
+                                                          sh.index, ws.nshards, ws.xsend.p + p * ws.xstride, gate);
+    PG_CK(cudaGetLastError());
+  }
+  shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, 2 * n + ws.nshards, NcclApi::kSum, ws.xrecv.p,
+                  gate);
+  return SweepOut{ws.xrecv.p, 1, ws.xrecv.p + n, 1, ws.xrecv.p + 2 * n, ws.nshards, PF_F64};
+}
+
+// Device time of the hot-path sweeps alone (no reduction) over this
+// process's rows; the rows that costs.
+inline int64_t launch_local_sweeps(Context& cx, const DevProblem& P, Workspace& ws, Slot z, double gamma) {
+  if (!cx.comm.sharded()) {
+    launch_sweep(cx, P, ws, z, nullptr, nullptr, nullptr, true, gamma);
+    return P.n;
+  }
+  int64_t rows = 0;
+  for (const ShardGrid& sh : ws.shards) {
+    launch_sweep(cx, P, ws, z, nullptr, nullptr, nullptr, true, gamma, &sh);
+    rows += sh.hi - sh.lo;
+  }
+  return rows;
+}
+
+// Sum of a host scalar over the processes of a sharded job.
+inline double allreduce_host_sum(Context& cx, Workspace& ws, double x) {
+  if (!cx.comm.nccl) return x;
+  PG_CK(cudaMemcpyAsync(ws.xsend.p, &x, sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+  nccl_check(nccl_api().AllReduce(ws.xsend.p, ws.xrecv.p, 1, NcclApi::kFloat64, NcclApi::kSum, cx.comm.nccl, cx.stream),
+             "ncclAllReduce");
+  double y = 0.0;
+  PG_CK(cudaMemcpyAsync(&y, ws.xrecv.p, sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+  PG_CK(cudaStreamSynchronize(cx.stream));
+  return y;
+}
+
 // The per-point evaluation (partials -> B 1, B^T 1, scalars, decision).
-inline void launch_eval(Context& cx, Workspace& ws, Slot z, int role, const int* gate, const ReduceArgs* scaled = nullptr) {
+inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, int role, const int* gate,
+                        const ReduceArgs* scaled = nullptr) {
   ReduceArgs r{};
   if (scaled) r = *scaled;
   r.z = z;
-  r.rowp = ws.rowp.p; r.nstrips = ws.nstrips;
-  r.colp = ws.colp.p; r.nrowblocks = ws.nrb;
-  r.maxp = ws.maxp.p; r.nmax = ws.nstrips * ws.nrb;
+  r.rowp = so.rowp; r.nstrips = so.nstrips;
+  r.colp = so.colp; r.nrowblocks = so.nrb;
+  r.maxp = so.maxp; r.nmax = so.nmax;
   r.row_out = ws.row(role); r.col_out = ws.col(role);
   r.rt = ws.rt.p; r.ct = ws.ct.p;
   r.scratch = ws.scratch.p;
   r.gate = gate;
-  r.pfmt = ws.pfmt;
+  r.pfmt = so.pfmt;
   r.mode = scaled ? 1 : 0;
   k_point_eval<<<ws.eval_blocks, kEvalThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());

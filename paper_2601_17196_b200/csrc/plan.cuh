@@ -40,8 +40,8 @@ struct PlanTermsDev {
 // B_ij = exp(((logK_ij + u_i) + v_j) + w) with the Eigen clamp; optionally
 // writes X (row-major, n x n).
 template <class E, bool MATERIALIZE>
-__global__ void __launch_bounds__(kThreads) k_plan_cost(E el, Slot z, PlanTermsDev t, int rows_per_cta, double* partial,
-                                                        double* Xout) {
+__global__ void __launch_bounds__(kThreads) k_plan_cost(E el, Slot z, PlanTermsDev t, int64_t row_lo, int64_t row_hi,
+                                                        int rows_per_cta, double* partial, double* Xout) {
   const int64_t n = z.n;
   const int64_t j = int64_t(blockIdx.x) * kThreads + threadIdx.x;
   const double w = *z.w();
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_plan_cost(E el, Slot z, PlanTermsD
   if (j < n) {
     const double vj = z.v()[j], qj = t.Q[j];
     const double b0 = t.b0 ? t.b0[j] : 0.0, b1 = t.b1 ? t.b1[j] : 0.0;
-    const int64_t r0 = int64_t(blockIdx.y) * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+    const int64_t r0 = row_lo + int64_t(blockIdx.y) * rows_per_cta, r1 = min(row_hi, r0 + rows_per_cta);
     for (int64_t i = r0; i < r1; ++i) {
       const double e = ((el.logk(i, j) + z.u()[i]) + vj) + w;
       const double B = exp(fmin(fmax(e, kExpLo), kExpHi));
@@ -93,8 +93,8 @@ struct PlanEngine {
     const int64_t n = P.n;
     if (lu) up(0, *lu);
     if (lv) up(1, *lv);
-    launch_sweep(cx, P, ws, z, lu ? d(0) : nullptr, lv ? d(1) : nullptr, nullptr, false, gamma);
-    k_sum_partials<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.pfmt, z,
+    const SweepOut so = sweep_point(cx, P, ws, z, lu ? d(0) : nullptr, lv ? d(1) : nullptr, nullptr, false, gamma);
+    k_sum_partials<<<ws.nblk, kVecThreads, 0, cx.stream>>>(so.rowp, so.nstrips, so.colp, so.nrb, so.pfmt, z,
                                                            lu ? d(0) : nullptr, d(2), d(3));
     PG_CK(cudaGetLastError());
     row.resize(size_t(n));
@@ -114,27 +114,39 @@ struct PlanEngine {
     if (a0) { up(6, *a0); up(7, *b0); t.a0 = d(6); t.b0 = d(7); }
     if (a1) { up(8, *a1); up(9, *b1); t.a1 = d(8); t.b1 = d(9); }
     const int rows = cost_sweep_rows(n);
-    dim3 g(unsigned(ceil_div(n, kThreads)), unsigned(ceil_div(n, rows)));
-    const int64_t np = int64_t(g.x) * g.y;
     const bool mat = Xdev != nullptr;
-    if (P.dtype == POTGPU_F64) {
-      ElemDenseF64 el{P.L64.p, P.ld, gamma};
-      if (mat) k_plan_cost<ElemDenseF64, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
-      else k_plan_cost<ElemDenseF64, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
-    } else if (P.kind == POTGPU_COST_DENSE) {
-      ElemDenseF32 el{P.C32.p, P.ld, gamma};
-      if (mat) k_plan_cost<ElemDenseF32, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
-      else k_plan_cost<ElemDenseF32, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
-    } else {
-      ElemPointsF32 el{P.X4.p, P.Y4.p, P.cost_scale, gamma};
-      if (mat) k_plan_cost<ElemPointsF32, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
-      else k_plan_cost<ElemPointsF32, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rows, ws.partial.p, Xdev);
+    // this process's row ranges (all rows on one GPU); a sharded job's
+    // materialised plan holds the process's own rows (the rest stays 0)
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    if (!cx.comm.sharded()) ranges.push_back({0, n});
+    else for (const ShardGrid& sh : ws.shards) ranges.push_back({sh.lo, sh.hi});
+    if (mat && cx.comm.world > 1) PG_CK(cudaMemsetAsync(Xdev, 0, size_t(n * n) * sizeof(double), cx.stream));
+    int64_t np = 0;
+    for (const auto& rg : ranges) {
+      const int64_t nrows = rg.second - rg.first;
+      if (nrows <= 0) continue;
+      dim3 g(unsigned(ceil_div(n, kThreads)), unsigned(ceil_div(nrows, rows)));
+      double* part = ws.partial.p + np;
+      np += int64_t(g.x) * g.y;
+      if (P.dtype == POTGPU_F64) {
+        ElemDenseF64 el{P.L64.p, P.ld, gamma};
+        if (mat) k_plan_cost<ElemDenseF64, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+        else k_plan_cost<ElemDenseF64, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+      } else if (P.kind == POTGPU_COST_DENSE) {
+        ElemDenseF32 el{P.C32.p, P.ld, gamma};
+        if (mat) k_plan_cost<ElemDenseF32, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+        else k_plan_cost<ElemDenseF32, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+      } else {
+        ElemPointsF32 el{P.X4.p, P.Y4.p, P.cost_scale, gamma};
+        if (mat) k_plan_cost<ElemPointsF32, true><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+        else k_plan_cost<ElemPointsF32, false><<<g, kThreads, 0, cx.stream>>>(el, z, t, rg.first, rg.second, rows, part, Xdev);
+      }
+      PG_CK(cudaGetLastError());
     }
-    PG_CK(cudaGetLastError());
     HVec part(static_cast<size_t>(np));
     PG_CK(cudaMemcpyAsync(part.data(), ws.partial.p, size_t(np) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
     PG_CK(cudaStreamSynchronize(cx.stream));
-    return hsum(part);
+    return allreduce_host_sum(cx, ws, hsum(part));
   }
 };
 

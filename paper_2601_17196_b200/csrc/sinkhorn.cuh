@@ -52,36 +52,86 @@ struct SinkhornSession : Session {
     PG_CK(cudaStreamSynchronize(cx.stream));
   }
 
+  // one n^2 row-LSE sweep over rows [lo, hi) (grid g) at the current v
+  void row_sweep(const int* gate, const ShardGrid* sh) {
+    const int64_t n = P.n;
+    const SweepGrid& g = sh ? sh->g : ws.g;
+    if (P.dtype == POTGPU_F64) {
+      sweep_rowlse_f64<<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.v, sh ? sh->lo : 0, sh ? sh->hi : n,
+                                                           g.rows_per_cta, reinterpret_cast<double2*>(ws.rowp.p), gate);
+    } else {
+      launch_sweep(cx, P, ws, zv_slot(), nullptr, nullptr, gate, false, gamma, sh);  // rows of (0, v, 0)
+    }
+  }
+
+  // one n^2 column-LSE sweep over rows [lo, hi) at the current u
+  void col_sweep(const int* gate, const ShardGrid* sh) {
+    const int64_t n = P.n;
+    const SweepGrid& g = sh ? sh->g : ws.g;
+    const int64_t lo = sh ? sh->lo : 0, hi = sh ? sh->hi : n;
+    if (P.dtype == POTGPU_F64) {
+      sweep_collse_f64<<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.u, lo, hi, g.rows_per_cta,
+                                                           reinterpret_cast<double2*>(ws.colp.p), gate);
+    } else if (P.kind == POTGPU_COST_DENSE) {
+      SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
+      sweep_collse_f32<SrcDenseF32><<<g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, lo, hi, g.rows_per_cta,
+                                                                        reinterpret_cast<float2*>(ws.colp.p), gate);
+    } else {
+      SrcPointsF32 s{P.XS4.p, P.YS4.p};
+      sweep_collse_f32<SrcPointsF32><<<g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, lo, hi, g.rows_per_cta,
+                                                                         reinterpret_cast<float2*>(ws.colp.p), gate);
+    }
+  }
+
+  int lse_fmt() const { return P.dtype == POTGPU_F64 ? LP_F64 : LP_F32; }
+
   void row_lse(const int* gate) {  // at the current v
     const int64_t n = P.n;
-    if (P.dtype == POTGPU_F64) {
-      sweep_rowlse_f64<<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.v, ws.g.rows_per_cta,
-                                                               reinterpret_cast<double2*>(ws.rowp.p), gate);
-    } else {
-      launch_sweep(cx, P, ws, zv_slot(), nullptr, nullptr, gate, false, gamma);  // rows of (0, v, 0)
+    const double* rowp = ws.rowp.p;
+    int64_t nstrips = ws.nstrips;
+    int fmt = lse_fmt();
+    if (!cx.comm.sharded()) {
+      row_sweep(gate, nullptr);
+    } else {  // rows are whole in a shard: gather (M, S) of own rows, SUM
+      for (size_t p = 0; p < ws.shards.size(); ++p) {
+        const ShardGrid& sh = ws.shards[p];
+        row_sweep(gate, &sh);
+        k_shard_gather_lse<true><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, fmt, n, sh.lo, sh.hi,
+                                                                        ws.xsend.p + p * ws.xstride, gate);
+      }
+      shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, 2 * n, NcclApi::kSum, ws.xrecv.p, gate);
+      rowp = ws.xrecv.p;
+      nstrips = 1;
+      fmt = LP_F64;
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.v, 0, gate);
-    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, ws.rowp.p, ws.nstrips,
-                                                      P.dtype == POTGPU_F64 ? LP_F64 : LP_F32, gate);
+    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, rowp, nstrips, fmt, gate);
   }
 
   void col_lse(int update, const int* gate) {  // at the current u
     const int64_t n = P.n;
-    if (P.dtype == POTGPU_F64) {
-      sweep_collse_f64<<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.u, ws.g.rows_per_cta,
-                                                               reinterpret_cast<double2*>(ws.colp.p), gate);
-    } else if (P.kind == POTGPU_COST_DENSE) {
-      SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
-      sweep_collse_f32<SrcDenseF32><<<ws.g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, ws.g.rows_per_cta,
-                                                                           reinterpret_cast<float2*>(ws.colp.p), gate);
-    } else {
-      SrcPointsF32 s{P.XS4.p, P.YS4.p};
-      sweep_collse_f32<SrcPointsF32><<<ws.g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, ws.g.rows_per_cta,
-                                                                            reinterpret_cast<float2*>(ws.colp.p), gate);
+    const double* colp = ws.colp.p;
+    int64_t nrb = ws.nrb;
+    int fmt = lse_fmt();
+    if (!cx.comm.sharded()) {
+      col_sweep(gate, nullptr);
+    } else {  // column LSE over shards: MAX of the shard maxima, rescale, SUM
+      for (size_t p = 0; p < ws.shards.size(); ++p) {
+        const ShardGrid& sh = ws.shards[p];
+        col_sweep(gate, &sh);
+        k_shard_gather_lse<false><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.colp.p, sh.g.grid.y, fmt, n, sh.lo, sh.hi,
+                                                                         ws.xsend.p + p * ws.xstride, gate);
+      }
+      shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, n, NcclApi::kMax, ws.xrecv.p, gate);
+      k_shard_lse_rescale<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.xsend.p, int(ws.shards.size()), ws.xstride, n,
+                                                                  ws.xrecv.p, gate);
+      shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p + n, ws.xstride, n, NcclApi::kSum, ws.xrecv.p + n, gate);
+      colp = ws.xrecv.p;
+      nrb = 1;
+      fmt = LP_SPLIT;
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
-    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, ws.colp.p, ws.nrb, P.dtype == POTGPU_F64 ? LP_F64 : LP_F32,
-                                                      update, sk_blocks(), gate);
+    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, colp, nrb, fmt, update, sk_blocks(), gate);
   }
 
   // solvers.hpp:463-476: u update, v update, B, E, ++iterations, record
@@ -320,20 +370,21 @@ struct SinkhornSession : Session {
   double time_sweep(int reps, double* elems, double* bytes) override {
     if (trivial) throw Error(POTGPU_INVALID_ARGUMENT, "trivial solve has no sweep");
     col_lse(0, nullptr);
+    int64_t rows = 0;
+    auto sweeps = [&] {
+      rows = 0;
+      if (!cx.comm.sharded()) { col_sweep(nullptr, nullptr); rows = P.n; return; }
+      for (const ShardGrid& sh : ws.shards) { col_sweep(nullptr, &sh); rows += sh.hi - sh.lo; }
+    };
     PG_CK(cudaEventRecord(ev0, cx.stream));
-    for (int k = 0; k < reps; ++k) {
-      if (P.dtype == POTGPU_F64)
-        sweep_collse_f64<<<ws.g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, P.n, sv.u, ws.g.rows_per_cta,
-                                                                 reinterpret_cast<double2*>(ws.colp.p), nullptr);
-      else col_lse(0, nullptr);
-    }
+    for (int k = 0; k < reps; ++k) sweeps();
     PG_CK(cudaEventRecord(ev1, cx.stream));
     PG_CK(cudaEventSynchronize(ev1));
     float fms = 0.f;
     PG_CK(cudaEventElapsedTime(&fms, ev0, ev1));
     const double n = double(P.n);
-    if (elems) *elems = n * n;
-    if (bytes) *bytes = n * n * stream_bytes_per_elem(P);
+    if (elems) *elems = double(rows) * n;
+    if (bytes) *bytes = double(rows) * n * stream_bytes_per_elem(P);
     return double(fms) / reps;
   }
 

@@ -17,7 +17,8 @@
 
 namespace potgpu {
 
-enum LsePartialFormat { LP_F64 = 0, LP_F32 = 1 };  // double2 (m, S) natural log | float2 (S, m) log2
+// double2 (m, S) natural log | float2 (S, m) log2 | split: m at p[k], S at p[split + k]
+enum LsePartialFormat { LP_F64 = 0, LP_F32 = 1, LP_SPLIT = 2 };
 
 __device__ __forceinline__ void lse_part(const double* p, int64_t idx, int fmt, double& m, double& S) {
   if (fmt == LP_F64) {
@@ -42,7 +43,7 @@ __device__ __forceinline__ void lse_merge(double& m, double& S, double m2, doubl
 // ---------------------------------------------------------------- fp64 --
 // Row LSE: x_ij = logK_ij + v_j (solvers.hpp:464-466).
 __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __restrict__ L, int64_t ld, int64_t n,
-                                                               const double* __restrict__ v, int rows_per_cta,
+                                                               const double* __restrict__ v, int64_t row_lo, int64_t row_hi, int rows_per_cta,
                                                                double2* rowp, const int* gate) {
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __
       const int64_t j = j0 + 2 * lane + 64 * k + e;
       vj[2 * k + e] = j < n ? v[j] : 0.0;  // padding columns of L hold -inf
     }
-  const int64_t r0 = int64_t(blockIdx.y) * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  const int64_t r0 = row_lo + int64_t(blockIdx.y) * rows_per_cta, r1 = min(row_hi, r0 + rows_per_cta);
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
     const double2* row = reinterpret_cast<const double2*>(L + i * ld + j0) + lane;
     double x[8];
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __
 // Column LSE: x_ij = logK_ij + u_i (solvers.hpp:469-471), rows in chunks of
 // 4 with a per-column running max.
 __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f64(const double* __restrict__ L, int64_t ld, int64_t n,
-                                                               const double* __restrict__ u, int rows_per_cta,
+                                                               const double* __restrict__ u, int64_t row_lo, int64_t row_hi, int rows_per_cta,
                                                                double2* colp, const int* gate) {
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f64(const double* __
   double m[8], S[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) { m[k] = -INFINITY; S[k] = 0.0; }
-  const int64_t r0 = int64_t(blockIdx.y) * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  const int64_t r0 = row_lo + int64_t(blockIdx.y) * rows_per_cta, r1 = min(row_hi, r0 + rows_per_cta);
   constexpr int R = 2;  // rows per chunk (register budget: no spills)
   for (int64_t base = r0 + R * warp; base < r1; base += R * kWarps) {
     double x[R][8];
@@ -146,7 +147,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f64(const double* __
 // partial = float2 (S, m) meaning S 2^m.
 template <class Src>
 __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t n, const double* __restrict__ u,
-                                                               int rows_per_cta, float2* colp, const int* gate) {
+                                                               int64_t row_lo, int64_t row_hi, int rows_per_cta,
+                                                               float2* colp, const int* gate) {
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t
   float m[2 * kPairs], S[2 * kPairs];
 #pragma unroll
   for (int k = 0; k < 2 * kPairs; ++k) { m[k] = -INFINITY; S[k] = 0.f; }
-  const int64_t r0 = int64_t(blockIdx.y) * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  const int64_t r0 = row_lo + int64_t(blockIdx.y) * rows_per_cta, r1 = min(row_hi, r0 + rows_per_cta);
   constexpr int R = 2;
   for (int64_t base = r0 + R * warp; base < r1; base += R * kWarps) {
     float2 t[R][kPairs];
@@ -227,6 +229,33 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t
       for (int w = 0; w < kWarps; ++w)
         if (sm[w][c] != -INFINITY) SS += sS[w][c] * ex2f(sm[w][c] - M);
     if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(M == -INFINITY ? 0.f : SS, M == -INFINITY ? 0.f : M);
+  }
+}
+
+// Sharded Sinkhorn (shard.cuh): one shard's LSE partials -> its slice of
+// the all-reduce vector. ROWS: (M_i, S_i) pairs (LP_F64 layout) for the
+// shard's rows, exact (0, 0) elsewhere (SUM-reduced). COLS: m_j at out[j],
+// S_j at out[n + j] (MAX-reduced, rescaled, SUM-reduced).
+template <bool ROWS>
+__global__ void k_shard_gather_lse(const double* p, int64_t cnt, int fmt, int64_t n, int64_t lo, int64_t hi, double* out,
+                                   const int* gate) {
+  if (gate && *gate == 0) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double M = -INFINITY, S = 0.0;
+    if (!ROWS || (i >= lo && i < hi))
+      for (int64_t k = 0; k < cnt; ++k) {
+        double m2, S2;
+        lse_part(p, i * cnt + k, fmt, m2, S2);
+        lse_merge(M, S, m2, S2);
+      }
+    if (ROWS) {
+      const bool own = i >= lo && i < hi;
+      out[2 * i] = own ? M : 0.0;
+      out[2 * i + 1] = own ? S : 0.0;
+    } else {
+      out[i] = M;
+      out[n + i] = S;
+    }
   }
 }
 
@@ -300,7 +329,14 @@ constexpr int kSkTPI = 4;  // threads per index
 // log-sum-exp of the cnt (max, sum) partials at p[base..] of one index,
 // split over a group of kSkTPI threads (max pass, then sum pass); result as
 // (M, S) in natural-log units, replicated in the group.
-__device__ __forceinline__ void group_lse(const double* p, int64_t base, int64_t cnt, int fmt, int q, double& M, double& S) {
+__device__ __forceinline__ void group_lse(const double* p, int64_t base, int64_t cnt, int fmt, int q, double& M, double& S,
+                                          int64_t split = 0) {
+  if (fmt == LP_SPLIT) {  // one (m, S) per index (all-reduced shards)
+    M = p[base];
+    S = p[split + base];
+    if (S == 0.0) M = -INFINITY;
+    return;
+  }
   M = -INFINITY;
   for (int64_t k = q; k < cnt; k += kSkTPI) {
     double m2, S2;
@@ -378,7 +414,7 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv
     const bool live = j < n;
     const int64_t jj = live ? j : n - 1;
     double M, S;
-    group_lse(colp, jj * nrb, nrb, fmt, q, M, S);
+    group_lse(colp, jj * nrb, nrb, fmt, q, M, S, n);
     if (!live || q != 0) continue;
     lse_merge(M, S, -0.0 + un, 1.0);
     const double lse = M + log(S);

@@ -20,6 +20,7 @@ namespace potgpu {
 
 struct SweepArgs {
   int64_t n;            // plan side
+  int64_t row_lo, row_hi;  // the row shard this launch covers ([0, n) unsharded)
   int rows_per_cta;
   const double* u;      // point (fp64 potentials)
   const double* v;
@@ -66,8 +67,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __r
 #pragma unroll
   for (int k = 0; k < 8; ++k) cacc[k] = 0.0;
   double mx = -INFINITY;
-  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
-  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
     double ui = a.u[i];
     if (a.lu) ui = ui + a.lu[i];
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
-  const int64_t r0 = int64_t(blockIdx.y) * a.rows_per_cta;
-  const int64_t r1 = min(n, r0 + a.rows_per_cta);
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
   const double w = *a.w;
   // row potentials of this CTA's rows, once, into shared memory
   extern __shared__ float s_A[];
@@ -373,11 +374,11 @@ inline int64_t gcd64(int64_t a, int64_t b) {
   return a;
 }
 
-inline SweepGrid choose_grid(int64_t n, int num_sms, int occupancy, int strip_cols) {
-  const int64_t strips = ceil_div(n, strip_cols);
+inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occupancy, int strip_cols) {
+  const int64_t strips = ceil_div(ncols, strip_cols);
   const int64_t cap = int64_t(num_sms) * occupancy;
   const int64_t base = cap / gcd64(cap, strips);  // row blocks per quantum
-  const int64_t max_rb = std::max<int64_t>(1, n / 8);
+  const int64_t max_rb = std::max<int64_t>(1, nrows / 8);
   int64_t rb;
   if (base <= max_rb) {
     // about 8 CTAs per resident slot per SM when n allows, at least 1 quantum
@@ -388,8 +389,8 @@ inline SweepGrid choose_grid(int64_t n, int num_sms, int occupancy, int strip_co
     rb = std::min<int64_t>(max_rb, std::max<int64_t>(1, ceil_div(2 * cap, strips)));
   }
   SweepGrid g;
-  g.rows_per_cta = int(ceil_div(n, rb));
-  rb = ceil_div(n, g.rows_per_cta);
+  g.rows_per_cta = int(ceil_div(std::max<int64_t>(nrows, 1), rb));
+  rb = ceil_div(std::max<int64_t>(nrows, 1), g.rows_per_cta);
   g.grid = dim3(unsigned(strips), unsigned(rb), 1);
   return g;
 }

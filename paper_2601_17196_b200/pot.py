@@ -22,7 +22,7 @@ import enum
 import math
 import os
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -144,7 +144,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_solve", "potgpu_dual_eval", "potgpu_round_pot", "potgpu_comm_unique_id", "potgpu_comm_init",
     "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
-    "potgpu_session_stats", "potgpu_solve_batched",
+    "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
 )
 
 _lib = None
@@ -177,6 +177,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_solve_batched.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), ctypes.c_int64, P(_Config),
                                          P(_Summary), P(_Outputs), ctypes.c_int]
     lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
+    lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+    lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.potgpu_comm_info.argtypes = [ctypes.c_void_p, P(ctypes.c_int), P(ctypes.c_int), P(ctypes.c_int)]
     lib.potgpu_make_synthetic.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_double, dp, dp, dp, dp]
     lib.potgpu_make_config.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, dp, dp, dp, dp,
@@ -303,6 +307,25 @@ class Context:
         self._h = h
         self.device = device
 
+    def shard_local(self, shards: int) -> "Context":
+        """Run the row-sharded arithmetic with `shards` shards in this
+        process (potgpu_comm_init_local): the multi-GPU data path on one GPU."""
+        _check(load_library().potgpu_comm_init_local(self._h, int(shards)))
+        return self
+
+    def init_comm(self, rank: int, world_size: int, unique_id: bytes) -> "Context":
+        """Join a row-sharded multi-GPU job (potgpu_comm_init, NCCL)."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        _check(load_library().potgpu_comm_init(self._h, int(rank), int(world_size), bytes(unique_id)))
+        return self
+
+    def comm_info(self) -> Tuple[int, int, int]:
+        """(rank, world_size, shards_per_rank)."""
+        r, w, v = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load_library().potgpu_comm_info(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(v)))
+        return r.value, w.value, v.value
+
     def close(self):
         if self._h:
             load_library().potgpu_destroy(self._h)
@@ -313,6 +336,31 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """potgpu_comm_unique_id: the 128-byte NCCL id rank 0 broadcasts."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().potgpu_comm_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(n: int, world: int, shards_per_rank: int = 1) -> List[Tuple[int, int]]:
+    """Row range [lo, hi) of every shard of a sharded job, in shard order
+    (rank r owns shards r*shards_per_rank ...); the split of shard.cuh Comm."""
+    total = world * shards_per_rank
+    return [((n * s) // total, (n * (s + 1)) // total) for s in range(total)]
+
+
+def init_distributed(ctx: Context, group=None) -> Context:
+    """Join the torch.distributed job this process belongs to as one rank of
+    a row-sharded solve: rank 0 creates the NCCL id, torch.distributed
+    broadcasts it (any backend), every rank initialises its communicator."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return ctx.init_comm(rank, world, box[0])
 
 
 _default_ctx: Optional[Context] = None
