@@ -92,6 +92,7 @@ struct ReduceArgs {
   double* scratch;                      // [gridDim.x][kNumAcc]
   const int* gate;
   int pfmt;                             // PartialFormat of rowp/colp
+  const double* rowshift;               // source row term of the fp32 row offset (log2), may be null
   // mode 1: no sweep; the point differs from a source point only in w, so
   // B = B(src) e^(w - w_src): sums are scaled (source b when *select_b).
   int mode;
@@ -250,7 +251,9 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     const double ui = u[ii], vi = v[ii];
     double rb, cb;
     if (a.mode == 0) {
-      rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, (ui + w) * kLog2e, q);
+      double off = (ui + w) * kLog2e;
+      if (a.rowshift) off = off + a.rowshift[ii];
+      rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
       cb = group_partial_sum(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
     } else {
       rb = srow[ii] * fs;

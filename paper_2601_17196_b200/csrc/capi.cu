@@ -184,15 +184,30 @@ __global__ void k_scale_points(const float4* X, int64_t n, float sc, float4* out
   }
 }
 
-// Coordinates pre-scaled by sqrt(log2 e * scale / gamma): the fp32 sweep's
+// 2 x' and the exact (fp64) squared norms -|x'|^2, -|y'|^2 of the scaled
+// coordinates for the expanded-norm sweep (SrcPointsDotF32).
+__global__ void k_dot_prep(const float4* XS, const float4* YS, int64_t n, float4* XD, double* xshift, double* yshift) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 a = XS[i], b = YS[i];
+    XD[i] = make_float4(2.f * a.x, 2.f * a.y, 2.f * a.z, 0.f);
+    xshift[i] = -((double(a.x) * a.x + double(a.y) * a.y) + double(a.z) * a.z);
+    yshift[i] = -((double(b.x) * b.x + double(b.y) * b.y) + double(b.z) * b.z);
+  }
+}
+
+// Coordinates pre-scaled by sqrt(log2 e * scale / gamma): the fp32 sweeps'
 // kappa is then |x' - y'|^2 in log2 units.
 void prepare_points(Context& cx, DevProblem& P, double gamma) {
   if (P.kind != POTGPU_COST_SQEUCLIDEAN || P.XS_gamma == gamma) return;
   P.XS4.alloc(size_t(P.n));
   P.YS4.alloc(size_t(P.n));
+  P.XD4.alloc(size_t(P.n));
+  P.xshift.alloc(size_t(P.n));
+  P.yshift.alloc(size_t(P.n));
   const float sc = float(std::sqrt(kLog2e * P.cost_scale / gamma));
   k_scale_points<<<cx.num_sms * 4, 256, 0, cx.stream>>>(P.X4.p, P.n, sc, P.XS4.p);
   k_scale_points<<<cx.num_sms * 4, 256, 0, cx.stream>>>(P.Y4.p, P.n, sc, P.YS4.p);
+  k_dot_prep<<<cx.num_sms * 4, 256, 0, cx.stream>>>(P.XS4.p, P.YS4.p, P.n, P.XD4.p, P.xshift.p, P.yshift.p);
   PG_CK(cudaGetLastError());
   P.XS_gamma = gamma;
 }

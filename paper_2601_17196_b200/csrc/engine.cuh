@@ -43,8 +43,12 @@ struct DevProblem {
   double L_gamma = -1.0;   // gamma L64 was built for
   DevBuf<float> C32;       // fp32 dense C (n x ld), 0-padded
   DevBuf<float4> X4, Y4;   // fp32 points
-  DevBuf<float4> XS4, YS4; // points pre-scaled by sqrt(log2 e * scale / gamma) for the fp32 sweep
+  DevBuf<float4> XS4, YS4; // points pre-scaled by sqrt(log2 e * scale / gamma) for the fp32 sweeps
+  DevBuf<float4> XD4;      // 2 x' (expanded-norm sweep, SrcPointsDotF32)
+  DevBuf<double> xshift, yshift;  // -|x'_i|^2, -|y'_j|^2 (fp64, log2 units)
   double XS_gamma = -1.0;
+  bool dot_form() const { return kind == POTGPU_COST_SQEUCLIDEAN && dtype == POTGPU_F32; }
+  const double* rowshift() const { return dot_form() ? xshift.p : nullptr; }
   double cost_scale = 1.0;
   double cmax = 0.0;
   std::vector<double> r, c;  // host copies (original marginals)
@@ -106,7 +110,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   } else if (P.kind == POTGPU_COST_DENSE) {
     PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f32<SrcDenseF32>, kThreads, 0));
   } else {
-    PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f32<SrcPointsF32>, kThreads, 0));
+    PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f32<SrcPointsDotF32>, kThreads, 0));
   }
   occ = std::max(occ, 1);
   ws.strip = P.dtype == POTGPU_F64 ? kStripCols : kStripCols32;
@@ -134,7 +138,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : sweep_f32_smem(max_rpc);
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcPointsF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcPointsDotF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
   }
   ws.nstrips = ws.g.grid.x;
   ws.nrb = ws.g.grid.y;
@@ -173,6 +177,8 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
   a.rows_per_cta = g.rows_per_cta;
   a.u = z.u(); a.v = z.v(); a.w = z.w();
   a.lu = lu; a.lv = lv;
+  a.rowshift = P.rowshift();
+  a.colshift = P.dot_form() ? P.yshift.p : nullptr;
   a.rowp = ws.rowp.p; a.colp = ws.colp.p; a.maxp = ws.maxp.p;
   a.gate = gate;
   a.gamma = gamma;
@@ -184,8 +190,8 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
     sweep_f32<SrcDenseF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   } else {
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
-    SrcPointsF32 s{P.XS4.p, P.YS4.p};
-    sweep_f32<SrcPointsF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
+    SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
+    sweep_f32<SrcPointsDotF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
   }
   PG_CK(cudaGetLastError());
 }
@@ -198,6 +204,7 @@ struct SweepOut {
   const double* colp; int64_t nrb;
   const double* maxp; int64_t nmax;
   int pfmt;
+  const double* rowshift;  // source row term of the fp32 row offsets (raw partials only)
 };
 
 // The hot path of every evaluation: sweep B(z) (own rows) and, when sharded,
@@ -207,19 +214,20 @@ inline SweepOut sweep_point(Context& cx, const DevProblem& P, Workspace& ws, Slo
   const int64_t n = P.n;
   if (!cx.comm.sharded()) {
     launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma);
-    return SweepOut{ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.maxp.p, ws.nstrips * ws.nrb, ws.pfmt};
+    return SweepOut{ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.maxp.p, ws.nstrips * ws.nrb, ws.pfmt, P.rowshift()};
   }
   for (size_t p = 0; p < ws.shards.size(); ++p) {
     const ShardGrid& sh = ws.shards[p];
     launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma, &sh);
     k_shard_gather<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, ws.colp.p, sh.g.grid.y, ws.maxp.p,
-                                                          int64_t(sh.g.grid.x) * sh.g.grid.y, ws.pfmt, z, lu, sh.lo, sh.hi,
+                                                          int64_t(sh.g.grid.x) * sh.g.grid.y, ws.pfmt, z, lu, P.rowshift(),
+                                                          sh.lo, sh.hi,
                                                           sh.index, ws.nshards, ws.xsend.p + p * ws.xstride, gate);
     PG_CK(cudaGetLastError());
   }
   shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, 2 * n + ws.nshards, NcclApi::kSum, ws.xrecv.p,
                   gate);
-  return SweepOut{ws.xrecv.p, 1, ws.xrecv.p + n, 1, ws.xrecv.p + 2 * n, ws.nshards, PF_F64};
+  return SweepOut{ws.xrecv.p, 1, ws.xrecv.p + n, 1, ws.xrecv.p + 2 * n, ws.nshards, PF_F64, nullptr};
 }
 
 // Device time of the hot-path sweeps alone (no reduction) over this
@@ -263,6 +271,7 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.scratch = ws.scratch.p;
   r.gate = gate;
   r.pfmt = so.pfmt;
+  r.rowshift = so.rowshift;
   r.mode = scaled ? 1 : 0;
   k_point_eval<<<ws.eval_blocks, kEvalThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());

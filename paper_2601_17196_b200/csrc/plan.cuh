@@ -17,11 +17,12 @@ namespace potgpu {
 // with the fp32 row-partial offset (u_i + lu_i + w) log2 e.
 __global__ void __launch_bounds__(kVecThreads) k_sum_partials(const double* rowp, int64_t nstrips, const double* colp,
                                                              int64_t nrb, int pfmt, Slot z, const double* lu,
-                                                             double* row, double* col) {
+                                                             const double* rowshift, double* row, double* col) {
   const int64_t n = z.n;
   const double w = *z.w();
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const double a2 = ((z.u()[i] + (lu ? lu[i] : 0.0)) + w) * kLog2e;
+    double a2 = ((z.u()[i] + (lu ? lu[i] : 0.0)) + w) * kLog2e;
+    if (rowshift) a2 = a2 + rowshift[i];
     double rr = 0.0, cc = 0.0;
     for (int64_t s = 0; s < nstrips; ++s) rr += partial_value(rowp, i * nstrips + s, pfmt, a2);
     for (int64_t s = 0; s < nrb; ++s) cc += partial_value(colp, i * nrb + s, pfmt);
@@ -95,7 +96,7 @@ struct PlanEngine {
     if (lv) up(1, *lv);
     const SweepOut so = sweep_point(cx, P, ws, z, lu ? d(0) : nullptr, lv ? d(1) : nullptr, nullptr, false, gamma);
     k_sum_partials<<<ws.nblk, kVecThreads, 0, cx.stream>>>(so.rowp, so.nstrips, so.colp, so.nrb, so.pfmt, z,
-                                                           lu ? d(0) : nullptr, d(2), d(3));
+                                                           lu ? d(0) : nullptr, so.rowshift, d(2), d(3));
     PG_CK(cudaGetLastError());
     row.resize(size_t(n));
     col.resize(size_t(n));

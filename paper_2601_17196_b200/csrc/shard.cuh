@@ -118,15 +118,16 @@ __global__ void k_shard_reduce(const double* send, int nsend, int64_t stride, in
 // out[i] (rows, own rows only), out[n + j] (columns), out[2n + s] (max
 // exponent of shard s; 0 in the other shards' slots).
 __global__ void k_shard_gather(const double* rowp, int64_t nstrips, const double* colp, int64_t nrb, const double* maxp,
-                               int64_t nmax, int pfmt, Slot z, const double* lu, int64_t lo, int64_t hi, int shard,
-                               int nshards, double* out, const int* gate) {
+                               int64_t nmax, int pfmt, Slot z, const double* lu, const double* rowshift, int64_t lo,
+                               int64_t hi, int shard, int nshards, double* out, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = z.n;
   const double w = *z.w();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double rr = 0.0;
     if (i >= lo && i < hi) {
-      const double a2 = ((z.u()[i] + (lu ? lu[i] : 0.0)) + w) * kLog2e;
+      double a2 = ((z.u()[i] + (lu ? lu[i] : 0.0)) + w) * kLog2e;
+      if (rowshift) a2 = a2 + rowshift[i];
       for (int64_t s = 0; s < nstrips; ++s) rr += partial_value(rowp, i * nstrips + s, pfmt, a2);
     }
     double cc = 0.0;

@@ -97,7 +97,7 @@ struct SinkhornSession : Session {
         const ShardGrid& sh = ws.shards[p];
         row_sweep(gate, &sh);
         k_shard_gather_lse<true><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, fmt, n, sh.lo, sh.hi,
-                                                                        ws.xsend.p + p * ws.xstride, gate);
+                                                                        P.rowshift(), ws.xsend.p + p * ws.xstride, gate);
       }
       shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, 2 * n, NcclApi::kSum, ws.xrecv.p, gate);
       rowp = ws.xrecv.p;
@@ -105,7 +105,8 @@ struct SinkhornSession : Session {
       fmt = LP_F64;
     }
     k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.v, 0, gate);
-    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, rowp, nstrips, fmt, gate);
+    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, rowp, nstrips, fmt,
+                                                      cx.comm.sharded() ? nullptr : P.rowshift(), gate);
   }
 
   void col_lse(int update, const int* gate) {  // at the current u
@@ -120,7 +121,7 @@ struct SinkhornSession : Session {
         const ShardGrid& sh = ws.shards[p];
         col_sweep(gate, &sh);
         k_shard_gather_lse<false><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.colp.p, sh.g.grid.y, fmt, n, sh.lo, sh.hi,
-                                                                         ws.xsend.p + p * ws.xstride, gate);
+                                                                         nullptr, ws.xsend.p + p * ws.xstride, gate);
       }
       shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, n, NcclApi::kMax, ws.xrecv.p, gate);
       k_shard_lse_rescale<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.xsend.p, int(ws.shards.size()), ws.xstride, n,

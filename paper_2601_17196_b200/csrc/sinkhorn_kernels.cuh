@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t
 // shard's rows, exact (0, 0) elsewhere (SUM-reduced). COLS: m_j at out[j],
 // S_j at out[n + j] (MAX-reduced, rescaled, SUM-reduced).
 template <bool ROWS>
-__global__ void k_shard_gather_lse(const double* p, int64_t cnt, int fmt, int64_t n, int64_t lo, int64_t hi, double* out,
-                                   const int* gate) {
+__global__ void k_shard_gather_lse(const double* p, int64_t cnt, int fmt, int64_t n, int64_t lo, int64_t hi,
+                                   const double* rowshift, double* out, const int* gate) {
   if (gate && *gate == 0) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double M = -INFINITY, S = 0.0;
@@ -248,6 +248,7 @@ __global__ void k_shard_gather_lse(const double* p, int64_t cnt, int fmt, int64_
         lse_part(p, i * cnt + k, fmt, m2, S2);
         lse_merge(M, S, m2, S2);
       }
+    if (ROWS && rowshift && M != -INFINITY) M = M + rowshift[i] * kLn2;
     if (ROWS) {
       const bool own = i >= lo && i < hi;
       out[2 * i] = own ? M : 0.0;
@@ -373,7 +374,7 @@ __device__ __forceinline__ void group_lse(const double* p, int64_t base, int64_t
 // LSE_i + the dummy column (logK_in = -0, x = v_n); row sums of B(u, v) =
 // exp(u_i + LSE_i); next u = log r - LSE.
 __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
-                                                        int fmt, const int* gate) {
+                                                        int fmt, const double* rowshift, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double vn = sv.v[n];
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv
     double M, S;
     group_lse(rowp, ii * nstrips, nstrips, fmt, q, M, S);
     if (!live || q != 0) continue;
+    if (rowshift && M != -INFINITY) M = M + rowshift[i] * kLn2;  // the source's row term (log2 -> natural)
     lse_merge(M, S, -0.0 + vn, 1.0);
     const double lse = M + log(S);
     const double row = exp(sv.u[i] + lse);

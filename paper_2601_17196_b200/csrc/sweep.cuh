@@ -14,6 +14,8 @@
 // (deterministic run to run).
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace potgpu {
@@ -27,6 +29,8 @@ struct SweepArgs {
   const double* w;
   const double* lu;     // optional additive row log-weights (rounding), may be null
   const double* lv;     // optional additive column log-weights
+  const double* rowshift;  // optional per-row / per-column exponent terms (log2 units) of the
+  const double* colshift;  // source (expanded-norm points: -|x'_i|^2, -|y'_j|^2); may be null
   double* rowp;         // [n][gridDim.x]: row partials, one per strip (contiguous per row)
   double* colp;         // [n][gridDim.y]: column partials, one per row block
   double* maxp;         // [gridDim.y][gridDim.x]: max exponent (natural log units)
@@ -184,6 +188,30 @@ struct SrcPointsF32 {
   }
 };
 
+// On-the-fly squared-Euclidean cost in expanded form: kappa = |x'|^2 +
+// |y'|^2 - 2 x'.y'. The norms are exact fp64 terms folded into the row offset
+// (rowshift = -|x'_i|^2) and the column constant (colshift = -|y'_j|^2), so
+// the per-entry exponent is one 3-deep FFMA2 chain on (2 x'_i) . y'_j —
+// half the FP32-pipe work of the difference form. Rounding happens at the
+// magnitude of B_j, as in the difference form.
+struct SrcPointsDotF32 {
+  const float4* X2;  // 2 x'_i (exact doubling of the pre-scaled coordinates)
+  const float4* Ys;  // y'_j
+  struct Col { float2 x, y, z; };
+  struct RowData { float4 p; };
+  static constexpr bool kHasCols = true;
+  __device__ __forceinline__ RowData load(int64_t i, int64_t, int) const { return RowData{X2[i]}; }
+  __device__ __forceinline__ void expo(const RowData& d, const Col* c, const float2 (&B)[kPairs], float2 (&t)[kPairs]) const {
+    const float2 px = make_float2(d.p.x, d.p.x), py = make_float2(d.p.y, d.p.y), pz = make_float2(d.p.z, d.p.z);
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      float2 tt = __ffma2_rn(px, c[q].x, B[q]);
+      tt = __ffma2_rn(py, c[q].y, tt);
+      t[q] = __ffma2_rn(pz, c[q].z, tt);
+    }
+  }
+};
+
 // Dynamic shared memory of the fp32 sweep: row potentials (rows_per_cta
 // floats, padded to 16 B) then 8 per-warp 32x33 row-sum tiles.
 __host__ __device__ constexpr int kRowTileOffset(int rows_per_cta) { return (rows_per_cta + 3) & ~3; }
@@ -216,9 +244,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
     double ud = a.u[i];
     if (a.lu) ud = ud + a.lu[i];
-    s_A[i - r0] = float((ud + w) * kLog2e);
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    s_A[i - r0] = float(A);
   }
-  float2 Bj[kPairs];  // v_j log2 e (+ lv_j)
+  float2 Bj[kPairs];  // v_j log2 e (+ lv_j) (+ colshift_j)
   typename Src::Col cols[kPairs];
 #pragma unroll
   for (int q = 0; q < kPairs; ++q) {
@@ -231,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
         vv = a.v[j];
         if (a.lv) vv = vv + a.lv[j];
         vv = vv * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
       }
       b[h] = float(vv);
     }
@@ -361,32 +392,46 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
 }
 
 // ------------------------------------------------------------------------
-// Grid shape: a 1-D-equivalent grid of (strips x row blocks) whose CTA count
-// is a multiple of the resident CTA capacity (SMs x occupancy) when that is
-// possible, so no partial last wave.
+// Grid shape: strips x row blocks, the row-block count chosen so the CTA
+// count fills the resident capacity (SMs x occupancy) as evenly as possible.
 struct SweepGrid {
   dim3 grid;
   int rows_per_cta;
 };
 
-inline int64_t gcd64(int64_t a, int64_t b) {
-  while (b) { const int64_t t = a % b; a = b; b = t; }
-  return a;
+// Target waves of resident CTAs per sweep ($POTGPU_SWEEP_WAVES, default 1:
+// measured on B200 at n = 16384, one wave of long-lived CTAs beats 8 waves
+// by 17% (per-CTA prologue/epilogue and fewer column partials); see
+// profiles/waves.sh).
+inline int sweep_waves() {
+  static const int w = [] {
+    const char* e = std::getenv("POTGPU_SWEEP_WAVES");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 1;
+  }();
+  return w;
 }
+
+constexpr int64_t kMaxRowsPerCta = 2048;
 
 inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occupancy, int strip_cols) {
   const int64_t strips = ceil_div(ncols, strip_cols);
-  const int64_t cap = int64_t(num_sms) * occupancy;
-  const int64_t base = cap / gcd64(cap, strips);  // row blocks per quantum
+  const int64_t cap = int64_t(num_sms) * occupancy;  // resident CTAs
   const int64_t max_rb = std::max<int64_t>(1, nrows / 8);
-  int64_t rb;
-  if (base <= max_rb) {
-    // about 8 CTAs per resident slot per SM when n allows, at least 1 quantum
-    int64_t quanta = std::max<int64_t>(1, (8 * cap) / (strips * base));
-    while (quanta > 1 && base * quanta > max_rb) --quanta;
-    rb = base * quanta;
-  } else {
-    rb = std::min<int64_t>(max_rb, std::max<int64_t>(1, ceil_div(2 * cap, strips)));
+  // row blocks: about sweep_waves() waves of resident CTAs, the count whose
+  // last wave is fullest (exact multiples of the capacity when possible)
+  // at most kMaxRowsPerCta rows per CTA: the fp32 sweep keeps the CTA's row
+  // potentials in shared memory (8 KB), which must not cost occupancy
+  const int64_t min_rb = std::min<int64_t>(max_rb, ceil_div(nrows, kMaxRowsPerCta));
+  const int64_t target =
+      std::max<int64_t>(min_rb, std::max<int64_t>(1, std::min<int64_t>(max_rb, (sweep_waves() * cap) / strips)));
+  int64_t rb = target;
+  double best = -1.0;
+  for (int64_t k = std::max<int64_t>(min_rb, target / 2); k <= std::min<int64_t>(max_rb, target + target / 2 + 1); ++k) {
+    const int64_t ctas = strips * k;
+    const double eff = double(ctas) / double(ceil_div(ctas, cap) * cap);
+    const double score = eff - 0.01 * double(std::llabs(k - target)) / double(target);
+    if (score > best) { best = score; rb = k; }
   }
   SweepGrid g;
   g.rows_per_cta = int(ceil_div(std::max<int64_t>(nrows, 1), rb));
