@@ -209,6 +209,10 @@ int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep,
 /* Counters of the session so far: kernels launched by iterate(), step
  * attempts (incl. halvings) and n^2 sweeps executed. */
 int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* attempts, int64_t* sweeps);
+/* Device and pinned host blocks freed by finished solves are cached per
+ * device and size class and reused by the next solve (no cudaMalloc /
+ * cudaFree on the solve path after the first); this returns them all. */
+void potgpu_release_cached_memory(void);
 /* The context's CUDA stream (cudaStream_t), for callers that time with events. */
 void* potgpu_ctx_stream(potgpu_ctx* ctx);
 

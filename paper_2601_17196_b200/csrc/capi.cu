@@ -1,6 +1,8 @@
 // capi.cu — the C-ABI (include/potgpu.h): context, problem upload and
 // validation, the accelerated solver driver, dual evaluation.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -139,12 +141,10 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     double maxd2;
     std::memcpy(&maxd2, &hm, sizeof(double));
     P.cost_scale = pr->cost_scale > 0 ? pr->cost_scale : (maxd2 > 0 ? 1.0 / maxd2 : 1.0);
-    // max C under the same fp64 formula as the cost views
-    mx.zero(cx.stream);
-    k_points_max<<<int(std::min<int64_t>(n, 4096)), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, P.cost_scale, mx.p);
-    PG_CK(cudaMemcpyAsync(&hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, cx.stream));
-    PG_CK(cudaStreamSynchronize(cx.stream));
-    std::memcpy(&P.cmax, &hm, sizeof(double));
+    // max C under the fp64 formula of the cost views, max_ij (d2_ij * scale):
+    // rounded multiplication by a positive scale is monotone, so it is
+    // exactly (max_ij d2_ij) * scale — no second pass over the n^2 pairs
+    P.cmax = maxd2 * P.cost_scale;
     if (pr->cost_kind == POTGPU_COST_SQEUCLIDEAN_STORED) {
       // materialise C = scale |x - y|^2 once (fp64 formula of the cost views)
       if (P.dtype == POTGPU_F64) P.C64.alloc(size_t(n * P.ld)); else P.C32.alloc(size_t(n * P.ld));
@@ -273,8 +273,7 @@ bool theory_bounds(const std::vector<double>& r, const std::vector<double>& c, d
   return true;
 }
 
-using HostClock = std::chrono::steady_clock;
-inline double secs(HostClock::time_point a) { return std::chrono::duration<double>(HostClock::now() - a).count(); }
+
 
 void fill_trivial(const DevProblem& P, double gamma, double plan_value, potgpu_summary* sm, potgpu_outputs* out,
                   const potgpu_config& cfg) {
@@ -390,6 +389,7 @@ struct AspotSession : Session {
   int64_t graph_nodes = kKernelsPerAttempt;
   explicit AspotSession(Context& c) : Session(c) {}
   ~AspotSession() override {
+    cudaStreamSynchronize(cx.stream);  // before any buffer returns to the cache
     if (exec) cudaGraphExecDestroy(exec);
   }
 
@@ -466,12 +466,16 @@ struct AspotSession : Session {
       trivial = true;
       return;
     }
+    PhaseTimer pt(cx.stream);
     st = aspot_setup(P, cfg.epsilon);
     gamma = cfg.gamma_override > 0 ? cfg.gamma_override : st.gamma;
     if (!(gamma > 0) || !std::isfinite(gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
     const double step_denom = 3.0 * (ksum(st.mr.data(), n) + ksum(st.mc.data(), n) - P.s);
+    pt.mark("aspot_setup (host)");
     build_logk(cx, P, gamma);
+    pt.mark("build_logk / points");
     prepare_workspace(cx, P, ws, trace_cap, log_cap);
+    pt.mark("prepare_workspace");
     PG_CK(cudaMemcpyAsync(ws.rt.p, st.mr.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     PG_CK(cudaMemcpyAsync(ws.ct.p, st.mc.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     ws.slots.zero(cx.stream);
@@ -499,8 +503,10 @@ struct AspotSession : Session {
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZC, nullptr, nullptr, nullptr, true, gamma), ZC, R_CHECK, nullptr);
     k_init_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p);
     sync_ctl();
+    pt.mark("first evaluation");
     if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
     if (cfg.record_rounded_cost && h.g_active) fill_last_record_cost(round_now(nullptr).cost);
+    pt.mark("record(0) rounding");
     if (cfg.use_graphs) {
       cudaGraph_t graph;
       PG_CK(cudaStreamBeginCapture(cx.stream, cudaStreamCaptureModeThreadLocal));
@@ -512,6 +518,7 @@ struct AspotSession : Session {
       PG_CK(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
     }
+    pt.mark("graph capture");
   }
 
   void launch_attempts(int64_t k) {
@@ -608,8 +615,10 @@ struct AspotSession : Session {
     DevBuf<double> Xd;
     const bool mat = cfg.materialize_plan && out && out->X;
     if (mat) Xd.alloc(size_t(n * n));
+    PhaseTimer pt(cx.stream);
     const PlanResult pr = round_now(mat ? Xd.p : nullptr);
     sync_ctl();
+    pt.mark("final rounding");
     const double wall = secs(t_start);
     sm->status = h.status;
     sm->iterations = h.t;
@@ -752,7 +761,9 @@ static std::unique_ptr<Session> make_session_cx(Context& cx, int kind, const pot
   }
   s->cfg = cfg;
   s->t_start = t_start;
+  PhaseTimer pt(cx.stream);
   upload_problem(cx, pr, s->P);
+  pt.mark("upload + validation");
   check_config(cfg);
   s->begin();
   return s;
@@ -968,6 +979,8 @@ int potgpu_comm_info(potgpu_ctx* c, int* rank, int* world_size, int* shards_per_
     if (shards_per_rank) *shards_per_rank = c->cx.comm.vshards;
   });
 }
+
+void potgpu_release_cached_memory(void) { BlockCache::get().release_all(); }
 
 int potgpu_round_pot(potgpu_ctx*, int64_t, const double*, const double*, const double*, double, double*) {
   g_last_error = "potgpu_round_pot on a dense user plan is not implemented yet";

@@ -5,6 +5,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -69,6 +71,84 @@ struct PointScalars {
 constexpr int kNumPartials = 11;  // total, maxu, maxv, seu, sev, ur, vc, score_u, score_v, gl1u, gl1v
 constexpr int kNumAcc = kNumPartials + 3;  // + maxe (11), minrow (12), mincol (13)
 
+// Process-wide caching allocator for device and pinned host blocks: a freed
+// block is kept (per device, per size class) and handed to the next request
+// of that class, so repeated solves pay neither cudaMalloc / cudaMallocHost
+// (milliseconds each) nor cudaFree (which synchronises the device and would
+// serialise the batched workers). Callers return a block only after the
+// stream that used it has been synchronised (sessions do so in their
+// destructors). potgpu_release_cached_memory() hands everything back.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // never destroyed: outlives static DevBufs
+    return *c;
+  }
+  static size_t size_class(size_t bytes) {
+    if (bytes <= (size_t(1) << 20)) {
+      size_t c = 256;
+      while (c < bytes) c <<= 1;
+      return c;
+    }
+    return (bytes + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1);
+  }
+  void* alloc(size_t bytes, bool host) {
+    const size_t cls = size_class(bytes);
+    int dev = -1;
+    if (!host) cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto it = free_.find(Key{dev, cls});
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = host ? cudaMallocHost(&p, cls) : cudaMalloc(&p, cls);
+    if (e != cudaSuccess) {  // out of memory: drop the cache and retry once
+      cudaGetLastError();
+      release_all();
+      e = host ? cudaMallocHost(&p, cls) : cudaMalloc(&p, cls);
+    }
+    if (e != cudaSuccess)
+      throw Error(POTGPU_ERR_CUDA, std::string(host ? "cudaMallocHost: " : "cudaMalloc: ") + cudaGetErrorString(e));
+    return p;
+  }
+  void free(void* p, size_t bytes, bool host) {
+    if (!p) return;
+    int dev = -1;
+    if (!host) cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu_);
+    free_.emplace(Key{dev, size_class(bytes)}, p);
+  }
+  void release_all() {
+    std::lock_guard<std::mutex> lk(mu_);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : free_) {
+      if (kv.first.dev < 0) {
+        cudaFreeHost(kv.second);
+      } else {
+        cudaSetDevice(kv.first.dev);
+        cudaFree(kv.second);
+      }
+    }
+    free_.clear();
+    cudaSetDevice(cur);
+  }
+
+ private:
+  struct Key {
+    int dev;
+    size_t cls;
+    bool operator<(const Key& o) const { return dev != o.dev ? dev < o.dev : cls < o.cls; }
+  };
+  std::mutex mu_;
+  std::multimap<Key, void*> free_;
+};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -78,7 +158,7 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) BlockCache::get().free(p, count * sizeof(T), false);
     p = nullptr;
     count = 0;
   }
@@ -86,11 +166,27 @@ struct DevBuf {
     if (k <= count && p) return;
     release();
     if (k == 0) return;
-    PG_CK(cudaMalloc(&p, k * sizeof(T)));
+    p = static_cast<T*>(BlockCache::get().alloc(k * sizeof(T), false));
     count = k;
   }
   void zero(cudaStream_t st) {
     if (p) PG_CK(cudaMemsetAsync(p, 0, count * sizeof(T), st));
+  }
+};
+
+// A pinned host object from the cache (control-block mirrors).
+template <class T>
+struct PinnedObj {
+  T* p = nullptr;
+  PinnedObj() = default;
+  PinnedObj(const PinnedObj&) = delete;
+  PinnedObj& operator=(const PinnedObj&) = delete;
+  ~PinnedObj() {
+    if (p) BlockCache::get().free(p, sizeof(T), true);
+  }
+  T* get() {
+    if (!p) p = static_cast<T*>(BlockCache::get().alloc(sizeof(T), true));
+    return p;
   }
 };
 

@@ -2,6 +2,9 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <memory>
 
@@ -24,6 +27,24 @@ inline double ksum(const double* x, int64_t n) {
   }
   return s + c;
 }
+
+using HostClock = std::chrono::steady_clock;
+inline double secs(HostClock::time_point a) { return std::chrono::duration<double>(HostClock::now() - a).count(); }
+
+// $POTGPU_TRACE_SETUP=1: host wall time of the setup / output phases on
+// stderr (after a stream sync), for the e2e breakdown.
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  HostClock::time_point t;
+  explicit PhaseTimer(cudaStream_t s) : on(std::getenv("POTGPU_TRACE_SETUP") != nullptr), st(s), t(HostClock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr, "[potgpu] %-24s %8.3f ms\n", what, secs(t) * 1e3);
+    t = HostClock::now();
+  }
+};
 
 struct Context {
   int device = 0;
@@ -82,12 +103,15 @@ struct Workspace {
   DevBuf<double> ro_r, ro_c;  // original marginals for rounding
   DevBuf<AspotCtl> ctl;
   DevBuf<unsigned> ticket;
+  PinnedObj<AspotCtl> host_ctl_buf;
   AspotCtl* host_ctl = nullptr;  // pinned mirror
+  cudaStream_t stream = nullptr;  // the stream every kernel on these buffers runs on
   DevBuf<TraceDev> trace;
   DevBuf<IterLogDev> iterlog;
   int64_t slot_stride = 0;
   ~Workspace() {
-    if (host_ctl) cudaFreeHost(host_ctl);
+    // blocks return to the cache only once nothing can still use them
+    if (stream) cudaStreamSynchronize(stream);
   }
   Slot slot(int k) const { return Slot{slots.p + k * slot_stride, n}; }
   double* row(int k) const { return sums.p + (2 * k) * n; }
@@ -104,6 +128,7 @@ enum SlotId { S_Z = 0, S_ZC = 1, S_ZB = 2, S_G = 3, S_ZG = 4, S_ZH = 5, S_ZN = 6
 inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, int64_t trace_cap, int64_t log_cap) {
   const int64_t n = P.n;
   ws.n = n;
+  ws.stream = cx.stream;
   int occ = 2;
   if (P.dtype == POTGPU_F64) {
     PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f64_dense<true>, kThreads, 0));
@@ -160,7 +185,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.ro_r.alloc(size_t(n));
   ws.ro_c.alloc(size_t(n));
   ws.ctl.alloc(1);
-  if (!ws.host_ctl) PG_CK(cudaMallocHost(&ws.host_ctl, sizeof(AspotCtl)));
+  if (!ws.host_ctl) ws.host_ctl = ws.host_ctl_buf.get();
   ws.trace.alloc(size_t(std::max<int64_t>(trace_cap, 1)));
   ws.iterlog.alloc(size_t(std::max<int64_t>(log_cap, 1)));
 }

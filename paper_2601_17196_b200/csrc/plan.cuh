@@ -84,6 +84,7 @@ struct PlanEngine {
   PlanEngine(Context& c, const DevProblem& p, Workspace& w, double g) : cx(c), P(p), ws(w), gamma(g) {
     buf.alloc(size_t(10 * P.n));
   }
+  ~PlanEngine() { cudaStreamSynchronize(cx.stream); }
   double* d(int k) { return buf.p + k * P.n; }
   void up(int k, const HVec& h) {
     PG_CK(cudaMemcpyAsync(d(k), h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
@@ -183,8 +184,10 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   // column clip: columns of diag(alpha rho) X1
   HVec lrp(n), lq = vlog(Q0);
   for (size_t i = 0; i < n; ++i) lrp[i] = std::log(rho[i] * P0[i]);
+  PhaseTimer pt(pe.cx.stream);
   HVec rr, cc;
   pe.block_sums(z, &lrp, &lq, rr, cc);
+  pt.mark("round: column clip sums");
   double sra = 0.0;
   if (a) { HVec t(n); for (size_t i = 0; i < n; ++i) t[i] = rho[i] * (*a)[i]; sra = hsum(t); }
   HVec kap(n, 1.0), col3(n);
@@ -196,6 +199,7 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   HVec lp = vlog(P0), lqk(n);
   for (size_t j = 0; j < n; ++j) lqk[j] = std::log(Q0[j] * kap[j]);
   pe.block_sums(z, &lp, &lqk, rr, cc);
+  pt.mark("round: final sums");
   double sbk = 0.0;
   if (b) { HVec t(n); for (size_t j = 0; j < n; ++j) t[j] = (*b)[j] * kap[j]; sbk = hsum(t); }
   HVec rowX3(n), colX3(n);
@@ -241,7 +245,9 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
     for (size_t i = 0; i < n; ++i) ra[i] = alpha * rho[i] * (*a)[i];
     for (size_t j = 0; j < n; ++j) kb[j] = (*b)[j] * kap[j];
   }
+  pt.mark("round: host O(n)");
   out.cost = pe.cost(z, Pf, Qf, &fa2, &fb, a ? &ra : nullptr, a ? &kb : nullptr, Xdev);
+  pt.mark("round: plan cost");
   return out;
 }
 

@@ -30,7 +30,9 @@ struct SinkhornSession : Session {
   DevBuf<double> vec;     // u, u_next, v, log_r, log_c, r, c (each n+1), scratch
   DevBuf<double> zv;      // point (0, v[0..n), 0) for the fp32 row-LSE sweep
   DevBuf<double> zf;      // point (u[0..n), v[0..n), 0) for the output stage
+  DevBuf<double> zuv;     // point (u[0..n), v[0..n), 0) of the fast column pass (fp32)
   DevBuf<SinkCtl> ctl;
+  PinnedObj<SinkCtl> hctl_buf;
   SinkCtl* hctl = nullptr;
   cudaGraphExec_t exec = nullptr;
   int64_t trace_cap = 1;
@@ -39,8 +41,8 @@ struct SinkhornSession : Session {
 
   SinkhornSession(Context& c, int k) : Session(c), kind(k) {}
   ~SinkhornSession() override {
+    cudaStreamSynchronize(cx.stream);  // before any buffer returns to the cache
     if (exec) cudaGraphExecDestroy(exec);
-    if (hctl) cudaFreeHost(hctl);
   }
 
   int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n * kSkTPI, kSkThreads), 4096)); }
@@ -109,17 +111,35 @@ struct SinkhornSession : Session {
                                                       cx.comm.sharded() ? nullptr : P.rowshift(), gate);
   }
 
+  // fp32: the column LSE comes from the fast row-shifted sweep at (u, v_old, 0)
+  // (sweep_f32, the production kernel) with v_old removed in fp64; the exact
+  // per-column-max pass runs only when that flags a flushed column.
+  bool fast_cols() const { return P.dtype == POTGPU_F32; }
+  Slot zuv_slot() const { return Slot{zuv.p, P.n}; }
+
   void col_lse(int update, const int* gate) {  // at the current u
+    k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
+    if (fast_cols()) {
+      col_pass(update, gate, true);
+      col_pass(update, &ctl.p->col_flush, false);  // gated: only after a flush
+    } else {
+      col_pass(update, gate, false);
+    }
+  }
+
+  void col_pass(int update, const int* gate, bool fast) {
     const int64_t n = P.n;
     const double* colp = ws.colp.p;
     int64_t nrb = ws.nrb;
     int fmt = lse_fmt();
     if (!cx.comm.sharded()) {
-      col_sweep(gate, nullptr);
+      if (fast) launch_sweep(cx, P, ws, zuv_slot(), nullptr, nullptr, gate, false, gamma);
+      else col_sweep(gate, nullptr);
     } else {  // column LSE over shards: MAX of the shard maxima, rescale, SUM
       for (size_t p = 0; p < ws.shards.size(); ++p) {
         const ShardGrid& sh = ws.shards[p];
-        col_sweep(gate, &sh);
+        if (fast) launch_sweep(cx, P, ws, zuv_slot(), nullptr, nullptr, gate, false, gamma, &sh);
+        else col_sweep(gate, &sh);
         k_shard_gather_lse<false><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.colp.p, sh.g.grid.y, fmt, n, sh.lo, sh.hi,
                                                                          nullptr, ws.xsend.p + p * ws.xstride, gate);
       }
@@ -131,8 +151,8 @@ struct SinkhornSession : Session {
       nrb = 1;
       fmt = LP_SPLIT;
     }
-    k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
-    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, colp, nrb, fmt, update, sk_blocks(), gate);
+    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, colp, nrb, fmt, update, sk_blocks(),
+                                                      fast ? sv.zuv_v : nullptr, gate);
   }
 
   // solvers.hpp:463-476: u update, v update, B, E, ++iterations, record
@@ -201,6 +221,12 @@ struct SinkhornSession : Session {
     zv.alloc(size_t(ws.slot_stride));
     zf.alloc(size_t(ws.slot_stride));
     sv.zv_v = zv.p + n;
+    if (fast_cols()) {
+      zuv.alloc(size_t(ws.slot_stride));
+      zuv.zero(cx.stream);
+      sv.zuv_u = zuv.p;
+      sv.zuv_v = zuv.p + n;
+    }
     HVec lr(m), lc(m);
     for (size_t i = 0; i < m; ++i) { lr[i] = std::log(r_ext[i]); lc[i] = std::log(c_ext[i]); }  // solvers.hpp:421-422
     vec.zero(cx.stream);
@@ -210,7 +236,7 @@ struct SinkhornSession : Session {
     PG_CK(cudaMemcpyAsync(sv.r, r_ext.data(), m * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     PG_CK(cudaMemcpyAsync(sv.c, c_ext.data(), m * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
     ctl.alloc(1);
-    if (!hctl) PG_CK(cudaMallocHost(&hctl, sizeof(SinkCtl)));
+    if (!hctl) hctl = hctl_buf.get();
     std::memset(hctl, 0, sizeof(SinkCtl));
     hctl->n = n;
     hctl->max_iterations = cfg.max_iterations;
@@ -374,8 +400,18 @@ struct SinkhornSession : Session {
     int64_t rows = 0;
     auto sweeps = [&] {
       rows = 0;
-      if (!cx.comm.sharded()) { col_sweep(nullptr, nullptr); rows = P.n; return; }
-      for (const ShardGrid& sh : ws.shards) { col_sweep(nullptr, &sh); rows += sh.hi - sh.lo; }
+      const bool fast = fast_cols();
+      if (!cx.comm.sharded()) {
+        if (fast) launch_sweep(cx, P, ws, zuv_slot(), nullptr, nullptr, nullptr, false, gamma);
+        else col_sweep(nullptr, nullptr);
+        rows = P.n;
+        return;
+      }
+      for (const ShardGrid& sh : ws.shards) {
+        if (fast) launch_sweep(cx, P, ws, zuv_slot(), nullptr, nullptr, nullptr, false, gamma, &sh);
+        else col_sweep(nullptr, &sh);
+        rows += sh.hi - sh.lo;
+      }
     };
     PG_CK(cudaEventRecord(ev0, cx.stream));
     for (int k = 0; k < reps; ++k) sweeps();

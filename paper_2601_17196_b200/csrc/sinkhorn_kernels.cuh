@@ -268,12 +268,17 @@ struct SinkCtl {
   double row_lse_n, col_lse_n;     // dummy row / column LSEs
   uint64_t t0_ns, loop_end_ns;
   int64_t sweeps;
+  int col_flush;  // fast column pass lost a column (fp32 flush): run the exact pass
+  int pad;
+  int64_t col_flush_count;  // iterations that needed the exact column pass
 };
 
 struct SinkVec {  // device vectors of the extended problem (length n + 1)
   double* u; double* u_next; double* v;
   double* log_r; double* log_c; double* r; double* c;
-  double* zv_v;    // v[0..n) mirrored into the fp32 row-sweep point slot
+  double* zv_v;    // v[0..n) mirrored into the fp32 row-sweep point slot (0, v, 0)
+  double* zuv_u;   // u[0..n), v[0..n) mirrored into the point slot (u, v, 0) of the
+  double* zuv_v;   // fp32 fast column pass (null: no fast pass)
   double* scratch; // block partials: [nblk][4] rows, [nblk][4] cols
 };
 
@@ -403,14 +408,20 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv
 // Columns (a thread group per column): LSE_j + the dummy row (logK_nj =
 // -0, x = u_n). update: v_j = log c_j - LSE_j; the column sums of B(u, v)
 // are exp(v_j + LSE_j) with the (updated or current) v.
+// vshift (fast pass): the partials are column sums of B(u, v_old), i.e. the
+// LSE in the frame shifted by v_old_j, removed here in fp64; a column whose
+// combined fp32 sum is below 2^-64 of its scale may have flushed and sets
+// ctl->col_flush (the exact pass then redoes every column).
+constexpr double kColFlushRel = 5.421010862427522e-20;  // 2^-64
 __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
-                                                        int update, int nblk_rows, const int* gate) {
+                                                        int update, int nblk_rows, const double* vshift, const int* gate) {
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double un = sv.u[n];
   const int q = threadIdx.x % kSkTPI;
   const int64_t per_block = kSkThreads / kSkTPI, span = int64_t(gridDim.x) * per_block;
   double acc[4] = {0, 0, 0, 0};  // |col - c|, masked v.c
+  bool flushed = false;
   for (int64_t j0 = int64_t(blockIdx.x) * per_block; j0 < n; j0 += span) {
     const int64_t j = j0 + threadIdx.x / kSkTPI;
     const bool live = j < n;
@@ -418,26 +429,42 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv
     double M, S;
     group_lse(colp, jj * nrb, nrb, fmt, q, M, S, n);
     if (!live || q != 0) continue;
-    lse_merge(M, S, -0.0 + un, 1.0);
-    const double lse = M + log(S);
+    double lse;
+    if (vshift) {
+      const double vo = vshift[j];
+      if (vo == -INFINITY) {
+        lse = 0.0;  // c_j = 0: B's column is 0 whatever the LSE (v stays -inf)
+      } else {
+        if (!(S >= kColFlushRel)) flushed = true;
+        lse_merge(M, S, (-0.0 + un) + vo, 1.0);
+        lse = (M + log(S)) - vo;
+      }
+    } else {
+      lse_merge(M, S, -0.0 + un, 1.0);
+      lse = M + log(S);
+    }
     double vj = sv.v[j];
     if (update) {
       vj = sv.log_c[j] - lse;
       sv.v[j] = vj;
       sv.zv_v[j] = vj;
+      if (sv.zuv_v) sv.zuv_v[j] = vj;
     }
     const double col = exp(vj + lse);
     acc[0] += fabs(col - sv.c[j]);
     if (sv.c[j] > 0) acc[1] += vj * sv.c[j];
   }
+  if (flushed) ctl->col_flush = 1;
   if (update && blockIdx.x == 0 && threadIdx.x == 0) sv.v[n] = sv.log_c[n] - ctl->col_lse_n;
   sk_block_store<4, kSkThreads>(acc, sv.scratch + 4 * nblk_rows);
 }
 
 __global__ void k_sk_commit_u(SinkCtl* ctl, SinkVec sv) {
   if (!ctl->g_active) return;
-  for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= ctl->n; i += int64_t(gridDim.x) * blockDim.x)
+  for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= ctl->n; i += int64_t(gridDim.x) * blockDim.x) {
     sv.u[i] = sv.u_next[i];
+    if (sv.zuv_u && i < ctl->n) sv.zuv_u[i] = sv.u_next[i];
+  }
 }
 
 __device__ void sk_loop_head(SinkCtl* ctl) {  // solvers.hpp:458-462
@@ -481,7 +508,9 @@ __global__ void __launch_bounds__(kVecThreads) k_sk_scalars(SinkCtl* ctl, SinkVe
   ctl->error = rerr + cerr;
   ctl->phi = (rsum - ur) - vc;
   sv.u_next[n] = sv.log_r[n] - ctl->row_lse_n;  // dummy row's u update
-  ctl->sweeps += init ? 2 : 2;
+  ctl->sweeps += 2 + ctl->col_flush;  // + the exact column pass after a flush
+  ctl->col_flush_count += ctl->col_flush;
+  ctl->col_flush = 0;
   if (!init) ctl->it += 1;
   const int64_t it = ctl->it;
   if (init || it % ctl->log_every == 0 || !(ctl->error > ctl->tol)) {

@@ -145,6 +145,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
+    "potgpu_release_cached_memory",
 )
 
 _lib = None
@@ -336,6 +337,11 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def release_cached_memory() -> None:
+    """potgpu_release_cached_memory: return cached device / pinned blocks."""
+    load_library().potgpu_release_cached_memory()
 
 
 def nccl_unique_id() -> bytes:
