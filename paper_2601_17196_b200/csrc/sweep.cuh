@@ -392,6 +392,187 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
 }
 
 // ------------------------------------------------------------------------
+// On-the-fly points sweep (C3, C4), software-pipelined on the row max.
+// The warp max of a row segment (CREDUX.MAX) has a long latency; here row
+// i+1's exponents are formed only to issue its max, and row i's exponents
+// are recomputed (24 FFMA2) and exponentiated with the max issued one
+// iteration earlier, so the reduction's latency hides behind a whole row of
+// work without holding a second row of exponents in registers. The CTA's
+// rows live in shared memory as (2 x'_i, A_i) float4s (no global loads in
+// the row loop). Epilogue and partial formats as sweep_f32.
+__host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta) {
+  return size_t(rows_per_cta) * sizeof(float4) + size_t(kWarps * 32 * 33) * sizeof(float);
+}
+
+__device__ __forceinline__ float warp_maxf_shfl(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+template <bool PIPE, bool SHFL>
+__global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src, SweepArgs a) {
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i), then the row-sum tiles
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
+  }
+  float2 Bj[kPairs];
+  SrcPointsDotF32::Col cols[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) {
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;  // padding column: exp2(-inf) = 0, ignored by max
+      y[h] = make_float4(0, 0, 0, 0);
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
+        y[h] = src.Ys[j];
+      }
+      b[h] = float(vv);
+    }
+    Bj[q] = make_float2(b[0], b[1]);
+    cols[q].x = make_float2(y[0].x, y[1].x);
+    cols[q].y = make_float2(y[0].y, y[1].y);
+    cols[q].z = make_float2(y[0].z, y[1].z);
+  }
+  __syncthreads();
+  float2 cacc[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY;
+  float mmax = -INFINITY;
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);  // [row][strip]
+  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;
+  float my_ms = 0.f;
+  int slot = 0;
+  int64_t ib = r0 + warp;
+  const int64_t ldp = gridDim.x;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+    }
+    __syncwarp();
+  };
+  auto lane_max = [](const float2 (&t)[kPairs]) {
+    float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
+#pragma unroll
+    for (int q = 4; q < kPairs; q += 4)
+      m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[q].x, t[q].y), fmaxf(t[q + 1].x, t[q + 1].y)), fmaxf(fmaxf(t[q + 2].x, t[q + 2].y), fmaxf(t[q + 3].x, t[q + 3].y))));
+    return m;
+  };
+  auto wmax = [](float x) { return SHFL ? warp_maxf_shfl(x) : warp_maxf(x); };
+  // prologue: the first row's max (pipelined variant)
+  float Mcur = -INFINITY;
+  if (PIPE && r0 + warp < r1) {
+    float2 t[kPairs];
+    src.expo(SrcPointsDotF32::RowData{s_R[warp]}, cols, Bj, t);
+    Mcur = wmax(lane_max(t));
+  }
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    // issue the next row's max (consumed one iteration later)
+    float Mnxt = -INFINITY;
+    if (PIPE && i + kWarps < r1) {
+      float2 tn[kPairs];
+      src.expo(SrcPointsDotF32::RowData{s_R[i + kWarps - r0]}, cols, Bj, tn);
+      Mnxt = wmax(lane_max(tn));
+    }
+    const float4 dc = s_R[i - r0];
+    float2 t[kPairs];
+    src.expo(SrcPointsDotF32::RowData{dc}, cols, Bj, t);  // (re)compute this row
+    const float m = PIPE ? Mcur : wmax(lane_max(t));
+    const float Ai = dc.w;
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    const float2 M2 = make_float2(-ms, -ms);
+    float2 p[kPairs];
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const float2 d = __fadd2_rn(t[q], M2);
+      p[q] = make_float2(ex2f(d.x), ex2f(d.y));
+    }
+    float2 rs = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
+#pragma unroll
+    for (int q = 4; q < kPairs; q += 4) rs = __fadd2_rn(rs, __fadd2_rn(__fadd2_rn(p[q], p[q + 1]), __fadd2_rn(p[q + 2], p[q + 3])));
+    *tslot = rs.x + rs.y;
+    tslot += 33;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      tslot = tile + lane;
+      ib = i + kWarps;
+    }
+    const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;
+    if (mA > sigma) {  // warp-uniform
+      const float sc = ex2f(sigma - mA);
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = mA;
+    }
+    mmax = fmaxf(mmax, mA);
+    const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+    const float2 F2 = make_float2(f, f);
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+    Mcur = Mnxt;
+  }
+  if (slot > 0) flush(slot);
+  __shared__ float cs[kWarps][kStripCols32];
+  __shared__ float ss[kWarps];
+  __shared__ float mm[kWarps];
+  if (lane == 0) {
+    ss[warp] = sigma;
+    mm[warp] = mmax;
+  }
+  __syncthreads();
+  float sig = ss[0];
+  for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+  const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) {
+    const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+    cs[warp][c] = cacc[q].x * fw;
+    cs[warp][c + 1] = cacc[q].y * fw;
+  }
+  __syncthreads();
+  float2* colp = reinterpret_cast<float2*>(a.colp);
+  for (int c = threadIdx.x; c < kStripCols32; c += kThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+  }
+  if (threadIdx.x == 0) {
+    float m = mm[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
+// ------------------------------------------------------------------------
 // Grid shape: strips x row blocks, the row-block count chosen so the CTA
 // count fills the resident capacity (SMs x occupancy) as evenly as possible.
 struct SweepGrid {
