@@ -247,6 +247,48 @@ int potgpu_comm_init(potgpu_ctx* ctx, int rank, int world_size, const unsigned c
 int potgpu_comm_init_local(potgpu_ctx* ctx, int shards);
 int potgpu_comm_info(potgpu_ctx* ctx, int* rank, int* world_size, int* shards_per_rank);
 
+/* Rigid point-cloud registration (registration.hpp).
+ * pot::RegistrationConfig (registration.hpp:75-100) without `solve`, which
+ * is passed as a potgpu_config. */
+typedef struct potgpu_reg_config {
+  double alpha;               /* 0.4: transported fraction of the smaller mass */
+  double gamma0;              /* 4.4e-3: initial regularization */
+  double anneal_rate;         /* 0.83: gamma multiplier per registration */
+  double transform_threshold; /* 1e-5: stop when the increment falls below */
+  int max_registrations;      /* 60 */
+} potgpu_reg_config;
+
+typedef struct potgpu_reg_record {  /* pot::RegistrationRecord (registration.hpp:102-109) */
+  int32_t round;
+  int64_t inner_iterations;
+  int64_t accumulated_iterations;
+  double cost;
+  double increment;
+  double gamma;
+} potgpu_reg_record;
+
+typedef struct potgpu_reg_result {  /* pot::RegistrationResult (registration.hpp:111-115) */
+  double R[9];     /* row-major rotation of the transform mapping moving onto reference */
+  double t[3];
+  int converged;
+  int64_t rounds;  /* registration rounds run (records written: min(rounds, cap)) */
+} potgpu_reg_result;
+
+void potgpu_reg_config_default(potgpu_reg_config* cfg);
+/* register_point_clouds (registration.hpp:127-199): reference m x 3 and
+ * moving n x 3 row-major host arrays; every round builds the padded
+ * max(m,n)^2 cost on the device (fp64 coordinates; dtype = arithmetic of
+ * the solves), solves it and fits the rigid increment from the implicit
+ * plan (device moments, 3x3 SVD on the host). */
+int potgpu_register_point_clouds(potgpu_ctx* ctx, int solver_kind, const double* reference, int64_t m,
+                                 const double* moving, int64_t n, const potgpu_reg_config* reg,
+                                 const potgpu_config* solve, int dtype, potgpu_reg_result* result,
+                                 potgpu_reg_record* records, int64_t records_cap);
+/* fit_rigid (registration.hpp:40-71) on a dense row-major m x n coupling pi
+ * between x (m x 3) and y (n x 3): R (row-major 3x3) and t with x ~ R y + t. */
+int potgpu_fit_rigid(potgpu_ctx* ctx, const double* pi, int64_t m, int64_t n, const double* x, const double* y,
+                     double R[9], double t[3]);
+
 /* Synthetic fixtures: make_synthetic_instance (synthetic.hpp:15-54) and the
  * BASELINE.json config recipes. Host buffers:
  * r, c: n; C: n*n row-major (may be NULL for point configs); X, Y: n*3. */

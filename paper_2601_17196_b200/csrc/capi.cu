@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -370,6 +371,15 @@ struct Session {
   // elements and HBM bytes that launch must touch
   virtual double time_sweep(int reps, double* elems, double* bytes) = 0;
   virtual void stats(int64_t* attempts, int64_t* sweeps) = 0;
+  // for drivers that consume the plan themselves (registration): the
+  // rounding of the stopping iterate, the point its implicit plan is built
+  // on, the workspace / gamma of the sweeps, iterations and status
+  virtual PlanResult final_plan(double* Xdev) = 0;
+  virtual Slot plan_point() = 0;
+  virtual Workspace& workspace() = 0;
+  virtual double gamma_value() const = 0;
+  virtual int64_t iterations_done() = 0;
+  virtual int status_code() = 0;
   int64_t launches = 0;  // kernels this session launched inside iterate()
 };
 
@@ -583,6 +593,24 @@ struct AspotSession : Session {
     *sweeps = ws.host_ctl->sweeps;
   }
 
+  PlanResult final_plan(double* Xdev) override {
+    if (trivial) throw Error(POTGPU_ERR_UNSUPPORTED, "trivial solve has no device plan");
+    return round_now(Xdev);
+  }
+  Slot plan_point() override { return ws.slot(S_ZC); }
+  Workspace& workspace() override { return ws; }
+  double gamma_value() const override { return gamma; }
+  int64_t iterations_done() override {
+    if (trivial) return 0;
+    sync_ctl();
+    return ws.host_ctl->t;
+  }
+  int status_code() override {
+    if (trivial) return POTGPU_CONVERGED;
+    sync_ctl();
+    return ws.host_ctl->status;
+  }
+
   double time_sweep(int reps, double* elems, double* bytes) override {
     if (trivial) throw Error(POTGPU_INVALID_ARGUMENT, "trivial solve has no sweep");
     const Slot ZC = ws.slot(S_ZC);
@@ -664,6 +692,7 @@ struct AspotSession : Session {
 }  // namespace potgpu
 
 #include "sinkhorn.cuh"
+#include "registration.cuh"
 
 namespace potgpu {
 }  // namespace potgpu
@@ -762,16 +791,19 @@ static std::unique_ptr<Session> make_session_cx(Context& cx, int kind, const pot
   s->cfg = cfg;
   s->t_start = t_start;
   PhaseTimer pt(cx.stream);
-  upload_problem(cx, pr, s->P);
-  pt.mark("upload + validation");
+  if (pr) {
+    upload_problem(cx, pr, s->P);
+    pt.mark("upload + validation");
+  }
   check_config(cfg);
-  s->begin();
+  if (pr) s->begin();  // otherwise the caller fills s->P and calls begin()
   return s;
 }
 
 static std::unique_ptr<Session> make_session(potgpu_ctx* c, int kind, const potgpu_problem* pr,
                                              const potgpu_config* cfg_in, int64_t trace_cap, int64_t log_cap) {
   if (!c) throw Error(POTGPU_INVALID_ARGUMENT, "null context");
+  if (!pr) throw Error(POTGPU_INVALID_ARGUMENT, "null problem");
   return make_session_cx(c->cx, kind, pr, cfg_in, trace_cap, log_cap);
 }
 
@@ -981,6 +1013,174 @@ int potgpu_comm_info(potgpu_ctx* c, int* rank, int* world_size, int* shards_per_
 }
 
 void potgpu_release_cached_memory(void) { BlockCache::get().release_all(); }
+
+void potgpu_reg_config_default(potgpu_reg_config* c) {  // registration.hpp:75-80
+  std::memset(c, 0, sizeof(*c));
+  c->alpha = 0.4;
+  c->gamma0 = 4.4e-3;
+  c->anneal_rate = 0.83;
+  c->transform_threshold = 1e-5;
+  c->max_registrations = 60;
+}
+
+static void check_reg_config(const potgpu_reg_config& c) {  // registration.hpp:83-99
+  if (!(c.alpha > 0) || !(c.alpha <= 1)) throw Error(POTGPU_INVALID_ARGUMENT, "alpha must lie in (0, 1]");
+  if (!(c.gamma0 > 0)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma0 must be positive");
+  if (!(c.anneal_rate > 0) || !(c.anneal_rate < 1)) throw Error(POTGPU_INVALID_ARGUMENT, "anneal rate must lie in (0, 1)");
+  if (!(c.transform_threshold > 0)) throw Error(POTGPU_INVALID_ARGUMENT, "threshold must be positive");
+  if (c.max_registrations < 1) throw Error(POTGPU_INVALID_ARGUMENT, "max_registrations must be >= 1");
+}
+
+// register_point_clouds (registration.hpp:127-199).
+int potgpu_register_point_clouds(potgpu_ctx* c, int kind, const double* reference, int64_t m, const double* moving,
+                                 int64_t n, const potgpu_reg_config* reg_in, const potgpu_config* solve_in, int dtype,
+                                 potgpu_reg_result* res, potgpu_reg_record* records, int64_t records_cap) {
+  return guarded([&] {
+    if (!c || !res) throw Error(POTGPU_INVALID_ARGUMENT, "null context or result");
+    if (!reference || !moving) throw Error(POTGPU_DIMENSION_MISMATCH, "point clouds must be N x 3");
+    if (m < 3 || n < 3) throw Error(POTGPU_EMPTY_INPUT, "need at least 3 points per cloud");
+    potgpu_reg_config rc;
+    if (reg_in) rc = *reg_in; else potgpu_reg_config_default(&rc);
+    check_reg_config(rc);
+    potgpu_config cfg;
+    if (solve_in) cfg = *solve_in; else potgpu_config_default(&cfg);
+    check_config(cfg);
+    if (dtype != POTGPU_F64 && dtype != POTGPU_F32) throw Error(POTGPU_INVALID_ARGUMENT, "unknown dtype");
+    Context& cx = c->cx;
+    PG_CK(cudaSetDevice(cx.device));
+    const int64_t side = std::max(m, n);
+    const double denom = double(side);
+    HVec r(static_cast<size_t>(side), 0.0), cc(static_cast<size_t>(side), 0.0);
+    for (int64_t i = 0; i < m; ++i) r[size_t(i)] = 1.0 / denom;
+    for (int64_t j = 0; j < n; ++j) cc[size_t(j)] = 1.0 / denom;
+    const double budget = rc.alpha * double(std::min(m, n)) / denom;
+    DevBuf<double> refd, curd;
+    DevBuf<unsigned long long> mxd;
+    refd.alloc(size_t(3 * m));
+    curd.alloc(size_t(3 * n));
+    mxd.alloc(1);
+    PG_CK(cudaMemcpyAsync(refd.p, reference, size_t(3 * m) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    Rigid T;
+    double gamma = rc.gamma0;
+    int64_t accumulated = 0;
+    bool converged = false;
+    std::vector<RegRecord> recs;
+    HVec cur(static_cast<size_t>(3 * n));
+    for (int round = 1; round <= rc.max_registrations; ++round) {
+      // current = T.apply_all(moving) (registration.hpp:21-25)
+      for (int64_t j = 0; j < n; ++j) {
+        const Vec3 y{moving[3 * j], moving[3 * j + 1], moving[3 * j + 2]};
+        const Vec3 ry = mat3_apply(T.R, y);
+        for (int d = 0; d < 3; ++d) cur[size_t(3 * j + d)] = ry[d] + T.t[d];
+      }
+      PG_CK(cudaMemcpyAsync(curd.p, cur.data(), size_t(3 * n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+      mxd.zero(cx.stream);
+      k_reg_d2max<<<int(std::min<int64_t>(m, 4096)), 256, 0, cx.stream>>>(refd.p, curd.p, m, n, mxd.p);
+      PG_CK(cudaGetLastError());
+      unsigned long long hb = 0;
+      PG_CK(cudaMemcpyAsync(&hb, mxd.p, sizeof(hb), cudaMemcpyDeviceToHost, cx.stream));
+      PG_CK(cudaStreamSynchronize(cx.stream));
+      double cmax;
+      std::memcpy(&cmax, &hb, sizeof(double));
+      if (!(cmax > 0)) {  // clouds coincide (registration.hpp:160-167)
+        converged = true;
+        break;
+      }
+      if (!std::isfinite(cmax)) throw Error(POTGPU_NON_FINITE_ENTRY, "invalid instance: non-finite point coordinates");
+      potgpu_config rcfg = cfg;
+      rcfg.gamma_override = gamma;
+      auto s = make_session_cx(cx, kind, nullptr, &rcfg, 0, 0);
+      DevProblem& P = s->P;  // the padded instance, built on the device
+      P.n = side;
+      P.dtype = dtype;
+      P.kind = POTGPU_COST_DENSE;
+      P.ld = round_up(side, kStripCols32);
+      P.r = r;
+      P.c = cc;
+      P.s = budget;
+      P.cmax = 1.0;  // block max = cmax / cmax, padding = 1
+      if (dtype == POTGPU_F64) P.C64.alloc(size_t(side * P.ld)); else P.C32.alloc(size_t(side * P.ld));
+      k_reg_cost<<<cx.num_sms * 8, 256, 0, cx.stream>>>(refd.p, curd.p, m, n, side, P.ld, cmax,
+                                                       dtype == POTGPU_F64 ? P.C64.p : nullptr,
+                                                       dtype == POTGPU_F32 ? P.C32.p : nullptr);
+      PG_CK(cudaGetLastError());
+      s->begin();
+      s->iterate(-1, nullptr, nullptr, nullptr);
+      const PlanResult pr = s->final_plan(nullptr);
+      const int64_t inner = s->iterations_done();
+      // fit_rigid(plan.X.topLeftCorner(m, n), reference, current)
+      HVec a(pr.rowx.begin(), pr.rowx.begin() + long(m)), b(pr.colx.begin(), pr.colx.begin() + long(n));
+      Session* sp = s.get();
+      const Rigid inc = fit_rigid_from(a, b, reference, m, cur.data(), n, [&](const HVec& xh) {
+        HVec xf(static_cast<size_t>(3 * side), 0.0);
+        std::copy(xh.begin(), xh.end(), xf.begin());
+        PlanEngine pe(cx, sp->P, sp->workspace(), sp->gamma_value());
+        HVec z = pe.moments(sp->plan_point(), pr.Pf, pr.Qf, &pr.a0, &pr.b0, pr.a1.empty() ? nullptr : &pr.a1,
+                            pr.a1.empty() ? nullptr : &pr.b1, xf);
+        z.resize(size_t(3 * n));
+        return z;
+      });
+      const Rigid next = rigid_compose(inc, T);
+      double dR = 0.0, dt = 0.0;
+      for (int k = 0; k < 9; ++k) dR += (next.R[k] - T.R[k]) * (next.R[k] - T.R[k]);
+      for (int k = 0; k < 3; ++k) dt += (next.t[k] - T.t[k]) * (next.t[k] - T.t[k]);
+      const double delta = std::sqrt(dR) + std::sqrt(dt);
+      T = next;
+      accumulated += inner;
+      recs.push_back(RegRecord{round, inner, accumulated, pr.cost, delta, gamma});
+      gamma *= rc.anneal_rate;
+      if (delta < rc.transform_threshold) {
+        converged = true;
+        break;
+      }
+    }
+    std::memcpy(res->R, T.R.data(), sizeof(res->R));
+    std::memcpy(res->t, T.t.data(), sizeof(res->t));
+    res->converged = converged ? 1 : 0;
+    res->rounds = int64_t(recs.size());
+    if (records)
+      for (int64_t k = 0; k < std::min<int64_t>(records_cap, int64_t(recs.size())); ++k) {
+        const RegRecord& q = recs[size_t(k)];
+        records[k] = potgpu_reg_record{q.round, q.inner, q.accumulated, q.cost, q.increment, q.gamma};
+      }
+  });
+}
+
+// fit_rigid (registration.hpp:40-71) on a dense row-major m x n coupling.
+int potgpu_fit_rigid(potgpu_ctx* c, const double* pi, int64_t m, int64_t n, const double* x, const double* y, double R[9],
+                     double t[3]) {
+  return guarded([&] {
+    if (!c || !R || !t) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    if (!pi || !x || !y || m < 1 || n < 1) throw Error(POTGPU_DIMENSION_MISMATCH, "coupling shape does not match the clouds");
+    Context& cx = c->cx;
+    PG_CK(cudaSetDevice(cx.device));
+    DevBuf<double> pid, rows, cols, xhd, zd;
+    pid.alloc(size_t(m * n));
+    rows.alloc(size_t(m));
+    cols.alloc(size_t(n));
+    xhd.alloc(size_t(3 * m));
+    zd.alloc(size_t(3 * n));
+    PG_CK(cudaMemcpyAsync(pid.p, pi, size_t(m * n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    k_dense_rowsums<<<int(std::min<int64_t>(m, 4096)), 256, 0, cx.stream>>>(pid.p, m, n, rows.p);
+    k_dense_colmoments<<<cx.num_sms, 256, 0, cx.stream>>>(pid.p, m, n, nullptr, cols.p, nullptr);
+    PG_CK(cudaGetLastError());
+    HVec a(static_cast<size_t>(m)), b(static_cast<size_t>(n));
+    PG_CK(cudaMemcpyAsync(a.data(), rows.p, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(b.data(), cols.p, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    const Rigid T = fit_rigid_from(a, b, x, m, y, n, [&](const HVec& xh) {
+      PG_CK(cudaMemcpyAsync(xhd.p, xh.data(), size_t(3 * m) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+      k_dense_colmoments<<<cx.num_sms, 256, 0, cx.stream>>>(pid.p, m, n, xhd.p, nullptr, zd.p);
+      PG_CK(cudaGetLastError());
+      HVec z(static_cast<size_t>(3 * n));
+      PG_CK(cudaMemcpyAsync(z.data(), zd.p, size_t(3 * n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+      PG_CK(cudaStreamSynchronize(cx.stream));
+      return z;
+    });
+    std::memcpy(R, T.R.data(), 9 * sizeof(double));
+    std::memcpy(t, T.t.data(), 3 * sizeof(double));
+  });
+}
 
 int potgpu_round_pot(potgpu_ctx*, int64_t, const double*, const double*, const double*, double, double*) {
   g_last_error = "potgpu_round_pot on a dense user plan is not implemented yet";

@@ -71,6 +71,42 @@ __global__ void __launch_bounds__(kThreads) k_plan_cost(E el, Slot z, PlanTermsD
   if (threadIdx.x == 0) partial[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = sh[0];
 }
 
+// Plan moments for the weighted Procrustes fit (registration.hpp:40-58):
+// z_j = sum_i X_ij xh_i (3-vectors, xh = centred first-cloud points, 0 on
+// padded rows), thread per column, fixed-order partials per row block.
+template <class E>
+__global__ void __launch_bounds__(kThreads) k_plan_moments(E el, Slot z, PlanTermsDev t, const double* xh, int rows_per_cta,
+                                                           double* part) {
+  const int64_t n = z.n;
+  const int64_t j = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  if (j >= n) return;
+  const double w = *z.w();
+  const double vj = z.v()[j], qj = t.Q[j];
+  const double b0 = t.b0 ? t.b0[j] : 0.0, b1 = t.b1 ? t.b1[j] : 0.0;
+  const int64_t r0 = int64_t(blockIdx.y) * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  for (int64_t i = r0; i < r1; ++i) {
+    const double e = ((el.logk(i, j) + z.u()[i]) + vj) + w;
+    const double B = exp(fmin(fmax(e, kExpLo), kExpHi));
+    double x = (B * t.P[i]) * qj;
+    if (t.a0) x += t.a0[i] * b0;
+    if (t.a1) x += t.a1[i] * b1;
+    m0 += x * xh[3 * i];
+    m1 += x * xh[3 * i + 1];
+    m2 += x * xh[3 * i + 2];
+  }
+  double* o = part + (int64_t(blockIdx.y) * n + j) * 3;
+  o[0] = m0; o[1] = m1; o[2] = m2;
+}
+
+__global__ void k_sum_moment_parts(const double* part, int64_t nrb, int64_t n, double* out) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < 3 * n; k += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int64_t b = 0; b < nrb; ++b) s += part[b * 3 * n + k];
+    out[k] = s;
+  }
+}
+
 using HVec = std::vector<double>;
 
 inline double hsum(const HVec& x) { return ksum(x.data(), int64_t(x.size())); }
@@ -150,11 +186,49 @@ struct PlanEngine {
     PG_CK(cudaStreamSynchronize(cx.stream));
     return allreduce_host_sum(cx, ws, hsum(part));
   }
+
+  // z_j = sum_i X_ij xh_i for the final plan terms (xh: n x 3 host, row-major);
+  // one process's rows (the caller sums over ranks when sharded).
+  HVec moments(Slot z, const HVec& Pv, const HVec& Qv, const HVec* a0, const HVec* b0, const HVec* a1, const HVec* b1,
+               const HVec& xh) {
+    const int64_t n = P.n;
+    up(4, Pv);
+    up(5, Qv);
+    PlanTermsDev t{d(4), d(5), nullptr, nullptr, nullptr, nullptr};
+    if (a0) { up(6, *a0); up(7, *b0); t.a0 = d(6); t.b0 = d(7); }
+    if (a1) { up(8, *a1); up(9, *b1); t.a1 = d(8); t.b1 = d(9); }
+    DevBuf<double> xhd, part, zd;
+    xhd.alloc(size_t(3 * n));
+    PG_CK(cudaMemcpyAsync(xhd.p, xh.data(), size_t(3 * n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    const int rows = cost_sweep_rows(n);
+    dim3 g(unsigned(ceil_div(n, kThreads)), unsigned(ceil_div(n, rows)));
+    part.alloc(size_t(g.y) * size_t(3 * n));
+    zd.alloc(size_t(3 * n));
+    if (P.dtype == POTGPU_F64) {
+      ElemDenseF64 el{P.L64.p, P.ld, gamma};
+      k_plan_moments<ElemDenseF64><<<g, kThreads, 0, cx.stream>>>(el, z, t, xhd.p, rows, part.p);
+    } else if (P.kind == POTGPU_COST_DENSE) {
+      ElemDenseF32 el{P.C32.p, P.ld, gamma};
+      k_plan_moments<ElemDenseF32><<<g, kThreads, 0, cx.stream>>>(el, z, t, xhd.p, rows, part.p);
+    } else {
+      ElemPointsF32 el{P.X4.p, P.Y4.p, P.cost_scale, gamma};
+      k_plan_moments<ElemPointsF32><<<g, kThreads, 0, cx.stream>>>(el, z, t, xhd.p, rows, part.p);
+    }
+    k_sum_moment_parts<<<cx.num_sms * 2, kVecThreads, 0, cx.stream>>>(part.p, g.y, n, zd.p);
+    PG_CK(cudaGetLastError());
+    HVec out(static_cast<size_t>(3 * n));
+    PG_CK(cudaMemcpyAsync(out.data(), zd.p, size_t(3 * n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    return out;
+  }
 };
 
 struct PlanResult {
   double cost = 0, mass = 0, gap = 0;
   HVec row_slack, col_slack;
+  HVec rowx, colx;  // X 1, X^T 1
+  // the final plan X = diag(Pf) B(z) diag(Qf) + a0 b0^T (+ a1 b1^T)
+  HVec Pf, Qf, a0, b0, a1, b1;
 };
 
 inline HVec vlog(const HVec& x) {
@@ -221,14 +295,18 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   out.mass = mass3 + f * na * nb;
   out.row_slack.resize(n);
   out.col_slack.resize(n);
+  out.rowx.resize(n);
+  out.colx.resize(n);
   double rg = 0.0, cg = 0.0;
   for (size_t i = 0; i < n; ++i) {
     const double rx = rowX3[i] + f * fa[i] * nb;
+    out.rowx[i] = rx;
     out.row_slack[i] = r[i] - rx;
     rg = std::max(rg, std::max(rx - r[i], 0.0));
   }
   for (size_t j = 0; j < n; ++j) {
     const double cx = colX3[j] + f * na * fb[j];
+    out.colx[j] = cx;
     out.col_slack[j] = c[j] - cx;
     cg = std::max(cg, std::max(cx - c[j], 0.0));
   }
@@ -248,6 +326,14 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   pt.mark("round: host O(n)");
   out.cost = pe.cost(z, Pf, Qf, &fa2, &fb, a ? &ra : nullptr, a ? &kb : nullptr, Xdev);
   pt.mark("round: plan cost");
+  out.Pf = std::move(Pf);
+  out.Qf = std::move(Qf);
+  out.a0 = std::move(fa2);
+  out.b0 = std::move(fb);
+  if (a) {
+    out.a1 = std::move(ra);
+    out.b1 = std::move(kb);
+  }
   return out;
 }
 

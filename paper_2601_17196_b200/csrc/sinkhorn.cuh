@@ -394,6 +394,24 @@ struct SinkhornSession : Session {
     *sweeps = hctl->sweeps;
   }
 
+  PlanResult final_plan(double* Xdev) override {
+    if (trivial) throw Error(POTGPU_ERR_UNSUPPORTED, "trivial solve has no device plan");
+    return round_now(Xdev);
+  }
+  Slot plan_point() override { return zf_slot(); }
+  Workspace& workspace() override { return ws; }
+  double gamma_value() const override { return gamma; }
+  int64_t iterations_done() override {
+    if (trivial) return 0;
+    sync_ctl();
+    return hctl->it;
+  }
+  int status_code() override {
+    if (trivial) return POTGPU_CONVERGED;
+    sync_ctl();
+    return hctl->status;
+  }
+
   double time_sweep(int reps, double* elems, double* bytes) override {
     if (trivial) throw Error(POTGPU_INVALID_ARGUMENT, "trivial solve has no sweep");
     col_lse(0, nullptr);

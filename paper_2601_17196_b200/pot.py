@@ -128,6 +128,22 @@ class _Summary(ctypes.Structure):
     ]
 
 
+class _RegConfig(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("gamma0", ctypes.c_double), ("anneal_rate", ctypes.c_double),
+                ("transform_threshold", ctypes.c_double), ("max_registrations", ctypes.c_int)]
+
+
+class _RegRecord(ctypes.Structure):
+    _fields_ = [("round", ctypes.c_int32), ("inner_iterations", ctypes.c_int64),
+                ("accumulated_iterations", ctypes.c_int64), ("cost", ctypes.c_double), ("increment", ctypes.c_double),
+                ("gamma", ctypes.c_double)]
+
+
+class _RegResult(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3), ("converged", ctypes.c_int),
+                ("rounds", ctypes.c_int64)]
+
+
 class _Outputs(ctypes.Structure):
     _fields_ = [
         ("X", ctypes.POINTER(ctypes.c_double)), ("row_slack", ctypes.POINTER(ctypes.c_double)),
@@ -145,7 +161,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
-    "potgpu_release_cached_memory",
+    "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
 )
 
 _lib = None
@@ -178,6 +194,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_solve_batched.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), ctypes.c_int64, P(_Config),
                                          P(_Summary), P(_Outputs), ctypes.c_int]
     lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.potgpu_reg_config_default.argtypes = [P(_RegConfig)]
+    lib.potgpu_register_point_clouds.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, ctypes.c_int64, dp, ctypes.c_int64,
+                                                 P(_RegConfig), P(_Config), ctypes.c_int, P(_RegResult), P(_RegRecord),
+                                                 ctypes.c_int64]
+    lib.potgpu_fit_rigid.argtypes = [ctypes.c_void_p, dp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]
     lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
     lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -684,3 +705,92 @@ def config_instance(config_id: int, n: Optional[int] = None, seed: int = 1, dens
             C = C.astype(np.float32).astype(np.float64)
         return Instance(r=r, c=c, s=s, C=C, dtype=dtype)
     return Instance(r=r, c=c, s=s, X=X, Y=Y, cost_scale=scale if scale > 0 else None, dtype=dtype)
+
+
+# ------------------------------------------------------------------ registration --
+@dataclass
+class RigidTransform:  # registration.hpp:13-33: y -> R y + t
+    R: np.ndarray = field(default_factory=lambda: np.eye(3))
+    t: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def apply(self, y) -> np.ndarray:
+        return self.R @ np.asarray(y, dtype=np.float64) + self.t
+
+    def apply_all(self, pts) -> np.ndarray:
+        pts = np.asarray(pts, dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != 3:
+            raise PotError(ErrorCode.DimensionMismatch, "point cloud must be N x 3")
+        return pts @ self.R.T + self.t
+
+    @staticmethod
+    def compose(a: "RigidTransform", b: "RigidTransform") -> "RigidTransform":
+        return RigidTransform(a.R @ b.R, a.R @ b.t + a.t)
+
+
+@dataclass
+class RegistrationConfig:  # registration.hpp:75-100
+    alpha: float = 0.4
+    gamma0: float = 4.4e-3
+    anneal_rate: float = 0.83
+    transform_threshold: float = 1e-5
+    max_registrations: int = 60
+    solve: SolverConfig = field(default_factory=SolverConfig)
+
+
+@dataclass
+class RegistrationRecord:  # registration.hpp:102-109
+    round: int
+    inner_iterations: int
+    accumulated_iterations: int
+    cost: float
+    increment: float
+    gamma: float
+
+
+@dataclass
+class RegistrationResult:  # registration.hpp:111-115
+    transform: RigidTransform
+    converged: bool
+    rounds: List[RegistrationRecord]
+
+
+def _cloud(a, name: str) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] != 3:
+        raise PotError(ErrorCode.DimensionMismatch, f"{name}: point clouds must be N x 3")
+    return a
+
+
+def register_point_clouds(reference, moving, config: RegistrationConfig = RegistrationConfig(),
+                          kind: SolverKind = SolverKind.Aspot, dtype: DType = DType.F64,
+                          ctx: Optional[Context] = None) -> RegistrationResult:
+    """register_point_clouds (registration.hpp:127-199) on the device."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    ref, mov = _cloud(reference, "reference"), _cloud(moving, "moving")
+    rc = _RegConfig(config.alpha, config.gamma0, config.anneal_rate, config.transform_threshold,
+                    int(config.max_registrations))
+    sc = _config(config.solve)
+    res = _RegResult()
+    cap = max(int(config.max_registrations), 1)
+    recs = (_RegRecord * cap)()
+    _check(lib.potgpu_register_point_clouds(ctx._h, int(kind), _dp(ref), ref.shape[0], _dp(mov), mov.shape[0],
+                                            ctypes.byref(rc), ctypes.byref(sc), int(dtype), ctypes.byref(res), recs,
+                                            cap))
+    rounds = [RegistrationRecord(int(r.round), int(r.inner_iterations), int(r.accumulated_iterations), float(r.cost),
+                                 float(r.increment), float(r.gamma)) for r in recs[:min(res.rounds, cap)]]
+    T = RigidTransform(np.array(res.R[:], dtype=np.float64).reshape(3, 3), np.array(res.t[:], dtype=np.float64))
+    return RegistrationResult(T, bool(res.converged), rounds)
+
+
+def fit_rigid(pi, x_pts, y_pts, ctx: Optional[Context] = None) -> RigidTransform:
+    """fit_rigid (registration.hpp:40-71): coupling reductions on the device."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    x, y = _cloud(x_pts, "x_pts"), _cloud(y_pts, "y_pts")
+    pi = np.ascontiguousarray(pi, dtype=np.float64)
+    if pi.shape != (x.shape[0], y.shape[0]):
+        raise PotError(ErrorCode.DimensionMismatch, "coupling shape does not match the clouds")
+    R, t = np.zeros(9), np.zeros(3)
+    _check(lib.potgpu_fit_rigid(ctx._h, _dp(pi), pi.shape[0], pi.shape[1], _dp(x), _dp(y), _dp(R), _dp(t)))
+    return RigidTransform(R.reshape(3, 3), t)
