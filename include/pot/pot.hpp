@@ -258,6 +258,19 @@ inline potgpu_ctx* context() {
   throw DeviceError(rc, msg);
 }
 
+inline potgpu_config to_cconfig(const SolverConfig& config, double epsilon, double p) {
+  potgpu_config cfg;
+  potgpu_config_default(&cfg);
+  cfg.epsilon = epsilon;
+  cfg.gamma_override = config.gamma_override.value_or(0.0);
+  cfg.max_iterations = config.max_iterations;
+  cfg.block_rule = config.block_rule == BlockRule::Greedy ? POTGPU_GREEDY : POTGPU_ROUND_ROBIN;
+  cfg.tuning_exponent_p = p;
+  cfg.deterministic = config.deterministic ? 1 : 0;
+  cfg.log_every = config.log_every;
+  return cfg;
+}
+
 inline SolveResult run(int kind, const Instance& in, const SolverConfig& config, double epsilon, double p) {
   config.check();
   const long n = in.size();
@@ -273,15 +286,7 @@ inline SolveResult run(int kind, const Instance& in, const SolverConfig& config,
   pr.s = in.s;
   if (in.c.size() != n || in.C.rows() != n || in.C.cols() != n)
     throw PotError(ErrorCode::DimensionMismatch, "instance shapes differ");
-  potgpu_config cfg;
-  potgpu_config_default(&cfg);
-  cfg.epsilon = epsilon;
-  cfg.gamma_override = config.gamma_override.value_or(0.0);
-  cfg.max_iterations = config.max_iterations;
-  cfg.block_rule = config.block_rule == BlockRule::Greedy ? POTGPU_GREEDY : POTGPU_ROUND_ROBIN;
-  cfg.tuning_exponent_p = p;
-  cfg.deterministic = config.deterministic ? 1 : 0;
-  cfg.log_every = config.log_every;
+  potgpu_config cfg = to_cconfig(config, epsilon, p);
   const int64_t cap = std::min<int64_t>(config.max_iterations / config.log_every + 4, 1 << 20);
   std::vector<potgpu_trace_record> trace(static_cast<size_t>(cap));
   SolveResult res;

@@ -1,10 +1,12 @@
 // test_dropin.cpp — the reference's own solver tests, unchanged in spirit,
 // compiled against the drop-in headers (include/pot/) and libpotgpu.so.
-// Ports of /root/reference/proj/tests/test_solvers.cpp cases; GTest-free.
+// Ports of /root/reference/proj/tests/test_solvers.cpp and test_apps.cpp
+// (FitRigid*, Registration*) cases; GTest-free.
 #include <cmath>
 #include <cstdio>
 #include <random>
 
+#include "pot/registration.hpp"
 #include "pot/solvers.hpp"
 #include "pot/synthetic.hpp"
 
@@ -100,6 +102,47 @@ int main() {
     bool threw = false;
     try { feasible_sinkhorn_solve(in, SolverConfig{}); } catch (const PotError& e) { threw = e.code() == ErrorCode::BudgetExceedsMass; }
     EXPECT(threw);
+  }
+  {  // FitRigid.IdentityForAlignedClouds / RecoversKnownTransform / Reflection (test_apps.cpp:160-195)
+    std::mt19937_64 rng(68);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    Matrix cloud(30, 3);
+    for (long i = 0; i < 30; ++i) for (int d = 0; d < 3; ++d) cloud(i, d) = u(rng);
+    Matrix coupling = Matrix::Zero(30, 30);
+    for (long i = 0; i < 30; ++i) coupling(i, i) = 1.0 / 30.0;
+    const RigidTransform I = fit_rigid(coupling, cloud, cloud);
+    EXPECT((I.R - Matrix3d::Identity()).norm() <= 1e-12 && I.t.norm() <= 1e-12);
+    const double a = 37.0 * M_PI / 180.0;
+    RigidTransform T0;
+    T0.R(0, 0) = std::cos(a); T0.R(0, 1) = -std::sin(a); T0.R(1, 0) = std::sin(a); T0.R(1, 1) = std::cos(a);
+    T0.t = Vector3d(0.4, -0.7, 0.2);
+    const Matrix moved = T0.apply_all(cloud);
+    const RigidTransform T = fit_rigid(coupling, moved, cloud);
+    EXPECT((T.R - T0.R).norm() <= 1e-8 && (T.t - T0.t).norm() <= 1e-8);
+    EXPECT((T.R.transpose() * T.R - Matrix3d::Identity()).norm() <= 1e-9);
+    EXPECT(std::fabs(T.R.determinant() - 1.0) <= 1e-9);
+    Matrix mirrored = cloud;
+    for (long i = 0; i < 30; ++i) mirrored(i, 2) *= -1.0;
+    EXPECT(std::fabs(fit_rigid(coupling, mirrored, cloud).R.determinant() - 1.0) <= 1e-9);
+    bool threw = false;
+    try { fit_rigid(Matrix::Zero(30, 30), cloud, cloud); } catch (const PotError& e) { threw = e.code() == ErrorCode::ZeroMassPlan; }
+    EXPECT(threw);
+  }
+  {  // Registration.IdenticalCloudsAreAFixedPoint (test_apps.cpp:216-230)
+    std::mt19937_64 rng(71);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    Matrix pts(40, 3);
+    for (long i = 0; i < 40; ++i) for (int d = 0; d < 3; ++d) pts(i, d) = u(rng);
+    RegistrationConfig cfg;
+    cfg.alpha = 1.0;
+    cfg.solve.epsilon = 0.01;
+    cfg.solve.max_iterations = 5000;
+    cfg.solve.log_every = 1000000;
+    const RegistrationResult res = register_point_clouds(pts, pts, cfg, SolverKind::Aspot);
+    EXPECT(res.converged);
+    EXPECT(res.rounds.size() <= 1u);
+    EXPECT((res.transform.R - Matrix3d::Identity()).norm() <= 1e-4);
+    EXPECT(res.transform.t.norm() <= 1e-4);
   }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;

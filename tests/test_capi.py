@@ -55,6 +55,8 @@ int main(void){
  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(potgpu_problem), sizeof(potgpu_config), sizeof(potgpu_summary),
         sizeof(potgpu_outputs), sizeof(potgpu_trace_record), sizeof(potgpu_iter_log));
  printf("%zu %zu %zu\n", offsetof(potgpu_problem, s), offsetof(potgpu_summary, stopping_iterate), offsetof(potgpu_config, sync_every));
+ printf("%zu %zu %zu %zu\n", sizeof(potgpu_reg_config), sizeof(potgpu_reg_record), sizeof(potgpu_reg_result),
+        offsetof(potgpu_reg_result, rounds));
  return 0; }
 '''
     with tempfile.TemporaryDirectory() as d:
@@ -69,6 +71,8 @@ int main(void){
     assert sizes[6] == pot._Problem.s.offset
     assert sizes[7] == pot._Summary.stopping_iterate.offset
     assert sizes[8] == pot._Config.sync_every.offset
+    assert sizes[9:12] == [ctypes.sizeof(t) for t in (pot._RegConfig, pot._RegRecord, pot._RegResult)]
+    assert sizes[12] == pot._RegResult.rounds.offset
 
 
 def test_config_generators_are_deterministic():
