@@ -135,10 +135,15 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   } else if (P.kind == POTGPU_COST_DENSE) {
     PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_f32<SrcDenseF32>, kThreads, 0));
   } else {
-    PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<false, false>, kThreads, 0));
+    const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
+    switch (pts_pairs()) {
+      case 4: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<4>, kThreads, sm_est)); break;
+      case 6: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<6>, kThreads, sm_est)); break;
+      default: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<8>, kThreads, sm_est)); break;
+    }
   }
   occ = std::max(occ, 1);
-  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : kStripCols32;
+  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * pts_pairs() : kStripCols32);
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
   ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip);
   int64_t max_rb = ws.g.grid.y;
@@ -163,11 +168,9 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts_smem(max_rpc), sweep_f32_smem(max_rpc));
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcPointsDotF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
   }
   ws.nstrips = ws.g.grid.x;
   ws.nrb = ws.g.grid.y;
@@ -195,17 +198,6 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
 }
 
 // --------------------------------------------------------------------------
-// Points-sweep kernel variant ($POTGPU_PTS_VARIANT, profiles/pts_variants.sh):
-// 0 generic sweep_f32, 1-4 sweep_pts_f32 <pipelined, shuffle max> = <0,0>
-// <0,1> <1,0> <1,1>. Measured on B200 (C3 / C4 sweep ms): 0.1186 / 1.685,
-// 0.1121 / 1.537, 0.1184 / 1.673, 0.1405 / 1.964, 0.1497 / 2.126 -> 1.
-inline int pts_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("POTGPU_PTS_VARIANT");
-    return e ? std::atoi(e) : 1;
-  }();
-  return v;
-}
 
 // Sweep dispatch (one launch over the rows of `sh`, or all rows).
 inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const double* lu, const double* lv,
@@ -232,12 +224,10 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
   } else {
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
-    switch (pts_variant()) {
-      case 1: sweep_pts_f32<false, false><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      case 2: sweep_pts_f32<false, true><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      case 3: sweep_pts_f32<true, false><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      case 4: sweep_pts_f32<true, true><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      default: sweep_f32<SrcPointsDotF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
+    switch (pts_pairs()) {
+      case 4: sweep_pts_f32<4><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
+      case 6: sweep_pts_f32<6><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
+      default: sweep_pts_f32<8><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
     }
   }
   PG_CK(cudaGetLastError());

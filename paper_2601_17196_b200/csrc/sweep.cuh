@@ -404,18 +404,16 @@ __host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta) {
   return size_t(rows_per_cta) * sizeof(float4) + size_t(kWarps * 32 * 33) * sizeof(float);
 }
 
-__device__ __forceinline__ float warp_maxf_shfl(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
-  return x;
-}
-
-template <bool PIPE, bool SHFL>
-__global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src, SweepArgs a) {
+// KP column pairs per lane (2 KP columns, a 64 KP-column warp strip); KP = 8
+// matches sweep_f32's map. Fewer pairs -> fewer registers -> more resident
+// warps to cover the per-row dependency chain (profiles/pts_variants.sh).
+template <int KP>
+__global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(SrcPointsDotF32 src, SweepArgs a) {
+  constexpr int kStrip = 64 * KP;
   if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
-  const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
+  const int64_t j0 = int64_t(blockIdx.x) * kStrip;
   const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
   const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
   const double w = *a.w;
@@ -428,10 +426,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src
     const float4 x2 = src.X2[i];
     s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
   }
-  float2 Bj[kPairs];
-  SrcPointsDotF32::Col cols[kPairs];
+  float2 Bj[KP], cx[KP], cy[KP], cz[KP];
 #pragma unroll
-  for (int q = 0; q < kPairs; ++q) {
+  for (int q = 0; q < KP; ++q) {
     float b[2];
     float4 y[2];
 #pragma unroll
@@ -449,14 +446,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src
       b[h] = float(vv);
     }
     Bj[q] = make_float2(b[0], b[1]);
-    cols[q].x = make_float2(y[0].x, y[1].x);
-    cols[q].y = make_float2(y[0].y, y[1].y);
-    cols[q].z = make_float2(y[0].z, y[1].z);
+    cx[q] = make_float2(y[0].x, y[1].x);
+    cy[q] = make_float2(y[0].y, y[1].y);
+    cz[q] = make_float2(y[0].z, y[1].z);
   }
   __syncthreads();
-  float2 cacc[kPairs];
+  float2 cacc[KP];
 #pragma unroll
-  for (int q = 0; q < kPairs; ++q) cacc[q] = make_float2(0.f, 0.f);
+  for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
   float sigma = -INFINITY;
   float mmax = -INFINITY;
   float2* rowp = reinterpret_cast<float2*>(a.rowp);  // [row][strip]
@@ -477,45 +474,32 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src
     }
     __syncwarp();
   };
-  auto lane_max = [](const float2 (&t)[kPairs]) {
-    float m = fmaxf(fmaxf(fmaxf(t[0].x, t[0].y), fmaxf(t[1].x, t[1].y)), fmaxf(fmaxf(t[2].x, t[2].y), fmaxf(t[3].x, t[3].y)));
-#pragma unroll
-    for (int q = 4; q < kPairs; q += 4)
-      m = fmaxf(m, fmaxf(fmaxf(fmaxf(t[q].x, t[q].y), fmaxf(t[q + 1].x, t[q + 1].y)), fmaxf(fmaxf(t[q + 2].x, t[q + 2].y), fmaxf(t[q + 3].x, t[q + 3].y))));
-    return m;
-  };
-  auto wmax = [](float x) { return SHFL ? warp_maxf_shfl(x) : warp_maxf(x); };
-  // prologue: the first row's max (pipelined variant)
-  float Mcur = -INFINITY;
-  if (PIPE && r0 + warp < r1) {
-    float2 t[kPairs];
-    src.expo(SrcPointsDotF32::RowData{s_R[warp]}, cols, Bj, t);
-    Mcur = wmax(lane_max(t));
-  }
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
-    // issue the next row's max (consumed one iteration later)
-    float Mnxt = -INFINITY;
-    if (PIPE && i + kWarps < r1) {
-      float2 tn[kPairs];
-      src.expo(SrcPointsDotF32::RowData{s_R[i + kWarps - r0]}, cols, Bj, tn);
-      Mnxt = wmax(lane_max(tn));
-    }
     const float4 dc = s_R[i - r0];
-    float2 t[kPairs];
-    src.expo(SrcPointsDotF32::RowData{dc}, cols, Bj, t);  // (re)compute this row
-    const float m = PIPE ? Mcur : wmax(lane_max(t));
+    const float2 px = make_float2(dc.x, dc.x), py = make_float2(dc.y, dc.y), pz = make_float2(dc.z, dc.z);
+    float2 t[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      float2 tt = __ffma2_rn(px, cx[q], Bj[q]);
+      tt = __ffma2_rn(py, cy[q], tt);
+      t[q] = __ffma2_rn(pz, cz[q], tt);
+    }
+    float m = fmaxf(t[0].x, t[0].y);
+#pragma unroll
+    for (int q = 1; q < KP; ++q) m = fmaxf(m, fmaxf(t[q].x, t[q].y));
+    m = warp_maxf(m);
     const float Ai = dc.w;
     const float ms = (m == -INFINITY) ? 0.f : m;
     const float2 M2 = make_float2(-ms, -ms);
-    float2 p[kPairs];
+    float2 p[KP];
 #pragma unroll
-    for (int q = 0; q < kPairs; ++q) {
+    for (int q = 0; q < KP; ++q) {
       const float2 d = __fadd2_rn(t[q], M2);
       p[q] = make_float2(ex2f(d.x), ex2f(d.y));
     }
-    float2 rs = __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3]));
+    float2 rs = p[0];
 #pragma unroll
-    for (int q = 4; q < kPairs; q += 4) rs = __fadd2_rn(rs, __fadd2_rn(__fadd2_rn(p[q], p[q + 1]), __fadd2_rn(p[q + 2], p[q + 3])));
+    for (int q = 1; q < KP; ++q) rs = __fadd2_rn(rs, p[q]);
     *tslot = rs.x + rs.y;
     tslot += 33;
     if (lane == slot) my_ms = ms;
@@ -529,18 +513,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src
     if (mA > sigma) {  // warp-uniform
       const float sc = ex2f(sigma - mA);
 #pragma unroll
-      for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
       sigma = mA;
     }
     mmax = fmaxf(mmax, mA);
     const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
     const float2 F2 = make_float2(f, f);
 #pragma unroll
-    for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
-    Mcur = Mnxt;
+    for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
   }
   if (slot > 0) flush(slot);
-  __shared__ float cs[kWarps][kStripCols32];
+  __shared__ float cs[kWarps][kStrip];
   __shared__ float ss[kWarps];
   __shared__ float mm[kWarps];
   if (lane == 0) {
@@ -552,14 +535,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts_f32(SrcPointsDotF32 src
   for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
   const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
 #pragma unroll
-  for (int q = 0; q < kPairs; ++q) {
+  for (int q = 0; q < KP; ++q) {
     const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
     cs[warp][c] = cacc[q].x * fw;
     cs[warp][c + 1] = cacc[q].y * fw;
   }
   __syncthreads();
   float2* colp = reinterpret_cast<float2*>(a.colp);
-  for (int c = threadIdx.x; c < kStripCols32; c += kThreads) {
+  for (int c = threadIdx.x; c < kStrip; c += kThreads) {
     float s = 0.f;
 #pragma unroll
     for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
@@ -591,6 +574,17 @@ inline int sweep_waves() {
     return v > 0 ? v : 1;
   }();
   return w;
+}
+
+// Column pairs per lane of the points sweep ($POTGPU_PTS_PAIRS: 4, 6, 8;
+// profiles/pts_variants.sh).
+inline int pts_pairs() {
+  static const int v = [] {
+    const char* e = std::getenv("POTGPU_PTS_PAIRS");
+    const int k = e ? std::atoi(e) : 0;
+    return (k == 4 || k == 6 || k == 8) ? k : 8;
+  }();
+  return v;
 }
 
 constexpr int64_t kMaxRowsPerCta = 2048;

@@ -1,10 +1,10 @@
-# points-sweep kernel variants (POTGPU_PTS_VARIANT), C3 and C4 sweep times
-for v in 0 1 2 3 4; do
-  POTGPU_PTS_VARIANT=$v python - <<'PY'
+# points-sweep column pairs per lane (POTGPU_PTS_PAIRS), C3 and C4 sweep times
+for v in 8 6 4; do
+  POTGPU_PTS_PAIRS=$v python - <<'PY'
 import os, json
 from paper_2601_17196_b200 import pot
 ctx = pot.Context(0)
-out = {"variant": int(os.environ["POTGPU_PTS_VARIANT"])}
+out = {"pairs": int(os.environ["POTGPU_PTS_PAIRS"])}
 for cid, eps in ((3, 1e-2), (4, 1e-3)):
     inst = pot.config_instance(cid)
     cfg = pot.SolverConfig(epsilon=eps, log_every=10**9, max_iterations=10**7, record_rounded_cost=False, materialize_plan=False)
