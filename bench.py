@@ -252,7 +252,7 @@ def main():
     mufu_peak = 16 * nsm * sm_mhz * 1e6 / 1e9  # G ex2/s at the measured clock
     achieved = elems / (ms_sweep * 1e-3) / 1e9
     roofline = {"bound": "mufu", "achieved": achieved, "peak": mufu_peak, "unit": "Gex2/s", "frac": achieved / mufu_peak,
-                "traffic": None, "kernel": "sweep_pts_f32<SrcPointsDotF32>", "ms_per_launch": ms_sweep,
+                "traffic": None, "kernel": "sweep_pts2_f32 (points, 2 rows x 16 columns per warp step)", "ms_per_launch": ms_sweep,
                 "per_unit": "1 MUFU.EX2 per plan entry; n^2 entries per launch",
                 "peak_source": f"16 ex2/clk/SM x {nsm} SMs x median SM clock {sm_mhz} MHz under load"}
     cpu = None

@@ -137,13 +137,14 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   } else {
     const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
     switch (pts_pairs()) {
+      case 2: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32, kThreads, sm_est)); break;
       case 4: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<4>, kThreads, sm_est)); break;
       case 6: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<6>, kThreads, sm_est)); break;
       default: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<8>, kThreads, sm_est)); break;
     }
   }
   occ = std::max(occ, 1);
-  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * pts_pairs() : kStripCols32);
+  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * (pts_pairs() == 2 ? kPairs : pts_pairs()) : kStripCols32);
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
   ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip);
   int64_t max_rb = ws.g.grid.y;
@@ -168,6 +169,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts_smem(max_rpc), sweep_f32_smem(max_rpc));
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
@@ -225,6 +227,7 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
     switch (pts_pairs()) {
+      case 2: sweep_pts2_f32<<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;  // two-row variant
       case 4: sweep_pts_f32<4><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
       case 6: sweep_pts_f32<6><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
       default: sweep_pts_f32<8><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;

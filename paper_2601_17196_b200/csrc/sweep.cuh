@@ -555,6 +555,194 @@ __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(Src
   }
 }
 
+// Two-row variant of sweep_pts_f32<8>: a warp exponentiates rows i and
+// i + 8 in one iteration (two independent max / CREDUX / MUFU chains in
+// flight). The column constants B'_j live in shared memory ([pair][lane]
+// float2, conflict-free) so the second row's exponents fit in registers.
+__global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 src, SweepArgs a) {
+  constexpr int KP = kPairs;
+  constexpr int kStrip = 64 * KP;
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStrip;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i), then the row-sum tiles
+  __shared__ float2 s_B[KP][32];
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
+  }
+  float2 cx[KP], cy[KP], cz[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;
+      y[h] = make_float4(0, 0, 0, 0);
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
+        y[h] = src.Ys[j];
+      }
+      b[h] = float(vv);
+    }
+    if (warp == 0) s_B[q][lane] = make_float2(b[0], b[1]);
+    cx[q] = make_float2(y[0].x, y[1].x);
+    cy[q] = make_float2(y[0].y, y[1].y);
+    cz[q] = make_float2(y[0].z, y[1].z);
+  }
+  __syncthreads();
+  float2 cacc[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY;
+  float mmax = -INFINITY;
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);
+  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;
+  float my_ms = 0.f;
+  int slot = 0;
+  int64_t ib = r0 + warp;
+  const int64_t ldp = gridDim.x;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+    }
+    __syncwarp();
+  };
+  // one row's tile slot, column scale update and accumulation
+  auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    float2 rs = p[0];
+#pragma unroll
+    for (int q = 1; q < KP; ++q) rs = __fadd2_rn(rs, p[q]);
+    *tslot = rs.x + rs.y;
+    tslot += 33;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      tslot = tile + lane;
+      ib = i + kWarps;
+    }
+    const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;
+    if (mA > sigma) {
+      const float sc = ex2f(sigma - mA);
+#pragma unroll
+      for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = mA;
+    }
+    mmax = fmaxf(mmax, mA);
+    const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+    const float2 F2 = make_float2(f, f);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+  };
+  int64_t i = r0 + warp;
+  for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
+    const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+    float2 ta[KP], tb[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 B = s_B[q][lane];
+      float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+      float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
+      xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+      xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
+      ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+      tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+    }
+    float ma = fmaxf(ta[0].x, ta[0].y), mb = fmaxf(tb[0].x, tb[0].y);
+#pragma unroll
+    for (int q = 1; q < KP; ++q) {
+      ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
+      mb = fmaxf(mb, fmaxf(tb[q].x, tb[q].y));
+    }
+    ma = warp_maxf(ma);
+    mb = warp_maxf(mb);
+    const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
+      tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+    }
+    finish_row(ma, da.w, ta, i);
+    finish_row(mb, db.w, tb, i + kWarps);
+  }
+  if (i < r1) {  // a last single row
+    const float4 da = s_R[i - r0];
+    float2 ta[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 B = s_B[q][lane];
+      float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+      xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+      ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+    }
+    float ma = fmaxf(ta[0].x, ta[0].y);
+#pragma unroll
+    for (int q = 1; q < KP; ++q) ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
+    ma = warp_maxf(ma);
+    const float msa = (ma == -INFINITY) ? 0.f : ma;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+    }
+    finish_row(ma, da.w, ta, i);
+  }
+  if (slot > 0) flush(slot);
+  __shared__ float cs[kWarps][kStrip];
+  __shared__ float ss[kWarps];
+  __shared__ float mm[kWarps];
+  if (lane == 0) {
+    ss[warp] = sigma;
+    mm[warp] = mmax;
+  }
+  __syncthreads();
+  float sig = ss[0];
+  for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+  const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+    cs[warp][c] = cacc[q].x * fw;
+    cs[warp][c + 1] = cacc[q].y * fw;
+  }
+  __syncthreads();
+  float2* colp = reinterpret_cast<float2*>(a.colp);
+  for (int c = threadIdx.x; c < kStrip; c += kThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+  }
+  if (threadIdx.x == 0) {
+    float m = mm[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
 // ------------------------------------------------------------------------
 // Grid shape: strips x row blocks, the row-block count chosen so the CTA
 // count fills the resident capacity (SMs x occupancy) as evenly as possible.
@@ -576,13 +764,14 @@ inline int sweep_waves() {
   return w;
 }
 
-// Column pairs per lane of the points sweep ($POTGPU_PTS_PAIRS: 4, 6, 8;
-// profiles/pts_variants.sh).
+// Points-sweep kernel ($POTGPU_PTS_PAIRS): 2 = sweep_pts2_f32 (8 pairs per
+// lane, two rows per iteration; default, fastest measured), 4 / 6 / 8 =
+// sweep_pts_f32<KP> (profiles/pts_variants.sh).
 inline int pts_pairs() {
   static const int v = [] {
     const char* e = std::getenv("POTGPU_PTS_PAIRS");
     const int k = e ? std::atoi(e) : 0;
-    return (k == 4 || k == 6 || k == 8) ? k : 8;
+    return (k == 2 || k == 4 || k == 6 || k == 8) ? k : 2;  // 2: the two-row 8-pair variant (default)
   }();
   return v;
 }

@@ -1,5 +1,5 @@
 # points-sweep column pairs per lane (POTGPU_PTS_PAIRS), C3 and C4 sweep times
-for v in 8 6 4; do
+for v in 8 2; do
   POTGPU_PTS_PAIRS=$v python - <<'PY'
 import os, json
 from paper_2601_17196_b200 import pot

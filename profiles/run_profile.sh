@@ -14,7 +14,7 @@ $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fi
   python bench.py --steps 3 --warmup 3 --no-tte --no-cpu > $OUT/ncu_launches.log 2>&1; echo "launches rc=$?"
 # full captures: the on-the-fly sweep mid-loop, the stored sweep, the point evaluation
 $NCU --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:sweep_pts_f32" --launch-skip 12 --launch-count 1 -o $OUT/sweep_points -f \
+  -k "regex:sweep_pts2_f32" --launch-skip 12 --launch-count 1 -o $OUT/sweep_points -f \
   python bench.py --steps 3 --warmup 3 --no-tte --no-cpu > $OUT/ncu_points.log 2>&1; echo "points rc=$?"
 $NCU --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k "regex:sweep_f32<potgpu::SrcDenseF32>" --launch-skip 4 --launch-count 1 -o $OUT/sweep_stored -f \

