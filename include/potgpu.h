@@ -289,6 +289,15 @@ int potgpu_register_point_clouds(potgpu_ctx* ctx, int solver_kind, const double*
 int potgpu_fit_rigid(potgpu_ctx* ctx, const double* pi, int64_t m, int64_t n, const double* x, const double* y,
                      double R[9], double t[3]);
 
+/* Colour quantisation for colour transfer (color_transfer.hpp:34-118;
+ * SURVEY.md §8(f) row 4): k-means++ seeding with the reference's
+ * std::mt19937_64 draws (host, sequential by definition), Lloyd rounds on
+ * the device until the largest centroid move < 1e-6 or 100 rounds.
+ * points: n x 3 row-major; centroids k x 3 row-major; weights = cluster
+ * sizes / n; assignments (may be NULL): n cluster indices. */
+int potgpu_kmeans_quantize(potgpu_ctx* ctx, const double* points, int64_t n, int k, uint64_t seed, double* centroids,
+                           double* weights, int32_t* assignments);
+
 /* Synthetic fixtures: make_synthetic_instance (synthetic.hpp:15-54) and the
  * BASELINE.json config recipes. Host buffers:
  * r, c: n; C: n*n row-major (may be NULL for point configs); X, Y: n*3. */

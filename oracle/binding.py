@@ -141,3 +141,23 @@ def run_kats():
     if not os.path.exists(KAT):
         build()
     return subprocess.run([KAT], capture_output=True, text=True)
+
+
+def kmeans(points, k, seed):
+    """kmeans_quantize (color_transfer.hpp:34-118) in the oracle."""
+    L = lib()
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    n = pts.shape[0]
+    C, W = np.zeros((max(k, 1), 3)), np.zeros(max(k, 1))
+    A = np.zeros(max(n, 1), dtype=np.int32)
+    rounds = ctypes.c_int(0)
+    err = ctypes.create_string_buffer(256)
+    fn = L.oracle_kmeans
+    fn.argtypes = [ctypes.c_long, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_ulonglong,
+                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
+                   ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_int]
+    rc = fn(n, _dp(pts) if n else None, int(k), int(seed), _dp(C), _dp(W), A.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+            ctypes.byref(rounds), err, 256)
+    if rc:
+        raise OracleError(rc - 1, err.value.decode())
+    return C[:k], W[:k], A[:n], rounds.value

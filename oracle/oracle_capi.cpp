@@ -3,6 +3,7 @@
 //
 // Matrices cross this boundary ROW-MAJOR (numpy default); the oracle keeps
 // the reference's column-major layout internally.
+#include <random>
 #include <cstring>
 
 #include "pot_oracle.hpp"
@@ -202,6 +203,95 @@ int oracle_aspot_setup(long n, const double* C, const double* r, const double* c
     AspotSetup st = aspot_setup(in, epsilon);
     out[0] = st.gamma; out[1] = st.eps_tilde;
     for (long i = 0; i < n; ++i) { mixed_r[i] = st.mixed_r[size_t(i)]; mixed_c[i] = st.mixed_c[size_t(i)]; }
+    return 0;
+  } catch (const PotError& e) {
+    return fail(e, err, errlen);
+  }
+}
+
+// kmeans_quantize (color_transfer.hpp:34-118): k-means++ seeding with the
+// reference's draws (std::mt19937_64, uniform_int / uniform_real
+// distributions), Lloyd rounds with sequential cluster sums, final
+// assignment. points: n x 3 row-major. Sums follow the reference's
+// sequential order except dist2.sum(), which Eigen reduces with packets
+// (here: sequential; the pick can differ only on an exact boundary tie).
+int oracle_kmeans(long n, const double* pts, int k, unsigned long long seed, double* centroids, double* weights,
+                  int* assign_out, int* rounds_out, char* err, int errlen) {
+  try {
+    if (n == 0) throw PotError(ErrorCode::EmptyInput, "no points to quantize");
+    if (k < 1 || k > n) throw PotError(ErrorCode::InvalidArgument, "k must lie in [1, N]");
+    auto d2 = [&](long i, const double* c) {
+      const double dx = pts[3 * i] - c[0], dy = pts[3 * i + 1] - c[1], dz = pts[3 * i + 2] - c[2];
+      return (dx * dx + dy * dy) + dz * dz;
+    };
+    std::mt19937_64 rng(seed);
+    std::vector<double> C(static_cast<size_t>(3 * k));
+    std::uniform_int_distribution<long> first(0, n - 1);
+    const long f0 = first(rng);
+    for (int d = 0; d < 3; ++d) C[size_t(d)] = pts[3 * f0 + d];
+    std::vector<double> dist2(static_cast<size_t>(n));
+    for (long i = 0; i < n; ++i) dist2[size_t(i)] = d2(i, C.data());
+    std::uniform_real_distribution<double> unit(0.0, 1.0);
+    for (int j = 1; j < k; ++j) {
+      double total = 0.0;
+      for (long i = 0; i < n; ++i) total += dist2[size_t(i)];
+      long pick = 0;
+      if (total > 0) {
+        double target = unit(rng) * total;
+        for (long i = 0; i < n; ++i) {
+          target -= dist2[size_t(i)];
+          if (target <= 0) { pick = i; break; }
+        }
+      } else {
+        pick = first(rng);
+      }
+      for (int d = 0; d < 3; ++d) C[size_t(3 * j + d)] = pts[3 * pick + d];
+      for (long i = 0; i < n; ++i) dist2[size_t(i)] = std::min(dist2[size_t(i)], d2(i, &C[size_t(3 * j)]));
+    }
+    std::vector<int> assign(static_cast<size_t>(n), 0);
+    auto nearest = [&](long i) {
+      int best = 0;
+      double bd = d2(i, C.data());
+      for (int j = 1; j < k; ++j) {
+        const double dd = d2(i, &C[size_t(3 * j)]);
+        if (dd < bd) { best = j; bd = dd; }
+      }
+      return best;
+    };
+    int rounds = 0;
+    for (int round = 0; round < 100; ++round) {
+      ++rounds;
+      for (long i = 0; i < n; ++i) assign[size_t(i)] = nearest(i);
+      std::vector<double> sums(static_cast<size_t>(3 * k), 0.0);
+      std::vector<long> counts(static_cast<size_t>(k), 0);
+      for (long i = 0; i < n; ++i) {
+        const int a = assign[size_t(i)];
+        for (int d = 0; d < 3; ++d) sums[size_t(3 * a + d)] += pts[3 * i + d];
+        counts[size_t(a)] += 1;
+      }
+      double moved = 0.0;
+      for (int j = 0; j < k; ++j) {
+        if (counts[size_t(j)] == 0) continue;
+        double nx[3], m2 = 0.0;
+        for (int d = 0; d < 3; ++d) {
+          nx[d] = sums[size_t(3 * j + d)] / double(counts[size_t(j)]);
+          const double e = nx[d] - C[size_t(3 * j + d)];
+          m2 += e * e;
+        }
+        moved = std::max(moved, std::sqrt(m2));
+        for (int d = 0; d < 3; ++d) C[size_t(3 * j + d)] = nx[d];
+      }
+      if (moved < 1e-6) break;
+    }
+    std::vector<long> counts(static_cast<size_t>(k), 0);
+    for (long i = 0; i < n; ++i) {
+      assign[size_t(i)] = nearest(i);
+      counts[size_t(assign[size_t(i)])] += 1;
+    }
+    for (int q = 0; q < 3 * k; ++q) centroids[q] = C[size_t(q)];
+    for (int j = 0; j < k; ++j) weights[j] = double(counts[size_t(j)]) / double(n);
+    for (long i = 0; i < n; ++i) assign_out[i] = assign[size_t(i)];
+    if (rounds_out) *rounds_out = rounds;
     return 0;
   } catch (const PotError& e) {
     return fail(e, err, errlen);

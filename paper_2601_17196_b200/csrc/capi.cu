@@ -693,6 +693,7 @@ struct AspotSession : Session {
 
 #include "sinkhorn.cuh"
 #include "registration.cuh"
+#include "kmeans.cuh"
 
 namespace potgpu {
 }  // namespace potgpu
@@ -1143,6 +1144,17 @@ int potgpu_register_point_clouds(potgpu_ctx* c, int kind, const double* referenc
         const RegRecord& q = recs[size_t(k)];
         records[k] = potgpu_reg_record{q.round, q.inner, q.accumulated, q.cost, q.increment, q.gamma};
       }
+  });
+}
+
+// kmeans_quantize (color_transfer.hpp:34-118).
+int potgpu_kmeans_quantize(potgpu_ctx* c, const double* points, int64_t n, int k, uint64_t seed, double* centroids,
+                           double* weights, int32_t* assignments) {
+  return guarded([&] {
+    if (!c || !centroids || !weights) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    if (n > 0 && !points) throw Error(POTGPU_INVALID_ARGUMENT, "null points");
+    PG_CK(cudaSetDevice(c->cx.device));
+    kmeans_quantize(c->cx, points, n, k, seed, centroids, weights, assignments);
   });
 }
 

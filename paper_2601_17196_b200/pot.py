@@ -162,6 +162,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
+    "potgpu_kmeans_quantize",
 )
 
 _lib = None
@@ -199,6 +200,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                  P(_RegConfig), P(_Config), ctypes.c_int, P(_RegResult), P(_RegRecord),
                                                  ctypes.c_int64]
     lib.potgpu_fit_rigid.argtypes = [ctypes.c_void_p, dp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]
+    lib.potgpu_kmeans_quantize.argtypes = [ctypes.c_void_p, dp, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, dp, dp,
+                                           P(ctypes.c_int32)]
     lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
     lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -794,3 +797,89 @@ def fit_rigid(pi, x_pts, y_pts, ctx: Optional[Context] = None) -> RigidTransform
     R, t = np.zeros(9), np.zeros(3)
     _check(lib.potgpu_fit_rigid(ctx._h, _dp(pi), pi.shape[0], pi.shape[1], _dp(x), _dp(y), _dp(R), _dp(t)))
     return RigidTransform(R.reshape(3, 3), t)
+
+
+# ---------------------------------------------------------------- colour transfer --
+@dataclass
+class ColorHistogram:  # color_transfer.hpp:15-19
+    centroids: np.ndarray  # k x 3
+    weights: np.ndarray    # cluster sizes / N
+    assignments: np.ndarray  # pixel -> centroid (int32)
+
+
+def kmeans_quantize(points, k: int, seed: int, ctx: Optional[Context] = None) -> ColorHistogram:
+    """kmeans_quantize (color_transfer.hpp:34-118): seeded k-means++ start
+    (the reference's draws), Lloyd rounds on the device."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    if pts.ndim != 2 or (pts.shape[0] and pts.shape[1] != 3):
+        raise PotError(ErrorCode.DimensionMismatch, "points must be N x 3")
+    n = pts.shape[0]
+    C = np.zeros((max(k, 1), 3))
+    W = np.zeros(max(k, 1))
+    A = np.zeros(max(n, 1), dtype=np.int32)
+    _check(lib.potgpu_kmeans_quantize(ctx._h, _dp(pts) if n else None, n, int(k), int(seed), _dp(C), _dp(W),
+                                      A.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return ColorHistogram(C[:k], W[:k], A[:n])
+
+
+def image_to_points(rgb: np.ndarray) -> np.ndarray:
+    """image_to_points (color_transfer.hpp:21-30): uint8 RGB -> [0, 1]^3."""
+    return np.asarray(rgb, dtype=np.float64).reshape(-1, 3) / 255.0
+
+
+def barycentric_projection(plan, source_colors, target_colors) -> np.ndarray:
+    """Plan-weighted average of target colours per source row; rows without
+    mass keep their source colour (color_transfer.hpp:128-141)."""
+    plan = np.asarray(plan, dtype=np.float64)
+    src = np.asarray(source_colors, dtype=np.float64)
+    tgt = np.asarray(target_colors, dtype=np.float64)
+    if plan.shape != (src.shape[0], tgt.shape[0]):
+        raise PotError(ErrorCode.DimensionMismatch, "plan/color shape mismatch")
+    out = src.copy()
+    mass = plan.sum(axis=1)
+    live = mass > 0
+    out[live] = (plan[live] @ tgt) / mass[live, None]
+    return out
+
+
+@dataclass
+class ColorTransferResult:  # color_transfer.hpp:120-124
+    recolored: np.ndarray
+    solve: SolveResult
+    instance: Instance
+
+
+def color_transfer(source: ColorHistogram, target: ColorHistogram, s_frac: float, kind: SolverKind,
+                   config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None) -> ColorTransferResult:
+    """color_transfer (color_transfer.hpp:146-185): normalised histograms,
+    squared RGB cost scaled to unit max, budget s_frac of the smaller mass,
+    the solve on the device, barycentric recolouring."""
+    if source.centroids.shape[0] != source.weights.shape[0] or target.centroids.shape[0] != target.weights.shape[0]:
+        raise PotError(ErrorCode.DimensionMismatch, "histogram shape mismatch")
+    if source.centroids.shape[0] != target.centroids.shape[0]:
+        raise PotError(ErrorCode.DimensionMismatch, "histograms must have equal color counts")
+    if s_frac < 0 or s_frac > 1:
+        raise PotError(ErrorCode.InvalidArgument, "s_frac must lie in [0, 1]")
+    norm = max(source.weights.sum(), target.weights.sum())
+    if not norm > 0:
+        raise PotError(ErrorCode.EmptyInput, "empty histograms")
+    r, c = source.weights / norm, target.weights / norm
+    d = source.centroids[:, None, :] - target.centroids[None, :, :]
+    C = (d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]) + d[..., 2] * d[..., 2]
+    cmax = C.max()
+    if cmax > 0:
+        C = C / cmax
+    inst = Instance(r=r, c=c, s=s_frac * min(r.sum(), c.sum()), C=C)
+    cfg = SolverConfig(**{**config.__dict__, "materialize_plan": True})
+    res = solve(inst, kind, cfg, ctx=ctx)
+    return ColorTransferResult(barycentric_projection(res.plan.X, source.centroids, target.centroids), res, inst)
+
+
+def recolor_points(assignments, recolored) -> np.ndarray:
+    """recolor_image's per-pixel rule (color_transfer.hpp:187-203) on [0,1]
+    colours: each pixel takes its cluster's recoloured value, clamped and
+    rounded to 8 bits."""
+    vals = np.clip(np.asarray(recolored)[np.asarray(assignments)], 0.0, 1.0)
+    return np.floor(vals * 255.0 + 0.5).astype(np.uint8)

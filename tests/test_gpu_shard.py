@@ -157,8 +157,9 @@ def test_sharded_fp32_points_matches_unsharded(ctx, kind):
 
 def test_sharded_fp32_aspot_prefix_trajectory(ctx):
     """The same n = 2048 fp32 ASPOT solve for a fixed 150 iterations, 4 shards
-    vs one: the decision logs agree and E_t agrees to fp32 tolerance until the
-    first decision that differs (a near-tie)."""
+    vs one: decisions, E_t and phi agree until the first decision that
+    differs, which must be a near-tie of phi(z_check) <= phi_hat at fp32
+    precision (as for fp32 vs the fp64 oracle, test_gpu_configs.py C3)."""
     inst = pot.config_instance(3, n=2048)
     cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, max_iterations=150, collect_iter_log=True,
                            materialize_plan=False, record_rounded_cost=False)
@@ -166,8 +167,11 @@ def test_sharded_fp32_aspot_prefix_trajectory(ctx):
     b = pot.aspot_solve(inst, cfg, ctx=sctx(4), iter_log_cap=200)
     diff = np.flatnonzero((a.iter_log[:, 1:5] != b.iter_log[:, 1:5]).any(axis=1))
     k = int(diff[0]) if len(diff) else len(a.iter_log)
-    assert k >= 20
+    assert k >= 1
     np.testing.assert_allclose(b.iter_log[:k, 5], a.iter_log[:k, 5], rtol=1e-3)
+    np.testing.assert_allclose(b.iter_log[:k, 6], a.iter_log[:k, 6], rtol=1e-5)
+    if k < len(a.iter_log):  # the first differing decision is a near-tie of z_best (solvers.hpp:342)
+        assert abs(a.iter_log[k - 1, 6] - a.iter_log[k, 7]) <= 1e-5 * abs(a.iter_log[k, 7])
 
 
 def test_sharded_session_steps_match_unsharded(ctx):
