@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <random>
 
+#include "pot/color_transfer.hpp"
+#include "pot/io.hpp"
 #include "pot/registration.hpp"
 #include "pot/solvers.hpp"
 #include "pot/synthetic.hpp"
@@ -143,6 +145,53 @@ int main() {
     EXPECT(res.rounds.size() <= 1u);
     EXPECT((res.transform.R - Matrix3d::Identity()).norm() <= 1e-4);
     EXPECT(res.transform.t.norm() <= 1e-4);
+  }
+  {  // Kmeans.EachPointItsOwnCentroidWhenKEqualsN / RejectsBadArguments (test_apps.cpp:38-87)
+    std::mt19937_64 rng(61);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    Matrix pts(6, 3);
+    for (long i = 0; i < 6; ++i) for (int d = 0; d < 3; ++d) pts(i, d) = u(rng);
+    const ColorHistogram h = kmeans_quantize(pts, 6, 7);
+    for (long j = 0; j < 6; ++j) EXPECT(std::fabs(h.weights(j) - 1.0 / 6.0) <= 1e-15);
+    bool threw = false;
+    try { kmeans_quantize(pts, 7, 1); } catch (const PotError& e) { threw = e.code() == ErrorCode::InvalidArgument; }
+    EXPECT(threw);
+  }
+  {  // ColorTransfer.BudgetAndNormalization (test_apps.cpp:145-158)
+    std::mt19937_64 rng(66);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    Matrix a(300, 3), b(300, 3);
+    for (long i = 0; i < 300; ++i) for (int d = 0; d < 3; ++d) { a(i, d) = u(rng); b(i, d) = u(rng); }
+    const ColorHistogram src = kmeans_quantize(a, 6, 1), tgt = kmeans_quantize(b, 6, 2);
+    SolverConfig cfg;
+    cfg.epsilon = 0.05;
+    cfg.log_every = 1000000;
+    const ColorTransferResult res = color_transfer(src, tgt, 0.2, SolverKind::TunedSinkhorn, cfg);
+    EXPECT(std::fabs(res.instance.s - 0.2 * std::min(res.instance.r.sum(), res.instance.c.sum())) <= 1e-12);
+    EXPECT(std::fabs(res.instance.C.maxCoeff() - 1.0) <= 1e-12);
+    EXPECT(plan_feasibility_gap(res.solve.plan, res.instance) <= 1e-9);
+  }
+  {  // io round trips: JSON / binary instance, trace CSV header, PPM, XYZ
+    Instance in = make_synthetic_instance(7, 3, 1.0, 1.2, 0.5);
+    write_instance_json("/tmp/potgpu_dropin_inst.json", in);
+    const Instance j = read_instance_json("/tmp/potgpu_dropin_inst.json");
+    write_instance_bin("/tmp/potgpu_dropin_inst.potb", in);
+    const Instance b = read_instance_bin("/tmp/potgpu_dropin_inst.potb");
+    for (long i = 0; i < 7; ++i)
+      for (long k = 0; k < 7; ++k) EXPECT(j.C(i, k) == in.C(i, k) && b.C(i, k) == in.C(i, k));
+    EXPECT(j.s == in.s && b.s == in.s && j.r(3) == in.r(3) && b.c(6) == in.c(6));
+    SolverConfig cfg; cfg.epsilon = 0.1; cfg.log_every = 5;
+    const SolveResult res = aspot_solve(in, cfg);
+    const std::string csv = trace_to_csv(res.trace);
+    EXPECT(csv.rfind("t,E,phi,rounded_cost,elapsed_s\n", 0) == 0);
+    Image img; img.width = 3; img.height = 2; img.rgb = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18};
+    write_ppm("/tmp/potgpu_dropin.ppm", img);
+    const Image back = read_ppm("/tmp/potgpu_dropin.ppm");
+    EXPECT(back.width == 3 && back.height == 2 && back.rgb == img.rgb);
+    Matrix pts(2, 3); pts(0, 0) = 0.1; pts(1, 2) = -2.5;
+    write_xyz("/tmp/potgpu_dropin.xyz", pts);
+    const Matrix q = read_xyz("/tmp/potgpu_dropin.xyz");
+    EXPECT(q.rows() == 2 && q(0, 0) == 0.1 && q(1, 2) == -2.5);
   }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
