@@ -247,12 +247,25 @@ def main():
     e2e_wall = max_over_ranks(e2e_wall, dist, local)
     e2e_val = r2.iterations / e2e_wall
 
+    # DRAM bytes per launch of the same kernels from the committed ncu --set full
+    # captures (profiles/run_profile.sh -> profiles/summarize_ncu.py)
+    ncu_sum = {}
+    for rnd in sorted(os.listdir(os.path.join(ROOT, "profiles"))) if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
+        f = os.path.join(ROOT, "profiles", rnd, "ncu_summary.json")
+        if os.path.exists(f):
+            ncu_sum = json.load(open(f))
+    def traffic(name):
+        v = ncu_sum.get(name)
+        return None if not v else v["dram_read_bytes"] + v["dram_write_bytes"]
+    if isinstance(stored, dict) and "bound" in stored:
+        stored["traffic"] = traffic("sweep_stored")
+        stored["traffic_source"] = "ncu --set full capture committed in profiles/ (bytes per launch)"
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     mufu_peak = 16 * nsm * sm_mhz * 1e6 / 1e9  # G ex2/s at the measured clock
     achieved = elems / (ms_sweep * 1e-3) / 1e9
     roofline = {"bound": "mufu", "achieved": achieved, "peak": mufu_peak, "unit": "Gex2/s", "frac": achieved / mufu_peak,
-                "traffic": None, "kernel": "sweep_pts2_f32 (points, 2 rows x 16 columns per warp step)", "ms_per_launch": ms_sweep,
+                "traffic": traffic("sweep_points"), "kernel": "sweep_pts2_f32 (points, 2 rows x 16 columns per warp step)", "ms_per_launch": ms_sweep,
                 "per_unit": "1 MUFU.EX2 per plan entry; n^2 entries per launch",
                 "peak_source": f"16 ex2/clk/SM x {nsm} SMs x median SM clock {sm_mhz} MHz under load"}
     cpu = None

@@ -69,6 +69,7 @@ __device__ __forceinline__ double theta_next_d(double th) {  // solvers.hpp:32-3
 
 // z_bar = (1 - theta) z_check + theta z   (solvers.hpp:336, DualPoint ops dual.hpp:33-43)
 __global__ void k_zbar(AspotCtl* ctl, Slot zc, Slot z, Slot zb) {
+  pdl_wait();
   if (!ctl->g_new) return;
   const double th = ctl->theta, om = 1.0 - th;
   const int64_t n = zb.n;
@@ -227,6 +228,7 @@ __device__ __forceinline__ double group_partial_sum(const double* p, int64_t bas
 // reduces all partials in a fixed order and takes the decision
 // (apply_role). Deterministic, one launch.
 __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
+  pdl_wait();
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.z.n;
   double acc[kNumAcc];
@@ -281,22 +283,25 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   if (a.mode == 0)
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
       acc[11] = nan_max(acc[11], a.maxp[k]);
-  __shared__ double sh[kNumAcc][kEvalThreads];
+  // block reduction: warp shuffles, then the kEvalThreads / 32 warp results
+  __shared__ double sh[kNumAcc][kEvalThreads / 32];
   __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   auto block_reduce = [&]() {
 #pragma unroll
-    for (int k = 0; k < kNumAcc; ++k) sh[k][threadIdx.x] = acc[k];
-    __syncthreads();
-    for (int stride = kEvalThreads / 2; stride > 0; stride >>= 1) {
-      if (threadIdx.x < stride) {
+    for (int k = 0; k < kNumAcc; ++k) {
+      double x = acc[k];
 #pragma unroll
-        for (int k = 0; k < kNumAcc; ++k) {
-          const double o = sh[k][threadIdx.x + stride];
-          sh[k][threadIdx.x] = acc_join(k, sh[k][threadIdx.x], o);
-        }
-      }
-      __syncthreads();
+      for (int o = 16; o > 0; o >>= 1) x = acc_join(k, x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (lane == 0) sh[k][wid] = x;
     }
+    __syncthreads();
+    if (threadIdx.x < kNumAcc) {
+      double x = sh[threadIdx.x][0];
+      for (int w2 = 1; w2 < kEvalThreads / 32; ++w2) x = acc_join(threadIdx.x, x, sh[threadIdx.x][w2]);
+      sh[threadIdx.x][0] = x;
+    }
+    __syncthreads();
   };
   block_reduce();
   if (threadIdx.x < kNumAcc) a.scratch[blockIdx.x * (kNumAcc) + threadIdx.x] = sh[threadIdx.x][0];
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
 // first (dual.hpp:129-131) and kept for the retries (halving keeps z_bar).
 __global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const double* rowb, const double* colb,
                          const double* rt, const double* ct) {
+  pdl_wait();
   if (!ctl->g_alive) return;
   const int64_t n = zb.n;
   const int fresh = ctl->g_new;
@@ -355,6 +361,7 @@ __global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const 
 __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* row_a, const double* col_a, int role_a,
                             Slot src_b, const double* row_b, const double* col_b, int role_b, Slot dst,
                             const double* rt, const double* ct) {
+  pdl_wait();
   if (!ctl->g_alive) return;
   int block;
   Slot src;
@@ -391,6 +398,7 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
 // z_check <- sums of z_check' (solvers.hpp:357-360). Element-parallel.
 __global__ void k_commit_copy(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, double* rowc, double* colc,
                               const double* rown, const double* coln) {
+  pdl_wait();
   if (!ctl->g_active || !ctl->attempt_ok) return;
   const bool keep = ctl->keep_check;
   const int64_t n = z.n;
@@ -454,6 +462,7 @@ __device__ void loop_head(AspotCtl* ctl) {
 }
 
 __global__ void k_resume(AspotCtl* ctl, int64_t pause_at) {
+  pdl_wait();
   ctl->pause_at = pause_at;
   if (!ctl->paused) return;
   ctl->paused = 0;
@@ -462,6 +471,7 @@ __global__ void k_resume(AspotCtl* ctl, int64_t pause_at) {
 }
 
 __global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
+  pdl_wait();
   if (!ctl->g_active) return;
   ctl->attempts += 1;
   if (!ctl->attempt_ok) {

@@ -409,13 +409,13 @@ struct AspotSession : Session {
     const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
                ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
     const int gv = ws.nblk;
-    k_zbar<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZC, Z, ZB);
+    launch_k(k_zbar, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZC, Z, ZB);
     const SweepOut none{};
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new);
-    k_zgrave<<<gv, kVecThreads, 0, cx.stream>>>(ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
+    launch_k(k_zgrave, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma), ZG, R_GRAVE,
                 &ctl->g_alive);
-    k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
+    launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
                                                    ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
     // z_hat: a sweep, or (block w, ~all iterations) B(z_grave) scaled by e^dw
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma), ZH, R_HAT,
@@ -425,7 +425,7 @@ struct AspotSession : Session {
       sc.src_row_a = ws.row(R_GRAVE); sc.src_col_a = ws.col(R_GRAVE); sc.src_w_a = ZG.w(); sc.src_role_a = R_GRAVE;
       launch_eval(cx, ws, none, ZH, R_HAT, &ctl->g_hat_scaled, &sc);
     }
-    k_gk_update<<<gv, kVecThreads, 0, cx.stream>>>(ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
+    launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
                                                    ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
     // z_check' = GK(z_best): a sweep, or (block w) B(z_best) scaled
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma), ZN, R_NEW,
@@ -437,9 +437,9 @@ struct AspotSession : Session {
       sc.select_b = &ctl->keep_check;
       launch_eval(cx, ws, none, ZN, R_NEW, &ctl->g_new_scaled, &sc);
     }
-    k_commit_copy<<<gv, kVecThreads, 0, cx.stream>>>(ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
+    launch_k(k_commit_copy, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
                                                      ws.col(R_NEW));
-    k_commit_state<<<1, 1, 0, cx.stream>>>(ctl, ws.trace.p, ws.iterlog.p);
+    launch_k(k_commit_state, dim3(1), dim3(1), 0, cx.stream, ctl, ws.trace.p, ws.iterlog.p);
     PG_CK(cudaGetLastError());
   }
 
@@ -542,7 +542,7 @@ struct AspotSession : Session {
   // Device loop until it pauses at `stop` or the solve stops.
   void run_until(int64_t stop) {
     AspotCtl& h = *ws.host_ctl;
-    k_resume<<<1, 1, 0, cx.stream>>>(ws.ctl.p, stop);
+    launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop);
     launches += 1;
     // first burst: exactly the iterations asked for (1 attempt each unless a
     // step is halved), then poll every sync_every attempts

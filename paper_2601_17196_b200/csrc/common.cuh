@@ -5,6 +5,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -149,6 +151,32 @@ class BlockCache {
   std::multimap<Key, void*> free_;
 };
 
+// $POTGPU_PDL (default on): launch the per-iteration kernels with
+// programmatic stream serialization (captured as programmatic edges in the
+// CUDA graphs), hiding the launch latency between dependent kernels.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PG_CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -209,6 +237,11 @@ __device__ __forceinline__ double rho_limit(double a, double b) {
   if (!(b > 0)) return __longlong_as_double(0x7ff0000000000000ULL);
   return b - a + a * log(a / b);
 }
+
+// Programmatic dependent launch: a kernel launched with the PDL attribute
+// may start while its predecessor drains; it waits here before touching
+// anything the predecessor writes (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;

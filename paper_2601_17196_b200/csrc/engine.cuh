@@ -218,19 +218,19 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
   a.gate = gate;
   a.gamma = gamma;
   if (P.dtype == POTGPU_F64) {
-    if (floor_exp) sweep_f64_dense<true><<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
-    else sweep_f64_dense<false><<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, a);
+    if (floor_exp) launch_k(sweep_f64_dense<true>, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, a);
+    else launch_k(sweep_f64_dense<false>, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, a);
   } else if (P.kind == POTGPU_COST_DENSE) {
     SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
-    sweep_f32<SrcDenseF32><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a);
+    launch_k(sweep_f32<SrcDenseF32>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a);
   } else {
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
     switch (pts_pairs()) {
-      case 2: sweep_pts2_f32<<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;  // two-row variant
-      case 4: sweep_pts_f32<4><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      case 6: sweep_pts_f32<6><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
-      default: sweep_pts_f32<8><<<g.grid, kThreads, ws.sweep_smem, cx.stream>>>(s, a); break;
+      case 2: launch_k(sweep_pts2_f32, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;  // two-row variant
+      case 4: launch_k(sweep_pts_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
+      case 6: launch_k(sweep_pts_f32<6>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
+      default: launch_k(sweep_pts_f32<8>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
     }
   }
   PG_CK(cudaGetLastError());
@@ -259,7 +259,7 @@ inline SweepOut sweep_point(Context& cx, const DevProblem& P, Workspace& ws, Slo
   for (size_t p = 0; p < ws.shards.size(); ++p) {
     const ShardGrid& sh = ws.shards[p];
     launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma, &sh);
-    k_shard_gather<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, ws.colp.p, sh.g.grid.y, ws.maxp.p,
+    launch_k(k_shard_gather, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, ws.rowp.p, ws.nstrips, ws.colp.p, sh.g.grid.y, ws.maxp.p,
                                                           int64_t(sh.g.grid.x) * sh.g.grid.y, ws.pfmt, z, lu, P.rowshift(),
                                                           sh.lo, sh.hi,
                                                           sh.index, ws.nshards, ws.xsend.p + p * ws.xstride, gate);
@@ -313,7 +313,7 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.pfmt = so.pfmt;
   r.rowshift = so.rowshift;
   r.mode = scaled ? 1 : 0;
-  k_point_eval<<<ws.eval_blocks, kEvalThreads, 0, cx.stream>>>(ws.ctl.p, role, r, ws.ticket.p);
+  launch_k(k_point_eval, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p);
   PG_CK(cudaGetLastError());
 }
 

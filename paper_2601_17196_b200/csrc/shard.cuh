@@ -103,6 +103,7 @@ struct Comm {
 // recv[k] = op over p of send[p * stride + k] in shard order (SUM / NaN-max).
 __global__ void k_shard_reduce(const double* send, int nsend, int64_t stride, int64_t count, int op, double* recv,
                                const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count; k += int64_t(gridDim.x) * blockDim.x) {
     double a = send[k];
@@ -120,6 +121,7 @@ __global__ void k_shard_reduce(const double* send, int nsend, int64_t stride, in
 __global__ void k_shard_gather(const double* rowp, int64_t nstrips, const double* colp, int64_t nrb, const double* maxp,
                                int64_t nmax, int pfmt, Slot z, const double* lu, const double* rowshift, int64_t lo,
                                int64_t hi, int shard, int nshards, double* out, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int64_t n = z.n;
   const double w = *z.w();
@@ -152,6 +154,7 @@ __global__ void k_shard_gather(const double* rowp, int64_t nstrips, const double
 // A shard's per-column LSE pair (m, S) -> rescaled to the global max M:
 // S' = S e^(m - M) (in place).
 __global__ void k_shard_lse_rescale(double* send, int nsend, int64_t stride, int64_t n, const double* M, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
     const double Mk = M[k];
@@ -170,7 +173,7 @@ inline void shard_allreduce(const Comm& cm, cudaStream_t st, int num_sms, double
   const bool multi = cm.nccl != nullptr;
   if (cm.vshards > 1 || !multi) {
     const int blocks = int(std::min<int64_t>(num_sms * 4, std::max<int64_t>(1, ceil_div(count, kVecThreads))));
-    k_shard_reduce<<<blocks, kVecThreads, 0, st>>>(send, cm.vshards, stride, count, op, recv, gate);
+    launch_k(k_shard_reduce, dim3(blocks), dim3(kVecThreads), 0, st, send, cm.vshards, stride, count, op, recv, gate);
     PG_CK(cudaGetLastError());
     if (multi) nccl_check(nccl_api().AllReduce(recv, recv, size_t(count), NcclApi::kFloat64, op, cm.nccl, st), "ncclAllReduce");
   } else {

@@ -59,7 +59,7 @@ struct SinkhornSession : Session {
     const int64_t n = P.n;
     const SweepGrid& g = sh ? sh->g : ws.g;
     if (P.dtype == POTGPU_F64) {
-      sweep_rowlse_f64<<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.v, sh ? sh->lo : 0, sh ? sh->hi : n,
+      launch_k(sweep_rowlse_f64, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, n, sv.v, sh ? sh->lo : 0, sh ? sh->hi : n,
                                                            g.rows_per_cta, reinterpret_cast<double2*>(ws.rowp.p), gate);
     } else {
       launch_sweep(cx, P, ws, zv_slot(), nullptr, nullptr, gate, false, gamma, sh);  // rows of (0, v, 0)
@@ -72,15 +72,15 @@ struct SinkhornSession : Session {
     const SweepGrid& g = sh ? sh->g : ws.g;
     const int64_t lo = sh ? sh->lo : 0, hi = sh ? sh->hi : n;
     if (P.dtype == POTGPU_F64) {
-      sweep_collse_f64<<<g.grid, kThreads, 0, cx.stream>>>(P.L64.p, P.ld, n, sv.u, lo, hi, g.rows_per_cta,
+      launch_k(sweep_collse_f64, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, n, sv.u, lo, hi, g.rows_per_cta,
                                                            reinterpret_cast<double2*>(ws.colp.p), gate);
     } else if (P.kind == POTGPU_COST_DENSE) {
       SrcDenseF32 s{P.C32.p, P.ld, float(kLog2e / gamma)};
-      sweep_collse_f32<SrcDenseF32><<<g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, lo, hi, g.rows_per_cta,
+      launch_k(sweep_collse_f32<SrcDenseF32>, dim3(g.grid), dim3(kThreads), 0, cx.stream, s, n, sv.u, lo, hi, g.rows_per_cta,
                                                                         reinterpret_cast<float2*>(ws.colp.p), gate);
     } else {
       SrcPointsF32 s{P.XS4.p, P.YS4.p};
-      sweep_collse_f32<SrcPointsF32><<<g.grid, kThreads, 0, cx.stream>>>(s, n, sv.u, lo, hi, g.rows_per_cta,
+      launch_k(sweep_collse_f32<SrcPointsF32>, dim3(g.grid), dim3(kThreads), 0, cx.stream, s, n, sv.u, lo, hi, g.rows_per_cta,
                                                                          reinterpret_cast<float2*>(ws.colp.p), gate);
     }
   }
@@ -98,7 +98,7 @@ struct SinkhornSession : Session {
       for (size_t p = 0; p < ws.shards.size(); ++p) {
         const ShardGrid& sh = ws.shards[p];
         row_sweep(gate, &sh);
-        k_shard_gather_lse<true><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.rowp.p, ws.nstrips, fmt, n, sh.lo, sh.hi,
+        launch_k(k_shard_gather_lse<true>, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, ws.rowp.p, ws.nstrips, fmt, n, sh.lo, sh.hi,
                                                                         P.rowshift(), ws.xsend.p + p * ws.xstride, gate);
       }
       shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, 2 * n, NcclApi::kSum, ws.xrecv.p, gate);
@@ -106,8 +106,8 @@ struct SinkhornSession : Session {
       nstrips = 1;
       fmt = LP_F64;
     }
-    k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.v, 0, gate);
-    k_sk_rows<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, rowp, nstrips, fmt,
+    launch_k(k_sk_dummy, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.v, 0, gate);
+    launch_k(k_sk_rows, dim3(sk_blocks()), dim3(kSkThreads), 0, cx.stream, ctl.p, sv, rowp, nstrips, fmt,
                                                       cx.comm.sharded() ? nullptr : P.rowshift(), gate);
   }
 
@@ -118,7 +118,7 @@ struct SinkhornSession : Session {
   Slot zuv_slot() const { return Slot{zuv.p, P.n}; }
 
   void col_lse(int update, const int* gate) {  // at the current u
-    k_sk_dummy<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv.u, 1, gate);
+    launch_k(k_sk_dummy, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.u, 1, gate);
     if (fast_cols()) {
       col_pass(update, gate, true);
       col_pass(update, &ctl.p->col_flush, false);  // gated: only after a flush
@@ -140,28 +140,28 @@ struct SinkhornSession : Session {
         const ShardGrid& sh = ws.shards[p];
         if (fast) launch_sweep(cx, P, ws, zuv_slot(), nullptr, nullptr, gate, false, gamma, &sh);
         else col_sweep(gate, &sh);
-        k_shard_gather_lse<false><<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.colp.p, sh.g.grid.y, fmt, n, sh.lo, sh.hi,
+        launch_k(k_shard_gather_lse<false>, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, ws.colp.p, sh.g.grid.y, fmt, n, sh.lo, sh.hi,
                                                                          nullptr, ws.xsend.p + p * ws.xstride, gate);
       }
       shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p, ws.xstride, n, NcclApi::kMax, ws.xrecv.p, gate);
-      k_shard_lse_rescale<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ws.xsend.p, int(ws.shards.size()), ws.xstride, n,
+      launch_k(k_shard_lse_rescale, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, ws.xsend.p, int(ws.shards.size()), ws.xstride, n,
                                                                   ws.xrecv.p, gate);
       shard_allreduce(cx.comm, cx.stream, cx.num_sms, ws.xsend.p + n, ws.xstride, n, NcclApi::kSum, ws.xrecv.p + n, gate);
       colp = ws.xrecv.p;
       nrb = 1;
       fmt = LP_SPLIT;
     }
-    k_sk_cols<<<sk_blocks(), kSkThreads, 0, cx.stream>>>(ctl.p, sv, colp, nrb, fmt, update, sk_blocks(),
+    launch_k(k_sk_cols, dim3(sk_blocks()), dim3(kSkThreads), 0, cx.stream, ctl.p, sv, colp, nrb, fmt, update, sk_blocks(),
                                                       fast ? sv.zuv_v : nullptr, gate);
   }
 
   // solvers.hpp:463-476: u update, v update, B, E, ++iterations, record
   void enqueue_iteration() {
     const int* gate = &ctl.p->g_active;
-    k_sk_commit_u<<<ws.nblk, kVecThreads, 0, cx.stream>>>(ctl.p, sv);
+    launch_k(k_sk_commit_u, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, ctl.p, sv);
     col_lse(1, gate);
     row_lse(gate);
-    k_sk_scalars<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv, sk_blocks(), 0, ws.trace.p, gate);
+    launch_k(k_sk_scalars, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv, sk_blocks(), 0, ws.trace.p, gate);
     PG_CK(cudaGetLastError());
   }
 
@@ -252,7 +252,7 @@ struct SinkhornSession : Session {
     // B at u = v = 0 and E (solvers.hpp:441-442), record(0)
     row_lse(nullptr);
     col_lse(0, nullptr);
-    k_sk_scalars<<<1, kVecThreads, 0, cx.stream>>>(ctl.p, sv, sk_blocks(), 1, ws.trace.p, nullptr);
+    launch_k(k_sk_scalars, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv, sk_blocks(), 1, ws.trace.p, nullptr);
     PG_CK(cudaGetLastError());
     sync_ctl();
     if (cfg.record_rounded_cost) fill_last_record_cost(round_now(nullptr).cost);
@@ -278,7 +278,7 @@ struct SinkhornSession : Session {
   }
 
   void run_until(int64_t stop) {
-    k_sk_resume<<<1, 1, 0, cx.stream>>>(ctl.p, stop);
+    launch_k(k_sk_resume, dim3(1), dim3(1), 0, cx.stream, ctl.p, stop);
     launches += 1;
     int64_t burst = stop == INT64_MAX ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, stop - hctl->it);
     burst = std::min<int64_t>(burst, 1 << 16);

@@ -45,6 +45,7 @@ __device__ __forceinline__ void lse_merge(double& m, double& S, double m2, doubl
 __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __restrict__ L, int64_t ld, int64_t n,
                                                                const double* __restrict__ v, int64_t row_lo, int64_t row_hi, int rows_per_cta,
                                                                double2* rowp, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_rowlse_f64(const double* __
 __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f64(const double* __restrict__ L, int64_t ld, int64_t n,
                                                                const double* __restrict__ u, int64_t row_lo, int64_t row_hi, int rows_per_cta,
                                                                double2* colp, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
@@ -149,6 +151,7 @@ template <class Src>
 __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t n, const double* __restrict__ u,
                                                                int64_t row_lo, int64_t row_hi, int rows_per_cta,
                                                                float2* colp, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_collse_f32(Src src, int64_t
 template <bool ROWS>
 __global__ void k_shard_gather_lse(const double* p, int64_t cnt, int fmt, int64_t n, int64_t lo, int64_t hi,
                                    const double* rowshift, double* out, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double M = -INFINITY, S = 0.0;
@@ -285,6 +289,7 @@ struct SinkVec {  // device vectors of the extended problem (length n + 1)
 // log-sum-exp of x_k = (-0 + a_k) (k < n) and corner + a_n (the dummy
 // row/column of the extension), single block, two passes.
 __global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   __shared__ double sh[kVecThreads];
@@ -380,6 +385,7 @@ __device__ __forceinline__ void group_lse(const double* p, int64_t base, int64_t
 // exp(u_i + LSE_i); next u = log r - LSE.
 __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv, const double* rowp, int64_t nstrips,
                                                         int fmt, const double* rowshift, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double vn = sv.v[n];
@@ -415,6 +421,7 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_rows(SinkCtl* ctl, SinkVec sv
 constexpr double kColFlushRel = 5.421010862427522e-20;  // 2^-64
 __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv, const double* colp, int64_t nrb, int fmt,
                                                         int update, int nblk_rows, const double* vshift, const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   const double un = sv.u[n];
@@ -460,6 +467,7 @@ __global__ void __launch_bounds__(kSkThreads) k_sk_cols(SinkCtl* ctl, SinkVec sv
 }
 
 __global__ void k_sk_commit_u(SinkCtl* ctl, SinkVec sv) {
+  pdl_wait();
   if (!ctl->g_active) return;
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= ctl->n; i += int64_t(gridDim.x) * blockDim.x) {
     sv.u[i] = sv.u_next[i];
@@ -480,6 +488,7 @@ __device__ void sk_loop_head(SinkCtl* ctl) {  // solvers.hpp:458-462
 // value (:436-438), record rule (:445) and the loop head.
 __global__ void __launch_bounds__(kVecThreads) k_sk_scalars(SinkCtl* ctl, SinkVec sv, int nblk, int init, TraceDev* trace,
                                                             const int* gate) {
+  pdl_wait();
   if (gate && *gate == 0) return;
   double part[5] = {0, 0, 0, 0, 0};  // rerr, rsum, ur, cerr, vc
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
@@ -526,6 +535,7 @@ __global__ void __launch_bounds__(kVecThreads) k_sk_scalars(SinkCtl* ctl, SinkVe
 }
 
 __global__ void k_sk_resume(SinkCtl* ctl, int64_t pause_at) {
+  pdl_wait();
   ctl->pause_at = pause_at;
   if (!ctl->paused) return;
   ctl->paused = 0;

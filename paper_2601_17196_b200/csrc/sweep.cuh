@@ -46,6 +46,7 @@ struct SweepArgs {
 // sweeps. Padding columns of L hold -inf.
 template <bool FLOOR>
 __global__ void __launch_bounds__(kThreads, 2) sweep_f64_dense(const double* __restrict__ L, int64_t ld, SweepArgs a) {
+  pdl_wait();
   if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
@@ -232,6 +233,7 @@ __device__ __forceinline__ double partial_value(const double* p, int64_t idx, in
 
 template <class Src>
 __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
+  pdl_wait();
   if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
@@ -409,6 +411,7 @@ __host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta) {
 // warps to cover the per-row dependency chain (profiles/pts_variants.sh).
 template <int KP>
 __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(SrcPointsDotF32 src, SweepArgs a) {
+  pdl_wait();
   constexpr int kStrip = 64 * KP;
   if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -560,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(Src
 // flight). The column constants B'_j live in shared memory ([pair][lane]
 // float2, conflict-free) so the second row's exponents fit in registers.
 __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 src, SweepArgs a) {
+  pdl_wait();
   constexpr int KP = kPairs;
   constexpr int kStrip = 64 * KP;
   if (a.gate && *a.gate == 0) return;
