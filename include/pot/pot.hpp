@@ -378,4 +378,118 @@ inline Instance make_scaling_instance(long n, std::uint64_t seed) {  // syntheti
   return make_synthetic_instance(n, seed, 5.0, 3.0, 0.2);
 }
 
+
+// ------------------------------------------------- rounding.hpp / extend.hpp --
+// validate (core.hpp:131-169): the first violation's code.
+inline void validate(const Instance& in) {
+  const long n = in.size();
+  if (n == 0) throw PotError(ErrorCode::EmptyInput, "invalid instance: marginals are empty");
+  if (in.c.size() != n || in.C.rows() != n || in.C.cols() != n)
+    throw PotError(ErrorCode::DimensionMismatch, "invalid instance: shapes differ");
+  if (!in.r.allFinite() || !in.c.allFinite() || !in.C.allFinite() || !std::isfinite(in.s))
+    throw PotError(ErrorCode::NonFiniteEntry, "invalid instance: non-finite entry");
+  if (in.r.minCoeff() < 0 || in.c.minCoeff() < 0 || in.C.minCoeff() < 0 || in.s < 0)
+    throw PotError(ErrorCode::NegativeEntry, "invalid instance: negative entry");
+  if (in.s > std::min(in.r.sum(), in.c.sum()) + kBudgetSlack)
+    throw PotError(ErrorCode::BudgetExceedsMass, "invalid instance: budget exceeds min marginal mass");
+}
+
+// TransportPlan::from (core.hpp:185-197): mass and marginal slacks of X.
+inline TransportPlan plan_from(Matrix X, const Instance& in) {
+  TransportPlan p;
+  const Vector rs = X.rowSums(), cs = X.colSums();
+  p.row_slack = Vector(in.size());
+  p.col_slack = Vector(in.size());
+  for (long i = 0; i < in.size(); ++i) { p.row_slack(i) = in.r(i) - rs(i); p.col_slack(i) = in.c(i) - cs(i); }
+  p.mass = X.sum();
+  p.X = std::move(X);
+  return p;
+}
+
+namespace detail {
+inline std::vector<double> to_rows(const Matrix& m) {
+  std::vector<double> o(static_cast<size_t>(m.size()));
+  for (long i = 0; i < m.rows(); ++i)
+    for (long j = 0; j < m.cols(); ++j) o[size_t(i * m.cols() + j)] = m(i, j);
+  return o;
+}
+inline Matrix from_rows(const std::vector<double>& v, long rows, long cols) {
+  Matrix m(rows, cols);
+  for (long i = 0; i < rows; ++i)
+    for (long j = 0; j < cols; ++j) m(i, j) = v[size_t(i * cols + j)];
+  return m;
+}
+}  // namespace detail
+
+// round_pot (rounding.hpp:46-77) on the device.
+inline TransportPlan round_pot(const Matrix& X, const Instance& in) {
+  validate(in);
+  if (X.rows() != in.size() || X.cols() != in.size())
+    throw PotError(ErrorCode::DimensionMismatch, "plan shape does not match the instance");
+  const std::vector<double> xr = detail::to_rows(X);
+  std::vector<double> out(xr.size());
+  if (int rc = potgpu_round_pot(detail::context(), in.size(), xr.data(), in.r.data(), in.c.data(), in.s, out.data()))
+    detail::rethrow(rc);
+  return plan_from(detail::from_rows(out, X.rows(), X.cols()), in);
+}
+
+// round_balanced (rounding.hpp:14-39) on the device.
+inline Matrix round_balanced(const Matrix& X, const Vector& r, const Vector& c) {
+  if (X.rows() != r.size() || X.cols() != c.size()) throw PotError(ErrorCode::DimensionMismatch, "plan/marginal shape mismatch");
+  const std::vector<double> xr = detail::to_rows(X);
+  std::vector<double> out(xr.size());
+  if (int rc = potgpu_round_balanced(detail::context(), X.rows(), X.cols(), xr.data(), r.data(), c.data(), out.data()))
+    detail::rethrow(rc);
+  return detail::from_rows(out, X.rows(), X.cols());
+}
+
+struct ExtendedOtInstance {  // extend.hpp:11-18
+  Matrix C_ext;
+  Vector r_ext;
+  Vector c_ext;
+  double penalty_A = 0.0;
+  long original_size() const { return r_ext.size() - 1; }
+};
+
+inline ExtendedOtInstance extend(const Instance& in, double penalty_A) {  // extend.hpp:22-39
+  validate(in);
+  if (!(penalty_A > in.max_cost()))
+    throw PotError(ErrorCode::PenaltyTooSmall, "penalty must exceed max cost " + std::to_string(in.max_cost()));
+  const long n = in.size();
+  ExtendedOtInstance ext;
+  ext.penalty_A = penalty_A;
+  ext.C_ext = Matrix::Zero(n + 1, n + 1);
+  for (long j = 0; j < n; ++j)
+    for (long i = 0; i < n; ++i) ext.C_ext(i, j) = in.C(i, j);
+  ext.C_ext(n, n) = penalty_A;
+  ext.r_ext = Vector(n + 1);
+  ext.c_ext = Vector(n + 1);
+  for (long i = 0; i < n; ++i) { ext.r_ext(i) = in.r(i); ext.c_ext(i) = in.c(i); }
+  ext.r_ext(n) = std::max(in.c.sum() - in.s, 0.0);
+  ext.c_ext(n) = std::max(in.r.sum() - in.s, 0.0);
+  return ext;
+}
+
+struct BlockDecomposition {  // extend.hpp:41-46
+  Matrix block;
+  Vector dummy_col;
+  Vector dummy_row;
+  double corner = 0.0;
+};
+
+inline BlockDecomposition extract_block(const Matrix& X_ext) {  // extend.hpp:48-60
+  if (X_ext.rows() != X_ext.cols() || X_ext.rows() < 2)
+    throw PotError(ErrorCode::DimensionMismatch, "extended plan must be square with side >= 2");
+  const long n = X_ext.rows() - 1;
+  BlockDecomposition out;
+  out.block = Matrix(n, n);
+  out.dummy_col = Vector(n);
+  out.dummy_row = Vector(n);
+  for (long j = 0; j < n; ++j)
+    for (long i = 0; i < n; ++i) out.block(i, j) = X_ext(i, j);
+  for (long i = 0; i < n; ++i) { out.dummy_col(i) = X_ext(i, n); out.dummy_row(i) = X_ext(n, i); }
+  out.corner = X_ext(n, n);
+  return out;
+}
+
 }  // namespace pot

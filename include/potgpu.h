@@ -226,9 +226,14 @@ void* potgpu_ctx_stream(potgpu_ctx* ctx);
 int potgpu_dual_eval(potgpu_ctx* ctx, const potgpu_problem* problem, double gamma, const double* u, const double* v,
                      double w, double* row, double* col, double* scalars);
 
-/* round_pot (rounding.hpp:46-77) on the device for a dense row-major X. */
+/* round_pot (rounding.hpp:46-77) on the device for a dense row-major n x n
+ * plan X (r, c, s validated as by validate(), core.hpp:131-169). */
 int potgpu_round_pot(potgpu_ctx* ctx, int64_t n, const double* X, const double* r, const double* c, double s,
                      double* X_out);
+/* round_balanced (rounding.hpp:14-39) on a dense row-major rows x cols plan;
+ * POTGPU_UNBALANCED_MARGINALS when |r|_1 != |c|_1. */
+int potgpu_round_balanced(potgpu_ctx* ctx, int64_t rows, int64_t cols, const double* X, const double* r,
+                          const double* c, double* X_out);
 
 /* Multi-GPU row-block sharding (no reference counterpart —
  * the reference is single-threaded). One process per GPU: rank 0 creates the

@@ -161,3 +161,35 @@ def kmeans(points, k, seed):
     if rc:
         raise OracleError(rc - 1, err.value.decode())
     return C[:k], W[:k], A[:n], rounds.value
+
+
+def round_pot(X, C, r, c, s):
+    """round_pot (rounding.hpp:46-77) in the oracle; returns (X_out, cost, gap, mass)."""
+    L = lib()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n = X.shape[0]
+    C = np.ascontiguousarray(C if C is not None else np.zeros((n, n)), dtype=np.float64)
+    out, cgm = np.empty_like(X), np.zeros(3)
+    err = ctypes.create_string_buffer(256)
+    fn = L.oracle_round_pot
+    fn.argtypes = [ctypes.c_long] + [ctypes.POINTER(ctypes.c_double)] * 4 + [ctypes.c_double] + \
+        [ctypes.POINTER(ctypes.c_double)] * 2 + [ctypes.c_char_p, ctypes.c_int]
+    rc = fn(n, _dp(X), _dp(C), _dp(np.ascontiguousarray(r, dtype=np.float64)),
+            _dp(np.ascontiguousarray(c, dtype=np.float64)), float(s), _dp(out), _dp(cgm), err, 256)
+    if rc:
+        raise OracleError(rc - 1, err.value.decode())
+    return out
+
+
+def round_balanced(X, r, c):
+    L = lib()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    out = np.empty_like(X)
+    err = ctypes.create_string_buffer(256)
+    fn = L.oracle_round_balanced
+    fn.argtypes = [ctypes.c_long, ctypes.c_long] + [ctypes.POINTER(ctypes.c_double)] * 4 + [ctypes.c_char_p, ctypes.c_int]
+    rc = fn(X.shape[0], X.shape[1], _dp(X), _dp(np.ascontiguousarray(r, dtype=np.float64)),
+            _dp(np.ascontiguousarray(c, dtype=np.float64)), _dp(out), err, 256)
+    if rc:
+        raise OracleError(rc - 1, err.value.decode())
+    return out

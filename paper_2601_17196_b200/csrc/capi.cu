@@ -694,6 +694,7 @@ struct AspotSession : Session {
 #include "sinkhorn.cuh"
 #include "registration.cuh"
 #include "kmeans.cuh"
+#include "dense_round.cuh"
 
 namespace potgpu {
 }  // namespace potgpu
@@ -1194,9 +1195,40 @@ int potgpu_fit_rigid(potgpu_ctx* c, const double* pi, int64_t m, int64_t n, cons
   });
 }
 
-int potgpu_round_pot(potgpu_ctx*, int64_t, const double*, const double*, const double*, double, double*) {
-  g_last_error = "potgpu_round_pot on a dense user plan is not implemented yet";
-  return POTGPU_ERR_UNSUPPORTED;
+static void check_marginals(int64_t n, const double* r, const double* c, double s) {  // validate (core.hpp:131-169) on r, c, s
+  if (n <= 0) throw Error(POTGPU_EMPTY_INPUT, "invalid instance: marginals are empty");
+  if (!r || !c) throw Error(POTGPU_INVALID_ARGUMENT, "null marginals");
+  bool finite = std::isfinite(s), neg = s < 0;
+  for (int64_t i = 0; i < n; ++i) {
+    finite = finite && std::isfinite(r[i]) && std::isfinite(c[i]);
+    neg = neg || r[i] < 0 || c[i] < 0;
+  }
+  if (!finite) throw Error(POTGPU_NON_FINITE_ENTRY, "invalid instance: non-finite entry in r, c or s");
+  if (neg) throw Error(POTGPU_NEGATIVE_ENTRY, "invalid instance: negative entry");
+  if (s > std::min(ksum(r, n), ksum(c, n)) + 1e-12)
+    throw Error(POTGPU_BUDGET_EXCEEDS_MASS, "invalid instance: budget exceeds min marginal mass");
+}
+
+// round_pot (rounding.hpp:46-77) on a dense row-major plan.
+int potgpu_round_pot(potgpu_ctx* c, int64_t n, const double* X, const double* r, const double* cm, double s,
+                     double* X_out) {
+  return guarded([&] {
+    if (!c || !X || !X_out) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    check_marginals(n, r, cm, s);
+    PG_CK(cudaSetDevice(c->cx.device));
+    round_pot_dense(c->cx, n, X, HVec(r, r + n), HVec(cm, cm + n), s, X_out);
+  });
+}
+
+// round_balanced (rounding.hpp:14-39) on a dense row-major rows x cols plan.
+int potgpu_round_balanced(potgpu_ctx* c, int64_t rows, int64_t cols, const double* X, const double* r, const double* cm,
+                          double* X_out) {
+  return guarded([&] {
+    if (!c || !X || !X_out || !r || !cm) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    if (rows <= 0 || cols <= 0) throw Error(POTGPU_DIMENSION_MISMATCH, "plan/marginal shape mismatch");
+    PG_CK(cudaSetDevice(c->cx.device));
+    round_balanced_dense(c->cx, rows, cols, X, HVec(r, r + rows), HVec(cm, cm + cols), X_out);
+  });
 }
 
 }  // extern "C"

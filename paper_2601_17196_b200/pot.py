@@ -162,7 +162,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
-    "potgpu_kmeans_quantize",
+    "potgpu_kmeans_quantize", "potgpu_round_balanced",
 )
 
 _lib = None
@@ -202,6 +202,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_fit_rigid.argtypes = [ctypes.c_void_p, dp, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]
     lib.potgpu_kmeans_quantize.argtypes = [ctypes.c_void_p, dp, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, dp, dp,
                                            P(ctypes.c_int32)]
+    lib.potgpu_round_pot.argtypes = [ctypes.c_void_p, ctypes.c_int64, dp, dp, dp, ctypes.c_double, dp]
+    lib.potgpu_round_balanced.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]
     lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
     lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -883,3 +885,75 @@ def recolor_points(assignments, recolored) -> np.ndarray:
     rounded to 8 bits."""
     vals = np.clip(np.asarray(recolored)[np.asarray(assignments)], 0.0, 1.0)
     return np.floor(vals * 255.0 + 0.5).astype(np.uint8)
+
+
+# ------------------------------------------------------------- rounding / extend --
+def round_pot(X, inst: Instance, ctx: Optional[Context] = None) -> TransportPlan:
+    """round_pot (rounding.hpp:46-77) on the device: X projected onto U(r, c, s)."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n = inst.size()
+    if X.shape != (n, n):
+        raise PotError(ErrorCode.DimensionMismatch, "plan shape does not match the instance")
+    r = np.ascontiguousarray(inst.r, dtype=np.float64)
+    c = np.ascontiguousarray(inst.c, dtype=np.float64)
+    out = np.empty_like(X)
+    _check(lib.potgpu_round_pot(ctx._h, n, _dp(X), _dp(r), _dp(c), float(inst.s), _dp(out)))
+    return TransportPlan(X=out, row_slack=r - out.sum(axis=1), col_slack=c - out.sum(axis=0), mass=float(out.sum()))
+
+
+def round_balanced(X, r, c, ctx: Optional[Context] = None) -> np.ndarray:
+    """round_balanced (rounding.hpp:14-39) on the device."""
+    lib = load_library()
+    ctx = ctx or default_context()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    if X.shape != (r.size, c.size):
+        raise PotError(ErrorCode.DimensionMismatch, "plan/marginal shape mismatch")
+    out = np.empty_like(X)
+    _check(lib.potgpu_round_balanced(ctx._h, X.shape[0], X.shape[1], _dp(X), _dp(r), _dp(c), _dp(out)))
+    return out
+
+
+@dataclass
+class ExtendedOtInstance:  # extend.hpp:11-18
+    C_ext: np.ndarray
+    r_ext: np.ndarray
+    c_ext: np.ndarray
+    penalty_A: float
+
+    def original_size(self) -> int:
+        return self.r_ext.size - 1
+
+
+def extend(inst: Instance, penalty_A: float) -> ExtendedOtInstance:
+    """extend (extend.hpp:22-39): the balanced dummy-node extension."""
+    C = inst.C if inst.C is not None else dense_cost(inst.X, inst.Y, inst.cost_scale)
+    if not penalty_A > C.max():
+        raise PotError(ErrorCode.PenaltyTooSmall, f"penalty must exceed max cost {C.max()}")
+    n = inst.size()
+    Ce = np.zeros((n + 1, n + 1))
+    Ce[:n, :n] = C
+    Ce[n, n] = penalty_A
+    r_ext = np.append(inst.r, max(inst.c.sum() - inst.s, 0.0))
+    c_ext = np.append(inst.c, max(inst.r.sum() - inst.s, 0.0))
+    return ExtendedOtInstance(Ce, r_ext, c_ext, float(penalty_A))
+
+
+@dataclass
+class BlockDecomposition:  # extend.hpp:41-46
+    block: np.ndarray
+    dummy_col: np.ndarray
+    dummy_row: np.ndarray
+    corner: float
+
+
+def extract_block(X_ext) -> BlockDecomposition:
+    """extract_block (extend.hpp:48-60)."""
+    X_ext = np.asarray(X_ext, dtype=np.float64)
+    if X_ext.ndim != 2 or X_ext.shape[0] != X_ext.shape[1] or X_ext.shape[0] < 2:
+        raise PotError(ErrorCode.DimensionMismatch, "extended plan must be square with side >= 2")
+    n = X_ext.shape[0] - 1
+    return BlockDecomposition(X_ext[:n, :n].copy(), X_ext[:n, n].copy(), X_ext[n, :n].copy(), float(X_ext[n, n]))
