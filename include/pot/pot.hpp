@@ -153,6 +153,13 @@ enum class BlockRule { Greedy, RoundRobin };
 enum class SolverKind { Aspot, FeasibleSinkhorn, TunedSinkhorn };
 enum class SolveStatus { Converged, MaxIterationsExceeded, StepSizeUnderflow };
 
+inline std::optional<SolverKind> solver_kind_from_name(const std::string& name) {  // core.hpp:234-239
+  if (name == "aspot") return SolverKind::Aspot;
+  if (name == "sinkhorn") return SolverKind::FeasibleSinkhorn;
+  if (name == "tuned-sinkhorn") return SolverKind::TunedSinkhorn;
+  return std::nullopt;
+}
+
 inline const char* solver_kind_name(SolverKind k) {
   switch (k) {
     case SolverKind::Aspot: return "aspot";
@@ -271,7 +278,10 @@ inline potgpu_config to_cconfig(const SolverConfig& config, double epsilon, doub
   return cfg;
 }
 
-inline SolveResult run(int kind, const Instance& in, const SolverConfig& config, double epsilon, double p) {
+// step_cb (optional): the solve runs through the session C-ABI one accepted
+// iteration at a time and step_cb(session) is called after each one.
+inline SolveResult run(int kind, const Instance& in, const SolverConfig& config, double epsilon, double p,
+                       const std::function<void(potgpu_session*)>& step_cb = {}) {
   config.check();
   const long n = in.size();
   potgpu_problem pr{};
@@ -301,7 +311,22 @@ inline SolveResult run(int kind, const Instance& in, const SolverConfig& config,
   out.trace = trace.data();
   out.trace_cap = cap;
   potgpu_summary sm{};
-  if (int rc = potgpu_solve(context(), kind, &pr, &cfg, &sm, &out)) rethrow(rc);
+  if (!step_cb) {
+    if (int rc = potgpu_solve(context(), kind, &pr, &cfg, &sm, &out)) rethrow(rc);
+  } else {
+    potgpu_session* ses = nullptr;
+    if (int rc = potgpu_session_begin(context(), kind, &pr, &cfg, cap, 0, &ses)) rethrow(rc);
+    struct Guard { potgpu_session* s; ~Guard() { potgpu_session_destroy(s); } } guard{ses};
+    while (true) {
+      double ms = 0.0;
+      int64_t it = 0;
+      int fin = 0;
+      if (int rc = potgpu_session_iterate(ses, 1, &ms, &it, &fin)) rethrow(rc);
+      if (it > 0) step_cb(ses);
+      if (fin) break;
+    }
+    if (int rc = potgpu_session_finish(ses, &sm, &out)) rethrow(rc);
+  }
   for (long i = 0; i < n; ++i)
     for (long j = 0; j < n; ++j) res.plan.X(i, j) = Xrm[size_t(i * n + j)];
   res.plan.mass = sm.mass;
@@ -327,9 +352,7 @@ inline SolveResult run(int kind, const Instance& in, const SolverConfig& config,
 
 }  // namespace detail
 
-// The AspotObserver hook of the reference (solvers.hpp:188-204) is not
-// offered: the loop is device resident. iterate-by-iterate access to the
-// dual points is the potgpu_session_* C-ABI.
+// The AspotObserver overload is below (after the dual types).
 inline SolveResult aspot_solve(const Instance& in, const SolverConfig& config) {  // solvers.hpp:265
   return detail::run(POTGPU_ASPOT, in, config, config.epsilon, config.tuning_exponent_p);
 }
@@ -380,18 +403,64 @@ inline Instance make_scaling_instance(long n, std::uint64_t seed) {  // syntheti
 
 
 // ------------------------------------------------- rounding.hpp / extend.hpp --
-// validate (core.hpp:131-169): the first violation's code.
-inline void validate(const Instance& in) {
-  const long n = in.size();
-  if (n == 0) throw PotError(ErrorCode::EmptyInput, "invalid instance: marginals are empty");
-  if (in.c.size() != n || in.C.rows() != n || in.C.cols() != n)
-    throw PotError(ErrorCode::DimensionMismatch, "invalid instance: shapes differ");
-  if (!in.r.allFinite() || !in.c.allFinite() || !in.C.allFinite() || !std::isfinite(in.s))
-    throw PotError(ErrorCode::NonFiniteEntry, "invalid instance: non-finite entry");
-  if (in.r.minCoeff() < 0 || in.c.minCoeff() < 0 || in.C.minCoeff() < 0 || in.s < 0)
-    throw PotError(ErrorCode::NegativeEntry, "invalid instance: negative entry");
-  if (in.s > std::min(in.r.sum(), in.c.sum()) + kBudgetSlack)
-    throw PotError(ErrorCode::BudgetExceedsMass, "invalid instance: budget exceeds min marginal mass");
+struct Violation {  // core.hpp:76-79
+  ErrorCode code;
+  std::string detail;
+};
+
+// Thrown by validate(); carries every violated invariant (core.hpp:82-104).
+class ValidationError : public PotError {
+ public:
+  explicit ValidationError(std::vector<Violation> violations)
+      : PotError(violations.empty() ? ErrorCode::InvalidArgument : violations.front().code, describe(violations)),
+        violations_(std::move(violations)) {}
+  const std::vector<Violation>& violations() const { return violations_; }
+
+ private:
+  static std::string describe(const std::vector<Violation>& vs) {
+    std::string msg = "invalid instance";
+    for (const auto& v : vs) {
+      msg += "; ";
+      msg += error_code_name(v.code);
+      msg += " (" + v.detail + ")";
+    }
+    return msg;
+  }
+  std::vector<Violation> violations_;
+};
+
+inline std::vector<Violation> validation_report(const Instance& in) {  // core.hpp:131-162
+  std::vector<Violation> out;
+  const long n = in.r.size();
+  if (n == 0) {
+    out.push_back({ErrorCode::EmptyInput, "marginals are empty"});
+    return out;
+  }
+  if (in.c.size() != n)
+    out.push_back({ErrorCode::DimensionMismatch, "r has " + std::to_string(n) + " entries, c has " + std::to_string(in.c.size())});
+  if (in.C.rows() != n || in.C.cols() != n)
+    out.push_back({ErrorCode::DimensionMismatch, "cost matrix is " + std::to_string(in.C.rows()) + "x" +
+                                                     std::to_string(in.C.cols()) + ", expected " + std::to_string(n) + "x" +
+                                                     std::to_string(n)});
+  if (!in.r.allFinite() || !in.c.allFinite() || !in.C.allFinite() || !std::isfinite(in.s)) {
+    out.push_back({ErrorCode::NonFiniteEntry, "non-finite entry in r, c, C or s"});
+  } else {
+    if ((in.r.size() && in.r.minCoeff() < 0) || (in.c.size() && in.c.minCoeff() < 0))
+      out.push_back({ErrorCode::NegativeEntry, "negative marginal entry"});
+    if (in.C.size() > 0 && in.C.minCoeff() < 0) out.push_back({ErrorCode::NegativeEntry, "negative cost entry"});
+    if (in.s < 0) out.push_back({ErrorCode::NegativeEntry, "negative budget"});
+    if (in.c.size() == n && in.s > std::min(in.r.sum(), in.c.sum()) + kBudgetSlack)
+      out.push_back({ErrorCode::BudgetExceedsMass, "budget " + std::to_string(in.s) + " exceeds min marginal mass " +
+                                                       std::to_string(std::min(in.r.sum(), in.c.sum()))});
+  }
+  return out;
+}
+
+// Returns the instance unchanged when every invariant holds (core.hpp:164-169).
+inline const Instance& validate(const Instance& in) {
+  auto violations = validation_report(in);
+  if (!violations.empty()) throw ValidationError(std::move(violations));
+  return in;
 }
 
 // TransportPlan::from (core.hpp:185-197): mass and marginal slacks of X.
@@ -490,6 +559,272 @@ inline BlockDecomposition extract_block(const Matrix& X_ext) {  // extend.hpp:48
   for (long i = 0; i < n; ++i) { out.dummy_col(i) = X_ext(i, n); out.dummy_row(i) = X_ext(n, i); }
   out.corner = X_ext(n, n);
   return out;
+}
+
+
+// ---------------------------------------------------------------- dual.hpp --
+struct DualPoint {  // dual.hpp:15-31
+  Vector u;
+  Vector v;
+  double w = 0.0;
+  static DualPoint zero(long n) { return DualPoint{Vector::Zero(n), Vector::Zero(n), 0.0}; }
+  bool all_finite() const { return u.allFinite() && v.allFinite() && std::isfinite(w); }
+};
+
+inline DualPoint operator*(double a, const DualPoint& z) {  // dual.hpp:33-43
+  DualPoint o{Vector(z.u.size()), Vector(z.v.size()), a * z.w};
+  for (long i = 0; i < z.u.size(); ++i) o.u(i) = a * z.u(i);
+  for (long i = 0; i < z.v.size(); ++i) o.v(i) = a * z.v(i);
+  return o;
+}
+inline DualPoint operator+(const DualPoint& a, const DualPoint& b) {
+  DualPoint o{Vector(a.u.size()), Vector(a.v.size()), a.w + b.w};
+  for (long i = 0; i < a.u.size(); ++i) o.u(i) = a.u(i) + b.u(i);
+  for (long i = 0; i < a.v.size(); ++i) o.v(i) = a.v(i) + b.v(i);
+  return o;
+}
+inline DualPoint operator-(const DualPoint& a, const DualPoint& b) {
+  DualPoint o{Vector(a.u.size()), Vector(a.v.size()), a.w - b.w};
+  for (long i = 0; i < a.u.size(); ++i) o.u(i) = a.u(i) - b.u(i);
+  for (long i = 0; i < a.v.size(); ++i) o.v(i) = a.v(i) - b.v(i);
+  return o;
+}
+
+inline constexpr double kMaxExponent = 700.0;  // dual.hpp:47
+
+// dual.hpp:52-75. logK is materialised on the host like the reference's
+// member; the reductions run on the device from C.
+struct EntropicContext {
+  double gamma = 0.0;
+  Matrix logK;
+  Vector r;
+  Vector c;
+  double s = 0.0;
+  Matrix C;  // kept for the device evaluations
+  EntropicContext(const Matrix& C_, double gamma_, Vector r_, Vector c_, double s_)
+      : gamma(gamma_), r(std::move(r_)), c(std::move(c_)), s(s_), C(C_) {
+    if (!(gamma > 0) || !std::isfinite(gamma)) throw PotError(ErrorCode::InvalidArgument, "gamma must be positive");
+    if (C.rows() != r.size() || C.cols() != c.size())
+      throw PotError(ErrorCode::DimensionMismatch, "cost/marginal shape mismatch");
+    logK = Matrix(C.rows(), C.cols());
+    for (long k = 0; k < C.size(); ++k) logK.data()[k] = -C.data()[k] / gamma;
+  }
+  static EntropicContext from_instance(const Instance& in, double gamma) {
+    return EntropicContext(in.C, gamma, in.r, in.c, in.s);
+  }
+  long size() const { return r.size(); }
+};
+
+namespace detail {
+inline void check_dual_shape(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:79-83
+  if (z.u.size() != ctx.size() || z.v.size() != ctx.size())
+    throw PotError(ErrorCode::DimensionMismatch, "dual point shape mismatch");
+}
+inline void check_exp_range(double max_exponent, const char* what) {  // dual.hpp:85-90
+  if (!(max_exponent <= kMaxExponent))
+    throw PotError(ErrorCode::Overflow, std::string(what) + " exponent exceeds representable range");
+}
+inline double eexp(double x) {  // Eigen's packet exp (clamped argument)
+  if (std::isnan(x) || x == std::numeric_limits<double>::infinity()) return std::exp(x);
+  return std::exp(std::min(std::max(x, -709.784), 709.784));
+}
+inline potgpu_problem dense_problem(const EntropicContext& ctx) {
+  potgpu_problem pr{};
+  pr.n = ctx.size();
+  pr.dtype = POTGPU_F64;
+  pr.cost_kind = POTGPU_COST_DENSE;
+  pr.C = ctx.C.data();
+  pr.ldc = ctx.C.rows();
+  pr.row_major = 0;
+  pr.r = ctx.r.data();
+  pr.c = ctx.c.data();
+  pr.s = ctx.s;
+  return pr;
+}
+inline double max_of(const Vector& x) {
+  double m = -std::numeric_limits<double>::infinity();
+  for (long i = 0; i < x.size(); ++i) { if (std::isnan(x(i))) return x(i); m = std::max(m, x(i)); }
+  return m;
+}
+// B 1, B^T 1, B.sum() at z on the device (potgpu_dual_eval).
+struct BSums { Vector row, col; double total = 0.0; };
+inline BSums b_sums(const EntropicContext& ctx, const DualPoint& z) {
+  const potgpu_problem pr = dense_problem(ctx);
+  BSums b{Vector(ctx.size()), Vector(ctx.size()), 0.0};
+  double sc[6];
+  if (int rc = potgpu_dual_eval(context(), &pr, ctx.gamma, z.u.data(), z.v.data(), z.w, b.row.data(), b.col.data(), sc))
+    rethrow(rc);
+  b.total = sc[0];
+  return b;
+}
+inline Matrix dual_matrix(const EntropicContext& ctx, const DualPoint& z, int which) {
+  const potgpu_problem pr = dense_problem(ctx);
+  const long n = ctx.size();
+  std::vector<double> o(static_cast<size_t>(n * n));
+  if (int rc = potgpu_dual_matrix(context(), &pr, ctx.gamma, z.u.data(), z.v.data(), z.w, which, o.data())) rethrow(rc);
+  return from_rows(o, n, n);
+}
+inline Matrix exponent_matrix(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:92-99
+  check_dual_shape(ctx, z);
+  return dual_matrix(ctx, z, 0);
+}
+inline double rho_limit(double a, double b);
+}  // namespace detail
+
+inline Matrix b_matrix(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:103-109
+  detail::check_dual_shape(ctx, z);
+  return detail::dual_matrix(ctx, z, 1);
+}
+
+inline DualPoint dual_gradient(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:122-133
+  detail::check_dual_shape(ctx, z);
+  detail::check_exp_range(detail::max_of(z.u), "exp(u)");
+  detail::check_exp_range(detail::max_of(z.v), "exp(v)");
+  const detail::BSums b = detail::b_sums(ctx, z);
+  DualPoint g{Vector(ctx.size()), Vector(ctx.size()), b.total - ctx.s};
+  for (long i = 0; i < ctx.size(); ++i) {
+    g.u(i) = (b.row(i) + detail::eexp(z.u(i))) - ctx.r(i);
+    g.v(i) = (b.col(i) + detail::eexp(z.v(i))) - ctx.c(i);
+  }
+  return g;
+}
+
+inline double dual_objective(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:111-120
+  detail::check_dual_shape(ctx, z);
+  detail::check_exp_range(detail::max_of(z.u), "exp(u)");
+  detail::check_exp_range(detail::max_of(z.v), "exp(v)");
+  const detail::BSums b = detail::b_sums(ctx, z);
+  double eu = 0.0, ev = 0.0, ur = 0.0, vc = 0.0;
+  for (long i = 0; i < ctx.size(); ++i) {
+    eu += detail::eexp(z.u(i));
+    ev += detail::eexp(z.v(i));
+    ur += z.u(i) * ctx.r(i);
+    vc += z.v(i) * ctx.c(i);
+  }
+  return ((((b.total + eu) + ev) - ur) - vc) - z.w * ctx.s;
+}
+
+inline double feasibility_error(const EntropicContext& ctx, const DualPoint& z) {  // dual.hpp:135-139
+  const DualPoint g = dual_gradient(ctx, z);
+  double e = 0.0;
+  for (long i = 0; i < g.u.size(); ++i) e += std::fabs(g.u(i));
+  for (long i = 0; i < g.v.size(); ++i) e += std::fabs(g.v(i));
+  return e + std::fabs(g.w);
+}
+
+namespace detail {
+inline double rho_limit(double a, double b) {  // dual.hpp:150-158
+  if (!(a > 0)) return b;
+  if (!(b > 0)) return std::numeric_limits<double>::infinity();
+  return rho(a, b);
+}
+}  // namespace detail
+
+// greenkhorn_step (solvers.hpp:43-89): the sums on the device, the block
+// choice and update on the host in the reference's order.
+inline DualPoint greenkhorn_step(const EntropicContext& ctx, const DualPoint& z, BlockRule rule, long t) {
+  detail::check_dual_shape(ctx, z);
+  detail::check_exp_range(detail::max_of(z.u), "exp(u)");
+  detail::check_exp_range(detail::max_of(z.v), "exp(v)");
+  const detail::BSums b = detail::b_sums(ctx, z);
+  const long n = ctx.size();
+  Vector row(n), col(n);
+  for (long i = 0; i < n; ++i) {
+    row(i) = b.row(i) + detail::eexp(z.u(i));
+    col(i) = b.col(i) + detail::eexp(z.v(i));
+  }
+  int block = 0;
+  if (rule == BlockRule::RoundRobin) {
+    block = int(t % 3);
+  } else {
+    double su = 0.0, sv = 0.0;
+    for (long i = 0; i < n; ++i) {
+      su += detail::rho_limit(ctx.r(i), row(i));
+      sv += detail::rho_limit(ctx.c(i), col(i));
+    }
+    const double sw = detail::rho_limit(ctx.s, b.total);
+    double best = su;
+    if (sv > best) { block = 1; best = sv; }
+    if (sw > best) block = 2;
+  }
+  DualPoint out = z;
+  if (block == 0) for (long i = 0; i < n; ++i) out.u(i) += std::log(ctx.r(i)) - std::log(row(i));
+  else if (block == 1) for (long i = 0; i < n; ++i) out.v(i) += std::log(ctx.c(i)) - std::log(col(i));
+  else out.w += std::log(ctx.s) - std::log(b.total);
+  if (!out.all_finite()) throw PotError(ErrorCode::Overflow, "block update left the exp range");
+  return out;
+}
+
+struct AspotSetup {  // solvers.hpp:94-99
+  double gamma = 0.0;
+  double eps_tilde = 0.0;
+  Vector mixed_r;
+  Vector mixed_c;
+};
+
+inline AspotSetup aspot_setup(const Instance& in, double epsilon) {  // solvers.hpp:100-133
+  validate(in);
+  if (!(epsilon > 0) || !std::isfinite(epsilon)) throw PotError(ErrorCode::InvalidArgument, "epsilon must be positive");
+  const long n = in.size();
+  if (n < 2) throw PotError(ErrorCode::DegenerateInstance, "accelerated setup needs n >= 2 (log n vanishes)");
+  AspotSetup st;
+  st.gamma = epsilon / (4.0 * std::log(double(n)));
+  const double cmax = in.max_cost();
+  st.eps_tilde = cmax > 0 ? epsilon / (8.0 * cmax) : std::numeric_limits<double>::infinity();
+  const double sr = in.r.sum(), sc = in.c.sum();
+  if (sr > 1) st.eps_tilde = std::min(st.eps_tilde, 8.0 * (sr - in.s) / (sr - 1.0));
+  if (sc > 1) st.eps_tilde = std::min(st.eps_tilde, 8.0 * (sc - in.s) / (sc - 1.0));
+  if (!(st.gamma > 0) || !std::isfinite(st.gamma)) throw PotError(ErrorCode::DegenerateInstance, "derived gamma is not positive");
+  if (!(st.eps_tilde > 0))
+    throw PotError(ErrorCode::DegenerateInstance, "stopping tolerance collapsed to zero (budget equals mass)");
+  const double lambda = std::min(st.eps_tilde / 8.0, 0.5);
+  st.mixed_r = Vector(n);
+  st.mixed_c = Vector(n);
+  for (long i = 0; i < n; ++i) {
+    st.mixed_r(i) = (1.0 - lambda) * in.r(i) + lambda / double(n);
+    st.mixed_c(i) = (1.0 - lambda) * in.c(i) + lambda / double(n);
+  }
+  return st;
+}
+
+// Per-iteration snapshot of the accelerated solver (solvers.hpp:188-202);
+// references valid only inside the callback.
+struct AspotIterate {
+  long t = 0;
+  double theta = 0.0;
+  double error = 0.0;
+  const EntropicContext& ctx;
+  const DualPoint& z_grave;
+  const DualPoint& z_hat;
+  const DualPoint& z_best;
+  const DualPoint& z_check;
+  double phi_hat = 0.0;
+  double phi_best = 0.0;
+  double phi_check = 0.0;
+};
+
+using AspotObserver = std::function<void(const AspotIterate&)>;
+
+// aspot_solve with an observer (solvers.hpp:265-266, 364-367): the device
+// loop advances one accepted iteration at a time and the four points are
+// copied to the host for the callback (a diagnostic slow path).
+inline SolveResult aspot_solve(const Instance& in, const SolverConfig& config, const AspotObserver& observer) {
+  if (!observer) return aspot_solve(in, config);
+  config.check();
+  validate(in);
+  if (in.s == 0 || in.size() < 2) return aspot_solve(in, config);  // trivial / degenerate: no iterations
+  const AspotSetup st = aspot_setup(in, config.epsilon);
+  const EntropicContext ectx(in.C, config.gamma_override.value_or(st.gamma), st.mixed_r, st.mixed_c, in.s);
+  const long n = in.size();
+  return detail::run(POTGPU_ASPOT, in, config, config.epsilon, config.tuning_exponent_p, [&](potgpu_session* ses) {
+    DualPoint pts[4];
+    double sc[6];
+    for (int k = 0; k < 4; ++k) {
+      pts[k] = DualPoint{Vector(n), Vector(n), 0.0};
+      if (int rc = potgpu_session_read_state(ses, k, pts[k].u.data(), pts[k].v.data(), &pts[k].w, sc)) detail::rethrow(rc);
+    }
+    observer(AspotIterate{long(sc[0]), sc[1], sc[2], ectx, pts[3], pts[2], pts[0], pts[1], sc[3], sc[4], sc[5]});
+  });
 }
 
 }  // namespace pot

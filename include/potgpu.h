@@ -206,6 +206,12 @@ int potgpu_session_destroy(potgpu_session* s);
  * on the session stream), with the algorithmic elements (n^2 exponentials)
  * and HBM bytes (stored cost only) of one launch. */
 int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep, double* elements, double* bytes);
+/* The accelerated solver's state after the last accepted iteration, for
+ * the reference's AspotObserver (solvers.hpp:188-204, 364-367): point
+ * which = 0 z_best, 1 z_check, 2 z_hat, 3 z_grave (u, v: n doubles; w: 1;
+ * any may be NULL); scalars[6] = {t, theta, error, phi_hat, phi_best,
+ * phi_check}. POTGPU_ERR_UNSUPPORTED for the Sinkhorn solvers. */
+int potgpu_session_read_state(potgpu_session* s, int which, double* u, double* v, double* w, double scalars[6]);
 /* Counters of the session so far: kernels launched by iterate(), step
  * attempts (incl. halvings) and n^2 sweeps executed. */
 int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* attempts, int64_t* sweeps);
@@ -225,6 +231,13 @@ void* potgpu_ctx_stream(potgpu_ctx* ctx);
  * when the reference's range checks would throw (scalars still filled). */
 int potgpu_dual_eval(potgpu_ctx* ctx, const potgpu_problem* problem, double gamma, const double* u, const double* v,
                      double w, double* row, double* col, double* scalars);
+
+/* exponent_matrix (which = 0) / b_matrix (which = 1) (dual.hpp:93-109) at
+ * z = (u, v, w) for logK = -C/gamma of `problem` (fp64 semantics): out is
+ * the dense n x n row-major matrix. POTGPU_OVERFLOW for B when the largest
+ * exponent is not <= 700 (check_exp_range; out is still written). */
+int potgpu_dual_matrix(potgpu_ctx* ctx, const potgpu_problem* problem, double gamma, const double* u, const double* v,
+                       double w, int which, double* out);
 
 /* round_pot (rounding.hpp:46-77) on the device for a dense row-major n x n
  * plan X (r, c, s validated as by validate(), core.hpp:131-169). */

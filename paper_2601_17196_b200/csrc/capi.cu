@@ -380,6 +380,11 @@ struct Session {
   virtual double gamma_value() const = 0;
   virtual int64_t iterations_done() = 0;
   virtual int status_code() = 0;
+  // ASPOT observer support: a dual point of the last accepted iteration and
+  // its scalars (t, theta, error, phi_hat, phi_best, phi_check)
+  virtual void read_state(int, double*, double*, double*, double*) {
+    throw Error(POTGPU_ERR_UNSUPPORTED, "iterate state is available for the accelerated solver only");
+  }
   int64_t launches = 0;  // kernels this session launched inside iterate()
 };
 
@@ -598,6 +603,26 @@ struct AspotSession : Session {
     return round_now(Xdev);
   }
   Slot plan_point() override { return ws.slot(S_ZC); }
+  void read_state(int which, double* u, double* v, double* w, double* scalars) override {
+    if (trivial) throw Error(POTGPU_ERR_UNSUPPORTED, "trivial solve has no iterates");
+    static const int slot_of[4] = {S_Z, S_ZC, S_ZH, S_ZG};  // z_best (= z), z_check, z_hat, z_grave
+    if (which < 0 || which > 3) throw Error(POTGPU_INVALID_ARGUMENT, "point index must be 0..3");
+    const Slot z = ws.slot(slot_of[which]);
+    const int64_t n = P.n;
+    if (u) PG_CK(cudaMemcpyAsync(u, z.u(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    if (v) PG_CK(cudaMemcpyAsync(v, z.v(), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    if (w) PG_CK(cudaMemcpyAsync(w, z.w(), sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    sync_ctl();
+    const AspotCtl& h = *ws.host_ctl;
+    if (scalars) {
+      scalars[0] = double(h.t);
+      scalars[1] = h.theta;
+      scalars[2] = h.error;
+      scalars[3] = h.phi_hat;
+      scalars[4] = h.phi_best;
+      scalars[5] = h.phi_check;
+    }
+  }
   Workspace& workspace() override { return ws; }
   double gamma_value() const override { return gamma; }
   int64_t iterations_done() override {
@@ -899,6 +924,13 @@ int potgpu_session_finish(potgpu_session* s, potgpu_summary* sm, potgpu_outputs*
 
 int potgpu_session_destroy(potgpu_session* s) {
   return guarded([&] { delete reinterpret_cast<Session*>(s); });
+}
+
+int potgpu_session_read_state(potgpu_session* s, int which, double* u, double* v, double* w, double scalars[6]) {
+  return guarded([&] {
+    if (!s) throw Error(POTGPU_INVALID_ARGUMENT, "null session");
+    reinterpret_cast<Session*>(s)->read_state(which, u, v, w, scalars);
+  });
 }
 
 int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep, double* elements, double* bytes) {
@@ -1210,6 +1242,72 @@ static void check_marginals(int64_t n, const double* r, const double* c, double 
 }
 
 // round_pot (rounding.hpp:46-77) on a dense row-major plan.
+// exponent_matrix / b_matrix (dual.hpp:93-109): e_ij = ((logK_ij + u_i) + v_j) + w,
+// B = exp(e) (POTGPU_OVERFLOW when max e > 700, as check_exp_range).
+__global__ void k_dual_matrix(Slot z, const double* L, int64_t ld, int64_t n, int which, double* out, unsigned long long* mx) {
+  unsigned long long m = 0;
+  bool nan = false;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n * n; k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = k / n, j = k % n;
+    const double e = ((L[i * ld + j] + z.u()[i]) + z.v()[j]) + *z.w();
+    out[k] = which == 0 ? e : eexp(e);
+    if (e != e) nan = true;
+    // order-preserving key of the double (max over signed values)
+    const unsigned long long b = (unsigned long long)__double_as_longlong(e);
+    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+    m = max(m, key);
+  }
+  if (nan) m = ~0ULL;
+  atomicMax(mx, m);
+}
+
+int potgpu_dual_matrix(potgpu_ctx* c, const potgpu_problem* pr, double gamma, const double* u, const double* v, double w,
+                       int which, double* out) {
+  int overflow = 0;
+  const int rc = guarded([&] {
+    if (!c || !out || !u || !v) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    if (!(gamma > 0) || !std::isfinite(gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
+    if (which != 0 && which != 1) throw Error(POTGPU_INVALID_ARGUMENT, "which: 0 exponent, 1 B");
+    PG_CK(cudaSetDevice(c->cx.device));
+    potgpu_problem p64 = *pr;
+    p64.dtype = POTGPU_F64;  // the reference's semantics
+    if (p64.cost_kind == POTGPU_COST_SQEUCLIDEAN) p64.cost_kind = POTGPU_COST_SQEUCLIDEAN_STORED;
+    DevProblem P;
+    upload_problem(c->cx, &p64, P);
+    build_logk(c->cx, P, gamma);
+    const int64_t n = P.n;
+    DevBuf<double> zb, ob;
+    DevBuf<unsigned long long> mx;
+    zb.alloc(size_t(2 * n + 1));
+    ob.alloc(size_t(n * n));
+    mx.alloc(1);
+    mx.zero(c->cx.stream);
+    PG_CK(cudaMemcpyAsync(zb.p, u, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(zb.p + n, v, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(zb.p + 2 * n, &w, sizeof(double), cudaMemcpyHostToDevice, c->cx.stream));
+    k_dual_matrix<<<c->cx.num_sms * 8, 256, 0, c->cx.stream>>>(Slot{zb.p, n}, P.L64.p, P.ld, n, which, ob.p, mx.p);
+    PG_CK(cudaGetLastError());
+    unsigned long long key = 0;
+    PG_CK(cudaMemcpyAsync(&key, mx.p, sizeof(key), cudaMemcpyDeviceToHost, c->cx.stream));
+    PG_CK(cudaMemcpyAsync(out, ob.p, size_t(n * n) * sizeof(double), cudaMemcpyDeviceToHost, c->cx.stream));
+    PG_CK(cudaStreamSynchronize(c->cx.stream));
+    double maxe;
+    if (key == ~0ULL) {
+      maxe = std::numeric_limits<double>::quiet_NaN();
+    } else {
+      const unsigned long long b = (key >> 63) ? (key & 0x7fffffffffffffffULL) : ~key;
+      std::memcpy(&maxe, &b, sizeof(double));
+    }
+    overflow = which == 1 && !(maxe <= kMaxExponent);
+  });
+  if (rc) return rc;
+  if (overflow) {
+    g_last_error = "Overflow: B(z) exponent exceeds representable range";
+    return POTGPU_OVERFLOW;
+  }
+  return 0;
+}
+
 int potgpu_round_pot(potgpu_ctx* c, int64_t n, const double* X, const double* r, const double* cm, double s,
                      double* X_out) {
   return guarded([&] {

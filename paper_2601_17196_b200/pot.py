@@ -162,7 +162,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
-    "potgpu_kmeans_quantize", "potgpu_round_balanced",
+    "potgpu_kmeans_quantize", "potgpu_round_balanced", "potgpu_dual_matrix", "potgpu_session_read_state",
 )
 
 _lib = None
@@ -204,6 +204,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                            P(ctypes.c_int32)]
     lib.potgpu_round_pot.argtypes = [ctypes.c_void_p, ctypes.c_int64, dp, dp, dp, ctypes.c_double, dp]
     lib.potgpu_round_balanced.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, dp, dp, dp, dp]
+    lib.potgpu_dual_matrix.argtypes = [ctypes.c_void_p, P(_Problem), ctypes.c_double, dp, dp, ctypes.c_double,
+                                       ctypes.c_int, dp]
+    lib.potgpu_session_read_state.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, dp, dp, dp]
     lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
     lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -561,9 +564,35 @@ class Session:
 
 
 def aspot_solve(inst: Instance, config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
-                **kw) -> SolveResult:
-    """solvers.hpp:265-385."""
-    return _run(SolverKind.Aspot, inst, config, ctx, **kw)
+                observer=None, **kw) -> SolveResult:
+    """solvers.hpp:265-385. observer(AspotIterate) (solvers.hpp:188-204,
+    364-367) is called after every accepted iteration: the device loop then
+    advances one iteration at a time and the points are copied to the host
+    (a diagnostic slow path)."""
+    if observer is None or inst.s == 0 or inst.size() < 2:
+        return _run(SolverKind.Aspot, inst, config, ctx, **kw)
+    st = aspot_setup(inst, config.epsilon)
+    gamma = config.gamma_override if config.gamma_override else st.gamma
+    ectx = EntropicContext(inst.C if inst.C is not None else dense_cost(inst.X, inst.Y, inst.cost_scale), gamma,
+                           st.mixed_r, st.mixed_c, inst.s)
+    sess = Session(SolverKind.Aspot, inst, config, ctx=ctx, **kw)
+    n = inst.size()
+    try:
+        while True:
+            _, it, fin = sess.iterate(1)
+            if it:
+                pts, sc = [], np.zeros(6)
+                for k in range(4):
+                    u, v, w = np.empty(n), np.empty(n), np.zeros(1)
+                    _check(sess.lib.potgpu_session_read_state(sess._h, k, _dp(u), _dp(v), _dp(w), _dp(sc)))
+                    pts.append(DualPoint(u, v, float(w[0])))
+                observer(AspotIterate(int(sc[0]), sc[1], sc[2], ectx, pts[3], pts[2], pts[0], pts[1], sc[3], sc[4],
+                                      sc[5]))
+            if fin:
+                break
+        return sess.finish()
+    finally:
+        sess.close()
 
 
 def feasible_sinkhorn_solve(inst: Instance, config: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
@@ -957,3 +986,273 @@ def extract_block(X_ext) -> BlockDecomposition:
         raise PotError(ErrorCode.DimensionMismatch, "extended plan must be square with side >= 2")
     n = X_ext.shape[0] - 1
     return BlockDecomposition(X_ext[:n, :n].copy(), X_ext[:n, n].copy(), X_ext[n, :n].copy(), float(X_ext[n, n]))
+
+
+# ------------------------------------------------------------- core / dual helpers --
+def solver_kind_from_name(name: str) -> Optional[SolverKind]:  # core.hpp:225-231
+    return {"aspot": SolverKind.Aspot, "sinkhorn": SolverKind.FeasibleSinkhorn,
+            "tuned-sinkhorn": SolverKind.TunedSinkhorn}.get(name)
+
+
+@dataclass
+class Violation:  # core.hpp:76-79
+    code: ErrorCode
+    detail: str
+
+
+class ValidationError(PotError):  # core.hpp:82-104: carries every violation
+    def __init__(self, violations: List[Violation]):
+        code = violations[0].code if violations else ErrorCode.InvalidArgument
+        msg = "invalid instance" + "".join(f"; {v.code.name} ({v.detail})" for v in violations)
+        super().__init__(code, msg)
+        self.violations = violations
+
+
+def validation_report(inst: Instance) -> List[Violation]:  # core.hpp:131-162
+    out: List[Violation] = []
+    r, c = np.asarray(inst.r, dtype=np.float64), np.asarray(inst.c, dtype=np.float64)
+    n = r.size
+    if n == 0:
+        return [Violation(ErrorCode.EmptyInput, "marginals are empty")]
+    C = inst.C
+    if c.size != n:
+        out.append(Violation(ErrorCode.DimensionMismatch, f"r has {n} entries, c has {c.size}"))
+    if C is not None and np.shape(C) != (n, n):
+        out.append(Violation(ErrorCode.DimensionMismatch, f"cost matrix is {np.shape(C)}, expected {n}x{n}"))
+    Cf = np.asarray(C if C is not None else np.zeros(0), dtype=np.float64)
+    if not (np.all(np.isfinite(r)) and np.all(np.isfinite(c)) and np.all(np.isfinite(Cf)) and math.isfinite(inst.s)):
+        out.append(Violation(ErrorCode.NonFiniteEntry, "non-finite entry in r, c, C or s"))
+    else:
+        if np.any(r < 0) or np.any(c < 0):
+            out.append(Violation(ErrorCode.NegativeEntry, "negative marginal entry"))
+        if Cf.size and np.any(Cf < 0):
+            out.append(Violation(ErrorCode.NegativeEntry, "negative cost entry"))
+        if inst.s < 0:
+            out.append(Violation(ErrorCode.NegativeEntry, "negative budget"))
+        if c.size == n and inst.s > min(r.sum(), c.sum()) + 1e-12:
+            out.append(Violation(ErrorCode.BudgetExceedsMass,
+                                 f"budget {inst.s} exceeds min marginal mass {min(r.sum(), c.sum())}"))
+    return out
+
+
+def validate(inst: Instance) -> Instance:  # core.hpp:164-169
+    v = validation_report(inst)
+    if v:
+        raise ValidationError(v)
+    return inst
+
+
+@dataclass
+class DualPoint:  # dual.hpp:15-43
+    u: np.ndarray
+    v: np.ndarray
+    w: float = 0.0
+
+    @staticmethod
+    def zero(n: int) -> "DualPoint":
+        return DualPoint(np.zeros(n), np.zeros(n), 0.0)
+
+    def all_finite(self) -> bool:
+        return bool(np.all(np.isfinite(self.u)) and np.all(np.isfinite(self.v)) and math.isfinite(self.w))
+
+    def __add__(self, o):
+        return DualPoint(self.u + o.u, self.v + o.v, self.w + o.w)
+
+    def __sub__(self, o):
+        return DualPoint(self.u - o.u, self.v - o.v, self.w - o.w)
+
+    def __rmul__(self, a: float):
+        return DualPoint(a * self.u, a * self.v, a * self.w)
+
+
+kMaxExponent = 700.0  # dual.hpp:47
+
+
+class EntropicContext:  # dual.hpp:52-75 (logK built on access; reductions on the device)
+    def __init__(self, C, gamma: float, r, c, s: float):
+        if not (gamma > 0) or not math.isfinite(gamma):
+            raise PotError(ErrorCode.InvalidArgument, "gamma must be positive")
+        self.C = np.ascontiguousarray(C, dtype=np.float64)
+        self.r, self.c = np.asarray(r, dtype=np.float64), np.asarray(c, dtype=np.float64)
+        if self.C.shape != (self.r.size, self.c.size):
+            raise PotError(ErrorCode.DimensionMismatch, "cost/marginal shape mismatch")
+        self.gamma, self.s = float(gamma), float(s)
+
+    @staticmethod
+    def from_instance(inst: Instance, gamma: float) -> "EntropicContext":
+        C = inst.C if inst.C is not None else dense_cost(inst.X, inst.Y, inst.cost_scale)
+        return EntropicContext(C, gamma, inst.r, inst.c, inst.s)
+
+    @property
+    def logK(self) -> np.ndarray:
+        return (-self.C) / self.gamma
+
+    def size(self) -> int:
+        return self.r.size
+
+    def _inst(self) -> Instance:
+        return Instance(r=self.r, c=self.c, s=self.s, C=self.C)
+
+
+def _eexp(x):  # Eigen's packet exp (clamped argument)
+    x = np.asarray(x, dtype=np.float64)
+    return np.where(np.isnan(x) | (x == np.inf), np.exp(x), np.exp(np.clip(x, -709.784, 709.784)))
+
+
+def _check_dual(ectx: EntropicContext, z: DualPoint, ranges=True):
+    if z.u.size != ectx.size() or z.v.size != ectx.size():
+        raise PotError(ErrorCode.DimensionMismatch, "dual point shape mismatch")
+    if ranges:
+        for x, what in ((z.u, "exp(u)"), (z.v, "exp(v)")):
+            m = np.max(x) if x.size else -np.inf
+            if not (m <= kMaxExponent):
+                raise PotError(ErrorCode.Overflow, f"{what} exponent exceeds representable range")
+
+
+def _dual_matrix(ectx: EntropicContext, z: DualPoint, which: int, ctx=None) -> np.ndarray:
+    lib = load_library()
+    ctx = ctx or default_context()
+    keep: list = []
+    prob = _problem(ectx._inst(), keep)
+    n = ectx.size()
+    out = np.empty((n, n))
+    u, v = np.ascontiguousarray(z.u, dtype=np.float64), np.ascontiguousarray(z.v, dtype=np.float64)
+    _check(lib.potgpu_dual_matrix(ctx._h, ctypes.byref(prob), ectx.gamma, _dp(u), _dp(v), float(z.w), which, _dp(out)))
+    return out
+
+
+def exponent_matrix(ectx: EntropicContext, z: DualPoint, ctx=None) -> np.ndarray:  # dual.hpp:92-99
+    _check_dual(ectx, z, ranges=False)
+    return _dual_matrix(ectx, z, 0, ctx)
+
+
+def b_matrix(ectx: EntropicContext, z: DualPoint, ctx=None) -> np.ndarray:  # dual.hpp:103-109
+    _check_dual(ectx, z, ranges=False)
+    return _dual_matrix(ectx, z, 1, ctx)
+
+
+def dual_gradient(ectx: EntropicContext, z: DualPoint, ctx=None) -> DualPoint:  # dual.hpp:122-133
+    _check_dual(ectx, z)
+    ev = dual_eval(ectx._inst(), ectx.gamma, z.u, z.v, z.w, ctx=ctx)
+    return DualPoint((ev.row + _eexp(z.u)) - ectx.r, (ev.col + _eexp(z.v)) - ectx.c, ev.total - ectx.s)
+
+
+def dual_objective(ectx: EntropicContext, z: DualPoint, ctx=None) -> float:  # dual.hpp:111-120
+    _check_dual(ectx, z)
+    ev = dual_eval(ectx._inst(), ectx.gamma, z.u, z.v, z.w, ctx=ctx)
+    return ((((ev.total + _eexp(z.u).sum()) + _eexp(z.v).sum()) - float(z.u @ ectx.r)) - float(z.v @ ectx.c)) \
+        - z.w * ectx.s
+
+
+def feasibility_error(ectx: EntropicContext, z: DualPoint, ctx=None) -> float:  # dual.hpp:135-139
+    g = dual_gradient(ectx, z, ctx)
+    return float(np.abs(g.u).sum() + np.abs(g.v).sum() + abs(g.w))
+
+
+def rho(a: float, b: float) -> float:  # dual.hpp:141-146
+    if not (a > 0) or not (b > 0):
+        raise PotError(ErrorCode.NonPositiveArgument, "rho requires a, b > 0")
+    return b - a + a * math.log(a / b)
+
+
+def rho_limit(a: float, b: float) -> float:  # dual.hpp:150-158
+    if not (a > 0):
+        return b
+    if not (b > 0):
+        return math.inf
+    return rho(a, b)
+
+
+def greenkhorn_step(ectx: EntropicContext, z: DualPoint, rule: BlockRule, t: int, ctx=None) -> DualPoint:
+    """solvers.hpp:43-89: sums on the device, block choice / update on the host."""
+    _check_dual(ectx, z)
+    ev = dual_eval(ectx._inst(), ectx.gamma, z.u, z.v, z.w, ctx=ctx)
+    row, col = ev.row + _eexp(z.u), ev.col + _eexp(z.v)
+    if rule == BlockRule.RoundRobin:
+        block = t % 3
+    else:
+        su = sum(rho_limit(a, b) for a, b in zip(ectx.r, row))
+        sv = sum(rho_limit(a, b) for a, b in zip(ectx.c, col))
+        sw = rho_limit(ectx.s, ev.total)
+        block, best = 0, su
+        if sv > best:
+            block, best = 1, sv
+        if sw > best:
+            block = 2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        if block == 0:
+            out = DualPoint(z.u + (np.log(ectx.r) - np.log(row)), z.v.copy(), z.w)
+        elif block == 1:
+            out = DualPoint(z.u.copy(), z.v + (np.log(ectx.c) - np.log(col)), z.w)
+        else:
+            out = DualPoint(z.u.copy(), z.v.copy(), z.w + (math.log(ectx.s) - math.log(ev.total)
+                                                           if ectx.s > 0 and ev.total > 0 else -math.inf))
+    if not out.all_finite():
+        raise PotError(ErrorCode.Overflow, "block update left the exp range")
+    return out
+
+
+@dataclass
+class AspotSetup:  # solvers.hpp:94-99
+    gamma: float
+    eps_tilde: float
+    mixed_r: np.ndarray
+    mixed_c: np.ndarray
+
+
+def aspot_setup(inst: Instance, epsilon: float) -> AspotSetup:  # solvers.hpp:100-133
+    validate(inst)
+    if not (epsilon > 0) or not math.isfinite(epsilon):
+        raise PotError(ErrorCode.InvalidArgument, "epsilon must be positive")
+    n = inst.size()
+    if n < 2:
+        raise PotError(ErrorCode.DegenerateInstance, "accelerated setup needs n >= 2 (log n vanishes)")
+    gamma = epsilon / (4.0 * math.log(float(n)))
+    C = inst.C if inst.C is not None else dense_cost(inst.X, inst.Y, inst.cost_scale)
+    cmax = float(np.max(C))
+    eps_t = epsilon / (8.0 * cmax) if cmax > 0 else math.inf
+    sr, sc = float(np.sum(inst.r)), float(np.sum(inst.c))
+    if sr > 1:
+        eps_t = min(eps_t, 8.0 * (sr - inst.s) / (sr - 1.0))
+    if sc > 1:
+        eps_t = min(eps_t, 8.0 * (sc - inst.s) / (sc - 1.0))
+    if not (gamma > 0) or not math.isfinite(gamma):
+        raise PotError(ErrorCode.DegenerateInstance, "derived gamma is not positive")
+    if not (eps_t > 0):
+        raise PotError(ErrorCode.DegenerateInstance, "stopping tolerance collapsed to zero (budget equals mass)")
+    lam = min(eps_t / 8.0, 0.5)
+    return AspotSetup(gamma, eps_t, (1.0 - lam) * np.asarray(inst.r) + lam / n, (1.0 - lam) * np.asarray(inst.c) + lam / n)
+
+
+def theta_next(theta: float) -> float:  # solvers.hpp:32-37
+    return theta * (math.sqrt(theta * theta + 4.0) - theta) / 2.0
+
+
+def entropy(x) -> float:  # solvers.hpp:19-28
+    x = np.asarray(x, dtype=np.float64)
+    if np.any(x < 0):
+        raise PotError(ErrorCode.NegativeEntry, "entropy requires x >= 0")
+    xp = x[x > 0]
+    return float(-(xp * np.log(xp)).sum())
+
+
+def dummy_penalty(cmax: float, epsilon: float) -> float:  # solvers.hpp:485-490
+    A = 8.0 * cmax / epsilon if cmax > 0 else 0.0
+    if not (A > cmax) or not math.isfinite(A):
+        A = 2.0 * cmax if cmax > 0 else 1.0
+    return A
+
+
+@dataclass
+class AspotIterate:  # solvers.hpp:188-202
+    t: int
+    theta: float
+    error: float
+    ctx: EntropicContext
+    z_grave: DualPoint
+    z_hat: DualPoint
+    z_best: DualPoint
+    z_check: DualPoint
+    phi_hat: float
+    phi_best: float
+    phi_check: float

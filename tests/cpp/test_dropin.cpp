@@ -193,6 +193,56 @@ int main() {
     const Matrix q = read_xyz("/tmp/potgpu_dropin.xyz");
     EXPECT(q.rows() == 2 && q(0, 0) == 0.1 && q(1, 2) == -2.5);
   }
+  {  // test_dual.cpp: hand values on the 1 x 1 instance, overflow, shape errors
+    const EntropicContext ctx(Matrix::Zero(1, 1), 1.0, Vector::Constant(1, 1.0), Vector::Constant(1, 1.0), 0.5);
+    const DualPoint z = DualPoint::zero(1);
+    EXPECT(dual_objective(ctx, z) == 3.0);
+    const DualPoint g = dual_gradient(ctx, z);
+    EXPECT(g.u(0) == 1.0 && g.v(0) == 1.0 && g.w == 0.5);
+    EXPECT(feasibility_error(ctx, z) == 2.5);
+    EXPECT(b_matrix(ctx, z)(0, 0) == 1.0);
+    DualPoint big{Vector::Constant(1, 400.0), Vector::Constant(1, 400.0), 0.0};
+    bool threw = false;
+    try { b_matrix(ctx, big); } catch (const PotError& e) { threw = e.code() == ErrorCode::Overflow; }
+    EXPECT(threw);
+    threw = false;
+    try { dual_objective(ctx, DualPoint::zero(2)); } catch (const PotError& e) { threw = e.code() == ErrorCode::DimensionMismatch; }
+    EXPECT(threw);
+    // greenkhorn on u makes the row marginal exact (solvers.hpp:74-76)
+    const DualPoint z1 = greenkhorn_step(ctx, z, BlockRule::RoundRobin, 0);
+    EXPECT(std::fabs(dual_gradient(ctx, z1).u(0)) <= 1e-15);
+  }
+  {  // AspotObserver: one callback per accepted iteration, t = 1..T (solvers.hpp:364-367)
+    Instance in = make_synthetic_instance(30, 5, 1.0, 1.2, 0.6);
+    SolverConfig cfg; cfg.epsilon = 0.05; cfg.log_every = 1000000;
+    long calls = 0, last_t = 0;
+    double last_err = 0.0;
+    const SolveResult res = aspot_solve(in, cfg, [&](const AspotIterate& it) {
+      ++calls;
+      EXPECT(it.t == last_t + 1);
+      last_t = it.t;
+      last_err = it.error;
+      EXPECT(it.phi_best <= it.phi_hat);
+    });
+    EXPECT(calls == res.iterations && last_t == res.iterations);
+    EXPECT(last_err == res.final_error);
+    const SolveResult plain = aspot_solve(in, cfg);
+    EXPECT(plain.iterations == res.iterations && plain.final_error == res.final_error);
+  }
+  {  // validation_report / ValidationError (test_core.cpp)
+    Instance in;
+    in.r = Vector::Constant(2, 1.0); in.r(1) = -1.0;
+    in.c = Vector::Constant(2, 1.0);
+    in.C = Matrix::Ones(2, 2);
+    in.s = 5.0;
+    EXPECT(validation_report(in).size() == 2u);
+    bool threw = false;
+    try { validate(in); } catch (const ValidationError& e) { threw = e.violations().size() == 2u && e.code() == ErrorCode::NegativeEntry; }
+    EXPECT(threw);
+    EXPECT(solver_kind_from_name("tuned-sinkhorn") == SolverKind::TunedSinkhorn && !solver_kind_from_name("x"));
+    const AspotSetup st = aspot_setup(make_synthetic_instance(10, 2, 1.0, 1.0, 0.5), 0.1);
+    EXPECT(std::fabs(st.gamma - 0.1 / (4.0 * std::log(10.0))) <= 1e-17);
+  }
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
 }
