@@ -1256,3 +1256,22 @@ class AspotIterate:  # solvers.hpp:188-202
     phi_hat: float
     phi_best: float
     phi_check: float
+
+
+def theory_bounds(inst: Instance, gamma: float, eps_prime: float) -> TheoryBounds:  # solvers.hpp:146-174
+    if not (gamma > 0) or not math.isfinite(gamma):
+        raise PotError(ErrorCode.InvalidArgument, "gamma must be positive")
+    if not (eps_prime > 0) or not math.isfinite(eps_prime):
+        raise PotError(ErrorCode.InvalidArgument, "eps_prime must be positive")
+    sr, sc = float(np.sum(inst.r)), float(np.sum(inst.c))
+    M = max(sr, sc)
+    if not (M > inst.s):
+        raise PotError(ErrorCode.DegenerateInstance, "dual radius is infinite when budget equals max mass")
+    me = min(float(np.min(inst.r)), float(np.min(inst.c)))
+    if not (me > 0):
+        raise PotError(ErrorCode.DegenerateInstance, "dual radius needs strictly positive marginals")
+    C = inst.C if inst.C is not None else dense_cost(inst.X, inst.Y, inst.cost_scale)
+    R = float(np.max(C)) * M / (gamma * (M - inst.s)) - math.log(me)
+    mu = gamma / (sr + sc - inst.s)
+    L = 3.0 / mu
+    return TheoryBounds(R, L, mu, 1.0 + (12.0 * math.sqrt(14.0 * inst.size() * L) * R / eps_prime) ** (2.0 / 3.0))
