@@ -69,8 +69,10 @@ enum potgpu_cost_kind {
   POTGPU_COST_SQEUCLIDEAN_STORED = 2
 };
 
-/* pot::Instance (core.hpp:108-118) plus the cost representation. All host
- * pointers (device pointers when device_ptrs = 1). */
+/* pot::Instance (core.hpp:108-118) plus the cost representation. Host
+ * pointers, or device pointers on the context's device when device_ptrs = 1
+ * (a dense C is then read in place; r, c and point coordinates, O(n), are
+ * staged through the host for the setup logic). */
 typedef struct potgpu_problem {
   int64_t n;
   int dtype;            /* potgpu_dtype */

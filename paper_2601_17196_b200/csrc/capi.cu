@@ -75,8 +75,8 @@ __global__ void k_points_store(const float4* X, const float4* Y, int64_t n, int6
 
 static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P) {
   if (!pr) throw Error(POTGPU_INVALID_ARGUMENT, "null problem");
-  if (pr->device_ptrs) throw Error(POTGPU_ERR_UNSUPPORTED, "device_ptrs=1 is not supported yet; pass host buffers");
   const int64_t n = pr->n;
+  const bool dev = pr->device_ptrs != 0;  // r, c, C, X, Y are device pointers (e.g. CUDA tensors)
   // validation_report (core.hpp:131-169): report the FIRST violation's code.
   if (n <= 0) throw Error(POTGPU_EMPTY_INPUT, "invalid instance: marginals are empty");
   if (!pr->r || !pr->c) throw Error(POTGPU_INVALID_ARGUMENT, "null marginals");
@@ -85,8 +85,16 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
   P.dtype = pr->dtype;
   P.kind = pr->cost_kind;
   P.ld = round_up(n, kStripCols32);  // covers both strip widths
-  P.r.assign(pr->r, pr->r + n);
-  P.c.assign(pr->c, pr->c + n);
+  if (dev) {  // the O(n) marginals are needed on the host (setup, rounding logic)
+    P.r.resize(size_t(n));
+    P.c.resize(size_t(n));
+    PG_CK(cudaMemcpyAsync(P.r.data(), pr->r, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(P.c.data(), pr->c, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+  } else {
+    P.r.assign(pr->r, pr->r + n);
+    P.c.assign(pr->c, pr->c + n);
+  }
   P.s = pr->s;
   bool finite = std::isfinite(pr->s);
   for (int64_t i = 0; i < n; ++i) finite = finite && std::isfinite(P.r[i]) && std::isfinite(P.c[i]);
@@ -95,13 +103,17 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     if (!pr->C) throw Error(POTGPU_DIMENSION_MISMATCH, "invalid instance: cost matrix missing");
     const int64_t ldc = pr->ldc > 0 ? pr->ldc : n;
     DevBuf<double> raw;
-    raw.alloc(size_t(n * ldc));
-    PG_CK(cudaMemcpyAsync(raw.p, pr->C, size_t(n * ldc) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+    const double* src = pr->C;  // device_ptrs: read in place
+    if (!dev) {
+      raw.alloc(size_t(n * ldc));
+      PG_CK(cudaMemcpyAsync(raw.p, pr->C, size_t(n * ldc) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+      src = raw.p;
+    }
     DevBuf<unsigned long long> flags;
     flags.alloc(3);
     flags.zero(cx.stream);
     if (pr->dtype == POTGPU_F64) P.C64.alloc(size_t(n * P.ld)); else P.C32.alloc(size_t(n * P.ld));
-    k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw.p, n, ldc, pr->row_major, P.ld,
+    k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(src, n, ldc, pr->row_major, P.ld,
                                                           pr->dtype == POTGPU_F64 ? P.C64.p : nullptr,
                                                           pr->dtype == POTGPU_F32 ? P.C32.p : nullptr, flags.p);
     PG_CK(cudaGetLastError());
@@ -118,11 +130,23 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
       throw Error(POTGPU_ERR_UNSUPPORTED, "on-the-fly costs run in fp32 (dtype=F32)");
     if (!pr->X || !pr->Y || pr->d < 1 || pr->d > 3) throw Error(POTGPU_INVALID_ARGUMENT, "points need X, Y and 1 <= d <= 3");
     std::vector<float4> hx(static_cast<size_t>(n)), hy(static_cast<size_t>(n));
+    std::vector<double> xd, yd;
+    const double* Xs = pr->X;
+    const double* Ys = pr->Y;
+    if (dev) {  // n x d coordinates: small, staged through the host
+      xd.resize(size_t(n * pr->d));
+      yd.resize(size_t(n * pr->d));
+      PG_CK(cudaMemcpyAsync(xd.data(), pr->X, xd.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+      PG_CK(cudaMemcpyAsync(yd.data(), pr->Y, yd.size() * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+      PG_CK(cudaStreamSynchronize(cx.stream));
+      Xs = xd.data();
+      Ys = yd.data();
+    }
     for (int64_t i = 0; i < n; ++i) {
       float a[3] = {0, 0, 0}, b[3] = {0, 0, 0};
       for (int k = 0; k < pr->d; ++k) {
-        a[k] = float(pr->X[i * pr->d + k]);
-        b[k] = float(pr->Y[i * pr->d + k]);
+        a[k] = float(Xs[i * pr->d + k]);
+        b[k] = float(Ys[i * pr->d + k]);
         finite = finite && std::isfinite(a[k]) && std::isfinite(b[k]);
       }
       hx[size_t(i)] = make_float4(a[0], a[1], a[2], 0.f);

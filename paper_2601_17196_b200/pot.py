@@ -248,7 +248,7 @@ class Instance:
     stored: bool = False  # points given, cost materialised once on the device and streamed
 
     def size(self) -> int:
-        return int(np.asarray(self.r).shape[0])
+        return int(self.r.shape[0]) if hasattr(self.r, "shape") else len(self.r)
 
     def source_mass(self) -> float:
         return float(np.sum(self.r))
@@ -408,7 +408,45 @@ def default_context() -> Context:
     return _default_ctx
 
 
+def _cuda_ptr(a, shape, what: str):
+    """Device pointer of a float64 C-contiguous CUDA array (__cuda_array_interface__)."""
+    cai = a.__cuda_array_interface__
+    if cai.get("typestr") not in ("<f8", "=f8"):
+        raise PotError(ErrorCode.InvalidArgument, f"{what}: device arrays must be float64")
+    if tuple(cai["shape"]) != tuple(shape):
+        raise PotError(ErrorCode.DimensionMismatch, f"{what} has shape {tuple(cai['shape'])}, expected {tuple(shape)}")
+    strides = cai.get("strides")
+    if strides is not None and tuple(strides) != tuple(8 * int(np.prod(shape[k + 1:])) for k in range(len(shape))):
+        raise PotError(ErrorCode.InvalidArgument, f"{what}: device arrays must be C-contiguous")
+    return ctypes.cast(ctypes.c_void_p(cai["data"][0]), ctypes.POINTER(ctypes.c_double))
+
+
+def _is_cuda(a) -> bool:
+    return a is not None and hasattr(a, "__cuda_array_interface__")
+
+
+def _problem_device(inst: Instance, keep: list) -> _Problem:
+    """Every array on the device (device_ptrs = 1): no host copies of C."""
+    n = int(inst.r.shape[0])
+    p = _Problem()
+    p.n, p.dtype, p.device_ptrs, p.s = n, int(inst.dtype), 1, float(inst.s)
+    p.r, p.c = _cuda_ptr(inst.r, (n,), "r"), _cuda_ptr(inst.c, (n,), "c")
+    keep += [inst.r, inst.c]
+    if inst.C is not None:
+        p.cost_kind, p.C, p.ldc, p.row_major = 0, _cuda_ptr(inst.C, (n, n), "C"), n, 1
+        keep.append(inst.C)
+    else:
+        d = int(inst.X.shape[1])
+        p.cost_kind, p.X, p.Y, p.d = (2 if inst.stored else 1), _cuda_ptr(inst.X, (n, d), "X"), \
+            _cuda_ptr(inst.Y, (n, d), "Y"), d
+        p.cost_scale = float(inst.cost_scale) if inst.cost_scale else 0.0
+        keep += [inst.X, inst.Y]
+    return p
+
+
 def _problem(inst: Instance, keep: list) -> _Problem:
+    if _is_cuda(inst.r):
+        return _problem_device(inst, keep)
     n = inst.size()
     p = _Problem()
     p.n = n

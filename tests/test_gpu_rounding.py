@@ -56,3 +56,24 @@ def test_rounding_errors(ctx):
     with pytest.raises(pot.PotError) as e:
         pot.round_balanced(X, np.ones(5), 2 * np.ones(5), ctx=ctx)
     assert e.value.code == pot.ErrorCode.UnbalancedMarginals
+
+
+def test_device_resident_inputs_match_host_inputs(ctx):
+    """device_ptrs = 1 (CUDA arrays, e.g. torch tensors; zero-copy for C):
+    the same solve as from host buffers."""
+    import torch
+    inst = pot.config_instance(1, n=300)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9)
+    a = pot.aspot_solve(inst, cfg, ctx=ctx)
+    dev = pot.Instance(r=torch.tensor(inst.r, device="cuda"), c=torch.tensor(inst.c, device="cuda"), s=inst.s,
+                       C=torch.tensor(inst.C, device="cuda"))
+    b = pot.aspot_solve(dev, cfg, ctx=ctx)
+    assert a.iterations == b.iterations and a.cost == b.cost
+    pts = pot.config_instance(3, n=1024)
+    cfg32 = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False)
+    a = pot.aspot_solve(pts, cfg32, ctx=ctx)
+    devp = pot.Instance(r=torch.tensor(pts.r, device="cuda"), c=torch.tensor(pts.c, device="cuda"), s=pts.s,
+                        X=torch.tensor(pts.X, device="cuda"), Y=torch.tensor(pts.Y, device="cuda"),
+                        cost_scale=pts.cost_scale, dtype=pot.DType.F32)
+    b = pot.aspot_solve(devp, cfg32, ctx=ctx)
+    assert a.iterations == b.iterations and a.cost == b.cost
