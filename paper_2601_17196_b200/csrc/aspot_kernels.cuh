@@ -470,8 +470,7 @@ __global__ void k_resume(AspotCtl* ctl, int64_t pause_at) {
   loop_head(ctl);
 }
 
-__global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
-  pdl_wait();
+__device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
   if (!ctl->g_active) return;
   ctl->attempts += 1;
   if (!ctl->attempt_ok) {
@@ -502,6 +501,51 @@ __global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
   if (ctl->t % ctl->log_every == 0 || !(ctl->error > ctl->eps_tilde))  // solvers.hpp:309
     append_trace(ctl, trace, ctl->t, ctl->error, ctl->phi_check);
   loop_head(ctl);
+}
+
+__global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
+  pdl_wait();
+  commit_state(ctl, trace, lg);
+}
+
+// End of a step attempt, one launch: on success z <- z_best, z_check <-
+// z_check', their sums, and already the next iteration's
+// z_bar = (1 - theta') z_check + theta' z (k_zbar's arithmetic with theta' =
+// theta_next(theta)); then the last block to finish takes the scalar
+// decisions of commit_state (halving / record / loop head).
+__global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot zb, double* rowc, double* colc,
+                         const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, unsigned* ticket) {
+  pdl_wait();
+  if (!ctl->g_active) return;  // uniform over the grid
+  if (ctl->attempt_ok) {
+    const bool keep = ctl->keep_check;
+    const double th = theta_next_d(ctl->theta), om = 1.0 - th;
+    const int64_t n = z.n;
+    for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+      const double zbst = keep ? zc.base[k] : zh.base[k];
+      const double zcn = zn.base[k];
+      z.base[k] = zbst;
+      zc.base[k] = zcn;
+      const double a = om * zcn;
+      const double b = th * zbst;
+      zb.base[k] = a + b;
+      if (k < n) {
+        rowc[k] = rown[k];
+        colc[k] = coln[k];
+      }
+    }
+  }
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    *ticket = 0u;
+    commit_state(ctl, trace, lg);
+  }
 }
 
 // Initial state after the first phi/grad evaluation at z_check = 0.

@@ -438,7 +438,8 @@ struct AspotSession : Session {
     const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
                ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
     const int gv = ws.nblk;
-    launch_k(k_zbar, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZC, Z, ZB);
+    // z_bar of a new iteration was formed by the previous attempt's k_commit
+    // (0 at the start: z = z_check = 0)
     const SweepOut none{};
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new);
     launch_k(k_zgrave, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
@@ -466,9 +467,8 @@ struct AspotSession : Session {
       sc.select_b = &ctl->keep_check;
       launch_eval(cx, ws, none, ZN, R_NEW, &ctl->g_new_scaled, &sc);
     }
-    launch_k(k_commit_copy, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ws.row(R_CHECK), ws.col(R_CHECK), ws.row(R_NEW),
-                                                     ws.col(R_NEW));
-    launch_k(k_commit_state, dim3(1), dim3(1), 0, cx.stream, ctl, ws.trace.p, ws.iterlog.p);
+    launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
+             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, ws.ticket.p + 1);
     PG_CK(cudaGetLastError());
   }
 

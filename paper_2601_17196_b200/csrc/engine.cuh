@@ -185,7 +185,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.maxp.alloc(size_t(ws.nstrips * max_rb));
   ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * kTPI, kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
-  ws.ticket.alloc(1);
+  ws.ticket.alloc(2);  // [0] k_point_eval, [1] k_commit
   ws.ticket.zero(cx.stream);
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n) + ws.nshards * ceil_div(n, kThreads))));
   ws.rt.alloc(size_t(n));
