@@ -9,6 +9,8 @@
 // host round trip; the host only polls the state every few attempts.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sweep.cuh"
 
@@ -186,12 +188,21 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
 // the last block to finish (atomic ticket) reduces all partials in a fixed
 // order and takes the decision (apply_role). Deterministic, one launch.
 constexpr int kEvalThreads = 128;
-constexpr int kTPI = 4;  // threads per index
+// threads per index of k_point_eval ($POTGPU_EVAL_TPI: 1, 2, 4)
+inline int eval_tpi() {
+  static const int v = [] {
+    const char* e = std::getenv("POTGPU_EVAL_TPI");
+    const int k = e ? std::atoi(e) : 0;
+    return (k == 1 || k == 2 || k == 4) ? k : 4;
+  }();
+  return v;
+}
 
 // Sum of the partials p[base .. base + cnt) of one index, split over the
 // kTPI threads of a group (thread q takes s = q, q + kTPI, ...). fp32
 // (sum, log2 scale) partials are combined relative to their max with MUFU
 // ex2 and turned into fp64 once: S 2^(M + offset).
+template <int kTPI>
 __device__ __forceinline__ double group_partial_sum(const double* p, int64_t base, int64_t cnt, int fmt, double offset,
                                                     int q) {
   if (fmt == PF_F64) {
@@ -227,6 +238,7 @@ __device__ __forceinline__ double group_partial_sum(const double* p, int64_t bas
 // fixed-order partials, and the last block to finish (atomic ticket)
 // reduces all partials in a fixed order and takes the decision
 // (apply_role). Deterministic, one launch.
+template <int kTPI>
 __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int role, ReduceArgs a, unsigned* ticket) {
   pdl_wait();
   if (a.gate && *a.gate == 0) return;
@@ -255,8 +267,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     if (a.mode == 0) {
       double off = (ui + w) * kLog2e;
       if (a.rowshift) off = off + a.rowshift[ii];
-      rb = group_partial_sum(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
-      cb = group_partial_sum(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
+      rb = group_partial_sum<kTPI>(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
+      cb = group_partial_sum<kTPI>(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
     } else {
       rb = srow[ii] * fs;
       cb = scol[ii] * fs;

@@ -183,7 +183,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * max_rb * n));
   ws.maxp.alloc(size_t(ws.nstrips * max_rb));
-  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * kTPI, kEvalThreads), 4096));
+  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * eval_tpi(), kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
   ws.ticket.alloc(2);  // [0] k_point_eval, [1] k_commit
   ws.ticket.zero(cx.stream);
@@ -313,7 +313,11 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.pfmt = so.pfmt;
   r.rowshift = so.rowshift;
   r.mode = scaled ? 1 : 0;
-  launch_k(k_point_eval, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p);
+  switch (eval_tpi()) {
+    case 1: launch_k(k_point_eval<1>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
+    case 2: launch_k(k_point_eval<2>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
+    default: launch_k(k_point_eval<4>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
+  }
   PG_CK(cudaGetLastError());
 }
 
