@@ -31,6 +31,8 @@ struct SinkhornSession : Session {
   DevBuf<double> zv;      // point (0, v[0..n), 0) for the fp32 row-LSE sweep
   DevBuf<double> zf;      // point (u[0..n), v[0..n), 0) for the output stage
   DevBuf<double> zuv;     // point (u[0..n), v[0..n), 0) of the fast column pass (fp32)
+  DevBuf<double> dummy;   // k_sk_dummy block partials
+  DevBuf<unsigned> dummy_ticket;
   DevBuf<SinkCtl> ctl;
   PinnedObj<SinkCtl> hctl_buf;
   SinkCtl* hctl = nullptr;
@@ -45,6 +47,9 @@ struct SinkhornSession : Session {
     if (exec) cudaGraphExecDestroy(exec);
   }
 
+  // k_sk_dummy grid: >= 2048 values per block (the last block merges the
+  // block partials sequentially)
+  int dummy_blocks() const { return int(std::max<int64_t>(1, std::min<int64_t>(kSkDummyBlocks, P.n / 2048))); }
   int sk_blocks() const { return int(std::min<int64_t>(ceil_div(P.n * kSkTPI, kSkThreads), 4096)); }
   Slot zv_slot() const { return Slot{zv.p, P.n}; }
   Slot zf_slot() const { return Slot{zf.p, P.n}; }
@@ -106,7 +111,7 @@ struct SinkhornSession : Session {
       nstrips = 1;
       fmt = LP_F64;
     }
-    launch_k(k_sk_dummy, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.v, 0, gate);
+    launch_k(k_sk_dummy, dim3(dummy_blocks()), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.v, 0, dummy.p, dummy_ticket.p, gate);
     launch_k(k_sk_rows, dim3(sk_blocks()), dim3(kSkThreads), 0, cx.stream, ctl.p, sv, rowp, nstrips, fmt,
                                                       cx.comm.sharded() ? nullptr : P.rowshift(), gate);
   }
@@ -118,7 +123,7 @@ struct SinkhornSession : Session {
   Slot zuv_slot() const { return Slot{zuv.p, P.n}; }
 
   void col_lse(int update, const int* gate) {  // at the current u
-    launch_k(k_sk_dummy, dim3(1), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.u, 1, gate);
+    launch_k(k_sk_dummy, dim3(dummy_blocks()), dim3(kVecThreads), 0, cx.stream, ctl.p, sv.u, 1, dummy.p, dummy_ticket.p, gate);
     if (fast_cols()) {
       col_pass(update, gate, true);
       col_pass(update, &ctl.p->col_flush, false);  // gated: only after a flush
@@ -220,6 +225,9 @@ struct SinkhornSession : Session {
     sv.r = vec.p + 5 * m; sv.c = vec.p + 6 * m; sv.scratch = vec.p + 7 * m;
     zv.alloc(size_t(ws.slot_stride));
     zf.alloc(size_t(ws.slot_stride));
+    dummy.alloc(size_t(2 * kSkDummyBlocks));
+    dummy_ticket.alloc(1);
+    dummy_ticket.zero(cx.stream);
     sv.zv_v = zv.p + n;
     if (fast_cols()) {
       zuv.alloc(size_t(ws.slot_stride));

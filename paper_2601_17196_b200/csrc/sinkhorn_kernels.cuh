@@ -287,15 +287,19 @@ struct SinkVec {  // device vectors of the extended problem (length n + 1)
 };
 
 // log-sum-exp of x_k = (-0 + a_k) (k < n) and corner + a_n (the dummy
-// row/column of the extension), single block, two passes.
-__global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, const int* gate) {
+// row/column of the extension): block partials (max, sum relative to it),
+// merged in block order by the last block to finish (atomic ticket).
+constexpr int kSkDummyBlocks = 148;
+__global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, double* part, unsigned* ticket, const int* gate) {
   pdl_wait();
   if (gate && *gate == 0) return;
   const int64_t n = ctl->n;
   __shared__ double sh[kVecThreads];
+  __shared__ bool last;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t k0 = int64_t(blockIdx.x) * chunk, k1 = min(n, k0 + chunk);
   double m = -INFINITY;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) m = fmax(m, -0.0 + a[k]);
-  if (threadIdx.x == 0) m = fmax(m, ctl->corner + a[n]);
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) m = fmax(m, -0.0 + a[k]);
   sh[threadIdx.x] = m;
   __syncthreads();
   for (int s = kVecThreads / 2; s > 0; s >>= 1) {
@@ -305,10 +309,8 @@ __global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, const int* 
   const double M = sh[0];
   __syncthreads();
   double S = 0.0;
-  if (M != -INFINITY) {
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) S += exp((-0.0 + a[k]) - M);
-    if (threadIdx.x == 0) S += exp((ctl->corner + a[n]) - M);
-  }
+  if (M != -INFINITY)
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) S += exp((-0.0 + a[k]) - M);
   sh[threadIdx.x] = S;
   __syncthreads();
   for (int s = kVecThreads / 2; s > 0; s >>= 1) {
@@ -316,9 +318,21 @@ __global__ void k_sk_dummy(SinkCtl* ctl, const double* a, int which, const int* 
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double lse = M + log(sh[0]);
-    if (which == 0) ctl->row_lse_n = lse; else ctl->col_lse_n = lse;
+    part[2 * blockIdx.x] = M;
+    part[2 * blockIdx.x + 1] = sh[0];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  *ticket = 0u;
+  const volatile double* vp = part;
+  double Mt = -INFINITY, St = 0.0;
+  for (int b = 0; b < int(gridDim.x); ++b) lse_merge(Mt, St, vp[2 * b], vp[2 * b + 1]);
+  lse_merge(Mt, St, ctl->corner + a[n], 1.0);
+  const double lse = Mt + log(St);
+  if (which == 0) ctl->row_lse_n = lse; else ctl->col_lse_n = lse;
 }
 
 template <int K, int T>
