@@ -89,7 +89,9 @@ struct Workspace {
   int nshards = 1;                // all shards of the job
   int64_t xstride = 0;            // per-shard length of the all-reduce vector
   DevBuf<double> xsend, xrecv;
-  int64_t nstrips = 0, nrb = 0;
+  int64_t nstrips = 0, nrb = 0;  // row partials per row, column partials per column
+  int64_t nmax = 0;               // max-exponent slots (CTAs of a full sweep)
+  int pts_cs = 1;                 // cluster size of the points sweep's row-partial merge
   int nblk = 0;  // O(n) kernel grid
   int eval_blocks = 0;  // k_point_eval grid (8 indices per block)
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
@@ -137,7 +139,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   } else {
     const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
     switch (pts_pairs()) {
-      case 2: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32, kThreads, sm_est)); break;
+      case 2: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32<1>, kThreads, sm_est)); break;
       case 4: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<4>, kThreads, sm_est)); break;
       case 6: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<6>, kThreads, sm_est)); break;
       default: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<8>, kThreads, sm_est)); break;
@@ -166,23 +168,29 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     ws.xsend.alloc(size_t(cx.comm.vshards * ws.xstride));
     ws.xrecv.alloc(size_t(ws.xstride));
   }
-  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts_smem(max_rpc), sweep_f32_smem(max_rpc));
+  ws.pts_cs = (P.dot_form() && pts_pairs() == 2) ? pts_cluster(ws.g.grid.x) : 1;
+  for (const ShardGrid& sh : ws.shards) ws.pts_cs = std::min(ws.pts_cs, pts_cluster(sh.g.grid.x));
+  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts_smem(max_rpc, ws.pts_cs > 1), sweep_f32_smem(max_rpc));
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
   }
-  ws.nstrips = ws.g.grid.x;
+  ws.nstrips = ws.g.grid.x / ws.pts_cs;
   ws.nrb = ws.g.grid.y;
+  ws.nmax = int64_t(ws.g.grid.x) * ws.g.grid.y;
   ws.nblk = int(std::min<int64_t>(cx.num_sms, std::max<int64_t>(1, ceil_div(n, kVecThreads))));
   ws.slot_stride = round_up(2 * n + 1, 32);
   ws.slots.alloc(size_t(kSlots * ws.slot_stride));
   ws.sums.alloc(size_t(2 * kRoles * n));
-  ws.rowp.alloc(size_t(2 * ws.nstrips * n));  // x2: (max, sum) LSE partials
+  ws.rowp.alloc(size_t(2 * ws.g.grid.x * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * max_rb * n));
-  ws.maxp.alloc(size_t(ws.nstrips * max_rb));
+  ws.maxp.alloc(size_t(ws.g.grid.x * max_rb));
   ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * eval_tpi(), kEvalThreads), 4096));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
   ws.ticket.alloc(2);  // [0] k_point_eval, [1] k_commit
@@ -227,7 +235,14 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
     switch (pts_pairs()) {
-      case 2: launch_k(sweep_pts2_f32, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;  // two-row variant
+      case 2:  // two-row variant, row partials merged over a cluster of ws.pts_cs strips
+        switch (ws.pts_cs) {
+          case 8: launch_kc(sweep_pts2_f32<8>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 8, s, a); break;
+          case 4: launch_kc(sweep_pts2_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 4, s, a); break;
+          case 2: launch_kc(sweep_pts2_f32<2>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 2, s, a); break;
+          default: launch_k(sweep_pts2_f32<1>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
+        }
+        break;
       case 4: launch_k(sweep_pts_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
       case 6: launch_k(sweep_pts_f32<6>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
       default: launch_k(sweep_pts_f32<8>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
@@ -254,7 +269,7 @@ inline SweepOut sweep_point(Context& cx, const DevProblem& P, Workspace& ws, Slo
   const int64_t n = P.n;
   if (!cx.comm.sharded()) {
     launch_sweep(cx, P, ws, z, lu, lv, gate, floor_exp, gamma);
-    return SweepOut{ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.maxp.p, ws.nstrips * ws.nrb, ws.pfmt, P.rowshift()};
+    return SweepOut{ws.rowp.p, ws.nstrips, ws.colp.p, ws.nrb, ws.maxp.p, ws.nmax, ws.pfmt, P.rowshift()};
   }
   for (size_t p = 0; p < ws.shards.size(); ++p) {
     const ShardGrid& sh = ws.shards[p];

@@ -14,6 +14,7 @@
 // (deterministic run to run).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -402,8 +403,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_f32(Src src, SweepArgs a) {
 // work without holding a second row of exponents in registers. The CTA's
 // rows live in shared memory as (2 x'_i, A_i) float4s (no global loads in
 // the row loop). Epilogue and partial formats as sweep_f32.
-__host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta) {
-  return size_t(rows_per_cta) * sizeof(float4) + size_t(kWarps * 32 * 33) * sizeof(float);
+__host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta, bool cluster_merge = false) {
+  // (2x', A_i) rows, the per-warp row-sum tiles (+ the row partials of the cluster merge)
+  return size_t(rows_per_cta) * sizeof(float4) + size_t(kWarps * 32 * 33) * sizeof(float) +
+         (cluster_merge ? size_t(rows_per_cta) * sizeof(float2) : 0);
 }
 
 // KP column pairs per lane (2 KP columns, a 64 KP-column warp strip); KP = 8
@@ -562,6 +565,11 @@ __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(Src
 // i + 8 in one iteration (two independent max / CREDUX / MUFU chains in
 // flight). The column constants B'_j live in shared memory ([pair][lane]
 // float2, conflict-free) so the second row's exponents fit in registers.
+// CS > 1: launched in clusters of CS CTAs along the strips; the row partials
+// of the cluster's CS strips are merged through distributed shared memory
+// before they are written (one partial per row per cluster: CS x fewer for
+// the evaluation to read).
+template <int CS>
 __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 src, SweepArgs a) {
   pdl_wait();
   constexpr int KP = kPairs;
@@ -615,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   float mmax = -INFINITY;
   float2* rowp = reinterpret_cast<float2*>(a.rowp);
   float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float2* s_rp = reinterpret_cast<float2*>(reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33);  // [rows]
   float* tslot = tile + lane;
   float my_ms = 0.f;
   int slot = 0;
@@ -627,7 +636,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
-      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+      const float2 part = make_float2((s0 + s1) + (s2 + s3), my_ms);
+      if constexpr (CS > 1) s_rp[ib + int64_t(kWarps) * lane - r0] = part;
+      else rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = part;
     }
     __syncwarp();
   };
@@ -740,6 +751,32 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
     for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
     if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
   }
+  if constexpr (CS > 1) {
+    // merge the cluster's row partials (sum, log2 scale) per row through DSMEM
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int rank = int(cl.block_rank());
+    const int nrows = int(r1 - r0);
+    const int64_t ldc = gridDim.x / CS;
+    const int64_t col = blockIdx.x / CS;
+    for (int lr = rank * kThreads + threadIdx.x; lr < nrows; lr += CS * kThreads) {
+      float2 q[CS];
+#pragma unroll
+      for (int c = 0; c < CS; ++c) q[c] = cl.map_shared_rank(s_rp, c)[lr];
+      float M = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < CS; ++c)
+        if (q[c].x != 0.f) M = fmaxf(M, q[c].y);
+      float S = 0.f;
+      if (M != -INFINITY)
+#pragma unroll
+        for (int c = 0; c < CS; ++c)
+          if (q[c].x != 0.f) S += q[c].x * ex2f(q[c].y - M);
+      rowp[(r0 + lr) * ldc + col] = M == -INFINITY ? make_float2(0.f, 0.f) : make_float2(S, M);
+    }
+    cl.sync();  // keep this CTA's shared memory until every remote read is done
+  }
   if (threadIdx.x == 0) {
     float m = mm[0];
     for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
@@ -778,6 +815,23 @@ inline int pts_pairs() {
     return (k == 2 || k == 4 || k == 6 || k == 8) ? k : 2;  // 2: the two-row 8-pair variant (default)
   }();
   return v;
+}
+
+// Cluster size of the points sweep's row-partial merge ($POTGPU_PTS_CLUSTER:
+// 1, 2, 4, 8): the largest allowed power of two dividing the strips.
+// Default 1 (off): measured on B200 (profiles/cluster_sizes.sh), clusters of
+// 8 / 4 / 2 slow the C3 sweep from 0.106 to 0.168 / 0.161 / 0.110 ms — the
+// one-wave grid no longer fits the GPCs in one wave of co-scheduled clusters
+// — more than the smaller evaluation saves.
+inline int pts_cluster(int64_t strips) {
+  static const int cap = [] {
+    const char* e = std::getenv("POTGPU_PTS_CLUSTER");
+    const int k = e ? std::atoi(e) : 0;
+    return (k == 1 || k == 2 || k == 4 || k == 8) ? k : 1;
+  }();
+  int c = cap;
+  while (c > 1 && strips % c != 0) c >>= 1;
+  return c;
 }
 
 constexpr int64_t kMaxRowsPerCta = 2048;
