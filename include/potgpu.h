@@ -195,7 +195,9 @@ int potgpu_solve_batched(potgpu_ctx* ctx, int solver_kind, const potgpu_problem*
  * begin = validation + setup + the first evaluation (+ record(0));
  * iterate = run until k more iterations are accepted or the solve stops
  * (k < 0: until it stops), device time of that loop in *device_ms;
- * finish = final rounding + outputs (the solve must have stopped).
+ * finish = final rounding + outputs; a session still paused after iterate(k)
+ * finishes exactly like a solve with max_iterations = t (status
+ * MAX_ITERATIONS_EXCEEDED, the plan rounded at the current iterate).
  * potgpu_solve == begin; iterate(-1); finish. */
 typedef struct potgpu_session potgpu_session;
 int potgpu_session_begin(potgpu_ctx* ctx, int solver_kind, const potgpu_problem* problem, const potgpu_config* config,

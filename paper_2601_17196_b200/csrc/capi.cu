@@ -683,7 +683,9 @@ struct AspotSession : Session {
       return;
     }
     AspotCtl& h = *ws.host_ctl;
-    if (h.paused) throw Error(POTGPU_INVALID_ARGUMENT, "session finish before the solve stopped");
+    // a session paused by iterate(k) finishes like a solve with
+    // max_iterations = t: the loop head stopped there (MaxIterationsExceeded)
+    const bool stopped_early = h.paused != 0;
     double tb[4];
     sm->has_bounds = theory_bounds(st.mr, st.mc, P.s, P.cmax, gamma, st.eps_tilde, tb) ? 1 : 0;
     if (sm->has_bounds) { sm->bound_R = tb[0]; sm->bound_L = tb[1]; sm->bound_mu_f = tb[2]; sm->iteration_bound = tb[3]; }
@@ -697,7 +699,7 @@ struct AspotSession : Session {
     sync_ctl();
     pt.mark("final rounding");
     const double wall = secs(t_start);
-    sm->status = h.status;
+    sm->status = stopped_early ? POTGPU_MAX_ITERATIONS_EXCEEDED : h.status;
     sm->iterations = h.t;
     sm->gamma = gamma;
     sm->tolerance = st.eps_tilde;

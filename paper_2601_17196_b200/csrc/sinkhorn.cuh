@@ -457,14 +457,14 @@ struct SinkhornSession : Session {
       fill_trivial(P, trivial_gamma, trivial_plan, sm, out, cfg);
       return;
     }
-    if (hctl->paused) throw Error(POTGPU_INVALID_ARGUMENT, "session finish before the solve stopped");
+    const bool stopped_early = hctl->paused != 0;  // as a solve with max_iterations = it
     DevBuf<double> Xd;
     const bool mat = cfg.materialize_plan && out && out->X;
     if (mat) Xd.alloc(size_t(n * n));
     const PlanResult pr = round_now(mat ? Xd.p : nullptr);
     sync_ctl();
     const double wall = secs(t_start);
-    sm->status = hctl->status;
+    sm->status = stopped_early ? POTGPU_MAX_ITERATIONS_EXCEEDED : hctl->status;
     sm->iterations = hctl->it;
     sm->gamma = gamma;
     sm->tolerance = tol;
