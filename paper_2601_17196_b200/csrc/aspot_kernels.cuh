@@ -69,19 +69,6 @@ __device__ __forceinline__ double theta_next_d(double th) {  // solvers.hpp:32-3
   return th * (sqrt(th * th + 4.0) - th) / 2.0;
 }
 
-// z_bar = (1 - theta) z_check + theta z   (solvers.hpp:336, DualPoint ops dual.hpp:33-43)
-__global__ void k_zbar(AspotCtl* ctl, Slot zc, Slot z, Slot zb) {
-  pdl_wait();
-  if (!ctl->g_new) return;
-  const double th = ctl->theta, om = 1.0 - th;
-  const int64_t n = zb.n;
-  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
-    const double a = om * zc.base[k];
-    const double b = th * z.base[k];
-    zb.base[k] = a + b;
-  }
-}
-
 // Per-point reduction of the sweep partials into B 1, B^T 1 and the scalar
 // partials of every functional the reference evaluates at that point.
 // One launch per point (k_point_eval).
@@ -408,23 +395,6 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
 
 // Commit of an accepted attempt: z <- z_best, z_check <- z_check', sums of
 // z_check <- sums of z_check' (solvers.hpp:357-360). Element-parallel.
-__global__ void k_commit_copy(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, double* rowc, double* colc,
-                              const double* rown, const double* coln) {
-  pdl_wait();
-  if (!ctl->g_active || !ctl->attempt_ok) return;
-  const bool keep = ctl->keep_check;
-  const int64_t n = z.n;
-  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
-    const double zbst = keep ? zc.base[k] : zh.base[k];
-    z.base[k] = zbst;
-    zc.base[k] = zn.base[k];
-    if (k < n) {
-      rowc[k] = rown[k];
-      colc[k] = coln[k];
-    }
-  }
-}
-
 __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double err, double phi) {
   if (ctl->trace_len < ctl->trace_cap) {
     TraceDev& r = trace[ctl->trace_len];
@@ -515,15 +485,10 @@ __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
   loop_head(ctl);
 }
 
-__global__ void k_commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
-  pdl_wait();
-  commit_state(ctl, trace, lg);
-}
-
 // End of a step attempt, one launch: on success z <- z_best, z_check <-
 // z_check', their sums, and already the next iteration's
-// z_bar = (1 - theta') z_check + theta' z (k_zbar's arithmetic with theta' =
-// theta_next(theta)); then the last block to finish takes the scalar
+// z_bar = (1 - theta') z_check + theta' z (solvers.hpp:336 with theta' =
+// theta_next(theta), DualPoint ops dual.hpp:33-43); then the last block to finish takes the scalar
 // decisions of commit_state (halving / record / loop head).
 __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot zb, double* rowc, double* colc,
                          const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, unsigned* ticket) {
