@@ -265,6 +265,15 @@ def main():
                "status": full.status.name, "final_error": full.final_error, "tolerance": full.tolerance,
                "cost": full.cost, "feasibility_gap": full.feasibility_gap}
 
+    # the tuned-Sinkhorn baseline on the same instance (solvers.hpp:547-589, p = 4)
+    tuned = None
+    if not args.no_tte:
+        ts = pot.tuned_sinkhorn_solve(inst, args.epsilon, 4.0, pot.SolverConfig(log_every=10 ** 9, record_rounded_cost=False,
+                                                                             materialize_plan=False), ctx=ctx)
+        tuned = {"seconds": ts.wall_seconds, "loop_seconds": ts.loop_seconds, "iterations": ts.iterations,
+                 "status": ts.status.name, "final_error": ts.final_error, "tolerance": ts.tolerance, "cost": ts.cost,
+                 "feasibility_gap": ts.feasibility_gap, "p": 4.0}
+
     # e2e: the public API from host buffers, K iterations per call
     e2e_cfg = pot.SolverConfig(epsilon=args.epsilon, log_every=10 ** 9, max_iterations=args.steps,
                                record_rounded_cost=False, materialize_plan=False)
@@ -311,7 +320,8 @@ def main():
                         "note": "one public-API call (aspot_solve, max_iterations=K) from host buffers: upload, setup, "
                                 "K iterations, rounding, download"},
                 "gpu_launches": k1 - k0, "sweeps_per_iteration": sweeps_per_it,
-                "roofline": roofline, "roofline_stored": stored, "time_to_eps": tte, "cpu_baseline": cpu}
+                "roofline": roofline, "roofline_stored": stored, "time_to_eps": tte, "tuned_sinkhorn_time_to_eps": tuned,
+                "cpu_baseline": cpu}
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
