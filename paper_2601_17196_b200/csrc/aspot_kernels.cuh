@@ -424,6 +424,7 @@ __device__ void finish(AspotCtl* ctl, int status) {
   ctl->g_active = 0;
   ctl->g_new = 0;
   ctl->g_alive = 0;
+  reset_point_gates(ctl);  // attempt graphs still queued after the stop must do nothing
   ctl->loop_end_ns = globaltimer_ns();
 }
 
@@ -437,6 +438,7 @@ __device__ void loop_head(AspotCtl* ctl) {
     ctl->g_active = 0;
     ctl->g_new = 0;
     ctl->g_alive = 0;
+    reset_point_gates(ctl);
     ctl->loop_end_ns = globaltimer_ns();
     return;
   }

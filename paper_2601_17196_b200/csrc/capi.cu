@@ -575,8 +575,10 @@ struct AspotSession : Session {
     launches += 1;
     // first burst: exactly the iterations asked for (1 attempt each unless a
     // step is halved), then poll every sync_every attempts
-    int64_t burst = stop == INT64_MAX ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, stop - h.t);
-    burst = std::min<int64_t>(burst, 1 << 16);
+    // (a distant stop, e.g. the next record of a large log_every, polls every
+    // sync_every attempts like an unbounded run)
+    int64_t burst = (stop == INT64_MAX || stop - h.t > 4096) ? std::max(1, cfg.sync_every)
+                                                              : std::max<int64_t>(1, stop - h.t);
     while (true) {
       launch_attempts(burst);
       PG_CK(cudaEventRecord(ev1, cx.stream));  // device end of the loop (before the host poll)

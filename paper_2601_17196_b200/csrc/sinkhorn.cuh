@@ -288,8 +288,8 @@ struct SinkhornSession : Session {
   void run_until(int64_t stop) {
     launch_k(k_sk_resume, dim3(1), dim3(1), 0, cx.stream, ctl.p, stop);
     launches += 1;
-    int64_t burst = stop == INT64_MAX ? std::max(1, cfg.sync_every) : std::max<int64_t>(1, stop - hctl->it);
-    burst = std::min<int64_t>(burst, 1 << 16);
+    int64_t burst = (stop == INT64_MAX || stop - hctl->it > 4096) ? std::max(1, cfg.sync_every)
+                                                                   : std::max<int64_t>(1, stop - hctl->it);
     while (true) {
       launch_iterations(burst);
       PG_CK(cudaEventRecord(ev1, cx.stream));
