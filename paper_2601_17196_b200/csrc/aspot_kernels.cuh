@@ -168,12 +168,6 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
   }
 }
 
-// One kernel per evaluated point: a thread per index i combines the
-// sweep's strip / row-block partials (contiguous per index) into (B 1)_i and
-// (B^T 1)_i and forms the per-element terms of every functional the
-// reference evaluates there; blocks reduce them to fixed-order partials, and
-// the last block to finish (atomic ticket) reduces all partials in a fixed
-// order and takes the decision (apply_role). Deterministic, one launch.
 constexpr int kEvalThreads = 128;
 // threads per index of k_point_eval ($POTGPU_EVAL_TPI: 1, 2, 4)
 inline int eval_tpi() {
@@ -189,30 +183,66 @@ inline int eval_tpi() {
 // kTPI threads of a group (thread q takes s = q, q + kTPI, ...). fp32
 // (sum, log2 scale) partials are combined relative to their max with MUFU
 // ex2 and turned into fp64 once: S 2^(M + offset).
+// Lists of up to kTPI * kGroupRegs partials are loaded into registers
+// before the max / sum passes (one L2 round trip instead of one per
+// partial); longer lists stream. Same M, per-thread order and shuffle tree
+// either way -> identical bits.
+constexpr int kGroupRegs = 16;
+
 template <int kTPI>
 __device__ __forceinline__ double group_partial_sum(const double* p, int64_t base, int64_t cnt, int fmt, double offset,
                                                     int q) {
+  const bool regs = cnt <= int64_t(kTPI) * kGroupRegs;
   if (fmt == PF_F64) {
     double s = 0.0;
-    for (int64_t k = q; k < cnt; k += kTPI) s += p[base + k];
+    if (regs) {
+      double x[kGroupRegs];
+#pragma unroll
+      for (int r = 0; r < kGroupRegs; ++r) {
+        const int64_t k = q + int64_t(r) * kTPI;
+        x[r] = k < cnt ? p[base + k] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kGroupRegs; ++r)
+        if (q + int64_t(r) * kTPI < cnt) s += x[r];
+    } else {
+      for (int64_t k = q; k < cnt; k += kTPI) s += p[base + k];
+    }
 #pragma unroll
     for (int o = kTPI / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
   }
   const float2* f = reinterpret_cast<const float2*>(p) + base;
-  float M = -INFINITY;
-  for (int64_t k = q; k < cnt; k += kTPI) {
-    const float2 x = f[k];
-    if (x.x != 0.f) M = fmaxf(M, x.y);
-  }
+  float M = -INFINITY, S = 0.f;
+  if (regs) {
+    float2 x[kGroupRegs];
 #pragma unroll
-  for (int o = kTPI / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float S = 0.f;
-  if (M != -INFINITY)
+    for (int r = 0; r < kGroupRegs; ++r) {
+      const int64_t k = q + int64_t(r) * kTPI;
+      x[r] = k < cnt ? f[k] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int r = 0; r < kGroupRegs; ++r)
+      if (x[r].x != 0.f) M = fmaxf(M, x[r].y);
+#pragma unroll
+    for (int o = kTPI / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (M != -INFINITY)
+#pragma unroll
+      for (int r = 0; r < kGroupRegs; ++r)
+        if (x[r].x != 0.f) S += x[r].x * ex2f(x[r].y - M);
+  } else {
     for (int64_t k = q; k < cnt; k += kTPI) {
       const float2 x = f[k];
-      if (x.x != 0.f) S += x.x * ex2f(x.y - M);
+      if (x.x != 0.f) M = fmaxf(M, x.y);
     }
+#pragma unroll
+    for (int o = kTPI / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (M != -INFINITY)
+      for (int64_t k = q; k < cnt; k += kTPI) {
+        const float2 x = f[k];
+        if (x.x != 0.f) S += x.x * ex2f(x.y - M);
+      }
+  }
 #pragma unroll
   for (int o = kTPI / 2; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
   return M == -INFINITY ? 0.0 : double(S) * exp2(double(M) + offset);

@@ -409,6 +409,32 @@ __host__ __device__ constexpr size_t sweep_pts_smem(int rows_per_cta, bool clust
          (cluster_merge ? size_t(rows_per_cta) * sizeof(float2) : 0);
 }
 
+// Balanced reductions over a lane's KP column pairs (depth log2(2 KP)
+// instead of a 2 KP-long dependency chain).
+template <int KP>
+__device__ __forceinline__ float tree_max2(const float2 (&t)[KP]) {
+  float m[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) m[q] = fmaxf(t[q].x, t[q].y);
+#pragma unroll
+  for (int w = 1; w < KP; w *= 2)
+#pragma unroll
+    for (int q = 0; q + w < KP; q += 2 * w) m[q] = fmaxf(m[q], m[q + w]);
+  return m[0];
+}
+
+template <int KP>
+__device__ __forceinline__ float tree_sum2(const float2 (&t)[KP]) {
+  float2 m[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) m[q] = t[q];
+#pragma unroll
+  for (int w = 1; w < KP; w *= 2)
+#pragma unroll
+    for (int q = 0; q + w < KP; q += 2 * w) m[q] = __fadd2_rn(m[q], m[q + w]);
+  return m[0].x + m[0].y;
+}
+
 // KP column pairs per lane (2 KP columns, a 64 KP-column warp strip); KP = 8
 // matches sweep_f32's map. Fewer pairs -> fewer registers -> more resident
 // warps to cover the per-row dependency chain (profiles/pts_variants.sh).
@@ -503,10 +529,7 @@ __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(Src
       const float2 d = __fadd2_rn(t[q], M2);
       p[q] = make_float2(ex2f(d.x), ex2f(d.y));
     }
-    float2 rs = p[0];
-#pragma unroll
-    for (int q = 1; q < KP; ++q) rs = __fadd2_rn(rs, p[q]);
-    *tslot = rs.x + rs.y;
+    *tslot = tree_sum2<KP>(p);
     tslot += 33;
     if (lane == slot) my_ms = ms;
     if (++slot == 32) {
@@ -645,10 +668,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   // one row's tile slot, column scale update and accumulation
   auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
     const float ms = (m == -INFINITY) ? 0.f : m;
-    float2 rs = p[0];
-#pragma unroll
-    for (int q = 1; q < KP; ++q) rs = __fadd2_rn(rs, p[q]);
-    *tslot = rs.x + rs.y;
+    *tslot = tree_sum2<KP>(p);
     tslot += 33;
     if (lane == slot) my_ms = ms;
     if (++slot == 32) {
@@ -684,12 +704,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
       tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
     }
-    float ma = fmaxf(ta[0].x, ta[0].y), mb = fmaxf(tb[0].x, tb[0].y);
-#pragma unroll
-    for (int q = 1; q < KP; ++q) {
-      ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
-      mb = fmaxf(mb, fmaxf(tb[q].x, tb[q].y));
-    }
+    float ma = tree_max2<KP>(ta), mb = tree_max2<KP>(tb);
     ma = warp_maxf(ma);
     mb = warp_maxf(mb);
     const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
