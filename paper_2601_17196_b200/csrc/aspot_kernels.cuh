@@ -65,6 +65,25 @@ struct AspotCtl {
   RoundOut ro;
 };
 
+// The scalar decisions (apply_role, commit_state) are single-thread code
+// with many dependent reads and writes of the control block; on global
+// memory each is an L2 round trip (measured: ~10 us of a 15 us evaluation
+// with the SMs idle). The deciding block stages the block in shared memory,
+// decides there, and writes it back (same arithmetic, same bits). Only that
+// block touches the control block at that point of the launch.
+constexpr int kCtlWords = int(sizeof(AspotCtl) / sizeof(uint32_t));
+static_assert(sizeof(AspotCtl) % sizeof(uint32_t) == 0, "control block is copied as 32-bit words");
+
+__device__ __forceinline__ void ctl_stage_in(uint32_t* sm, const AspotCtl* ctl) {
+  const uint32_t* g = reinterpret_cast<const uint32_t*>(ctl);
+  for (int k = threadIdx.x; k < kCtlWords; k += blockDim.x) sm[k] = __ldcg(g + k);
+}
+
+__device__ __forceinline__ void ctl_stage_out(AspotCtl* ctl, const uint32_t* sm) {
+  uint32_t* g = reinterpret_cast<uint32_t*>(ctl);
+  for (int k = threadIdx.x; k < kCtlWords; k += blockDim.x) g[k] = sm[k];
+}
+
 __device__ __forceinline__ double theta_next_d(double th) {  // solvers.hpp:32-37
   return th * (sqrt(th * th + 4.0) - th) / 2.0;
 }
@@ -89,6 +108,10 @@ struct ReduceArgs {
   const double* src_row_a; const double* src_col_a; const double* src_w_a; int src_role_a;
   const double* src_row_b; const double* src_col_b; const double* src_w_b; int src_role_b;
   const int* select_b;
+  // deferred decision: write this launch's block partials to scratch and
+  // stop; the next O(n) kernel of the attempt reduces them and decides
+  // (decide_pending), so no block waits on a ticket here
+  int defer;
 };
 
 __device__ __forceinline__ bool is_max_slot(int k) { return k == 1 || k == 2 || k == 11; }
@@ -177,6 +200,38 @@ inline int eval_tpi() {
     return (k == 1 || k == 2 || k == 4) ? k : 4;
   }();
   return v;
+}
+
+// Per-index terms of every functional the reference evaluates at a point
+// (dual.hpp:112-141, solvers.hpp:49-52): B 1 = rb, B^T 1 = cb at z = (u, v, w).
+__device__ __forceinline__ void add_index_terms(double (&acc)[kNumAcc], double rb, double cb, double ui, double vi,
+                                                double rti, double cti) {
+  const double eu = eexp(ui), ev = eexp(vi);
+  acc[0] += rb;
+  acc[1] = nan_max(acc[1], ui);
+  acc[2] = nan_max(acc[2], vi);
+  acc[3] += eu;
+  acc[4] += ev;
+  acc[5] += ui * rti;
+  acc[6] += vi * cti;
+  const double rowf = rb + eu, colf = cb + ev;
+  acc[7] += rho_limit(rti, rowf);
+  acc[8] += rho_limit(cti, colf);
+  acc[9] += fabs(rowf - rti);
+  acc[10] += fabs(colf - cti);
+  acc[12] = fmin(acc[12], rb);
+  acc[13] = fmin(acc[13], cb);
+}
+
+// Grid cap of k_point_eval: $POTGPU_EVAL_BLOCKS_PER_SM (default 2) x SMs.
+// Fewer blocks mean fewer block partials to reduce for the decision; 2 and 4
+// per SM measured equal at C3 / C4, 1 per SM slower (profiles/eval_variants.sh).
+inline int64_t eval_blocks_cap(int num_sms) {
+  static const int v = [] {
+    const char* e = std::getenv("POTGPU_EVAL_BLOCKS_PER_SM");
+    return e ? std::atoi(e) : 0;
+  }();
+  return int64_t(v > 0 ? v : 2) * num_sms;
 }
 
 // Sum of the partials p[base .. base + cnt) of one index, split over the
@@ -293,21 +348,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     if (!live || q != 0) continue;
     a.row_out[i] = rb;
     a.col_out[i] = cb;
-    const double eu = eexp(ui), ev = eexp(vi);
-    acc[0] += rb;
-    acc[1] = nan_max(acc[1], ui);
-    acc[2] = nan_max(acc[2], vi);
-    acc[3] += eu;
-    acc[4] += ev;
-    acc[5] += ui * a.rt[i];
-    acc[6] += vi * a.ct[i];
-    const double rowf = rb + eu, colf = cb + ev;
-    acc[7] += rho_limit(a.rt[i], rowf);
-    acc[8] += rho_limit(a.ct[i], colf);
-    acc[9] += fabs(rowf - a.rt[i]);
-    acc[10] += fabs(colf - a.ct[i]);
-    acc[12] = fmin(acc[12], rb);
-    acc[13] = fmin(acc[13], cb);
+    add_index_terms(acc, rb, cb, ui, vi, a.rt[i], a.ct[i]);
   }
   if (a.mode == 0)
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
@@ -334,93 +375,251 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   };
   block_reduce();
   if (threadIdx.x < kNumAcc) a.scratch[blockIdx.x * (kNumAcc) + threadIdx.x] = sh[threadIdx.x][0];
+  if (a.defer) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const volatile double* sc = a.scratch;
+  __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
+  ctl_stage_in(ctl_sm, ctl);
+  const double* sc = a.scratch;
 #pragma unroll
   for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_init(k);
   for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x)
 #pragma unroll
-    for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_join(k, acc[k], sc[b * (kNumAcc) + k]);
+    for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_join(k, acc[k], __ldcg(sc + b * (kNumAcc) + k));
   __syncthreads();
   block_reduce();
   if (threadIdx.x == 0) {
+    AspotCtl* sctl = reinterpret_cast<AspotCtl*>(ctl_sm);
     double tot[kNumAcc];
 #pragma unroll
     for (int k = 0; k < kNumAcc; ++k) tot[k] = sh[k][0];
     *ticket = 0u;  // ready for the next launch
-    if (a.mode == 1) tot[11] = ctl->ps[useb ? a.src_role_b : a.src_role_a].maxe + dw;  // max exponent shifts by dw
-    apply_role(ctl, role, tot, w, a.mode == 0);
+    if (a.mode == 1) tot[11] = sctl->ps[useb ? a.src_role_b : a.src_role_a].maxe + dw;  // max exponent shifts by dw
+    apply_role(sctl, role, tot, w, a.mode == 0);
   }
+  __syncthreads();
+  ctl_stage_out(ctl, ctl_sm);
+}
+
+// ---------------------------------------------------------------------------
+// Deferred decisions. The per-point evaluations of an attempt (launch_eval
+// with defer = 1) only write their block partials; the O(n) kernel that
+// consumes the point (k_zgrave, k_gk_update, k_commit) reduces them in
+// every block in one fixed order (reduce_partials_wide), and takes the reference's decision at that point (apply_role) on a
+// shared-memory copy of the control block. All blocks see identical inputs,
+// so all copies agree; the block that finishes last (ticket) writes its copy
+// back. No block of an evaluation waits on a ticket, and the decision costs
+// no serial tail.
+struct Pending {
+  const double* eval_part; int eval_nb;  // k_point_eval block partials [eval_nb][kNumAcc]
+  double* gk_part; int gk_nb;            // k_gk_update partials of a w-block point [gridDim.x][kNumAcc]
+  int* flag;                             // non-finite block update seen by some block (solvers.hpp:83-87)
+  unsigned* ticket;
+};
+
+// Fixed-order reduction of [nb][kNumAcc] partials over all threads of the
+// calling block (blockDim.x a multiple of 32): thread t takes rows t and
+// t + blockDim.x (all loads issued before the first join; nb <= 2
+// blockDim.x), then warp trees and warps in order. Result in sh[k][0].
+__device__ void reduce_partials_wide(const double* sc, int nb, double (&sh)[kNumAcc][32]) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  double x0[kNumAcc], x1[kNumAcc];
+  const int b0 = t, b1 = t + blockDim.x;
+#pragma unroll
+  for (int k = 0; k < kNumAcc; ++k) {
+    x0[k] = b0 < nb ? __ldcg(sc + b0 * kNumAcc + k) : acc_init(k);
+    x1[k] = b1 < nb ? __ldcg(sc + b1 * kNumAcc + k) : acc_init(k);
+  }
+#pragma unroll
+  for (int k = 0; k < kNumAcc; ++k) {
+    double x = acc_join(k, x0[k], x1[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = acc_join(k, x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) sh[k][wid] = x;
+  }
+  __syncthreads();
+  if (t < kNumAcc) {
+    double x = sh[t][0];
+    for (int w2 = 1; w2 < nw; ++w2) x = acc_join(t, x, sh[t][w2]);
+    sh[t][0] = x;
+  }
+  __syncthreads();
+}
+
+__device__ void decide_pending(AspotCtl* c, int role, const double* sc, int nb, double w, bool swept) {
+  __shared__ double sh[kNumAcc][32];
+  reduce_partials_wide(sc, nb, sh);
+  if (threadIdx.x == 0) {
+    double tot[kNumAcc];
+#pragma unroll
+    for (int k = 0; k < kNumAcc; ++k) tot[k] = sh[k][0];
+    apply_role(c, role, tot, w, swept);
+  }
+  __syncthreads();
+}
+
+// Block tree of kNumAcc accumulators over blockDim.x (a multiple of 32,
+// at most 1024) threads; result in sh[k][0].
+__device__ void block_reduce_acc(double (&acc)[kNumAcc], double (&sh)[kNumAcc][32]) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kNumAcc; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = acc_join(k, x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) sh[k][wid] = x;
+  }
+  __syncthreads();
+  if (t < kNumAcc) {
+    double x = sh[t][0];
+    for (int w2 = 1; w2 < nw; ++w2) x = acc_join(t, x, sh[t][w2]);
+    sh[t][0] = x;
+  }
+  __syncthreads();
+}
+
+// End of a consuming kernel: the last block (ticket) folds in the
+// non-finite flag, runs `last_fn` on its copy and writes the copy back.
+template <class F>
+__device__ void ctl_finish(AspotCtl* ctl, uint32_t* ctl_sm, const Pending& pd, F last_fn) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(pd.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    AspotCtl* c = reinterpret_cast<AspotCtl*>(ctl_sm);
+    *pd.ticket = 0u;
+    if (pd.flag && __ldcg(pd.flag)) {  // solvers.hpp:83-87: non-finite update -> Overflow
+      c->g_alive = 0;
+      c->g_hat_sweep = c->g_hat_scaled = c->g_new_sweep = c->g_new_scaled = 0;
+      *pd.flag = 0;
+    }
+    last_fn(c);
+  }
+  __syncthreads();
+  ctl_stage_out(ctl, ctl_sm);
+}
+
+__device__ __forceinline__ AspotCtl* ctl_stage(uint32_t* ctl_sm, const AspotCtl* ctl) {
+  ctl_stage_in(ctl_sm, ctl);
+  __syncthreads();
+  return reinterpret_cast<AspotCtl*>(ctl_sm);
 }
 
 // z_next = z_bar - step grad ; z_grave = z_bar + theta (z_next - z)
-// (solvers.hpp:337-339). On a new iteration the gradient of z_bar is formed
-// first (dual.hpp:129-131) and kept for the retries (halving keeps z_bar).
+// (solvers.hpp:337-339). On a new iteration the decision at z_bar (range
+// check) is taken first and the gradient of z_bar formed (dual.hpp:129-131)
+// and kept for the retries (halving keeps z_bar).
 __global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const double* rowb, const double* colb,
-                         const double* rt, const double* ct) {
+                         const double* rt, const double* ct, Pending pd) {
   pdl_wait();
-  if (!ctl->g_alive) return;
-  const int64_t n = zb.n;
-  const int fresh = ctl->g_new;
-  const double step = ctl->step, th = ctl->theta;
-  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
-    double gk;
-    if (fresh) {
-      if (k < n) gk = (rowb[k] + eexp(zb.base[k])) - rt[k];
-      else if (k < 2 * n) gk = (colb[k - n] + eexp(zb.base[k])) - ct[k - n];
-      else gk = ctl->ps[R_BAR].total - ctl->s;
-      g.base[k] = gk;
-    } else {
-      gk = g.base[k];
+  __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
+  AspotCtl* c = ctl_stage(ctl_sm, ctl);
+  const int fresh = c->g_new;
+  if (!fresh && !c->g_alive) return;  // uniform: nothing to decide or update
+  if (fresh) decide_pending(c, R_BAR, pd.eval_part, pd.eval_nb, *zb.w(), true);
+  if (c->g_alive) {
+    const int64_t n = zb.n;
+    const double step = c->step, th = c->theta;
+    for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+      double gk;
+      if (fresh) {
+        if (k < n) gk = (rowb[k] + eexp(zb.base[k])) - rt[k];
+        else if (k < 2 * n) gk = (colb[k - n] + eexp(zb.base[k])) - ct[k - n];
+        else gk = c->ps[R_BAR].total - c->s;
+        g.base[k] = gk;
+      } else {
+        gk = g.base[k];
+      }
+      const double zn = zb.base[k] - step * gk;
+      zg.base[k] = zb.base[k] + th * (zn - z.base[k]);
     }
-    const double zn = zb.base[k] - step * gk;
-    zg.base[k] = zb.base[k] + th * (zn - z.base[k]);
   }
+  ctl_finish(ctl, ctl_sm, pd, [](AspotCtl*) {});
 }
 
 // Exact block minimisation (solvers.hpp:71-88) of src with the B sums of
 // src; dst = src with the chosen block replaced. `which` selects the source:
 // 0 = (src_a, rows_a, ps_a) [z_grave], 1 = z_best (z_check if keep_check
-// else z_hat).
+// else z_hat). First the pending decision at the source point (which = 0:
+// z_grave's Greenkhorn block; which = 1: z_hat's phi, z_best and its block).
+// When the new point is to be scaled rather than swept (block w: B scales
+// by e^dw), its sums (dst_row, dst_col) and the block partials of its
+// functionals are formed here (pd.gk_part), for the next kernel to decide on.
 __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* row_a, const double* col_a, int role_a,
                             Slot src_b, const double* row_b, const double* col_b, int role_b, Slot dst,
-                            const double* rt, const double* ct) {
+                            const double* rt, const double* ct, double* dst_row, double* dst_col, Pending pd) {
   pdl_wait();
-  if (!ctl->g_alive) return;
-  int block;
-  Slot src;
-  const double *rowb, *colb;
-  int role;
+  __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
+  AspotCtl* c = ctl_stage(ctl_sm, ctl);
   if (which == 0) {
-    block = ctl->block_hat; src = src_a; rowb = row_a; colb = col_a; role = role_a;
+    if (!c->g_alive) return;  // uniform: z_grave was not evaluated
+    decide_pending(c, R_GRAVE, pd.eval_part, pd.eval_nb, *src_a.w(), true);
   } else {
-    block = ctl->block_check;
-    const bool keep = ctl->keep_check;
-    src = keep ? src_b : src_a; rowb = keep ? row_b : row_a; colb = keep ? col_b : col_a; role = keep ? role_b : role_a;
+    const bool swept = c->g_hat_sweep, scaled = c->g_hat_scaled;
+    if (!swept && !scaled) return;  // uniform: z_hat was not evaluated
+    decide_pending(c, R_HAT, swept ? pd.eval_part : pd.gk_part, swept ? pd.eval_nb : pd.gk_nb, *src_a.w(), swept);
   }
-  const int64_t n = src.n;
-  bool finite = true;
-  for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
-    double x = src.base[k];
-    if (k < n) {
-      if (block == 0) x = x + (log(rt[k]) - log(rowb[k] + eexp(x)));
-    } else if (k < 2 * n) {
-      if (block == 1) x = x + (log(ct[k - n]) - log(colb[k - n] + eexp(x)));
+  if (c->g_alive) {
+    int block;
+    Slot src;
+    const double *rowb, *colb;
+    int role;
+    if (which == 0) {
+      block = c->block_hat; src = src_a; rowb = row_a; colb = col_a; role = role_a;
     } else {
-      if (block == 2) x = x + (log(ctl->s) - log(ctl->ps[role].total));
+      block = c->block_check;
+      const bool keep = c->keep_check;
+      src = keep ? src_b : src_a; rowb = keep ? row_b : row_a; colb = keep ? col_b : col_a; role = keep ? role_b : role_a;
     }
-    dst.base[k] = x;
-    finite = finite && isfinite(x);
+    const int64_t n = src.n;
+    bool finite = true;
+    for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
+      double x = src.base[k];
+      if (k < n) {
+        if (block == 0) x = x + (log(rt[k]) - log(rowb[k] + eexp(x)));
+      } else if (k < 2 * n) {
+        if (block == 1) x = x + (log(ct[k - n]) - log(colb[k - n] + eexp(x)));
+      } else {
+        if (block == 2) x = x + (log(c->s) - log(c->ps[role].total));
+      }
+      dst.base[k] = x;
+      finite = finite && isfinite(x);
+    }
+    if (!finite) *pd.flag = 1;
+    const bool scaled = which == 0 ? c->g_hat_scaled : c->g_new_scaled;
+    if (scaled) {  // block w: B(dst) = B(src) e^dw, the point's sums and functionals without a sweep
+      const double ws = *src.w();
+      const double wd = ws + (log(c->s) - log(c->ps[role].total));  // = dst.w (same arithmetic as the update)
+      const double dw = wd - ws;
+      const double fs = exp(dw);
+      double acc[kNumAcc];
+#pragma unroll
+      for (int k = 0; k < kNumAcc; ++k) acc[k] = acc_init(k);
+      const double* u = src.u();
+      const double* v = src.v();
+      for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double rb = rowb[i] * fs, cb = colb[i] * fs;
+        dst_row[i] = rb;
+        dst_col[i] = cb;
+        add_index_terms(acc, rb, cb, u[i], v[i], rt[i], ct[i]);
+      }
+      acc[11] = c->ps[role].maxe + dw;  // the max exponent shifts by dw
+      __shared__ double sh[kNumAcc][32];
+      block_reduce_acc(acc, sh);
+      if (threadIdx.x < kNumAcc) pd.gk_part[blockIdx.x * kNumAcc + threadIdx.x] = sh[threadIdx.x][0];
+    }
   }
-  if (!finite) {  // solvers.hpp:83-87: non-finite update -> Overflow
-    ctl->g_alive = 0;
-    ctl->g_hat_sweep = ctl->g_hat_scaled = ctl->g_new_sweep = ctl->g_new_scaled = 0;
-  }
+  ctl_finish(ctl, ctl_sm, pd, [](AspotCtl*) {});
 }
 
 // Commit of an accepted attempt: z <- z_best, z_check <- z_check', sums of
@@ -523,12 +722,17 @@ __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
 // theta_next(theta), DualPoint ops dual.hpp:33-43); then the last block to finish takes the scalar
 // decisions of commit_state (halving / record / loop head).
 __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot zb, double* rowc, double* colc,
-                         const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, unsigned* ticket) {
+                         const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, Pending pd) {
   pdl_wait();
-  if (!ctl->g_active) return;  // uniform over the grid
-  if (ctl->attempt_ok) {
-    const bool keep = ctl->keep_check;
-    const double th = theta_next_d(ctl->theta), om = 1.0 - th;
+  __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
+  AspotCtl* c = ctl_stage(ctl_sm, ctl);
+  if (!c->g_active) return;  // uniform over the grid
+  const bool swept = c->g_new_sweep, scaled = c->g_new_scaled;
+  if (swept || scaled)  // decision at z_check' (solvers.hpp:345-352)
+    decide_pending(c, R_NEW, swept ? pd.eval_part : pd.gk_part, swept ? pd.eval_nb : pd.gk_nb, *zn.w(), swept);
+  if (c->attempt_ok) {
+    const bool keep = c->keep_check;
+    const double th = theta_next_d(c->theta), om = 1.0 - th;
     const int64_t n = z.n;
     for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
       const double zbst = keep ? zc.base[k] : zh.base[k];
@@ -544,17 +748,7 @@ __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot 
       }
     }
   }
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    *ticket = 0u;
-    commit_state(ctl, trace, lg);
-  }
+  ctl_finish(ctl, ctl_sm, pd, [&](AspotCtl* cc) { commit_state(cc, trace, lg); });
 }
 
 // Initial state after the first phi/grad evaluation at z_check = 0.

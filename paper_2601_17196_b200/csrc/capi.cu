@@ -424,7 +424,7 @@ struct AspotSession : Session {
   Setup st;
   cudaGraphExec_t exec = nullptr;
   int64_t trace_cap = 1, log_cap = 0;
-  static constexpr int64_t kKernelsPerAttempt = 16;
+  static constexpr int64_t kKernelsPerAttempt = 12;
   int64_t graph_nodes = kKernelsPerAttempt;
   explicit AspotSession(Context& c) : Session(c) {}
   ~AspotSession() override {
@@ -437,38 +437,32 @@ struct AspotSession : Session {
     AspotCtl* ctl = ws.ctl.p;
     const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
                ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
-    const int gv = ws.nblk;
+    const int gv = ws.gv;
     // z_bar of a new iteration was formed by the previous attempt's k_commit
-    // (0 at the start: z = z_check = 0)
-    const SweepOut none{};
-    launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new);
-    launch_k(k_zgrave, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p, ws.ct.p);
+    // (0 at the start: z = z_check = 0). Each evaluation defers its decision
+    // to the O(n) kernel that follows it (Pending, aspot_kernels.cuh).
+    const Pending pd = pending_of(ws);
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new,
+                nullptr, true);
+    launch_k(k_zgrave, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p,
+             ws.ct.p, pd);
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma), ZG, R_GRAVE,
-                &ctl->g_alive);
-    launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZG,
-                                                   ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p);
-    // z_hat: a sweep, or (block w, ~all iterations) B(z_grave) scaled by e^dw
+                &ctl->g_alive, nullptr, true);
+    // decides z_grave's block; forms z_hat, and when z_hat only differs in w
+    // (~all iterations) also its scaled sums B(z_grave) e^dw and functionals
+    launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE,
+             ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p, ws.row(R_HAT), ws.col(R_HAT), pd);
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma), ZH, R_HAT,
-                &ctl->g_hat_sweep);
-    {
-      ReduceArgs sc{};
-      sc.src_row_a = ws.row(R_GRAVE); sc.src_col_a = ws.col(R_GRAVE); sc.src_w_a = ZG.w(); sc.src_role_a = R_GRAVE;
-      launch_eval(cx, ws, none, ZH, R_HAT, &ctl->g_hat_scaled, &sc);
-    }
+                &ctl->g_hat_sweep, nullptr, true);
+    // decides z_hat (phi, z_best, its block); forms z_check' = GK(z_best)
+    // (scaled sums and functionals when its block is w)
     launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
-                                                   ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p);
-    // z_check' = GK(z_best): a sweep, or (block w) B(z_best) scaled
+             ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p, ws.row(R_NEW), ws.col(R_NEW), pd);
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma), ZN, R_NEW,
-                &ctl->g_new_sweep);
-    {
-      ReduceArgs sc{};
-      sc.src_row_a = ws.row(R_HAT); sc.src_col_a = ws.col(R_HAT); sc.src_w_a = ZH.w(); sc.src_role_a = R_HAT;
-      sc.src_row_b = ws.row(R_CHECK); sc.src_col_b = ws.col(R_CHECK); sc.src_w_b = ZC.w(); sc.src_role_b = R_CHECK;
-      sc.select_b = &ctl->keep_check;
-      launch_eval(cx, ws, none, ZN, R_NEW, &ctl->g_new_scaled, &sc);
-    }
+                &ctl->g_new_sweep, nullptr, true);
+    // decides z_check' and commits the attempt
     launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
-             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, ws.ticket.p + 1);
+             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd);
     PG_CK(cudaGetLastError());
   }
 

@@ -93,6 +93,7 @@ struct Workspace {
   int64_t nmax = 0;               // max-exponent slots (CTAs of a full sweep)
   int pts_cs = 1;                 // cluster size of the points sweep's row-partial merge
   int nblk = 0;  // O(n) kernel grid
+  int gv = 0;    // grid of the ASPOT attempt's O(n) kernels (one element of 2n + 1 per thread, <= 2 per SM)
   int eval_blocks = 0;  // k_point_eval grid (8 indices per block)
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
   int strip = 256;
@@ -100,6 +101,8 @@ struct Workspace {
   DevBuf<double> slots;     // 7 dual points
   DevBuf<double> sums;      // 6 x (row, col)
   DevBuf<double> rowp, colp, maxp, scratch, partial;
+  DevBuf<double> dpart, gpart;  // deferred-decision partials: k_point_eval (defer) / k_gk_update (scaled point)
+  DevBuf<int> gflag;            // non-finite Greenkhorn update seen (k_gk_update)
   DevBuf<double> rt, ct;    // marginals the dual targets
   DevBuf<double> ro_buf;    // rounding vectors: rho, kappa, lu, lv, rowx, colx, a, b, row_slack, col_slack
   DevBuf<double> ro_r, ro_c;  // original marginals for rounding
@@ -191,10 +194,17 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.rowp.alloc(size_t(2 * ws.g.grid.x * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * max_rb * n));
   ws.maxp.alloc(size_t(ws.g.grid.x * max_rb));
-  ws.eval_blocks = int(std::min<int64_t>(ceil_div(n * eval_tpi(), kEvalThreads), 4096));
+  // <= 2 kVecThreads: the deferred decisions reduce at most two partial rows per thread
+  ws.eval_blocks = int(std::min<int64_t>(std::min<int64_t>(ceil_div(n * eval_tpi(), kEvalThreads), eval_blocks_cap(cx.num_sms)),
+                                         2 * kVecThreads));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
-  ws.ticket.alloc(2);  // [0] k_point_eval, [1] k_commit
+  ws.ticket.alloc(2);  // [0] k_point_eval, [1] the attempt's O(n) kernels (k_zgrave, k_gk_update, k_commit)
   ws.ticket.zero(cx.stream);
+  ws.dpart.alloc(size_t(kNumAcc * ws.eval_blocks));
+  ws.gv = int(std::min<int64_t>(2 * cx.num_sms, ceil_div(2 * n + 1, kVecThreads)));
+  ws.gpart.alloc(size_t(kNumAcc * ws.gv));
+  ws.gflag.alloc(1);
+  ws.gflag.zero(cx.stream);
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n) + ws.nshards * ceil_div(n, kThreads))));
   ws.rt.alloc(size_t(n));
   ws.ct.alloc(size_t(n));
@@ -314,7 +324,7 @@ inline double allreduce_host_sum(Context& cx, Workspace& ws, double x) {
 
 // The per-point evaluation (partials -> B 1, B^T 1, scalars, decision).
 inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, int role, const int* gate,
-                        const ReduceArgs* scaled = nullptr) {
+                        const ReduceArgs* scaled = nullptr, bool defer = false) {
   ReduceArgs r{};
   if (scaled) r = *scaled;
   r.z = z;
@@ -323,7 +333,8 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.maxp = so.maxp; r.nmax = so.nmax;
   r.row_out = ws.row(role); r.col_out = ws.col(role);
   r.rt = ws.rt.p; r.ct = ws.ct.p;
-  r.scratch = ws.scratch.p;
+  r.scratch = defer ? ws.dpart.p : ws.scratch.p;
+  r.defer = defer ? 1 : 0;
   r.gate = gate;
   r.pfmt = so.pfmt;
   r.rowshift = so.rowshift;
@@ -334,6 +345,18 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
     default: launch_k(k_point_eval<4>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
   }
   PG_CK(cudaGetLastError());
+}
+
+// Where an attempt's deferred decisions find their partials (aspot_kernels.cuh Pending).
+inline Pending pending_of(Workspace& ws) {
+  Pending pd;
+  pd.eval_part = ws.dpart.p;
+  pd.eval_nb = ws.eval_blocks;
+  pd.gk_part = ws.gpart.p;
+  pd.gk_nb = ws.gv;
+  pd.flag = ws.gflag.p;
+  pd.ticket = ws.ticket.p + 1;
+  return pd;
 }
 
 }  // namespace potgpu
