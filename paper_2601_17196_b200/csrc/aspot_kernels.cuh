@@ -56,6 +56,7 @@ struct AspotCtl {
   int g_hat_sweep, g_hat_scaled, g_new_sweep, g_new_scaled;
   int clamp_guard;  // fp64 (Eigen-clamped exp) problems: scale only far above the clamp floor
   int64_t pause_at;
+  int64_t loop_budget;  // attempts the device loop (graph WHILE node) may still run in this launch
   int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
   int64_t trace_len, trace_cap, log_len, log_cap;
   double theta, step, gamma, eps_tilde, step_denom, s;
@@ -674,9 +675,10 @@ __device__ void loop_head(AspotCtl* ctl) {
   begin_iteration(ctl);
 }
 
-__global__ void k_resume(AspotCtl* ctl, int64_t pause_at) {
+__global__ void k_resume(AspotCtl* ctl, int64_t pause_at, int64_t budget) {
   pdl_wait();
   ctl->pause_at = pause_at;
+  ctl->loop_budget = budget;
   if (!ctl->paused) return;
   ctl->paused = 0;
   ctl->g_active = 1;
@@ -721,12 +723,20 @@ __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
 // z_bar = (1 - theta') z_check + theta' z (solvers.hpp:336 with theta' =
 // theta_next(theta), DualPoint ops dual.hpp:33-43); then the last block to finish takes the scalar
 // decisions of commit_state (halving / record / loop head).
+// In the device loop (a CUDA-graph WHILE node around the attempt, `loop`
+// = its condition handle) the deciding block also tells the graph whether
+// to run another attempt: while the solve is active and the launch's
+// attempt budget lasts.
 __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot zb, double* rowc, double* colc,
-                         const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, Pending pd) {
+                         const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, Pending pd,
+                         cudaGraphConditionalHandle loop, int in_loop) {
   pdl_wait();
   __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
   AspotCtl* c = ctl_stage(ctl_sm, ctl);
-  if (!c->g_active) return;  // uniform over the grid
+  if (!c->g_active) {  // uniform over the grid
+    if (in_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
+    return;
+  }
   const bool swept = c->g_new_sweep, scaled = c->g_new_scaled;
   if (swept || scaled)  // decision at z_check' (solvers.hpp:345-352)
     decide_pending(c, R_NEW, swept ? pd.eval_part : pd.gk_part, swept ? pd.eval_nb : pd.gk_nb, *zn.w(), swept);
@@ -748,7 +758,13 @@ __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot 
       }
     }
   }
-  ctl_finish(ctl, ctl_sm, pd, [&](AspotCtl* cc) { commit_state(cc, trace, lg); });
+  ctl_finish(ctl, ctl_sm, pd, [&](AspotCtl* cc) {
+    commit_state(cc, trace, lg);
+    if (in_loop) {
+      cc->loop_budget -= 1;
+      cudaGraphSetConditional(loop, (cc->g_active && cc->loop_budget > 0) ? 1u : 0u);
+    }
+  });
 }
 
 // Initial state after the first phi/grad evaluation at z_check = 0.

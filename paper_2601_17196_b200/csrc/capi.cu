@@ -8,6 +8,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 
 #include "engine.cuh"
 #include "plan.cuh"
@@ -17,7 +18,8 @@ namespace potgpu {
 thread_local std::string g_last_error;
 
 // ------------------------------------------------------------------ setup --
-__global__ void k_dense_prepare(const double* __restrict__ src, int64_t n, int64_t ldc, int row_major, int64_t ld,
+template <class S>
+__global__ void k_dense_prepare(const S* __restrict__ src, int64_t n, int64_t ldc, int row_major, int64_t ld,
                                 double* C64, float* C32, unsigned long long* flags) {
   // flags[0]: non-finite, flags[1]: negative, flags[2]: max (bit pattern, >= 0 values)
   const int64_t total = n * ld;
@@ -27,7 +29,7 @@ __global__ void k_dense_prepare(const double* __restrict__ src, int64_t n, int64
     double x = 0.0;
     if (j < n) {
       if (!src) x = double(C32[k]);  // rescan of an already stored fp32 matrix
-      else x = row_major ? src[i * ldc + j] : src[i + j * ldc];
+      else x = double(row_major ? src[i * ldc + j] : src[i + j * ldc]);
       if (C32) x = double(float(x));  // fp32 instances: every semantic on the rounded value
       if (!isfinite(x)) nf = 1;
       else if (x < 0) neg = 1;
@@ -73,6 +75,38 @@ __global__ void k_points_store(const float4* X, const float4* Y, int64_t n, int6
   }
 }
 
+// Host dense cost -> device through two pinned staging chunks (the copy of
+// chunk k + 1 into pinned memory overlaps the DMA of chunk k). fp32
+// instances are rounded to float on the host (every semantic of an fp32
+// instance is on the rounded value, k_dense_prepare), halving the bytes over
+// the link. Each batched worker stages its own problems, so uploads proceed
+// in parallel instead of through the driver's pageable-copy path one at a
+// time (configs[4]: 256 x 33.5 MB).
+template <class T>
+static void upload_dense_host(Context& cx, const double* C, int64_t count, T* dst) {
+  constexpr int64_t kChunk = int64_t(1) << 20;  // elements per staging chunk
+  void* stage[2] = {BlockCache::get().alloc(kChunk * sizeof(T), true), BlockCache::get().alloc(kChunk * sizeof(T), true)};
+  cudaEvent_t ev[2];
+  PG_CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  PG_CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  for (int64_t off = 0, k = 0; off < count; off += kChunk, ++k) {
+    const int b = int(k & 1);
+    const int64_t m = std::min(kChunk, count - off);
+    if (k >= 2) PG_CK(cudaEventSynchronize(ev[b]));
+    T* h = static_cast<T*>(stage[b]);
+    if constexpr (std::is_same<T, double>::value) std::memcpy(h, C + off, size_t(m) * sizeof(double));
+    else for (int64_t e = 0; e < m; ++e) h[e] = float(C[off + e]);
+    PG_CK(cudaMemcpyAsync(dst + off, h, size_t(m) * sizeof(T), cudaMemcpyHostToDevice, cx.stream));
+    PG_CK(cudaEventRecord(ev[b], cx.stream));
+  }
+  PG_CK(cudaEventSynchronize(ev[0]));
+  PG_CK(cudaEventSynchronize(ev[1]));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  BlockCache::get().free(stage[0], kChunk * sizeof(T), true);
+  BlockCache::get().free(stage[1], kChunk * sizeof(T), true);
+}
+
 static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P) {
   if (!pr) throw Error(POTGPU_INVALID_ARGUMENT, "null problem");
   const int64_t n = pr->n;
@@ -103,19 +137,24 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     if (!pr->C) throw Error(POTGPU_DIMENSION_MISMATCH, "invalid instance: cost matrix missing");
     const int64_t ldc = pr->ldc > 0 ? pr->ldc : n;
     DevBuf<double> raw;
-    const double* src = pr->C;  // device_ptrs: read in place
-    if (!dev) {
-      raw.alloc(size_t(n * ldc));
-      PG_CK(cudaMemcpyAsync(raw.p, pr->C, size_t(n * ldc) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
-      src = raw.p;
-    }
+    DevBuf<float> raw32;
     DevBuf<unsigned long long> flags;
     flags.alloc(3);
     flags.zero(cx.stream);
     if (pr->dtype == POTGPU_F64) P.C64.alloc(size_t(n * P.ld)); else P.C32.alloc(size_t(n * P.ld));
-    k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(src, n, ldc, pr->row_major, P.ld,
-                                                          pr->dtype == POTGPU_F64 ? P.C64.p : nullptr,
-                                                          pr->dtype == POTGPU_F32 ? P.C32.p : nullptr, flags.p);
+    double* c64 = pr->dtype == POTGPU_F64 ? P.C64.p : nullptr;
+    float* c32 = pr->dtype == POTGPU_F32 ? P.C32.p : nullptr;
+    if (dev) {  // device_ptrs: read in place
+      k_dense_prepare<double><<<cx.num_sms * 8, 256, 0, cx.stream>>>(pr->C, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
+    } else if (pr->dtype == POTGPU_F32) {
+      raw32.alloc(size_t(n * ldc));
+      upload_dense_host<float>(cx, pr->C, n * ldc, raw32.p);
+      k_dense_prepare<float><<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw32.p, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
+    } else {
+      raw.alloc(size_t(n * ldc));
+      upload_dense_host<double>(cx, pr->C, n * ldc, raw.p);
+      k_dense_prepare<double><<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw.p, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
+    }
     PG_CK(cudaGetLastError());
     unsigned long long hf[3];
     PG_CK(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, cx.stream));
@@ -182,7 +221,7 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
         DevBuf<unsigned long long> m2;
         m2.alloc(3);
         m2.zero(cx.stream);
-        k_dense_prepare<<<cx.num_sms * 8, 256, 0, cx.stream>>>(nullptr, n, P.ld, 2, P.ld, nullptr, P.C32.p, m2.p);
+        k_dense_prepare<float><<<cx.num_sms * 8, 256, 0, cx.stream>>>(static_cast<const float*>(nullptr), n, P.ld, 2, P.ld, nullptr, P.C32.p, m2.p);
         unsigned long long hf[3];
         PG_CK(cudaMemcpyAsync(hf, m2.p, sizeof(hf), cudaMemcpyDeviceToHost, cx.stream));
         PG_CK(cudaStreamSynchronize(cx.stream));
@@ -422,7 +461,8 @@ struct AspotSession : Session {
   Workspace ws;
   double gamma = 0;
   Setup st;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec = nullptr;       // one step attempt (host-launched per attempt)
+  cudaGraphExec_t loop_exec = nullptr;  // the attempt inside a WHILE node: the whole loop in one launch
   int64_t trace_cap = 1, log_cap = 0;
   static constexpr int64_t kKernelsPerAttempt = 12;
   int64_t graph_nodes = kKernelsPerAttempt;
@@ -430,10 +470,51 @@ struct AspotSession : Session {
   ~AspotSession() override {
     cudaStreamSynchronize(cx.stream);  // before any buffer returns to the cache
     if (exec) cudaGraphExecDestroy(exec);
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+  }
+
+  // The device loop: a graph whose WHILE node runs the attempt until
+  // k_commit clears the condition (solve stopped or paused, or the
+  // launch's attempt budget spent). One host launch per run instead of one
+  // per attempt (the host launch rate bounds small problems, and batched
+  // solves whose workers share the driver). Returns false (no loop graph)
+  // when the driver refuses conditional nodes.
+  bool build_loop_graph() {
+    cudaGraph_t g = nullptr;
+    if (cudaGraphCreate(&g, 0) != cudaSuccess) { cudaGetLastError(); return false; }
+    cudaGraphConditionalHandle h;
+    cudaGraphNodeParams cp = {};
+    cudaGraphNode_t node;
+    bool ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+    if (ok) {
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+    }
+    if (ok) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      ok = cudaStreamBeginCaptureToGraph(cx.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+           cudaSuccess;
+      if (ok) {
+        enqueue_attempt(h, 1);
+        ok = cudaStreamEndCapture(cx.stream, &body) == cudaSuccess;
+        size_t nodes = 0;
+        if (ok && cudaGraphGetNodes(body, nullptr, &nodes) == cudaSuccess) graph_nodes = int64_t(nodes);
+      }
+    }
+    if (ok) ok = cudaGraphInstantiate(&loop_exec, g, 0) == cudaSuccess;
+    cudaGraphDestroy(g);
+    if (!ok) {
+      cudaGetLastError();
+      loop_exec = nullptr;
+    }
+    return ok;
   }
 
   // One step attempt of the halving loop (solvers.hpp:334-352) + commit.
-  void enqueue_attempt() {
+  void enqueue_attempt(cudaGraphConditionalHandle loop = 0, int in_loop = 0) {
     AspotCtl* ctl = ws.ctl.p;
     const Slot Z = ws.slot(S_Z), ZC = ws.slot(S_ZC), ZB = ws.slot(S_ZB), G = ws.slot(S_G), ZG = ws.slot(S_ZG),
                ZH = ws.slot(S_ZH), ZN = ws.slot(S_ZN);
@@ -462,7 +543,7 @@ struct AspotSession : Session {
                 &ctl->g_new_sweep, nullptr, true);
     // decides z_check' and commits the attempt
     launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
-             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd);
+             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd, loop, in_loop);
     PG_CK(cudaGetLastError());
   }
 
@@ -540,7 +621,8 @@ struct AspotSession : Session {
     if (h.fatal) throw Error(h.fatal, "Overflow: B(z) exponent exceeds representable range at z = 0");
     if (cfg.record_rounded_cost && h.g_active) fill_last_record_cost(round_now(nullptr).cost);
     pt.mark("record(0) rounding");
-    if (cfg.use_graphs) {
+    if (cfg.use_graphs && graph_loop_enabled()) build_loop_graph();
+    if (cfg.use_graphs && !loop_exec) {
       cudaGraph_t graph;
       PG_CK(cudaStreamBeginCapture(cx.stream, cudaStreamCaptureModeThreadLocal));
       enqueue_attempt();
@@ -565,7 +647,23 @@ struct AspotSession : Session {
   // Device loop until it pauses at `stop` or the solve stops.
   void run_until(int64_t stop) {
     AspotCtl& h = *ws.host_ctl;
-    launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop);
+    if (loop_exec) {
+      while (true) {
+        // an accepted iteration takes at most 61 attempts (solvers.hpp:334):
+        // the budget only bounds a launch, the solve stops the loop first
+        const int64_t left = std::max<int64_t>(1, std::min(stop, h.max_iterations) - h.t);
+        const int64_t budget = left > (int64_t(1) << 34) ? (int64_t(1) << 40) : 64 * left + 64;
+        const int64_t a0 = h.attempts;
+        launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop, budget);
+        PG_CK(cudaGraphLaunch(loop_exec, cx.stream));
+        PG_CK(cudaEventRecord(ev1, cx.stream));  // device end of the loop (before the host poll)
+        sync_ctl();
+        launches += 1 + (h.attempts - a0) * graph_nodes;
+        if (!h.g_active || h.fatal) break;
+      }
+      return;
+    }
+    launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop, int64_t(0));
     launches += 1;
     // first burst: exactly the iterations asked for (1 attempt each unless a
     // step is halved), then poll every sync_every attempts
@@ -874,6 +972,11 @@ int potgpu_solve_batched(potgpu_ctx* c, int kind, const potgpu_problem* problems
     for (int t = 0; t < workers; ++t) {
       pool.emplace_back([&] {
         Context cx = c->cx;
+        // each worker plans its grids for its share of the SMs, so the
+        // workers' sweeps run side by side instead of each filling the GPU
+        // for a few microseconds in turn (profiles/c5_batched.py)
+        cx.num_sms = std::max(1, c->cx.num_sms / workers);
+        tl_no_pdl = true;
         try {
           PG_CK(cudaSetDevice(cx.device));
           PG_CK(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));

@@ -154,10 +154,28 @@ class BlockCache {
 // $POTGPU_PDL (default on): launch the per-iteration kernels with
 // programmatic stream serialization (captured as programmatic edges in the
 // CUDA graphs), hiding the launch latency between dependent kernels.
+// Worker threads of a batched solve turn PDL off for their launches: with
+// several streams in flight, early-launched dependents hold SM slots while
+// they wait and the streams' kernels overlap worse (measured at configs[4]:
+// 118 vs 70 problems/s at 8 workers, profiles/c5_batched.py).
+inline thread_local bool tl_no_pdl = false;
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("POTGPU_PDL");
     return !(e && e[0] == '0');
+  }();
+  return on && !tl_no_pdl;
+}
+
+// $POTGPU_GRAPH_LOOP=1: run the ASPOT loop as a CUDA-graph WHILE node (one
+// host launch per run) instead of one graph launch per attempt. Off by
+// default: measured equal on one stream (C3 2584 vs 2592 it/s; the host
+// launches run ahead of the GPU) and slower with concurrent batched workers
+// (54-59 vs 118 problems/s at configs[4]).
+inline bool graph_loop_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_GRAPH_LOOP");
+    return e && e[0] == '1';
   }();
   return on;
 }

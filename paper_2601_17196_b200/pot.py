@@ -660,7 +660,10 @@ def solve(inst: Instance, kind: SolverKind, config: SolverConfig = SolverConfig(
 def solve_batched(kind: SolverKind, instances: List[Instance], config: SolverConfig = SolverConfig(),
                   ctx: Optional[Context] = None, concurrency: int = 8, trace_cap: int = 16) -> List[SolveResult]:
     """Independent problems solved concurrently (potgpu_solve_batched;
-    BASELINE configs[4]). Same per-problem results as `solve`."""
+    BASELINE configs[4]). Each of the `concurrency` workers plans its grids
+    for its share of the SMs, so per-problem results agree with `solve` to
+    rounding (different reduction grouping) and are deterministic for a given
+    concurrency."""
     lib = load_library()
     ctx = ctx or default_context()
     keep: list = []

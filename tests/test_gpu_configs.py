@@ -190,3 +190,17 @@ def test_c5_batched_problems_match_oracle(ctx):
             assert abs(g.cost - o.cost) <= TOL_F32_OBJ * abs(o.cost)
             assert abs(g.iterations - o.iterations) <= max(3, 0.05 * o.iterations)
             check_properties(g, inst.s, TOL_F32_VIOL)
+
+
+def test_batched_matches_single_solves(ctx):
+    """potgpu_solve_batched (workers on SM shares, own streams) against one
+    solve per problem: fp64 decisions, iteration counts and statuses equal,
+    costs to rounding."""
+    insts = [pot.config_instance(1, n=300, seed=10 + k) for k in range(6)]
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10 ** 9, materialize_plan=False)
+    for kind in (pot.SolverKind.Aspot, pot.SolverKind.FeasibleSinkhorn):
+        res = pot.solve_batched(kind, insts, cfg, ctx=ctx, concurrency=3)
+        for inst, b in zip(insts, res):
+            g = pot.solve(inst, kind, cfg, ctx=ctx)
+            assert b.status == g.status and b.iterations == g.iterations, (kind, b.iterations, g.iterations)
+            assert abs(b.cost - g.cost) <= 1e-9 * abs(g.cost)
