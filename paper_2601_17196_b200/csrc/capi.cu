@@ -147,12 +147,13 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     if (dev) {  // device_ptrs: read in place
       k_dense_prepare<double><<<cx.num_sms * 8, 256, 0, cx.stream>>>(pr->C, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
     } else if (pr->dtype == POTGPU_F32) {
+      // the last row / column ends at (n - 1) ldc + n: nothing past it is read
       raw32.alloc(size_t(n * ldc));
-      upload_dense_host<float>(cx, pr->C, n * ldc, raw32.p);
+      upload_dense_host<float>(cx, pr->C, (n - 1) * ldc + n, raw32.p);
       k_dense_prepare<float><<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw32.p, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
     } else {
       raw.alloc(size_t(n * ldc));
-      upload_dense_host<double>(cx, pr->C, n * ldc, raw.p);
+      upload_dense_host<double>(cx, pr->C, (n - 1) * ldc + n, raw.p);
       k_dense_prepare<double><<<cx.num_sms * 8, 256, 0, cx.stream>>>(raw.p, n, ldc, pr->row_major, P.ld, c64, c32, flags.p);
     }
     PG_CK(cudaGetLastError());

@@ -444,6 +444,27 @@ def _problem_device(inst: Instance, keep: list) -> _Problem:
     return p
 
 
+def _dense_layout(C, n: int):
+    """(array, ldc, row_major) of a float64 n x n cost without a copy when its
+    layout is one the C-ABI reads directly: C order, Fortran order (Eigen's
+    column-major MatrixXd), or a row / column view with a padded leading
+    dimension (e.g. C[:n, :n] of a wider array); anything else is copied."""
+    C = np.asarray(C)
+    if C.shape != (n, n):
+        raise PotError(ErrorCode.DimensionMismatch, f"cost matrix is {C.shape}, expected {(n, n)}")
+    if C.dtype == np.float64 and n > 0:
+        s0, s1 = C.strides
+        if C.flags.c_contiguous:
+            return C, n, 1
+        if C.flags.f_contiguous:
+            return C, n, 0
+        if s1 == 8 and s0 > 0 and s0 % 8 == 0 and s0 // 8 >= n:
+            return C, s0 // 8, 1
+        if s0 == 8 and s1 > 0 and s1 % 8 == 0 and s1 // 8 >= n:
+            return C, s1 // 8, 0
+    return np.ascontiguousarray(C, dtype=np.float64), n, 1
+
+
 def _problem(inst: Instance, keep: list) -> _Problem:
     if _is_cuda(inst.r):
         return _problem_device(inst, keep)
@@ -456,11 +477,10 @@ def _problem(inst: Instance, keep: list) -> _Problem:
     keep += [r, c]
     p.r, p.c, p.s = _dp(r), _dp(c), float(inst.s)
     if inst.C is not None:
-        C = np.ascontiguousarray(inst.C, dtype=np.float64)
-        if C.shape != (n, n):
-            raise PotError(ErrorCode.DimensionMismatch, f"cost matrix is {C.shape}, expected {(n, n)}")
+        C, ldc, row_major = _dense_layout(inst.C, n)
         keep.append(C)
-        p.cost_kind, p.C, p.ldc, p.row_major = 0, _dp(C), n, 1
+        p.cost_kind, p.C, p.ldc, p.row_major = 0, ctypes.cast(ctypes.c_void_p(C.ctypes.data),
+                                                             ctypes.POINTER(ctypes.c_double)), ldc, row_major
     else:
         X = np.ascontiguousarray(inst.X, dtype=np.float64)
         Y = np.ascontiguousarray(inst.Y, dtype=np.float64)

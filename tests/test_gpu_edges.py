@@ -96,3 +96,25 @@ def test_max_iterations_one_and_session_pause(ctx):
     b = pot.aspot_solve(inst, pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, max_iterations=done,
                                                materialize_plan=False, record_rounded_cost=False), ctx=ctx)
     assert a.final_error == b.final_error and a.cost == b.cost
+
+
+@pytest.mark.parametrize("dtype", [pot.DType.F64, pot.DType.F32])
+def test_dense_layouts_give_identical_solves(ctx, dtype):
+    """The dense cost read from C order, Fortran order (Eigen's column-major
+    MatrixXd) and padded row / column views (leading dimension > n): the
+    device sees the same values, so the solves agree bit for bit. n x ldc
+    spans more than one pinned staging chunk, the last one partial."""
+    n = 1100
+    base = pot.config_instance(1, n=n, seed=4, dtype=dtype)
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10 ** 9, max_iterations=60)
+    ref = pot.aspot_solve(base, cfg, ctx=ctx)
+    wide = np.full((n, n + 37), np.nan)
+    wide[:, :n] = base.C
+    tall = np.full((n + 11, n), np.nan)
+    tall[:n, :] = base.C
+    for C in (np.asfortranarray(base.C), wide[:, :n], np.asfortranarray(tall)[:n, :]):
+        inst = pot.Instance(r=base.r, c=base.c, s=base.s, C=C, dtype=dtype)
+        g = pot.aspot_solve(inst, cfg, ctx=ctx)
+        assert g.iterations == ref.iterations and g.status == ref.status
+        assert g.cost == ref.cost and g.final_error == ref.final_error
+        assert np.array_equal(g.plan.row_slack, ref.plan.row_slack)
