@@ -432,8 +432,8 @@ __device__ void reduce_partials_wide(const double* sc, int nb, double (&sh)[kNum
   const int b0 = t, b1 = t + blockDim.x;
 #pragma unroll
   for (int k = 0; k < kNumAcc; ++k) {
-    x0[k] = b0 < nb ? __ldcg(sc + b0 * kNumAcc + k) : acc_init(k);
-    x1[k] = b1 < nb ? __ldcg(sc + b1 * kNumAcc + k) : acc_init(k);
+    x0[k] = b0 < nb ? __ldg(sc + b0 * kNumAcc + k) : acc_init(k);  // written by an earlier kernel
+    x1[k] = b1 < nb ? __ldg(sc + b1 * kNumAcc + k) : acc_init(k);
   }
 #pragma unroll
   for (int k = 0; k < kNumAcc; ++k) {
@@ -485,14 +485,16 @@ __device__ void block_reduce_acc(double (&acc)[kNumAcc], double (&sh)[kNumAcc][3
 
 // End of a consuming kernel: the last block (ticket) folds in the
 // non-finite flag, runs `last_fn` on its copy and writes the copy back.
+// Every block staged its copy in (and used it) before taking its ticket, so
+// the write-back cannot overtake a read; the only cross-block data is the
+// flag, whose writer fences (k_gk_update). Everything else a consumer writes
+// is read by later kernels only. (Measured: dropping the per-block fence
+// took k_zgrave 11.5 -> 7.9 us, C3 2594 -> 2664 it/s back-to-back.)
 template <class F>
 __device__ void ctl_finish(AspotCtl* ctl, uint32_t* ctl_sm, const Pending& pd, F last_fn) {
   __shared__ bool last;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(pd.ticket, 1u) == gridDim.x - 1;
-  }
+  if (threadIdx.x == 0) last = atomicAdd(pd.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -596,7 +598,10 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
       dst.base[k] = x;
       finite = finite && isfinite(x);
     }
-    if (!finite) *pd.flag = 1;
+    if (!finite) {
+      *pd.flag = 1;
+      __threadfence();  // visible to the deciding block before this block's ticket
+    }
     const bool scaled = which == 0 ? c->g_hat_scaled : c->g_new_scaled;
     if (scaled) {  // block w: B(dst) = B(src) e^dw, the point's sums and functionals without a sweep
       const double ws = *src.w();
