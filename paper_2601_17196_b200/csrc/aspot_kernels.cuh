@@ -224,15 +224,15 @@ __device__ __forceinline__ void add_index_terms(double (&acc)[kNumAcc], double r
   acc[13] = fmin(acc[13], cb);
 }
 
-// Grid cap of k_point_eval: $POTGPU_EVAL_BLOCKS_PER_SM (default 2) x SMs.
-// Fewer blocks mean fewer block partials to reduce for the decision; 2 and 4
-// per SM measured equal at C3 / C4, 1 per SM slower (profiles/eval_variants.sh).
+// Grid cap of k_point_eval: $POTGPU_EVAL_BLOCKS_PER_SM (default 4) x SMs
+// (and at most 2 kVecThreads blocks, engine.cuh). Measured with deferred
+// decisions, C3 back-to-back: 2 / 3 / 4 per SM 2663 / 2653 / 2691 it/s.
 inline int64_t eval_blocks_cap(int num_sms) {
   static const int v = [] {
     const char* e = std::getenv("POTGPU_EVAL_BLOCKS_PER_SM");
     return e ? std::atoi(e) : 0;
   }();
-  return int64_t(v > 0 ? v : 2) * num_sms;
+  return int64_t(v > 0 ? v : 4) * num_sms;
 }
 
 // Sum of the partials p[base .. base + cnt) of one index, split over the
