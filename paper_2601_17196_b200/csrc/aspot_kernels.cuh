@@ -680,14 +680,31 @@ __device__ void loop_head(AspotCtl* ctl) {
   begin_iteration(ctl);
 }
 
-__global__ void k_resume(AspotCtl* ctl, int64_t pause_at, int64_t budget) {
-  pdl_wait();
+__device__ __forceinline__ void resume(AspotCtl* ctl, int64_t pause_at, int64_t budget) {
   ctl->pause_at = pause_at;
   ctl->loop_budget = budget;
   if (!ctl->paused) return;
   ctl->paused = 0;
   ctl->g_active = 1;
   loop_head(ctl);
+}
+
+__global__ void k_resume(AspotCtl* ctl, int64_t pause_at, int64_t budget) {
+  pdl_wait();
+  resume(ctl, pause_at, budget);
+}
+
+// Resume as the first node of a captured "resume + attempt" graph: the
+// arguments come from pinned host memory written before the launch (read
+// through UVA), so a run starts with ONE host launch and the GPU does not
+// idle between a separate resume kernel and the graph.
+struct ResumeArgs {
+  int64_t pause_at, budget;
+};
+__global__ void k_resume_pinned(AspotCtl* ctl, const ResumeArgs* args) {
+  pdl_wait();
+  const volatile ResumeArgs* va = args;
+  resume(ctl, va->pause_at, va->budget);
 }
 
 __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {

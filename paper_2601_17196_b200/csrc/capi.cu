@@ -463,6 +463,8 @@ struct AspotSession : Session {
   double gamma = 0;
   Setup st;
   cudaGraphExec_t exec = nullptr;       // one step attempt (host-launched per attempt)
+  cudaGraphExec_t exec_first = nullptr; // resume (k_resume_pinned) + one step attempt: the first launch of a run
+  PinnedObj<ResumeArgs> resume_args;
   cudaGraphExec_t loop_exec = nullptr;  // the attempt inside a WHILE node: the whole loop in one launch
   int64_t trace_cap = 1, log_cap = 0;
   static constexpr int64_t kKernelsPerAttempt = 12;
@@ -471,6 +473,7 @@ struct AspotSession : Session {
   ~AspotSession() override {
     cudaStreamSynchronize(cx.stream);  // before any buffer returns to the cache
     if (exec) cudaGraphExecDestroy(exec);
+    if (exec_first) cudaGraphExecDestroy(exec_first);
     if (loop_exec) cudaGraphExecDestroy(loop_exec);
   }
 
@@ -633,6 +636,13 @@ struct AspotSession : Session {
       graph_nodes = int64_t(nodes);
       PG_CK(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
+      const ResumeArgs* ra = resume_args.get();  // pinned allocation outside the capture
+      PG_CK(cudaStreamBeginCapture(cx.stream, cudaStreamCaptureModeThreadLocal));
+      launch_k(k_resume_pinned, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, ra);
+      enqueue_attempt();
+      PG_CK(cudaStreamEndCapture(cx.stream, &graph));
+      PG_CK(cudaGraphInstantiate(&exec_first, graph, 0));
+      cudaGraphDestroy(graph);
     }
     pt.mark("graph capture");
   }
@@ -664,7 +674,14 @@ struct AspotSession : Session {
       }
       return;
     }
-    launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop, int64_t(0));
+    bool resumed = false;
+    if (exec_first) {  // the resume travels inside the first graph launch (nothing of this session in flight)
+      resume_args.get()->pause_at = stop;
+      resume_args.get()->budget = 0;
+    } else {
+      launch_k(k_resume, dim3(1), dim3(1), 0, cx.stream, ws.ctl.p, stop, int64_t(0));
+      resumed = true;
+    }
     launches += 1;
     // first burst: exactly the iterations asked for (1 attempt each unless a
     // step is halved), then poll every sync_every attempts
@@ -673,7 +690,14 @@ struct AspotSession : Session {
     int64_t burst = (stop == INT64_MAX || stop - h.t > 4096) ? std::max(1, cfg.sync_every)
                                                               : std::max<int64_t>(1, stop - h.t);
     while (true) {
-      launch_attempts(burst);
+      if (!resumed) {
+        PG_CK(cudaGraphLaunch(exec_first, cx.stream));
+        launches += graph_nodes;
+        resumed = true;
+        if (burst > 1) launch_attempts(burst - 1);
+      } else {
+        launch_attempts(burst);
+      }
       PG_CK(cudaEventRecord(ev1, cx.stream));  // device end of the loop (before the host poll)
       sync_ctl();
       if (!h.g_active || h.fatal) break;
