@@ -143,15 +143,27 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
     switch (pts_pairs()) {
       case 2: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32<1>, kThreads, sm_est)); break;
+      case 5:
+        PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sweep_pts_smem(int(kMaxRowsPerCta)))));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_ptsR_f32<4>, kThreads, sm_est));
+        break;
+      case 3:
+        PG_CK(cudaFuncSetAttribute(sweep_pts2s_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sweep_pts_smem(int(kMaxRowsPerCtaS)))));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2s_f32, kThreads,
+                                                            sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCtaS)))));
+        break;
       case 4: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<4>, kThreads, sm_est)); break;
       case 6: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<6>, kThreads, sm_est)); break;
       default: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts_f32<8>, kThreads, sm_est)); break;
     }
   }
   occ = std::max(occ, 1);
-  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * (pts_pairs() == 2 ? kPairs : pts_pairs()) : kStripCols32);
+  ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * ((pts_pairs() == 2 || pts_pairs() == 3 || pts_pairs() == 5) ? kPairs : pts_pairs()) : kStripCols32);
+  const int64_t max_rows = (P.dot_form() && pts_pairs() == 3) ? kMaxRowsPerCtaS : kMaxRowsPerCta;
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
-  ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip);
+  ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip, max_rows);
   int64_t max_rb = ws.g.grid.y;
   int max_rpc = ws.g.rows_per_cta;
   ws.shards.clear();
@@ -162,7 +174,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
       sg.index = cx.comm.shard_index(p);
       sg.lo = cx.comm.lo(n, sg.index);
       sg.hi = cx.comm.hi(n, sg.index);
-      sg.g = choose_grid(n, sg.hi - sg.lo, cx.num_sms, occ, ws.strip);
+      sg.g = choose_grid(n, sg.hi - sg.lo, cx.num_sms, occ, ws.strip, max_rows);
       max_rb = std::max<int64_t>(max_rb, sg.g.grid.y);
       max_rpc = std::max(max_rpc, sg.g.rows_per_cta);
       ws.shards.push_back(sg);
@@ -177,6 +189,8 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts2s_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
@@ -245,6 +259,8 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
     if (P.XS_gamma != gamma) throw Error(POTGPU_ERR_CUDA, "internal: scaled coordinates not prepared for this gamma");
     SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
     switch (pts_pairs()) {
+      case 3: launch_k(sweep_pts2s_f32, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
+      case 5: launch_k(sweep_ptsR_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
       case 2:  // two-row variant, row partials merged over a cluster of ws.pts_cs strips
         switch (ws.pts_cs) {
           case 8: launch_kc(sweep_pts2_f32<8>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 8, s, a); break;

@@ -799,6 +799,376 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   }
 }
 
+// sweep_pts2_f32 with the column constants in shared memory instead of
+// registers ($POTGPU_PTS_PAIRS=3): ~48 fewer registers for 3 CTAs (24
+// warps) per SM to cover the per-row dependency chain, at the cost of two
+// LDS.128 per column pair and warp step. Rows per CTA are capped at
+// kMaxRowsPerCtaS so three CTAs' shared memory fits; the epilogue's column
+// combine reuses the row-sum tiles.
+constexpr int64_t kMaxRowsPerCtaS = 1280;
+__global__ void __launch_bounds__(kThreads, 3) sweep_pts2s_f32(SrcPointsDotF32 src, SweepArgs a) {
+  pdl_wait();
+  constexpr int KP = kPairs;
+  constexpr int kStrip = 64 * KP;
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStrip;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i), then the row-sum tiles
+  // the lane's column constants: (cx, cy) and (cz, B') per pair, read per warp step
+  __shared__ float4 s_XY[KP][32], s_ZB[KP][32];
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
+  }
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    if (warp != 0) break;
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;
+      y[h] = make_float4(0, 0, 0, 0);
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
+        y[h] = src.Ys[j];
+      }
+      b[h] = float(vv);
+    }
+    s_XY[q][lane] = make_float4(y[0].x, y[1].x, y[0].y, y[1].y);
+    s_ZB[q][lane] = make_float4(y[0].z, y[1].z, b[0], b[1]);
+  }
+  __syncthreads();
+  float2 cacc[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY;
+  float mmax = -INFINITY;
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);
+  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;
+  float my_ms = 0.f;
+  int slot = 0;
+  int64_t ib = r0 + warp;
+  const int64_t ldp = gridDim.x;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      const float2 part = make_float2((s0 + s1) + (s2 + s3), my_ms);
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = part;
+    }
+    __syncwarp();
+  };
+  // one row's tile slot, column scale update and accumulation
+  auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    *tslot = tree_sum2<KP>(p);
+    tslot += 33;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      tslot = tile + lane;
+      ib = i + kWarps;
+    }
+    const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;
+    if (mA > sigma) {
+      const float sc = ex2f(sigma - mA);
+#pragma unroll
+      for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = mA;
+    }
+    mmax = fmaxf(mmax, mA);
+    const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+    const float2 F2 = make_float2(f, f);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+  };
+  int64_t i = r0 + warp;
+  for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
+    const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+    float2 ta[KP], tb[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float4 xy = s_XY[q][lane], zb = s_ZB[q][lane];
+      const float2 cxq = make_float2(xy.x, xy.y), cyq = make_float2(xy.z, xy.w), czq = make_float2(zb.x, zb.y);
+      const float2 B = make_float2(zb.z, zb.w);
+      float2 xa = __ffma2_rn(make_float2(da.x, da.x), cxq, B);
+      float2 xb = __ffma2_rn(make_float2(db.x, db.x), cxq, B);
+      xa = __ffma2_rn(make_float2(da.y, da.y), cyq, xa);
+      xb = __ffma2_rn(make_float2(db.y, db.y), cyq, xb);
+      ta[q] = __ffma2_rn(make_float2(da.z, da.z), czq, xa);
+      tb[q] = __ffma2_rn(make_float2(db.z, db.z), czq, xb);
+    }
+    float ma = tree_max2<KP>(ta), mb = tree_max2<KP>(tb);
+    ma = warp_maxf(ma);
+    mb = warp_maxf(mb);
+    const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
+      tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+    }
+    finish_row(ma, da.w, ta, i);
+    finish_row(mb, db.w, tb, i + kWarps);
+  }
+  if (i < r1) {  // a last single row
+    const float4 da = s_R[i - r0];
+    float2 ta[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float4 xy = s_XY[q][lane], zb = s_ZB[q][lane];
+      float2 xa = __ffma2_rn(make_float2(da.x, da.x), make_float2(xy.x, xy.y), make_float2(zb.z, zb.w));
+      xa = __ffma2_rn(make_float2(da.y, da.y), make_float2(xy.z, xy.w), xa);
+      ta[q] = __ffma2_rn(make_float2(da.z, da.z), make_float2(zb.x, zb.y), xa);
+    }
+    float ma = fmaxf(ta[0].x, ta[0].y);
+#pragma unroll
+    for (int q = 1; q < KP; ++q) ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
+    ma = warp_maxf(ma);
+    const float msa = (ma == -INFINITY) ? 0.f : ma;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+    }
+    finish_row(ma, da.w, ta, i);
+  }
+  if (slot > 0) flush(slot);
+  float (*cs)[kStrip] = reinterpret_cast<float (*)[kStrip]>(reinterpret_cast<float*>(s_R + a.rows_per_cta));  // the tiles, done
+  __shared__ float ss[kWarps];
+  __shared__ float mm[kWarps];
+  if (lane == 0) {
+    ss[warp] = sigma;
+    mm[warp] = mmax;
+  }
+  __syncthreads();
+  float sig = ss[0];
+  for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+  const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+    cs[warp][c] = cacc[q].x * fw;
+    cs[warp][c + 1] = cacc[q].y * fw;
+  }
+  __syncthreads();
+  float2* colp = reinterpret_cast<float2*>(a.colp);
+  for (int c = threadIdx.x; c < kStrip; c += kThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+  }
+  if (threadIdx.x == 0) {
+    float m = mm[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
+// R rows per warp step with the column constants in shared memory
+// ($POTGPU_PTS_PAIRS=5: R = 4): R independent max / CREDUX / MUFU chains in
+// flight per warp. Same partial formats and epilogue as sweep_pts2s_f32.
+template <int R>
+__global__ void __launch_bounds__(kThreads, 2) sweep_ptsR_f32(SrcPointsDotF32 src, SweepArgs a) {
+  pdl_wait();
+  constexpr int KP = kPairs;
+  constexpr int kStrip = 64 * KP;
+  if (a.gate && *a.gate == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStrip;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i), then the row-sum tiles
+  // the lane's column constants: (cx, cy) and (cz, B') per pair, read per warp step
+  __shared__ float4 s_XY[KP][32], s_ZB[KP][32];
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
+  }
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    if (warp != 0) break;
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;
+      y[h] = make_float4(0, 0, 0, 0);
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
+        y[h] = src.Ys[j];
+      }
+      b[h] = float(vv);
+    }
+    s_XY[q][lane] = make_float4(y[0].x, y[1].x, y[0].y, y[1].y);
+    s_ZB[q][lane] = make_float4(y[0].z, y[1].z, b[0], b[1]);
+  }
+  __syncthreads();
+  float2 cacc[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY;
+  float mmax = -INFINITY;
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);
+  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;
+  float my_ms = 0.f;
+  int slot = 0;
+  int64_t ib = r0 + warp;
+  const int64_t ldp = gridDim.x;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      const float2 part = make_float2((s0 + s1) + (s2 + s3), my_ms);
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = part;
+    }
+    __syncwarp();
+  };
+  // one row's tile slot, column scale update and accumulation
+  auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    *tslot = tree_sum2<KP>(p);
+    tslot += 33;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      tslot = tile + lane;
+      ib = i + kWarps;
+    }
+    const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;
+    if (mA > sigma) {
+      const float sc = ex2f(sigma - mA);
+#pragma unroll
+      for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+      sigma = mA;
+    }
+    mmax = fmaxf(mmax, mA);
+    const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+    const float2 F2 = make_float2(f, f);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+  };
+  int64_t i = r0 + warp;
+  for (; i + (R - 1) * kWarps < r1; i += R * kWarps) {  // rows i, i + 8, ..., i + 8 (R - 1)
+    float4 d[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) d[rr] = s_R[i + rr * kWarps - r0];
+    float2 t[R][KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float4 xy = s_XY[q][lane], zb = s_ZB[q][lane];
+      const float2 cxq = make_float2(xy.x, xy.y), cyq = make_float2(xy.z, xy.w), czq = make_float2(zb.x, zb.y);
+      const float2 B = make_float2(zb.z, zb.w);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float2 x = __ffma2_rn(make_float2(d[rr].x, d[rr].x), cxq, B);
+        x = __ffma2_rn(make_float2(d[rr].y, d[rr].y), cyq, x);
+        t[rr][q] = __ffma2_rn(make_float2(d[rr].z, d[rr].z), czq, x);
+      }
+    }
+    float m[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) m[rr] = warp_maxf(tree_max2<KP>(t[rr]));
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const float ms = (m[rr] == -INFINITY) ? 0.f : m[rr];
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 e = __fadd2_rn(t[rr][q], make_float2(-ms, -ms));
+        t[rr][q] = make_float2(ex2f(e.x), ex2f(e.y));
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) finish_row(m[rr], d[rr].w, t[rr], i + rr * kWarps);
+  }
+  for (; i < r1; i += kWarps) {  // the last rows, one at a time
+    const float4 da = s_R[i - r0];
+    float2 ta[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float4 xy = s_XY[q][lane], zb = s_ZB[q][lane];
+      float2 xa = __ffma2_rn(make_float2(da.x, da.x), make_float2(xy.x, xy.y), make_float2(zb.z, zb.w));
+      xa = __ffma2_rn(make_float2(da.y, da.y), make_float2(xy.z, xy.w), xa);
+      ta[q] = __ffma2_rn(make_float2(da.z, da.z), make_float2(zb.x, zb.y), xa);
+    }
+    float ma = warp_maxf(tree_max2<KP>(ta));
+    const float msa = (ma == -INFINITY) ? 0.f : ma;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 e = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+      ta[q] = make_float2(ex2f(e.x), ex2f(e.y));
+    }
+    finish_row(ma, da.w, ta, i);
+  }
+  if (slot > 0) flush(slot);
+  float (*cs)[kStrip] = reinterpret_cast<float (*)[kStrip]>(reinterpret_cast<float*>(s_R + a.rows_per_cta));  // the tiles, done
+  __shared__ float ss[kWarps];
+  __shared__ float mm[kWarps];
+  if (lane == 0) {
+    ss[warp] = sigma;
+    mm[warp] = mmax;
+  }
+  __syncthreads();
+  float sig = ss[0];
+  for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+  const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+    cs[warp][c] = cacc[q].x * fw;
+    cs[warp][c + 1] = cacc[q].y * fw;
+  }
+  __syncthreads();
+  float2* colp = reinterpret_cast<float2*>(a.colp);
+  for (int c = threadIdx.x; c < kStrip; c += kThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) s += cs[ww][c];
+    if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : s, sig == -INFINITY ? 0.f : sig);
+  }
+  if (threadIdx.x == 0) {
+    float m = mm[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
+
 // ------------------------------------------------------------------------
 // Grid shape: strips x row blocks, the row-block count chosen so the CTA
 // count fills the resident capacity (SMs x occupancy) as evenly as possible.
@@ -827,7 +1197,7 @@ inline int pts_pairs() {
   static const int v = [] {
     const char* e = std::getenv("POTGPU_PTS_PAIRS");
     const int k = e ? std::atoi(e) : 0;
-    return (k == 2 || k == 4 || k == 6 || k == 8) ? k : 2;  // 2: the two-row 8-pair variant (default)
+    return (k == 2 || k == 3 || k == 4 || k == 5 || k == 6 || k == 8) ? k : 2;  // 2: the two-row 8-pair variant (default); 3: its smem-column form
   }();
   return v;
 }
@@ -851,7 +1221,8 @@ inline int pts_cluster(int64_t strips) {
 
 constexpr int64_t kMaxRowsPerCta = 2048;
 
-inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occupancy, int strip_cols) {
+inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occupancy, int strip_cols,
+                             int64_t max_rows = kMaxRowsPerCta) {
   const int64_t strips = ceil_div(ncols, strip_cols);
   const int64_t cap = int64_t(num_sms) * occupancy;  // resident CTAs
   const int64_t max_rb = std::max<int64_t>(1, nrows / 8);
@@ -859,7 +1230,7 @@ inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occu
   // last wave is fullest (exact multiples of the capacity when possible)
   // at most kMaxRowsPerCta rows per CTA: the fp32 sweep keeps the CTA's row
   // potentials in shared memory (8 KB), which must not cost occupancy
-  const int64_t min_rb = std::min<int64_t>(max_rb, ceil_div(nrows, kMaxRowsPerCta));
+  const int64_t min_rb = std::min<int64_t>(max_rb, ceil_div(nrows, max_rows));
   const int64_t target =
       std::max<int64_t>(min_rb, std::max<int64_t>(1, std::min<int64_t>(max_rb, (sweep_waves() * cap) / strips)));
   int64_t rb = target;

@@ -1,0 +1,95 @@
+// MUFU.EX2 throughput microbenchmark (B200): the denominator of the on-the-fly
+// sweep's roofline. Each thread runs K independent chains x <- ex2(x) * a + b
+// (one MUFU.EX2 + one FFMA per element, the FFMA keeps the chain in range),
+// with 2..32 warps per SM; reports ex2/clk/SM against the nominal 16.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mufu_peak mufu_peak.cu && ./mufu_peak
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int K>
+__global__ void k_ex2(float* out, int iters, float a, float b) {
+  float x[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = -0.001f * (threadIdx.x + k);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float y;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[k]));
+      x[k] = fmaf(y, a, b);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) s += x[k];
+  if (s == 123.456f) out[0] = s;
+}
+
+// The sweep's mix: per ex2, 5 more FP32-pipe ops (3 FFMA of the exponent,
+// a max, the subtraction of the shift), K independent chains per thread.
+template <int K>
+__global__ void k_mix(float* out, int iters, float a, float b) {
+  float x[K], m[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) { x[k] = -0.001f * (threadIdx.x + k); m[k] = 0.f; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float t = fmaf(x[k], a, b);
+      t = fmaf(t, a, b);
+      t = fmaf(t, a, b);
+      m[k] = fmaxf(m[k], t);
+      float y;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t - 0.125f));
+      x[k] = y;
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) s += x[k] + m[k];
+  if (s == 123.456f) out[0] = s;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk_khz = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  float* out;
+  cudaMalloc(&out, 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4096;
+  printf("{\"sms\": %d, \"attr_clock_mhz\": %.0f, \"runs\": [", sms, clk_khz / 1e3);
+  bool first = true;
+  for (int warps = 4; warps <= 32; warps *= 2) {
+    const int threads = 256, blocks = sms * warps * 32 / threads;
+    k_ex2<8><<<blocks, threads>>>(out, 64, 0.5f, -0.25f);
+    cudaEventRecord(e0);
+    k_ex2<8><<<blocks, threads>>>(out, iters, 0.5f, -0.25f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ex2 = double(blocks) * threads * iters * 8;
+    printf("%s{\"warps_per_sm\": %d, \"ms\": %.4f, \"gex2_s\": %.1f}", first ? "" : ", ", warps, ms, ex2 / (ms * 1e-3) / 1e9);
+    first = false;
+  }
+  printf("], \"mix5\": [");
+  first = true;
+  for (int warps = 8; warps <= 32; warps *= 2) {
+    const int threads = 256, blocks = sms * warps * 32 / threads;
+    k_mix<8><<<blocks, threads>>>(out, 64, 0.5f, -0.25f);
+    cudaEventRecord(e0);
+    k_mix<8><<<blocks, threads>>>(out, iters, 0.5f, -0.25f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ex2 = double(blocks) * threads * iters * 8;
+    printf("%s{\"warps_per_sm\": %d, \"ms\": %.4f, \"gex2_s\": %.1f}", first ? "" : ", ", warps, ms, ex2 / (ms * 1e-3) / 1e9);
+    first = false;
+  }
+  printf("]}\n");
+  return 0;
+}
