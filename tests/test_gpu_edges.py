@@ -118,3 +118,26 @@ def test_dense_layouts_give_identical_solves(ctx, dtype):
         assert g.iterations == ref.iterations and g.status == ref.status
         assert g.cost == ref.cost and g.final_error == ref.final_error
         assert np.array_equal(g.plan.row_slack, ref.plan.row_slack)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_device_cost_scale_is_the_exact_fp64_max(ctx, seed):
+    """The on-the-fly cost scale derived on the device (two fp32 passes, then
+    fp64 on the candidate pairs) equals 1 / max_ij |x_i - y_j|^2 in the fp64
+    formula the host uses, so a solve with the scale derived on the device
+    and one with the host's scale are bit-identical. Seed 2 adds many pairs
+    that tie or nearly tie for the maximum."""
+    rng = np.random.default_rng(seed)
+    n = 3000
+    X = rng.uniform(-1, 1, (n, 3)).astype(np.float32).astype(np.float64)
+    Y = rng.uniform(-1, 1, (n, 3)).astype(np.float32).astype(np.float64)
+    if seed == 2:  # corners: many (near-)maximal pairs
+        X[:50] = np.float32(-1.0)
+        Y[:50] = np.float32(1.0)
+        Y[50:60] = np.nextafter(np.float32(1.0), np.float32(0.0))
+    r = np.full(n, 1.0 / n)
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10 ** 9, max_iterations=30, materialize_plan=False)
+    a = pot.aspot_solve(pot.Instance(r=r, c=r, s=0.9, X=X, Y=Y, cost_scale=None, dtype=pot.DType.F32), cfg, ctx=ctx)
+    b = pot.aspot_solve(pot.Instance(r=r, c=r, s=0.9, X=X, Y=Y, cost_scale=pot.points_scale(X, Y),
+                                     dtype=pot.DType.F32), cfg, ctx=ctx)
+    assert a.iterations == b.iterations and a.cost == b.cost and a.final_error == b.final_error
