@@ -58,7 +58,8 @@ __global__ void k_build_logk(const double* __restrict__ C64, int64_t n, int64_t 
 // n = 16384). Pass 1 takes the fp32 maximum M of the same difference-square
 // sums (nonnegative terms: relative error below 12 * 2^-24 of the fp64 value);
 // pass 2 re-evaluates in fp64 only the pairs whose fp32 value reaches
-// M (1 - 2^-18), a set that contains every maximising pair. Result: the
+// M (1 - 2^-18), a set that contains every maximising pair (only rows whose
+// fp32 maximum reaches it are rescanned). Result: the
 // exact fp64 maximum (bit pattern, atomicMax over nonnegative doubles).
 // Grid: (row blocks of 256, column slices); Y staged in shared memory.
 constexpr int kPmaxCols = 256;
@@ -67,16 +68,25 @@ __device__ __forceinline__ float d2_f32(const float4& a, const float4& b) {
   return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
 }
 
+__device__ __noinline__ unsigned long long d2_f64_bits(const float4* X, const float4* Y, int64_t i, int64_t j) {
+  const ElemPointsF32 el{X, Y, 1.0, 1.0};
+  return (unsigned long long)__double_as_longlong(el.cost(i, j));
+}
+
+// EXACT = false: fp32 maxima per row (rowmax, bit patterns of nonnegative
+// floats) and overall (out32). EXACT = true: only rows whose fp32 maximum
+// reaches the threshold are rescanned; their candidate pairs in fp64.
 template <bool EXACT>
-__global__ void __launch_bounds__(256) k_points_max2(const float4* X, const float4* Y, int64_t n, const unsigned* m32,
+__global__ void __launch_bounds__(256) k_points_max2(const float4* X, const float4* Y, int64_t n, unsigned* rowmax,
                                                      unsigned* out32, unsigned long long* out64) {
   __shared__ float4 sY[kPmaxCols];
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t per = (n + gridDim.y - 1) / gridDim.y;
   const int64_t c0 = int64_t(blockIdx.y) * per, c1 = min(n, c0 + per);
   const float4 a = i < n ? X[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const float thr = EXACT ? __uint_as_float(*m32) * (1.0f - 0x1p-18f) : 0.f;
-  ElemPointsF32 el{X, Y, 1.0, 1.0};
+  const float thr = EXACT ? __uint_as_float(*out32) * (1.0f - 0x1p-18f) : 0.f;
+  const bool active = i < n && (!EXACT || __uint_as_float(rowmax[i]) >= thr);
+  if (EXACT && !__syncthreads_or(active)) return;  // no candidate row in this block
   float m = 0.f;
   unsigned long long mx = 0;
   for (int64_t j0 = c0; j0 < c1; j0 += kPmaxCols) {
@@ -84,15 +94,16 @@ __global__ void __launch_bounds__(256) k_points_max2(const float4* X, const floa
     __syncthreads();
     if (threadIdx.x < cnt) sY[threadIdx.x] = Y[j0 + threadIdx.x];
     __syncthreads();
-    if (i < n) {
+    if (active) {
       for (int k = 0; k < cnt; ++k) {
         const float d = d2_f32(a, sY[k]);
         if (!EXACT) m = fmaxf(m, d);
-        else if (d >= thr) mx = max(mx, (unsigned long long)__double_as_longlong(el.cost(i, j0 + k)));
+        else if (d >= thr) mx = max(mx, d2_f64_bits(X, Y, i, j0 + k));
       }
     }
   }
   if (!EXACT) {
+    if (i < n && m > 0.f) atomicMax(rowmax + i, __float_as_uint(m));
     m = warp_maxf(m);
     if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out32, __float_as_uint(m));
   } else if (mx) {
@@ -234,17 +245,22 @@ static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P)
     PG_CK(cudaMemcpyAsync(P.X4.p, hx.data(), size_t(n) * sizeof(float4), cudaMemcpyHostToDevice, cx.stream));
     PG_CK(cudaMemcpyAsync(P.Y4.p, hy.data(), size_t(n) * sizeof(float4), cudaMemcpyHostToDevice, cx.stream));
     DevBuf<unsigned long long> mx;
-    DevBuf<unsigned> m32;
+    DevBuf<unsigned> m32, rowmax;
     mx.alloc(1);
     mx.zero(cx.stream);
     m32.alloc(1);
     m32.zero(cx.stream);
+    rowmax.alloc(size_t(n));
+    rowmax.zero(cx.stream);
     {
       const unsigned rb = unsigned(ceil_div(n, int64_t(256)));
       const unsigned cs = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, int64_t(kPmaxCols)),
                                                                            ceil_div(int64_t(cx.num_sms) * 4, int64_t(rb)))));
-      k_points_max2<false><<<dim3(rb, cs), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, nullptr, m32.p, nullptr);
-      k_points_max2<true><<<dim3(rb, cs), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, m32.p, nullptr, mx.p);
+      k_points_max2<false><<<dim3(rb, cs), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, rowmax.p, m32.p, nullptr);
+      // rescan in column slices of one staging chunk: a block holding a
+      // candidate row does little serial work; the others exit at once
+      const unsigned cs2 = unsigned(ceil_div(n, int64_t(kPmaxCols)));
+      k_points_max2<true><<<dim3(rb, cs2), 256, 0, cx.stream>>>(P.X4.p, P.Y4.p, n, rowmax.p, m32.p, mx.p);
       PG_CK(cudaGetLastError());
     }
     unsigned long long hm = 0;
