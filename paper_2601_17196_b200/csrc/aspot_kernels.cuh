@@ -193,14 +193,19 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
 }
 
 constexpr int kEvalThreads = 128;
-// threads per index of k_point_eval ($POTGPU_EVAL_TPI: 1, 2, 4)
-inline int eval_tpi() {
+// threads per index of k_point_eval ($POTGPU_EVAL_TPI: 1, 2, 4, 8; default:
+// 4, or 8 when an index's partial list would not fit the register path of
+// 4 threads (more than 4 kGroupRegs strips: C4, 128 strips). Measured: C3
+// (32 strips) 2693 / 2624 it/s with 4 / 8, C4 214.9 / 216.8 it/s.
+constexpr int kGroupRegsDecl = 16;
+inline int eval_tpi(int64_t nstrips = 0) {
   static const int v = [] {
     const char* e = std::getenv("POTGPU_EVAL_TPI");
     const int k = e ? std::atoi(e) : 0;
-    return (k == 1 || k == 2 || k == 4) ? k : 4;
+    return (k == 1 || k == 2 || k == 4 || k == 8) ? k : 0;
   }();
-  return v;
+  if (v) return v;
+  return nstrips > 4 * kGroupRegsDecl ? 8 : 4;
 }
 
 // Per-index terms of every functional the reference evaluates at a point
@@ -243,7 +248,7 @@ inline int64_t eval_blocks_cap(int num_sms) {
 // before the max / sum passes (one L2 round trip instead of one per
 // partial); longer lists stream. Same M, per-thread order and shuffle tree
 // either way -> identical bits.
-constexpr int kGroupRegs = 16;
+constexpr int kGroupRegs = kGroupRegsDecl;
 
 template <int kTPI>
 __device__ __forceinline__ double group_partial_sum(const double* p, int64_t base, int64_t cnt, int fmt, double offset,

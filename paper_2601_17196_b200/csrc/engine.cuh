@@ -94,7 +94,8 @@ struct Workspace {
   int pts_cs = 1;                 // cluster size of the points sweep's row-partial merge
   int nblk = 0;  // O(n) kernel grid
   int gv = 0;    // grid of the ASPOT attempt's O(n) kernels (one element of 2n + 1 per thread, <= 2 per SM)
-  int eval_blocks = 0;  // k_point_eval grid (8 indices per block)
+  int eval_blocks = 0;  // k_point_eval grid
+  int eval_tpi = 4;     // k_point_eval threads per index
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
   int strip = 256;
   size_t sweep_smem = 0;
@@ -209,7 +210,8 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.colp.alloc(size_t(2 * max_rb * n));
   ws.maxp.alloc(size_t(ws.g.grid.x * max_rb));
   // <= 2 kVecThreads: the deferred decisions reduce at most two partial rows per thread
-  ws.eval_blocks = int(std::min<int64_t>(std::min<int64_t>(ceil_div(n * eval_tpi(), kEvalThreads), eval_blocks_cap(cx.num_sms)),
+  ws.eval_tpi = eval_tpi(ws.nstrips);
+  ws.eval_blocks = int(std::min<int64_t>(std::min<int64_t>(ceil_div(n * ws.eval_tpi, kEvalThreads), eval_blocks_cap(cx.num_sms)),
                                          2 * kVecThreads));
   ws.scratch.alloc(size_t(std::max(8192, kNumAcc * ws.eval_blocks)));
   ws.ticket.alloc(2);  // [0] k_point_eval, [1] the attempt's O(n) kernels (k_zgrave, k_gk_update, k_commit)
@@ -355,9 +357,10 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.pfmt = so.pfmt;
   r.rowshift = so.rowshift;
   r.mode = scaled ? 1 : 0;
-  switch (eval_tpi()) {
+  switch (ws.eval_tpi) {
     case 1: launch_k(k_point_eval<1>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
     case 2: launch_k(k_point_eval<2>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
+    case 8: launch_k(k_point_eval<8>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
     default: launch_k(k_point_eval<4>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
   }
   PG_CK(cudaGetLastError());
