@@ -54,6 +54,9 @@ struct AspotCtl {
   int paused;     // loop stopped at pause_at (session API), not finished
   // sweep-vs-scale gates of z_hat and z_check' (block w: B scales by e^dw)
   int g_hat_sweep, g_hat_scaled, g_new_sweep, g_new_scaled;
+  // z_check' by the one-sided sweep (block u or v from z_best = z_hat; sweep_pts1_f32)
+  // and the gate of its evaluation (g_new_sweep | g_new_one); one_sided_ok: problem allows it
+  int g_new_one, g_new_eval, one_sided_ok;
   int clamp_guard;  // fp64 (Eigen-clamped exp) problems: scale only far above the clamp floor
   int64_t pause_at;
   int64_t loop_budget;  // attempts the device loop (graph WHILE node) may still run in this launch
@@ -177,7 +180,11 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
       const PointScalars& pb = keep ? ctl->ps[R_CHECK] : ps;
       ctl->block_check = ctl->block_rule == POTGPU_ROUND_ROBIN ? int((ctl->gk_calls + 1) % 3) : greedy_block(pb, ctl->s);
       ctl->g_new_scaled = ctl->block_check == 2 && (!ctl->clamp_guard || scale_safe(pb, ctl->s));
-      ctl->g_new_sweep = !ctl->g_new_scaled;
+      // one side of B(z_check') is an O(n) rescale of z_hat's; the other one
+      // sweep with the row shifts z_hat's sweep left in rowp
+      ctl->g_new_one = ctl->one_sided_ok && !keep && !ctl->g_new_scaled && ctl->block_check != 2;
+      ctl->g_new_sweep = !ctl->g_new_scaled && !ctl->g_new_one;
+      ctl->g_new_eval = ctl->g_new_sweep | ctl->g_new_one;
       break;
     }
     case R_NEW:
@@ -509,6 +516,7 @@ __device__ void ctl_finish(AspotCtl* ctl, uint32_t* ctl_sm, const Pending& pd, F
     if (pd.flag && __ldcg(pd.flag)) {  // solvers.hpp:83-87: non-finite update -> Overflow
       c->g_alive = 0;
       c->g_hat_sweep = c->g_hat_scaled = c->g_new_sweep = c->g_new_scaled = 0;
+      c->g_new_one = c->g_new_eval = 0;
       *pd.flag = 0;
     }
     last_fn(c);
@@ -602,6 +610,10 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
       }
       dst.base[k] = x;
       finite = finite && isfinite(x);
+      if (which == 1 && c->g_new_one) {  // the side of z_check' that only rescales: B' = B e^(x' - x)
+        if (k < n && block == 0) dst_row[k] = rowb[k] * exp(x - src.base[k]);
+        else if (k >= n && k < 2 * n && block == 1) dst_col[k - n] = colb[k - n] * exp(x - src.base[k]);
+      }
     }
     if (!finite) {
       *pd.flag = 1;
@@ -647,6 +659,7 @@ __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double e
 
 __device__ void reset_point_gates(AspotCtl* ctl) {
   ctl->g_hat_sweep = ctl->g_hat_scaled = ctl->g_new_sweep = ctl->g_new_scaled = 0;
+  ctl->g_new_one = ctl->g_new_eval = 0;
 }
 
 __device__ void begin_iteration(AspotCtl* ctl) {
@@ -764,7 +777,7 @@ __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot 
     if (in_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
     return;
   }
-  const bool swept = c->g_new_sweep, scaled = c->g_new_scaled;
+  const bool swept = c->g_new_sweep || c->g_new_one, scaled = c->g_new_scaled;
   if (swept || scaled)  // decision at z_check' (solvers.hpp:345-352)
     decide_pending(c, R_NEW, swept ? pd.eval_part : pd.gk_part, swept ? pd.eval_nb : pd.gk_nb, *zn.w(), swept);
   if (c->attempt_ok) {

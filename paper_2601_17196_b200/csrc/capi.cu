@@ -528,6 +528,7 @@ struct AspotSession : Session {
   cudaGraphExec_t exec = nullptr;       // one step attempt (host-launched per attempt)
   cudaGraphExec_t exec_first = nullptr; // resume (k_resume_pinned) + one step attempt: the first launch of a run
   PinnedObj<ResumeArgs> resume_args;
+  bool one_sided = false;  // z_check' by sweep_pts1_f32 when its block is u or v (fp32 points)
   cudaGraphExec_t loop_exec = nullptr;  // the attempt inside a WHILE node: the whole loop in one launch
   int64_t trace_cap = 1, log_cap = 0;
   static constexpr int64_t kKernelsPerAttempt = 12;
@@ -606,8 +607,10 @@ struct AspotSession : Session {
     // (scaled sums and functionals when its block is w)
     launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
              ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p, ws.row(R_NEW), ws.col(R_NEW), pd);
-    launch_eval(cx, ws, sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma), ZN, R_NEW,
-                &ctl->g_new_sweep, nullptr, true);
+    const SweepOut so_n = sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma);
+    if (one_sided) launch_one_sided(cx, P, ws, ZN, &ctl->g_new_one, OneSidedArgs{ws.row(R_NEW), ws.col(R_NEW), ZH.v(),
+                                                                                &ctl->block_check});
+    launch_eval(cx, ws, so_n, ZN, R_NEW, &ctl->g_new_eval, nullptr, true);
     // decides z_check' and commits the attempt
     launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
              ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd, loop, in_loop);
@@ -676,6 +679,8 @@ struct AspotSession : Session {
     h.s = P.s;
     h.status = ST_RUNNING;
     h.clamp_guard = P.dtype == POTGPU_F64 ? 1 : 0;
+    one_sided = one_sided_supported(cx, P) && ws.pts_cs == 1;
+    h.one_sided_ok = one_sided ? 1 : 0;
     PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(AspotCtl), cudaMemcpyHostToDevice, cx.stream));
     AspotCtl* ctl = ws.ctl.p;
     k_stamp_t0<<<1, 1, 0, cx.stream>>>(ctl);

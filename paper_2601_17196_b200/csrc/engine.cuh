@@ -99,6 +99,7 @@ struct Workspace {
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
   int strip = 256;
   size_t sweep_smem = 0;
+  size_t one_smem = 0;  // sweep_pts1_f32 (one-sided z_check' sweep)
   DevBuf<double> slots;     // 7 dual points
   DevBuf<double> sums;      // 6 x (row, col)
   DevBuf<double> rowp, colp, maxp, scratch, partial;
@@ -191,6 +192,9 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2s_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    PG_CK(cudaFuncSetAttribute(sweep_pts1_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(std::max(ws.sweep_smem, sweep_pts1_smem(max_rpc)))));
+    ws.one_smem = std::max(ws.sweep_smem, sweep_pts1_smem(max_rpc));
     PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
@@ -364,6 +368,34 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
     default: launch_k(k_point_eval<4>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
   }
   PG_CK(cudaGetLastError());
+}
+
+// One-sided points sweep of z_check' (sweep_pts1_f32): the same grid and
+// partial buffers as launch_sweep, unsharded fp32 points problems only.
+inline bool one_sided_supported(const Context& cx, const DevProblem& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_ONE_SIDED");
+    return !(e && e[0] == '0');
+  }();
+  return on && P.dtype == POTGPU_F32 && P.dot_form() && !cx.comm.sharded() && pts_pairs() == 2 && true;
+}
+
+inline void launch_one_sided(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const int* gate, const OneSidedArgs& o) {
+  const SweepGrid& g = ws.g;
+  SweepArgs a;
+  a.n = P.n;
+  a.row_lo = 0;
+  a.row_hi = P.n;
+  a.rows_per_cta = g.rows_per_cta;
+  a.u = z.u(); a.v = z.v(); a.w = z.w();
+  a.lu = nullptr; a.lv = nullptr;
+  a.rowshift = P.rowshift();
+  a.colshift = P.yshift.p;
+  a.rowp = ws.rowp.p; a.colp = ws.colp.p; a.maxp = ws.maxp.p;
+  a.gate = gate;
+  a.gamma = 0.0;
+  SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
+  launch_k(sweep_pts1_f32, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o);
 }
 
 // Where an attempt's deferred decisions find their partials (aspot_kernels.cuh Pending).

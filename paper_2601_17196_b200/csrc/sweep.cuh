@@ -1169,6 +1169,221 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_ptsR_f32(SrcPointsDotF32 sr
 }
 
 
+// One-sided points sweep of z_check' (ASPOT) when its Greenkhorn block is u
+// or v and z_best = z_hat: one side of B(z_check') is an O(n) rescale of
+// z_hat's sums (k_gk_update writes it to krow / kcol), the other needs one
+// pass, and the row shifts need no max: u enters the fp64 row offset A_i,
+// not t, so for block u each row segment's max is exactly the one z_hat's
+// sweep (or z_grave's, when z_hat differs only in w) left in rowp; for block
+// v it is that max plus at most the strip's largest change of B'_j (exact up
+// to the strip's spread of changes; a wider spread takes the exact warp max).
+// The known side is written into the partials in the reduce kernels' format
+// (one nonzero partial per index: S 2^(M + offset) = the known sum), so the
+// evaluation is the same kernel. block (device): 0 = u (columns swept),
+// 1 = v (rows swept).
+struct OneSidedArgs {
+  const double* krow;  // B' 1 (block u)
+  const double* kcol;  // B'^T 1 (block v)
+  const double* vsrc;  // v of the source point (block v)
+  const int* block;
+};
+constexpr float kOneSidedSpread = 40.f;
+__host__ __device__ constexpr size_t sweep_pts1_smem(int rows_per_cta) {
+  return sweep_pts_smem(rows_per_cta) + size_t((rows_per_cta + 3) & ~3) * sizeof(float);
+}
+__device__ __forceinline__ float2 encode_sum(double R, double off) {  // (S, M): S 2^(M + off) = R
+  if (!(R > 0.0)) return make_float2(0.f, 0.f);
+  const double M = floor(log2(R) - off);
+  return make_float2(float(R * exp2(-(M + off))), float(M));
+}
+
+__global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 src, SweepArgs a, OneSidedArgs o) {
+  pdl_wait();
+  constexpr int KP = kPairs;
+  constexpr int kStrip = 64 * KP;
+  if (a.gate && *a.gate == 0) return;
+  const int mode = *o.block;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStrip;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const double w = *a.w;
+  const int64_t ldp = gridDim.x;
+  extern __shared__ float4 s_R[];  // rows (2x', A_i), the row-sum tiles, then [rows] source segment maxima
+  float* s_M = reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33;
+  __shared__ float2 s_B[KP][32];
+  __shared__ float s_dv[2][kWarps];
+  float2* rowp = reinterpret_cast<float2*>(a.rowp);
+  float2* colp = reinterpret_cast<float2*>(a.colp);
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double A = (a.u[i] + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
+    const float2 pp = rowp[i * ldp + blockIdx.x];  // read before this thread overwrites it
+    s_M[i - r0] = pp.x != 0.f ? pp.y : -INFINITY;
+    if (mode == 0) rowp[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.krow[i], A) : make_float2(0.f, 0.f);
+  }
+  float2 cx[KP], cy[KP], cz[KP];
+  float dmax = -INFINITY, dmin = INFINITY;
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;
+      y[h] = make_float4(0, 0, 0, 0);
+      if (j < n) {
+        vv = a.v[j] * kLog2e;
+        if (a.colshift) vv = vv + a.colshift[j];
+        y[h] = src.Ys[j];
+        if (mode == 1) {
+          double vs = o.vsrc[j] * kLog2e;
+          if (a.colshift) vs = vs + a.colshift[j];
+          const float d = float(vv) - float(vs);
+          dmax = fmaxf(dmax, d);
+          dmin = fminf(dmin, d);
+        }
+      }
+      b[h] = float(vv);
+    }
+    if (warp == 0) s_B[q][lane] = make_float2(b[0], b[1]);
+    cx[q] = make_float2(y[0].x, y[1].x);
+    cy[q] = make_float2(y[0].y, y[1].y);
+    cz[q] = make_float2(y[0].z, y[1].z);
+  }
+  if (mode == 1) {
+    dmax = warp_maxf(dmax);
+    dmin = -warp_maxf(-dmin);
+    if (lane == 0) { s_dv[0][warp] = dmax; s_dv[1][warp] = dmin; }
+    for (int c = threadIdx.x; c < kStrip; c += kThreads)  // the known column sums
+      if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = blockIdx.y == 0 ? encode_sum(o.kcol[j0 + c], 0.0) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float dvmax = -INFINITY, dvmin = INFINITY;
+  if (mode == 1)
+    for (int ww = 0; ww < kWarps; ++ww) { dvmax = fmaxf(dvmax, s_dv[0][ww]); dvmin = fminf(dvmin, s_dv[1][ww]); }
+  const bool exact = mode == 1 && !(dvmax - dvmin <= kOneSidedSpread);  // CTA-uniform
+  float mmax = -INFINITY;
+  auto dots = [&](const float4& d, float2 (&t)[KP]) {
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 B = s_B[q][lane];
+      float2 x = __ffma2_rn(make_float2(d.x, d.x), cx[q], B);
+      x = __ffma2_rn(make_float2(d.y, d.y), cy[q], x);
+      t[q] = __ffma2_rn(make_float2(d.z, d.z), cz[q], x);
+    }
+  };
+  if (mode == 0) {  // block u: column sums of B' at the source's row-segment maxima
+    float2 cacc[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
+    float sigma = -INFINITY;
+    for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+      const float4 d = s_R[i - r0];
+      const float m = s_M[i - r0];
+      if (m == -INFINITY) continue;  // empty segment (warp-uniform)
+      float2 t[KP];
+      dots(d, t);
+      const float mA = m + d.w;
+      mmax = fmaxf(mmax, mA);
+      if (mA > sigma) {
+        const float sc = ex2f(sigma - mA);
+#pragma unroll
+        for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+        sigma = mA;
+      }
+      const float f = ex2f(mA - sigma);
+      const float2 F2 = make_float2(f, f);
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 e = __fadd2_rn(t[q], make_float2(-m, -m));
+        cacc[q] = __ffma2_rn(make_float2(ex2f(e.x), ex2f(e.y)), F2, cacc[q]);
+      }
+    }
+    __shared__ float cs[kWarps][kStrip];
+    __shared__ float ss[kWarps], mm[kWarps];
+    if (lane == 0) { ss[warp] = sigma; mm[warp] = mmax; }
+    __syncthreads();
+    float sig = ss[0];
+    for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+    const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+      cs[warp][c] = cacc[q].x * fw;
+      cs[warp][c + 1] = cacc[q].y * fw;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kStrip; c += kThreads) {
+      float sc = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kWarps; ++ww) sc += cs[ww][c];
+      if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : sc, sig == -INFINITY ? 0.f : sig);
+    }
+    if (threadIdx.x == 0) {
+      float m = mm[0];
+      for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+      a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+    }
+    return;
+  }
+  // block v: row sums of B' at the source's segment maxima + the strip's largest change
+  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
+  float* tslot = tile + lane;
+  float my_ms = 0.f;
+  int slot = 0;
+  int64_t ib = r0 + warp;
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    if (lane < cnt) {
+      const float* rowv = tile + lane * 33;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
+      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+    }
+    __syncwarp();
+  };
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    const float4 d = s_R[i - r0];
+    float2 t[KP];
+    dots(d, t);
+    const float lm = tree_max2<KP>(t);
+    mmax = fmaxf(mmax, lm + d.w);
+    const float sm = s_M[i - r0];
+    const float m = exact ? warp_maxf(lm) : (sm == -INFINITY ? -INFINITY : sm + dvmax);
+    const float ms = (m == -INFINITY) ? 0.f : m;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const float2 e = __fadd2_rn(t[q], make_float2(-ms, -ms));
+      t[q] = make_float2(ex2f(e.x), ex2f(e.y));
+    }
+    *tslot = tree_sum2<KP>(t);
+    tslot += 33;
+    if (lane == slot) my_ms = ms;
+    if (++slot == 32) {
+      flush(32);
+      slot = 0;
+      tslot = tile + lane;
+      ib = i + kWarps;
+    }
+  }
+  if (slot > 0) flush(slot);
+  mmax = warp_maxf(mmax);
+  __shared__ float mm1[kWarps];
+  if (lane == 0) mm1[warp] = mmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = mm1[0];
+    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm1[ww]);
+    a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+}
+
 // ------------------------------------------------------------------------
 // Grid shape: strips x row blocks, the row-block count chosen so the CTA
 // count fills the resident capacity (SMs x occupancy) as evenly as possible.
