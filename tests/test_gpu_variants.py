@@ -2,7 +2,7 @@
 switches read once per process, so each runs in a subprocess) solves the
 same small problems as the default build: the fp64 dense ASPOT path with
 the same decisions and objective to rounding, the fp32 on-the-fly path
-within the fp32 bar. Covers the CUDA-graph WHILE loop, PDL off, the
+within the fp32 bar. Covers the CUDA-graph WHILE loop, the full z_check' sweep instead of the one-sided one, PDL off, the
 evaluation's threads per index, and the measured points-sweep variants."""
 import json
 import os
@@ -47,6 +47,7 @@ def baseline():
 
 @pytest.mark.parametrize("env", [
     {"POTGPU_GRAPH_LOOP": "1"},
+    {"POTGPU_ONE_SIDED": "0"},
     {"POTGPU_PDL": "0"},
     {"POTGPU_EVAL_TPI": "1"},
     {"POTGPU_EVAL_BLOCKS_PER_SM": "1"},
