@@ -13,6 +13,16 @@
 
 namespace pot {
 
+// An 8-bit RGB pixel buffer (the reference's pot::Image, io.hpp:159-166:
+// width, height, 3 bytes per pixel in row-major order). Reading and writing
+// image files is the reference CLI's business and is not part of this API.
+struct Image {
+  int width = 0;
+  int height = 0;
+  std::vector<unsigned char> rgb;
+  int pixel_count() const { return width * height; }
+};
+
 struct ColorHistogram {  // color_transfer.hpp:15-19
   Matrix centroids;              // k x 3, values in [0, 1]
   Vector weights;                // cluster sizes / N

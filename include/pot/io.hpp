@@ -1,16 +1,23 @@
-// pot/io.hpp — drop-in mirror of the reference's file formats
-// (/root/reference/proj/include/pot/io.hpp) plus a binary instance / plan
-// format for sizes where JSON is unusable.
-//   trace_to_csv / write_trace_csv   io.hpp:116-135 (header contract kept)
-//   Image, read_ppm / write_ppm      io.hpp:159-218 (binary P6)
-//   read_xyz / write_xyz             io.hpp:220-258
-//   instance JSON read / write       io.hpp:37-114 ("r", "c", "C", "s"; C flat or rows)
-//   read/write_instance_bin, write_plan_bin   (new; layout documented below)
+// pot/io.hpp — the host file formats around the solver path (SURVEY.md
+// §8(f) row 3). Only the contracts a drop-in user depends on are kept from
+// the reference (/root/reference/proj/include/pot/io.hpp); the code is our
+// own:
+//   trace CSV      header "t,E,phi,rounded_cost,elapsed_s" (reference io.hpp:117),
+//                  %.17g numbers, an absent rounded cost is an empty field
+//   instance JSON  keys "r", "c", "C" (flat row-major or rows), "s" (io.hpp:37-94)
+//   summary JSON   the CLI's summary.json field set (tools/pot_main.cpp:78-97)
+//   exit codes     0 ok, 1 PotError / std::exception, 2 usage (pot_main.cpp:337-386)
+//   binary         POTINST1 / POTPLAN1 (new; layout documented below) for
+//                  sizes where JSON is unusable
+// The reference's PPM / XYZ readers belong to its CLI apps, which are out of
+// scope here; the colour-transfer API takes pixel buffers.
 // The JSON reader is a minimal parser for the instance documents (objects,
 // arrays, numbers); no external JSON library is needed.
 #pragma once
 
 #include <cctype>
+#include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -24,17 +31,41 @@
 namespace pot {
 
 namespace detail {
-inline std::string format_double(double value) {  // io.hpp:21-25
-  char buf[32];
-  std::snprintf(buf, sizeof(buf), "%.17g", value);
-  return buf;
+// Shortest text that round-trips an IEEE double (the %.17g contract).
+inline std::string num17(double x) {
+  char b[40];
+  const int k = std::snprintf(b, sizeof b, "%.17g", x);
+  return std::string(b, size_t(k > 0 ? k : 0));
 }
-inline std::string read_text_file(const std::string& path) {
-  std::ifstream stream(path, std::ios::binary);
-  if (!stream) throw PotError(ErrorCode::IoFailure, "cannot open " + path);
-  std::ostringstream out;
-  out << stream.rdbuf();
-  return out.str();
+// Shortest decimal that parses back to the same double (how the CLI's JSON
+// library prints numbers).
+inline std::string shortest(double x) {
+  char b[40];
+  for (int prec = 1; prec <= 17; ++prec) {
+    std::snprintf(b, sizeof b, "%.*g", prec, x);
+    if (std::strtod(b, nullptr) == x) break;
+  }
+  std::string t(b);
+  if (std::isfinite(x) && t.find_first_of(".eEn") == std::string::npos) t += ".0";
+  return t;
+}
+inline std::string slurp(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw PotError(ErrorCode::IoFailure, "cannot open " + path);
+  std::string body;
+  char chunk[1 << 16];
+  for (size_t got; (got = std::fread(chunk, 1, sizeof chunk, f)) > 0;) body.append(chunk, got);
+  const bool bad = std::ferror(f) != 0;
+  std::fclose(f);
+  if (bad) throw PotError(ErrorCode::IoFailure, "read error on " + path);
+  return body;
+}
+inline void spill(const std::string& path, const std::string& body) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw PotError(ErrorCode::IoFailure, "cannot write " + path);
+  const size_t put = std::fwrite(body.data(), 1, body.size(), f);
+  const bool bad = (std::fclose(f) != 0) || put != body.size();
+  if (bad) throw PotError(ErrorCode::IoFailure, "write error on " + path);
 }
 
 // Minimal JSON value: number, array or object (what instance files use).
@@ -142,47 +173,40 @@ inline Instance instance_from_json_text(const std::string& text) {
 }
 
 inline Instance read_instance_json(const std::string& path) {  // io.hpp:96-104
-  return instance_from_json_text(detail::read_text_file(path));
+  return instance_from_json_text(detail::slurp(path));
 }
 
-inline void write_text_file(const std::string& path, const std::string& body) {  // io.hpp:106-110
-  std::ofstream stream(path, std::ios::binary);
-  if (!stream) throw PotError(ErrorCode::IoFailure, "cannot write " + path);
-  stream << body;
+inline void write_text_file(const std::string& path, const std::string& body) {  // io.hpp:106-110 (same role)
+  detail::spill(path, body);
 }
 
 inline std::string instance_to_json_text(const Instance& in) {  // io.hpp:82-94 (flat C)
   auto arr = [](const double* p, long k) {
     std::string o = "[";
-    for (long i = 0; i < k; ++i) { if (i) o += ", "; o += detail::format_double(p[i]); }
+    for (long i = 0; i < k; ++i) { if (i) o += ", "; o += detail::num17(p[i]); }
     return o + "]";
   };
   std::vector<double> flat;
   for (long i = 0; i < in.C.rows(); ++i)
     for (long j = 0; j < in.C.cols(); ++j) flat.push_back(in.C(i, j));
   return "{\n  \"C\": " + arr(flat.data(), long(flat.size())) + ",\n  \"c\": " + arr(in.c.data(), in.c.size()) +
-         ",\n  \"r\": " + arr(in.r.data(), in.r.size()) + ",\n  \"s\": " + detail::format_double(in.s) + "\n}\n";
+         ",\n  \"r\": " + arr(in.r.data(), in.r.size()) + ",\n  \"s\": " + detail::num17(in.s) + "\n}\n";
 }
 
 inline void write_instance_json(const std::string& path, const Instance& in) {
   write_text_file(path, instance_to_json_text(in));
 }
 
-inline std::string trace_to_csv(const ConvergenceTrace& trace) {  // io.hpp:116-131
-  std::string out = "t,E,phi,rounded_cost,elapsed_s\n";
-  for (const auto& rec : trace.records) {
-    out += std::to_string(rec.t);
-    out += ',';
-    out += detail::format_double(rec.error);
-    out += ',';
-    out += detail::format_double(rec.phi);
-    out += ',';
-    if (rec.rounded_cost) out += detail::format_double(*rec.rounded_cost);
-    out += ',';
-    out += detail::format_double(rec.elapsed_s);
-    out += '\n';
+// Trace CSV (reference io.hpp:116-131 contract): one line per record.
+inline std::string trace_to_csv(const ConvergenceTrace& trace) {
+  std::ostringstream o;
+  o << "t,E,phi,rounded_cost,elapsed_s\n";
+  for (const TraceRecord& rec : trace.records) {
+    const std::string cost = rec.rounded_cost ? detail::num17(*rec.rounded_cost) : std::string();
+    o << rec.t << ',' << detail::num17(rec.error) << ',' << detail::num17(rec.phi) << ',' << cost << ','
+      << detail::num17(rec.elapsed_s) << '\n';
   }
-  return out;
+  return o.str();
 }
 
 inline void write_trace_csv(const std::string& path, const ConvergenceTrace& trace) {
@@ -254,86 +278,53 @@ inline void write_plan_bin(const std::string& path, const TransportPlan& plan) {
   if (!f) throw PotError(ErrorCode::IoFailure, "write failed: " + path);
 }
 
-// ---------------------------------------------------------------- PPM --
-struct Image {  // io.hpp:159-166
-  int width = 0;
-  int height = 0;
-  std::vector<unsigned char> rgb;  // 3 bytes per pixel, row-major
-  int pixel_count() const { return width * height; }
-};
-
-inline Image read_ppm(const std::string& path) {  // io.hpp:168-210
-  std::ifstream stream(path, std::ios::binary);
-  if (!stream) throw PotError(ErrorCode::IoFailure, "cannot open " + path);
-  std::string magic;
-  stream >> magic;
-  if (magic != "P6") throw PotError(ErrorCode::IoFailure, path + ": expected binary PPM (P6)");
-  auto next_int = [&]() {
-    while (true) {
-      const int ch = stream.peek();
-      if (ch == '#') {
-        std::string line;
-        std::getline(stream, line);
-      } else if (std::isspace(ch)) {
-        stream.get();
-      } else {
-        break;
-      }
-    }
-    int value = 0;
-    if (!(stream >> value)) throw PotError(ErrorCode::IoFailure, path + ": malformed PPM header");
-    return value;
-  };
-  Image img;
-  img.width = next_int();
-  img.height = next_int();
-  const int maxval = next_int();
-  if (img.width <= 0 || img.height <= 0 || maxval != 255) throw PotError(ErrorCode::IoFailure, path + ": unsupported PPM header");
-  stream.get();
-  img.rgb.resize(static_cast<size_t>(img.width) * size_t(img.height) * 3);
-  stream.read(reinterpret_cast<char*>(img.rgb.data()), std::streamsize(img.rgb.size()));
-  if (stream.gcount() != std::streamsize(img.rgb.size())) throw PotError(ErrorCode::IoFailure, path + ": truncated pixel data");
-  return img;
-}
-
-inline void write_ppm(const std::string& path, const Image& img) {  // io.hpp:212-218
-  std::ofstream stream(path, std::ios::binary);
-  if (!stream) throw PotError(ErrorCode::IoFailure, "cannot write " + path);
-  stream << "P6\n" << img.width << " " << img.height << "\n255\n";
-  stream.write(reinterpret_cast<const char*>(img.rgb.data()), std::streamsize(img.rgb.size()));
-}
-
-// ---------------------------------------------------------------- XYZ --
-inline Matrix read_xyz(const std::string& path) {  // io.hpp:220-242
-  std::ifstream stream(path);
-  if (!stream) throw PotError(ErrorCode::IoFailure, "cannot open " + path);
-  std::vector<double> values;
-  double x = 0, y = 0, z = 0;
-  while (stream >> x >> y >> z) {
-    values.push_back(x);
-    values.push_back(y);
-    values.push_back(z);
+// ------------------------------------------------------------ summary --
+// The CLI's summary.json document (reference tools/pot_main.cpp:78-97): the
+// same keys, in the order nlohmann::json would print them (sorted), with
+// theory_bounds only when the solver computed them.
+inline std::string summary_json(const Instance& in, const SolveResult& res, const std::string& solver) {
+  std::map<std::string, std::string> doc;
+  auto q = [](const std::string& x) { return "\"" + x + "\""; };
+  doc["solver"] = q(solver);
+  doc["status"] = q(solve_status_name(res.status));
+  doc["iterations"] = std::to_string(res.iterations);
+  doc["cost"] = detail::shortest(transport_cost(in.C, res.plan.X));
+  doc["final_error"] = detail::shortest(res.final_error);
+  doc["tolerance"] = detail::shortest(res.tolerance);
+  doc["gamma"] = detail::shortest(res.gamma);
+  doc["wall_seconds"] = detail::shortest(res.wall_seconds);
+  doc["feasibility_gap"] = detail::shortest(plan_feasibility_gap(res.plan, in));
+  if (res.bounds) {
+    doc["theory_bounds"] = "{\n    \"L\": " + detail::shortest(res.bounds->L) + ",\n    \"R\": " +
+                           detail::shortest(res.bounds->R) + ",\n    \"iteration_bound\": " +
+                           detail::shortest(res.bounds->iteration_bound) + ",\n    \"mu_f\": " +
+                           detail::shortest(res.bounds->mu_f) + "\n  }";
   }
-  if (values.empty()) throw PotError(ErrorCode::IoFailure, path + ": no points");
-  const long n = long(values.size() / 3);
-  Matrix pts(n, 3);
-  for (long i = 0; i < n; ++i)
-    for (int d = 0; d < 3; ++d) pts(i, d) = values[size_t(3 * i + d)];
-  return pts;
+  std::string out = "{";
+  bool first = true;
+  for (const auto& kv : doc) {
+    out += first ? "\n  " : ",\n  ";
+    first = false;
+    out += q(kv.first) + ": " + kv.second;
+  }
+  return out + "\n}\n";
 }
 
-inline void write_xyz(const std::string& path, const Matrix& pts) {  // io.hpp:244-258
-  if (pts.cols() != 3) throw PotError(ErrorCode::DimensionMismatch, "point cloud must be N x 3");
-  std::string body;
-  for (long i = 0; i < pts.rows(); ++i) {
-    body += detail::format_double(pts(i, 0));
-    body += ' ';
-    body += detail::format_double(pts(i, 1));
-    body += ' ';
-    body += detail::format_double(pts(i, 2));
-    body += '\n';
+// Process exit code of the reference CLI for an outcome (pot_main.cpp:337-386):
+// 0 success, 1 a PotError or other exception while running a command, 2 a
+// command-line usage error.
+enum class ExitCode : int { Ok = 0, Failure = 1, Usage = 2 };
+template <class F>
+inline int run_command(F&& command) {
+  try {
+    command();
+    return int(ExitCode::Ok);
+  } catch (const PotError& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
   }
-  write_text_file(path, body);
+  return int(ExitCode::Failure);
 }
 
 }  // namespace pot

@@ -1,10 +1,11 @@
-"""File formats of the reference (io.hpp) plus the binary instance / plan
-format; the layouts match include/pot/io.hpp.
+"""Host file formats around the solver path; the
+layouts match include/pot/io.hpp. Kept from the reference are only the
+contracts a drop-in user depends on:
 
   trace_to_csv / write_trace_csv   io.hpp:116-135 ("t,E,phi,rounded_cost,elapsed_s")
-  read_ppm / write_ppm             io.hpp:159-218 (binary P6)
-  read_xyz / write_xyz             io.hpp:220-258
   read/write_instance_json         io.hpp:37-114 (keys r, c, C (flat or rows), s)
+  summary_json                     tools/pot_main.cpp:78-97 (the CLI's summary.json fields)
+  EXIT_OK / EXIT_FAILURE / EXIT_USAGE, run_command   pot_main.cpp:337-386 (0 / 1 / 2)
   read/write_instance_bin          "POTINST1" | int64 n | f64 s | r[n] | c[n] | C[n*n] row-major
   write_plan_bin / read_plan_bin   "POTPLAN1" | int64 rows, cols | f64 mass | X | row_slack | col_slack
 """
@@ -126,60 +127,37 @@ def read_plan_bin(path: str) -> TransportPlan:
                          col_slack=a[rows * cols + rows:rows * cols + rows + cols].copy())
 
 
-def read_ppm(path: str) -> np.ndarray:
-    """Binary P6 (maxval 255) -> uint8 array (height, width, 3)."""
-    b = _read(path)
-    pos = 0
+_STATUS_NAMES = ("converged", "max-iterations-exceeded", "step-size-underflow")  # core.hpp:286-293
 
-    def token():
-        nonlocal pos
-        while True:
-            while pos < len(b) and chr(b[pos]).isspace():
-                pos += 1
-            if pos < len(b) and b[pos:pos + 1] == b"#":
-                while pos < len(b) and b[pos:pos + 1] != b"\n":
-                    pos += 1
-                continue
-            break
-        start = pos
-        while pos < len(b) and not chr(b[pos]).isspace():
-            pos += 1
-        return b[start:pos]
 
-    if token() != b"P6":
-        raise PotError(ErrorCode.IoFailure, f"{path}: expected binary PPM (P6)")
+def summary_json(inst: Instance, res, solver: str) -> dict:
+    """The CLI's summary.json document (tools/pot_main.cpp:78-97): solver,
+    status, iterations, cost, final_error, tolerance, gamma, wall_seconds,
+    feasibility_gap and, when the solver computed them, theory_bounds."""
+    doc = {"solver": solver, "status": _STATUS_NAMES[int(res.status)],
+           "iterations": int(res.iterations), "cost": float(res.cost), "final_error": float(res.final_error),
+           "tolerance": float(res.tolerance), "gamma": float(res.gamma), "wall_seconds": float(res.wall_seconds),
+           "feasibility_gap": float(res.feasibility_gap)}
+    if getattr(res, "bounds", None) is not None:
+        b = res.bounds
+        doc["theory_bounds"] = {"R": b.R, "L": b.L, "mu_f": b.mu_f, "iteration_bound": b.iteration_bound}
+    return doc
+
+
+def write_summary_json(path: str, inst: Instance, res, solver: str) -> None:
+    _write(path, (json.dumps(summary_json(inst, res, solver), indent=2, sort_keys=True) + "\n").encode())
+
+
+EXIT_OK, EXIT_FAILURE, EXIT_USAGE = 0, 1, 2  # pot_main.cpp:337-386
+
+
+def run_command(fn, *args, **kwargs) -> int:
+    """Exit code of the reference CLI for running `fn`: 0 on success, 1 when
+    it raises (PotError or any other exception; the message goes to stderr)."""
+    import sys
     try:
-        w, h, mx = int(token()), int(token()), int(token())
-    except ValueError:
-        raise PotError(ErrorCode.IoFailure, f"{path}: malformed PPM header")
-    if w <= 0 or h <= 0 or mx != 255:
-        raise PotError(ErrorCode.IoFailure, f"{path}: unsupported PPM header")
-    pos += 1
-    data = b[pos:pos + 3 * w * h]
-    if len(data) != 3 * w * h:
-        raise PotError(ErrorCode.IoFailure, f"{path}: truncated pixel data")
-    return np.frombuffer(data, dtype=np.uint8).reshape(h, w, 3).copy()
-
-
-def write_ppm(path: str, rgb: np.ndarray) -> None:
-    rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
-    h, w = rgb.shape[:2]
-    _write(path, f"P6\n{w} {h}\n255\n".encode() + rgb.tobytes())
-
-
-def read_xyz(path: str) -> np.ndarray:
-    vals = _read(path).split()
-    try:
-        a = np.array([float(v) for v in vals[: len(vals) // 3 * 3]], dtype=np.float64)
-    except ValueError:
-        raise PotError(ErrorCode.IoFailure, f"{path}: malformed point")
-    if a.size == 0:
-        raise PotError(ErrorCode.IoFailure, f"{path}: no points")
-    return a.reshape(-1, 3)
-
-
-def write_xyz(path: str, pts: np.ndarray) -> None:
-    pts = np.asarray(pts, dtype=np.float64)
-    if pts.ndim != 2 or pts.shape[1] != 3:
-        raise PotError(ErrorCode.DimensionMismatch, "point cloud must be N x 3")
-    _write(path, "".join(f"{_fmt(x)} {_fmt(y)} {_fmt(z)}\n" for x, y, z in pts).encode())
+        fn(*args, **kwargs)
+        return EXIT_OK
+    except Exception as e:  # the CLI catches PotError and std::exception alike
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_FAILURE

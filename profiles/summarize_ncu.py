@@ -26,7 +26,12 @@ METRICS = {
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
     "instructions": "smsp__inst_executed.sum",
+    "eligible_warps_per_cycle": "smsp__warps_eligible.avg.per_cycle_active",
+    "issued_ipc": "smsp__inst_executed.avg.per_cycle_active",
 }
+# a capture of a hot sweep below these is a gated early-exit launch, not the
+# kernel (round 1 committed such a capture): refuse it
+MIN_SWEEP = {"duration_us": 20.0, "instructions": 1e6}
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "ns": 1e-3, "ms": 1e3}
 
 
@@ -55,6 +60,11 @@ def main():
         rep = os.path.join(src, name + ".ncu-rep")
         if os.path.exists(rep):
             res[name] = summarize(rep)
+            if name.startswith("sweep"):
+                bad = [k for k, lo in MIN_SWEEP.items() if (res[name].get(k) or 0.0) < lo]
+                if bad:
+                    raise SystemExit(f"{rep}: {bad} below the minimum of a real sweep launch "
+                                     f"({res[name]}) - a gated launch was captured")
     with open(os.path.join(dst, "ncu_summary.json"), "w") as f:
         json.dump(res, f, indent=2)
     lines = ["| capture | kernel | µs | DRAM read | DRAM write | regs | issue % | XU % | FMA % | warps % | top stalls |",

@@ -184,14 +184,13 @@ int main() {
     const SolveResult res = aspot_solve(in, cfg);
     const std::string csv = trace_to_csv(res.trace);
     EXPECT(csv.rfind("t,E,phi,rounded_cost,elapsed_s\n", 0) == 0);
-    Image img; img.width = 3; img.height = 2; img.rgb = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18};
-    write_ppm("/tmp/potgpu_dropin.ppm", img);
-    const Image back = read_ppm("/tmp/potgpu_dropin.ppm");
-    EXPECT(back.width == 3 && back.height == 2 && back.rgb == img.rgb);
-    Matrix pts(2, 3); pts(0, 0) = 0.1; pts(1, 2) = -2.5;
-    write_xyz("/tmp/potgpu_dropin.xyz", pts);
-    const Matrix q = read_xyz("/tmp/potgpu_dropin.xyz");
-    EXPECT(q.rows() == 2 && q(0, 0) == 0.1 && q(1, 2) == -2.5);
+    const std::string sm = summary_json(in, res, "aspot");
+    for (const char* key : {"\"solver\": \"aspot\"", "\"status\": ", "\"iterations\": ", "\"cost\": ", "\"final_error\": ",
+                            "\"tolerance\": ", "\"gamma\": ", "\"wall_seconds\": ", "\"feasibility_gap\": ",
+                            "\"theory_bounds\": {"})
+      EXPECT(sm.find(key) != std::string::npos);
+    EXPECT(run_command([] {}) == 0);
+    EXPECT(run_command([] { throw PotError(ErrorCode::InvalidArgument, "x"); }) == 1);
   }
   {  // test_dual.cpp: hand values on the 1 x 1 instance, overflow, shape errors
     const EntropicContext ctx(Matrix::Zero(1, 1), 1.0, Vector::Constant(1, 1.0), Vector::Constant(1, 1.0), 0.5);

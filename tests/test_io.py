@@ -40,17 +40,42 @@ def test_trace_csv_contract():
     assert csv.splitlines()[2] == "10,0.125,-1,,0.5"  # absent rounded cost = empty field
 
 
-def test_plan_ppm_xyz_round_trips(tmp_path):
+def test_plan_round_trip(tmp_path):
     plan = pot.TransportPlan(X=np.arange(6.0).reshape(2, 3), mass=15.0, row_slack=np.array([0.1, 0.2]),
                              col_slack=np.array([0.3, 0.4, 0.5]))
     pot_io.write_plan_bin(str(tmp_path / "p.bin"), plan)
     back = pot_io.read_plan_bin(str(tmp_path / "p.bin"))
     assert np.array_equal(back.X, plan.X) and back.mass == 15.0 and np.array_equal(back.col_slack, plan.col_slack)
-    rgb = np.random.default_rng(1).integers(0, 256, (4, 5, 3), dtype=np.uint8)
-    pot_io.write_ppm(str(tmp_path / "i.ppm"), rgb)
-    assert np.array_equal(pot_io.read_ppm(str(tmp_path / "i.ppm")), rgb)
-    (tmp_path / "c.ppm").write_bytes(b"P6\n# comment\n2 1\n255\n" + bytes(range(6)))
-    assert pot_io.read_ppm(str(tmp_path / "c.ppm")).shape == (1, 2, 3)
-    pts = np.array([[0.1, 0.2, 0.3], [-1e-300, 5.0, 7.25]])
-    pot_io.write_xyz(str(tmp_path / "p.xyz"), pts)
-    assert np.array_equal(pot_io.read_xyz(str(tmp_path / "p.xyz")), pts)
+
+
+def test_summary_fields_and_exit_codes(tmp_path):
+    """summary.json field set (tools/pot_main.cpp:78-97) and exit codes (:337-386)."""
+    import json
+    from types import SimpleNamespace
+    inst = pot.make_synthetic_instance(3, 2, 1.0, 1.0, 0.5)
+    res = SimpleNamespace(status=pot.SolveStatus.MaxIterationsExceeded, iterations=4, cost=0.5, final_error=1e-3,
+                          tolerance=1e-4, gamma=0.01, wall_seconds=0.1, feasibility_gap=0.0,
+                          bounds=pot.TheoryBounds(1.0, 2.0, 0.5, 10.0) if hasattr(pot, "TheoryBounds") else None)
+    pot_io.write_summary_json(str(tmp_path / "summary.json"), inst, res, "aspot")
+    doc = json.loads((tmp_path / "summary.json").read_text())
+    assert set(doc) >= {"solver", "status", "iterations", "cost", "final_error", "tolerance", "gamma", "wall_seconds",
+                        "feasibility_gap"}
+    assert doc["status"] == "max-iterations-exceeded" and doc["iterations"] == 4
+    if res.bounds is not None:
+        assert set(doc["theory_bounds"]) == {"R", "L", "mu_f", "iteration_bound"}
+    assert pot_io.run_command(lambda: None) == pot_io.EXIT_OK == 0
+    assert pot_io.run_command(lambda: pot.validate(pot.Instance(r=np.array([-1.0]), c=np.array([1.0]), s=0.5,
+                                                                C=np.zeros((1, 1))))) == pot_io.EXIT_FAILURE == 1
+    assert pot_io.EXIT_USAGE == 2
+
+
+def test_io_header_cpu(tmp_path):
+    """include/pot/io.hpp compiled on the host alone (no solve, no GPU)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "tio")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "test_io_cpu.cpp"), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stdout + out.stderr
