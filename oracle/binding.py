@@ -99,6 +99,28 @@ def solve(kind: int, r, c, s, C=None, X=None, Y=None, scale=1.0, epsilon=0.1, ga
                         tuple(summary[11:15]) if summary[10] else None, plan, log[:k].copy(), trace[:tl].copy())
 
 
+def config_points(config_id: int, n: int, seed: int = 1):
+    """BASELINE.json configs[config_id - 1] as points through the fixture
+    generator linked into the oracle library (the same synthetic.cpp as
+    pot.make_config_points, without loading libpotgpu.so): returns
+    (r, c, X, Y, s, cost_scale)."""
+    L = lib()
+    r, c = np.empty(n), np.empty(n)
+    X, Y = np.empty((n, 3)), np.empty((n, 3))
+    d = ctypes.c_int(0)
+    s, sc = np.empty(1), np.empty(1)
+    fn = L.potgpu_make_config
+    fn.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64] + [ctypes.POINTER(ctypes.c_double)] * 4 + \
+        [ctypes.POINTER(ctypes.c_int)] + [ctypes.POINTER(ctypes.c_double)] * 2
+    rc = fn(config_id, n, seed, _dp(r), _dp(c), _dp(X), _dp(Y), ctypes.byref(d), _dp(s), _dp(sc))
+    if rc:
+        raise OracleError(rc - 1, "invalid config id / size")
+    dd = d.value
+    X = X.reshape(-1)[: n * dd].reshape(n, dd).copy()
+    Y = Y.reshape(-1)[: n * dd].reshape(n, dd).copy()
+    return r, c, X, Y, float(s[0]), float(sc[0])
+
+
 def sweep(C, gamma, u, v, w):
     """Row/col sums, total and max exponent of B(z) at logK = -C/gamma."""
     L = lib()
