@@ -219,6 +219,10 @@ int potgpu_session_read_state(potgpu_session* s, int which, double* u, double* v
 /* Counters of the session so far: kernels launched by iterate(), step
  * attempts (incl. halvings) and n^2 sweeps executed. */
 int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* attempts, int64_t* sweeps);
+/* CTAs of the fp32 points sweep (sweep_pts2_f32) so far that exponentiated
+ * at a carried shift / at the exact row maxima (both 0 for
+ * other problem kinds or with POTGPU_CARRY=0). */
+int potgpu_session_carry_stats(potgpu_session* s, int64_t* carried, int64_t* exact);
 /* Device and pinned host blocks freed by finished solves are cached per
  * device and size class and reused by the next solve (no cudaMalloc /
  * cudaFree on the solve path after the first); this returns them all. */

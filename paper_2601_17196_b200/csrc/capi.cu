@@ -1171,6 +1171,20 @@ int potgpu_session_stats(potgpu_session* s, int64_t* kernel_launches, int64_t* a
   });
 }
 
+int potgpu_session_carry_stats(potgpu_session* s, int64_t* carried, int64_t* exact) {
+  return guarded([&] {
+    if (!s) throw Error(POTGPU_INVALID_ARGUMENT, "null session");
+    Workspace& ws = reinterpret_cast<Session*>(s)->workspace();
+    unsigned long long h[2] = {0, 0};
+    if (ws.carry_stats.p) {
+      PG_CK(cudaMemcpyAsync(h, ws.carry_stats.p, sizeof h, cudaMemcpyDeviceToHost, ws.stream));
+      PG_CK(cudaStreamSynchronize(ws.stream));
+    }
+    if (carried) *carried = int64_t(h[0]);
+    if (exact) *exact = int64_t(h[1]);
+  });
+}
+
 void* potgpu_ctx_stream(potgpu_ctx* c) { return c ? reinterpret_cast<void*>(c->cx.stream) : nullptr; }
 
 int potgpu_dual_eval(potgpu_ctx* c, const potgpu_problem* pr, double gamma, const double* u, const double* v, double w,

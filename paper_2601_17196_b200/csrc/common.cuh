@@ -319,4 +319,10 @@ __device__ __forceinline__ double warp_nanmax(double x) {
   return x;
 }
 
+__global__ void k_fill_f32(float* p, int64_t count, float value) {
+  pdl_wait();
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < count; k += int64_t(gridDim.x) * blockDim.x)
+    p[k] = value;
+}
+
 }  // namespace potgpu

@@ -12,6 +12,7 @@
 #include "rounding.cuh"
 #include "shard.cuh"
 #include "sweep.cuh"
+#include "sweep_tc.cuh"
 
 namespace potgpu {
 
@@ -76,6 +77,30 @@ struct DevProblem {
   double s = 0.0;
 };
 
+// The tensor-core points sweep (sweep_tc.cuh), opt-in with $POTGPU_TC=1.
+// Measured on B200 at C3: 0.131 ms per sweep against 0.108
+// for sweep_pts2_f32 — reading S back from TMEM (32x32b loads) is paced at
+// about the MUFU rate, so the two do not overlap enough.
+inline bool tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_TC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// Carried shifts for the fp32 points sweep (sweep.cuh, sweep_tc.cuh):
+// $POTGPU_CARRY=1, or implied by $POTGPU_TC=1. Off by default: on the CUDA-
+// core sweep they measured neutral (C3 0.1106 vs 0.1078 ms per sweep; the
+// per-row max/CREDUX chain was not the binding limit).
+inline bool carry_supported(const DevProblem& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_CARRY");
+    return (e && e[0] == '1') || tc_enabled();
+  }();
+  return on && P.dot_form() && pts_pairs() == 2;
+}
+
 struct ShardGrid {
   int64_t lo = 0, hi = 0;  // rows [lo, hi)
   int index = 0;           // global shard index
@@ -97,12 +122,16 @@ struct Workspace {
   int eval_blocks = 0;  // k_point_eval grid
   int eval_tpi = 4;     // k_point_eval threads per index
   int pfmt = 0;  // PartialFormat of rowp/colp written by the sweep
+  bool use_tc = false;  // fp32 points sweeps run sweep_tc_f32 (tensor-core exponents)
   int strip = 256;
   size_t sweep_smem = 0;
   size_t one_smem = 0;  // sweep_pts1_f32 (one-sided z_check' sweep)
   DevBuf<double> slots;     // 7 dual points
   DevBuf<double> sums;      // 6 x (row, col)
   DevBuf<double> rowp, colp, maxp, scratch, partial;
+  DevBuf<float> carry, carry_b;  // carried shifts of the points sweep (sweep_pts2_f32): [strip][n], [vshard][n]
+  DevBuf<unsigned> carry_ticket; // [vshard][strip]
+  DevBuf<unsigned long long> carry_stats;  // CTAs of sweep_pts2_f32 launches: carried, exact
   DevBuf<double> dpart, gpart;  // deferred-decision partials: k_point_eval (defer) / k_gk_update (scaled point)
   DevBuf<int> gflag;            // non-finite Greenkhorn update seen (k_gk_update)
   DevBuf<double> rt, ct;    // marginals the dual targets
@@ -144,7 +173,12 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   } else {
     const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
     switch (pts_pairs()) {
-      case 2: PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32<1>, kThreads, sm_est)); break;
+      case 2:
+        PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sweep_pts2_smem(int(kMaxRowsPerCta)))));
+        PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32<1>, kThreads,
+                                                            sweep_pts2_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)))));
+        break;
       case 5:
         PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(sweep_pts_smem(int(kMaxRowsPerCta)))));
@@ -162,10 +196,16 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     }
   }
   occ = std::max(occ, 1);
+  const bool use_tc = carry_supported(P) && tc_enabled();
+  ws.use_tc = use_tc;
   ws.strip = P.dtype == POTGPU_F64 ? kStripCols : (P.dot_form() ? 64 * ((pts_pairs() == 2 || pts_pairs() == 3 || pts_pairs() == 5) ? kPairs : pts_pairs()) : kStripCols32);
   const int64_t max_rows = (P.dot_form() && pts_pairs() == 3) ? kMaxRowsPerCtaS : kMaxRowsPerCta;
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
-  ws.g = choose_grid(n, n, cx.num_sms, occ, ws.strip, max_rows);
+  const int64_t tc_cap = int64_t(cx.num_sms) * 4;
+  if (use_tc) {
+    PG_CK(cudaFuncSetAttribute(sweep_tc_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sweep_tc_smem())));
+  }
+  ws.g = use_tc ? choose_grid_tc(n, n, tc_cap) : choose_grid(n, n, cx.num_sms, occ, ws.strip, max_rows);
   int64_t max_rb = ws.g.grid.y;
   int max_rpc = ws.g.rows_per_cta;
   ws.shards.clear();
@@ -176,7 +216,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
       sg.index = cx.comm.shard_index(p);
       sg.lo = cx.comm.lo(n, sg.index);
       sg.hi = cx.comm.hi(n, sg.index);
-      sg.g = choose_grid(n, sg.hi - sg.lo, cx.num_sms, occ, ws.strip, max_rows);
+      sg.g = use_tc ? choose_grid_tc(n, sg.hi - sg.lo, tc_cap) : choose_grid(n, sg.hi - sg.lo, cx.num_sms, occ, ws.strip, max_rows);
       max_rb = std::max<int64_t>(max_rb, sg.g.grid.y);
       max_rpc = std::max(max_rpc, sg.g.rows_per_cta);
       ws.shards.push_back(sg);
@@ -185,9 +225,9 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     ws.xsend.alloc(size_t(cx.comm.vshards * ws.xstride));
     ws.xrecv.alloc(size_t(ws.xstride));
   }
-  ws.pts_cs = (P.dot_form() && pts_pairs() == 2) ? pts_cluster(ws.g.grid.x) : 1;
+  ws.pts_cs = (P.dot_form() && pts_pairs() == 2 && !use_tc) ? pts_cluster(ws.g.grid.x) : 1;
   for (const ShardGrid& sh : ws.shards) ws.pts_cs = std::min(ws.pts_cs, pts_cluster(sh.g.grid.x));
-  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts_smem(max_rpc, ws.pts_cs > 1), sweep_f32_smem(max_rpc));
+  ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts2_smem(max_rpc, ws.pts_cs > 1), sweep_f32_smem(max_rpc));
   if (P.dtype != POTGPU_F64) {
     PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
     PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
@@ -204,6 +244,19 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     PG_CK(cudaFuncSetAttribute(sweep_pts_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
   }
   ws.nstrips = ws.g.grid.x / ws.pts_cs;
+  if (carry_supported(P) && ws.pts_cs == 1) {
+    // -inf carries: the first launch of a row segment takes the exact path
+    const int vsh = std::max(1, cx.comm.sharded() ? cx.comm.vshards : 1);
+    ws.carry.alloc(size_t(ws.g.grid.x) * size_t(n));
+    ws.carry_b.alloc(size_t(vsh) * size_t(n));
+    ws.carry_ticket.alloc(size_t(vsh) * ws.g.grid.x);
+    launch_k(k_fill_f32, dim3(cx.num_sms), dim3(kVecThreads), 0, cx.stream, ws.carry.p, int64_t(ws.g.grid.x) * n,
+             -INFINITY);
+    launch_k(k_fill_f32, dim3(cx.num_sms), dim3(kVecThreads), 0, cx.stream, ws.carry_b.p, int64_t(vsh) * n, NAN);
+    ws.carry_ticket.zero(cx.stream);
+    ws.carry_stats.alloc(2);
+    ws.carry_stats.zero(cx.stream);
+  }
   ws.nrb = ws.g.grid.y;
   ws.nmax = int64_t(ws.g.grid.x) * ws.g.grid.y;
   ws.nblk = int(std::min<int64_t>(cx.num_sms, std::max<int64_t>(1, ceil_div(n, kVecThreads))));
@@ -243,7 +296,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
 inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const double* lu, const double* lv,
                          const int* gate, bool floor_exp, double gamma, const ShardGrid* sh = nullptr) {
   const SweepGrid& g = sh ? sh->g : ws.g;
-  SweepArgs a;
+  SweepArgs a{};
   a.n = P.n;
   a.row_lo = sh ? sh->lo : 0;
   a.row_hi = sh ? sh->hi : P.n;
@@ -255,6 +308,15 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
   a.rowp = ws.rowp.p; a.colp = ws.colp.p; a.maxp = ws.maxp.p;
   a.gate = gate;
   a.gamma = gamma;
+  if (ws.carry.p && pts_pairs() == 2 && ws.pts_cs == 1 && P.dot_form()) {
+    const int64_t k = sh ? int64_t(sh - ws.shards.data()) : 0;
+    a.carry = ws.carry.p;
+    a.carry_b = ws.carry_b.p + k * P.n;
+    a.carry_ticket = ws.carry_ticket.p + k * g.grid.x;
+    a.carry_stats = ws.carry_stats.p;
+    static const int dbg = [] { const char* e = std::getenv("POTGPU_TC_DEBUG"); return e ? std::atoi(e) : 0; }();
+    a.tc_debug = dbg;
+  }
   if (P.dtype == POTGPU_F64) {
     if (floor_exp) launch_k(sweep_f64_dense<true>, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, a);
     else launch_k(sweep_f64_dense<false>, dim3(g.grid), dim3(kThreads), 0, cx.stream, P.L64.p, P.ld, a);
@@ -272,7 +334,10 @@ inline void launch_sweep(Context& cx, const DevProblem& P, Workspace& ws, Slot z
           case 8: launch_kc(sweep_pts2_f32<8>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 8, s, a); break;
           case 4: launch_kc(sweep_pts2_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 4, s, a); break;
           case 2: launch_kc(sweep_pts2_f32<2>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, 2, s, a); break;
-          default: launch_k(sweep_pts2_f32<1>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
+          default:
+            if (ws.use_tc && a.carry) launch_k(sweep_tc_f32, dim3(g.grid), dim3(kTcThreads), sweep_tc_smem(), cx.stream, s, a);
+            else launch_k(sweep_pts2_f32<1>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a);
+            break;
         }
         break;
       case 4: launch_k(sweep_pts_f32<4>, dim3(g.grid), dim3(kThreads), ws.sweep_smem, cx.stream, s, a); break;
@@ -377,12 +442,12 @@ inline bool one_sided_supported(const Context& cx, const DevProblem& P) {
     const char* e = std::getenv("POTGPU_ONE_SIDED");
     return !(e && e[0] == '0');
   }();
-  return on && P.dtype == POTGPU_F32 && P.dot_form() && !cx.comm.sharded() && pts_pairs() == 2 && true;
+  return on && P.dtype == POTGPU_F32 && P.dot_form() && !cx.comm.sharded() && pts_pairs() == 2;
 }
 
 inline void launch_one_sided(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const int* gate, const OneSidedArgs& o) {
   const SweepGrid& g = ws.g;
-  SweepArgs a;
+  SweepArgs a{};
   a.n = P.n;
   a.row_lo = 0;
   a.row_hi = P.n;

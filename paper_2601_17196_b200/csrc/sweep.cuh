@@ -37,6 +37,12 @@ struct SweepArgs {
   double* maxp;         // [gridDim.y][gridDim.x]: max exponent (natural log units)
   const int* gate;      // kernel runs iff *gate != 0 (null: always)
   double gamma;         // for fp32 sources: exponent scale log2(e)/gamma folded in src
+  // carried shifts of the points sweep (sweep_pts2_f32; null: exact path only)
+  float* carry;             // [strip][n]: c_i of the last launch (log2 units, t' frame)
+  float* carry_b;           // [n]: that launch's column constants B_j (one array per row shard)
+  unsigned* carry_ticket;   // [strips]: last-CTA tickets (one array per row shard)
+  unsigned long long* carry_stats;  // [2]: CTAs that took the carried / the exact path
+  int tc_debug;  // timing experiments of sweep_tc_f32 ($POTGPU_TC_DEBUG; 0 = normal)
 };
 
 // ------------------------------------------------------------------------
@@ -592,6 +598,36 @@ __global__ void __launch_bounds__(kThreads, (KP <= 4 ? 3 : 2)) sweep_pts_f32(Src
 // of the cluster's CS strips are merged through distributed shared memory
 // before they are written (one partial per row per cluster: CS x fewer for
 // the evaluation to read).
+//
+// Carried shifts (a.carry != null, CS == 1). The exact path above serialises
+// every row: segment max -> CREDUX -> shift -> 32-wide MUFU burst, and the
+// warps of a scheduler fall into lock step (all in their FMA phase with the
+// MUFU idle, then all in the MUFU burst). The shift only has to be an upper
+// bound of the row segment's max within ~60 log2 units (fp32 keeps its
+// relative precision at any magnitude; only over- and underflow matter), and
+// one is known before the sweep starts:
+//   t'_ij = B_j + 2 x'_i . y'_j   (the row offset A_i is not in t'),
+//   max_j t'_new <= max_j t'_old + max_j (B_new - B_old)_j  over the strip,
+// and the previous launch left c_i = s_i + log2(sum_j 2^(t'_old - s_i)), which
+// lies in [max t'_old, max t'_old + log2(512)]. So s_i = c_i + dB_max bounds
+// the new max from above with slack <= 9 + (dB_max - dB_min). A CTA whose
+// strip moved by at most kCarrySpread takes this path: no max tree, no
+// CREDUX, no per-row column-scale MUFU (one CTA-wide column scale sigma,
+// f_i = 2^(s_i + A_i - sigma) formed in the prologue), and each pair's MUFU
+// depends only on its own 3-FFMA2 chain, so the MUFU work interleaves freely
+// with the FMA work. Row partials are (sum, s_i): the same format. The max
+// exponent of the CTA (the reference's 700 overflow test, dual.hpp:85-90) is
+// reported as the bound max_i (c_i^new + A_i) (exact to within 9 log2 units)
+// and recomputed exactly when that bound is within 10 of the threshold.
+// Every launch (either path) writes its carries c_i and its column constants
+// (the latter by the strip's last CTA, by ticket), so the state stays
+// consistent whichever launch ran last.
+constexpr float kCarrySpread = 48.f;
+__host__ __device__ constexpr size_t sweep_pts2_smem(int rows_per_cta, bool cluster_merge = false) {
+  // + (f_i, A_i) per row for the carried path
+  return sweep_pts_smem(rows_per_cta, cluster_merge) + size_t(rows_per_cta) * sizeof(float2);
+}
+
 template <int CS>
 __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 src, SweepArgs a) {
   pdl_wait();
@@ -603,18 +639,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   const int64_t j0 = int64_t(blockIdx.x) * kStrip;
   const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
   const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  const int nrows = int(r1 - r0);
   const double w = *a.w;
-  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i), then the row-sum tiles
+  const bool use_carry = CS == 1 && a.carry != nullptr;
+  extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i) or (2x', s_i), then the row-sum tiles, then (f_i, A_i)
   __shared__ float2 s_B[KP][32];
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
-    double ud = a.u[i];
-    if (a.lu) ud = ud + a.lu[i];
-    double A = (ud + w) * kLog2e;
-    if (a.rowshift) A = A + a.rowshift[i];
-    const float4 x2 = src.X2[i];
-    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
-  }
+  __shared__ float s_red[3][kWarps];
+  float2* s_FA = reinterpret_cast<float2*>(reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33 +
+                                           (CS > 1 ? 2 * a.rows_per_cta : 0));
   float2 cx[KP], cy[KP], cz[KP];
+  float dmax = -INFINITY, dmin = INFINITY;
+  int dbad = 0;
 #pragma unroll
   for (int q = 0; q < KP; ++q) {
     float b[2];
@@ -632,18 +667,79 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
         y[h] = src.Ys[j];
       }
       b[h] = float(vv);
+      if (use_carry && j < n) {
+        const float bo = a.carry_b[j];
+        if (!(b[h] == -INFINITY && bo == -INFINITY)) {  // a column masked before and after moves nothing
+          const float d = b[h] - bo;
+          dbad |= !(fabsf(d) < 1e30f);  // NaN, +-inf: a column appeared, vanished or is not finite
+          dmax = fmaxf(dmax, d);
+          dmin = fminf(dmin, d);
+        }
+      }
     }
     if (warp == 0) s_B[q][lane] = make_float2(b[0], b[1]);
     cx[q] = make_float2(y[0].x, y[1].x);
     cy[q] = make_float2(y[0].y, y[1].y);
     cz[q] = make_float2(y[0].z, y[1].z);
   }
+  bool carried = false;
+  float dBmax = 0.f;
+  if (use_carry) {
+    dbad = __any_sync(0xffffffffu, dbad);
+    dmax = warp_maxf(dmax);
+    dmin = -warp_maxf(-dmin);
+    if (lane == 0) { s_red[0][warp] = dmax; s_red[1][warp] = dmin; s_red[2][warp] = dbad ? 1.f : 0.f; }
+    __syncthreads();
+    float dx = -INFINITY, dn = INFINITY, bad = 0.f;
+    for (int ww = 0; ww < kWarps; ++ww) { dx = fmaxf(dx, s_red[0][ww]); dn = fminf(dn, s_red[1][ww]); bad += s_red[2][ww]; }
+    carried = bad == 0.f && dx > -INFINITY && dx - dn <= kCarrySpread;
+    dBmax = dx;
+    __syncthreads();  // s_red is reused below
+  }
+  // rows: (2x', A_i), or for the carried path (2x', s_i) and (f_i, A_i)
+  float lsig = -INFINITY;
+  int rbad = 0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+    double ud = a.u[i];
+    if (a.lu) ud = ud + a.lu[i];
+    double A = (ud + w) * kLog2e;
+    if (a.rowshift) A = A + a.rowshift[i];
+    const float4 x2 = src.X2[i];
+    const float Af = float(A);
+    if (carried) {
+      const float si = a.carry[int64_t(blockIdx.x) * n + i] + dBmax;
+      rbad |= !(fabsf(si) < 1e30f) || !(fabsf(Af) < 1e30f);
+      lsig = fmaxf(lsig, si + Af);
+      s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, si);
+      s_FA[i - r0] = make_float2(0.f, Af);
+    } else {
+      s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, Af);
+      if (use_carry) s_FA[i - r0] = make_float2(0.f, Af);
+    }
+  }
+  float sigma_c = -INFINITY;
+  if (carried) {
+    rbad = __syncthreads_or(rbad);
+    lsig = warp_maxf(lsig);
+    if (lane == 0) s_red[0][warp] = lsig;
+    __syncthreads();
+    for (int ww = 0; ww < kWarps; ++ww) sigma_c = fmaxf(sigma_c, s_red[0][ww]);
+    if (rbad || !(sigma_c > -INFINITY)) {
+      carried = false;  // CTA-uniform: back to the exact path, rows as (2x', A_i)
+      for (int k = threadIdx.x; k < nrows; k += kThreads) s_R[k].w = s_FA[k].y;
+    } else {
+      for (int k = threadIdx.x; k < nrows; k += kThreads) s_FA[k].x = ex2f(s_R[k].w + s_FA[k].y - sigma_c);
+    }
+  }
   __syncthreads();
+  if (use_carry && a.carry_stats && threadIdx.x == 0) atomicAdd(a.carry_stats + (carried ? 0 : 1), 1ull);
   float2 cacc[KP];
 #pragma unroll
   for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
-  float sigma = -INFINITY;
+  float sigma = carried ? sigma_c : -INFINITY;
   float mmax = -INFINITY;
+  float ubmax = -INFINITY;  // carried: max over flushed rows of c_i + A_i
+  int ubnan = 0;
   float2* rowp = reinterpret_cast<float2*>(a.rowp);
   float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
   float2* s_rp = reinterpret_cast<float2*>(reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33);  // [rows]
@@ -659,16 +755,24 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
-      const float2 part = make_float2((s0 + s1) + (s2 + s3), my_ms);
-      if constexpr (CS > 1) s_rp[ib + int64_t(kWarps) * lane - r0] = part;
-      else rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = part;
+      const float sum = (s0 + s1) + (s2 + s3);
+      const int64_t row = ib + int64_t(kWarps) * lane;
+      const float2 part = make_float2(sum, my_ms);
+      if constexpr (CS > 1) s_rp[row - r0] = part;
+      else rowp[row * ldp + blockIdx.x] = part;
+      if (use_carry) {
+        float lg;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(sum));
+        const float c = my_ms + lg;  // -inf for an empty segment
+        a.carry[int64_t(blockIdx.x) * n + row] = c;
+        const float ub = c + s_FA[row - r0].y;
+        ubnan |= ub != ub;
+        ubmax = fmaxf(ubmax, ub);
+      }
     }
     __syncwarp();
   };
-  // one row's tile slot, column scale update and accumulation
-  auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
-    const float ms = (m == -INFINITY) ? 0.f : m;
-    *tslot = tree_sum2<KP>(p);
+  auto next_slot = [&](float ms, int64_t i) {
     tslot += 33;
     if (lane == slot) my_ms = ms;
     if (++slot == 32) {
@@ -677,6 +781,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       tslot = tile + lane;
       ib = i + kWarps;
     }
+  };
+  // exact path: one row's tile slot, column scale update and accumulation
+  auto finish_row = [&](float m, float Ai, const float2 (&p)[KP], int64_t i) {
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    *tslot = tree_sum2<KP>(p);
+    next_slot(ms, i);
     const float mA = (m == -INFINITY) ? -INFINITY : m + Ai;
     if (mA > sigma) {
       const float sc = ex2f(sigma - mA);
@@ -690,60 +800,134 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
 #pragma unroll
     for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
   };
+  // carried path: exponents at the carried shift, column scale f_i precomputed
+  auto finish_row_c = [&](float si, float fi, const float2 (&p)[KP], int64_t i) {
+    *tslot = tree_sum2<KP>(p);
+    next_slot(si, i);
+    const float2 F2 = make_float2(fi, fi);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+  };
   int64_t i = r0 + warp;
-  for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
-    const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
-    float2 ta[KP], tb[KP];
+  if (carried) {
+    for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
+      const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+      const float fa = s_FA[i - r0].x, fb = s_FA[i + kWarps - r0].x;
+      float2 ta[KP], tb[KP];
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      const float2 B = s_B[q][lane];
-      float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
-      float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
-      xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
-      xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
-      ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
-      tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+      for (int q = 0; q < KP; ++q) {
+        const float2 B = s_B[q][lane];
+        float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+        float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
+        xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+        xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
+        xa = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+        xb = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+        const float2 d = __fadd2_rn(xa, make_float2(-da.w, -da.w));
+        const float2 e = __fadd2_rn(xb, make_float2(-db.w, -db.w));
+        ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+        tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+      }
+      finish_row_c(da.w, fa, ta, i);
+      finish_row_c(db.w, fb, tb, i + kWarps);
     }
-    float ma = tree_max2<KP>(ta), mb = tree_max2<KP>(tb);
-    ma = warp_maxf(ma);
-    mb = warp_maxf(mb);
-    const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
+    if (i < r1) {
+      const float4 da = s_R[i - r0];
+      const float fa = s_FA[i - r0].x;
+      float2 ta[KP];
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
-      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
-      const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
-      tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+      for (int q = 0; q < KP; ++q) {
+        const float2 B = s_B[q][lane];
+        float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+        xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+        xa = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+        const float2 d = __fadd2_rn(xa, make_float2(-da.w, -da.w));
+        ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      }
+      finish_row_c(da.w, fa, ta, i);
     }
-    finish_row(ma, da.w, ta, i);
-    finish_row(mb, db.w, tb, i + kWarps);
-  }
-  if (i < r1) {  // a last single row
-    const float4 da = s_R[i - r0];
-    float2 ta[KP];
+  } else {
+    for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
+      const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+      float2 ta[KP], tb[KP];
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      const float2 B = s_B[q][lane];
-      float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
-      xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
-      ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+      for (int q = 0; q < KP; ++q) {
+        const float2 B = s_B[q][lane];
+        float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+        float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
+        xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+        xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
+        ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+        tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+      }
+      float ma = tree_max2<KP>(ta), mb = tree_max2<KP>(tb);
+      ma = warp_maxf(ma);
+      mb = warp_maxf(mb);
+      const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+        ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+        const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
+        tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+      }
+      finish_row(ma, da.w, ta, i);
+      finish_row(mb, db.w, tb, i + kWarps);
     }
-    float ma = fmaxf(ta[0].x, ta[0].y);
+    if (i < r1) {  // a last single row
+      const float4 da = s_R[i - r0];
+      float2 ta[KP];
 #pragma unroll
-    for (int q = 1; q < KP; ++q) ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
-    ma = warp_maxf(ma);
-    const float msa = (ma == -INFINITY) ? 0.f : ma;
+      for (int q = 0; q < KP; ++q) {
+        const float2 B = s_B[q][lane];
+        float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+        xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+        ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+      }
+      float ma = fmaxf(ta[0].x, ta[0].y);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
-      ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      for (int q = 1; q < KP; ++q) ma = fmaxf(ma, fmaxf(ta[q].x, ta[q].y));
+      ma = warp_maxf(ma);
+      const float msa = (ma == -INFINITY) ? 0.f : ma;
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 d = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+        ta[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      }
+      finish_row(ma, da.w, ta, i);
     }
-    finish_row(ma, da.w, ta, i);
   }
   if (slot > 0) flush(slot);
   __shared__ float cs[kWarps][kStrip];
   __shared__ float ss[kWarps];
   __shared__ float mm[kWarps];
+  if (carried) {
+    // the bound of the CTA's max exponent; exact when it is near the
+    // reference's overflow threshold (kMaxExponent, natural log units)
+    ubnan = __any_sync(0xffffffffu, ubnan);
+    float ub = ubnan ? NAN : warp_maxf(ubmax);
+    if (lane == 0) s_red[0][warp] = ub;
+    __syncthreads();
+    float cub = s_red[0][0];
+    for (int ww = 1; ww < kWarps; ++ww) cub = (cub != cub || s_red[0][ww] != s_red[0][ww]) ? NAN : fmaxf(cub, s_red[0][ww]);
+    mmax = cub;
+    if (double(cub) * kLn2 > kMaxExponent - 10.0) {  // CTA-uniform, rare: the exact max of t' + A_i
+      mmax = -INFINITY;
+      for (int64_t k = r0 + warp; k < r1; k += kWarps) {
+        const float4 d = s_R[k - r0];
+        float2 t[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 B = s_B[q][lane];
+          float2 x = __ffma2_rn(make_float2(d.x, d.x), cx[q], B);
+          x = __ffma2_rn(make_float2(d.y, d.y), cy[q], x);
+          t[q] = __ffma2_rn(make_float2(d.z, d.z), cz[q], x);
+        }
+        const float m = warp_maxf(tree_max2<KP>(t));
+        if (m != -INFINITY) mmax = fmaxf(mmax, m + s_FA[k - r0].y);
+      }
+    }
+  }
   if (lane == 0) {
     ss[warp] = sigma;
     mm[warp] = mmax;
@@ -772,7 +956,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     const int rank = int(cl.block_rank());
-    const int nrows = int(r1 - r0);
     const int64_t ldc = gridDim.x / CS;
     const int64_t col = blockIdx.x / CS;
     for (int lr = rank * kThreads + threadIdx.x; lr < nrows; lr += CS * kThreads) {
@@ -794,8 +977,28 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   }
   if (threadIdx.x == 0) {
     float m = mm[0];
-    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+    for (int ww = 1; ww < kWarps; ++ww) m = (m != m || mm[ww] != mm[ww]) ? NAN : fmaxf(m, mm[ww]);
     a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+  }
+  if (use_carry) {
+    // the strip's column constants for the next launch: written by the last
+    // CTA of the strip, after every CTA of it has read the previous ones
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(a.carry_ticket + blockIdx.x, 1u) == gridDim.y - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      for (int k = threadIdx.x; k < kStrip; k += kThreads) {
+        const int q = k >> 5, l = k & 31;
+        const float2 b = s_B[q][l];
+        const int64_t jj = f32_col(j0, l, q, 0);
+        if (jj < n) a.carry_b[jj] = b.x;
+        if (jj + 1 < n) a.carry_b[jj + 1] = b.y;
+      }
+      if (threadIdx.x == 0) a.carry_ticket[blockIdx.x] = 0u;
+    }
   }
 }
 
@@ -1435,6 +1638,25 @@ inline int pts_cluster(int64_t strips) {
 }
 
 constexpr int64_t kMaxRowsPerCta = 2048;
+
+// Grid of the tensor-core points sweep (sweep_tc.cuh): strips of 512
+// columns, row blocks of 128 x tiles rows; tiles (1..4) chosen for the
+// fullest last wave of `cap` resident CTAs, preferring more rows per CTA
+// (the column sums' cross-lane combine is paid once per tile group).
+inline SweepGrid choose_grid_tc(int64_t ncols, int64_t nrows, int64_t cap, int max_tiles = 4) {
+  const int64_t strips = ceil_div(ncols, 512);
+  int best_t = max_tiles;
+  double best = -1.0;
+  for (int t = max_tiles; t >= 2; --t) {
+    const int64_t ctas = strips * ceil_div(std::max<int64_t>(nrows, 1), 128 * t);
+    const double eff = double(ctas) / double(ceil_div(ctas, cap) * cap);
+    if (eff > best + 0.02) { best = eff; best_t = t; }
+  }
+  SweepGrid g;
+  g.rows_per_cta = 128 * best_t;
+  g.grid = dim3(unsigned(strips), unsigned(ceil_div(std::max<int64_t>(nrows, 1), g.rows_per_cta)), 1);
+  return g;
+}
 
 inline SweepGrid choose_grid(int64_t ncols, int64_t nrows, int num_sms, int occupancy, int strip_cols,
                              int64_t max_rows = kMaxRowsPerCta) {

@@ -163,6 +163,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
     "potgpu_kmeans_quantize", "potgpu_round_balanced", "potgpu_dual_matrix", "potgpu_session_read_state",
+    "potgpu_session_carry_stats",
 )
 
 _lib = None
@@ -195,6 +196,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_solve_batched.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), ctypes.c_int64, P(_Config),
                                          P(_Summary), P(_Outputs), ctypes.c_int]
     lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
+    lib.potgpu_session_carry_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64)]
     lib.potgpu_reg_config_default.argtypes = [P(_RegConfig)]
     lib.potgpu_register_point_clouds.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, ctypes.c_int64, dp, ctypes.c_int64,
                                                  P(_RegConfig), P(_Config), ctypes.c_int, P(_RegResult), P(_RegRecord),
@@ -597,6 +599,13 @@ class Session:
         ms, el, by = np.zeros(1), np.zeros(1), np.zeros(1)
         _check(self.lib.potgpu_session_time_sweep(self._h, int(reps), _dp(ms), _dp(el), _dp(by)))
         return float(ms[0]), float(el[0]), float(by[0])
+
+    def carry_stats(self):
+        """(carried, exact): CTAs of the fp32 points sweep that used a carried
+        shift / the exact row maxima so far."""
+        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(self.lib.potgpu_session_carry_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)
 
     def stats(self):
         """(kernel launches by iterate(), attempts, sweeps) so far."""
