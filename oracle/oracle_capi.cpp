@@ -3,6 +3,7 @@
 //
 // Matrices cross this boundary ROW-MAJOR (numpy default); the oracle keeps
 // the reference's column-major layout internally.
+#include <algorithm>
 #include <random>
 #include <cstring>
 
@@ -49,9 +50,19 @@ int oracle_solve(int kind, long n, const double* C, const double* r, const doubl
   try {
     Instance in = make_instance(n, X ? nullptr : C, r, c, s);
     if (X) {
-      // Points mode: C is never materialised; `scale` normalises max C to 1.
+      // Points mode: C is never materialised. max_cost (core.hpp:117) is the
+      // max of the fp64 costs scale * |x_i - y_j|^2 themselves (one pass;
+      // with scale = 1 / max d^2 it can be 1 + 1 ulp).
       in.points_mode = true;
-      in.cmax_hint = 1.0;
+      LogK lk;
+      lk.n = n; lk.X = X; lk.Y = Y; lk.d = d; lk.scale = scale;
+      std::vector<double> rowmax(static_cast<size_t>(n), 0.0);
+      parallel_for(n, [&](long i) {
+        double m = 0.0;
+        for (long j = 0; j < n; ++j) m = std::max(m, lk.cost(i, j));
+        rowmax[size_t(i)] = m;
+      });
+      in.cmax_hint = n > 0 ? *std::max_element(rowmax.begin(), rowmax.end()) : 0.0;
     }
     SolverConfig sc;
     sc.epsilon = cfg[0];

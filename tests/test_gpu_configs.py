@@ -88,6 +88,54 @@ def test_c2_tuned_sinkhorn_full(ctx, dtype, p):
         check_properties(g, inst.s, TOL_F32_VIOL)
 
 
+@pytest.mark.slow
+def test_c2_tuned_sinkhorn_p1_capped(ctx):
+    """p = 1: gamma = 2 eps / (49 H_min) is tiny and the solve is long; both
+    capped at 300 iterations: same status and trace (fp64)."""
+    inst = pot.config_instance(2)
+    cfg = pot.SolverConfig(epsilon=1e-3, tuning_exponent_p=1.0, log_every=50, max_iterations=300,
+                           record_rounded_cost=False, materialize_plan=False)
+    g = pot.tuned_sinkhorn_solve(inst, cfg, ctx=ctx)
+    o = binding.solve(2, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-3, p=1.0, max_iterations=300, log_every=50,
+                      skip_plan=True)
+    assert int(g.status) == o.status and g.iterations == o.iterations
+    assert g.gamma == o.gamma and g.tolerance == o.tolerance
+    assert [r.t for r in g.trace] == [int(x) for x in o.trace[:, 0]]
+    np.testing.assert_allclose([r.error for r in g.trace], o.trace[:, 1], rtol=1e-9)
+
+
+@pytest.mark.slow
+def test_c2_feasible_sinkhorn_full(ctx):
+    """n = 4096 fp64, eps = 1e-3, feasible Sinkhorn (the ASPOT gamma) to convergence."""
+    inst = pot.config_instance(2)
+    cfg = pot.SolverConfig(epsilon=1e-3, log_every=10 ** 9, materialize_plan=False, max_iterations=20000)
+    g = pot.feasible_sinkhorn_solve(inst, cfg, ctx=ctx)
+    o = binding.solve(1, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-3, max_iterations=20000, want_plan=False)
+    assert int(g.status) == o.status and g.iterations == o.iterations
+    assert abs(g.cost - o.cost) <= TOL_F64_OBJ * abs(o.cost)
+    check_properties(g, inst.s, TOL_F64_VIOL)
+
+
+@pytest.mark.slow
+def test_c2_aspot_prefix_fp32(ctx):
+    """n = 4096 fp32 stored cost: 12 iterations against the fp64 oracle on the
+    fp32-rounded C; decisions identical until the first fp32 near-tie of
+    z_best, E_t and phi to the fp32 bars up to there."""
+    inst = pot.config_instance(2, dtype=pot.DType.F32)
+    cfg = pot.SolverConfig(epsilon=1e-3, log_every=10 ** 9, max_iterations=12, collect_iter_log=True,
+                           materialize_plan=False)
+    g = pot.aspot_solve(inst, cfg, ctx=ctx, iter_log_cap=100)
+    o = binding.solve(0, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-3, max_iterations=12, skip_plan=True)
+    assert g.iterations == o.iterations == 12
+    diff = np.flatnonzero((g.iter_log[:, 1:5] != o.log[:, 1:5]).any(axis=1))
+    k = int(diff[0]) if len(diff) else 12
+    assert k >= 2
+    np.testing.assert_allclose(g.iter_log[:k, 5], o.log[:k, 5], rtol=1e-4)
+    np.testing.assert_allclose(g.iter_log[:k, 6:8], o.log[:k, 6:8], rtol=1e-6)
+    if k < 12:
+        assert abs(o.log[k - 1, 6] - o.log[k, 7]) <= 1e-5 * abs(o.log[k, 7]), (o.log, g.iter_log)
+
+
 # ---------------------------------------------------------- configs[2] --
 @pytest.mark.slow
 def test_c3_aspot_prefix_and_full(ctx):

@@ -1,0 +1,118 @@
+"""Parity at the headline sizes, to convergence (VERDICT r01 "next" item 1).
+
+configs[2] (n = 16384, the bench workload) is solved twice on the device:
+the fp32 on-the-fly headline path, and an fp64 anchor on the SAME
+fp32-rounded coordinates (C materialised once in fp64 on the device, logK =
+-C/gamma by IEEE division, the reference's fp64 semantics). The anchor is
+pinned to the CPU oracle (points mode, all host threads) by a 20-iteration
+prefix with identical decisions; the fp32 solve is then compared with the
+anchor at convergence on north_star's fp32 bars (objective 1e-4, violation
+1e-5) plus the iteration count. configs[3] (n = 65536) gets a 3-iteration
+ASPOT prefix against the oracle in points mode.
+
+Measured on B200 (profiles/c3_anchor.py, profiles/r02/c3_anchor.jsonl): both
+C3 solves converge in 2360 iterations; one decision differs (iteration 2, a
+fp32 near-tie of z_best); cost 1.50389e-3 vs 1.50391e-3 (rel 1.2e-5); phi
+rel 8e-10."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import binding
+from paper_2601_17196_b200 import pot
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL_F32_OBJ, TOL_F32_VIOL = 1e-4, 1e-5
+
+
+@pytest.fixture(autouse=True)
+def oracle_threads():
+    binding.lib().oracle_set_threads(os.cpu_count() or 1)
+    yield
+    binding.lib().oracle_set_threads(1)
+
+
+@pytest.fixture(scope="module")
+def c3():
+    inst = pot.config_instance(3)  # fp32-rounded coordinates
+    inst.cost_scale = pot.points_scale(inst.X, inst.Y)
+    anchor = pot.Instance(r=inst.r, c=inst.c, s=inst.s, X=inst.X, Y=inst.Y, cost_scale=inst.cost_scale,
+                          dtype=pot.DType.F64, stored=True)
+    return inst, anchor
+
+
+def cfg(**k):
+    return pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False,
+                            collect_iter_log=True, **k)
+
+
+def test_c3_fp64_anchor_prefix_is_the_oracle(ctx, c3):
+    """The anchor's first 20 iterations take the oracle's decisions (halvings,
+    both Greenkhorn blocks, z_best) bit for bit; E_t and phi to rounding."""
+    inst, anchor = c3
+    g = pot.aspot_solve(anchor, cfg(max_iterations=20), ctx=ctx, iter_log_cap=100)
+    o = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=1e-2,
+                      max_iterations=20, skip_plan=True)
+    assert g.iterations == o.iterations == 20
+    assert g.gamma == o.gamma and g.tolerance == o.tolerance
+    np.testing.assert_array_equal(g.iter_log[:, 1:5], o.log[:, 1:5])
+    np.testing.assert_allclose(g.iter_log[:, 5], o.log[:, 5], rtol=1e-9)
+    np.testing.assert_allclose(g.iter_log[:, 6:8], o.log[:, 6:8], rtol=1e-12)
+
+
+def test_c3_fp32_headline_matches_fp64_anchor_at_convergence(ctx, c3):
+    inst, anchor = c3
+    a = pot.aspot_solve(anchor, cfg(), ctx=ctx, iter_log_cap=100000)
+    f = pot.aspot_solve(inst, cfg(), ctx=ctx, iter_log_cap=100000)
+    assert a.status == f.status == pot.SolveStatus.Converged
+    # iteration count: measured equal (2360); bound 1 %
+    assert abs(f.iterations - a.iterations) <= max(2, 0.01 * a.iterations), (f.iterations, a.iterations)
+    assert abs(f.cost - a.cost) <= TOL_F32_OBJ * abs(a.cost), (f.cost, a.cost)
+    assert abs(f.phi - a.phi) <= 1e-6 * abs(a.phi)
+    assert f.feasibility_gap <= TOL_F32_VIOL and abs(f.plan.mass - inst.s) <= TOL_F32_VIOL
+    assert f.final_error <= f.tolerance and a.final_error <= a.tolerance
+    # decisions: identical except at fp32 near-ties of z_best (phi(z_check) vs phi_hat within 1e-6)
+    m = min(len(a.iter_log), len(f.iter_log))
+    diff = (a.iter_log[:m, 1:5] != f.iter_log[:m, 1:5]).any(axis=1)
+    assert diff.sum() <= 0.01 * m, int(diff.sum())
+    for k in np.flatnonzero(diff):
+        prev_check = a.iter_log[k - 1, 6] if k > 0 else a.iter_log[k, 6]
+        assert abs(prev_check - a.iter_log[k, 7]) <= 1e-6 * abs(a.iter_log[k, 7]) or \
+            a.iter_log[k, 1] != f.iter_log[k, 1] or a.iter_log[k, 2] != f.iter_log[k, 2], k
+
+
+def test_c4_aspot_prefix_matches_oracle(ctx):
+    """n = 65536 (2^32 entries, 64-bit indexing), fp32 on the fly: the first
+    3 iterations against the fp64 oracle in points mode on the same
+    fp32-rounded coordinates and the same cost normalisation."""
+    inst = pot.config_instance(4)
+    inst.cost_scale = pot.points_scale(inst.X, inst.Y, chunk=1024)
+    c = pot.SolverConfig(epsilon=1e-3, log_every=10 ** 9, max_iterations=3, collect_iter_log=True,
+                         materialize_plan=False, record_rounded_cost=False)
+    g = pot.aspot_solve(inst, c, ctx=ctx, iter_log_cap=10)
+    o = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=1e-3,
+                      max_iterations=3, skip_plan=True)
+    assert g.iterations == o.iterations == 3
+    assert g.gamma == o.gamma and g.tolerance == o.tolerance
+    diff = np.flatnonzero((g.iter_log[:, 1:5] != o.log[:, 1:5]).any(axis=1))
+    k = int(diff[0]) if len(diff) else 3
+    assert k >= 1
+    np.testing.assert_allclose(g.iter_log[:k, 5], o.log[:k, 5], rtol=1e-4)  # E_t
+    np.testing.assert_allclose(g.iter_log[:k, 6:8], o.log[:k, 6:8], rtol=1e-6)  # phi
+    if k < 3:  # a near-tie of z_best at fp32 precision
+        assert abs(o.log[k - 1, 6] - o.log[k, 7]) <= 1e-5 * abs(o.log[k, 7]), (o.log, g.iter_log)
+
+
+def test_theory_bounds_match_oracle(ctx):
+    """SolveResult.bounds (R, L, mu_f, iteration bound: solvers.hpp:146-174)
+    against the oracle's, on configs[0] and a reference fixture."""
+    for inst in (pot.config_instance(1), pot.make_synthetic_instance(40, 3, 1.0, 1.3, 0.7)):
+        g = pot.aspot_solve(inst, pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, max_iterations=2,
+                                                   materialize_plan=False), ctx=ctx)
+        o = binding.solve(0, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-2, max_iterations=2, skip_plan=True)
+        assert (g.bounds is None) == (o.bounds is None)
+        if o.bounds is not None:
+            got = (g.bounds.R, g.bounds.L, g.bounds.mu_f, g.bounds.iteration_bound)
+            np.testing.assert_allclose(got, o.bounds, rtol=1e-12)

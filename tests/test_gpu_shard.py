@@ -136,13 +136,11 @@ def test_sharded_sinkhorn_matches_oracle(kind, shards, nccl):
 
 @pytest.mark.parametrize("kind", [pot.SolverKind.Aspot, pot.SolverKind.TunedSinkhorn])
 def test_sharded_fp32_points_matches_unsharded(ctx, kind):
-    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one.
-    Converged solves: the fp32 column sums are reassociated by sharding, so
-    ASPOT may stop a few iterations apart; the rounded cost of an
-    eps-approximate plan moves by ~1e-3 relative between such neighbouring
-    stopping iterates here (the guarantee is OPT + eps with eps = 1e-2 against
-    a cost of 1.5e-3), hence the 5e-3 bound; the tight check is the
-    fixed-prefix trajectory test below."""
+    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one,
+    on north_star's fp32 objective bar. The fp32 column sums are
+    reassociated by sharding; measured on B200 for seeds 1-4
+    (tools/shard_meas.py, profiles/r02/shard_meas.jsonl): the same stopping
+    iteration and rounded costs within 5.3e-5 relative (2 and 4 shards)."""
     inst = pot.config_instance(3, n=2048)
     p = 4.0 if kind == pot.SolverKind.TunedSinkhorn else 1.0
     cfg = pot.SolverConfig(epsilon=1e-2, tuning_exponent_p=p, log_every=10 ** 9, materialize_plan=False)
@@ -150,8 +148,7 @@ def test_sharded_fp32_points_matches_unsharded(ctx, kind):
     b = pot.solve(inst, kind, cfg, ctx=sctx(4))
     assert a.status == b.status == pot.SolveStatus.Converged
     assert abs(a.iterations - b.iterations) <= max(2, 0.02 * a.iterations)
-    bound = TOL_F32_OBJ if kind != pot.SolverKind.Aspot else 5e-3
-    assert abs(a.cost - b.cost) <= bound * abs(a.cost)
+    assert abs(a.cost - b.cost) <= TOL_F32_OBJ * abs(a.cost)
     assert b.feasibility_gap <= TOL_F32_VIOL and abs(b.plan.mass - inst.s) <= TOL_F32_VIOL
 
 
