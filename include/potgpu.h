@@ -91,6 +91,17 @@ typedef struct potgpu_problem {
   const double* c;
   double s;
   int device_ptrs;
+  /* device_ptrs = 1 only: where the arrays were produced, so the solver's
+   * reads are ordered after the producer's writes (its context stream is a
+   * non-blocking stream and does not synchronise with the default stream).
+   * The __cuda_array_interface__ v3 "stream" convention:
+   *   0  = unknown: the device is synchronised before the arrays are read
+   *        (the zero-initialised default; always correct),
+   *   1  = the legacy default stream, 2 = the per-thread default stream,
+   *   -1 = the producer guarantees the arrays are complete (CAI "stream": None),
+   *   else a cudaStream_t handle: the solver's stream waits on an event
+   *        recorded on it (work queued there later is not waited for). */
+  int64_t producer_stream;
 } potgpu_problem;
 
 /* pot::SolverConfig (core.hpp:241-267) + device options. */

@@ -155,10 +155,27 @@ static void upload_dense_host(Context& cx, const double* C, int64_t count, T* ds
   BlockCache::get().free(stage[1], kChunk * sizeof(T), true);
 }
 
+// device_ptrs inputs: order the context stream (non-blocking) after the
+// producer's writes (potgpu_problem.producer_stream, CAI v3 convention).
+static void wait_for_producer(Context& cx, int64_t ps) {
+  if (ps == -1) return;
+  if (ps == 0) {
+    PG_CK(cudaDeviceSynchronize());
+    return;
+  }
+  cudaStream_t s = ps == 1 ? cudaStreamLegacy : ps == 2 ? cudaStreamPerThread : reinterpret_cast<cudaStream_t>(ps);
+  cudaEvent_t ev;
+  PG_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  PG_CK(cudaEventRecord(ev, s));
+  PG_CK(cudaStreamWaitEvent(cx.stream, ev, 0));
+  PG_CK(cudaEventDestroy(ev));
+}
+
 static void upload_problem(Context& cx, const potgpu_problem* pr, DevProblem& P) {
   if (!pr) throw Error(POTGPU_INVALID_ARGUMENT, "null problem");
   const int64_t n = pr->n;
   const bool dev = pr->device_ptrs != 0;  // r, c, C, X, Y are device pointers (e.g. CUDA tensors)
+  if (dev) wait_for_producer(cx, pr->producer_stream);
   // validation_report (core.hpp:131-169): report the FIRST violation's code.
   if (n <= 0) throw Error(POTGPU_EMPTY_INPUT, "invalid instance: marginals are empty");
   if (!pr->r || !pr->c) throw Error(POTGPU_INVALID_ARGUMENT, "null marginals");

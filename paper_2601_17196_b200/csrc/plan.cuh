@@ -107,6 +107,155 @@ __global__ void k_sum_moment_parts(const double* part, int64_t nrb, int64_t n, d
   }
 }
 
+// ------------------------------------------------------------------------
+// fp32 output stage: round_pot's final row sums and <C, X> in ONE pass over
+// the plan (rounding.hpp:57-77 + core.hpp:199-204). For the final plan
+//   X = diag(Pf) B diag(Qf) + a0 b0^T + a1 b1^T,  Pf = (alpha rho) P0, Qf = Q0 kap
+// every n^2 quantity the output stage needs is a per-row sum over the
+// weights known before the pass (lu = log P0, lv = log(Q0 kap), b0, b1):
+//   R_i  = sum_j P0_i B_ij Qf_j          (the final row sums)
+//   W_i  = sum_j C_ij P0_i B_ij Qf_j     (<C, X> = sum_i alpha rho_i W_i + ...)
+//   K0_i = sum_j C_ij b0_j,  K1_i = sum_j C_ij b1_j   (the rank-1 terms)
+// Exponents as the fp32 sweeps (log2 units relative to each row segment's
+// exact max, the row potential added back in fp64 by k_rowcost_reduce), the
+// cost c_ij in fp32: the stored C, or |x_i - y_j|^2 of the raw coordinates
+// (cost_scale applied in fp64 by the reduce). The dense plan (materialize)
+// and fp64 problems keep k_plan_cost.
+struct RowCostArgs {
+  int64_t n, row_lo, row_hi;
+  int rows_per_cta;
+  const double* u; const double* v; const double* w;
+  const double* lv;                  // log column weights (may be null)
+  const double* b0; const double* b1;  // rank-1 column factors (may be null)
+  float g;                           // log2 e / gamma (dense C) or log2 e cost_scale / gamma (points)
+  float4* part;                      // [row][strip]: (R, W) relative to 2^m, (K0, K1)
+  float* pm;                         // [row][strip]: m
+};
+
+template <bool POINTS>
+__global__ void __launch_bounds__(kThreads, 2) k_rowcost_f32(const float* __restrict__ C, int64_t ld,
+                                                             const float4* __restrict__ X, const float4* __restrict__ Y,
+                                                             RowCostArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  // the rank-1 column factors in shared memory (registers hold B_j and y_j)
+  __shared__ float2 s_c0[kStripCols32 / 2], s_c1[kStripCols32 / 2];
+  for (int k = threadIdx.x; k < kStripCols32; k += kThreads) {
+    const int64_t j = j0 + k;
+    reinterpret_cast<float*>(s_c0)[k] = (j < n && a.b0) ? float(a.b0[j]) : 0.f;
+    reinterpret_cast<float*>(s_c1)[k] = (j < n && a.b1) ? float(a.b1[j]) : 0.f;
+  }
+  float2 Bj[kPairs];
+  float2 yx[kPairs], yy[kPairs], yz[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) {
+    float b[2];
+    float4 y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;  // padding column: exp2(-inf) = 0
+      y[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        vv = vv * kLog2e;
+        if (POINTS) y[h] = Y[j];
+      }
+      b[h] = float(vv);
+    }
+    Bj[q] = make_float2(b[0], b[1]);
+    yx[q] = make_float2(y[0].x, y[1].x);
+    yy[q] = make_float2(y[0].y, y[1].y);
+    yz[q] = make_float2(y[0].z, y[1].z);
+  }
+  __syncthreads();
+  const bool has_b1 = a.b1 != nullptr;
+  const float2 G = make_float2(-a.g, -a.g);
+  const int64_t ldp = gridDim.x;
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    float2 c[kPairs];
+    if constexpr (POINTS) {
+      const float4 xi = X[i];
+      const float2 px = make_float2(-xi.x, -xi.x), py = make_float2(-xi.y, -xi.y), pz = make_float2(-xi.z, -xi.z);
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) {
+        const float2 dx = __fadd2_rn(yx[q], px), dy = __fadd2_rn(yy[q], py), dz = __fadd2_rn(yz[q], pz);
+        c[q] = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+      }
+    } else {
+      const float4* rowp = reinterpret_cast<const float4*>(C + i * ld + j0) + lane;
+#pragma unroll
+      for (int k = 0; k < kPairs / 2; ++k) {
+        const float4 f = __ldcs(rowp + 32 * k);
+        c[2 * k] = make_float2(f.x, f.y);
+        c[2 * k + 1] = make_float2(f.z, f.w);
+      }
+    }
+    float2 t[kPairs];
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) t[q] = __ffma2_rn(G, c[q], Bj[q]);
+    float m = tree_max2<kPairs>(t);
+    m = warp_maxf(m);
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    const float2 M2 = make_float2(-ms, -ms);
+    float2 R = make_float2(0.f, 0.f), Wc = R, K0 = R, K1 = R;
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const float2 d = __fadd2_rn(t[q], M2);
+      const float2 p = make_float2(ex2f(d.x), ex2f(d.y));
+      R = __fadd2_rn(R, p);
+      Wc = __ffma2_rn(c[q], p, Wc);
+      const int cc = 2 * lane + 64 * (q >> 1) + (q & 1);  // float2 index of f32_col(0, lane, q, 0)
+      K0 = __ffma2_rn(c[q], s_c0[cc], K0);
+      if (has_b1) K1 = __ffma2_rn(c[q], s_c1[cc], K1);
+    }
+    float4 o = make_float4(R.x + R.y, Wc.x + Wc.y, K0.x + K0.y, K1.x + K1.y);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      o.x += __shfl_xor_sync(0xffffffffu, o.x, off);
+      o.y += __shfl_xor_sync(0xffffffffu, o.y, off);
+      o.z += __shfl_xor_sync(0xffffffffu, o.z, off);
+      o.w += __shfl_xor_sync(0xffffffffu, o.w, off);
+    }
+    if (lane == 0) {
+      a.part[i * ldp + blockIdx.x] = o;
+      a.pm[i * ldp + blockIdx.x] = ms;
+    }
+  }
+}
+
+// Per row: R_i, W_i (x cost_scale) with the fp64 row offset ((u_i + lu_i) + w) log2 e,
+// K0_i, K1_i (x cost_scale); fixed strip order.
+__global__ void __launch_bounds__(kVecThreads) k_rowcost_reduce(const float4* part, const float* pm, int64_t nstrips,
+                                                               int64_t row_lo, int64_t row_hi, const double* u,
+                                                               const double* lu, const double* w, double wscale,
+                                                               double* R, double* W, double* K0, double* K1) {
+  const double ww = *w;
+  for (int64_t i = row_lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < row_hi;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double a2 = ((u[i] + (lu ? lu[i] : 0.0)) + ww) * kLog2e;
+    double r = 0.0, wc = 0.0, k0 = 0.0, k1 = 0.0;
+    for (int64_t s = 0; s < nstrips; ++s) {
+      const float4 o = part[i * nstrips + s];
+      if (o.x != 0.f) {
+        const double sc = exp2(double(pm[i * nstrips + s]) + a2);
+        r += double(o.x) * sc;
+        wc += double(o.y) * sc;
+      }
+      k0 += double(o.z);
+      k1 += double(o.w);
+    }
+    R[i] = r;
+    W[i] = wc * wscale;
+    K0[i] = k0 * wscale;
+    K1[i] = k1 * wscale;
+  }
+}
+
 using HVec = std::vector<double>;
 
 inline double hsum(const HVec& x) { return ksum(x.data(), int64_t(x.size())); }
@@ -141,6 +290,70 @@ struct PlanEngine {
     PG_CK(cudaMemcpyAsync(col.data(), d(3), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
     PG_CK(cudaStreamSynchronize(cx.stream));
   }
+
+  // The fused fp32 pass (k_rowcost_f32) serves unsharded fp32 problems when
+  // no dense plan is requested.
+  bool fused_ok(const double* Xdev) const {
+    return Xdev == nullptr && P.dtype == POTGPU_F32 && !cx.comm.sharded() && !fused_disabled() &&
+           (P.kind == POTGPU_COST_DENSE || P.kind == POTGPU_COST_SQEUCLIDEAN || P.kind == POTGPU_COST_SQEUCLIDEAN_STORED);
+  }
+  static bool fused_disabled() {
+    static const bool off = [] {
+      const char* e = std::getenv("POTGPU_FUSED_ROUND");
+      return e && e[0] == '0';
+    }();
+    return off;
+  }
+
+  // Per-row R, W, K0, K1 of the final plan (see RowCostArgs) in one pass.
+  void row_cost_sums(Slot z, const HVec& lu, const HVec& lv, const HVec* b0, const HVec* b1, HVec& R, HVec& W,
+                     HVec& K0, HVec& K1) {
+    const int64_t n = P.n;
+    up(0, lu);
+    up(1, lv);
+    if (b0) up(6, *b0);
+    if (b1) up(7, *b1);
+    const int64_t strips = ceil_div(n, kStripCols32);
+    const int64_t target_rb = std::max<int64_t>(1, ceil_div(int64_t(cx.num_sms) * 4, strips));
+    const int rpc = int(std::max<int64_t>(8, ceil_div(n, target_rb)));
+    const dim3 g(unsigned(strips), unsigned(ceil_div(n, rpc)));
+    if (rc_part.count < size_t(n * strips)) {
+      rc_part.alloc(size_t(n * strips));
+      rc_pm.alloc(size_t(n * strips));
+    }
+    RowCostArgs a{};
+    a.n = n;
+    a.row_lo = 0;
+    a.row_hi = n;
+    a.rows_per_cta = rpc;
+    a.u = z.u(); a.v = z.v(); a.w = z.w();
+    a.lv = d(1);
+    a.b0 = b0 ? d(6) : nullptr;
+    a.b1 = b1 ? d(7) : nullptr;
+    a.part = rc_part.p;
+    a.pm = rc_pm.p;
+    double wscale = 1.0;
+    if (P.kind == POTGPU_COST_SQEUCLIDEAN) {
+      a.g = float(kLog2e * P.cost_scale / gamma);
+      wscale = P.cost_scale;
+      k_rowcost_f32<true><<<g, kThreads, 0, cx.stream>>>(nullptr, 0, P.X4.p, P.Y4.p, a);
+    } else {
+      a.g = float(kLog2e / gamma);
+      k_rowcost_f32<false><<<g, kThreads, 0, cx.stream>>>(P.C32.p, P.ld, nullptr, nullptr, a);
+    }
+    // R, W, K0, K1 land in d(2), d(3), d(8), d(9)
+    k_rowcost_reduce<<<ws.nblk, kVecThreads, 0, cx.stream>>>(rc_part.p, rc_pm.p, strips, 0, n, z.u(), d(0), z.w(),
+                                                             wscale, d(2), d(3), d(8), d(9));
+    PG_CK(cudaGetLastError());
+    for (HVec* h : {&R, &W, &K0, &K1}) h->resize(size_t(n));
+    PG_CK(cudaMemcpyAsync(R.data(), d(2), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(W.data(), d(3), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(K0.data(), d(8), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(K1.data(), d(9), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaStreamSynchronize(cx.stream));
+  }
+  DevBuf<float4> rc_part;
+  DevBuf<float> rc_pm;
 
   // <C, X> for X = diag(Pv) B diag(Qv) + a0 b0^T + a1 b1^T; Xdev optional.
   double cost(Slot z, const HVec& Pv, const HVec& Qv, const HVec* a0, const HVec* b0, const HVec* a1, const HVec* b1,
@@ -272,19 +485,25 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   // rows / cols after both clips
   HVec lp = vlog(P0), lqk(n);
   for (size_t j = 0; j < n; ++j) lqk[j] = std::log(Q0[j] * kap[j]);
-  pe.block_sums(z, &lp, &lqk, rr, cc);
-  pt.mark("round: final sums");
-  double sbk = 0.0;
-  if (b) { HVec t(n); for (size_t j = 0; j < n; ++j) t[j] = (*b)[j] * kap[j]; sbk = hsum(t); }
-  HVec rowX3(n), colX3(n);
-  for (size_t i = 0; i < n; ++i) rowX3[i] = alpha * rho[i] * (rr[i] + (a ? (*a)[i] * sbk : 0.0));
+  HVec colX3(n), fb(n), kb0;
   for (size_t j = 0; j < n; ++j) colX3[j] = kap[j] * col3[j];
+  for (size_t j = 0; j < n; ++j) fb[j] = std::max(c[j] - colX3[j], 0.0);
+  if (b) { kb0.resize(n); for (size_t j = 0; j < n; ++j) kb0[j] = (*b)[j] * kap[j]; }
+  // fused fp32 pass: final row sums + the cost's per-row terms (RowCostArgs);
+  // the column factors of both rank-1 terms (fb, b kap) are known already
+  const bool fused = pe.fused_ok(Xdev);
+  HVec Wr, K0r, K1r;
+  if (fused) pe.row_cost_sums(z, lp, lqk, &fb, b ? &kb0 : nullptr, rr, Wr, K0r, K1r);
+  else pe.block_sums(z, &lp, &lqk, rr, cc);
+  pt.mark("round: final sums");
+  const double sbk = b ? hsum(kb0) : 0.0;
+  HVec rowX3(n);
+  for (size_t i = 0; i < n; ++i) rowX3[i] = alpha * rho[i] * (rr[i] + (a ? (*a)[i] * sbk : 0.0));
   // deficit fill (rounding.hpp:63-75)
   const double mass3 = hsum(rowX3);
   const double deficit = s - mass3;
-  HVec fa(n), fb(n);
+  HVec fa(n);
   for (size_t i = 0; i < n; ++i) fa[i] = std::max(r[i] - rowX3[i], 0.0);
-  for (size_t j = 0; j < n; ++j) fb[j] = std::max(c[j] - colX3[j], 0.0);
   const double na = hsum(fa), nb = hsum(fb);
   double f = 0.0;
   if (deficit > 0) {
@@ -324,7 +543,18 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
     for (size_t j = 0; j < n; ++j) kb[j] = (*b)[j] * kap[j];
   }
   pt.mark("round: host O(n)");
-  out.cost = pe.cost(z, Pf, Qf, &fa2, &fb, a ? &ra : nullptr, a ? &kb : nullptr, Xdev);
+  if (fused) {
+    // <C, X> = sum_i (alpha rho_i) W_i + f fa_i K0_i + alpha rho_i a_i K1_i
+    HVec terms(3 * n, 0.0);
+    for (size_t i = 0; i < n; ++i) {
+      terms[i] = (alpha * rho[i]) * Wr[i];
+      terms[n + i] = fa2[i] * K0r[i];
+      if (a) terms[2 * n + i] = ra[i] * K1r[i];
+    }
+    out.cost = hsum(terms);
+  } else {
+    out.cost = pe.cost(z, Pf, Qf, &fa2, &fb, a ? &ra : nullptr, a ? &kb : nullptr, Xdev);
+  }
   pt.mark("round: plan cost");
   out.Pf = std::move(Pf);
   out.Qf = std::move(Qf);

@@ -92,7 +92,7 @@ class _Problem(ctypes.Structure):
         ("X", ctypes.POINTER(ctypes.c_double)), ("Y", ctypes.POINTER(ctypes.c_double)), ("d", ctypes.c_int),
         ("cost_scale", ctypes.c_double),
         ("r", ctypes.POINTER(ctypes.c_double)), ("c", ctypes.POINTER(ctypes.c_double)), ("s", ctypes.c_double),
-        ("device_ptrs", ctypes.c_int),
+        ("device_ptrs", ctypes.c_int), ("producer_stream", ctypes.c_int64),
     ]
 
 
@@ -423,6 +423,29 @@ def _cuda_ptr(a, shape, what: str):
     return ctypes.cast(ctypes.c_void_p(cai["data"][0]), ctypes.POINTER(ctypes.c_double))
 
 
+def _producer_stream(arrays) -> int:
+    """potgpu_problem.producer_stream from the arrays' __cuda_array_interface__
+    v3 "stream" keys: the one stream they name (the solver orders its reads
+    after work queued on it), -1 when every array says "no sync needed"
+    (None), 0 (synchronise the device) when absent or when they disagree."""
+    seen = set()
+    for a in arrays:
+        if type(a).__module__.startswith("torch"):
+            # torch exports CAI v2 (no "stream"); its producer is the current
+            # stream of the tensor's device (handle 0 = the legacy default)
+            import torch
+            h = int(torch.cuda.current_stream(a.device).cuda_stream)
+            seen.add(h if h else 1)
+            continue
+        cai = a.__cuda_array_interface__
+        if "stream" not in cai:
+            return 0
+        seen.add(-1 if cai["stream"] is None else int(cai["stream"]))
+    if len(seen) == 1:
+        return seen.pop()
+    return 0
+
+
 def _is_cuda(a) -> bool:
     return a is not None and hasattr(a, "__cuda_array_interface__")
 
@@ -443,6 +466,7 @@ def _problem_device(inst: Instance, keep: list) -> _Problem:
             _cuda_ptr(inst.Y, (n, d), "Y"), d
         p.cost_scale = float(inst.cost_scale) if inst.cost_scale else 0.0
         keep += [inst.X, inst.Y]
+    p.producer_stream = _producer_stream([a for a in (inst.r, inst.c, inst.C, inst.X, inst.Y) if a is not None])
     return p
 
 

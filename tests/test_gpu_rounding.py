@@ -77,3 +77,52 @@ def test_device_resident_inputs_match_host_inputs(ctx):
                         cost_scale=pts.cost_scale, dtype=pot.DType.F32)
     b = pot.aspot_solve(devp, cfg32, ctx=ctx)
     assert a.iterations == b.iterations and a.cost == b.cost
+
+
+@pytest.mark.parametrize("side_stream", [False, True])
+def test_device_inputs_are_ordered_after_their_producer(ctx, side_stream):
+    """A cost still being written by torch when the solve is called (a long
+    sleep kernel ahead of it on the producer's stream) is read only after it
+    is complete: potgpu_problem.producer_stream."""
+    import torch
+    inst = pot.config_instance(1, n=512)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, max_iterations=30)
+    a = pot.aspot_solve(inst, cfg, ctx=ctx)
+    C_host = torch.tensor(inst.C)
+    stream = torch.cuda.Stream() if side_stream else torch.cuda.current_stream()
+    with torch.cuda.stream(stream):
+        C = torch.zeros((512, 512), dtype=torch.float64, device="cuda")
+        torch.cuda._sleep(200_000_000)  # ~0.1 s of device time before the copy lands
+        C.copy_(C_host.pin_memory().to("cuda", non_blocking=True))
+        dev = pot.Instance(r=torch.tensor(inst.r, device="cuda"), c=torch.tensor(inst.c, device="cuda"), s=inst.s, C=C)
+        b = pot.aspot_solve(dev, cfg, ctx=ctx)
+    assert a.iterations == b.iterations and a.cost == b.cost
+
+
+@pytest.mark.parametrize("kind", ["aspot", "tuned", "feasible"])
+@pytest.mark.parametrize("cost", ["points", "dense32"])
+def test_fused_fp32_output_stage_matches_dense_plan(ctx, kind, cost):
+    """The fused fp32 output pass (k_rowcost_f32: final row sums + <C, X> in
+    one sweep, no dense plan) against the dense-plan path of the same solve
+    (k_plan_cost, fp64 exponentials, materialize_plan=True) and numpy's
+    <C, X> of that plan: cost within 1e-6 relative, marginals within 1e-9."""
+    pts = pot.config_instance(3, n=1500)
+    if cost == "dense32":
+        inst = pot.Instance(r=pts.r, c=pts.c, s=pts.s, C=pot.dense_cost(pts.X, pts.Y, pts.cost_scale),
+                            dtype=pot.DType.F32)
+    else:
+        inst = pts
+    sk = {"aspot": pot.SolverKind.Aspot, "tuned": pot.SolverKind.TunedSinkhorn,
+          "feasible": pot.SolverKind.FeasibleSinkhorn}[kind]
+    base = dict(epsilon=2e-2, tuning_exponent_p=4.0, log_every=10 ** 9, max_iterations=300)
+    a = pot.solve(inst, sk, pot.SolverConfig(materialize_plan=False, **base), ctx=ctx)
+    b = pot.solve(inst, sk, pot.SolverConfig(materialize_plan=True, **base), ctx=ctx)
+    assert a.iterations == b.iterations
+    f32 = lambda x: np.asarray(x, dtype=np.float32).astype(np.float64)  # noqa: E731
+    C = pot.dense_cost(f32(pts.X), f32(pts.Y), pts.cost_scale) if cost == "points" else f32(inst.C)
+    ref = float(np.sum(C * b.plan.X))
+    assert abs(b.cost - ref) <= 1e-9 * abs(ref), (b.cost, ref)
+    assert abs(a.cost - ref) <= 1e-6 * abs(ref), (a.cost, ref)
+    np.testing.assert_allclose(a.plan.row_slack, b.plan.row_slack, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(a.plan.col_slack, b.plan.col_slack, rtol=0, atol=1e-9)
+    assert a.feasibility_gap <= 1e-5
