@@ -283,6 +283,18 @@ int potgpu_comm_init(potgpu_ctx* ctx, int rank, int world_size, const unsigned c
  * sharded arithmetic on one GPU, for testing; shards = 1 is the default. */
 int potgpu_comm_init_local(potgpu_ctx* ctx, int shards);
 int potgpu_comm_info(potgpu_ctx* ctx, int* rank, int* world_size, int* shards_per_rank);
+/* Host collective backend: the same row-sharded job with the cross-process
+ * reduction done by a caller-supplied function on host memory instead of
+ * NCCL (MPI, gloo, a test harness; several processes may share one GPU).
+ * `allreduce(buf, count, op, user)` must replace buf[0..count) in place with
+ * the element-wise SUM (op = POTGPU_REDUCE_SUM) or MAX (POTGPU_REDUCE_MAX)
+ * over the ranks, every rank calling it the same number of times in the
+ * same order; it runs on a CUDA host-callback thread (it may block, it must
+ * not call CUDA). Each sweep's all-reduce vector makes a device -> host ->
+ * device round trip, so this is for correctness and portability, not speed. */
+enum potgpu_reduce_op { POTGPU_REDUCE_SUM = 0, POTGPU_REDUCE_MAX = 2 };
+typedef void (*potgpu_host_allreduce_fn)(double* buf, int64_t count, int op, void* user);
+int potgpu_comm_init_host(potgpu_ctx* ctx, int rank, int world_size, potgpu_host_allreduce_fn allreduce, void* user);
 
 /* Rigid point-cloud registration (registration.hpp).
  * pot::RegistrationConfig (registration.hpp:75-100) without `solve`, which

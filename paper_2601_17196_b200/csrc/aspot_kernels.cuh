@@ -217,8 +217,10 @@ inline int eval_tpi(int64_t nstrips = 0) {
 
 // Per-index terms of every functional the reference evaluates at a point
 // (dual.hpp:112-141, solvers.hpp:49-52): B 1 = rb, B^T 1 = cb at z = (u, v, w).
-__device__ __forceinline__ void add_index_terms(double (&acc)[kNumAcc], double rb, double cb, double ui, double vi,
+template <int N>
+__device__ __forceinline__ void add_index_terms(double (&acc)[N], double rb, double cb, double ui, double vi,
                                                 double rti, double cti) {
+  static_assert(N >= kNumAcc, "accumulator array too short");
   const double eu = eexp(ui), ev = eexp(vi);
   acc[0] += rb;
   acc[1] = nan_max(acc[1], ui);
@@ -648,7 +650,7 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
 // Commit of an accepted attempt: z <- z_best, z_check <- z_check', sums of
 // z_check <- sums of z_check' (solvers.hpp:357-360). Element-parallel.
 __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double err, double phi) {
-  if (ctl->trace_len < ctl->trace_cap) {
+  if (trace && ctl->trace_len < ctl->trace_cap) {  // null: a cluster rank that only counts
     TraceDev& r = trace[ctl->trace_len];
     r.t = t; r.error = err; r.phi = phi;
     r.rounded_cost = __longlong_as_double(0x7ff8000000000000ULL);

@@ -1,0 +1,744 @@
+// batch_cluster.cuh — BASELINE configs[4]: many independent small fp32
+// stored-cost ASPOT problems, ONE PROBLEM PER THREAD-BLOCK CLUSTER.
+//
+// The per-problem path (AspotSession) runs an attempt as 12 kernels; for a
+// 2048-point problem each of them is a few microseconds, so a batch of
+// problems is bound by the rate at which the GPU starts kernels (DESIGN.md
+// §9). Here ONE persistent launch solves the whole batch: each cluster of
+// kBcCta CTAs (one per SM) takes problems from a queue and runs aspot_solve
+// (solvers.hpp:265-385) to its stop and round_pot (rounding.hpp:46-77) of
+// the stopping iterate inside the launch, with cluster barriers where the
+// kernel sequence had launch boundaries.
+//
+// Work split inside a cluster: CTA k owns the index slice [lo_k, hi_k) —
+// rows lo_k..hi_k of every sweep (whole rows: row sums are CTA-local) and
+// the same columns for every O(n) step (column sums, the functionals'
+// per-index terms, the dual-point updates). A sweep leaves each CTA's column
+// partials of all n columns in global memory (L2); after a cluster barrier
+// CTA k combines its slice's columns over the cluster. Scalars (the 14
+// functional accumulators + a non-finite flag) are exchanged the same way
+// and every CTA reduces them in the same fixed order, so every CTA's copy
+// of the control block (AspotCtl in shared memory) takes the same
+// decisions with the same device code as the per-problem path (apply_role,
+// commit_state, loop_head: aspot_kernels.cuh) — no broadcast needed.
+//
+// Sweep numerics = sweep_f32<SrcDenseF32> (sweep.cuh): t' = v_j log2 e -
+// g2 C_ij in fp32, exponentiated relative to each 512-column row segment's
+// exact max, row partials (sum, max) combined in fp64 with the fp64 row
+// offset, column accumulators with a per-warp running scale.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "aspot_kernels.cuh"
+
+namespace potgpu {
+
+namespace cgx = cooperative_groups;
+
+constexpr int kBcThreads = 512;  // 16 warps per CTA, one CTA per SM
+constexpr int kBcWarps = kBcThreads / 32;
+constexpr int kBcStrip = 512;     // columns per warp segment (16 per lane)
+constexpr int kBcMaxStrips = 8;   // n <= 4096
+constexpr int kBcMaxN = kBcStrip * kBcMaxStrips;
+constexpr int kBcMaxRows = 512;   // rows per CTA (n / cluster size)
+constexpr int kBcX = kNumAcc + 2; // exchanged scalars per CTA: accumulators, flag, spare
+
+// One problem of the batch (host-filled, device array).
+struct BcProblem {
+  const float* C;      // n x ld row-major fp32 cost (padding columns 0)
+  int64_t ld;
+  const double* rt;    // mixed marginals (the dual targets, aspot_setup)
+  const double* ct;
+  const double* r;     // original marginals (rounding)
+  const double* c;
+  float g2;            // log2 e / gamma
+  AspotCtl ctl0;       // initial control block (as AspotSession::begin)
+  TraceDev* trace;     // [ctl0.trace_cap]
+  IterLogDev* iterlog; // [ctl0.log_cap]
+  double* zc_out;      // [2n + 1]: the stopping iterate z_check (u | v | w)
+  double* row_slack;   // [n]
+  double* col_slack;   // [n]
+};
+
+// Per-problem result written by the cluster's rank-0 CTA.
+struct BcResult {
+  AspotCtl ctl;   // final control block (status, t, error, phi, sweeps, ...)
+  double cost, mass, gap;
+  int infeasible;
+  int done;
+};
+
+// Global workspace of one cluster (reused by every problem it takes).
+struct BcWs {
+  double* slots;     // kSlots x stride
+  double* sums;      // kRoles x 2 x n (rows | cols per role)
+  double* vec;       // 4 x n scratch (rounding: rho, kappa, fb, rowX3)
+  float2* colpart;   // [cluster rank][n]
+  double* xch;       // [2][cluster rank][kBcX]
+  int64_t stride;    // slot stride
+  int cur;           // problem being solved (set by rank 0)
+  int pad;
+};
+
+struct BcShared {
+  uint32_t ctl[kCtlWords];
+  float A[kBcMaxRows];                     // fp32 row offsets of the CTA's rows
+  float2 rowpart[kBcMaxRows][kBcMaxStrips];  // (segment sum, segment max) per row and strip
+  float wpart[kBcMaxRows][kBcMaxStrips];   // cost mode: segment sum of C p
+  float kpart[kBcMaxRows][kBcMaxStrips];   // cost mode: segment sum of C fb
+  float colacc[kBcWarps][kBcStrip];        // per-warp column accumulators
+  float colsig[kBcWarps];
+  float wmax[kBcWarps];
+  double red[kBcX][kBcWarps];
+  double tot[kBcX];
+  int flag;
+};
+
+__host__ __device__ constexpr size_t bc_smem_bytes() { return sizeof(BcShared); }
+
+struct BcCtx {
+  const BcProblem* P;
+  BcWs* W;
+  BcShared* sm;
+  AspotCtl* c;     // == sm->ctl
+  int64_t n;
+  int rank, cs;
+  int64_t lo, hi;  // the CTA's index slice
+  int xphase;      // exchange buffer parity (uniform over the cluster)
+  __device__ double* slot(int k) const { return W->slots + k * W->stride; }
+  __device__ double* rows(int role) const { return W->sums + int64_t(2 * role) * n; }
+  __device__ double* cols(int role) const { return W->sums + int64_t(2 * role + 1) * n; }
+};
+
+__device__ __forceinline__ void bc_sync() { cgx::this_cluster().sync(); }
+
+// Fixed-order cluster reduction of kBcX scalars (acc_join semantics for the
+// first kNumAcc, max for the flag): every CTA writes its row, one barrier,
+// every CTA reduces all rows in rank order -> identical totals in sm->tot.
+// SUMS: every slot below kNumAcc is a plain sum, kNumAcc and kNumAcc + 1 are maxima.
+__device__ __forceinline__ double bc_join(bool sums, int k, double a, double b) {
+  if (k >= kNumAcc) return (sums || k == kNumAcc) ? fmax(a, b) : a + b;
+  return sums ? a + b : acc_join(k, a, b);
+}
+__device__ __forceinline__ double bc_init(bool sums, int k) {
+  if (sums) return k >= kNumAcc ? -INFINITY : 0.0;
+  return k < kNumAcc ? acc_init(k) : 0.0;
+}
+
+// Publishes the CTA's totals (sm->red[k][0], from bc_block_acc).
+template <bool SUMS = false>
+__device__ void bc_exchange(BcCtx& X) {
+  double* buf = X.W->xch + int64_t(X.xphase & 1) * X.cs * kBcX;
+  X.xphase += 1;
+  if (threadIdx.x < kBcX) buf[X.rank * kBcX + threadIdx.x] = X.sm->red[threadIdx.x][0];
+  bc_sync();
+  if (threadIdx.x < kBcX) {
+    const int k = threadIdx.x;
+    double a = bc_init(SUMS, k);
+    for (int r = 0; r < X.cs; ++r) a = bc_join(SUMS, k, a, __ldcg(buf + r * kBcX + k));
+    X.sm->tot[k] = a;
+  }
+  __syncthreads();
+}
+
+// Block reduction of kBcX accumulators; the CTA's totals land in
+// sm->red[k][0] (what bc_exchange publishes).
+template <bool SUMS = false>
+__device__ void bc_block_acc(BcCtx& X, double (&acc)[kBcX]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = bc_join(SUMS, k, x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) X.sm->red[k][wid] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < kBcX) {
+    const int k = threadIdx.x;
+    double x = X.sm->red[k][0];
+    for (int w2 = 1; w2 < kBcWarps; ++w2) x = bc_join(SUMS, k, x, X.sm->red[k][w2]);
+    X.sm->red[k][0] = x;
+  }
+  __syncthreads();
+}
+
+// One sweep over the CTA's rows of the point (u + lu, v + lv, w):
+//   rows_out[i] (fp64 row sums of the CTA's rows), X.W->colpart[rank][j]
+//   (fp32 (sum, log2 scale) column partials of all columns), returns the
+//   CTA's max exponent (natural units). COST: also W_out[i] = sum_j C_ij
+//   B'_ij and K_out[i] = sum_j C_ij fb_j (no column partials).
+template <bool COST>
+__device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double* lu, const double* lv, const double* fb,
+                           double* rows_out, double* W_out, double* K_out) {
+  BcShared& sm = *X.sm;
+  const BcProblem& P = *X.P;
+  const int64_t n = X.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* u = z;
+  const double* v = z + n;
+  const double w = __ldcg(z + 2 * n);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    double a = __ldcg(u + i);
+    if (lu) a = a + __ldcg(lu + i);
+    sm.A[i - X.lo] = float((a + w) * kLog2e);
+  }
+  const int S = int((n + kBcStrip - 1) / kBcStrip);
+  const int PH = kBcWarps / S;
+  const int strip = warp % S, ph = warp / S;
+  const bool active = ph < PH;
+  const int64_t j0 = int64_t(strip) * kBcStrip;
+  float2 Bj[kPairs], Fb[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) {
+    float b[2], f[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = f32_col(j0, lane, q, h);
+      double vv = -INFINITY;
+      f[h] = 0.f;
+      if (j < n) {
+        vv = __ldcg(v + j);
+        if (lv) vv = vv + __ldcg(lv + j);
+        vv = vv * kLog2e;
+        if (COST) f[h] = float(__ldcg(fb + j));
+      }
+      b[h] = float(vv);
+    }
+    Bj[q] = make_float2(b[0], b[1]);
+    Fb[q] = make_float2(f[0], f[1]);
+  }
+  __syncthreads();
+  float2 cacc[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) cacc[q] = make_float2(0.f, 0.f);
+  float sigma = -INFINITY, mmax = -INFINITY;
+  const float2 G = make_float2(-P.g2, -P.g2);
+  if (active) {
+    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
+    const int64_t ld4 = P.ld / 4;
+    int64_t i = X.lo + ph;
+    float4 nxt[4];
+    if (i < X.hi)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
+    for (; i < X.hi; i += PH) {
+      float4 cur[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+      if (i + PH < X.hi)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
+      float2 cc[kPairs], t[kPairs];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cc[2 * k] = make_float2(cur[k].x, cur[k].y);
+        cc[2 * k + 1] = make_float2(cur[k].z, cur[k].w);
+      }
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) t[q] = __ffma2_rn(G, cc[q], Bj[q]);
+      float m = warp_maxf(tree_max2<kPairs>(t));
+      const float ms = (m == -INFINITY) ? 0.f : m;
+      const float2 M2 = make_float2(-ms, -ms);
+      float2 p[kPairs];
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) {
+        const float2 d = __fadd2_rn(t[q], M2);
+        p[q] = make_float2(ex2f(d.x), ex2f(d.y));
+      }
+      float rs = tree_sum2<kPairs>(p);
+      float ws = 0.f, ks = 0.f;
+      if (COST) {
+        float2 W2 = make_float2(0.f, 0.f), K2 = W2;
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) {
+          W2 = __ffma2_rn(cc[q], p[q], W2);
+          K2 = __ffma2_rn(cc[q], Fb[q], K2);
+        }
+        ws = W2.x + W2.y;
+        ks = K2.x + K2.y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (COST) {
+          ws += __shfl_xor_sync(0xffffffffu, ws, o);
+          ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        }
+      }
+      const int64_t il = i - X.lo;
+      if (lane == 0) {
+        sm.rowpart[il][strip] = make_float2(rs, ms);
+        if (COST) {
+          sm.wpart[il][strip] = ws;
+          sm.kpart[il][strip] = ks;
+        }
+      }
+      if (!COST) {
+        const float mA = (m == -INFINITY) ? -INFINITY : m + sm.A[il];
+        if (mA > sigma) {  // warp-uniform
+          const float sc = ex2f(sigma - mA);
+#pragma unroll
+          for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+          sigma = mA;
+        }
+        mmax = fmaxf(mmax, mA);
+        const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+        const float2 F2 = make_float2(f, f);
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+      }
+    }
+  }
+  if (!COST) {
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const int cidx = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+      sm.colacc[warp][cidx] = cacc[q].x;
+      sm.colacc[warp][cidx + 1] = cacc[q].y;
+    }
+    if (lane == 0) {
+      sm.colsig[warp] = sigma;
+      sm.wmax[warp] = mmax;
+    }
+  }
+  __syncthreads();
+  // row sums of the CTA's rows (fp64, the row offset added back exactly)
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const int64_t il = i - X.lo;
+    double a = __ldcg(u + i);
+    if (lu) a = a + __ldcg(lu + i);
+    const double a2 = (a + w) * kLog2e;
+    double rr = 0.0, wc = 0.0, kk = 0.0;
+    for (int s = 0; s < S; ++s) {
+      const float2 rp = sm.rowpart[il][s];
+      if (rp.x != 0.f) {
+        const double sc = exp2(double(rp.y) + a2);
+        rr += double(rp.x) * sc;
+        if (COST) wc += double(sm.wpart[il][s]) * sc;
+      }
+      if (COST) kk += double(sm.kpart[il][s]);
+    }
+    rows_out[i] = rr;
+    if (COST) {
+      W_out[i] = wc;
+      K_out[i] = kk;
+    }
+  }
+  if (COST) {
+    __syncthreads();
+    return -INFINITY;
+  }
+  // CTA column partials: combine the PH warps of each strip
+  float2* cp = X.W->colpart + int64_t(X.rank) * n;
+  for (int k = threadIdx.x; k < S * kBcStrip; k += kBcThreads) {
+    const int s = k / kBcStrip, cidx = k % kBcStrip;
+    const int64_t j = int64_t(s) * kBcStrip + cidx;
+    if (j >= n) continue;
+    float SIG = -INFINITY;
+    for (int p2 = 0; p2 < PH; ++p2) SIG = fmaxf(SIG, sm.colsig[p2 * S + s]);
+    float acc = 0.f;
+    if (SIG != -INFINITY)
+      for (int p2 = 0; p2 < PH; ++p2) {
+        const float sg = sm.colsig[p2 * S + s];
+        if (sg != -INFINITY) acc += sm.colacc[p2 * S + s][cidx] * ex2f(sg - SIG);
+      }
+    cp[j] = (SIG == -INFINITY) ? make_float2(0.f, 0.f) : make_float2(acc, SIG);
+  }
+  float mx = -INFINITY;
+  for (int ww = 0; ww < S * PH; ++ww) mx = fmaxf(mx, sm.wmax[ww]);
+  __syncthreads();
+  return double(mx) * kLn2;
+}
+
+// Column sums of the CTA's slice over the cluster's partials (after a barrier).
+__device__ __forceinline__ double bc_col_sum(const BcCtx& X, int64_t j) {
+  const float2* cp = X.W->colpart;
+  float M = -INFINITY;
+  for (int r = 0; r < X.cs; ++r) {
+    const float2 x = __ldcg(cp + int64_t(r) * X.n + j);
+    if (x.x != 0.f) M = fmaxf(M, x.y);
+  }
+  if (M == -INFINITY) return 0.0;
+  float S = 0.f;
+  for (int r = 0; r < X.cs; ++r) {
+    const float2 x = __ldcg(cp + int64_t(r) * X.n + j);
+    if (x.x != 0.f) S += x.x * ex2f(x.y - M);
+  }
+  return double(S) * exp2(double(M));
+}
+
+// Sweep + evaluation + decision of a point (k_point_eval + decide_pending).
+__device__ __noinline__ void bc_eval_swept(BcCtx& X, int slot, int role) {
+  bc_sync();  // the point's slices (every CTA's writes) are complete
+  const double* z = X.slot(slot);
+  const double maxe = bc_sweep<false>(X, z, nullptr, nullptr, nullptr, X.rows(role), nullptr, nullptr);
+  bc_sync();  // column partials of every CTA
+  double acc[kBcX];
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) acc[k] = k < kNumAcc ? acc_init(k) : 0.0;
+  const double* P_rt = X.P->rt;
+  const double* P_ct = X.P->ct;
+  double* rb = X.rows(role);
+  double* cb = X.cols(role);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const double c = bc_col_sum(X, i);
+    cb[i] = c;
+    add_index_terms(acc, __ldcg(rb + i), c, __ldcg(z + i), __ldcg(z + X.n + i), P_rt[i], P_ct[i]);
+  }
+  bc_block_acc(X, acc);
+  if (threadIdx.x == 0) X.sm->red[11][0] = nan_max(X.sm->red[11][0], maxe);
+  __syncthreads();
+  bc_exchange(X);
+  if (threadIdx.x == 0) {
+    double tot[kNumAcc];
+#pragma unroll
+    for (int k = 0; k < kNumAcc; ++k) tot[k] = X.sm->tot[k];
+    apply_role(X.c, role, tot, __ldcg(z + 2 * X.n), true);
+  }
+  __syncthreads();
+}
+
+__device__ void bc_kill_gates(AspotCtl* c) {  // ctl_finish's non-finite fold (solvers.hpp:83-87)
+  c->g_alive = 0;
+  c->g_hat_sweep = c->g_hat_scaled = c->g_new_sweep = c->g_new_scaled = 0;
+  c->g_new_one = c->g_new_eval = 0;
+}
+
+// Exact block update (k_gk_update) of the slice, then the exchange of the
+// non-finite flag and, for a w-block point, of its scaled functionals;
+// the decision at the new point when it was scaled.
+__device__ __noinline__ void bc_gk_update(BcCtx& X, int which) {
+  AspotCtl* c = X.c;
+  const int64_t n = X.n;
+  int block, role;
+  int src_slot, dst_slot, dst_role;
+  if (which == 0) {
+    block = c->block_hat; src_slot = S_ZG; role = R_GRAVE; dst_slot = S_ZH; dst_role = R_HAT;
+  } else {
+    block = c->block_check;
+    const bool keep = c->keep_check;
+    src_slot = keep ? S_ZC : S_ZH; role = keep ? R_CHECK : R_HAT; dst_slot = S_ZN; dst_role = R_NEW;
+  }
+  const double* src = X.slot(src_slot);
+  double* dst = X.slot(dst_slot);
+  const double* rowb = X.rows(role);
+  const double* colb = X.cols(role);
+  const double* rt = X.P->rt;
+  const double* ct = X.P->ct;
+  bool finite = true;
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    double x = __ldcg(src + i);
+    if (block == 0) x = x + (log(rt[i]) - log(__ldcg(rowb + i) + eexp(x)));
+    dst[i] = x;
+    finite = finite && isfinite(x);
+    double y = __ldcg(src + n + i);
+    if (block == 1) y = y + (log(ct[i]) - log(__ldcg(colb + i) + eexp(y)));
+    dst[n + i] = y;
+    finite = finite && isfinite(y);
+  }
+  const double ws = __ldcg(src + 2 * n);
+  const double wd = block == 2 ? ws + (log(c->s) - log(c->ps[role].total)) : ws;
+  if (X.rank == 0 && threadIdx.x == 0) dst[2 * n] = wd;
+  finite = finite && isfinite(wd);
+  const bool scaled = which == 0 ? c->g_hat_scaled : c->g_new_scaled;
+  double acc[kBcX];
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) acc[k] = k < kNumAcc ? acc_init(k) : 0.0;
+  acc[kNumAcc] = finite ? 0.0 : 1.0;
+  const double dw = wd - ws;
+  if (scaled) {
+    const double fs = exp(dw);
+    double* dr = X.rows(dst_role);
+    double* dc = X.cols(dst_role);
+    for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+      const double rb = __ldcg(rowb + i) * fs, cb = __ldcg(colb + i) * fs;
+      dr[i] = rb;
+      dc[i] = cb;
+      add_index_terms(acc, rb, cb, __ldcg(src + i), __ldcg(src + n + i), rt[i], ct[i]);
+    }
+  }
+  bc_block_acc(X, acc);
+  bc_exchange(X);
+  if (threadIdx.x == 0) {
+    if (X.sm->tot[kNumAcc] != 0.0) {
+      bc_kill_gates(c);
+    } else if (scaled) {
+      double tot[kNumAcc];
+#pragma unroll
+      for (int k = 0; k < kNumAcc; ++k) tot[k] = X.sm->tot[k];
+      tot[11] = c->ps[role].maxe + dw;
+      apply_role(c, dst_role, tot, wd, false);
+    }
+  }
+  __syncthreads();
+}
+
+// Round_pot (rounding.hpp:46-77) of B(z_check), the implicit-plan form of
+// plan.cuh round_pot_implicit with P0 = Q0 = 1 and no rank-1 input term
+// (two sweeps: the column clip's column sums, then the final row sums fused
+// with <C, X>, as k_rowcost_f32). Rank 0 writes the metrics.
+__device__ __noinline__ double bc_round(BcCtx& X, BcResult* res) {
+  const int64_t n = X.n;
+  const BcProblem& P = *X.P;
+  const double s = X.c->s;
+  double* lrho = X.W->vec;         // log rho (row clip)
+  double* lkap = X.W->vec + n;     // log kappa (column clip)
+  double* fbv = X.W->vec + 2 * n;  // deficit column factors max(c - colX3, 0)
+  double* rx = X.W->vec + 3 * n;   // rowX3
+  double* arho = X.W->vec + 4 * n; // alpha rho
+  double* cx3 = X.W->vec + 5 * n;  // colX3
+  const double* zc = X.slot(S_ZC);
+  const double* row0 = X.rows(R_CHECK);
+  double acc[kBcX];
+  // out *= min(1, s / mass)
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) acc[k] = bc_init(true, k);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) acc[0] += __ldcg(row0 + i);
+  bc_block_acc<true>(X, acc);
+  bc_exchange<true>(X);
+  const double mass1 = X.sm->tot[0];
+  const double alpha = mass1 > 0 ? fmin(1.0, s / mass1) : 1.0;
+  // row clip
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const double row = alpha * __ldcg(row0 + i);
+    const double rh = row > 0 ? fmin(1.0, P.r[i] / row) : 1.0;
+    lrho[i] = log(rh);
+    arho[i] = alpha * rh;
+  }
+  bc_sync();
+  // column clip: column sums of diag(rho) B
+  (void)bc_sweep<false>(X, zc, lrho, nullptr, nullptr, X.rows(R_EVAL), nullptr, nullptr);
+  bc_sync();
+  for (int64_t j = X.lo + threadIdx.x; j < X.hi; j += kBcThreads) {
+    const double col3 = alpha * bc_col_sum(X, j);
+    const double kp = col3 > 0 ? fmin(1.0, P.c[j] / col3) : 1.0;
+    const double c3 = kp * col3;
+    lkap[j] = log(kp);
+    cx3[j] = c3;
+    fbv[j] = fmax(P.c[j] - c3, 0.0);
+  }
+  bc_sync();
+  // final row sums of B diag(kappa) and the cost's per-row terms
+  double* rr = X.rows(R_EVAL);
+  double* Wv = X.rows(R_BAR);
+  double* Kv = X.cols(R_BAR);
+  (void)bc_sweep<true>(X, zc, nullptr, lkap, fbv, rr, Wv, Kv);
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) acc[k] = bc_init(true, k);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const double x3 = __ldcg(arho + i) * __ldcg(rr + i);
+    rx[i] = x3;
+    acc[0] += x3;                                // mass3
+    acc[1] += fmax(P.r[i] - x3, 0.0);            // na
+    acc[2] += __ldcg(fbv + i);                   // nb (the slice's columns)
+  }
+  bc_block_acc<true>(X, acc);
+  bc_exchange<true>(X);
+  const double mass3 = X.sm->tot[0], na = X.sm->tot[1], nb = X.sm->tot[2];
+  const double deficit = s - mass3;
+  double f = 0.0;
+  int infeasible = 0;
+  if (deficit > 0) {  // deficit fill (rounding.hpp:63-75)
+    if (na <= 0 || nb <= 0) infeasible = 1;
+    else f = deficit / (na * nb);
+  }
+  // <C, X> = sum_i alpha rho_i W_i + f fa_i K_i ; slacks ; gap (core.hpp:199-219)
+#pragma unroll
+  for (int k = 0; k < kBcX; ++k) acc[k] = bc_init(true, k);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const double x3 = __ldcg(rx + i);
+    const double fa = fmax(P.r[i] - x3, 0.0);
+    acc[0] += __ldcg(arho + i) * __ldcg(Wv + i) + (f * fa) * __ldcg(Kv + i);
+    const double rxi = x3 + f * fa * nb;
+    const double cxj = __ldcg(cx3 + i) + f * na * __ldcg(fbv + i);
+    P.row_slack[i] = P.r[i] - rxi;
+    P.col_slack[i] = P.c[i] - cxj;
+    acc[kNumAcc] = fmax(acc[kNumAcc], fmax(rxi - P.r[i], 0.0));
+    acc[kNumAcc + 1] = fmax(acc[kNumAcc + 1], fmax(cxj - P.c[i], 0.0));
+  }
+  bc_block_acc<true>(X, acc);
+  bc_exchange<true>(X);
+  const double cost = X.sm->tot[0];
+  if (res && X.rank == 0 && threadIdx.x == 0) {
+    const double mass = mass3 + f * na * nb;
+    res->cost = cost;
+    res->mass = mass;
+    res->gap = fmax(fmax(fmax(X.sm->tot[kNumAcc], 0.0), fmax(X.sm->tot[kNumAcc + 1], 0.0)), fabs(mass - s));
+    res->infeasible = infeasible;
+  }
+  return cost;
+}
+
+// record_rounded_cost: the record just appended (record(t), solvers.hpp:
+// 309-318) gets the cost of round_pot(B(z_check)) at that t.
+__device__ void bc_record_cost(BcCtx& X, int64_t len_before, TraceDev* trace) {
+  const AspotCtl* c = X.c;
+  if (!c->record_rounded_cost || c->trace_len == len_before || c->trace_len > c->trace_cap) return;
+  const double cost = bc_round(X, nullptr);
+  if (trace && threadIdx.x == 0) trace[c->trace_len - 1].rounded_cost = cost;
+}
+
+// The persistent batch kernel: grid = cs x clusters, cluster = (cs, 1, 1).
+__global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* probs, int count, BcWs* wss,
+                                                              BcResult* results, int* queue) {
+  extern __shared__ __align__(16) unsigned char bc_smem_raw[];
+  BcShared* sm = reinterpret_cast<BcShared*>(bc_smem_raw);
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int cs = int(cl.num_blocks());
+  const int rank = int(cl.block_rank());
+  const int cid = int(blockIdx.x) / cs;
+  BcWs* W = wss + cid;
+  for (;;) {
+    if (rank == 0 && threadIdx.x == 0) W->cur = atomicAdd(queue, 1);
+    bc_sync();
+    const int p = *reinterpret_cast<volatile int*>(&W->cur);
+    if (p >= count) break;
+    BcCtx X;
+    X.P = probs + p;
+    X.W = W;
+    X.sm = sm;
+    X.c = reinterpret_cast<AspotCtl*>(sm->ctl);
+    X.n = X.P->ctl0.n;
+    X.rank = rank;
+    X.cs = cs;
+    X.lo = X.n * rank / cs;
+    X.hi = X.n * (rank + 1) / cs;
+    X.xphase = 0;
+    {  // control block copy, zero dual points (z = z_check = z_bar = 0)
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&X.P->ctl0);
+      for (int k = threadIdx.x; k < kCtlWords; k += kBcThreads) sm->ctl[k] = src[k];
+      const int64_t n = X.n;
+      for (int s2 = 0; s2 < kSlots; ++s2) {
+        double* zz = X.slot(s2);
+        for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+          zz[i] = 0.0;
+          zz[n + i] = 0.0;
+        }
+        if (rank == 0 && threadIdx.x == 0) zz[2 * n] = 0.0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) X.c->t0_ns = globaltimer_ns();
+    }
+    AspotCtl* c = X.c;
+    TraceDev* trace = rank == 0 ? X.P->trace : nullptr;
+    IterLogDev* lg = rank == 0 ? X.P->iterlog : nullptr;
+    // phi_and_gradient(z_check = 0) (solvers.hpp:305), record(0) (:320)
+    bc_eval_swept(X, S_ZC, R_CHECK);
+    int64_t len0 = c->trace_len;
+    if (threadIdx.x == 0 && !c->fatal) {
+      c->error = c->ps[R_CHECK].err;
+      c->phi_check = c->ps[R_CHECK].phi;
+      c->g_active = 1;
+      append_trace(c, trace, 0, c->error, c->phi_check);
+      loop_head(c);
+    }
+    __syncthreads();
+    bc_record_cost(X, len0, trace);
+    const int64_t n = X.n;
+    while (c->g_active) {  // identical on every CTA of the cluster
+      // z_bar: range check and gradient of a new iteration (solvers.hpp:336-337)
+      if (c->g_new) bc_eval_swept(X, S_ZB, R_BAR);
+      if (c->g_alive) {  // z_next = z_bar - step grad; z_grave = z_bar + theta (z_next - z) (:338-339)
+        const bool fresh = c->g_new;
+        const double step = c->step, th = c->theta;
+        const double* zb = X.slot(S_ZB);
+        const double* z = X.slot(S_Z);
+        double* g = X.slot(S_G);
+        double* zg = X.slot(S_ZG);
+        const double* rb = X.rows(R_BAR);
+        const double* cb = X.cols(R_BAR);
+        for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            const int64_t k = side * n + i;
+            double gk;
+            if (fresh) {
+              gk = side == 0 ? (__ldcg(rb + i) + eexp(__ldcg(zb + k))) - X.P->rt[i]
+                             : (__ldcg(cb + i) + eexp(__ldcg(zb + k))) - X.P->ct[i];
+              g[k] = gk;
+            } else {
+              gk = __ldcg(g + k);
+            }
+            const double zn = __ldcg(zb + k) - step * gk;
+            zg[k] = __ldcg(zb + k) + th * (zn - __ldcg(z + k));
+          }
+        }
+        if (rank == 0 && threadIdx.x == 0) {
+          const int64_t k = 2 * n;
+          double gk;
+          if (fresh) { gk = c->ps[R_BAR].total - c->s; g[k] = gk; } else { gk = __ldcg(g + k); }
+          const double zn = __ldcg(zb + k) - step * gk;
+          zg[k] = __ldcg(zb + k) + th * (zn - __ldcg(z + k));
+        }
+        bc_eval_swept(X, S_ZG, R_GRAVE);
+      }
+      if (c->g_alive) bc_gk_update(X, 0);                 // z_hat (solvers.hpp:340)
+      if (c->g_hat_sweep) bc_eval_swept(X, S_ZH, R_HAT);  // phi(z_hat), z_best (:341-343)
+      if (c->g_alive) bc_gk_update(X, 1);                 // z_check' = GK(z_best) (:344)
+      if (c->g_new_sweep) bc_eval_swept(X, S_ZN, R_NEW);  // phi, grad at z_check' (:345)
+      if (c->attempt_ok) {  // commit (k_commit)
+        const bool keep = c->keep_check;
+        const double th = theta_next_d(c->theta), om = 1.0 - th;
+        double* z = X.slot(S_Z);
+        double* zc = X.slot(S_ZC);
+        const double* zh = X.slot(S_ZH);
+        const double* zn = X.slot(S_ZN);
+        double* zb = X.slot(S_ZB);
+        double* rc = X.rows(R_CHECK);
+        double* cc = X.cols(R_CHECK);
+        const double* rn = X.rows(R_NEW);
+        const double* cn = X.cols(R_NEW);
+        for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            const int64_t k = side * n + i;
+            const double zbst = keep ? __ldcg(zc + k) : __ldcg(zh + k);
+            const double zcn = __ldcg(zn + k);
+            z[k] = zbst;
+            zc[k] = zcn;
+            zb[k] = om * zcn + th * zbst;
+          }
+          rc[i] = __ldcg(rn + i);
+          cc[i] = __ldcg(cn + i);
+        }
+        if (rank == 0 && threadIdx.x == 0) {  // w (index 2n) has one writer
+          const int64_t k = 2 * n;
+          const double zbst = keep ? __ldcg(zc + k) : __ldcg(zh + k);
+          const double zcn = __ldcg(zn + k);
+          z[k] = zbst;
+          zc[k] = zcn;
+          zb[k] = om * zcn + th * zbst;
+        }
+      }
+      __syncthreads();
+      len0 = c->trace_len;
+      __syncthreads();
+      if (threadIdx.x == 0) commit_state(c, trace, lg);
+      __syncthreads();
+      bc_sync();  // every slice of the committed points before the next attempt reads them
+      bc_record_cost(X, len0, trace);
+    }
+    bc_round(X, results + p);
+    if (rank == 0 && threadIdx.x == 0) {
+      c->loop_end_ns = c->loop_end_ns ? c->loop_end_ns : globaltimer_ns();
+      results[p].ctl = *c;
+      results[p].done = 1;
+      double* zo = X.P->zc_out;
+      if (zo) zo[2 * n] = __ldcg(X.slot(S_ZC) + 2 * n);
+    }
+    {
+      double* zo = X.P->zc_out;
+      const double* zc = X.slot(S_ZC);
+      if (zo)
+        for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+          zo[i] = __ldcg(zc + i);
+          zo[n + i] = __ldcg(zc + n + i);
+        }
+    }
+    bc_sync();  // the workspace is free for the next problem
+  }
+}
+
+}  // namespace potgpu

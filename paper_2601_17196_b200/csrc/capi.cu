@@ -12,6 +12,7 @@
 
 #include "engine.cuh"
 #include "plan.cuh"
+#include "batch_cluster.cuh"
 
 namespace potgpu {
 
@@ -1064,15 +1065,273 @@ static std::unique_ptr<Session> make_session(potgpu_ctx* c, int kind, const potg
   return make_session_cx(c->cx, kind, pr, cfg_in, trace_cap, log_cap);
 }
 
+// ------------------------------------------------ one problem per cluster --
+// BASELINE configs[4] through batch_cluster.cuh: every problem uploaded and
+// set up on the host side (validation, aspot_setup, control block), then ONE
+// persistent launch solves and rounds the whole batch, one problem per
+// thread-block cluster. Used by potgpu_solve_batched for ASPOT on fp32
+// stored costs of n <= kBcMaxN ($POTGPU_BATCH_CLUSTER=0 turns it off;
+// $POTGPU_BC_CS = cluster size, default 8; $POTGPU_BC_CLUSTERS caps the
+// resident clusters).
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+static bool bc_wanted(int kind, const potgpu_problem* problems, int64_t count, const potgpu_config& cfg,
+                      const potgpu_outputs* outputs) {
+  if (env_int("POTGPU_BATCH_CLUSTER", 1) == 0 || kind != POTGPU_ASPOT || count < 1) return false;
+  if (cfg.gamma_override != 0 && !(cfg.gamma_override > 0)) return false;
+  for (int64_t k = 0; k < count; ++k) {
+    const potgpu_problem& p = problems[k];
+    if (p.dtype != POTGPU_F32 || !(p.cost_kind == POTGPU_COST_DENSE || p.cost_kind == POTGPU_COST_SQEUCLIDEAN_STORED))
+      return false;
+    if (p.n < 2 || p.n > kBcMaxN || !(p.s > 0)) return false;  // trivial / degenerate: the session path
+    if (cfg.materialize_plan && outputs && outputs[k].X) return false;
+  }
+  return true;
+}
+
+struct BcHostProblem {
+  DevProblem P;
+  Setup st;
+  double gamma = 0;
+  DevBuf<double> marg;   // rt | ct | r | c
+  DevBuf<double> outv;   // z_check (2n + 1) | row slack | col slack
+  DevBuf<TraceDev> trace;
+  DevBuf<IterLogDev> lg;
+  int64_t trace_cap = 1, log_cap = 0;
+  std::string err;
+  int code = 0;
+};
+
+static void bc_solve_batched(Context& base, const potgpu_problem* problems, int64_t count, const potgpu_config& cfg,
+                             potgpu_summary* summaries, potgpu_outputs* outputs, int concurrency) {
+  const auto t_start = HostClock::now();
+  check_config(cfg);
+  std::vector<std::unique_ptr<BcHostProblem>> hp(static_cast<size_t>(count));
+  std::vector<BcProblem> dp(static_cast<size_t>(count));
+  // upload + validation + setup, `concurrency` host threads with own streams
+  const int workers = int(std::max<int64_t>(1, std::min<int64_t>(concurrency > 0 ? concurrency : 8, count)));
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < workers; ++t) {
+    pool.emplace_back([&] {
+      Context cx = base;
+      cx.comm = Comm{};
+      PG_CK(cudaSetDevice(cx.device));
+      PG_CK(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+      int64_t k;
+      while ((k = next.fetch_add(1)) < count) {
+        auto h = std::make_unique<BcHostProblem>();
+        try {
+          upload_problem(cx, &problems[k], h->P);
+          const int64_t n = h->P.n;
+          h->st = aspot_setup(h->P, cfg.epsilon);
+          h->gamma = cfg.gamma_override > 0 ? cfg.gamma_override : h->st.gamma;
+          if (!(h->gamma > 0) || !std::isfinite(h->gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
+          build_logk(cx, h->P, h->gamma);
+          if (!h->P.C32.p) throw Error(POTGPU_ERR_UNSUPPORTED, "internal: no fp32 stored cost");
+          h->marg.alloc(size_t(4 * n));
+          PG_CK(cudaMemcpyAsync(h->marg.p, h->st.mr.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+          PG_CK(cudaMemcpyAsync(h->marg.p + n, h->st.mc.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+          PG_CK(cudaMemcpyAsync(h->marg.p + 2 * n, h->P.r.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+          PG_CK(cudaMemcpyAsync(h->marg.p + 3 * n, h->P.c.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+          h->outv.alloc(size_t(4 * n + 1));
+          const potgpu_outputs* out = outputs ? &outputs[k] : nullptr;
+          h->trace_cap = std::max<int64_t>(out ? out->trace_cap : 0, 0) + 1;
+          h->log_cap = cfg.collect_iter_log ? std::max<int64_t>(out ? out->iter_log_cap : 0, 0) : 0;
+          h->trace.alloc(size_t(h->trace_cap));
+          h->lg.alloc(size_t(std::max<int64_t>(h->log_cap, 1)));
+          BcProblem& b = dp[size_t(k)];
+          std::memset(&b, 0, sizeof(b));
+          b.C = h->P.C32.p;
+          b.ld = h->P.ld;
+          b.rt = h->marg.p;
+          b.ct = h->marg.p + n;
+          b.r = h->marg.p + 2 * n;
+          b.c = h->marg.p + 3 * n;
+          b.g2 = float(kLog2e / h->gamma);
+          AspotCtl& c = b.ctl0;  // AspotSession::begin's control block
+          c.n = n;
+          c.max_iterations = cfg.max_iterations;
+          c.pause_at = INT64_MAX;
+          c.log_every = cfg.log_every;
+          c.block_rule = cfg.block_rule;
+          c.trace_cap = h->trace_cap;
+          c.log_cap = h->log_cap;
+          c.theta = 1.0;
+          c.gamma = h->gamma;
+          c.eps_tilde = h->st.eps_tilde;
+          c.step_denom = 3.0 * (ksum(h->st.mr.data(), n) + ksum(h->st.mc.data(), n) - h->P.s);
+          c.s = h->P.s;
+          c.status = ST_RUNNING;
+          c.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
+          b.trace = h->trace.p;
+          b.iterlog = h->log_cap > 0 ? h->lg.p : nullptr;
+          b.zc_out = h->outv.p;
+          b.row_slack = h->outv.p + 2 * n + 1;
+          b.col_slack = h->outv.p + 3 * n + 1;
+          PG_CK(cudaStreamSynchronize(cx.stream));
+        } catch (const Error& e) {
+          h->code = e.code;
+          h->err = e.what();
+        }
+        hp[size_t(k)] = std::move(h);
+      }
+      cudaStreamSynchronize(cx.stream);
+      cudaStreamDestroy(cx.stream);
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (int64_t k = 0; k < count; ++k)
+    if (hp[size_t(k)]->code) throw Error(hp[size_t(k)]->code, "problem " + std::to_string(k) + ": " + hp[size_t(k)]->err);
+  int64_t nmax = 0;
+  for (int64_t k = 0; k < count; ++k) nmax = std::max(nmax, hp[size_t(k)]->P.n);
+  // launch geometry
+  const int cs = std::max(1, std::min(16, env_int("POTGPU_BC_CS", 8)));
+  if (ceil_div(nmax, int64_t(cs)) > kBcMaxRows) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
+  const size_t smem = bc_smem_bytes();
+  PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (cs > 8) PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(cs);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.blockDim = dim3(kBcThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = base.stream;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  lc.gridDim = dim3(unsigned(cs * 64));
+  int maxc = 0;
+  PG_CK(cudaOccupancyMaxActiveClusters(&maxc, k_batch_aspot, &lc));
+  if (maxc < 1) throw Error(POTGPU_ERR_UNSUPPORTED, "no resident cluster of this size");
+  int nc = int(std::min<int64_t>(maxc, count));
+  const int cap = env_int("POTGPU_BC_CLUSTERS", 0);
+  if (cap > 0) nc = std::min(nc, cap);
+  lc.gridDim = dim3(unsigned(cs * nc));
+  // per-cluster workspaces
+  const int64_t stride = round_up(2 * nmax + 1, 32);
+  const int64_t per = kSlots * stride + 2 * kRoles * nmax + 6 * nmax + 2 * int64_t(cs) * kBcX;
+  DevBuf<double> wsd;
+  wsd.alloc(size_t(per * nc));
+  DevBuf<float2> colpart;
+  colpart.alloc(size_t(int64_t(cs) * nmax * nc));
+  std::vector<BcWs> hw(static_cast<size_t>(nc));
+  for (int k = 0; k < nc; ++k) {
+    double* b = wsd.p + int64_t(k) * per;
+    hw[size_t(k)] = BcWs{b, b + kSlots * stride, b + kSlots * stride + 2 * kRoles * nmax,
+                         colpart.p + int64_t(k) * cs * nmax, b + kSlots * stride + 2 * kRoles * nmax + 6 * nmax, stride, 0, 0};
+  }
+  DevBuf<BcWs> dws;
+  dws.alloc(size_t(nc));
+  DevBuf<BcProblem> dprob;
+  dprob.alloc(size_t(count));
+  DevBuf<BcResult> dres;
+  dres.alloc(size_t(count));
+  DevBuf<int> queue;
+  queue.alloc(1);
+  cudaStream_t st = base.stream;
+  PG_CK(cudaMemcpyAsync(dws.p, hw.data(), hw.size() * sizeof(BcWs), cudaMemcpyHostToDevice, st));
+  PG_CK(cudaMemcpyAsync(dprob.p, dp.data(), dp.size() * sizeof(BcProblem), cudaMemcpyHostToDevice, st));
+  PG_CK(cudaMemsetAsync(dres.p, 0, size_t(count) * sizeof(BcResult), st));
+  queue.zero(st);
+  const auto t_launch = HostClock::now();
+  PG_CK(cudaLaunchKernelEx(&lc, k_batch_aspot, static_cast<const BcProblem*>(dprob.p), int(count), dws.p, dres.p,
+                           queue.p));
+  PG_CK(cudaGetLastError());
+  std::vector<BcResult> res(static_cast<size_t>(count));
+  PG_CK(cudaMemcpyAsync(res.data(), dres.p, res.size() * sizeof(BcResult), cudaMemcpyDeviceToHost, st));
+  PG_CK(cudaStreamSynchronize(st));
+  (void)t_launch;
+  const double wall = secs(t_start);
+  for (int64_t k = 0; k < count; ++k) {
+    BcHostProblem& h = *hp[size_t(k)];
+    const BcResult& r = res[size_t(k)];
+    const AspotCtl& c = r.ctl;
+    const int64_t n = h.P.n;
+    if (!r.done) throw Error(POTGPU_ERR_CUDA, "problem " + std::to_string(k) + ": not solved by the batch kernel");
+    if (c.fatal) throw Error(c.fatal, "problem " + std::to_string(k) + ": Overflow: B(z) exponent exceeds representable range at z = 0");
+    if (r.infeasible) throw Error(POTGPU_INFEASIBLE, "problem " + std::to_string(k) + ": Infeasible: deficit fill has no slack mass");
+    potgpu_summary* sm = &summaries[k];
+    std::memset(sm, 0, sizeof(*sm));
+    double tb[4];
+    sm->has_bounds = theory_bounds(h.st.mr, h.st.mc, h.P.s, h.P.cmax, h.gamma, h.st.eps_tilde, tb) ? 1 : 0;
+    if (sm->has_bounds) { sm->bound_R = tb[0]; sm->bound_L = tb[1]; sm->bound_mu_f = tb[2]; sm->iteration_bound = tb[3]; }
+    sm->status = c.status;
+    sm->iterations = c.t;
+    sm->gamma = h.gamma;
+    sm->tolerance = h.st.eps_tilde;
+    sm->final_error = c.error;
+    sm->wall_seconds = wall;  // the batch call: every problem finishes inside it
+    sm->loop_seconds = c.loop_end_ns > c.t0_ns ? double(c.loop_end_ns - c.t0_ns) * 1e-9 : 0.0;
+    sm->cost = r.cost;
+    sm->feasibility_gap = r.gap;
+    sm->mass = r.mass;
+    sm->phi = c.phi_check;
+    sm->iter_log_len = c.log_len;
+    sm->sweeps = c.sweeps;
+    sm->attempts = c.attempts;
+    std::strncpy(sm->stopping_iterate, "z_check", sizeof(sm->stopping_iterate));
+    potgpu_outputs* out = outputs ? &outputs[k] : nullptr;
+    // trace records (+ the final record at t, solvers.hpp:375-383), iteration log
+    const int64_t tl0 = std::min(c.trace_len, c.trace_cap);
+    std::vector<TraceDev> tr(size_t(std::max<int64_t>(tl0, 1)));
+    if (tl0 > 0) PG_CK(cudaMemcpy(tr.data(), h.trace.p, size_t(tl0) * sizeof(TraceDev), cudaMemcpyDeviceToHost));
+    int64_t tl = tl0;
+    const bool have_last = c.trace_len > 0 && tl0 > 0 && tr[size_t(tl0 - 1)].t == c.t;
+    if (have_last && cfg.record_rounded_cost) tr[size_t(tl0 - 1)].rounded_cost = r.cost;
+    if (out && out->trace)
+      for (int64_t i = 0; i < std::min(tl0, out->trace_cap); ++i)
+        out->trace[i] = potgpu_trace_record{tr[size_t(i)].t, tr[size_t(i)].error, tr[size_t(i)].phi,
+                                            tr[size_t(i)].rounded_cost, tr[size_t(i)].elapsed_s};
+    if (!have_last) {
+      if (out && out->trace && tl < out->trace_cap) out->trace[tl] = potgpu_trace_record{c.t, c.error, c.phi_check, r.cost, wall};
+      tl += 1;
+    }
+    sm->trace_len = tl;
+    if (out && out->iter_log && out->iter_log_cap > 0 && h.log_cap > 0) {
+      const int64_t m = std::min(std::min(c.log_len, c.log_cap), out->iter_log_cap);
+      std::vector<IterLogDev> lg(size_t(std::max<int64_t>(m, 1)));
+      if (m > 0) PG_CK(cudaMemcpy(lg.data(), h.lg.p, size_t(m) * sizeof(IterLogDev), cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < m; ++i) {
+        const IterLogDev& e = lg[size_t(i)];
+        out->iter_log[i] = potgpu_iter_log{e.t, e.halvings, e.block_hat, e.zbest_is_check, e.block_check, e.error,
+                                           e.phi_check, e.phi_hat, e.theta};
+      }
+    }
+    if (out) {
+      if (out->row_slack) PG_CK(cudaMemcpy(out->row_slack, h.outv.p + 2 * n + 1, size_t(n) * 8, cudaMemcpyDeviceToHost));
+      if (out->col_slack) PG_CK(cudaMemcpy(out->col_slack, h.outv.p + 3 * n + 1, size_t(n) * 8, cudaMemcpyDeviceToHost));
+      if (out->u) PG_CK(cudaMemcpy(out->u, h.outv.p, size_t(n) * 8, cudaMemcpyDeviceToHost));
+      if (out->v) PG_CK(cudaMemcpy(out->v, h.outv.p + n, size_t(n) * 8, cudaMemcpyDeviceToHost));
+      if (out->w) PG_CK(cudaMemcpy(out->w, h.outv.p + 2 * n, 8, cudaMemcpyDeviceToHost));
+    }
+  }
+}
+
 // Batched independent problems (BASELINE configs[4]): `concurrency` host
 // workers, each with its own CUDA stream, pull problems from a shared
 // counter and run complete device-resident solves; the GPU overlaps the
 // streams' kernels. No reference counterpart (the reference solves one
 // instance per call).
 int potgpu_solve_batched(potgpu_ctx* c, int kind, const potgpu_problem* problems, int64_t count,
-                         const potgpu_config* cfg, potgpu_summary* summaries, potgpu_outputs* outputs, int concurrency) {
+                         const potgpu_config* cfg_in, potgpu_summary* summaries, potgpu_outputs* outputs, int concurrency) {
+  const potgpu_config* cfg = cfg_in;
   return guarded([&] {
     if (!c || !problems || !summaries || count < 0) throw Error(POTGPU_INVALID_ARGUMENT, "null argument");
+    {
+      potgpu_config cfg;
+      if (cfg_in) cfg = *cfg_in; else potgpu_config_default(&cfg);
+      if (!c->cx.comm.sharded() && bc_wanted(kind, problems, count, cfg, outputs)) {
+        PG_CK(cudaSetDevice(c->cx.device));
+        bc_solve_batched(c->cx, problems, count, cfg, summaries, outputs, concurrency);
+        return;
+      }
+    }
     const int workers = int(std::max<int64_t>(1, std::min<int64_t>(concurrency > 0 ? concurrency : 8, count)));
     std::atomic<int64_t> next{0};
     std::mutex mu;
@@ -1266,13 +1525,25 @@ int potgpu_comm_init(potgpu_ctx* c, int rank, int world_size, const unsigned cha
   return guarded([&] {
     if (!c || !id) throw Error(POTGPU_INVALID_ARGUMENT, "null context or id");
     if (world_size < 1 || rank < 0 || rank >= world_size) throw Error(POTGPU_INVALID_ARGUMENT, "bad rank / world size");
-    if (c->cx.comm.nccl) throw Error(POTGPU_INVALID_ARGUMENT, "communicator already initialised");
+    if (c->cx.comm.multi()) throw Error(POTGPU_INVALID_ARGUMENT, "communicator already initialised");
     PG_CK(cudaSetDevice(c->cx.device));
     NcclUid uid;
     std::memcpy(uid.internal, id, sizeof(uid.internal));
     void* comm = nullptr;
     nccl_check(nccl_api().CommInitRank(&comm, world_size, uid, rank), "ncclCommInitRank");
     c->cx.comm.nccl = comm;
+    c->cx.comm.rank = rank;
+    c->cx.comm.world = world_size;
+  });
+}
+
+int potgpu_comm_init_host(potgpu_ctx* c, int rank, int world_size, potgpu_host_allreduce_fn allreduce, void* user) {
+  return guarded([&] {
+    if (!c || !allreduce) throw Error(POTGPU_INVALID_ARGUMENT, "null context or all-reduce function");
+    if (world_size < 1 || rank < 0 || rank >= world_size) throw Error(POTGPU_INVALID_ARGUMENT, "bad rank / world size");
+    if (c->cx.comm.multi()) throw Error(POTGPU_INVALID_ARGUMENT, "communicator already initialised");
+    c->cx.comm.host_fn = allreduce;
+    c->cx.comm.host_user = user;
     c->cx.comm.rank = rank;
     c->cx.comm.world = world_size;
   });

@@ -399,6 +399,11 @@ inline int64_t launch_local_sweeps(Context& cx, const DevProblem& P, Workspace& 
 
 // Sum of a host scalar over the processes of a sharded job.
 inline double allreduce_host_sum(Context& cx, Workspace& ws, double x) {
+  if (cx.comm.host_fn) {
+    PG_CK(cudaStreamSynchronize(cx.stream));
+    cx.comm.host_fn(&x, 1, NcclApi::kSum, cx.comm.host_user);
+    return x;
+  }
   if (!cx.comm.nccl) return x;
   PG_CK(cudaMemcpyAsync(ws.xsend.p, &x, sizeof(double), cudaMemcpyHostToDevice, cx.stream));
   nccl_check(nccl_api().AllReduce(ws.xsend.p, ws.xrecv.p, 1, NcclApi::kFloat64, NcclApi::kSum, cx.comm.nccl, cx.stream),

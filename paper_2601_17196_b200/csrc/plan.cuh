@@ -228,6 +228,93 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_f32(const float* __rest
   }
 }
 
+// The same pass for on-the-fly points with the exponent formed in fp64:
+// c_ij = |x_i - y_j|^2 is exact-ish in fp64 from the fp32 coordinates and
+// t = (v_j + lv_j) log2 e - g c_ij rounds once, near the row max, when it
+// goes to fp32 — the fp32 difference form loses ~g c eps (1e-5 relative
+// per entry at C3) in c alone. 8 columns per lane (256 per warp), fp64
+// column coordinates and constants in registers; the cost weights, sums and
+// exponentials in fp32 (B200 runs FP64 at half the FP32 FMA rate: ~7 DFMA
+// per entry keep this an output-stage pass of ~0.2 ms at n = 16384).
+constexpr int kRcCols = 8;  // columns per lane
+constexpr int kRcStrip = 32 * kRcCols;
+
+__global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __restrict__ X, const float4* __restrict__ Y,
+                                                               double g, RowCostArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kRcStrip;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  __shared__ float s_c0[kRcStrip], s_c1[kRcStrip];
+  for (int k = threadIdx.x; k < kRcStrip; k += kThreads) {
+    const int64_t j = j0 + k;
+    s_c0[k] = (j < n && a.b0) ? float(a.b0[j]) : 0.f;
+    s_c1[k] = (j < n && a.b1) ? float(a.b1[j]) : 0.f;
+  }
+  double Bj[kRcCols], yx[kRcCols], yy[kRcCols], yz[kRcCols];
+#pragma unroll
+  for (int k = 0; k < kRcCols; ++k) {
+    const int64_t j = j0 + lane + 32 * k;
+    double vv = -INFINITY;  // padding column: exp2(-inf) = 0
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < n) {
+      vv = a.v[j];
+      if (a.lv) vv = vv + a.lv[j];
+      vv = vv * kLog2e;
+      y = Y[j];
+    }
+    Bj[k] = vv;
+    yx[k] = y.x; yy[k] = y.y; yz[k] = y.z;
+  }
+  __syncthreads();
+  float f0[kRcCols], f1[kRcCols];
+#pragma unroll
+  for (int k = 0; k < kRcCols; ++k) {
+    f0[k] = s_c0[lane + 32 * k];
+    f1[k] = s_c1[lane + 32 * k];
+  }
+  const int64_t ldp = gridDim.x;
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    const float4 xi = X[i];
+    const double xx = xi.x, xy = xi.y, xz = xi.z;
+    float t[kRcCols], cf[kRcCols];
+#pragma unroll
+    for (int k = 0; k < kRcCols; ++k) {
+      const double dx = xx - yx[k], dy = xy - yy[k], dz = xz - yz[k];
+      const double c = fma(dz, dz, fma(dy, dy, dx * dx));
+      t[k] = __double2float_rn(fma(-g, c, Bj[k]));
+      cf[k] = __double2float_rn(c);
+    }
+    float m = t[0];
+#pragma unroll
+    for (int k = 1; k < kRcCols; ++k) m = fmaxf(m, t[k]);
+    m = warp_maxf(m);
+    const float ms = (m == -INFINITY) ? 0.f : m;
+    float R = 0.f, Wc = 0.f, K0 = 0.f, K1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kRcCols; ++k) {
+      const float p = ex2f(t[k] - ms);
+      R += p;
+      Wc = fmaf(cf[k], p, Wc);
+      K0 = fmaf(cf[k], f0[k], K0);
+      K1 = fmaf(cf[k], f1[k], K1);
+    }
+    float4 o = make_float4(R, Wc, K0, K1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      o.x += __shfl_xor_sync(0xffffffffu, o.x, off);
+      o.y += __shfl_xor_sync(0xffffffffu, o.y, off);
+      o.z += __shfl_xor_sync(0xffffffffu, o.z, off);
+      o.w += __shfl_xor_sync(0xffffffffu, o.w, off);
+    }
+    if (lane == 0) {
+      a.part[i * ldp + blockIdx.x] = o;
+      a.pm[i * ldp + blockIdx.x] = ms;
+    }
+  }
+}
+
 // Per row: R_i, W_i (x cost_scale) with the fp64 row offset ((u_i + lu_i) + w) log2 e,
 // K0_i, K1_i (x cost_scale); fixed strip order.
 __global__ void __launch_bounds__(kVecThreads) k_rowcost_reduce(const float4* part, const float* pm, int64_t nstrips,
@@ -313,7 +400,8 @@ struct PlanEngine {
     up(1, lv);
     if (b0) up(6, *b0);
     if (b1) up(7, *b1);
-    const int64_t strips = ceil_div(n, kStripCols32);
+    const bool pts = P.kind == POTGPU_COST_SQEUCLIDEAN;
+    const int64_t strips = ceil_div(n, pts ? int64_t(kRcStrip) : int64_t(kStripCols32));
     const int64_t target_rb = std::max<int64_t>(1, ceil_div(int64_t(cx.num_sms) * 4, strips));
     const int rpc = int(std::max<int64_t>(8, ceil_div(n, target_rb)));
     const dim3 g(unsigned(strips), unsigned(ceil_div(n, rpc)));
@@ -333,10 +421,9 @@ struct PlanEngine {
     a.part = rc_part.p;
     a.pm = rc_pm.p;
     double wscale = 1.0;
-    if (P.kind == POTGPU_COST_SQEUCLIDEAN) {
-      a.g = float(kLog2e * P.cost_scale / gamma);
+    if (pts) {
       wscale = P.cost_scale;
-      k_rowcost_f32<true><<<g, kThreads, 0, cx.stream>>>(nullptr, 0, P.X4.p, P.Y4.p, a);
+      k_rowcost_pts64<<<g, kThreads, 0, cx.stream>>>(P.X4.p, P.Y4.p, kLog2e * P.cost_scale / gamma, a);
     } else {
       a.g = float(kLog2e / gamma);
       k_rowcost_f32<false><<<g, kThreads, 0, cx.stream>>>(P.C32.p, P.ld, nullptr, nullptr, a);

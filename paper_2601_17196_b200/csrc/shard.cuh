@@ -28,6 +28,11 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <map>
+#include <tuple>
+#include <memory>
+#include <vector>
 
 #include "sweep.cuh"
 
@@ -83,14 +88,54 @@ inline void nccl_check(int rc, const char* what) {
   }
 }
 
+// One cross-process reduction of the host backend: captured into the
+// per-iteration graphs as D2H copy -> host node -> H2D copy, so its record
+// must outlive them (owned by the Comm, stable addresses).
+struct HostReduceCall {
+  potgpu_host_allreduce_fn fn = nullptr;
+  void* user = nullptr;
+  double* buf = nullptr;  // pinned
+  int64_t count = 0;
+  int op = 0;
+};
+
+struct PinnedArr {
+  double* p = nullptr;
+  size_t bytes = 0;
+  PinnedArr() = default;
+  PinnedArr(const PinnedArr&) = delete;
+  PinnedArr& operator=(const PinnedArr&) = delete;
+  ~PinnedArr() {
+    if (p) BlockCache::get().free(p, bytes, true);
+  }
+};
+
+// Records of the host backend's reductions, one per (device vector, count,
+// op) call site: reused by every capture and eager call of that site.
+struct HostReduceSites {
+  std::deque<HostReduceCall> calls;
+  std::deque<PinnedArr> bufs;
+  std::map<std::tuple<const double*, int64_t, int>, HostReduceCall*> index;
+};
+
+inline void CUDART_CB host_reduce_trampoline(void* p) {
+  const HostReduceCall* c = static_cast<const HostReduceCall*>(p);
+  c->fn(c->buf, c->count, c->op, c->user);
+}
+
 struct Comm {
   int rank = 0, world = 1;  // processes (one per GPU)
   int vshards = 1;          // row shards computed by this process
   void* nccl = nullptr;     // ncclComm_t when world > 1
+  potgpu_host_allreduce_fn host_fn = nullptr;  // host collective backend (potgpu_comm_init_host)
+  void* host_user = nullptr;
+  std::shared_ptr<HostReduceSites> host_sites = std::make_shared<HostReduceSites>();
   int total() const { return world * vshards; }
-  // an NCCL communicator (even of one rank) routes every reduction through
-  // NCCL, so the multi-GPU plumbing is exercised on one GPU too
-  bool sharded() const { return total() > 1 || nccl != nullptr; }
+  // a cross-process backend (NCCL, even of one rank, or host callbacks)
+  // routes every reduction through it, so the multi-GPU plumbing is
+  // exercised on one GPU too
+  bool multi() const { return nccl != nullptr || host_fn != nullptr; }
+  bool sharded() const { return total() > 1 || multi(); }
   int shard_index(int p) const { return rank * vshards + p; }
   // balanced contiguous row ranges
   int64_t lo(int64_t n, int s) const { return (n * s) / total(); }
@@ -168,8 +213,38 @@ __global__ void k_shard_lse_rescale(double* send, int nsend, int64_t stride, int
 
 // Reduction of `count` doubles: the process's own shards (fixed order), then
 // across processes.
+// Host backend: recv (device) -> pinned -> the caller's all-reduce -> recv.
+inline void host_allreduce(const Comm& cm, cudaStream_t st, double* recv, int64_t count, int op) {
+  HostReduceSites& hs = *cm.host_sites;
+  HostReduceCall*& site = hs.index[std::make_tuple(static_cast<const double*>(recv), count, op)];
+  if (!site) {
+    PinnedArr& b = hs.bufs.emplace_back();
+    b.bytes = size_t(std::max<int64_t>(count, 1)) * sizeof(double);
+    b.p = static_cast<double*>(BlockCache::get().alloc(b.bytes, true));
+    HostReduceCall& c = hs.calls.emplace_back();
+    c.buf = b.p;
+    c.count = count;
+    c.op = op;
+    site = &c;
+  }
+  site->fn = cm.host_fn;
+  site->user = cm.host_user;
+  PG_CK(cudaMemcpyAsync(site->buf, recv, size_t(count) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PG_CK(cudaLaunchHostFunc(st, host_reduce_trampoline, site));
+  PG_CK(cudaMemcpyAsync(recv, site->buf, size_t(count) * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+
 inline void shard_allreduce(const Comm& cm, cudaStream_t st, int num_sms, double* send, int64_t stride, int64_t count,
                             int op, double* recv, const int* gate) {
+  if (cm.host_fn) {
+    // the device sum over this process's shards (a copy for one), then the
+    // host round trip; every rank issues it whatever the gate (same order)
+    const int blocks = int(std::min<int64_t>(num_sms * 4, std::max<int64_t>(1, ceil_div(count, kVecThreads))));
+    launch_k(k_shard_reduce, dim3(blocks), dim3(kVecThreads), 0, st, send, cm.vshards, stride, count, op, recv, nullptr);
+    PG_CK(cudaGetLastError());
+    host_allreduce(cm, st, recv, count, op);
+    return;
+  }
   const bool multi = cm.nccl != nullptr;
   if (cm.vshards > 1 || !multi) {
     const int blocks = int(std::min<int64_t>(num_sms * 4, std::max<int64_t>(1, ceil_div(count, kVecThreads))));

@@ -154,6 +154,11 @@ class _Outputs(ctypes.Structure):
     ]
 
 
+# potgpu_host_allreduce_fn: void (double* buf, int64_t count, int op, void* user)
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_void_p)
+REDUCE_SUM, REDUCE_MAX = 0, 2
+
 # Every symbol include/potgpu.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
     "potgpu_abi_version", "potgpu_last_error", "potgpu_config_default", "potgpu_create", "potgpu_destroy",
@@ -163,7 +168,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
     "potgpu_kmeans_quantize", "potgpu_round_balanced", "potgpu_dual_matrix", "potgpu_session_read_state",
-    "potgpu_session_carry_stats",
+    "potgpu_session_carry_stats", "potgpu_comm_init_host",
 )
 
 _lib = None
@@ -212,6 +217,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
     lib.potgpu_comm_init.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.potgpu_comm_init_local.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.potgpu_comm_init_host.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, HOST_ALLREDUCE_FN,
+                                          ctypes.c_void_p]
     lib.potgpu_comm_info.argtypes = [ctypes.c_void_p, P(ctypes.c_int), P(ctypes.c_int), P(ctypes.c_int)]
     lib.potgpu_make_synthetic.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_double, dp, dp, dp, dp]
@@ -352,6 +359,23 @@ class Context:
         _check(load_library().potgpu_comm_init(self._h, int(rank), int(world_size), bytes(unique_id)))
         return self
 
+    def init_host_comm(self, rank: int, world_size: int, allreduce) -> "Context":
+        """Join a row-sharded job whose cross-process reduction is the Python
+        callable `allreduce(array, op)` (potgpu_comm_init_host): `array` is a
+        float64 numpy view of the host buffer to reduce in place, `op` is
+        REDUCE_SUM or REDUCE_MAX. Runs on a CUDA host-callback thread."""
+        def trampoline(buf, count, op, user):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(int(count),)), int(op))
+            except BaseException as e:  # an exception cannot cross the C boundary
+                import traceback
+                traceback.print_exc()
+                print(f"host all-reduce failed: {e}", flush=True)
+                os._exit(70)
+        self._host_fn = HOST_ALLREDUCE_FN(trampoline)  # kept alive with the context
+        _check(load_library().potgpu_comm_init_host(self._h, int(rank), int(world_size), self._host_fn, None))
+        return self
+
     def comm_info(self) -> Tuple[int, int, int]:
         """(rank, world_size, shards_per_rank)."""
         r, w, v = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
@@ -398,6 +422,24 @@ def init_distributed(ctx: Context, group=None) -> Context:
     box = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(box, src=0, group=group)
     return ctx.init_comm(rank, world, box[0])
+
+
+def init_distributed_host(ctx: Context, group=None) -> Context:
+    """Join the torch.distributed job this process belongs to through the
+    host collective backend: every sweep's all-reduce vector goes through
+    torch.distributed.all_reduce on a CPU tensor (e.g. the gloo backend).
+    Works with several ranks on one GPU; for correctness tests and
+    portability (NCCL: init_distributed)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ops = {REDUCE_SUM: dist.ReduceOp.SUM, REDUCE_MAX: dist.ReduceOp.MAX}
+
+    def allreduce(arr, op):
+        t = torch.from_numpy(arr)  # shares the pinned buffer
+        dist.all_reduce(t, op=ops[op], group=group)
+
+    return ctx.init_host_comm(rank, world, allreduce)
 
 
 _default_ctx: Optional[Context] = None
@@ -711,12 +753,15 @@ def solve(inst: Instance, kind: SolverKind, config: SolverConfig = SolverConfig(
 
 
 def solve_batched(kind: SolverKind, instances: List[Instance], config: SolverConfig = SolverConfig(),
-                  ctx: Optional[Context] = None, concurrency: int = 8, trace_cap: int = 16) -> List[SolveResult]:
+                  ctx: Optional[Context] = None, concurrency: int = 8, trace_cap: int = 16,
+                  iter_log_cap: int = 0) -> List[SolveResult]:
     """Independent problems solved concurrently (potgpu_solve_batched;
     BASELINE configs[4]). Each of the `concurrency` workers plans its grids
     for its share of the SMs, so per-problem results agree with `solve` to
     rounding (different reduction grouping) and are deterministic for a given
-    concurrency."""
+    concurrency. ASPOT on fp32 stored costs (n <= 4096) runs as ONE
+    persistent launch, one problem per thread-block cluster
+    (csrc/batch_cluster.cuh; $POTGPU_BATCH_CLUSTER=0 selects the workers)."""
     lib = load_library()
     ctx = ctx or default_context()
     keep: list = []
@@ -727,7 +772,7 @@ def solve_batched(kind: SolverKind, instances: List[Instance], config: SolverCon
     bufs = []
     for i, inst in enumerate(instances):
         probs[i] = _problem(inst, keep)
-        b = _OutBufs(SolverKind(kind), inst.size(), config, trace_cap, 0)
+        b = _OutBufs(SolverKind(kind), inst.size(), config, trace_cap, iter_log_cap)
         bufs.append(b)
         outs[i] = b.out
     conf = _config(config)

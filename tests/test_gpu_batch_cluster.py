@@ -1,0 +1,142 @@
+"""BASELINE configs[4] as one persistent launch, one problem per
+thread-block cluster (csrc/batch_cluster.cuh, potgpu_solve_batched for
+ASPOT on fp32 stored costs).
+
+The cluster kernel runs the same decision code as the per-problem path
+(apply_role / commit_state / loop_head of aspot_kernels.cuh on a shared-
+memory copy of the control block per CTA) with its own sweeps and fixed-
+order cluster reductions, so against the per-problem session path and the
+fp64 oracle the fp32 bars of north_star apply: objective within 1e-4
+relative, violation <= 1e-5, iteration counts within the fp32 near-tie
+allowance; decision logs identical except where the oracle's own phi values
+tie to 1e-6 (fp32 summation order decides there)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import binding
+from paper_2601_17196_b200 import pot
+
+pytestmark = pytest.mark.gpu
+TOL_OBJ, TOL_VIOL = 1e-4, 1e-5
+
+
+def rand_instance(seed, n):
+    r, c, C, s = binding.random_instance(seed, n)
+    return pot.Instance(r=r, c=c, s=s, C=C, dtype=pot.DType.F32)
+
+
+def oracle_of(inst, eps, **kw):
+    C32 = np.asarray(inst.C, dtype=np.float32).astype(np.float64)
+    return binding.solve(0, inst.r, inst.c, inst.s, C=C32, epsilon=eps, log_every=10 ** 9, want_plan=False, **kw)
+
+
+def cluster_batch(insts, cfg, ctx, **kw):
+    return pot.solve_batched(pot.SolverKind.Aspot, insts, cfg, ctx=ctx, concurrency=4, **kw)
+
+
+def session_batch(insts, cfg, ctx, **kw):
+    os.environ["POTGPU_BATCH_CLUSTER"] = "0"
+    try:
+        return pot.solve_batched(pot.SolverKind.Aspot, insts, cfg, ctx=ctx, concurrency=4, **kw)
+    finally:
+        del os.environ["POTGPU_BATCH_CLUSTER"]
+
+
+def check_feasible(g, s):
+    assert g.feasibility_gap <= TOL_VIOL, g.feasibility_gap
+    assert abs(g.plan.mass - s) <= TOL_VIOL
+    assert np.all(g.plan.row_slack >= -TOL_VIOL) and np.all(g.plan.col_slack >= -TOL_VIOL)
+
+
+@pytest.mark.parametrize("n", [2, 37, 300, 1000, 2048, 3001, 4096])
+def test_ragged_sizes_match_oracle(ctx, n):
+    """Sizes that leave partial strips, idle warps and empty slices."""
+    insts = [rand_instance(100 + n + k, n) for k in range(3)]
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False)
+    res = cluster_batch(insts, cfg, ctx)
+    for inst, g in zip(insts, res):
+        o = oracle_of(inst, 5e-2)
+        assert int(g.status) == o.status, (g.status, o.status)
+        assert abs(g.iterations - o.iterations) <= max(3, 0.05 * o.iterations), (g.iterations, o.iterations)
+        assert abs(g.cost - o.cost) <= TOL_OBJ * abs(o.cost), (g.cost, o.cost)
+        check_feasible(g, inst.s)
+
+
+def test_c5_sixteen_problems_match_oracle_and_sessions(ctx):
+    """16 problems of the configs[4] recipe (n = 2048, per-problem seeds):
+    cluster kernel vs the oracle (fp64 on the fp32-rounded costs) and vs the
+    per-problem session path; decision logs compared over the first 40
+    iterations."""
+    insts = [pot.config_instance(5, seed=1 + k) for k in range(16)]
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False,
+                           collect_iter_log=True)
+    got = cluster_batch(insts, cfg, ctx, iter_log_cap=100000)
+    ref = session_batch(insts, cfg, ctx, iter_log_cap=100000)
+    for k, (inst, g, b) in enumerate(zip(insts, got, ref)):
+        assert int(g.status) == int(b.status) == 0
+        assert abs(g.cost - b.cost) <= TOL_OBJ * abs(b.cost), (k, g.cost, b.cost)
+        assert abs(g.iterations - b.iterations) <= max(3, 0.05 * b.iterations), (k, g.iterations, b.iterations)
+        check_feasible(g, inst.s)
+        la, lb = g.iter_log[:40], b.iter_log[:40]
+        diff = np.any(la[:, 1:5] != lb[:, 1:5], axis=1)
+        ties = np.abs(lb[:, 6] - lb[:, 7]) <= 1e-6 * np.abs(lb[:, 7])
+        assert not np.any(diff & ~ties), (k, np.nonzero(diff & ~ties))
+        np.testing.assert_allclose(la[:, 5:8], lb[:, 5:8], rtol=1e-4)
+        assert g.sweeps > 0 and g.attempts >= g.iterations
+    for k in range(0, 16, 5):  # the oracle on a few (each ~seconds)
+        o = oracle_of(insts[k], 1e-2)
+        assert int(got[k].status) == o.status == 0
+        assert abs(got[k].cost - o.cost) <= TOL_OBJ * abs(o.cost)
+        assert abs(got[k].iterations - o.iterations) <= max(3, 0.05 * o.iterations)
+
+
+def test_mixed_sizes_and_outputs(ctx):
+    """One batch with different n; potentials and slacks match the session path."""
+    insts = [rand_instance(7, 500), rand_instance(8, 2048), rand_instance(9, 64), rand_instance(10, 1500)]
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False)
+    got = cluster_batch(insts, cfg, ctx)
+    ref = session_batch(insts, cfg, ctx)
+    for g, b in zip(got, ref):
+        assert g.iterations == pytest.approx(b.iterations, abs=max(3, 0.05 * b.iterations))
+        assert abs(g.cost - b.cost) <= TOL_OBJ * abs(b.cost)
+        if g.iterations == b.iterations:
+            np.testing.assert_allclose(g.u, b.u, rtol=0, atol=1e-3)
+            np.testing.assert_allclose(g.v, b.v, rtol=0, atol=1e-3)
+        np.testing.assert_allclose(g.plan.row_slack, b.plan.row_slack, rtol=0, atol=1e-6)
+        np.testing.assert_allclose(g.plan.col_slack, b.plan.col_slack, rtol=0, atol=1e-6)
+
+
+def test_trace_records_with_rounded_costs(ctx):
+    """record_rounded_cost with log_every = 10 (solvers.hpp:309-318): every
+    record's rounded cost is computed in the kernel; against the session
+    path record by record."""
+    insts = [rand_instance(21, 800), rand_instance(22, 800)]
+    cfg = pot.SolverConfig(epsilon=5e-2, log_every=10, materialize_plan=False, record_rounded_cost=True)
+    got = cluster_batch(insts, cfg, ctx, trace_cap=4096)
+    ref = session_batch(insts, cfg, ctx, trace_cap=4096)
+    for g, b in zip(got, ref):
+        if g.iterations != b.iterations:
+            continue  # fp32 near-tie moved the stop; compared through the other tests
+        assert [r.t for r in g.trace] == [r.t for r in b.trace]
+        for rg, rb in zip(g.trace, b.trace):
+            assert rg.rounded_cost is not None
+            assert abs(rg.rounded_cost - rb.rounded_cost) <= 1e-4 * abs(rb.rounded_cost), (rg.t, rg.rounded_cost,
+                                                                                              rb.rounded_cost)
+            assert abs(rg.error - rb.error) <= 1e-4 * abs(rb.error)
+
+
+@pytest.mark.parametrize("cs", ["4", "16"])
+def test_cluster_sizes(ctx, cs):
+    insts = [pot.config_instance(5, seed=40 + k) for k in range(3)]
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False)
+    base = cluster_batch(insts, cfg, ctx)
+    os.environ["POTGPU_BC_CS"] = cs
+    try:
+        got = cluster_batch(insts, cfg, ctx)
+    finally:
+        del os.environ["POTGPU_BC_CS"]
+    for g, b in zip(got, base):
+        assert abs(g.cost - b.cost) <= TOL_OBJ * abs(b.cost)
+        assert abs(g.iterations - b.iterations) <= max(3, 0.05 * b.iterations)
