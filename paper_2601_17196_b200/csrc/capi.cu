@@ -640,9 +640,16 @@ struct AspotSession : Session {
     PG_CK(cudaStreamSynchronize(cx.stream));
   }
 
-  // round_pot(b_matrix(ctx, z_check), in) (solvers.hpp:315, :371)
-  PlanResult round_now(double* Xdev) {
+  // round_pot(b_matrix(ctx, z_check), in) (solvers.hpp:315, :371): on the
+  // device (plan.cuh enqueue_round_device) unless a dense plan is wanted or
+  // the job is sharded; `full` also returns the plan terms (registration).
+  PlanResult round_now(double* Xdev, bool full = false) {
     const int64_t n = P.n;
+    if (!Xdev && device_round_ok(cx, P, ws)) {
+      enqueue_round_device(cx, P, ws, gamma, ws.slot(S_ZC), ws.row(R_CHECK), &ws.ctl.p->ro, nullptr, nullptr, nullptr);
+      sync_ctl();
+      return collect_round_device(cx, P, ws, ws.host_ctl->ro, full);
+    }
     PlanEngine pe(cx, P, ws, gamma);
     HVec row0(static_cast<size_t>(n)), ones(static_cast<size_t>(n), 1.0);
     PG_CK(cudaMemcpy(row0.data(), ws.row(R_CHECK), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
@@ -829,7 +836,7 @@ struct AspotSession : Session {
 
   PlanResult final_plan(double* Xdev) override {
     if (trivial) throw Error(POTGPU_ERR_UNSUPPORTED, "trivial solve has no device plan");
-    return round_now(Xdev);
+    return round_now(Xdev, true);
   }
   Slot plan_point() override { return ws.slot(S_ZC); }
   void read_state(int which, double* u, double* v, double* w, double* scalars) override {

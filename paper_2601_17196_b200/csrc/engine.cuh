@@ -137,6 +137,10 @@ struct Workspace {
   DevBuf<double> rt, ct;    // marginals the dual targets
   DevBuf<double> ro_buf;    // rounding vectors: rho, kappa, lu, lv, rowx, colx, a, b, row_slack, col_slack
   DevBuf<double> ro_r, ro_c;  // original marginals for rounding
+  DevBuf<float4> rc_part;     // fused final pass of the device rounding (plan.cuh): fp32 [row][strip] partials
+  DevBuf<float> rc_pm;
+  DevBuf<double> rc_part64;   // fp64 problems: [row][strip][3]
+  DevBuf<int> rc_gate;
   DevBuf<AspotCtl> ctl;
   DevBuf<unsigned> ticket;
   PinnedObj<AspotCtl> host_ctl_buf;
@@ -284,6 +288,17 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.ro_buf.alloc(size_t(10 * n));
   ws.ro_r.alloc(size_t(n));
   ws.ro_c.alloc(size_t(n));
+  PG_CK(cudaMemcpyAsync(ws.ro_r.p, P.r.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+  PG_CK(cudaMemcpyAsync(ws.ro_c.p, P.c.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+  if (!cx.comm.sharded()) {  // the device rounding's fused pass (plan.cuh round_device)
+    if (P.dtype == POTGPU_F64) {
+      if (P.kind == POTGPU_COST_DENSE) ws.rc_part64.alloc(size_t(3 * n * ceil_div(n, kStripCols)));
+    } else {
+      const int64_t strips = ceil_div(n, P.kind == POTGPU_COST_SQEUCLIDEAN ? int64_t(256) : int64_t(512));
+      ws.rc_part.alloc(size_t(n * strips));
+      ws.rc_pm.alloc(size_t(n * strips));
+    }
+  }
   ws.ctl.alloc(1);
   if (!ws.host_ctl) ws.host_ctl = ws.host_ctl_buf.get();
   ws.trace.alloc(size_t(std::max<int64_t>(trace_cap, 1)));

@@ -17,7 +17,10 @@ namespace potgpu {
 // with the fp32 row-partial offset (u_i + lu_i + w) log2 e.
 __global__ void __launch_bounds__(kVecThreads) k_sum_partials(const double* rowp, int64_t nstrips, const double* colp,
                                                              int64_t nrb, int pfmt, Slot z, const double* lu,
-                                                             const double* rowshift, double* row, double* col) {
+                                                             const double* rowshift, double* row, double* col,
+                                                             const int* gate) {
+  pdl_wait();
+  if (gate && *gate == 0) return;
   const int64_t n = z.n;
   const double w = *z.w();
   for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -130,12 +133,15 @@ struct RowCostArgs {
   float g;                           // log2 e / gamma (dense C) or log2 e cost_scale / gamma (points)
   float4* part;                      // [row][strip]: (R, W) relative to 2^m, (K0, K1)
   float* pm;                         // [row][strip]: m
+  const int* gate;                   // null: always
 };
 
 template <bool POINTS>
 __global__ void __launch_bounds__(kThreads, 2) k_rowcost_f32(const float* __restrict__ C, int64_t ld,
                                                              const float4* __restrict__ X, const float4* __restrict__ Y,
                                                              RowCostArgs a) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t j0 = int64_t(blockIdx.x) * kStripCols32;
@@ -241,6 +247,8 @@ constexpr int kRcStrip = 32 * kRcCols;
 
 __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __restrict__ X, const float4* __restrict__ Y,
                                                                double g, RowCostArgs a) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t j0 = int64_t(blockIdx.x) * kRcStrip;
@@ -320,7 +328,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
 __global__ void __launch_bounds__(kVecThreads) k_rowcost_reduce(const float4* part, const float* pm, int64_t nstrips,
                                                                int64_t row_lo, int64_t row_hi, const double* u,
                                                                const double* lu, const double* w, double wscale,
-                                                               double* R, double* W, double* K0, double* K1) {
+                                                               double* R, double* W, double* K0, double* K1,
+                                                               const int* gate) {
+  pdl_wait();
+  if (gate && *gate == 0) return;
   const double ww = *w;
   for (int64_t i = row_lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < row_hi;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -369,7 +380,7 @@ struct PlanEngine {
     if (lv) up(1, *lv);
     const SweepOut so = sweep_point(cx, P, ws, z, lu ? d(0) : nullptr, lv ? d(1) : nullptr, nullptr, false, gamma);
     k_sum_partials<<<ws.nblk, kVecThreads, 0, cx.stream>>>(so.rowp, so.nstrips, so.colp, so.nrb, so.pfmt, z,
-                                                           lu ? d(0) : nullptr, so.rowshift, d(2), d(3));
+                                                           lu ? d(0) : nullptr, so.rowshift, d(2), d(3), nullptr);
     PG_CK(cudaGetLastError());
     row.resize(size_t(n));
     col.resize(size_t(n));
@@ -430,7 +441,7 @@ struct PlanEngine {
     }
     // R, W, K0, K1 land in d(2), d(3), d(8), d(9)
     k_rowcost_reduce<<<ws.nblk, kVecThreads, 0, cx.stream>>>(rc_part.p, rc_pm.p, strips, 0, n, z.u(), d(0), z.w(),
-                                                             wscale, d(2), d(3), d(8), d(9));
+                                                             wscale, d(2), d(3), d(8), d(9), nullptr);
     PG_CK(cudaGetLastError());
     for (HVec* h : {&R, &W, &K0, &K1}) h->resize(size_t(n));
     PG_CK(cudaMemcpyAsync(R.data(), d(2), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, cx.stream));
@@ -650,6 +661,345 @@ inline PlanResult round_pot_implicit(PlanEngine& pe, Slot z, const HVec& P0, con
   if (a) {
     out.a1 = std::move(ra);
     out.b1 = std::move(kb);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------------
+// round_pot (rounding.hpp:46-77) of B(z) ON THE DEVICE for the ASPOT plan
+// (P0 = Q0 = 1, no rank-1 input term): the same arithmetic as
+// round_pot_implicit with the O(n) scaling logic in three single-block
+// kernels around the two sweeps (column-clip column sums; fused final row
+// sums + <C, X>), no host round trip in between. Capturable: the per-record
+// rounding of record_rounded_cost runs inside the attempt graph (gate).
+//
+// ro vectors (Workspace::rv): 0 log rho, 1 log kappa, 2 alpha rho, 3 colX3,
+// 4 fb = max(c - colX3, 0), 5 R (final row sums of B diag(kappa)), 6 W, 7 K,
+// 8 row slack, 9 col slack; + the column sums of the clip sweep in 3.
+constexpr int kDrThreads = 1024;
+
+__device__ __forceinline__ double dr_block_sum(double x, double* sh) {  // fixed order, all threads get it
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if (lane == 0) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    x = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sh[32] = x;
+  }
+  __syncthreads();
+  return sh[32];
+}
+__device__ __forceinline__ double dr_block_max(double x, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  if (lane == 0) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    x = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) sh[32] = x;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+struct DevRoundArgs {
+  int64_t n;
+  const double* row0;  // B(z) 1
+  const double* r;     // original marginals
+  const double* c;
+  double s;
+  double* v;           // 10 n ro vectors
+  RoundOut* ro;
+  const int* gate;     // null: always
+  // record rounding: the last appended trace record gets the cost
+  const AspotCtl* ctl;
+  TraceDev* trace;
+};
+
+// out *= min(1, s / mass); row clip rho (rounding.hpp:52-56)
+__global__ void __launch_bounds__(kDrThreads) k_dr_rowclip(DevRoundArgs a) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  __shared__ double sh[33];
+  const int64_t n = a.n;
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m += a.row0[i];
+  const double mass1 = dr_block_sum(m, sh);
+  const double alpha = mass1 > 0 ? fmin(1.0, a.s / mass1) : 1.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double row = alpha * a.row0[i];
+    const double rh = row > 0 ? fmin(1.0, a.r[i] / row) : 1.0;
+    a.v[i] = log(rh);
+    a.v[2 * n + i] = alpha * rh;
+  }
+  if (threadIdx.x == 0) a.ro->alpha = alpha;
+}
+
+// column clip kappa (rounding.hpp:57-61) from the column sums cc of diag(rho) B
+__global__ void __launch_bounds__(kDrThreads) k_dr_colclip(DevRoundArgs a, const double* cc) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  const int64_t n = a.n;
+  const double alpha = a.ro->alpha;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double col3 = alpha * cc[j];
+    const double kp = col3 > 0 ? fmin(1.0, a.c[j] / col3) : 1.0;
+    const double cx3 = kp * col3;
+    a.v[n + j] = log(kp);
+    a.v[3 * n + j] = cx3;
+    a.v[4 * n + j] = fmax(a.c[j] - cx3, 0.0);
+  }
+}
+
+// deficit fill (rounding.hpp:63-75), <C, X> (core.hpp:199-204), slacks and
+// plan_feasibility_gap (core.hpp:207-219)
+__global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  __shared__ double sh[33];
+  const int64_t n = a.n;
+  const double* arho = a.v + 2 * n;
+  const double* cx3 = a.v + 3 * n;
+  const double* fb = a.v + 4 * n;
+  const double* R = a.v + 5 * n;
+  const double* W = a.v + 6 * n;
+  const double* K = a.v + 7 * n;
+  double m3 = 0.0, na = 0.0, nb = 0.0, saw = 0.0, sfk = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x3 = arho[i] * R[i];
+    const double fa = fmax(a.r[i] - x3, 0.0);
+    m3 += x3;
+    na += fa;
+    nb += fb[i];
+    saw += arho[i] * W[i];
+    sfk += fa * K[i];
+  }
+  m3 = dr_block_sum(m3, sh);
+  na = dr_block_sum(na, sh);
+  nb = dr_block_sum(nb, sh);
+  saw = dr_block_sum(saw, sh);
+  sfk = dr_block_sum(sfk, sh);
+  const double deficit = a.s - m3;
+  double f = 0.0;
+  int infeasible = 0;
+  if (deficit > 0) {
+    if (na <= 0 || nb <= 0) infeasible = 1;
+    else f = deficit / (na * nb);
+  }
+  double rg = 0.0, cg = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x3 = arho[i] * R[i];
+    const double fa = fmax(a.r[i] - x3, 0.0);
+    const double rx = x3 + f * fa * nb;
+    const double cx = cx3[i] + f * na * fb[i];
+    a.v[8 * n + i] = a.r[i] - rx;
+    a.v[9 * n + i] = a.c[i] - cx;
+    rg = fmax(rg, fmax(rx - a.r[i], 0.0));
+    cg = fmax(cg, fmax(cx - a.c[i], 0.0));
+  }
+  rg = dr_block_max(rg, sh);
+  cg = dr_block_max(cg, sh);
+  if (threadIdx.x == 0) {
+    RoundOut& o = *a.ro;
+    o.mass3 = m3; o.na = na; o.nb = nb; o.f = f;
+    o.mass = m3 + f * na * nb;
+    o.cost = saw + f * sfk;
+    o.row_gap = rg; o.col_gap = cg;
+    o.gap = fmax(fmax(rg, cg), fabs(o.mass - a.s));
+    o.infeasible = infeasible;
+    if (a.trace && a.ctl && a.ctl->trace_len >= 1 && a.ctl->trace_len <= a.ctl->trace_cap)
+      a.trace[a.ctl->trace_len - 1].rounded_cost = o.cost;
+  }
+}
+
+// fp64 stored logK: the fused final pass (rows of B diag(kappa), W, K) with
+// the reference's exponent association and clamp (k_plan_cost), cost
+// C_ij = -logK_ij gamma (ElemDenseF64). Partials [row][strip] x 3 (fp64).
+__global__ void __launch_bounds__(kThreads, 2) k_rowcost_f64(const double* __restrict__ L, int64_t ld, double gamma,
+                                                             RowCostArgs a, double* part) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t j0 = int64_t(blockIdx.x) * kStripCols;
+  double vj[8], fbj[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t j = j0 + 2 * lane + 64 * k + e;
+      double vv = -INFINITY, ff = 0.0;
+      if (j < n) {
+        vv = a.v[j];
+        if (a.lv) vv = vv + a.lv[j];
+        if (a.b0) ff = a.b0[j];
+      }
+      vj[2 * k + e] = vv;
+      fbj[2 * k + e] = ff;
+    }
+  const double w = *a.w;
+  const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
+  const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    const double ui = a.u[i];
+    const double2* row = reinterpret_cast<const double2*>(L + i * ld + j0) + lane;
+    double R = 0.0, Wc = 0.0, K = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 x = __ldcs(row + 32 * k);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double lk = e ? x.y : x.x;
+        const double ee = ((lk + ui) + vj[2 * k + e]) + w;
+        const double B = vj[2 * k + e] == -INFINITY ? 0.0 : exp(fmin(fmax(ee, kExpLo), kExpHi));
+        const double cst = vj[2 * k + e] == -INFINITY ? 0.0 : -lk * gamma;
+        R += B;
+        Wc += cst * B;
+        K += cst * fbj[2 * k + e];
+      }
+    }
+    R = warp_sum(R);
+    Wc = warp_sum(Wc);
+    K = warp_sum(K);
+    if (lane == 0) {
+      double* o = part + (i * gridDim.x + blockIdx.x) * 3;
+      o[0] = R; o[1] = Wc; o[2] = K;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_rowcost_reduce64(const double* part, int64_t nstrips, int64_t n,
+                                                                 const int* gate, double* R, double* W, double* K) {
+  pdl_wait();
+  if (gate && *gate == 0) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double r = 0.0, wc = 0.0, k = 0.0;
+    for (int64_t s = 0; s < nstrips; ++s) {
+      const double* o = part + (i * nstrips + s) * 3;
+      r += o[0]; wc += o[1]; k += o[2];
+    }
+    R[i] = r; W[i] = wc; K[i] = k;
+  }
+}
+
+__global__ void k_gate_copy(const int* gate, int* dst) {  // a kernel-side copy of a gate for kernels without one
+  pdl_wait();
+  *dst = gate ? *gate : 1;
+}
+
+// The device rounding of the ASPOT plan: enqueue (capturable) ...
+inline bool device_round_ok(const Context& cx, const DevProblem& P, const Workspace& ws) {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_DEVICE_ROUND");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || cx.comm.sharded()) return false;
+  if (P.dtype == POTGPU_F64) return P.kind == POTGPU_COST_DENSE && ws.rc_part64.p;
+  return ws.rc_part.p != nullptr;
+}
+
+inline void enqueue_round_device(Context& cx, const DevProblem& P, Workspace& ws, double gamma, Slot z,
+                                 const double* row0, RoundOut* ro, const int* gate, const AspotCtl* ctl,
+                                 TraceDev* trace) {
+  const int64_t n = P.n;
+  DevRoundArgs a{n, row0, ws.ro_r.p, ws.ro_c.p, P.s, ws.rv(0), ro, gate, ctl, trace};
+  launch_k(k_dr_rowclip, dim3(1), dim3(kDrThreads), 0, cx.stream, a);
+  // column clip: column sums of diag(rho) B (plain exp, the reference's b_matrix of the rounding input)
+  launch_sweep(cx, P, ws, z, ws.rv(0), nullptr, gate, false, gamma);
+  launch_k(k_sum_partials, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, static_cast<const double*>(ws.rowp.p),
+           ws.nstrips, static_cast<const double*>(ws.colp.p), ws.nrb, ws.pfmt, z, static_cast<const double*>(ws.rv(0)),
+           P.rowshift(), ws.rv(5), ws.rv(3), gate);
+  launch_k(k_dr_colclip, dim3(1), dim3(kDrThreads), 0, cx.stream, a, static_cast<const double*>(ws.rv(3)));
+  // final row sums of B diag(kappa) + the cost's per-row terms
+  RowCostArgs ra{};
+  ra.n = n;
+  ra.row_lo = 0;
+  ra.row_hi = n;
+  ra.u = z.u(); ra.v = z.v(); ra.w = z.w();
+  ra.lv = ws.rv(1);
+  ra.b0 = ws.rv(4);
+  ra.b1 = nullptr;
+  ra.gate = gate;
+  if (P.dtype == POTGPU_F64) {
+    const int64_t strips = ceil_div(n, int64_t(kStripCols));
+    const int64_t target_rb = std::max<int64_t>(1, ceil_div(int64_t(cx.num_sms) * 4, strips));
+    ra.rows_per_cta = int(std::max<int64_t>(8, ceil_div(n, target_rb)));
+    const dim3 g(unsigned(strips), unsigned(ceil_div(n, ra.rows_per_cta)));
+    launch_k(k_rowcost_f64, g, dim3(kThreads), 0, cx.stream, static_cast<const double*>(P.L64.p), P.ld, gamma, ra,
+             ws.rc_part64.p);
+    launch_k(k_rowcost_reduce64, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream,
+             static_cast<const double*>(ws.rc_part64.p), strips, n, gate, ws.rv(5), ws.rv(6), ws.rv(7));
+  } else {
+    const bool pts = P.kind == POTGPU_COST_SQEUCLIDEAN;
+    const int64_t strips = ceil_div(n, pts ? int64_t(kRcStrip) : int64_t(kStripCols32));
+    const int64_t target_rb = std::max<int64_t>(1, ceil_div(int64_t(cx.num_sms) * 4, strips));
+    ra.rows_per_cta = int(std::max<int64_t>(8, ceil_div(n, target_rb)));
+    const dim3 g(unsigned(strips), unsigned(ceil_div(n, ra.rows_per_cta)));
+    ra.part = ws.rc_part.p;
+    ra.pm = ws.rc_pm.p;
+    double wscale = 1.0;
+    if (pts) {
+      wscale = P.cost_scale;
+      launch_k(k_rowcost_pts64, g, dim3(kThreads), 0, cx.stream, static_cast<const float4*>(P.X4.p),
+               static_cast<const float4*>(P.Y4.p), kLog2e * P.cost_scale / gamma, ra);
+    } else {
+      ra.g = float(kLog2e / gamma);
+      launch_k(k_rowcost_f32<false>, g, dim3(kThreads), 0, cx.stream, static_cast<const float*>(P.C32.p), P.ld,
+               static_cast<const float4*>(nullptr), static_cast<const float4*>(nullptr), ra);
+    }
+    launch_k(k_rowcost_reduce, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, static_cast<const float4*>(ws.rc_part.p),
+             static_cast<const float*>(ws.rc_pm.p), strips, int64_t(0), n, z.u(), static_cast<const double*>(nullptr),
+             z.w(), wscale, ws.rv(5), ws.rv(6), ws.rv(7), ws.rv(8) /* K1 = 0 (no rank-1 input); slack slot, rewritten */, gate);
+  }
+  launch_k(k_dr_finish, dim3(1), dim3(kDrThreads), 0, cx.stream, a);
+  PG_CK(cudaGetLastError());
+}
+
+// ... and collect: the PlanResult of round_pot_implicit (plan terms only when `full`).
+inline PlanResult collect_round_device(Context& cx, const DevProblem& P, Workspace& ws, const RoundOut& ro, bool full) {
+  const int64_t n = P.n;
+  if (ro.infeasible) throw Error(POTGPU_INFEASIBLE, "Infeasible: deficit fill has no slack mass");
+  PlanResult out;
+  out.cost = ro.cost;
+  out.mass = ro.mass;
+  out.gap = ro.gap;
+  out.row_slack.resize(size_t(n));
+  out.col_slack.resize(size_t(n));
+  PG_CK(cudaMemcpyAsync(out.row_slack.data(), ws.rv(8), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  PG_CK(cudaMemcpyAsync(out.col_slack.data(), ws.rv(9), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  HVec lk, arho, cx3, fb, R;
+  if (full) {
+    for (HVec* h : {&lk, &arho, &cx3, &fb, &R}) h->resize(size_t(n));
+    PG_CK(cudaMemcpyAsync(lk.data(), ws.rv(1), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(arho.data(), ws.rv(2), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(cx3.data(), ws.rv(3), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(fb.data(), ws.rv(4), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+    PG_CK(cudaMemcpyAsync(R.data(), ws.rv(5), size_t(n) * 8, cudaMemcpyDeviceToHost, cx.stream));
+  }
+  PG_CK(cudaStreamSynchronize(cx.stream));
+  if (full) {
+    out.Pf = arho;
+    out.Qf.resize(size_t(n));
+    out.a0.resize(size_t(n));
+    out.rowx.resize(size_t(n));
+    out.colx.resize(size_t(n));
+    for (int64_t i = 0; i < n; ++i) {
+      const double x3 = arho[size_t(i)] * R[size_t(i)];
+      const double fa = std::max(P.r[size_t(i)] - x3, 0.0);
+      out.Qf[size_t(i)] = std::exp(lk[size_t(i)]);
+      out.a0[size_t(i)] = ro.f * fa;
+      out.rowx[size_t(i)] = x3 + ro.f * fa * ro.nb;
+      out.colx[size_t(i)] = cx3[size_t(i)] + ro.f * ro.na * fb[size_t(i)];
+    }
+    out.b0 = std::move(fb);
   }
   return out;
 }

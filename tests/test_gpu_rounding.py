@@ -122,7 +122,61 @@ def test_fused_fp32_output_stage_matches_dense_plan(ctx, kind, cost):
     C = pot.dense_cost(f32(pts.X), f32(pts.Y), pts.cost_scale) if cost == "points" else f32(inst.C)
     ref = float(np.sum(C * b.plan.X))
     assert abs(b.cost - ref) <= 1e-9 * abs(ref), (b.cost, ref)
-    assert abs(a.cost - ref) <= 1e-6 * abs(ref), (a.cost, ref)
+    # dense32: both paths sum the same fp32 exponents; points: the fused
+    # pass forms the exponent in fp64 (k_rowcost_pts64) while the dense-plan
+    # path's final row sums come from the solver's fp32 sweep, and the
+    # deficit fill moves with those sums (measured 2.2e-6 on B200)
+    tol = 1e-6 if cost == "dense32" else 1e-5
+    assert abs(a.cost - ref) <= tol * abs(ref), (a.cost, ref)
     np.testing.assert_allclose(a.plan.row_slack, b.plan.row_slack, rtol=0, atol=1e-9)
     np.testing.assert_allclose(a.plan.col_slack, b.plan.col_slack, rtol=0, atol=1e-9)
     assert a.feasibility_gap <= 1e-5
+
+
+DEVICE_ROUND_SNIPPET = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+from paper_2601_17196_b200 import pot
+out = {}
+pts = pot.config_instance(3, n=1200)
+cases = {"f64": pot.config_instance(1, n=700),
+         "dense32": pot.Instance(r=pts.r, c=pts.c, s=pts.s, C=pot.dense_cost(pts.X, pts.Y, pts.cost_scale),
+                                 dtype=pot.DType.F32),
+         "points": pts}
+for name, inst in cases.items():
+    cfg = pot.SolverConfig(epsilon=2e-2, log_every=10 ** 9, max_iterations=400, materialize_plan=False)
+    g = pot.aspot_solve(inst, cfg)
+    out[name] = {"it": g.iterations, "cost": g.cost, "gap": g.feasibility_gap, "mass": g.plan.mass,
+                 "rs": g.plan.row_slack.tolist(), "cs": g.plan.col_slack.tolist()}
+print(json.dumps(out))
+"""
+
+
+def test_device_rounding_matches_host_rounding():
+    """round_pot of the ASPOT plan on the device (plan.cuh enqueue_round_device:
+    single-block O(n) kernels around the two sweeps, one download) against
+    the host-orchestrated implicit rounding ($POTGPU_DEVICE_ROUND=0), fp64
+    stored, fp32 stored and fp32 points."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, POTGPU_DEVICE_ROUND=flag)
+        r = subprocess.run([sys.executable, "-c", DEVICE_ROUND_SNIPPET % root], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[flag] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in ("f64", "dense32", "points"):
+        d, h = res["1"][name], res["0"][name]
+        assert d["it"] == h["it"]
+        tol = 1e-12 if name == "f64" else (1e-6 if name == "dense32" else 1e-5)
+        assert abs(d["cost"] - h["cost"]) <= tol * abs(h["cost"]), (name, d["cost"], h["cost"])
+        assert abs(d["mass"] - h["mass"]) <= 1e-12
+        atol = 1e-14 if name == "f64" else 1e-8
+        np.testing.assert_allclose(d["rs"], h["rs"], rtol=0, atol=atol)
+        np.testing.assert_allclose(d["cs"], h["cs"], rtol=0, atol=atol)
+        assert d["gap"] <= (1e-7 if name == "f64" else 1e-5)
