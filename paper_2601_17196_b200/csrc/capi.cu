@@ -1247,13 +1247,24 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaMemsetAsync(dres.p, 0, size_t(count) * sizeof(BcResult), st));
   queue.zero(st);
   const auto t_launch = HostClock::now();
+  cudaEvent_t e0, e1;
+  PG_CK(cudaEventCreate(&e0));
+  PG_CK(cudaEventCreate(&e1));
+  PG_CK(cudaEventRecord(e0, st));
   PG_CK(cudaLaunchKernelEx(&lc, k_batch_aspot, static_cast<const BcProblem*>(dprob.p), int(count), dws.p, dres.p,
                            queue.p));
   PG_CK(cudaGetLastError());
+  PG_CK(cudaEventRecord(e1, st));
   std::vector<BcResult> res(static_cast<size_t>(count));
   PG_CK(cudaMemcpyAsync(res.data(), dres.p, res.size() * sizeof(BcResult), cudaMemcpyDeviceToHost, st));
   PG_CK(cudaStreamSynchronize(st));
-  (void)t_launch;
+  float kms = 0.f;
+  PG_CK(cudaEventElapsedTime(&kms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (std::getenv("POTGPU_TRACE_SETUP"))
+    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d)\n",
+                 (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs);
   const double wall = secs(t_start);
   for (int64_t k = 0; k < count; ++k) {
     BcHostProblem& h = *hp[size_t(k)];
