@@ -41,7 +41,6 @@ constexpr int kBcWarps = kBcThreads / 32;
 constexpr int kBcStrip = 512;     // columns per warp segment (16 per lane)
 constexpr int kBcMaxStrips = 8;   // n <= 4096
 constexpr int kBcMaxN = kBcStrip * kBcMaxStrips;
-constexpr int kBcMaxRows = 512;   // rows per CTA (n / cluster size)
 constexpr int kBcX = kNumAcc + 2; // exchanged scalars per CTA: accumulators, flag, spare
 
 // One problem of the batch (host-filled, device array).
@@ -81,13 +80,13 @@ struct BcWs {
   int pad;
 };
 
+// Fixed part of the CTA's shared memory; the row-sized arrays follow it
+// (bc_smem_layout): A[rows] (fp32 row offsets), rowpart[rows][S] (segment
+// (sum, max) per row and strip), then a region used either as the per-warp
+// column accumulators [16][512] or, in the cost pass, as wk[rows][S]
+// (segment sums of C p and C fb). rows = ceil(n_max / cluster size).
 struct BcShared {
   uint32_t ctl[kCtlWords];
-  float A[kBcMaxRows];                     // fp32 row offsets of the CTA's rows
-  float2 rowpart[kBcMaxRows][kBcMaxStrips];  // (segment sum, segment max) per row and strip
-  float wpart[kBcMaxRows][kBcMaxStrips];   // cost mode: segment sum of C p
-  float kpart[kBcMaxRows][kBcMaxStrips];   // cost mode: segment sum of C fb
-  float colacc[kBcWarps][kBcStrip];        // per-warp column accumulators
   float colsig[kBcWarps];
   float wmax[kBcWarps];
   double red[kBcX][kBcWarps];
@@ -95,12 +94,26 @@ struct BcShared {
   int flag;
 };
 
-__host__ __device__ constexpr size_t bc_smem_bytes() { return sizeof(BcShared); }
+struct BcLayout {
+  int rows_cap, s_cap;
+  __host__ __device__ size_t off_A() const { return (sizeof(BcShared) + 15) & ~size_t(15); }
+  __host__ __device__ size_t off_rowpart() const { return (off_A() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
+  __host__ __device__ size_t off_u() const { return off_rowpart() + size_t(rows_cap) * s_cap * 8; }
+  __host__ __device__ size_t bytes() const {
+    const size_t u = size_t(rows_cap) * s_cap * 8, c = size_t(kBcWarps) * kBcStrip * 4;
+    return off_u() + (u > c ? u : c);
+  }
+};
 
 struct BcCtx {
   const BcProblem* P;
   BcWs* W;
   BcShared* sm;
+  float* A;         // [rows_cap]
+  float2* rowpart;  // [rows_cap][s_cap]
+  float* colacc;    // [kBcWarps][kBcStrip] (sweep) ...
+  float2* wk;       // ... or [rows_cap][s_cap] (cost pass)
+  int s_cap;
   AspotCtl* c;     // == sm->ctl
   int64_t n;
   int rank, cs;
@@ -182,7 +195,7 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
   for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
     double a = __ldcg(u + i);
     if (lu) a = a + __ldcg(lu + i);
-    sm.A[i - X.lo] = float((a + w) * kLog2e);
+    X.A[i - X.lo] = float((a + w) * kLog2e);
   }
   const int S = int((n + kBcStrip - 1) / kBcStrip);
   const int PH = kBcWarps / S;
@@ -269,14 +282,11 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
       }
       const int64_t il = i - X.lo;
       if (lane == 0) {
-        sm.rowpart[il][strip] = make_float2(rs, ms);
-        if (COST) {
-          sm.wpart[il][strip] = ws;
-          sm.kpart[il][strip] = ks;
-        }
+        X.rowpart[il * X.s_cap + strip] = make_float2(rs, ms);
+        if (COST) X.wk[il * X.s_cap + strip] = make_float2(ws, ks);
       }
       if (!COST) {
-        const float mA = (m == -INFINITY) ? -INFINITY : m + sm.A[il];
+        const float mA = (m == -INFINITY) ? -INFINITY : m + X.A[il];
         if (mA > sigma) {  // warp-uniform
           const float sc = ex2f(sigma - mA);
 #pragma unroll
@@ -295,8 +305,8 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
 #pragma unroll
     for (int q = 0; q < kPairs; ++q) {
       const int cidx = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
-      sm.colacc[warp][cidx] = cacc[q].x;
-      sm.colacc[warp][cidx + 1] = cacc[q].y;
+      X.colacc[warp * kBcStrip + cidx] = cacc[q].x;
+      X.colacc[warp * kBcStrip + cidx + 1] = cacc[q].y;
     }
     if (lane == 0) {
       sm.colsig[warp] = sigma;
@@ -312,13 +322,14 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
     const double a2 = (a + w) * kLog2e;
     double rr = 0.0, wc = 0.0, kk = 0.0;
     for (int s = 0; s < S; ++s) {
-      const float2 rp = sm.rowpart[il][s];
+      const float2 rp = X.rowpart[il * X.s_cap + s];
+      const float2 wkp = COST ? X.wk[il * X.s_cap + s] : make_float2(0.f, 0.f);
       if (rp.x != 0.f) {
         const double sc = exp2(double(rp.y) + a2);
         rr += double(rp.x) * sc;
-        if (COST) wc += double(sm.wpart[il][s]) * sc;
+        if (COST) wc += double(wkp.x) * sc;
       }
-      if (COST) kk += double(sm.kpart[il][s]);
+      if (COST) kk += double(wkp.y);
     }
     rows_out[i] = rr;
     if (COST) {
@@ -342,7 +353,7 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
     if (SIG != -INFINITY)
       for (int p2 = 0; p2 < PH; ++p2) {
         const float sg = sm.colsig[p2 * S + s];
-        if (sg != -INFINITY) acc += sm.colacc[p2 * S + s][cidx] * ex2f(sg - SIG);
+        if (sg != -INFINITY) acc += X.colacc[(p2 * S + s) * kBcStrip + cidx] * ex2f(sg - SIG);
       }
     cp[j] = (SIG == -INFINITY) ? make_float2(0.f, 0.f) : make_float2(acc, SIG);
   }
@@ -582,7 +593,7 @@ __device__ void bc_record_cost(BcCtx& X, int64_t len_before, TraceDev* trace) {
 
 // The persistent batch kernel: grid = cs x clusters, cluster = (cs, 1, 1).
 __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* probs, int count, BcWs* wss,
-                                                              BcResult* results, int* queue) {
+                                                              BcResult* results, int* queue, BcLayout lay) {
   extern __shared__ __align__(16) unsigned char bc_smem_raw[];
   BcShared* sm = reinterpret_cast<BcShared*>(bc_smem_raw);
   cgx::cluster_group cl = cgx::this_cluster();
@@ -600,6 +611,11 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.W = W;
     X.sm = sm;
     X.c = reinterpret_cast<AspotCtl*>(sm->ctl);
+    X.A = reinterpret_cast<float*>(bc_smem_raw + lay.off_A());
+    X.rowpart = reinterpret_cast<float2*>(bc_smem_raw + lay.off_rowpart());
+    X.colacc = reinterpret_cast<float*>(bc_smem_raw + lay.off_u());
+    X.wk = reinterpret_cast<float2*>(bc_smem_raw + lay.off_u());
+    X.s_cap = lay.s_cap;
     X.n = X.P->ctl0.n;
     X.rank = rank;
     X.cs = cs;

@@ -1196,9 +1196,22 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   int64_t nmax = 0;
   for (int64_t k = 0; k < count; ++k) nmax = std::max(nmax, hp[size_t(k)]->P.n);
   // launch geometry
-  const int cs = std::max(1, std::min(16, env_int("POTGPU_BC_CS", 8)));
-  if (ceil_div(nmax, int64_t(cs)) > kBcMaxRows) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
-  const size_t smem = bc_smem_bytes();
+  // cluster size: $POTGPU_BC_CS, else the smallest whose per-CTA rows fit
+  // shared memory (every problem's CTAs stream at the per-SM rate and share
+  // HBM, so more, smaller clusters win: measured C5, kernel 0.90 / 1.20 /
+  // 1.96 s with 4 / 8 / 16 CTAs per cluster)
+  const int64_t scap = ceil_div(nmax, int64_t(kBcStrip));
+  auto layout_of = [&](int c) { return BcLayout{int(ceil_div(nmax, int64_t(c))), int(scap)}; };
+  int cs = env_int("POTGPU_BC_CS", 0);
+  if (cs <= 0) {
+    cs = 16;
+    for (int c : {1, 2, 4, 8, 16})
+      if (layout_of(c).bytes() <= size_t(200) * 1024) { cs = c; break; }
+  }
+  cs = std::max(1, std::min(16, cs));
+  const BcLayout lay = layout_of(cs);
+  const size_t smem = lay.bytes();
+  if (smem > size_t(227) * 1024) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
   PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (cs > 8) PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
@@ -1252,7 +1265,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaEventCreate(&e1));
   PG_CK(cudaEventRecord(e0, st));
   PG_CK(cudaLaunchKernelEx(&lc, k_batch_aspot, static_cast<const BcProblem*>(dprob.p), int(count), dws.p, dres.p,
-                           queue.p));
+                           queue.p, lay));
   PG_CK(cudaGetLastError());
   PG_CK(cudaEventRecord(e1, st));
   std::vector<BcResult> res(static_cast<size_t>(count));

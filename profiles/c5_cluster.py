@@ -19,7 +19,7 @@ from paper_2601_17196_b200 import pot  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--count", type=int, default=256)
-    ap.add_argument("--variants", default="8:0,16:0,4:0,16:6,8:7")
+    ap.add_argument("--variants", default="0:0,2:0,4:0,8:0")
     args = ap.parse_args()
     ctx = pot.Context(0)
     insts = [pot.config_instance(5, seed=1 + k) for k in range(args.count)]
@@ -29,7 +29,7 @@ def main():
     pot.solve_batched(pot.SolverKind.Aspot, insts[:8], cfg, ctx=ctx)  # warm
     for v in args.variants.split(","):
         cs, cap = v.split(":")
-        os.environ["POTGPU_BC_CS"] = cs
+        os.environ["POTGPU_BC_CS"] = cs  # 0: automatic
         os.environ["POTGPU_BC_CLUSTERS"] = cap
         t0 = time.perf_counter()
         res = pot.solve_batched(pot.SolverKind.Aspot, insts, cfg, ctx=ctx)

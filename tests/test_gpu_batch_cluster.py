@@ -147,7 +147,7 @@ def test_trace_records_with_rounded_costs(ctx):
             assert abs(rg.error - rb.error) <= 1e-4 * abs(rb.error)
 
 
-@pytest.mark.parametrize("cs", ["4", "16"])
+@pytest.mark.parametrize("cs", ["2", "4", "8", "16"])
 def test_cluster_sizes(ctx, cs):
     insts = [pot.config_instance(5, seed=40 + k) for k in range(3)]
     cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, materialize_plan=False, record_rounded_cost=False)
