@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 
 #include "aspot_kernels.cuh"
+#include "sweep_tc.cuh"  // smem_u32, mbarrier helpers
 
 namespace potgpu {
 
@@ -94,15 +95,21 @@ struct BcShared {
   int flag;
 };
 
+// + a per-warp ring of nst row-segment buffers (2 KB each) that the bulk
+// copy engine fills (cp.async.bulk, one mbarrier per stage): every warp
+// keeps nst rows of C in flight without holding them in registers.
+constexpr int kBcSeg = kBcStrip * 4;  // bytes of one row segment
 struct BcLayout {
-  int rows_cap, s_cap;
+  int rows_cap, s_cap, nst;
   __host__ __device__ size_t off_A() const { return (sizeof(BcShared) + 15) & ~size_t(15); }
   __host__ __device__ size_t off_rowpart() const { return (off_A() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
   __host__ __device__ size_t off_u() const { return off_rowpart() + size_t(rows_cap) * s_cap * 8; }
-  __host__ __device__ size_t bytes() const {
+  __host__ __device__ size_t off_ring() const {
     const size_t u = size_t(rows_cap) * s_cap * 8, c = size_t(kBcWarps) * kBcStrip * 4;
-    return off_u() + (u > c ? u : c);
+    return (off_u() + (u > c ? u : c) + 127) & ~size_t(127);
   }
+  __host__ __device__ size_t off_bar() const { return off_ring() + size_t(kBcWarps) * nst * kBcSeg; }
+  __host__ __device__ size_t bytes() const { return off_bar() + size_t(kBcWarps) * nst * 8 + kBcWarps * 4; }
 };
 
 struct BcCtx {
@@ -114,6 +121,10 @@ struct BcCtx {
   float* colacc;    // [kBcWarps][kBcStrip] (sweep) ...
   float2* wk;       // ... or [rows_cap][s_cap] (cost pass)
   int s_cap;
+  int nst;
+  float4* ring;                 // [kBcWarps][nst][kBcStrip / 4]
+  unsigned long long* bars;     // [kBcWarps][nst]
+  uint32_t* uses;               // [kBcWarps]: row segments this warp consumed so far
   AspotCtl* c;     // == sm->ctl
   int64_t n;
   int rank, cs;
@@ -125,6 +136,14 @@ struct BcCtx {
 };
 
 __device__ __forceinline__ void bc_sync() { cgx::this_cluster().sync(); }
+
+// bulk copy (TMA, non-tensor) of `bytes` from global memory into this CTA's
+// shared memory, completing on `bar` (which the issuing lane arms)
+__device__ __forceinline__ void bc_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 
 // Fixed-order cluster reduction of kBcX scalars (acc_join semantics for the
 // first kNumAcc, max for the flag): every CTA writes its row, one barrier,
@@ -229,20 +248,30 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
   float sigma = -INFINITY, mmax = -INFINITY;
   const float2 G = make_float2(-P.g2, -P.g2);
   if (active) {
-    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
-    const int64_t ld4 = P.ld / 4;
-    int64_t i = X.lo + ph;
-    float4 nxt[4];
-    if (i < X.hi)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
-    for (; i < X.hi; i += PH) {
+    // rows i = lo + ph + k PH, k < cnt, streamed through the warp's ring
+    const int64_t cnt = X.hi > X.lo + ph ? (X.hi - X.lo - ph + PH - 1) / PH : 0;
+    const float* gseg = P.C + j0;
+    float4* ring = X.ring + int64_t(warp) * X.nst * (kBcStrip / 4);
+    unsigned long long* bars = X.bars + warp * X.nst;
+    const uint32_t u0 = X.uses[warp];
+    auto issue = [&](int64_t k) {  // lane 0: row k of this warp into its stage
+      const uint32_t st = (u0 + uint32_t(k)) % uint32_t(X.nst);
+      fence_async_smem();
+      bc_bulk_g2s(ring + st * (kBcStrip / 4), gseg + (X.lo + ph + k * PH) * P.ld, kBcSeg, bars + st);
+    };
+    if (lane == 0)
+      for (int64_t k = 0; k < cnt && k < X.nst; ++k) issue(k);
+    for (int64_t k = 0; k < cnt; ++k) {
+      const int64_t i = X.lo + ph + k * PH;
+      const uint32_t uk = u0 + uint32_t(k);
+      const uint32_t st = uk % uint32_t(X.nst);
+      mbar_wait(bars + st, (uk / uint32_t(X.nst)) & 1u);
       float4 cur[4];
+      const float4* seg = ring + st * (kBcStrip / 4) + lane;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
-      if (i + PH < X.hi)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
+      for (int q4 = 0; q4 < 4; ++q4) cur[q4] = seg[32 * q4];
+      __syncwarp();
+      if (lane == 0 && k + X.nst < cnt) issue(k + X.nst);
       float2 cc[kPairs], t[kPairs];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -300,6 +329,8 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
         for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
       }
     }
+    __syncwarp();
+    if (lane == 0) X.uses[warp] = u0 + uint32_t(cnt);
   }
   if (!COST) {
 #pragma unroll
@@ -601,6 +632,14 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
   const int rank = int(cl.block_rank());
   const int cid = int(blockIdx.x) / cs;
   BcWs* W = wss + cid;
+  {  // the warps' ring barriers (live for the whole launch)
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(bc_smem_raw + lay.off_bar());
+    uint32_t* uses = reinterpret_cast<uint32_t*>(bc_smem_raw + lay.off_bar() + size_t(kBcWarps) * lay.nst * 8);
+    if (threadIdx.x < kBcWarps * lay.nst) mbar_init(bars + threadIdx.x, 1);
+    if (threadIdx.x < kBcWarps) uses[threadIdx.x] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+  }
   for (;;) {
     if (rank == 0 && threadIdx.x == 0) W->cur = atomicAdd(queue, 1);
     bc_sync();
@@ -616,6 +655,10 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.colacc = reinterpret_cast<float*>(bc_smem_raw + lay.off_u());
     X.wk = reinterpret_cast<float2*>(bc_smem_raw + lay.off_u());
     X.s_cap = lay.s_cap;
+    X.nst = lay.nst;
+    X.ring = reinterpret_cast<float4*>(bc_smem_raw + lay.off_ring());
+    X.bars = reinterpret_cast<unsigned long long*>(bc_smem_raw + lay.off_bar());
+    X.uses = reinterpret_cast<uint32_t*>(bc_smem_raw + lay.off_bar() + size_t(kBcWarps) * lay.nst * 8);
     X.n = X.P->ctl0.n;
     X.rank = rank;
     X.cs = cs;

@@ -1201,17 +1201,25 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   // HBM, so more, smaller clusters win: measured C5, kernel 0.90 / 1.20 /
   // 1.96 s with 4 / 8 / 16 CTAs per cluster)
   const int64_t scap = ceil_div(nmax, int64_t(kBcStrip));
-  auto layout_of = [&](int c) { return BcLayout{int(ceil_div(nmax, int64_t(c))), int(scap)}; };
+  // (stages of each warp's bulk-copy ring: $POTGPU_BC_STAGES, default 4,
+  // fewer when shared memory is short)
+  const int want_nst = std::max(1, std::min(8, env_int("POTGPU_BC_STAGES", 4)));
+  constexpr size_t kSmemMax = size_t(227) * 1024;
+  auto layout_of = [&](int c) {
+    BcLayout l{int(ceil_div(nmax, int64_t(c))), int(scap), want_nst};
+    while (l.nst > 1 && l.bytes() > kSmemMax) --l.nst;
+    return l;
+  };
   int cs = env_int("POTGPU_BC_CS", 0);
   if (cs <= 0) {
     cs = 16;
     for (int c : {1, 2, 4, 8, 16})
-      if (layout_of(c).bytes() <= size_t(200) * 1024) { cs = c; break; }
+      if (layout_of(c).bytes() <= kSmemMax && layout_of(c).nst >= std::min(want_nst, 3)) { cs = c; break; }
   }
   cs = std::max(1, std::min(16, cs));
   const BcLayout lay = layout_of(cs);
   const size_t smem = lay.bytes();
-  if (smem > size_t(227) * 1024) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
+  if (smem > kSmemMax) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
   PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (cs > 8) PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
@@ -1276,8 +1284,9 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (std::getenv("POTGPU_TRACE_SETUP"))
-    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d)\n",
-                 (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs);
+    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %d ring stages, %zu B smem)\n",
+                 (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs,
+                 lay.nst, smem);
   const double wall = secs(t_start);
   for (int64_t k = 0; k < count; ++k) {
     BcHostProblem& h = *hp[size_t(k)];
