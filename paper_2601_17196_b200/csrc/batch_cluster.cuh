@@ -67,6 +67,7 @@ struct BcResult {
   double cost, mass, gap;
   int infeasible;
   int done;
+  uint64_t sweep_ns, total_ns;  // rank 0's device time inside the solve's sweeps / the whole problem
 };
 
 // Global workspace of one cluster (reused by every problem it takes).
@@ -130,6 +131,7 @@ struct BcCtx {
   int rank, cs;
   int64_t lo, hi;  // the CTA's index slice
   int xphase;      // exchange buffer parity (uniform over the cluster)
+  uint64_t sweep_ns;  // time spent in sweeps (thread 0)
   __device__ double* slot(int k) const { return W->slots + k * W->stride; }
   __device__ double* rows(int role) const { return W->sums + int64_t(2 * role) * n; }
   __device__ double* cols(int role) const { return W->sums + int64_t(2 * role + 1) * n; }
@@ -415,8 +417,10 @@ __device__ __forceinline__ double bc_col_sum(const BcCtx& X, int64_t j) {
 __device__ __noinline__ void bc_eval_swept(BcCtx& X, int slot, int role) {
   bc_sync();  // the point's slices (every CTA's writes) are complete
   const double* z = X.slot(slot);
+  const uint64_t ts = globaltimer_ns();
   const double maxe = bc_sweep<false>(X, z, nullptr, nullptr, nullptr, X.rows(role), nullptr, nullptr);
   bc_sync();  // column partials of every CTA
+  X.sweep_ns += globaltimer_ns() - ts;
   double acc[kBcX];
 #pragma unroll
   for (int k = 0; k < kBcX; ++k) acc[k] = k < kNumAcc ? acc_init(k) : 0.0;
@@ -665,6 +669,8 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.lo = X.n * rank / cs;
     X.hi = X.n * (rank + 1) / cs;
     X.xphase = 0;
+    X.sweep_ns = 0;
+    const uint64_t t_problem = globaltimer_ns();
     {  // control block copy, zero dual points (z = z_check = z_bar = 0)
       const uint32_t* src = reinterpret_cast<const uint32_t*>(&X.P->ctl0);
       for (int k = threadIdx.x; k < kCtlWords; k += kBcThreads) sm->ctl[k] = src[k];
@@ -784,6 +790,8 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
       c->loop_end_ns = c->loop_end_ns ? c->loop_end_ns : globaltimer_ns();
       results[p].ctl = *c;
       results[p].done = 1;
+      results[p].sweep_ns = X.sweep_ns;
+      results[p].total_ns = globaltimer_ns() - t_problem;
       double* zo = X.P->zc_out;
       if (zo) zo[2 * n] = __ldcg(X.slot(S_ZC) + 2 * n);
     }

@@ -1283,6 +1283,12 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaEventElapsedTime(&kms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (std::getenv("POTGPU_TRACE_SETUP")) {
+    double sw = 0, tot = 0;
+    for (const BcResult& r : res) { sw += double(r.sweep_ns); tot += double(r.total_ns); }
+    std::fprintf(stderr, "[potgpu] batch cluster: per problem %.3f ms on its cluster, %.1f %% in sweeps (rank 0)\n",
+                 tot / double(count) * 1e-6, tot > 0 ? 100.0 * sw / tot : 0.0);
+  }
   if (std::getenv("POTGPU_TRACE_SETUP"))
     std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %d ring stages, %zu B smem)\n",
                  (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs,
