@@ -263,72 +263,107 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
     };
     if (lane == 0)
       for (int64_t k = 0; k < cnt && k < X.nst; ++k) issue(k);
-    for (int64_t k = 0; k < cnt; ++k) {
-      const int64_t i = X.lo + ph + k * PH;
-      const uint32_t uk = u0 + uint32_t(k);
-      const uint32_t st = uk % uint32_t(X.nst);
-      mbar_wait(bars + st, (uk / uint32_t(X.nst)) & 1u);
-      float4 cur[4];
-      const float4* seg = ring + st * (kBcStrip / 4) + lane;
+    // two rows per step: two independent chains (segment max -> CREDUX ->
+    // MUFU burst -> sums) per warp instead of one
+    for (int64_t k = 0; k < cnt; k += 2) {
+      const bool two = k + 1 < cnt;
+      float2 cc[2][kPairs];
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) cur[q4] = seg[32 * q4];
+      for (int r = 0; r < 2; ++r) {
+        if (r == 1 && !two) {
+#pragma unroll
+          for (int q = 0; q < kPairs; ++q) cc[1][q] = make_float2(0.f, 0.f);
+          continue;
+        }
+        const uint32_t uk = u0 + uint32_t(k + r);
+        const uint32_t st = uk % uint32_t(X.nst);
+        mbar_wait(bars + st, (uk / uint32_t(X.nst)) & 1u);
+        const float4* seg = ring + st * (kBcStrip / 4) + lane;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 v4 = seg[32 * q4];
+          cc[r][2 * q4] = make_float2(v4.x, v4.y);
+          cc[r][2 * q4 + 1] = make_float2(v4.z, v4.w);
+        }
+      }
       __syncwarp();
-      if (lane == 0 && k + X.nst < cnt) issue(k + X.nst);
-      float2 cc[kPairs], t[kPairs];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        cc[2 * k] = make_float2(cur[k].x, cur[k].y);
-        cc[2 * k + 1] = make_float2(cur[k].z, cur[k].w);
+      if (lane == 0) {
+        if (k + X.nst < cnt) issue(k + X.nst);
+        if (k + 1 + X.nst < cnt) issue(k + 1 + X.nst);
       }
+      float2 p[2][kPairs];
+      float m[2], ms[2];
 #pragma unroll
-      for (int q = 0; q < kPairs; ++q) t[q] = __ffma2_rn(G, cc[q], Bj[q]);
-      float m = warp_maxf(tree_max2<kPairs>(t));
-      const float ms = (m == -INFINITY) ? 0.f : m;
-      const float2 M2 = make_float2(-ms, -ms);
-      float2 p[kPairs];
+      for (int r = 0; r < 2; ++r) {
+        const bool live = r == 0 || two;
 #pragma unroll
-      for (int q = 0; q < kPairs; ++q) {
-        const float2 d = __fadd2_rn(t[q], M2);
-        p[q] = make_float2(ex2f(d.x), ex2f(d.y));
-      }
-      float rs = tree_sum2<kPairs>(p);
-      float ws = 0.f, ks = 0.f;
-      if (COST) {
-        float2 W2 = make_float2(0.f, 0.f), K2 = W2;
+        for (int q = 0; q < kPairs; ++q)
+          p[r][q] = live ? __ffma2_rn(G, cc[r][q], Bj[q]) : make_float2(-INFINITY, -INFINITY);
+        m[r] = warp_maxf(tree_max2<kPairs>(p[r]));
+        ms[r] = (m[r] == -INFINITY) ? 0.f : m[r];
+        const float2 M2 = make_float2(-ms[r], -ms[r]);
 #pragma unroll
         for (int q = 0; q < kPairs; ++q) {
-          W2 = __ffma2_rn(cc[q], p[q], W2);
-          K2 = __ffma2_rn(cc[q], Fb[q], K2);
+          const float2 d = __fadd2_rn(p[r][q], M2);
+          p[r][q] = make_float2(ex2f(d.x), ex2f(d.y));
         }
-        ws = W2.x + W2.y;
-        ks = K2.x + K2.y;
+      }
+      float rs[2], ws[2] = {0.f, 0.f}, ks[2] = {0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        rs[r] = tree_sum2<kPairs>(p[r]);
+        if (COST) {
+          float2 W2 = make_float2(0.f, 0.f), K2 = W2;
+#pragma unroll
+          for (int q = 0; q < kPairs; ++q) {
+            W2 = __ffma2_rn(cc[r][q], p[r][q], W2);
+            K2 = __ffma2_rn(cc[r][q], Fb[q], K2);
+          }
+          ws[r] = W2.x + W2.y;
+          ks[r] = K2.x + K2.y;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        rs += __shfl_xor_sync(0xffffffffu, rs, o);
-        if (COST) {
-          ws += __shfl_xor_sync(0xffffffffu, ws, o);
-          ks += __shfl_xor_sync(0xffffffffu, ks, o);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], o);
+          if (COST) {
+            ws[r] += __shfl_xor_sync(0xffffffffu, ws[r], o);
+            ks[r] += __shfl_xor_sync(0xffffffffu, ks[r], o);
+          }
         }
       }
-      const int64_t il = i - X.lo;
+      const int64_t il0 = X.lo + ph + k * PH - X.lo;
       if (lane == 0) {
-        X.rowpart[il * X.s_cap + strip] = make_float2(rs, ms);
-        if (COST) X.wk[il * X.s_cap + strip] = make_float2(ws, ks);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (r == 1 && !two) break;
+          const int64_t il = il0 + r * PH;
+          X.rowpart[il * X.s_cap + strip] = make_float2(rs[r], ms[r]);
+          if (COST) X.wk[il * X.s_cap + strip] = make_float2(ws[r], ks[r]);
+        }
       }
       if (!COST) {
-        const float mA = (m == -INFINITY) ? -INFINITY : m + X.A[il];
-        if (mA > sigma) {  // warp-uniform
-          const float sc = ex2f(sigma - mA);
+        float mA[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          mA[r] = (m[r] == -INFINITY) ? -INFINITY : m[r] + X.A[il0 + (r == 1 && two ? PH : 0)];
+        const float mx = fmaxf(mA[0], mA[1]);
+        if (mx > sigma) {  // warp-uniform
+          const float sc = ex2f(sigma - mx);
 #pragma unroll
           for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
-          sigma = mA;
+          sigma = mx;
         }
-        mmax = fmaxf(mmax, mA);
-        const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
-        const float2 F2 = make_float2(f, f);
+        mmax = fmaxf(mmax, mx);
 #pragma unroll
-        for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
+        for (int r = 0; r < 2; ++r) {
+          const float f = (mA[r] == -INFINITY) ? 0.f : ex2f(mA[r] - sigma);
+          const float2 F2 = make_float2(f, f);
+#pragma unroll
+          for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[r][q], F2, cacc[q]);
+        }
       }
     }
     __syncwarp();
