@@ -31,7 +31,6 @@
 #include <cooperative_groups.h>
 
 #include "aspot_kernels.cuh"
-#include "sweep_tc.cuh"  // smem_u32, mbarrier helpers
 
 namespace potgpu {
 
@@ -96,21 +95,15 @@ struct BcShared {
   int flag;
 };
 
-// + a per-warp ring of nst row-segment buffers (2 KB each) that the bulk
-// copy engine fills (cp.async.bulk, one mbarrier per stage): every warp
-// keeps nst rows of C in flight without holding them in registers.
-constexpr int kBcSeg = kBcStrip * 4;  // bytes of one row segment
 struct BcLayout {
-  int rows_cap, s_cap, nst;
+  int rows_cap, s_cap;
   __host__ __device__ size_t off_A() const { return (sizeof(BcShared) + 15) & ~size_t(15); }
   __host__ __device__ size_t off_rowpart() const { return (off_A() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
   __host__ __device__ size_t off_u() const { return off_rowpart() + size_t(rows_cap) * s_cap * 8; }
-  __host__ __device__ size_t off_ring() const {
+  __host__ __device__ size_t bytes() const {
     const size_t u = size_t(rows_cap) * s_cap * 8, c = size_t(kBcWarps) * kBcStrip * 4;
-    return (off_u() + (u > c ? u : c) + 127) & ~size_t(127);
+    return off_u() + (u > c ? u : c);
   }
-  __host__ __device__ size_t off_bar() const { return off_ring() + size_t(kBcWarps) * nst * kBcSeg; }
-  __host__ __device__ size_t bytes() const { return off_bar() + size_t(kBcWarps) * nst * 8 + kBcWarps * 4; }
 };
 
 struct BcCtx {
@@ -122,10 +115,6 @@ struct BcCtx {
   float* colacc;    // [kBcWarps][kBcStrip] (sweep) ...
   float2* wk;       // ... or [rows_cap][s_cap] (cost pass)
   int s_cap;
-  int nst;
-  float4* ring;                 // [kBcWarps][nst][kBcStrip / 4]
-  unsigned long long* bars;     // [kBcWarps][nst]
-  uint32_t* uses;               // [kBcWarps]: row segments this warp consumed so far
   AspotCtl* c;     // == sm->ctl
   int64_t n;
   int rank, cs;
@@ -138,14 +127,6 @@ struct BcCtx {
 };
 
 __device__ __forceinline__ void bc_sync() { cgx::this_cluster().sync(); }
-
-// bulk copy (TMA, non-tensor) of `bytes` from global memory into this CTA's
-// shared memory, completing on `bar` (which the issuing lane arms)
-__device__ __forceinline__ void bc_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 // Fixed-order cluster reduction of kBcX scalars (acc_join semantics for the
 // first kNumAcc, max for the flag): every CTA writes its row, one barrier,
@@ -250,124 +231,77 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
   float sigma = -INFINITY, mmax = -INFINITY;
   const float2 G = make_float2(-P.g2, -P.g2);
   if (active) {
-    // rows i = lo + ph + k PH, k < cnt, streamed through the warp's ring
-    const int64_t cnt = X.hi > X.lo + ph ? (X.hi - X.lo - ph + PH - 1) / PH : 0;
-    const float* gseg = P.C + j0;
-    float4* ring = X.ring + int64_t(warp) * X.nst * (kBcStrip / 4);
-    unsigned long long* bars = X.bars + warp * X.nst;
-    const uint32_t u0 = X.uses[warp];
-    auto issue = [&](int64_t k) {  // lane 0: row k of this warp into its stage
-      const uint32_t st = (u0 + uint32_t(k)) % uint32_t(X.nst);
-      fence_async_smem();
-      bc_bulk_g2s(ring + st * (kBcStrip / 4), gseg + (X.lo + ph + k * PH) * P.ld, kBcSeg, bars + st);
-    };
-    if (lane == 0)
-      for (int64_t k = 0; k < cnt && k < X.nst; ++k) issue(k);
-    // two rows per step: two independent chains (segment max -> CREDUX ->
-    // MUFU burst -> sums) per warp instead of one
-    for (int64_t k = 0; k < cnt; k += 2) {
-      const bool two = k + 1 < cnt;
-      float2 cc[2][kPairs];
+    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
+    const int64_t ld4 = P.ld / 4;
+    int64_t i = X.lo + ph;
+    float4 nxt[4];
+    if (i < X.hi)
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (r == 1 && !two) {
+      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
+    for (; i < X.hi; i += PH) {
+      float4 cur[4];
 #pragma unroll
-          for (int q = 0; q < kPairs; ++q) cc[1][q] = make_float2(0.f, 0.f);
-          continue;
-        }
-        const uint32_t uk = u0 + uint32_t(k + r);
-        const uint32_t st = uk % uint32_t(X.nst);
-        mbar_wait(bars + st, (uk / uint32_t(X.nst)) & 1u);
-        const float4* seg = ring + st * (kBcStrip / 4) + lane;
+      for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+      if (i + PH < X.hi)
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const float4 v4 = seg[32 * q4];
-          cc[r][2 * q4] = make_float2(v4.x, v4.y);
-          cc[r][2 * q4 + 1] = make_float2(v4.z, v4.w);
-        }
+        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
+      float2 cc[kPairs], t[kPairs];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cc[2 * k] = make_float2(cur[k].x, cur[k].y);
+        cc[2 * k + 1] = make_float2(cur[k].z, cur[k].w);
       }
-      __syncwarp();
-      if (lane == 0) {
-        if (k + X.nst < cnt) issue(k + X.nst);
-        if (k + 1 + X.nst < cnt) issue(k + 1 + X.nst);
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) t[q] = __ffma2_rn(G, cc[q], Bj[q]);
+      float m = warp_maxf(tree_max2<kPairs>(t));
+      const float ms = (m == -INFINITY) ? 0.f : m;
+      const float2 M2 = make_float2(-ms, -ms);
+      float2 p[kPairs];
+#pragma unroll
+      for (int q = 0; q < kPairs; ++q) {
+        const float2 d = __fadd2_rn(t[q], M2);
+        p[q] = make_float2(ex2f(d.x), ex2f(d.y));
       }
-      float2 p[2][kPairs];
-      float m[2], ms[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const bool live = r == 0 || two;
-#pragma unroll
-        for (int q = 0; q < kPairs; ++q)
-          p[r][q] = live ? __ffma2_rn(G, cc[r][q], Bj[q]) : make_float2(-INFINITY, -INFINITY);
-        m[r] = warp_maxf(tree_max2<kPairs>(p[r]));
-        ms[r] = (m[r] == -INFINITY) ? 0.f : m[r];
-        const float2 M2 = make_float2(-ms[r], -ms[r]);
+      float rs = tree_sum2<kPairs>(p);
+      float ws = 0.f, ks = 0.f;
+      if (COST) {
+        float2 W2 = make_float2(0.f, 0.f), K2 = W2;
 #pragma unroll
         for (int q = 0; q < kPairs; ++q) {
-          const float2 d = __fadd2_rn(p[r][q], M2);
-          p[r][q] = make_float2(ex2f(d.x), ex2f(d.y));
+          W2 = __ffma2_rn(cc[q], p[q], W2);
+          K2 = __ffma2_rn(cc[q], Fb[q], K2);
         }
-      }
-      float rs[2], ws[2] = {0.f, 0.f}, ks[2] = {0.f, 0.f};
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        rs[r] = tree_sum2<kPairs>(p[r]);
-        if (COST) {
-          float2 W2 = make_float2(0.f, 0.f), K2 = W2;
-#pragma unroll
-          for (int q = 0; q < kPairs; ++q) {
-            W2 = __ffma2_rn(cc[r][q], p[r][q], W2);
-            K2 = __ffma2_rn(cc[r][q], Fb[q], K2);
-          }
-          ws[r] = W2.x + W2.y;
-          ks[r] = K2.x + K2.y;
-        }
+        ws = W2.x + W2.y;
+        ks = K2.x + K2.y;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], o);
-          if (COST) {
-            ws[r] += __shfl_xor_sync(0xffffffffu, ws[r], o);
-            ks[r] += __shfl_xor_sync(0xffffffffu, ks[r], o);
-          }
+        rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (COST) {
+          ws += __shfl_xor_sync(0xffffffffu, ws, o);
+          ks += __shfl_xor_sync(0xffffffffu, ks, o);
         }
       }
-      const int64_t il0 = X.lo + ph + k * PH - X.lo;
+      const int64_t il = i - X.lo;
       if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          if (r == 1 && !two) break;
-          const int64_t il = il0 + r * PH;
-          X.rowpart[il * X.s_cap + strip] = make_float2(rs[r], ms[r]);
-          if (COST) X.wk[il * X.s_cap + strip] = make_float2(ws[r], ks[r]);
-        }
+        X.rowpart[il * X.s_cap + strip] = make_float2(rs, ms);
+        if (COST) X.wk[il * X.s_cap + strip] = make_float2(ws, ks);
       }
       if (!COST) {
-        float mA[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-          mA[r] = (m[r] == -INFINITY) ? -INFINITY : m[r] + X.A[il0 + (r == 1 && two ? PH : 0)];
-        const float mx = fmaxf(mA[0], mA[1]);
-        if (mx > sigma) {  // warp-uniform
-          const float sc = ex2f(sigma - mx);
+        const float mA = (m == -INFINITY) ? -INFINITY : m + X.A[il];
+        if (mA > sigma) {  // warp-uniform
+          const float sc = ex2f(sigma - mA);
 #pragma unroll
           for (int q = 0; q < kPairs; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
-          sigma = mx;
+          sigma = mA;
         }
-        mmax = fmaxf(mmax, mx);
+        mmax = fmaxf(mmax, mA);
+        const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sigma);
+        const float2 F2 = make_float2(f, f);
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const float f = (mA[r] == -INFINITY) ? 0.f : ex2f(mA[r] - sigma);
-          const float2 F2 = make_float2(f, f);
-#pragma unroll
-          for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[r][q], F2, cacc[q]);
-        }
+        for (int q = 0; q < kPairs; ++q) cacc[q] = __ffma2_rn(p[q], F2, cacc[q]);
       }
     }
-    __syncwarp();
-    if (lane == 0) X.uses[warp] = u0 + uint32_t(cnt);
   }
   if (!COST) {
 #pragma unroll
@@ -671,14 +605,6 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
   const int rank = int(cl.block_rank());
   const int cid = int(blockIdx.x) / cs;
   BcWs* W = wss + cid;
-  {  // the warps' ring barriers (live for the whole launch)
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(bc_smem_raw + lay.off_bar());
-    uint32_t* uses = reinterpret_cast<uint32_t*>(bc_smem_raw + lay.off_bar() + size_t(kBcWarps) * lay.nst * 8);
-    if (threadIdx.x < kBcWarps * lay.nst) mbar_init(bars + threadIdx.x, 1);
-    if (threadIdx.x < kBcWarps) uses[threadIdx.x] = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-  }
   for (;;) {
     if (rank == 0 && threadIdx.x == 0) W->cur = atomicAdd(queue, 1);
     bc_sync();
@@ -694,10 +620,6 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.colacc = reinterpret_cast<float*>(bc_smem_raw + lay.off_u());
     X.wk = reinterpret_cast<float2*>(bc_smem_raw + lay.off_u());
     X.s_cap = lay.s_cap;
-    X.nst = lay.nst;
-    X.ring = reinterpret_cast<float4*>(bc_smem_raw + lay.off_ring());
-    X.bars = reinterpret_cast<unsigned long long*>(bc_smem_raw + lay.off_bar());
-    X.uses = reinterpret_cast<uint32_t*>(bc_smem_raw + lay.off_bar() + size_t(kBcWarps) * lay.nst * 8);
     X.n = X.P->ctl0.n;
     X.rank = rank;
     X.cs = cs;

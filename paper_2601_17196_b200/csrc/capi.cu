@@ -1201,20 +1201,16 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   // HBM, so more, smaller clusters win: measured C5, kernel 0.90 / 1.20 /
   // 1.96 s with 4 / 8 / 16 CTAs per cluster)
   const int64_t scap = ceil_div(nmax, int64_t(kBcStrip));
-  // (stages of each warp's bulk-copy ring: $POTGPU_BC_STAGES, default 4,
-  // fewer when shared memory is short)
-  const int want_nst = std::max(1, std::min(8, env_int("POTGPU_BC_STAGES", 4)));
+  // (measured alternatives: a per-warp cp.async.bulk ring of
+  // 4 row segments streamed faster per SM with few SMs busy but was slower
+  // at full load, 1.06 vs 0.84 s; two rows per warp step did not help)
   constexpr size_t kSmemMax = size_t(227) * 1024;
-  auto layout_of = [&](int c) {
-    BcLayout l{int(ceil_div(nmax, int64_t(c))), int(scap), want_nst};
-    while (l.nst > 1 && l.bytes() > kSmemMax) --l.nst;
-    return l;
-  };
+  auto layout_of = [&](int c) { return BcLayout{int(ceil_div(nmax, int64_t(c))), int(scap)}; };
   int cs = env_int("POTGPU_BC_CS", 0);
   if (cs <= 0) {
     cs = 16;
-    for (int c : {1, 2, 4, 8, 16})
-      if (layout_of(c).bytes() <= kSmemMax && layout_of(c).nst >= std::min(want_nst, 3)) { cs = c; break; }
+    for (int c : {2, 4, 8, 16})
+      if (layout_of(c).bytes() <= size_t(200) * 1024) { cs = c; break; }
   }
   cs = std::max(1, std::min(16, cs));
   const BcLayout lay = layout_of(cs);
@@ -1290,9 +1286,9 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
                  tot / double(count) * 1e-6, tot > 0 ? 100.0 * sw / tot : 0.0);
   }
   if (std::getenv("POTGPU_TRACE_SETUP"))
-    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %d ring stages, %zu B smem)\n",
+    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %zu B smem)\n",
                  (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs,
-                 lay.nst, smem);
+                 smem);
   const double wall = secs(t_start);
   for (int64_t k = 0; k < count; ++k) {
     BcHostProblem& h = *hp[size_t(k)];
