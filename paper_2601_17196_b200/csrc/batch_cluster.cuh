@@ -71,10 +71,11 @@ struct BcResult {
 
 // Global workspace of one cluster (reused by every problem it takes).
 struct BcWs {
-  double* slots;     // kSlots x stride
+  double* slots;     // kBcSlots x stride
   double* sums;      // kRoles x 2 x n (rows | cols per role)
   double* vec;       // 4 x n scratch (rounding: rho, kappa, fb, rowX3)
   float2* colpart;   // [cluster rank][n]
+  float2* colpart2;  // [cluster rank][n]: the fused sweep's second point
   double* xch;       // [2][cluster rank][kBcX]
   int64_t stride;    // slot stride
   int cur;           // problem being solved (set by rank 0)
@@ -92,25 +93,36 @@ struct BcShared {
   float wmax[kBcWarps];
   double red[kBcX][kBcWarps];
   double tot[kBcX];
+  double stash[kNumAcc];  // z_bar's functional totals from the fused sweep (K1'')
+  int stash_valid;
   int flag;
 };
 
+// The fused two-point sweep (K1'') also uses A2[rows] (the second point's
+// row offsets), the union region for the second point's row partials, and
+// Bs[2][s_cap * 512] (both points' column constants).
 struct BcLayout {
   int rows_cap, s_cap;
   __host__ __device__ size_t off_A() const { return (sizeof(BcShared) + 15) & ~size_t(15); }
-  __host__ __device__ size_t off_rowpart() const { return (off_A() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
+  __host__ __device__ size_t off_A2() const { return (off_A() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
+  __host__ __device__ size_t off_rowpart() const { return (off_A2() + size_t(rows_cap) * 4 + 15) & ~size_t(15); }
   __host__ __device__ size_t off_u() const { return off_rowpart() + size_t(rows_cap) * s_cap * 8; }
-  __host__ __device__ size_t bytes() const {
+  __host__ __device__ size_t off_B() const {
     const size_t u = size_t(rows_cap) * s_cap * 8, c = size_t(kBcWarps) * kBcStrip * 4;
-    return off_u() + (u > c ? u : c);
+    return (off_u() + (u > c ? u : c) + 15) & ~size_t(15);
   }
+  __host__ __device__ size_t bytes() const { return off_B() + size_t(2) * s_cap * kBcStrip * 4; }
 };
+constexpr int kBcSlots = kSlots + 1;  // + the provisional next z_bar of the fused sweep
+constexpr int S_ZB2 = kSlots;
 
 struct BcCtx {
   const BcProblem* P;
   BcWs* W;
   BcShared* sm;
   float* A;         // [rows_cap]
+  float* A2;        // [rows_cap]: second point of the fused sweep
+  float* Bs;        // [2][s_cap * kBcStrip]: column constants of the fused sweep
   float2* rowpart;  // [rows_cap][s_cap]
   float* colacc;    // [kBcWarps][kBcStrip] (sweep) ...
   float2* wk;       // ... or [rows_cap][s_cap] (cost pass)
@@ -121,6 +133,7 @@ struct BcCtx {
   int64_t lo, hi;  // the CTA's index slice
   int xphase;      // exchange buffer parity (uniform over the cluster)
   uint64_t sweep_ns;  // time spent in sweeps (thread 0)
+  bool fuse;          // K1'' fused z_check' + next z_bar sweep
   __device__ double* slot(int k) const { return W->slots + k * W->stride; }
   __device__ double* rows(int role) const { return W->sums + int64_t(2 * role) * n; }
   __device__ double* cols(int role) const { return W->sums + int64_t(2 * role + 1) * n; }
@@ -366,8 +379,7 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
 }
 
 // Column sums of the CTA's slice over the cluster's partials (after a barrier).
-__device__ __forceinline__ double bc_col_sum(const BcCtx& X, int64_t j) {
-  const float2* cp = X.W->colpart;
+__device__ __forceinline__ double bc_col_sum(const BcCtx& X, int64_t j, const float2* cp) {
   float M = -INFINITY;
   for (int r = 0; r < X.cs; ++r) {
     const float2 x = __ldcg(cp + int64_t(r) * X.n + j);
@@ -398,7 +410,7 @@ __device__ __noinline__ void bc_eval_swept(BcCtx& X, int slot, int role) {
   double* rb = X.rows(role);
   double* cb = X.cols(role);
   for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
-    const double c = bc_col_sum(X, i);
+    const double c = bc_col_sum(X, i, X.W->colpart);
     cb[i] = c;
     add_index_terms(acc, __ldcg(rb + i), c, __ldcg(z + i), __ldcg(z + X.n + i), P_rt[i], P_ct[i]);
   }
@@ -413,6 +425,205 @@ __device__ __noinline__ void bc_eval_swept(BcCtx& X, int slot, int role) {
     apply_role(X.c, role, tot, __ldcg(z + 2 * X.n), true);
   }
   __syncthreads();
+}
+
+// K1'': ONE pass over the CTA's rows of C for two points (z_check' and the
+// provisional next z_bar): each loaded entry is exponentiated
+// for both, with the numerics of bc_sweep per point. Row sums -> rowsA /
+// rowsB, column partials -> colpart / colpart2, max exponents -> maxe[2].
+__device__ __noinline__ void bc_sweep2(BcCtx& X, const double* zA, const double* zB, double* rowsA, double* rowsB,
+                                       double (&maxe)[2]) {
+  const BcProblem& P = *X.P;
+  const int64_t n = X.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double wA = __ldcg(zA + 2 * n), wB = __ldcg(zB + 2 * n);
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    X.A[i - X.lo] = float((__ldcg(zA + i) + wA) * kLog2e);
+    X.A2[i - X.lo] = float((__ldcg(zB + i) + wB) * kLog2e);
+  }
+  const int S = int((n + kBcStrip - 1) / kBcStrip);
+  const int PH = kBcWarps / S;
+  const int strip = warp % S, ph = warp / S;
+  const bool active = ph < PH;
+  const int64_t j0 = int64_t(strip) * kBcStrip;
+  float* BsA = X.Bs;
+  float* BsB = X.Bs + int64_t(X.s_cap) * kBcStrip;
+  for (int64_t j = threadIdx.x; j < int64_t(S) * kBcStrip; j += kBcThreads) {
+    BsA[j] = j < n ? float(__ldcg(zA + n + j) * kLog2e) : -INFINITY;
+    BsB[j] = j < n ? float(__ldcg(zB + n + j) * kLog2e) : -INFINITY;
+  }
+  __syncthreads();
+  float2 caA[kPairs], caB[kPairs];
+#pragma unroll
+  for (int q = 0; q < kPairs; ++q) caA[q] = caB[q] = make_float2(0.f, 0.f);
+  float sigA = -INFINITY, sigB = -INFINITY, mmA = -INFINITY, mmB = -INFINITY;
+  const float2 G = make_float2(-P.g2, -P.g2);
+  float2* rpB = X.wk;  // the union region holds the second point's row partials during the loop
+  if (active) {
+    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
+    const int64_t ld4 = P.ld / 4;
+    int64_t i = X.lo + ph;
+    float4 nxt[4];
+    if (i < X.hi)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
+    for (; i < X.hi; i += PH) {
+      float2 cc[kPairs];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cc[2 * k] = make_float2(nxt[k].x, nxt[k].y);
+        cc[2 * k + 1] = make_float2(nxt[k].z, nxt[k].w);
+      }
+      if (i + PH < X.hi)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
+      const int64_t il = i - X.lo;
+      // each point: exact segment max, MUFU burst, row partial, column update
+      // (unrolled over the two points, so every select below is static)
+#pragma unroll
+      for (int pt = 0; pt < 2; ++pt) {
+        float2 p[kPairs];
+        const float4* b4 = reinterpret_cast<const float4*>((pt ? BsB : BsA) + j0) + lane;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 b = b4[32 * q4];
+          p[2 * q4] = __ffma2_rn(G, cc[2 * q4], make_float2(b.x, b.y));
+          p[2 * q4 + 1] = __ffma2_rn(G, cc[2 * q4 + 1], make_float2(b.z, b.w));
+        }
+        const float m = warp_maxf(tree_max2<kPairs>(p));
+        const float ms = (m == -INFINITY) ? 0.f : m;
+        const float2 M2 = make_float2(-ms, -ms);
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) {
+          const float2 d = __fadd2_rn(p[q], M2);
+          p[q] = make_float2(ex2f(d.x), ex2f(d.y));
+        }
+        float rs = tree_sum2<kPairs>(p);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (lane == 0) (pt ? rpB : X.rowpart)[il * X.s_cap + strip] = make_float2(rs, ms);
+        const float mA = (m == -INFINITY) ? -INFINITY : m + (pt ? X.A2 : X.A)[il];
+        float sg = pt ? sigB : sigA;
+        if (mA > sg) {  // warp-uniform
+          const float sc = ex2f(sg - mA);
+#pragma unroll
+          for (int q = 0; q < kPairs; ++q) {
+            if (pt) caB[q] = __fmul2_rn(caB[q], make_float2(sc, sc));
+            else caA[q] = __fmul2_rn(caA[q], make_float2(sc, sc));
+          }
+          sg = mA;
+        }
+        if (pt) { sigB = sg; mmB = fmaxf(mmB, mA); } else { sigA = sg; mmA = fmaxf(mmA, mA); }
+        const float f = (mA == -INFINITY) ? 0.f : ex2f(mA - sg);
+        const float2 F2 = make_float2(f, f);
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) {
+          if (pt) caB[q] = __ffma2_rn(p[q], F2, caB[q]);
+          else caA[q] = __ffma2_rn(p[q], F2, caA[q]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // row sums of both points (fp64 row offsets)
+  for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+    const int64_t il = i - X.lo;
+    const double a2A = (__ldcg(zA + i) + wA) * kLog2e, a2B = (__ldcg(zB + i) + wB) * kLog2e;
+    double ra = 0.0, rb = 0.0;
+    for (int s2 = 0; s2 < S; ++s2) {
+      const float2 pa = X.rowpart[il * X.s_cap + s2], pb = rpB[il * X.s_cap + s2];
+      if (pa.x != 0.f) ra += double(pa.x) * exp2(double(pa.y) + a2A);
+      if (pb.x != 0.f) rb += double(pb.x) * exp2(double(pb.y) + a2B);
+    }
+    rowsA[i] = ra;
+    rowsB[i] = rb;
+  }
+  __syncthreads();  // rpB is dead: the region takes the column accumulators
+  // column partials, one point at a time through the per-warp accumulators
+  // (explicit per point: selecting between two register arrays by pointer
+  // would put them in local memory)
+#pragma unroll
+  for (int pt = 0; pt < 2; ++pt) {
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const int cidx = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
+      const float2 v = pt == 0 ? caA[q] : caB[q];
+      X.colacc[warp * kBcStrip + cidx] = v.x;
+      X.colacc[warp * kBcStrip + cidx + 1] = v.y;
+    }
+    if (lane == 0) {
+      X.sm->colsig[warp] = pt == 0 ? sigA : sigB;
+      X.sm->wmax[warp] = pt == 0 ? mmA : mmB;
+    }
+    __syncthreads();
+    float2* cp = (pt == 0 ? X.W->colpart : X.W->colpart2) + int64_t(X.rank) * n;
+    for (int k = threadIdx.x; k < S * kBcStrip; k += kBcThreads) {
+      const int s2 = k / kBcStrip, cidx = k % kBcStrip;
+      const int64_t j = int64_t(s2) * kBcStrip + cidx;
+      if (j >= n) continue;
+      float SIG = -INFINITY;
+      for (int p2 = 0; p2 < PH; ++p2) SIG = fmaxf(SIG, X.sm->colsig[p2 * S + s2]);
+      float acc = 0.f;
+      if (SIG != -INFINITY)
+        for (int p2 = 0; p2 < PH; ++p2) {
+          const float sg = X.sm->colsig[p2 * S + s2];
+          if (sg != -INFINITY) acc += X.colacc[(p2 * S + s2) * kBcStrip + cidx] * ex2f(sg - SIG);
+        }
+      cp[j] = (SIG == -INFINITY) ? make_float2(0.f, 0.f) : make_float2(acc, SIG);
+    }
+    float mx = -INFINITY;
+    for (int ww = 0; ww < S * PH; ++ww) mx = fmaxf(mx, X.sm->wmax[ww]);
+    maxe[pt] = double(mx) * kLn2;
+    __syncthreads();
+  }
+}
+
+// Fused evaluation of z_check' (R_NEW, decided now) and the provisional next
+// z_bar (S_ZB2: its sums go to R_BAR, its totals are stashed for the next
+// iteration's z_bar decision, which then needs no sweep).
+__device__ __noinline__ void bc_eval2_swept(BcCtx& X) {
+  bc_sync();
+  const double* zA = X.slot(S_ZN);
+  const double* zB = X.slot(S_ZB2);
+  const uint64_t ts = globaltimer_ns();
+  double maxe[2];
+  bc_sweep2(X, zA, zB, X.rows(R_NEW), X.rows(R_BAR), maxe);
+  bc_sync();
+  X.sweep_ns += globaltimer_ns() - ts;
+  const double* rt = X.P->rt;
+  const double* ct = X.P->ct;
+#pragma unroll 1
+  for (int pt = 0; pt < 2; ++pt) {
+    const double* z = pt == 0 ? zA : zB;
+    const int role = pt == 0 ? R_NEW : R_BAR;
+    const float2* cp = pt == 0 ? X.W->colpart : X.W->colpart2;
+    double acc[kBcX];
+#pragma unroll
+    for (int k = 0; k < kBcX; ++k) acc[k] = k < kNumAcc ? acc_init(k) : 0.0;
+    double* rb = X.rows(role);
+    double* cb = X.cols(role);
+    for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
+      const double c = bc_col_sum(X, i, cp);
+      cb[i] = c;
+      add_index_terms(acc, __ldcg(rb + i), c, __ldcg(z + i), __ldcg(z + X.n + i), rt[i], ct[i]);
+    }
+    bc_block_acc(X, acc);
+    if (threadIdx.x == 0) X.sm->red[11][0] = nan_max(X.sm->red[11][0], maxe[pt]);
+    __syncthreads();
+    bc_exchange(X);
+    if (threadIdx.x == 0) {
+      double tot[kNumAcc];
+#pragma unroll
+      for (int k = 0; k < kNumAcc; ++k) tot[k] = X.sm->tot[k];
+      if (pt == 0) {
+        apply_role(X.c, R_NEW, tot, __ldcg(z + 2 * X.n), true);
+      } else {
+        for (int k = 0; k < kNumAcc; ++k) X.sm->stash[k] = tot[k];
+        X.sm->stash_valid = 1;
+      }
+    }
+    __syncthreads();
+  }
 }
 
 __device__ void bc_kill_gates(AspotCtl* c) {  // ctl_finish's non-finite fold (solvers.hpp:83-87)
@@ -527,7 +738,7 @@ __device__ __noinline__ double bc_round(BcCtx& X, BcResult* res) {
   (void)bc_sweep<false>(X, zc, lrho, nullptr, nullptr, X.rows(R_EVAL), nullptr, nullptr);
   bc_sync();
   for (int64_t j = X.lo + threadIdx.x; j < X.hi; j += kBcThreads) {
-    const double col3 = alpha * bc_col_sum(X, j);
+    const double col3 = alpha * bc_col_sum(X, j, X.W->colpart);
     const double kp = col3 > 0 ? fmin(1.0, P.c[j] / col3) : 1.0;
     const double c3 = kp * col3;
     lkap[j] = log(kp);
@@ -597,7 +808,7 @@ __device__ void bc_record_cost(BcCtx& X, int64_t len_before, TraceDev* trace) {
 
 // The persistent batch kernel: grid = cs x clusters, cluster = (cs, 1, 1).
 __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* probs, int count, BcWs* wss,
-                                                              BcResult* results, int* queue, BcLayout lay) {
+                                                              BcResult* results, int* queue, BcLayout lay, int fuse) {
   extern __shared__ __align__(16) unsigned char bc_smem_raw[];
   BcShared* sm = reinterpret_cast<BcShared*>(bc_smem_raw);
   cgx::cluster_group cl = cgx::this_cluster();
@@ -615,6 +826,9 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.W = W;
     X.sm = sm;
     X.c = reinterpret_cast<AspotCtl*>(sm->ctl);
+    X.A2 = reinterpret_cast<float*>(bc_smem_raw + lay.off_A2());
+    X.Bs = reinterpret_cast<float*>(bc_smem_raw + lay.off_B());
+    X.fuse = fuse != 0;
     X.A = reinterpret_cast<float*>(bc_smem_raw + lay.off_A());
     X.rowpart = reinterpret_cast<float2*>(bc_smem_raw + lay.off_rowpart());
     X.colacc = reinterpret_cast<float*>(bc_smem_raw + lay.off_u());
@@ -632,7 +846,8 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
       const uint32_t* src = reinterpret_cast<const uint32_t*>(&X.P->ctl0);
       for (int k = threadIdx.x; k < kCtlWords; k += kBcThreads) sm->ctl[k] = src[k];
       const int64_t n = X.n;
-      for (int s2 = 0; s2 < kSlots; ++s2) {
+      if (threadIdx.x == 0) sm->stash_valid = 0;
+      for (int s2 = 0; s2 < kBcSlots; ++s2) {
         double* zz = X.slot(s2);
         for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads) {
           zz[i] = 0.0;
@@ -661,7 +876,17 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     const int64_t n = X.n;
     while (c->g_active) {  // identical on every CTA of the cluster
       // z_bar: range check and gradient of a new iteration (solvers.hpp:336-337)
-      if (c->g_new) bc_eval_swept(X, S_ZB, R_BAR);
+      if (c->g_new) {
+        if (X.sm->stash_valid) {  // z_bar was swept with the last z_check' (K1'')
+          if (threadIdx.x == 0) {
+            apply_role(c, R_BAR, X.sm->stash, __ldcg(X.slot(S_ZB) + 2 * n), false);
+            X.sm->stash_valid = 0;
+          }
+          __syncthreads();
+        } else {
+          bc_eval_swept(X, S_ZB, R_BAR);
+        }
+      }
       if (c->g_alive) {  // z_next = z_bar - step grad; z_grave = z_bar + theta (z_next - z) (:338-339)
         const bool fresh = c->g_new;
         const double step = c->step, th = c->theta;
@@ -699,7 +924,29 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
       if (c->g_alive) bc_gk_update(X, 0);                 // z_hat (solvers.hpp:340)
       if (c->g_hat_sweep) bc_eval_swept(X, S_ZH, R_HAT);  // phi(z_hat), z_best (:341-343)
       if (c->g_alive) bc_gk_update(X, 1);                 // z_check' = GK(z_best) (:344)
-      if (c->g_new_sweep) bc_eval_swept(X, S_ZN, R_NEW);  // phi, grad at z_check' (:345)
+      if (c->g_new_sweep) {  // phi, grad at z_check' (:345), fused with the next z_bar
+        if (X.fuse) {
+          const bool keep = c->keep_check;
+          const double th = theta_next_d(c->theta), om = 1.0 - th;
+          const double* zc = X.slot(S_ZC);
+          const double* zh = X.slot(S_ZH);
+          const double* zn = X.slot(S_ZN);
+          double* zb2 = X.slot(S_ZB2);
+          for (int64_t i = X.lo + threadIdx.x; i < X.hi; i += kBcThreads)
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+              const int64_t k = side * n + i;
+              zb2[k] = om * __ldcg(zn + k) + th * (keep ? __ldcg(zc + k) : __ldcg(zh + k));
+            }
+          if (rank == 0 && threadIdx.x == 0) {
+            const int64_t k = 2 * n;
+            zb2[k] = om * __ldcg(zn + k) + th * (keep ? __ldcg(zc + k) : __ldcg(zh + k));
+          }
+          bc_eval2_swept(X);
+        } else {
+          bc_eval_swept(X, S_ZN, R_NEW);
+        }
+      }
       if (c->attempt_ok) {  // commit (k_commit)
         const bool keep = c->keep_check;
         const double th = theta_next_d(c->theta), om = 1.0 - th;
@@ -735,6 +982,7 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
         }
       }
       __syncthreads();
+      if (threadIdx.x == 0 && !c->attempt_ok) X.sm->stash_valid = 0;  // a retry keeps z_bar (no stash)
       len0 = c->trace_len;
       __syncthreads();
       if (threadIdx.x == 0) commit_state(c, trace, lg);

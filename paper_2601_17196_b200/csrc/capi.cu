@@ -1239,17 +1239,27 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   lc.gridDim = dim3(unsigned(cs * nc));
   // per-cluster workspaces
   const int64_t stride = round_up(2 * nmax + 1, 32);
-  const int64_t per = kSlots * stride + 2 * kRoles * nmax + 6 * nmax + 2 * int64_t(cs) * kBcX;
+  const int64_t per = kBcSlots * stride + 2 * kRoles * nmax + 6 * nmax + 2 * int64_t(cs) * kBcX;
   DevBuf<double> wsd;
   wsd.alloc(size_t(per * nc));
   DevBuf<float2> colpart;
-  colpart.alloc(size_t(int64_t(cs) * nmax * nc));
+  colpart.alloc(size_t(2 * int64_t(cs) * nmax * nc));
   std::vector<BcWs> hw(static_cast<size_t>(nc));
   for (int k = 0; k < nc; ++k) {
     double* b = wsd.p + int64_t(k) * per;
-    hw[size_t(k)] = BcWs{b, b + kSlots * stride, b + kSlots * stride + 2 * kRoles * nmax,
-                         colpart.p + int64_t(k) * cs * nmax, b + kSlots * stride + 2 * kRoles * nmax + 6 * nmax, stride, 0, 0};
+    BcWs& h = hw[size_t(k)];
+    h.slots = b;
+    h.sums = b + kBcSlots * stride;
+    h.vec = h.sums + 2 * kRoles * nmax;
+    h.xch = h.vec + 6 * nmax;
+    h.colpart = colpart.p + int64_t(2 * k) * cs * nmax;
+    h.colpart2 = h.colpart + int64_t(cs) * nmax;
+    h.stride = stride;
+    h.cur = 0;
+    h.pad = 0;
   }
+  // K1'': z_check' and the next z_bar in one pass over C ($POTGPU_BC_FUSE=0: separate)
+  const int fuse = env_int("POTGPU_BC_FUSE", 1) != 0 ? 1 : 0;
   DevBuf<BcWs> dws;
   dws.alloc(size_t(nc));
   DevBuf<BcProblem> dprob;
@@ -1269,7 +1279,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaEventCreate(&e1));
   PG_CK(cudaEventRecord(e0, st));
   PG_CK(cudaLaunchKernelEx(&lc, k_batch_aspot, static_cast<const BcProblem*>(dprob.p), int(count), dws.p, dres.p,
-                           queue.p, lay));
+                           queue.p, lay, fuse));
   PG_CK(cudaGetLastError());
   PG_CK(cudaEventRecord(e1, st));
   std::vector<BcResult> res(static_cast<size_t>(count));
