@@ -73,7 +73,7 @@ struct BcResult {
 struct BcWs {
   double* slots;     // kBcSlots x stride
   double* sums;      // kRoles x 2 x n (rows | cols per role)
-  double* vec;       // 4 x n scratch (rounding: rho, kappa, fb, rowX3)
+  double* vec;       // 8 x n scratch (rounding)
   float2* colpart;   // [cluster rank][n]
   float2* colpart2;  // [cluster rank][n]: the fused sweep's second point
   double* xch;       // [2][cluster rank][kBcX]
@@ -748,8 +748,8 @@ __device__ __noinline__ double bc_round(BcCtx& X, BcResult* res) {
   bc_sync();
   // final row sums of B diag(kappa) and the cost's per-row terms
   double* rr = X.rows(R_EVAL);
-  double* Wv = X.rows(R_BAR);
-  double* Kv = X.cols(R_BAR);
+  double* Wv = X.W->vec + 6 * n;  // (not R_BAR's sums: a record rounding runs between the fused
+  double* Kv = X.W->vec + 7 * n;  //  sweep that wrote the next z_bar's sums and their use)
   (void)bc_sweep<true>(X, zc, nullptr, lkap, fbv, rr, Wv, Kv);
 #pragma unroll
   for (int k = 0; k < kBcX; ++k) acc[k] = bc_init(true, k);
@@ -877,7 +877,9 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     while (c->g_active) {  // identical on every CTA of the cluster
       // z_bar: range check and gradient of a new iteration (solvers.hpp:336-337)
       if (c->g_new) {
-        if (X.sm->stash_valid) {  // z_bar was swept with the last z_check' (K1'')
+        const int stashed = X.sm->stash_valid;
+        __syncthreads();  // every thread has read the flag before thread 0 clears it
+        if (stashed) {  // z_bar was swept with the last z_check' (K1'')
           if (threadIdx.x == 0) {
             apply_role(c, R_BAR, X.sm->stash, __ldcg(X.slot(S_ZB) + 2 * n), false);
             X.sm->stash_valid = 0;

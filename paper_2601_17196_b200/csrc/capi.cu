@@ -1239,7 +1239,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   lc.gridDim = dim3(unsigned(cs * nc));
   // per-cluster workspaces
   const int64_t stride = round_up(2 * nmax + 1, 32);
-  const int64_t per = kBcSlots * stride + 2 * kRoles * nmax + 6 * nmax + 2 * int64_t(cs) * kBcX;
+  const int64_t per = kBcSlots * stride + 2 * kRoles * nmax + 8 * nmax + 2 * int64_t(cs) * kBcX;
   DevBuf<double> wsd;
   wsd.alloc(size_t(per * nc));
   DevBuf<float2> colpart;
@@ -1251,7 +1251,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
     h.slots = b;
     h.sums = b + kBcSlots * stride;
     h.vec = h.sums + 2 * kRoles * nmax;
-    h.xch = h.vec + 6 * nmax;
+    h.xch = h.vec + 8 * nmax;
     h.colpart = colpart.p + int64_t(2 * k) * cs * nmax;
     h.colpart2 = h.colpart + int64_t(cs) * nmax;
     h.stride = stride;
