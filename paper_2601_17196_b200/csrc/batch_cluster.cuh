@@ -111,7 +111,46 @@ struct BcLayout {
     const size_t u = size_t(rows_cap) * s_cap * 8, c = size_t(kBcWarps) * kBcStrip * 4;
     return (off_u() + (u > c ? u : c) + 15) & ~size_t(15);
   }
-  __host__ __device__ size_t bytes() const { return off_B() + size_t(2) * s_cap * kBcStrip * 4; }
+  int nst;  // stages of each warp's row ring (cp.async)
+  __host__ __device__ size_t off_ring() const { return (off_B() + size_t(2) * s_cap * kBcStrip * 4 + 127) & ~size_t(127); }
+  __host__ __device__ size_t bytes() const { return off_ring() + size_t(kBcWarps) * nst * kBcStrip * 4; }
+};
+
+// Per-lane cp.async (LDGSTS) ring of row segments: each lane streams ITS 4 x
+// 16 B of every row segment into its own slots of the warp's ring, so the
+// lane's wait_group is the only synchronisation; nst - 1 rows are in flight
+// per warp while one is exponentiated (a register double buffer holds one;
+// ncu: the sweep was long_scoreboard-bound on C at 2.4 TB/s).
+struct BcRowStream {
+  float4* ring;       // warp ring + lane: slot (k % nst) at ring + (k % nst) * 128
+  const float4* g;    // P.C + j0 (as float4) + lane
+  int64_t ld4, i0, step, cnt;
+  int nst;
+  __device__ __forceinline__ void issue(int64_t k) const {
+    if (k < cnt) {
+      const float4* src = g + (i0 + k * step) * ld4;
+      float4* dst = ring + (k % nst) * (kBcStrip / 4);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 32 * q4)), "l"(src + 32 * q4)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __device__ __forceinline__ void wait() const {  // all but the nst - 1 newest groups done
+    switch (nst) {
+      case 2: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+      case 3: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+      case 4: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+      case 5: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+      default: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    }
+  }
+  __device__ __forceinline__ void get(int64_t k, float4 (&v)[4]) const {
+    const float4* src = ring + (k % nst) * (kBcStrip / 4);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) v[q4] = src[32 * q4];
+  }
 };
 constexpr int kBcSlots = kSlots + 1;  // + the provisional next z_bar of the fused sweep
 constexpr int S_ZB2 = kSlots;
@@ -123,6 +162,8 @@ struct BcCtx {
   float* A;         // [rows_cap]
   float* A2;        // [rows_cap]: second point of the fused sweep
   float* Bs;        // [2][s_cap * kBcStrip]: column constants of the fused sweep
+  float4* ring;     // [kBcWarps][nst][kBcStrip / 4]
+  int nst;
   float2* rowpart;  // [rows_cap][s_cap]
   float* colacc;    // [kBcWarps][kBcStrip] (sweep) ...
   float2* wk;       // ... or [rows_cap][s_cap] (cost pass)
@@ -244,20 +285,16 @@ __device__ __noinline__ double bc_sweep(BcCtx& X, const double* z, const double*
   float sigma = -INFINITY, mmax = -INFINITY;
   const float2 G = make_float2(-P.g2, -P.g2);
   if (active) {
-    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
-    const int64_t ld4 = P.ld / 4;
-    int64_t i = X.lo + ph;
-    float4 nxt[4];
-    if (i < X.hi)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
-    for (; i < X.hi; i += PH) {
+    const int64_t cnt = X.hi > X.lo + ph ? (X.hi - X.lo - ph + PH - 1) / PH : 0;
+    const BcRowStream rsm{X.ring + warp * X.nst * (kBcStrip / 4) + lane,
+                          reinterpret_cast<const float4*>(P.C + j0) + lane, P.ld / 4, X.lo + ph, PH, cnt, X.nst};
+    for (int k = 0; k < X.nst - 1; ++k) rsm.issue(k);
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+      const int64_t i = X.lo + ph + kk * PH;
+      rsm.issue(kk + X.nst - 1);  // into the slot of row kk - 1, consumed last step
+      rsm.wait();
       float4 cur[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
-      if (i + PH < X.hi)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
+      rsm.get(kk, cur);
       float2 cc[kPairs], t[kPairs];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -460,23 +497,22 @@ __device__ __noinline__ void bc_sweep2(BcCtx& X, const double* zA, const double*
   const float2 G = make_float2(-P.g2, -P.g2);
   float2* rpB = X.wk;  // the union region holds the second point's row partials during the loop
   if (active) {
-    const float4* base = reinterpret_cast<const float4*>(P.C + j0) + lane;
-    const int64_t ld4 = P.ld / 4;
-    int64_t i = X.lo + ph;
-    float4 nxt[4];
-    if (i < X.hi)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + i * ld4 + 32 * k);
-    for (; i < X.hi; i += PH) {
+    const int64_t cnt = X.hi > X.lo + ph ? (X.hi - X.lo - ph + PH - 1) / PH : 0;
+    const BcRowStream rsm{X.ring + warp * X.nst * (kBcStrip / 4) + lane,
+                          reinterpret_cast<const float4*>(P.C + j0) + lane, P.ld / 4, X.lo + ph, PH, cnt, X.nst};
+    for (int k = 0; k < X.nst - 1; ++k) rsm.issue(k);
+    for (int64_t kk = 0; kk < cnt; ++kk) {
+      const int64_t i = X.lo + ph + kk * PH;
+      rsm.issue(kk + X.nst - 1);
+      rsm.wait();
+      float4 cur[4];
+      rsm.get(kk, cur);
       float2 cc[kPairs];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        cc[2 * k] = make_float2(nxt[k].x, nxt[k].y);
-        cc[2 * k + 1] = make_float2(nxt[k].z, nxt[k].w);
+        cc[2 * k] = make_float2(cur[k].x, cur[k].y);
+        cc[2 * k + 1] = make_float2(cur[k].z, cur[k].w);
       }
-      if (i + PH < X.hi)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) nxt[k] = __ldcg(base + (i + PH) * ld4 + 32 * k);
       const int64_t il = i - X.lo;
       // each point: exact segment max, MUFU burst, row partial, column update
       // (unrolled over the two points, so every select below is static)
@@ -829,6 +865,8 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
     X.A2 = reinterpret_cast<float*>(bc_smem_raw + lay.off_A2());
     X.Bs = reinterpret_cast<float*>(bc_smem_raw + lay.off_B());
     X.fuse = fuse != 0;
+    X.ring = reinterpret_cast<float4*>(bc_smem_raw + lay.off_ring());
+    X.nst = lay.nst;
     X.A = reinterpret_cast<float*>(bc_smem_raw + lay.off_A());
     X.rowpart = reinterpret_cast<float2*>(bc_smem_raw + lay.off_rowpart());
     X.colacc = reinterpret_cast<float*>(bc_smem_raw + lay.off_u());

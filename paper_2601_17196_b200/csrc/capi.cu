@@ -1205,12 +1205,17 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   // 4 row segments streamed faster per SM with few SMs busy but was slower
   // at full load, 1.06 vs 0.84 s; two rows per warp step did not help)
   constexpr size_t kSmemMax = size_t(227) * 1024;
-  auto layout_of = [&](int c) { return BcLayout{int(ceil_div(nmax, int64_t(c))), int(scap)}; };
+  const int want_nst = std::max(2, std::min(5, env_int("POTGPU_BC_STAGES", 4)));
+  auto layout_of = [&](int c) {  // the deepest ring (<= want_nst, >= 2) that fits
+    BcLayout l{int(ceil_div(nmax, int64_t(c))), int(scap), want_nst};
+    while (l.nst > 2 && l.bytes() > kSmemMax) --l.nst;
+    return l;
+  };
   int cs = env_int("POTGPU_BC_CS", 0);
   if (cs <= 0) {
     cs = 16;
     for (int c : {2, 4, 8, 16})
-      if (layout_of(c).bytes() <= size_t(200) * 1024) { cs = c; break; }
+      if (layout_of(c).bytes() <= kSmemMax && layout_of(c).nst >= std::min(want_nst, 3)) { cs = c; break; }
   }
   cs = std::max(1, std::min(16, cs));
   const BcLayout lay = layout_of(cs);
@@ -1296,9 +1301,9 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
                  tot / double(count) * 1e-6, tot > 0 ? 100.0 * sw / tot : 0.0);
   }
   if (std::getenv("POTGPU_TRACE_SETUP"))
-    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %zu B smem)\n",
+    std::fprintf(stderr, "[potgpu] batch cluster: %lld problems, upload+setup %.3f ms, kernel %.3f ms (%d clusters of %d, %d-stage rings, %zu B smem)\n",
                  (long long)count, std::chrono::duration<double, std::milli>(t_launch - t_start).count(), double(kms), nc, cs,
-                 smem);
+                 lay.nst, smem);
   const double wall = secs(t_start);
   for (int64_t k = 0; k < count; ++k) {
     BcHostProblem& h = *hp[size_t(k)];
