@@ -1205,7 +1205,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   // 4 row segments streamed faster per SM with few SMs busy but was slower
   // at full load, 1.06 vs 0.84 s; two rows per warp step did not help)
   constexpr size_t kSmemMax = size_t(227) * 1024;
-  const int want_nst = std::max(2, std::min(5, env_int("POTGPU_BC_STAGES", 4)));
+  const int want_nst = std::max(2, std::min(5, env_int("POTGPU_BC_STAGES", 3)));  // measured: 2-3 stages 0.90 s, 4 (225 KB smem) 1.26 s
   auto layout_of = [&](int c) {  // the deepest ring (<= want_nst, >= 2) that fits
     BcLayout l{int(ceil_div(nmax, int64_t(c))), int(scap), want_nst};
     while (l.nst > 2 && l.bytes() > kSmemMax) --l.nst;
