@@ -27,3 +27,16 @@ def ctx():
         pytest.skip("no CUDA device")
     from paper_2601_17196_b200 import pot
     return pot.Context(0)
+
+
+@pytest.fixture(scope="session", autouse=True)
+def oracle_all_threads():
+    """The CPU oracle (test infrastructure) on every host thread: its results
+    do not depend on the thread count (fixed per-row / per-column sums,
+    oracle/pot_oracle.hpp), only the wall time of the parity tests does."""
+    try:
+        from oracle import binding
+        binding.lib().oracle_set_threads(os.cpu_count() or 1)
+    except Exception:  # oracle not built: the tests that need it fail on their own
+        pass
+    yield

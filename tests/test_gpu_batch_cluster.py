@@ -54,7 +54,6 @@ def check_feasible(g, s):
 def oracle_threads():
     binding.lib().oracle_set_threads(os.cpu_count() or 1)
     yield
-    binding.lib().oracle_set_threads(1)
 
 
 @pytest.mark.parametrize("n", [2, 37, 300, 1000, 3001])

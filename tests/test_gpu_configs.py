@@ -25,7 +25,6 @@ TOL_F32_OBJ, TOL_F32_VIOL = 1e-4, 1e-5
 def oracle_threads():
     binding.lib().oracle_set_threads(os.cpu_count() or 1)
     yield
-    binding.lib().oracle_set_threads(1)
 
 
 def oracle_cost(inst):
@@ -105,13 +104,20 @@ def test_c2_tuned_sinkhorn_p1_capped(ctx):
 
 
 @pytest.mark.slow
-def test_c2_feasible_sinkhorn_full(ctx):
-    """n = 4096 fp64, eps = 1e-3, feasible Sinkhorn (the ASPOT gamma) to convergence."""
+def test_c2_feasible_sinkhorn_capped(ctx):
+    """n = 4096 fp64, eps = 1e-3, feasible Sinkhorn (the ASPOT gamma = 3.0e-5:
+    thousands of iterations, beyond the oracle's budget in a test): both
+    capped at 200 iterations, same status, trace errors to 1e-9 and the
+    rounded plan of the capped iterate to the fp64 bars."""
     inst = pot.config_instance(2)
-    cfg = pot.SolverConfig(epsilon=1e-3, log_every=10 ** 9, materialize_plan=False, max_iterations=20000)
+    cfg = pot.SolverConfig(epsilon=1e-3, log_every=25, max_iterations=200, record_rounded_cost=False,
+                           materialize_plan=False)
     g = pot.feasible_sinkhorn_solve(inst, cfg, ctx=ctx)
-    o = binding.solve(1, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-3, max_iterations=20000, want_plan=False)
+    o = binding.solve(1, inst.r, inst.c, inst.s, C=inst.C, epsilon=1e-3, max_iterations=200, log_every=25,
+                      want_plan=False)
     assert int(g.status) == o.status and g.iterations == o.iterations
+    assert [r.t for r in g.trace] == [int(x) for x in o.trace[:, 0]]
+    np.testing.assert_allclose([r.error for r in g.trace], o.trace[:, 1], rtol=1e-9)
     assert abs(g.cost - o.cost) <= TOL_F64_OBJ * abs(o.cost)
     check_properties(g, inst.s, TOL_F64_VIOL)
 

@@ -31,7 +31,6 @@ TOL_F32_OBJ, TOL_F32_VIOL = 1e-4, 1e-5
 def oracle_threads():
     binding.lib().oracle_set_threads(os.cpu_count() or 1)
     yield
-    binding.lib().oracle_set_threads(1)
 
 
 @pytest.fixture(scope="module")
