@@ -755,8 +755,12 @@ __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
     e.theta = ctl->theta;
   }
   ctl->log_len += 1;
-  if (ctl->t % ctl->log_every == 0 || !(ctl->error > ctl->eps_tilde))  // solvers.hpp:309
+  if (ctl->t % ctl->log_every == 0 || !(ctl->error > ctl->eps_tilde)) {  // solvers.hpp:309
     append_trace(ctl, trace, ctl->t, ctl->error, ctl->phi_check);
+    // the record's rounded cost (solvers.hpp:314-315): the attempt graph's
+    // device-rounding tail runs when this is set (and clears it)
+    ctl->g_record = ctl->record_rounded_cost && ctl->trace_len <= ctl->trace_cap;
+  }
   loop_head(ctl);
 }
 

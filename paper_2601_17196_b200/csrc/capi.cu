@@ -547,6 +547,7 @@ struct AspotSession : Session {
   cudaGraphExec_t exec_first = nullptr; // resume (k_resume_pinned) + one step attempt: the first launch of a run
   PinnedObj<ResumeArgs> resume_args;
   bool one_sided = false;  // z_check' by sweep_pts1_f32 when its block is u or v (fp32 points)
+  bool round_tail = false; // per-record rounding inside the attempt graph (record_rounded_cost)
   cudaGraphExec_t loop_exec = nullptr;  // the attempt inside a WHILE node: the whole loop in one launch
   int64_t trace_cap = 1, log_cap = 0;
   static constexpr int64_t kKernelsPerAttempt = 12;
@@ -633,6 +634,11 @@ struct AspotSession : Session {
     launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
              ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd, loop, in_loop);
     PG_CK(cudaGetLastError());
+    // record_rounded_cost with records inside the loop: the record's rounding
+    // (round_pot of B(z_check), solvers.hpp:314-315) as a gated device tail
+    // of the attempt, instead of pausing the loop for a host rounding
+    if (round_tail)
+      enqueue_round_device(cx, P, ws, gamma, ZC, ws.row(R_CHECK), &ctl->ro, &ctl->g_record, ctl, ws.trace.p);
   }
 
   void sync_ctl() {
@@ -706,6 +712,9 @@ struct AspotSession : Session {
     h.clamp_guard = P.dtype == POTGPU_F64 ? 1 : 0;
     one_sided = one_sided_supported(cx, P) && ws.pts_cs == 1;
     h.one_sided_ok = one_sided ? 1 : 0;
+    h.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
+    round_tail = cfg.record_rounded_cost && cfg.use_graphs && cfg.log_every < cfg.max_iterations &&
+                 device_round_ok(cx, P, ws) && !std::getenv("POTGPU_NO_ROUND_TAIL");
     PG_CK(cudaMemcpyAsync(ws.ctl.p, &h, sizeof(AspotCtl), cudaMemcpyHostToDevice, cx.stream));
     AspotCtl* ctl = ws.ctl.p;
     k_stamp_t0<<<1, 1, 0, cx.stream>>>(ctl);
@@ -812,10 +821,10 @@ struct AspotSession : Session {
     PG_CK(cudaEventRecord(ev0, cx.stream));
     while (true) {
       int64_t stop = target;
-      if (cfg.record_rounded_cost) stop = std::min(stop, (h.t / cfg.log_every + 1) * cfg.log_every);
+      if (cfg.record_rounded_cost && !round_tail) stop = std::min(stop, (h.t / cfg.log_every + 1) * cfg.log_every);
       run_until(stop);
       if (h.fatal) break;
-      if (cfg.record_rounded_cost && h.paused) fill_last_record_cost(round_now(nullptr).cost);
+      if (cfg.record_rounded_cost && !round_tail && h.paused) fill_last_record_cost(round_now(nullptr).cost);
       if (!h.paused || h.t >= target) break;
     }
     PG_CK(cudaEventSynchronize(ev1));

@@ -254,13 +254,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
   const int64_t j0 = int64_t(blockIdx.x) * kRcStrip;
   const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
   const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
+  // expanded fp64 exponent: t = (v_j log2e - g |y_j|^2) + (2 g y_j) . x_i - g |x_i|^2,
+  // every term exact to ~1e-16 of its magnitude, so t rounds once (to fp32)
+  // near the row max; the fp32 cost weight from the fp32 coordinates in smem
   __shared__ float s_c0[kRcStrip], s_c1[kRcStrip];
+  __shared__ float4 s_y[kRcStrip];
   for (int k = threadIdx.x; k < kRcStrip; k += kThreads) {
     const int64_t j = j0 + k;
     s_c0[k] = (j < n && a.b0) ? float(a.b0[j]) : 0.f;
     s_c1[k] = (j < n && a.b1) ? float(a.b1[j]) : 0.f;
+    s_y[k] = j < n ? Y[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  double Bj[kRcCols], yx[kRcCols], yy[kRcCols], yz[kRcCols];
+  double Bq[kRcCols], gx[kRcCols], gy[kRcCols], gz[kRcCols];
 #pragma unroll
   for (int k = 0; k < kRcCols; ++k) {
     const int64_t j = j0 + lane + 32 * k;
@@ -272,27 +277,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
       vv = vv * kLog2e;
       y = Y[j];
     }
-    Bj[k] = vv;
-    yx[k] = y.x; yy[k] = y.y; yz[k] = y.z;
+    const double yx = y.x, yy = y.y, yz = y.z;
+    Bq[k] = vv - g * fma(yz, yz, fma(yy, yy, yx * yx));
+    gx[k] = 2.0 * g * yx; gy[k] = 2.0 * g * yy; gz[k] = 2.0 * g * yz;
   }
   __syncthreads();
-  float f0[kRcCols], f1[kRcCols];
-#pragma unroll
-  for (int k = 0; k < kRcCols; ++k) {
-    f0[k] = s_c0[lane + 32 * k];
-    f1[k] = s_c1[lane + 32 * k];
-  }
   const int64_t ldp = gridDim.x;
   for (int64_t i = r0 + warp; i < r1; i += kWarps) {
     const float4 xi = X[i];
     const double xx = xi.x, xy = xi.y, xz = xi.z;
+    const double ax = g * fma(xz, xz, fma(xy, xy, xx * xx));
     float t[kRcCols], cf[kRcCols];
 #pragma unroll
     for (int k = 0; k < kRcCols; ++k) {
-      const double dx = xx - yx[k], dy = xy - yy[k], dz = xz - yz[k];
-      const double c = fma(dz, dz, fma(dy, dy, dx * dx));
-      t[k] = __double2float_rn(fma(-g, c, Bj[k]));
-      cf[k] = __double2float_rn(c);
+      t[k] = __double2float_rn(fma(xz, gz[k], fma(xy, gy[k], fma(xx, gx[k], Bq[k]))) - ax);
+      const float4 y = s_y[lane + 32 * k];
+      const float dx = xi.x - y.x, dy = xi.y - y.y, dz = xi.z - y.z;
+      cf[k] = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
     }
     float m = t[0];
 #pragma unroll
@@ -305,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
       const float p = ex2f(t[k] - ms);
       R += p;
       Wc = fmaf(cf[k], p, Wc);
-      K0 = fmaf(cf[k], f0[k], K0);
-      K1 = fmaf(cf[k], f1[k], K1);
+      K0 = fmaf(cf[k], s_c0[lane + 32 * k], K0);
+      K1 = fmaf(cf[k], s_c1[lane + 32 * k], K1);
     }
     float4 o = make_float4(R, Wc, K0, K1);
 #pragma unroll
@@ -723,6 +724,7 @@ struct DevRoundArgs {
   // record rounding: the last appended trace record gets the cost
   const AspotCtl* ctl;
   TraceDev* trace;
+  int* clear;          // set to 0 at the end (the record gate), may be null
 };
 
 // out *= min(1, s / mass); row clip rho (rounding.hpp:52-56)
@@ -818,6 +820,7 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
     o.infeasible = infeasible;
     if (a.trace && a.ctl && a.ctl->trace_len >= 1 && a.ctl->trace_len <= a.ctl->trace_cap)
       a.trace[a.ctl->trace_len - 1].rounded_cost = o.cost;
+    if (a.clear) *a.clear = 0;
   }
 }
 
@@ -910,7 +913,7 @@ inline void enqueue_round_device(Context& cx, const DevProblem& P, Workspace& ws
                                  const double* row0, RoundOut* ro, const int* gate, const AspotCtl* ctl,
                                  TraceDev* trace) {
   const int64_t n = P.n;
-  DevRoundArgs a{n, row0, ws.ro_r.p, ws.ro_c.p, P.s, ws.rv(0), ro, gate, ctl, trace};
+  DevRoundArgs a{n, row0, ws.ro_r.p, ws.ro_c.p, P.s, ws.rv(0), ro, gate, ctl, trace, const_cast<int*>(gate)};
   launch_k(k_dr_rowclip, dim3(1), dim3(kDrThreads), 0, cx.stream, a);
   // column clip: column sums of diag(rho) B (plain exp, the reference's b_matrix of the rounding input)
   launch_sweep(cx, P, ws, z, ws.rv(0), nullptr, gate, false, gamma);

@@ -206,3 +206,43 @@ def test_device_rounding_matches_host_rounding():
         np.testing.assert_allclose(d["rs"], h["rs"], rtol=0, atol=atol)
         np.testing.assert_allclose(d["cs"], h["cs"], rtol=0, atol=atol)
         assert d["gap"] <= (1e-7 if name == "f64" else 1e-5)
+
+
+TAIL_SNIPPET = r"""
+import json, sys
+sys.path.insert(0, %r)
+from paper_2601_17196_b200 import pot
+out = {}
+for name, inst in (("f64", pot.config_instance(1, n=600)), ("points", pot.config_instance(3, n=1500))):
+    cfg = pot.SolverConfig(epsilon=2e-2, log_every=3, max_iterations=90, materialize_plan=False,
+                           record_rounded_cost=True)
+    g = pot.aspot_solve(inst, cfg, trace_cap=1000)
+    out[name] = {"t": [r.t for r in g.trace], "rc": [r.rounded_cost for r in g.trace], "cost": g.cost}
+print(json.dumps(out))
+"""
+
+
+def test_record_rounding_tail_matches_host_rounding():
+    """record_rounded_cost with records inside the loop: the per-record
+    round_pot runs as a gated device tail of the attempt graph (no pause,
+    no host round trip); every record's cost equals the paused host-driven
+    rounding ($POTGPU_NO_ROUND_TAIL=1)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("", "1"):
+        env = dict(os.environ)
+        if flag:
+            env["POTGPU_NO_ROUND_TAIL"] = flag
+        r = subprocess.run([sys.executable, "-c", TAIL_SNIPPET % root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[flag] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, tol in (("f64", 1e-13), ("points", 1e-9)):
+        a, b = res[""][name], res["1"][name]
+        assert a["t"] == b["t"] and len(a["t"]) >= 30
+        assert all(x is not None for x in a["rc"])
+        np.testing.assert_allclose(a["rc"], b["rc"], rtol=tol)
