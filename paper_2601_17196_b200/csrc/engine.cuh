@@ -140,7 +140,7 @@ struct Workspace {
   DevBuf<float4> rc_part;     // fused final pass of the device rounding (plan.cuh): fp32 [row][strip] partials
   DevBuf<float> rc_pm;
   DevBuf<double> rc_part64;   // fp64 problems: [row][strip][3]
-  DevBuf<int> rc_gate;
+  DevBuf<double> rc_scratch;  // device rounding's block partials
   DevBuf<AspotCtl> ctl;
   DevBuf<unsigned> ticket;
   PinnedObj<AspotCtl> host_ctl_buf;
@@ -290,6 +290,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.ro_c.alloc(size_t(n));
   PG_CK(cudaMemcpyAsync(ws.ro_r.p, P.r.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
   PG_CK(cudaMemcpyAsync(ws.ro_c.p, P.c.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+  ws.rc_scratch.alloc(size_t(8 * 32));
   if (!cx.comm.sharded()) {  // the device rounding's fused pass (plan.cuh round_device)
     if (P.dtype == POTGPU_F64) {
       if (P.kind == POTGPU_COST_DENSE) ws.rc_part64.alloc(size_t(3 * n * ceil_div(n, kStripCols)));

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_f32(const float* __rest
 constexpr int kRcCols = 8;  // columns per lane
 constexpr int kRcStrip = 32 * kRcCols;
 
+template <bool B1>  // a second rank-1 column factor (Sinkhorn plans); without it one sum fewer per row
 __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __restrict__ X, const float4* __restrict__ Y,
                                                                double g, RowCostArgs a) {
   pdl_wait();
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
       R += p;
       Wc = fmaf(cf[k], p, Wc);
       K0 = fmaf(cf[k], s_c0[lane + 32 * k], K0);
-      K1 = fmaf(cf[k], s_c1[lane + 32 * k], K1);
+      if (B1) K1 = fmaf(cf[k], s_c1[lane + 32 * k], K1);
     }
     float4 o = make_float4(R, Wc, K0, K1);
 #pragma unroll
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rowcost_pts64(const float4* __r
       o.x += __shfl_xor_sync(0xffffffffu, o.x, off);
       o.y += __shfl_xor_sync(0xffffffffu, o.y, off);
       o.z += __shfl_xor_sync(0xffffffffu, o.z, off);
-      o.w += __shfl_xor_sync(0xffffffffu, o.w, off);
+      if (B1) o.w += __shfl_xor_sync(0xffffffffu, o.w, off);
     }
     if (lane == 0) {
       a.part[i * ldp + blockIdx.x] = o;
@@ -435,7 +436,8 @@ struct PlanEngine {
     double wscale = 1.0;
     if (pts) {
       wscale = P.cost_scale;
-      k_rowcost_pts64<<<g, kThreads, 0, cx.stream>>>(P.X4.p, P.Y4.p, kLog2e * P.cost_scale / gamma, a);
+      if (b1) k_rowcost_pts64<true><<<g, kThreads, 0, cx.stream>>>(P.X4.p, P.Y4.p, kLog2e * P.cost_scale / gamma, a);
+      else k_rowcost_pts64<false><<<g, kThreads, 0, cx.stream>>>(P.X4.p, P.Y4.p, kLog2e * P.cost_scale / gamma, a);
     } else {
       a.g = float(kLog2e / gamma);
       k_rowcost_f32<false><<<g, kThreads, 0, cx.stream>>>(P.C32.p, P.ld, nullptr, nullptr, a);
@@ -727,23 +729,38 @@ struct DevRoundArgs {
   int* clear;          // set to 0 at the end (the record gate), may be null
 };
 
-// out *= min(1, s / mass); row clip rho (rounding.hpp:52-56)
-__global__ void __launch_bounds__(kDrThreads) k_dr_rowclip(DevRoundArgs a) {
+// The O(n) steps run on kDrBlocks blocks: a first pass writes per-block
+// partials, the next kernel reduces them in block order (every block alike,
+// fixed order) and goes on element-wise.
+constexpr int kDrBlocks = 32;
+
+// block partials of the mass of B(z): part[b]
+__global__ void __launch_bounds__(kDrThreads) k_dr_mass(DevRoundArgs a, double* part) {
   pdl_wait();
   if (a.gate && *a.gate == 0) return;
   __shared__ double sh[33];
-  const int64_t n = a.n;
   double m = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m += a.row0[i];
-  const double mass1 = dr_block_sum(m, sh);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += int64_t(gridDim.x) * blockDim.x)
+    m += a.row0[i];
+  m = dr_block_sum(m, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+// out *= min(1, s / mass); row clip rho (rounding.hpp:52-56)
+__global__ void __launch_bounds__(kDrThreads) k_dr_rowclip(DevRoundArgs a, const double* part) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  const int64_t n = a.n;
+  double mass1 = 0.0;
+  for (int b = 0; b < kDrBlocks; ++b) mass1 += part[b];
   const double alpha = mass1 > 0 ? fmin(1.0, a.s / mass1) : 1.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double row = alpha * a.row0[i];
     const double rh = row > 0 ? fmin(1.0, a.r[i] / row) : 1.0;
     a.v[i] = log(rh);
     a.v[2 * n + i] = alpha * rh;
   }
-  if (threadIdx.x == 0) a.ro->alpha = alpha;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ro->alpha = alpha;
 }
 
 // column clip kappa (rounding.hpp:57-61) from the column sums cc of diag(rho) B
@@ -752,7 +769,7 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_colclip(DevRoundArgs a, const
   if (a.gate && *a.gate == 0) return;
   const int64_t n = a.n;
   const double alpha = a.ro->alpha;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
     const double col3 = alpha * cc[j];
     const double kp = col3 > 0 ? fmin(1.0, a.c[j] / col3) : 1.0;
     const double cx3 = kp * col3;
@@ -762,21 +779,19 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_colclip(DevRoundArgs a, const
   }
 }
 
-// deficit fill (rounding.hpp:63-75), <C, X> (core.hpp:199-204), slacks and
-// plan_feasibility_gap (core.hpp:207-219)
-__global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
+// block partials of the deficit fill's sums: part[5 b + (mass3, na, nb, sum arho W, sum fa K)]
+__global__ void __launch_bounds__(kDrThreads) k_dr_sums(DevRoundArgs a, double* part) {
   pdl_wait();
   if (a.gate && *a.gate == 0) return;
   __shared__ double sh[33];
   const int64_t n = a.n;
   const double* arho = a.v + 2 * n;
-  const double* cx3 = a.v + 3 * n;
   const double* fb = a.v + 4 * n;
   const double* R = a.v + 5 * n;
   const double* W = a.v + 6 * n;
   const double* K = a.v + 7 * n;
   double m3 = 0.0, na = 0.0, nb = 0.0, saw = 0.0, sfk = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double x3 = arho[i] * R[i];
     const double fa = fmax(a.r[i] - x3, 0.0);
     m3 += x3;
@@ -790,6 +805,28 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
   nb = dr_block_sum(nb, sh);
   saw = dr_block_sum(saw, sh);
   sfk = dr_block_sum(sfk, sh);
+  if (threadIdx.x == 0) {
+    double* o = part + 5 * blockIdx.x;
+    o[0] = m3; o[1] = na; o[2] = nb; o[3] = saw; o[4] = sfk;
+  }
+}
+
+// deficit fill (rounding.hpp:63-75), <C, X> (core.hpp:199-204), slacks and
+// plan_feasibility_gap (core.hpp:207-219); the gap maxima as block partials
+__global__ void __launch_bounds__(kDrThreads) k_dr_slacks(DevRoundArgs a, const double* part, double* gpart) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  __shared__ double sh[33];
+  const int64_t n = a.n;
+  const double* arho = a.v + 2 * n;
+  const double* cx3 = a.v + 3 * n;
+  const double* fb = a.v + 4 * n;
+  const double* R = a.v + 5 * n;
+  double m3 = 0.0, na = 0.0, nb = 0.0, saw = 0.0, sfk = 0.0;
+  for (int b = 0; b < kDrBlocks; ++b) {
+    const double* o = part + 5 * b;
+    m3 += o[0]; na += o[1]; nb += o[2]; saw += o[3]; sfk += o[4];
+  }
   const double deficit = a.s - m3;
   double f = 0.0;
   int infeasible = 0;
@@ -798,7 +835,7 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
     else f = deficit / (na * nb);
   }
   double rg = 0.0, cg = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double x3 = arho[i] * R[i];
     const double fa = fmax(a.r[i] - x3, 0.0);
     const double rx = x3 + f * fa * nb;
@@ -811,13 +848,30 @@ __global__ void __launch_bounds__(kDrThreads) k_dr_finish(DevRoundArgs a) {
   rg = dr_block_max(rg, sh);
   cg = dr_block_max(cg, sh);
   if (threadIdx.x == 0) {
+    gpart[2 * blockIdx.x] = rg;
+    gpart[2 * blockIdx.x + 1] = cg;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     RoundOut& o = *a.ro;
     o.mass3 = m3; o.na = na; o.nb = nb; o.f = f;
     o.mass = m3 + f * na * nb;
     o.cost = saw + f * sfk;
+    o.infeasible = infeasible;
+  }
+}
+
+__global__ void k_dr_finish(DevRoundArgs a, const double* gpart) {
+  pdl_wait();
+  if (a.gate && *a.gate == 0) return;
+  if (threadIdx.x == 0) {
+    double rg = 0.0, cg = 0.0;
+    for (int b = 0; b < kDrBlocks; ++b) {
+      rg = fmax(rg, gpart[2 * b]);
+      cg = fmax(cg, gpart[2 * b + 1]);
+    }
+    RoundOut& o = *a.ro;
     o.row_gap = rg; o.col_gap = cg;
     o.gap = fmax(fmax(rg, cg), fabs(o.mass - a.s));
-    o.infeasible = infeasible;
     if (a.trace && a.ctl && a.ctl->trace_len >= 1 && a.ctl->trace_len <= a.ctl->trace_cap)
       a.trace[a.ctl->trace_len - 1].rounded_cost = o.cost;
     if (a.clear) *a.clear = 0;
@@ -914,13 +968,15 @@ inline void enqueue_round_device(Context& cx, const DevProblem& P, Workspace& ws
                                  TraceDev* trace) {
   const int64_t n = P.n;
   DevRoundArgs a{n, row0, ws.ro_r.p, ws.ro_c.p, P.s, ws.rv(0), ro, gate, ctl, trace, const_cast<int*>(gate)};
-  launch_k(k_dr_rowclip, dim3(1), dim3(kDrThreads), 0, cx.stream, a);
+  double* drp = ws.rc_scratch.p;  // [kDrBlocks * 5] sums, then [kDrBlocks * 2] gap maxima
+  launch_k(k_dr_mass, dim3(kDrBlocks), dim3(kDrThreads), 0, cx.stream, a, drp);
+  launch_k(k_dr_rowclip, dim3(kDrBlocks), dim3(kDrThreads), 0, cx.stream, a, static_cast<const double*>(drp));
   // column clip: column sums of diag(rho) B (plain exp, the reference's b_matrix of the rounding input)
   launch_sweep(cx, P, ws, z, ws.rv(0), nullptr, gate, false, gamma);
   launch_k(k_sum_partials, dim3(ws.nblk), dim3(kVecThreads), 0, cx.stream, static_cast<const double*>(ws.rowp.p),
            ws.nstrips, static_cast<const double*>(ws.colp.p), ws.nrb, ws.pfmt, z, static_cast<const double*>(ws.rv(0)),
            P.rowshift(), ws.rv(5), ws.rv(3), gate);
-  launch_k(k_dr_colclip, dim3(1), dim3(kDrThreads), 0, cx.stream, a, static_cast<const double*>(ws.rv(3)));
+  launch_k(k_dr_colclip, dim3(kDrBlocks), dim3(kDrThreads), 0, cx.stream, a, static_cast<const double*>(ws.rv(3)));
   // final row sums of B diag(kappa) + the cost's per-row terms
   RowCostArgs ra{};
   ra.n = n;
@@ -951,7 +1007,7 @@ inline void enqueue_round_device(Context& cx, const DevProblem& P, Workspace& ws
     double wscale = 1.0;
     if (pts) {
       wscale = P.cost_scale;
-      launch_k(k_rowcost_pts64, g, dim3(kThreads), 0, cx.stream, static_cast<const float4*>(P.X4.p),
+      launch_k(k_rowcost_pts64<false>, g, dim3(kThreads), 0, cx.stream, static_cast<const float4*>(P.X4.p),
                static_cast<const float4*>(P.Y4.p), kLog2e * P.cost_scale / gamma, ra);
     } else {
       ra.g = float(kLog2e / gamma);
@@ -962,7 +1018,10 @@ inline void enqueue_round_device(Context& cx, const DevProblem& P, Workspace& ws
              static_cast<const float*>(ws.rc_pm.p), strips, int64_t(0), n, z.u(), static_cast<const double*>(nullptr),
              z.w(), wscale, ws.rv(5), ws.rv(6), ws.rv(7), ws.rv(8) /* K1 = 0 (no rank-1 input); slack slot, rewritten */, gate);
   }
-  launch_k(k_dr_finish, dim3(1), dim3(kDrThreads), 0, cx.stream, a);
+  launch_k(k_dr_sums, dim3(kDrBlocks), dim3(kDrThreads), 0, cx.stream, a, drp);
+  launch_k(k_dr_slacks, dim3(kDrBlocks), dim3(kDrThreads), 0, cx.stream, a, static_cast<const double*>(drp),
+           drp + 5 * kDrBlocks);
+  launch_k(k_dr_finish, dim3(1), dim3(32), 0, cx.stream, a, static_cast<const double*>(drp + 5 * kDrBlocks));
   PG_CK(cudaGetLastError());
 }
 
