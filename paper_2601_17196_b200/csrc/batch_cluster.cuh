@@ -79,7 +79,7 @@ struct BcWs {
   double* xch;       // [2][cluster rank][kBcX]
   int64_t stride;    // slot stride
   int cur;           // problem being solved (set by rank 0)
-  int pad;
+  int skip;          // that problem failed its upload / never arrived (set by rank 0)
 };
 
 // Fixed part of the CTA's shared memory; the row-sized arrays follow it
@@ -844,7 +844,8 @@ __device__ void bc_record_cost(BcCtx& X, int64_t len_before, TraceDev* trace) {
 
 // The persistent batch kernel: grid = cs x clusters, cluster = (cs, 1, 1).
 __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* probs, int count, BcWs* wss,
-                                                              BcResult* results, int* queue, BcLayout lay, int fuse) {
+                                                              BcResult* results, int* queue, BcLayout lay, int fuse,
+                                                              const int* ready) {
   extern __shared__ __align__(16) unsigned char bc_smem_raw[];
   BcShared* sm = reinterpret_cast<BcShared*>(bc_smem_raw);
   cgx::cluster_group cl = cgx::this_cluster();
@@ -853,10 +854,30 @@ __global__ void __launch_bounds__(kBcThreads, 1) k_batch_aspot(const BcProblem* 
   const int cid = int(blockIdx.x) / cs;
   BcWs* W = wss + cid;
   for (;;) {
-    if (rank == 0 && threadIdx.x == 0) W->cur = atomicAdd(queue, 1);
+    if (rank == 0 && threadIdx.x == 0) {
+      const int q = atomicAdd(queue, 1);
+      W->cur = q;
+      // the host uploads problems while the launch runs: wait for this one
+      // (1 = ready, 2 = its upload failed; bounded so a lost flag cannot hang the GPU)
+      int st = 1;
+      if (ready && q < count) {
+        const uint64_t t0 = globaltimer_ns();
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(st) : "l"(ready + q) : "memory");
+          if (st != 0) break;
+          if (globaltimer_ns() - t0 > 60000000000ull) { st = 3; break; }
+          __nanosleep(200);
+        }
+      }
+      W->skip = st != 1;
+    }
     bc_sync();
     const int p = *reinterpret_cast<volatile int*>(&W->cur);
     if (p >= count) break;
+    if (*reinterpret_cast<volatile int*>(&W->skip)) {  // uniform over the cluster
+      bc_sync();
+      continue;
+    }
     BcCtx X;
     X.P = probs + p;
     X.W = W;

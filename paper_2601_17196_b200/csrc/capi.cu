@@ -1127,83 +1127,12 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   check_config(cfg);
   std::vector<std::unique_ptr<BcHostProblem>> hp(static_cast<size_t>(count));
   std::vector<BcProblem> dp(static_cast<size_t>(count));
-  // upload + validation + setup, `concurrency` host threads with own streams
-  const int workers = int(std::max<int64_t>(1, std::min<int64_t>(concurrency > 0 ? concurrency : 8, count)));
-  std::atomic<int64_t> next{0};
-  std::vector<std::thread> pool;
-  for (int t = 0; t < workers; ++t) {
-    pool.emplace_back([&] {
-      Context cx = base;
-      cx.comm = Comm{};
-      PG_CK(cudaSetDevice(cx.device));
-      PG_CK(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
-      int64_t k;
-      while ((k = next.fetch_add(1)) < count) {
-        auto h = std::make_unique<BcHostProblem>();
-        try {
-          upload_problem(cx, &problems[k], h->P);
-          const int64_t n = h->P.n;
-          h->st = aspot_setup(h->P, cfg.epsilon);
-          h->gamma = cfg.gamma_override > 0 ? cfg.gamma_override : h->st.gamma;
-          if (!(h->gamma > 0) || !std::isfinite(h->gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
-          build_logk(cx, h->P, h->gamma);
-          if (!h->P.C32.p) throw Error(POTGPU_ERR_UNSUPPORTED, "internal: no fp32 stored cost");
-          h->marg.alloc(size_t(4 * n));
-          PG_CK(cudaMemcpyAsync(h->marg.p, h->st.mr.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
-          PG_CK(cudaMemcpyAsync(h->marg.p + n, h->st.mc.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
-          PG_CK(cudaMemcpyAsync(h->marg.p + 2 * n, h->P.r.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
-          PG_CK(cudaMemcpyAsync(h->marg.p + 3 * n, h->P.c.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
-          h->outv.alloc(size_t(4 * n + 1));
-          const potgpu_outputs* out = outputs ? &outputs[k] : nullptr;
-          h->trace_cap = std::max<int64_t>(out ? out->trace_cap : 0, 0) + 1;
-          h->log_cap = cfg.collect_iter_log ? std::max<int64_t>(out ? out->iter_log_cap : 0, 0) : 0;
-          h->trace.alloc(size_t(h->trace_cap));
-          h->lg.alloc(size_t(std::max<int64_t>(h->log_cap, 1)));
-          BcProblem& b = dp[size_t(k)];
-          std::memset(&b, 0, sizeof(b));
-          b.C = h->P.C32.p;
-          b.ld = h->P.ld;
-          b.rt = h->marg.p;
-          b.ct = h->marg.p + n;
-          b.r = h->marg.p + 2 * n;
-          b.c = h->marg.p + 3 * n;
-          b.g2 = float(kLog2e / h->gamma);
-          AspotCtl& c = b.ctl0;  // AspotSession::begin's control block
-          c.n = n;
-          c.max_iterations = cfg.max_iterations;
-          c.pause_at = INT64_MAX;
-          c.log_every = cfg.log_every;
-          c.block_rule = cfg.block_rule;
-          c.trace_cap = h->trace_cap;
-          c.log_cap = h->log_cap;
-          c.theta = 1.0;
-          c.gamma = h->gamma;
-          c.eps_tilde = h->st.eps_tilde;
-          c.step_denom = 3.0 * (ksum(h->st.mr.data(), n) + ksum(h->st.mc.data(), n) - h->P.s);
-          c.s = h->P.s;
-          c.status = ST_RUNNING;
-          c.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
-          b.trace = h->trace.p;
-          b.iterlog = h->log_cap > 0 ? h->lg.p : nullptr;
-          b.zc_out = h->outv.p;
-          b.row_slack = h->outv.p + 2 * n + 1;
-          b.col_slack = h->outv.p + 3 * n + 1;
-          PG_CK(cudaStreamSynchronize(cx.stream));
-        } catch (const Error& e) {
-          h->code = e.code;
-          h->err = e.what();
-        }
-        hp[size_t(k)] = std::move(h);
-      }
-      cudaStreamSynchronize(cx.stream);
-      cudaStreamDestroy(cx.stream);
-    });
-  }
-  for (auto& th : pool) th.join();
-  for (int64_t k = 0; k < count; ++k)
-    if (hp[size_t(k)]->code) throw Error(hp[size_t(k)]->code, "problem " + std::to_string(k) + ": " + hp[size_t(k)]->err);
   int64_t nmax = 0;
-  for (int64_t k = 0; k < count; ++k) nmax = std::max(nmax, hp[size_t(k)]->P.n);
+  bool dev_inputs = false;
+  for (int64_t k = 0; k < count; ++k) {
+    nmax = std::max(nmax, problems[k].n);
+    dev_inputs = dev_inputs || problems[k].device_ptrs != 0;
+  }
   // launch geometry
   // cluster size: $POTGPU_BC_CS, else the smallest whose per-CTA rows fit
   // shared memory (every problem's CTAs stream at the per-SM rate and share
@@ -1248,6 +1177,12 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaOccupancyMaxActiveClusters(&maxc, k_batch_aspot, &lc));
   if (maxc < 1) throw Error(POTGPU_ERR_UNSUPPORTED, "no resident cluster of this size");
   int nc = int(std::min<int64_t>(maxc, count));
+  // the uploads overlap the launch ($POTGPU_BC_OVERLAP=0: upload first): keep
+  // SMs free for the upload path's own kernels (validation, layout), which
+  // the resident clusters would otherwise block while waiting for them;
+  // device-resident inputs may need a device synchronise: never overlapped
+  const bool overlap = !dev_inputs && env_int("POTGPU_BC_OVERLAP", 1) != 0;
+  if (overlap) nc = std::max(1, std::min(nc, (base.num_sms - 8) / cs));
   const int cap = env_int("POTGPU_BC_CLUSTERS", 0);
   if (cap > 0) nc = std::min(nc, cap);
   lc.gridDim = dim3(unsigned(cs * nc));
@@ -1270,7 +1205,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
     h.colpart2 = h.colpart + int64_t(cs) * nmax;
     h.stride = stride;
     h.cur = 0;
-    h.pad = 0;
+    h.skip = 0;
   }
   // K1'': z_check' and the next z_bar in one pass over C ($POTGPU_BC_FUSE=0: separate)
   const int fuse = env_int("POTGPU_BC_FUSE", 1) != 0 ? 1 : 0;
@@ -1280,22 +1215,124 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   dprob.alloc(size_t(count));
   DevBuf<BcResult> dres;
   dres.alloc(size_t(count));
-  DevBuf<int> queue;
+  DevBuf<int> queue, ready;
   queue.alloc(1);
+  ready.alloc(size_t(count));
+  PG_CK(cudaMemsetAsync(ready.p, 0, size_t(count) * sizeof(int), base.stream));
   cudaStream_t st = base.stream;
   PG_CK(cudaMemcpyAsync(dws.p, hw.data(), hw.size() * sizeof(BcWs), cudaMemcpyHostToDevice, st));
-  PG_CK(cudaMemcpyAsync(dprob.p, dp.data(), dp.size() * sizeof(BcProblem), cudaMemcpyHostToDevice, st));
+
   PG_CK(cudaMemsetAsync(dres.p, 0, size_t(count) * sizeof(BcResult), st));
   queue.zero(st);
+  auto run_uploads = [&] {
+  // upload + validation + setup, `concurrency` host threads with own streams
+    const int workers = int(std::max<int64_t>(1, std::min<int64_t>(concurrency > 0 ? concurrency : 8, count)));
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < workers; ++t) {
+      pool.emplace_back([&] {
+        Context cx = base;
+        cx.comm = Comm{};
+        PG_CK(cudaSetDevice(cx.device));
+        PG_CK(cudaStreamCreateWithFlags(&cx.stream, cudaStreamNonBlocking));
+        int64_t k;
+        while ((k = next.fetch_add(1)) < count) {
+          auto h = std::make_unique<BcHostProblem>();
+          try {
+            upload_problem(cx, &problems[k], h->P);
+            const int64_t n = h->P.n;
+            h->st = aspot_setup(h->P, cfg.epsilon);
+            h->gamma = cfg.gamma_override > 0 ? cfg.gamma_override : h->st.gamma;
+            if (!(h->gamma > 0) || !std::isfinite(h->gamma)) throw Error(POTGPU_INVALID_ARGUMENT, "gamma must be positive");
+            build_logk(cx, h->P, h->gamma);
+            if (!h->P.C32.p) throw Error(POTGPU_ERR_UNSUPPORTED, "internal: no fp32 stored cost");
+            h->marg.alloc(size_t(4 * n));
+            PG_CK(cudaMemcpyAsync(h->marg.p, h->st.mr.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+            PG_CK(cudaMemcpyAsync(h->marg.p + n, h->st.mc.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+            PG_CK(cudaMemcpyAsync(h->marg.p + 2 * n, h->P.r.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+            PG_CK(cudaMemcpyAsync(h->marg.p + 3 * n, h->P.c.data(), size_t(n) * 8, cudaMemcpyHostToDevice, cx.stream));
+            h->outv.alloc(size_t(4 * n + 1));
+            const potgpu_outputs* out = outputs ? &outputs[k] : nullptr;
+            h->trace_cap = std::max<int64_t>(out ? out->trace_cap : 0, 0) + 1;
+            h->log_cap = cfg.collect_iter_log ? std::max<int64_t>(out ? out->iter_log_cap : 0, 0) : 0;
+            h->trace.alloc(size_t(h->trace_cap));
+            h->lg.alloc(size_t(std::max<int64_t>(h->log_cap, 1)));
+            BcProblem& b = dp[size_t(k)];
+            std::memset(&b, 0, sizeof(b));
+            b.C = h->P.C32.p;
+            b.ld = h->P.ld;
+            b.rt = h->marg.p;
+            b.ct = h->marg.p + n;
+            b.r = h->marg.p + 2 * n;
+            b.c = h->marg.p + 3 * n;
+            b.g2 = float(kLog2e / h->gamma);
+            AspotCtl& c = b.ctl0;  // AspotSession::begin's control block
+            c.n = n;
+            c.max_iterations = cfg.max_iterations;
+            c.pause_at = INT64_MAX;
+            c.log_every = cfg.log_every;
+            c.block_rule = cfg.block_rule;
+            c.trace_cap = h->trace_cap;
+            c.log_cap = h->log_cap;
+            c.theta = 1.0;
+            c.gamma = h->gamma;
+            c.eps_tilde = h->st.eps_tilde;
+            c.step_denom = 3.0 * (ksum(h->st.mr.data(), n) + ksum(h->st.mc.data(), n) - h->P.s);
+            c.s = h->P.s;
+            c.status = ST_RUNNING;
+            c.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
+            b.trace = h->trace.p;
+            b.iterlog = h->log_cap > 0 ? h->lg.p : nullptr;
+            b.zc_out = h->outv.p;
+            b.row_slack = h->outv.p + 2 * n + 1;
+            b.col_slack = h->outv.p + 3 * n + 1;
+            PG_CK(cudaStreamSynchronize(cx.stream));
+            if (overlap) {  // publish: the problem record, then its ready flag (same stream: ordered)
+              static const int kReady = 1;
+              PG_CK(cudaMemcpyAsync(dprob.p + k, &b, sizeof(BcProblem), cudaMemcpyHostToDevice, cx.stream));
+              PG_CK(cudaMemcpyAsync(ready.p + k, &kReady, sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+              PG_CK(cudaStreamSynchronize(cx.stream));
+            }
+          } catch (const Error& e) {
+            h->code = e.code;
+            h->err = e.what();
+            if (overlap) {
+              static const int kFailed = 2;
+              cudaMemcpyAsync(ready.p + k, &kFailed, sizeof(int), cudaMemcpyHostToDevice, cx.stream);
+              cudaStreamSynchronize(cx.stream);
+            }
+          }
+          hp[size_t(k)] = std::move(h);
+        }
+        cudaStreamSynchronize(cx.stream);
+        cudaStreamDestroy(cx.stream);
+      });
+    }
+    for (auto& th : pool) th.join();
+  };
+  if (!overlap) run_uploads();
   const auto t_launch = HostClock::now();
   cudaEvent_t e0, e1;
   PG_CK(cudaEventCreate(&e0));
   PG_CK(cudaEventCreate(&e1));
   PG_CK(cudaEventRecord(e0, st));
+  if (!overlap) {
+    for (int64_t k = 0; k < count; ++k)
+      if (hp[size_t(k)]->code) throw Error(hp[size_t(k)]->code, "problem " + std::to_string(k) + ": " + hp[size_t(k)]->err);
+    PG_CK(cudaMemcpyAsync(dprob.p, dp.data(), dp.size() * sizeof(BcProblem), cudaMemcpyHostToDevice, st));
+  }
   PG_CK(cudaLaunchKernelEx(&lc, k_batch_aspot, static_cast<const BcProblem*>(dprob.p), int(count), dws.p, dres.p,
-                           queue.p, lay, fuse));
+                           queue.p, lay, fuse, overlap ? static_cast<const int*>(ready.p) : nullptr));
   PG_CK(cudaGetLastError());
   PG_CK(cudaEventRecord(e1, st));
+  if (overlap) {
+    run_uploads();
+    for (int64_t k = 0; k < count; ++k)
+      if (hp[size_t(k)]->code) {
+        cudaStreamSynchronize(st);  // the launch skips the failed problem and finishes
+        throw Error(hp[size_t(k)]->code, "problem " + std::to_string(k) + ": " + hp[size_t(k)]->err);
+      }
+  }
   std::vector<BcResult> res(static_cast<size_t>(count));
   PG_CK(cudaMemcpyAsync(res.data(), dres.p, res.size() * sizeof(BcResult), cudaMemcpyDeviceToHost, st));
   PG_CK(cudaStreamSynchronize(st));
