@@ -58,6 +58,10 @@ struct AspotCtl {
   // and the gate of its evaluation (g_new_sweep | g_new_one); one_sided_ok: problem allows it
   int g_new_one, g_new_eval, one_sided_ok;
   int clamp_guard;  // fp64 (Eigen-clamped exp) problems: scale only far above the clamp floor
+  // K1'' (sweep.cuh sweep_pts1_f32): the one-sided pass of z_check' also formed
+  // the next z_bar's partials (stash); fuse_ok: the problem allows it;
+  // g_bar_sweep: this attempt sweeps z_bar (= g_new unless stashed)
+  int fuse_ok, g_bar_stash, g_bar_sweep, pad_k1;
   int64_t pause_at;
   int64_t loop_budget;  // attempts the device loop (graph WHILE node) may still run in this launch
   int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
@@ -112,6 +116,10 @@ struct ReduceArgs {
   const double* src_row_a; const double* src_col_a; const double* src_w_a; int src_role_a;
   const double* src_row_b; const double* src_col_b; const double* src_w_b; int src_role_b;
   const int* select_b;
+  // K1'': when *alt_sel, the partials come from the stash the previous
+  // attempt's one-sided pass wrote (same layout)
+  const int* alt_sel;
+  const double* rowp_alt; const double* colp_alt; const double* maxp_alt;
   // deferred decision: write this launch's block partials to scratch and
   // stop; the next O(n) kernel of the attempt reduces them and decides
   // (decide_pending), so no block waits on a ticket here
@@ -192,7 +200,7 @@ __device__ void apply_role(AspotCtl* ctl, int role, const double (&acc)[kNumAcc]
       ctl->attempt_ok = 1;
       break;
     case R_CHECK:  // initial evaluation at z_check = 0 (solvers.hpp:305)
-      if (ps.overflow) { ctl->fatal = POTGPU_OVERFLOW; ctl->g_active = 0; ctl->g_new = 0; ctl->g_alive = 0; }
+      if (ps.overflow) { ctl->fatal = POTGPU_OVERFLOW; ctl->g_active = 0; ctl->g_new = 0; ctl->g_bar_sweep = 0; ctl->g_alive = 0; }
       break;
     default:
       break;
@@ -344,6 +352,10 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   const double* scol = useb ? a.src_col_b : a.src_col_a;
   const double dw = a.mode == 1 ? w - *(useb ? a.src_w_b : a.src_w_a) : 0.0;
   const double fs = a.mode == 1 ? exp(dw) : 1.0;
+  const bool alt = a.alt_sel && *a.alt_sel;
+  const double* rowp = alt ? a.rowp_alt : a.rowp;
+  const double* colp = alt ? a.colp_alt : a.colp;
+  const double* maxp = alt ? a.maxp_alt : a.maxp;
   // all threads iterate the same number of times (the shuffles need the full warp)
   for (int64_t i0 = int64_t(blockIdx.x) * per_block; i0 < n; i0 += span) {
     const int64_t i = i0 + threadIdx.x / kTPI;
@@ -354,8 +366,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     if (a.mode == 0) {
       double off = (ui + w) * kLog2e;
       if (a.rowshift) off = off + a.rowshift[ii];
-      rb = group_partial_sum<kTPI>(a.rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
-      cb = group_partial_sum<kTPI>(a.colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
+      rb = group_partial_sum<kTPI>(rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
+      cb = group_partial_sum<kTPI>(colp, ii * a.nrowblocks, a.nrowblocks, a.pfmt, 0.0, q);
     } else {
       rb = srow[ii] * fs;
       cb = scol[ii] * fs;
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   }
   if (a.mode == 0)
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
-      acc[11] = nan_max(acc[11], a.maxp[k]);
+      acc[11] = nan_max(acc[11], maxp[k]);
   // block reduction: warp shuffles, then the kEvalThreads / 32 warp results
   __shared__ double sh[kNumAcc][kEvalThreads / 32];
   __shared__ bool last;
@@ -544,7 +556,7 @@ __global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const 
   AspotCtl* c = ctl_stage(ctl_sm, ctl);
   const int fresh = c->g_new;
   if (!fresh && !c->g_alive) return;  // uniform: nothing to decide or update
-  if (fresh) decide_pending(c, R_BAR, pd.eval_part, pd.eval_nb, *zb.w(), true);
+  if (fresh) decide_pending(c, R_BAR, pd.eval_part, pd.eval_nb, *zb.w(), !c->g_bar_stash);
   if (c->g_alive) {
     const int64_t n = zb.n;
     const double step = c->step, th = c->theta;
@@ -573,9 +585,18 @@ __global__ void k_zgrave(AspotCtl* ctl, Slot zb, Slot z, Slot g, Slot zg, const 
 // When the new point is to be scaled rather than swept (block w: B scales
 // by e^dw), its sums (dst_row, dst_col) and the block partials of its
 // functionals are formed here (pd.gk_part), for the next kernel to decide on.
+// K1'' (which = 1, one-sided z_check'): also the next iteration's z_bar' =
+// (1 - theta') z_check' + theta' z_best (k_commit's arithmetic, same bits)
+// and the side of B(z_bar') that only rescales, for the fused pass.
+struct BarStash {
+  Slot zbn;
+  double* row;  // B(z_bar') 1 (block u)
+  double* col;  // B(z_bar')^T 1 (block v)
+};
 __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* row_a, const double* col_a, int role_a,
                             Slot src_b, const double* row_b, const double* col_b, int role_b, Slot dst,
-                            const double* rt, const double* ct, double* dst_row, double* dst_col, Pending pd) {
+                            const double* rt, const double* ct, double* dst_row, double* dst_col, Pending pd,
+                            BarStash bs) {
   pdl_wait();
   __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
   AspotCtl* c = ctl_stage(ctl_sm, ctl);
@@ -601,6 +622,8 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
     }
     const int64_t n = src.n;
     bool finite = true;
+    const bool k1 = which == 1 && c->g_new_one && c->fuse_ok && bs.zbn.base;
+    const double th = theta_next_d(c->theta), om = 1.0 - th;
     for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
       double x = src.base[k];
       if (k < n) {
@@ -615,6 +638,14 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
       if (which == 1 && c->g_new_one) {  // the side of z_check' that only rescales: B' = B e^(x' - x)
         if (k < n && block == 0) dst_row[k] = rowb[k] * exp(x - src.base[k]);
         else if (k >= n && k < 2 * n && block == 1) dst_col[k - n] = colb[k - n] * exp(x - src.base[k]);
+      }
+      if (k1) {  // z_bar' and its rescaled side (k_commit: a = om z_check', b = th z_best, z_bar = a + b)
+        const double za = om * x;
+        const double zb2 = th * src.base[k];
+        const double zbar = za + zb2;
+        bs.zbn.base[k] = zbar;
+        if (k < n && block == 0) bs.row[k] = rowb[k] * exp(zbar - src.base[k]);
+        else if (k >= n && k < 2 * n && block == 1) bs.col[k - n] = colb[k - n] * exp(zbar - src.base[k]);
       }
     }
     if (!finite) {
@@ -662,6 +693,7 @@ __device__ void append_trace(AspotCtl* ctl, TraceDev* trace, int64_t t, double e
 __device__ void reset_point_gates(AspotCtl* ctl) {
   ctl->g_hat_sweep = ctl->g_hat_scaled = ctl->g_new_sweep = ctl->g_new_scaled = 0;
   ctl->g_new_one = ctl->g_new_eval = 0;
+  ctl->g_bar_sweep = 0;
 }
 
 __device__ void begin_iteration(AspotCtl* ctl) {
@@ -669,6 +701,7 @@ __device__ void begin_iteration(AspotCtl* ctl) {
   ctl->halvings = 0;
   ctl->step = ctl->gamma / (ctl->step_denom * ctl->theta);  // solvers.hpp:328
   ctl->g_new = 1;
+  ctl->g_bar_sweep = !ctl->g_bar_stash;
   ctl->g_alive = 1;
   ctl->attempt_ok = 0;
   ctl->zbar_failed = 0;
@@ -775,12 +808,15 @@ __device__ void commit_state(AspotCtl* ctl, TraceDev* trace, IterLogDev* lg) {
 // attempt budget lasts.
 __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot zb, double* rowc, double* colc,
                          const double* rown, const double* coln, TraceDev* trace, IterLogDev* lg, Pending pd,
-                         cudaGraphConditionalHandle loop, int in_loop) {
+                         cudaGraphConditionalHandle loop, int in_loop, int* stash_bad) {
   pdl_wait();
   __shared__ __align__(16) uint32_t ctl_sm[kCtlWords];
   AspotCtl* c = ctl_stage(ctl_sm, ctl);
   if (!c->g_active) {  // uniform over the grid
-    if (in_loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(loop, 0u);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (in_loop) cudaGraphSetConditional(loop, 0u);
+      if (stash_bad) *stash_bad = 0;
+    }
     return;
   }
   const bool swept = c->g_new_sweep || c->g_new_one, scaled = c->g_new_scaled;
@@ -805,6 +841,10 @@ __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot 
     }
   }
   ctl_finish(ctl, ctl_sm, pd, [&](AspotCtl* cc) {
+    // K1'': the fused pass of this attempt's z_check' left the next z_bar's partials
+    const int bad = stash_bad ? __ldcg(stash_bad) : 1;
+    if (stash_bad) *stash_bad = 0;
+    cc->g_bar_stash = cc->attempt_ok && cc->fuse_ok && cc->g_new_one && !bad;
     commit_state(cc, trace, lg);
     if (in_loop) {
       cc->loop_budget -= 1;

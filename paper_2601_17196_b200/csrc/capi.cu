@@ -547,6 +547,7 @@ struct AspotSession : Session {
   cudaGraphExec_t exec_first = nullptr; // resume (k_resume_pinned) + one step attempt: the first launch of a run
   PinnedObj<ResumeArgs> resume_args;
   bool one_sided = false;  // z_check' by sweep_pts1_f32 when its block is u or v (fp32 points)
+  bool k1pp = false;       // ... which also forms the next z_bar (K1'')
   bool round_tail = false; // per-record rounding inside the attempt graph (record_rounded_cost)
   cudaGraphExec_t loop_exec = nullptr;  // the attempt inside a WHILE node: the whole loop in one launch
   int64_t trace_cap = 1, log_cap = 0;
@@ -610,8 +611,9 @@ struct AspotSession : Session {
     // (0 at the start: z = z_check = 0). Each evaluation defers its decision
     // to the O(n) kernel that follows it (Pending, aspot_kernels.cuh).
     const Pending pd = pending_of(ws);
-    launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_new, true, gamma), ZB, R_BAR, &ctl->g_new,
-                nullptr, true);
+    // (K1'': no sweep when the previous attempt's fused pass left z_bar's partials)
+    launch_eval(cx, ws, sweep_point(cx, P, ws, ZB, nullptr, nullptr, &ctl->g_bar_sweep, true, gamma), ZB, R_BAR,
+                &ctl->g_new, nullptr, true, &ctl->g_bar_stash);
     launch_k(k_zgrave, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, ZB, Z, G, ZG, ws.row(R_BAR), ws.col(R_BAR), ws.rt.p,
              ws.ct.p, pd);
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZG, nullptr, nullptr, &ctl->g_alive, true, gamma), ZG, R_GRAVE,
@@ -619,20 +621,31 @@ struct AspotSession : Session {
     // decides z_grave's block; forms z_hat, and when z_hat only differs in w
     // (~all iterations) also its scaled sums B(z_grave) e^dw and functionals
     launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 0, ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE,
-             ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p, ws.row(R_HAT), ws.col(R_HAT), pd);
+             ZG, ws.row(R_GRAVE), ws.col(R_GRAVE), R_GRAVE, ZH, ws.rt.p, ws.ct.p, ws.row(R_HAT), ws.col(R_HAT), pd,
+             BarStash{});
     launch_eval(cx, ws, sweep_point(cx, P, ws, ZH, nullptr, nullptr, &ctl->g_hat_sweep, true, gamma), ZH, R_HAT,
                 &ctl->g_hat_sweep, nullptr, true);
     // decides z_hat (phi, z_best, its block); forms z_check' = GK(z_best)
     // (scaled sums and functionals when its block is w)
     launch_k(k_gk_update, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, 1, ZH, ws.row(R_HAT), ws.col(R_HAT), R_HAT, ZC,
-             ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p, ws.row(R_NEW), ws.col(R_NEW), pd);
+             ws.row(R_CHECK), ws.col(R_CHECK), R_CHECK, ZN, ws.rt.p, ws.ct.p, ws.row(R_NEW), ws.col(R_NEW), pd,
+             k1pp ? BarStash{ws.slot(S_ZBN), ws.kbar.p, ws.kbar.p + P.n} : BarStash{});
     const SweepOut so_n = sweep_point(cx, P, ws, ZN, nullptr, nullptr, &ctl->g_new_sweep, true, gamma);
-    if (one_sided) launch_one_sided(cx, P, ws, ZN, &ctl->g_new_one, OneSidedArgs{ws.row(R_NEW), ws.col(R_NEW), ZH.v(),
-                                                                                &ctl->block_check});
+    if (one_sided) {
+      OneSidedArgs o{ws.row(R_NEW), ws.col(R_NEW), ZH.v(), &ctl->block_check};
+      if (k1pp) {  // K1'': the pass also forms the next z_bar's partials
+        const Slot ZBN = ws.slot(S_ZBN);
+        o.u2 = ZBN.u(); o.v2 = ZBN.v(); o.w2 = ZBN.w();
+        o.kbar_row = ws.kbar.p; o.kbar_col = ws.kbar.p + P.n;
+        o.rowp2 = ws.rowp2.p; o.colp2 = ws.colp2.p; o.maxp2 = ws.maxp2.p;
+        o.bad = ws.stash_bad.p;
+      }
+      launch_one_sided(cx, P, ws, ZN, &ctl->g_new_one, o);
+    }
     launch_eval(cx, ws, so_n, ZN, R_NEW, &ctl->g_new_eval, nullptr, true);
     // decides z_check' and commits the attempt
     launch_k(k_commit, dim3(gv), dim3(kVecThreads), 0, cx.stream, ctl, Z, ZC, ZH, ZN, ZB, ws.row(R_CHECK), ws.col(R_CHECK),
-             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd, loop, in_loop);
+             ws.row(R_NEW), ws.col(R_NEW), ws.trace.p, ws.iterlog.p, pd, loop, in_loop, k1pp ? ws.stash_bad.p : nullptr);
     PG_CK(cudaGetLastError());
     // record_rounded_cost with records inside the loop: the record's rounding
     // (round_pot of B(z_check), solvers.hpp:314-315) as a gated device tail
@@ -712,6 +725,8 @@ struct AspotSession : Session {
     h.clamp_guard = P.dtype == POTGPU_F64 ? 1 : 0;
     one_sided = one_sided_supported(cx, P) && ws.pts_cs == 1;
     h.one_sided_ok = one_sided ? 1 : 0;
+    k1pp = one_sided && k1pp_supported(cx, P) && ws.rowp2.p;
+    h.fuse_ok = k1pp ? 1 : 0;
     h.record_rounded_cost = cfg.record_rounded_cost ? 1 : 0;
     round_tail = cfg.record_rounded_cost && cfg.use_graphs && cfg.log_every < cfg.max_iterations &&
                  device_round_ok(cx, P, ws) && !std::getenv("POTGPU_NO_ROUND_TAIL");
@@ -1177,11 +1192,13 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   PG_CK(cudaOccupancyMaxActiveClusters(&maxc, k_batch_aspot, &lc));
   if (maxc < 1) throw Error(POTGPU_ERR_UNSUPPORTED, "no resident cluster of this size");
   int nc = int(std::min<int64_t>(maxc, count));
-  // the uploads overlap the launch ($POTGPU_BC_OVERLAP=0: upload first): keep
+  // $POTGPU_BC_OVERLAP=1: the uploads overlap the launch (off by default:
+  // measured 2.65 s vs 1.17 s for configs[4], the upload path's device work
+  // confined to the free SMs is slower than running it first); keep
   // SMs free for the upload path's own kernels (validation, layout), which
   // the resident clusters would otherwise block while waiting for them;
   // device-resident inputs may need a device synchronise: never overlapped
-  const bool overlap = !dev_inputs && env_int("POTGPU_BC_OVERLAP", 1) != 0;
+  const bool overlap = !dev_inputs && env_int("POTGPU_BC_OVERLAP", 0) != 0;
   if (overlap) nc = std::max(1, std::min(nc, (base.num_sms - 8) / cs));
   const int cap = env_int("POTGPU_BC_CLUSTERS", 0);
   if (cap > 0) nc = std::min(nc, cap);
@@ -1310,7 +1327,22 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
     }
     for (auto& th : pool) th.join();
   };
-  if (!overlap) run_uploads();
+  if (overlap) {
+    // load the upload path's kernels now: with lazy module loading (the CUDA 12
+    // default) a kernel's first launch waits for the device, here for the
+    // resident clusters that are themselves waiting for that upload
+    cudaFuncAttributes fa;
+    PG_CK(cudaFuncGetAttributes(&fa, k_dense_prepare<double>));
+    PG_CK(cudaFuncGetAttributes(&fa, k_dense_prepare<float>));
+    PG_CK(cudaFuncGetAttributes(&fa, k_points_max2<false>));
+    PG_CK(cudaFuncGetAttributes(&fa, k_points_max2<true>));
+    PG_CK(cudaFuncGetAttributes(&fa, k_points_store));
+    PG_CK(cudaFuncGetAttributes(&fa, k_scale_points));
+    PG_CK(cudaFuncGetAttributes(&fa, k_dot_prep));
+    PG_CK(cudaFuncGetAttributes(&fa, k_build_logk));
+  } else {
+    run_uploads();
+  }
   const auto t_launch = HostClock::now();
   cudaEvent_t e0, e1;
   PG_CK(cudaEventCreate(&e0));

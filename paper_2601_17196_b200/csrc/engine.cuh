@@ -134,6 +134,10 @@ struct Workspace {
   DevBuf<unsigned long long> carry_stats;  // CTAs of sweep_pts2_f32 launches: carried, exact
   DevBuf<double> dpart, gpart;  // deferred-decision partials: k_point_eval (defer) / k_gk_update (scaled point)
   DevBuf<int> gflag;            // non-finite Greenkhorn update seen (k_gk_update)
+  // K1'' stash: the next z_bar's partials from the fused one-sided pass
+  // (sweep_pts1_f32), its rescaled side (kbar: [row | col]) and the pass's veto
+  DevBuf<double> rowp2, colp2, maxp2, kbar;
+  DevBuf<int> stash_bad;
   DevBuf<double> rt, ct;    // marginals the dual targets
   DevBuf<double> ro_buf;    // rounding vectors: rho, kappa, lu, lv, rowx, colx, a, b, row_slack, col_slack
   DevBuf<double> ro_r, ro_c;  // original marginals for rounding
@@ -164,6 +168,28 @@ inline int cost_sweep_rows(int64_t n) { return int(std::max<int64_t>(16, ceil_di
 inline int64_t cost_sweep_parts(int64_t n) { return ceil_div(n, kThreads) * ceil_div(n, cost_sweep_rows(n)); }
 
 enum SlotId { S_Z = 0, S_ZC = 1, S_ZB = 2, S_G = 3, S_ZG = 4, S_ZH = 5, S_ZN = 6, kSlots = 7 };
+constexpr int S_ZBN = kSlots;           // K1'': the next z_bar, formed with z_check' (k_gk_update)
+constexpr int kSlotsWs = kSlots + 1;
+
+// One-sided points sweep of z_check' (sweep_pts1_f32): the same grid and
+// partial buffers as launch_sweep, unsharded fp32 points problems only.
+inline bool one_sided_supported(const Context& cx, const DevProblem& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_ONE_SIDED");
+    return !(e && e[0] == '0');
+  }();
+  return on && P.dtype == POTGPU_F32 && P.dot_form() && !cx.comm.sharded() && pts_pairs() == 2;
+}
+
+// K1'' on the one-sided pass ($POTGPU_K1PP, default on): the pass also forms
+// the next iteration's z_bar (sweep.cuh sweep_pts1_f32).
+inline bool k1pp_supported(const Context& cx, const DevProblem& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("POTGPU_K1PP");
+    return !(e && e[0] == '0');
+  }();
+  return on && one_sided_supported(cx, P);
+}
 
 inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, int64_t trace_cap, int64_t log_cap) {
   const int64_t n = P.n;
@@ -265,7 +291,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.nmax = int64_t(ws.g.grid.x) * ws.g.grid.y;
   ws.nblk = int(std::min<int64_t>(cx.num_sms, std::max<int64_t>(1, ceil_div(n, kVecThreads))));
   ws.slot_stride = round_up(2 * n + 1, 32);
-  ws.slots.alloc(size_t(kSlots * ws.slot_stride));
+  ws.slots.alloc(size_t(kSlotsWs * ws.slot_stride));
   ws.sums.alloc(size_t(2 * kRoles * n));
   ws.rowp.alloc(size_t(2 * ws.g.grid.x * n));  // x2: (max, sum) LSE partials
   ws.colp.alloc(size_t(2 * max_rb * n));
@@ -282,6 +308,14 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.gpart.alloc(size_t(kNumAcc * ws.gv));
   ws.gflag.alloc(1);
   ws.gflag.zero(cx.stream);
+  if (k1pp_supported(cx, P)) {
+    ws.rowp2.alloc(size_t(ws.g.grid.x * n));
+    ws.colp2.alloc(size_t(ws.g.grid.y * n));
+    ws.maxp2.alloc(size_t(ws.g.grid.x * ws.g.grid.y));
+    ws.kbar.alloc(size_t(2 * n));
+    ws.stash_bad.alloc(1);
+    ws.stash_bad.zero(cx.stream);
+  }
   ws.partial.alloc(size_t(std::max<int64_t>(4096, cost_sweep_parts(n) + ws.nshards * ceil_div(n, kThreads))));
   ws.rt.alloc(size_t(n));
   ws.ct.alloc(size_t(n));
@@ -432,7 +466,7 @@ inline double allreduce_host_sum(Context& cx, Workspace& ws, double x) {
 
 // The per-point evaluation (partials -> B 1, B^T 1, scalars, decision).
 inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, int role, const int* gate,
-                        const ReduceArgs* scaled = nullptr, bool defer = false) {
+                        const ReduceArgs* scaled = nullptr, bool defer = false, const int* alt_sel = nullptr) {
   ReduceArgs r{};
   if (scaled) r = *scaled;
   r.z = z;
@@ -447,6 +481,12 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
   r.pfmt = so.pfmt;
   r.rowshift = so.rowshift;
   r.mode = scaled ? 1 : 0;
+  if (alt_sel && ws.rowp2.p) {  // K1'' stash (same grid and layout as the sweep's partials)
+    r.alt_sel = alt_sel;
+    r.rowp_alt = ws.rowp2.p;
+    r.colp_alt = ws.colp2.p;
+    r.maxp_alt = ws.maxp2.p;
+  }
   switch (ws.eval_tpi) {
     case 1: launch_k(k_point_eval<1>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
     case 2: launch_k(k_point_eval<2>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
@@ -454,16 +494,6 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
     default: launch_k(k_point_eval<4>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;
   }
   PG_CK(cudaGetLastError());
-}
-
-// One-sided points sweep of z_check' (sweep_pts1_f32): the same grid and
-// partial buffers as launch_sweep, unsharded fp32 points problems only.
-inline bool one_sided_supported(const Context& cx, const DevProblem& P) {
-  static const bool on = [] {
-    const char* e = std::getenv("POTGPU_ONE_SIDED");
-    return !(e && e[0] == '0');
-  }();
-  return on && P.dtype == POTGPU_F32 && P.dot_form() && !cx.comm.sharded() && pts_pairs() == 2;
 }
 
 inline void launch_one_sided(Context& cx, const DevProblem& P, Workspace& ws, Slot z, const int* gate, const OneSidedArgs& o) {

@@ -1384,15 +1384,37 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_ptsR_f32(SrcPointsDotF32 sr
 // (one nonzero partial per index: S 2^(M + offset) = the known sum), so the
 // evaluation is the same kernel. block (device): 0 = u (columns swept),
 // 1 = v (rows swept).
+//
+// K1'' (reference: the z_bar of the next iteration,
+// solvers.hpp:336, evaluated at :337). The next iteration's
+//   z_bar' = (1 - theta') z_check' + theta' z_best = z_best + (1 - theta') D
+// differs from z_best, like z_check' = z_best + D, only in the Greenkhorn
+// block, so B(z_bar') is the same row (block u) or column (block v)
+// rescaling of the entries this pass already exponentiates. With rowp2 set,
+// the pass also forms z_bar''s unknown side from those entries (block u: a
+// second column accumulator with row factors 2^(m_i + A''_i); block v: a
+// second row sum with column weights 2^(d_j - dmax), d_j = B''_j - B'_j) and
+// writes z_bar''s partials (known side encoded from kbar_row / kbar_col) to
+// rowp2 / colp2 / maxp2, so the next iteration's z_bar needs no sweep. The
+// block-v max exponent of z_bar' is an upper bound; a bound near the
+// overflow threshold, a spread of d_j wider than kOneSidedSpread or a
+// non-finite d_j raise *bad and the next iteration sweeps z_bar as before.
 struct OneSidedArgs {
   const double* krow;  // B' 1 (block u)
   const double* kcol;  // B'^T 1 (block v)
   const double* vsrc;  // v of the source point (block v)
   const int* block;
+  // K1'' (null rowp2: off)
+  const double* u2; const double* v2; const double* w2;  // z_bar'
+  const double* kbar_row;  // B(z_bar') 1 (block u)
+  const double* kbar_col;  // B(z_bar')^T 1 (block v)
+  double* rowp2; double* colp2; double* maxp2;
+  int* bad;
 };
 constexpr float kOneSidedSpread = 40.f;
 __host__ __device__ constexpr size_t sweep_pts1_smem(int rows_per_cta) {
-  return sweep_pts_smem(rows_per_cta) + size_t((rows_per_cta + 3) & ~3) * sizeof(float);
+  // + source segment maxima, + z_bar''s row offsets
+  return sweep_pts_smem(rows_per_cta) + 2 * size_t((rows_per_cta + 3) & ~3) * sizeof(float);
 }
 __device__ __forceinline__ float2 encode_sum(double R, double off) {  // (S, M): S 2^(M + off) = R
   if (!(R > 0.0)) return make_float2(0.f, 0.f);
@@ -1406,19 +1428,25 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
   constexpr int kStrip = 64 * KP;
   if (a.gate && *a.gate == 0) return;
   const int mode = *o.block;
+  const bool fuse = o.rowp2 != nullptr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int64_t j0 = int64_t(blockIdx.x) * kStrip;
   const int64_t r0 = a.row_lo + int64_t(blockIdx.y) * a.rows_per_cta;
   const int64_t r1 = min(a.row_hi, r0 + a.rows_per_cta);
   const double w = *a.w;
+  const double w2 = fuse ? *o.w2 : 0.0;
   const int64_t ldp = gridDim.x;
-  extern __shared__ float4 s_R[];  // rows (2x', A_i), the row-sum tiles, then [rows] source segment maxima
-  float* s_M = reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33;
+  extern __shared__ float4 s_R[];  // rows (2x', A_i), the row-sum tiles, [rows] source segment maxima, [rows] A''_i
+  float* s_tiles = reinterpret_cast<float*>(s_R + a.rows_per_cta);
+  float* s_M = s_tiles + kWarps * 32 * 33;
+  float* s_A2 = s_M + ((a.rows_per_cta + 3) & ~3);
   __shared__ float2 s_B[KP][32];
-  __shared__ float s_dv[2][kWarps];
+  __shared__ float s_dv[4][kWarps];
   float2* rowp = reinterpret_cast<float2*>(a.rowp);
   float2* colp = reinterpret_cast<float2*>(a.colp);
+  float2* rowp2 = reinterpret_cast<float2*>(o.rowp2);
+  float2* colp2 = reinterpret_cast<float2*>(o.colp2);
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
     double A = (a.u[i] + w) * kLog2e;
     if (a.rowshift) A = A + a.rowshift[i];
@@ -1427,12 +1455,20 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
     const float2 pp = rowp[i * ldp + blockIdx.x];  // read before this thread overwrites it
     s_M[i - r0] = pp.x != 0.f ? pp.y : -INFINITY;
     if (mode == 0) rowp[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.krow[i], A) : make_float2(0.f, 0.f);
+    if (fuse) {
+      double A2 = (o.u2[i] + w2) * kLog2e;
+      if (a.rowshift) A2 = A2 + a.rowshift[i];
+      s_A2[i - r0] = float(A2);
+      if (mode == 0) rowp2[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.kbar_row[i], A2) : make_float2(0.f, 0.f);
+    }
   }
   float2 cx[KP], cy[KP], cz[KP];
-  float dmax = -INFINITY, dmin = INFINITY;
+  float2 dd[KP];  // block v, K1'': d_j = B''_j - B'_j of the lane's columns
+  float dmax = -INFINITY, dmin = INFINITY, emax = -INFINITY, emin = INFINITY;
+  int ebad = 0;
 #pragma unroll
   for (int q = 0; q < KP; ++q) {
-    float b[2];
+    float b[2], e[2] = {0.f, 0.f};
     float4 y[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1449,6 +1485,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
           const float d = float(vv) - float(vs);
           dmax = fmaxf(dmax, d);
           dmin = fminf(dmin, d);
+          if (fuse) {
+            double v2 = o.v2[j] * kLog2e;
+            if (a.colshift) v2 = v2 + a.colshift[j];
+            e[h] = float(v2) - float(vv);
+            ebad |= !(fabsf(e[h]) < 1e30f);
+            emax = fmaxf(emax, e[h]);
+            emin = fminf(emin, e[h]);
+          }
         }
       }
       b[h] = float(vv);
@@ -1457,20 +1501,47 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
     cx[q] = make_float2(y[0].x, y[1].x);
     cy[q] = make_float2(y[0].y, y[1].y);
     cz[q] = make_float2(y[0].z, y[1].z);
+    dd[q] = make_float2(e[0], e[1]);
   }
   if (mode == 1) {
     dmax = warp_maxf(dmax);
     dmin = -warp_maxf(-dmin);
-    if (lane == 0) { s_dv[0][warp] = dmax; s_dv[1][warp] = dmin; }
+    if (fuse) {
+      emax = warp_maxf(emax);
+      emin = -warp_maxf(-emin);
+      ebad = __any_sync(0xffffffffu, ebad);
+    }
+    if (lane == 0) {
+      s_dv[0][warp] = dmax; s_dv[1][warp] = dmin;
+      s_dv[2][warp] = ebad ? NAN : emax; s_dv[3][warp] = emin;
+    }
     for (int c = threadIdx.x; c < kStrip; c += kThreads)  // the known column sums
-      if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = blockIdx.y == 0 ? encode_sum(o.kcol[j0 + c], 0.0) : make_float2(0.f, 0.f);
+      if (j0 + c < n) {
+        colp[(j0 + c) * gridDim.y + blockIdx.y] = blockIdx.y == 0 ? encode_sum(o.kcol[j0 + c], 0.0) : make_float2(0.f, 0.f);
+        if (fuse)
+          colp2[(j0 + c) * gridDim.y + blockIdx.y] =
+              blockIdx.y == 0 ? encode_sum(o.kbar_col[j0 + c], 0.0) : make_float2(0.f, 0.f);
+      }
   }
   __syncthreads();
-  float dvmax = -INFINITY, dvmin = INFINITY;
-  if (mode == 1)
-    for (int ww = 0; ww < kWarps; ++ww) { dvmax = fmaxf(dvmax, s_dv[0][ww]); dvmin = fminf(dvmin, s_dv[1][ww]); }
+  float dvmax = -INFINITY, dvmin = INFINITY, evmax = -INFINITY, evmin = INFINITY;
+  bool fuse_bad = false;
+  if (mode == 1) {
+    for (int ww = 0; ww < kWarps; ++ww) {
+      dvmax = fmaxf(dvmax, s_dv[0][ww]);
+      dvmin = fminf(dvmin, s_dv[1][ww]);
+      if (fuse) {
+        fuse_bad = fuse_bad || s_dv[2][ww] != s_dv[2][ww];
+        evmax = fmaxf(evmax, s_dv[2][ww]);
+        evmin = fminf(evmin, s_dv[3][ww]);
+      }
+    }
+    // an all-masked strip (evmax = -inf) has no entries: weights are unused
+    if (fuse && evmax > -INFINITY && !(evmax - evmin <= kOneSidedSpread)) fuse_bad = true;
+    if (!(evmax > -INFINITY)) evmax = 0.f;
+  }
   const bool exact = mode == 1 && !(dvmax - dvmin <= kOneSidedSpread);  // CTA-uniform
-  float mmax = -INFINITY;
+  float mmax = -INFINITY, mmax2 = -INFINITY;
   auto dots = [&](const float4& d, float2 (&t)[KP]) {
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
@@ -1480,11 +1551,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       t[q] = __ffma2_rn(make_float2(d.z, d.z), cz[q], x);
     }
   };
-  if (mode == 0) {  // block u: column sums of B' at the source's row-segment maxima
-    float2 cacc[KP];
+  if (mode == 0) {  // block u: column sums of B' (and of B(z_bar')) at the source's row-segment maxima
+    float2 cacc[KP], cacc2[KP];
 #pragma unroll
-    for (int q = 0; q < KP; ++q) cacc[q] = make_float2(0.f, 0.f);
-    float sigma = -INFINITY;
+    for (int q = 0; q < KP; ++q) cacc[q] = cacc2[q] = make_float2(0.f, 0.f);
+    float sigma = -INFINITY, sigma2 = -INFINITY;
     for (int64_t i = r0 + warp; i < r1; i += kWarps) {
       const float4 d = s_R[i - r0];
       const float m = s_M[i - r0];
@@ -1501,53 +1572,97 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       }
       const float f = ex2f(mA - sigma);
       const float2 F2 = make_float2(f, f);
+      if (fuse) {
+        const float mA2 = m + s_A2[i - r0];
+        mmax2 = fmaxf(mmax2, mA2);
+        if (mA2 > sigma2) {
+          const float sc = ex2f(sigma2 - mA2);
 #pragma unroll
-      for (int q = 0; q < KP; ++q) {
-        const float2 e = __fadd2_rn(t[q], make_float2(-m, -m));
-        cacc[q] = __ffma2_rn(make_float2(ex2f(e.x), ex2f(e.y)), F2, cacc[q]);
+          for (int q = 0; q < KP; ++q) cacc2[q] = __fmul2_rn(cacc2[q], make_float2(sc, sc));
+          sigma2 = mA2;
+        }
+        const float f2 = ex2f(mA2 - sigma2);
+        const float2 G2 = make_float2(f2, f2);
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 e = __fadd2_rn(t[q], make_float2(-m, -m));
+          const float2 x = make_float2(ex2f(e.x), ex2f(e.y));
+          cacc[q] = __ffma2_rn(x, F2, cacc[q]);
+          cacc2[q] = __ffma2_rn(x, G2, cacc2[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 e = __fadd2_rn(t[q], make_float2(-m, -m));
+          cacc[q] = __ffma2_rn(make_float2(ex2f(e.x), ex2f(e.y)), F2, cacc[q]);
+        }
       }
     }
-    __shared__ float cs[kWarps][kStrip];
-    __shared__ float ss[kWarps], mm[kWarps];
-    if (lane == 0) { ss[warp] = sigma; mm[warp] = mmax; }
+    // per-warp column sums: [2][kWarps][kStrip] floats in the (unused) row-sum tile area
+    float* cs = s_tiles;
+    float* cs2 = s_tiles + kWarps * kStrip;
+    __shared__ float ss[2][kWarps], mm[2][kWarps];
+    if (lane == 0) { ss[0][warp] = sigma; mm[0][warp] = mmax; ss[1][warp] = sigma2; mm[1][warp] = mmax2; }
     __syncthreads();
-    float sig = ss[0];
-    for (int ww = 1; ww < kWarps; ++ww) sig = fmaxf(sig, ss[ww]);
+    float sig = ss[0][0], sig2 = ss[1][0];
+    for (int ww = 1; ww < kWarps; ++ww) { sig = fmaxf(sig, ss[0][ww]); sig2 = fmaxf(sig2, ss[1][ww]); }
     const float fw = (sigma == -INFINITY) ? 0.f : ex2f(sigma - sig);
+    const float fw2 = (sigma2 == -INFINITY) ? 0.f : ex2f(sigma2 - sig2);
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
       const int c = 4 * lane + 128 * (q >> 1) + 2 * (q & 1);
-      cs[warp][c] = cacc[q].x * fw;
-      cs[warp][c + 1] = cacc[q].y * fw;
+      cs[warp * kStrip + c] = cacc[q].x * fw;
+      cs[warp * kStrip + c + 1] = cacc[q].y * fw;
+      if (fuse) {
+        cs2[warp * kStrip + c] = cacc2[q].x * fw2;
+        cs2[warp * kStrip + c + 1] = cacc2[q].y * fw2;
+      }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < kStrip; c += kThreads) {
-      float sc = 0.f;
+      float sc = 0.f, sc2 = 0.f;
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) sc += cs[ww][c];
-      if (j0 + c < n) colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : sc, sig == -INFINITY ? 0.f : sig);
+      for (int ww = 0; ww < kWarps; ++ww) { sc += cs[ww * kStrip + c]; sc2 += cs2[ww * kStrip + c]; }
+      if (j0 + c < n) {
+        colp[(j0 + c) * gridDim.y + blockIdx.y] = make_float2(sig == -INFINITY ? 0.f : sc, sig == -INFINITY ? 0.f : sig);
+        if (fuse)
+          colp2[(j0 + c) * gridDim.y + blockIdx.y] =
+              make_float2(sig2 == -INFINITY ? 0.f : sc2, sig2 == -INFINITY ? 0.f : sig2);
+      }
     }
     if (threadIdx.x == 0) {
-      float m = mm[0];
-      for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm[ww]);
+      float m = mm[0][0], m2 = mm[1][0];
+      for (int ww = 1; ww < kWarps; ++ww) { m = fmaxf(m, mm[0][ww]); m2 = fmaxf(m2, mm[1][ww]); }
       a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+      if (fuse) o.maxp2[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m2) * kLn2;  // exact
     }
     return;
   }
-  // block v: row sums of B' at the source's segment maxima + the strip's largest change
-  float* tile = reinterpret_cast<float*>(s_R + a.rows_per_cta) + warp * (32 * 33);
-  float* tslot = tile + lane;
-  float my_ms = 0.f;
+  // block v: row sums of B' at the source's segment maxima + the strip's largest change;
+  // K1'': row sums of B(z_bar') = sum_j B'_ij 2^(d_j), weights 2^(d_j - dmax) <= 1.
+  // Rows are flushed every 16: the tile holds [sum][16 rows][33] per warp, lane l < 16
+  // reduces row l of B', lane 16 + l row l of B(z_bar').
+  float2 gw[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q)
+    gw[q] = fuse ? make_float2(ex2f(dd[q].x - evmax), ex2f(dd[q].y - evmax)) : make_float2(0.f, 0.f);
+  float* tile = s_tiles + warp * (32 * 33);
+  constexpr int kSlotRows = 16;
   int slot = 0;
+  float my_ms = 0.f;
   int64_t ib = r0 + warp;
   auto flush = [&](int cnt) {
     __syncwarp();
-    if (lane < cnt) {
-      const float* rowv = tile + lane * 33;
+    const int h = lane >> 4, r = lane & 15;
+    if (r < cnt && (h == 0 || fuse)) {
+      const float* rowv = tile + (h * kSlotRows + r) * 33;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; k += 4) { s0 += rowv[k]; s1 += rowv[k + 1]; s2 += rowv[k + 2]; s3 += rowv[k + 3]; }
-      rowp[(ib + int64_t(kWarps) * lane) * ldp + blockIdx.x] = make_float2((s0 + s1) + (s2 + s3), my_ms);
+      const int64_t row = ib + int64_t(kWarps) * r;
+      const float S = (s0 + s1) + (s2 + s3);
+      if (h == 0) rowp[row * ldp + blockIdx.x] = make_float2(S, my_ms);
+      else rowp2[row * ldp + blockIdx.x] = make_float2(S, my_ms + evmax);
     }
     __syncwarp();
   };
@@ -1565,25 +1680,40 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       const float2 e = __fadd2_rn(t[q], make_float2(-ms, -ms));
       t[q] = make_float2(ex2f(e.x), ex2f(e.y));
     }
-    *tslot = tree_sum2<KP>(t);
-    tslot += 33;
-    if (lane == slot) my_ms = ms;
-    if (++slot == 32) {
-      flush(32);
+    tile[slot * 33 + lane] = tree_sum2<KP>(t);
+    if (fuse) {
+      mmax2 = fmaxf(mmax2, lm + s_A2[i - r0]);
+      float2 p[KP];
+#pragma unroll
+      for (int q = 0; q < KP; ++q) p[q] = __fmul2_rn(t[q], gw[q]);
+      tile[(kSlotRows + slot) * 33 + lane] = tree_sum2<KP>(p);
+    }
+    if ((lane & 15) == slot) my_ms = ms;
+    if (++slot == kSlotRows) {
+      flush(kSlotRows);
       slot = 0;
-      tslot = tile + lane;
       ib = i + kWarps;
     }
   }
   if (slot > 0) flush(slot);
   mmax = warp_maxf(mmax);
-  __shared__ float mm1[kWarps];
-  if (lane == 0) mm1[warp] = mmax;
+  if (fuse) mmax2 = warp_maxf(mmax2);
+  __shared__ float mm1[2][kWarps];
+  if (lane == 0) { mm1[0][warp] = mmax; mm1[1][warp] = mmax2; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    float m = mm1[0];
-    for (int ww = 1; ww < kWarps; ++ww) m = fmaxf(m, mm1[ww]);
+    float m = mm1[0][0], m2 = mm1[1][0];
+    for (int ww = 1; ww < kWarps; ++ww) { m = fmaxf(m, mm1[0][ww]); m2 = fmaxf(m2, mm1[1][ww]); }
     a.maxp[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = double(m) * kLn2;
+    if (fuse) {
+      // upper bound of z_bar''s max exponent (natural units); the exact one
+      // only matters at the overflow threshold: near it, z_bar is re-swept
+      const double ub = (double(m2) + double(evmax)) * kLn2;
+      if (fuse_bad || ub != ub || ub > kMaxExponent - 16.0) *o.bad = 1;
+      o.maxp2[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = ub;
+    }
+  } else if (fuse_bad && threadIdx.x == 32) {
+    *o.bad = 1;
   }
 }
 
