@@ -59,9 +59,12 @@ struct AspotCtl {
   int g_new_one, g_new_eval, one_sided_ok;
   int clamp_guard;  // fp64 (Eigen-clamped exp) problems: scale only far above the clamp floor
   // K1'' (sweep.cuh sweep_pts1_f32): the one-sided pass of z_check' also formed
-  // the next z_bar's partials (stash); fuse_ok: the problem allows it;
-  // g_bar_sweep: this attempt sweeps z_bar (= g_new unless stashed)
+  // the next z_bar's partials (g_bar_stash = 1), or z_check''s block was w and
+  // z_bar's sums are z_best's scaled (= 2, sums in kbar, max exponent bar_maxe);
+  // fuse_ok: the problem allows it; g_bar_sweep: this attempt sweeps z_bar
+  // (= g_new unless stashed)
   int fuse_ok, g_bar_stash, g_bar_sweep, pad_k1;
+  double bar_maxe;
   int64_t pause_at;
   int64_t loop_budget;  // attempts the device loop (graph WHILE node) may still run in this launch
   int64_t n, t, gk_calls, max_iterations, log_every, attempts, sweeps;
@@ -116,10 +119,12 @@ struct ReduceArgs {
   const double* src_row_a; const double* src_col_a; const double* src_w_a; int src_role_a;
   const double* src_row_b; const double* src_col_b; const double* src_w_b; int src_role_b;
   const int* select_b;
-  // K1'': when *alt_sel, the partials come from the stash the previous
-  // attempt's one-sided pass wrote (same layout)
+  // K1'': when *alt_sel == 1, the partials come from the stash the previous
+  // attempt's one-sided pass wrote (same layout); == 2: the sums themselves
+  // (direct_row / direct_col) and the max exponent (ctl->bar_maxe)
   const int* alt_sel;
   const double* rowp_alt; const double* colp_alt; const double* maxp_alt;
+  const double* direct_row; const double* direct_col;
   // deferred decision: write this launch's block partials to scratch and
   // stop; the next O(n) kernel of the attempt reduces them and decides
   // (decide_pending), so no block waits on a ticket here
@@ -352,7 +357,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
   const double* scol = useb ? a.src_col_b : a.src_col_a;
   const double dw = a.mode == 1 ? w - *(useb ? a.src_w_b : a.src_w_a) : 0.0;
   const double fs = a.mode == 1 ? exp(dw) : 1.0;
-  const bool alt = a.alt_sel && *a.alt_sel;
+  const int alt_mode = a.alt_sel ? *a.alt_sel : 0;
+  const bool alt = alt_mode == 1, direct = alt_mode == 2;
   const double* rowp = alt ? a.rowp_alt : a.rowp;
   const double* colp = alt ? a.colp_alt : a.colp;
   const double* maxp = alt ? a.maxp_alt : a.maxp;
@@ -363,7 +369,10 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     const int64_t ii = live ? i : n - 1;
     const double ui = u[ii], vi = v[ii];
     double rb, cb;
-    if (a.mode == 0) {
+    if (direct) {
+      rb = a.direct_row[ii];
+      cb = a.direct_col[ii];
+    } else if (a.mode == 0) {
       double off = (ui + w) * kLog2e;
       if (a.rowshift) off = off + a.rowshift[ii];
       rb = group_partial_sum<kTPI>(rowp, ii * a.nstrips, a.nstrips, a.pfmt, off, q);
@@ -377,9 +386,12 @@ __global__ void __launch_bounds__(kEvalThreads) k_point_eval(AspotCtl* ctl, int 
     a.col_out[i] = cb;
     add_index_terms(acc, rb, cb, ui, vi, a.rt[i], a.ct[i]);
   }
-  if (a.mode == 0)
+  if (direct) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) acc[11] = __ldcg(&ctl->bar_maxe);
+  } else if (a.mode == 0) {
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < a.nmax; k += int64_t(gridDim.x) * blockDim.x)
       acc[11] = nan_max(acc[11], maxp[k]);
+  }
   // block reduction: warp shuffles, then the kEvalThreads / 32 warp results
   __shared__ double sh[kNumAcc][kEvalThreads / 32];
   __shared__ bool last;
@@ -622,8 +634,20 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
     }
     const int64_t n = src.n;
     bool finite = true;
-    const bool k1 = which == 1 && c->g_new_one && c->fuse_ok && bs.zbn.base;
     const double th = theta_next_d(c->theta), om = 1.0 - th;
+    const bool k1 = which == 1 && c->g_new_one && c->fuse_ok && bs.zbn.base;
+    // block w: B(z_bar') = B(z_best) e^(w' - w_best), z_bar's sums without any pass
+    const bool k1w = which == 1 && c->g_new_scaled && c->fuse_ok && bs.zbn.base;
+    double fbar = 0.0;
+    if (k1w) {
+      const double ws = *src.w();
+      const double wd = ws + (log(c->s) - log(c->ps[role].total));  // = dst.w
+      const double za = om * wd;
+      const double zb2 = th * ws;
+      const double dwb = (za + zb2) - ws;  // k_commit's z_bar w
+      fbar = exp(dwb);
+      if (threadIdx.x == 0) c->bar_maxe = c->ps[role].maxe + dwb;  // every block's copy agrees
+    }
     for (int64_t k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * n + 1; k += int64_t(gridDim.x) * blockDim.x) {
       double x = src.base[k];
       if (k < n) {
@@ -638,6 +662,10 @@ __global__ void k_gk_update(AspotCtl* ctl, int which, Slot src_a, const double* 
       if (which == 1 && c->g_new_one) {  // the side of z_check' that only rescales: B' = B e^(x' - x)
         if (k < n && block == 0) dst_row[k] = rowb[k] * exp(x - src.base[k]);
         else if (k >= n && k < 2 * n && block == 1) dst_col[k - n] = colb[k - n] * exp(x - src.base[k]);
+      }
+      if (k1w) {
+        if (k < n) bs.row[k] = rowb[k] * fbar;
+        else if (k < 2 * n) bs.col[k - n] = colb[k - n] * fbar;
       }
       if (k1) {  // z_bar' and its rescaled side (k_commit: a = om z_check', b = th z_best, z_bar = a + b)
         const double za = om * x;
@@ -844,7 +872,7 @@ __global__ void k_commit(AspotCtl* ctl, Slot z, Slot zc, Slot zh, Slot zn, Slot 
     // K1'': the fused pass of this attempt's z_check' left the next z_bar's partials
     const int bad = stash_bad ? __ldcg(stash_bad) : 1;
     if (stash_bad) *stash_bad = 0;
-    cc->g_bar_stash = cc->attempt_ok && cc->fuse_ok && cc->g_new_one && !bad;
+    cc->g_bar_stash = !(cc->attempt_ok && cc->fuse_ok) ? 0 : (cc->g_new_one && !bad) ? 1 : cc->g_new_scaled ? 2 : 0;
     commit_state(cc, trace, lg);
     if (in_loop) {
       cc->loop_budget -= 1;

@@ -486,6 +486,8 @@ inline void launch_eval(Context& cx, Workspace& ws, const SweepOut& so, Slot z, 
     r.rowp_alt = ws.rowp2.p;
     r.colp_alt = ws.colp2.p;
     r.maxp_alt = ws.maxp2.p;
+    r.direct_row = ws.kbar.p;
+    r.direct_col = ws.kbar.p + ws.n;
   }
   switch (ws.eval_tpi) {
     case 1: launch_k(k_point_eval<1>, dim3(ws.eval_blocks), dim3(kEvalThreads), 0, cx.stream, ws.ctl.p, role, r, ws.ticket.p); break;

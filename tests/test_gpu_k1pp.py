@@ -1,0 +1,94 @@
+"""K1'' on the points path (sweep.cuh sweep_pts1_f32 + the z_bar stash,
+aspot_kernels.cuh): the one-sided z_check' pass also forms the next z_bar's
+partials, or z_bar's sums are z_best's scaled when z_check''s block is w.
+Against the same solve with the stash off ($POTGPU_K1PP=0: z_bar swept every
+iteration) and with the one-sided pass off too ($POTGPU_ONE_SIDED=0: full
+sweeps), at the headline config (C3, n = 16384) to convergence and at C4
+(n = 65536) over a prefix: the same decisions, per-iteration E_t / phi to
+fp32 summation-order noise, the converged objective within the fp32 bar,
+and the sweep count the design promises (2 per iteration at C3 instead of 3).
+Reference: the z_bar of the next iteration, solvers.hpp:336-337."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SNIPPET = r"""
+import json, sys
+sys.path.insert(0, %r)
+from paper_2601_17196_b200 import pot
+cfg_id, n, iters, eps = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), float(sys.argv[4])
+inst = pot.config_instance(cfg_id, n=n)
+cfg = pot.SolverConfig(epsilon=eps, log_every=10 ** 9, max_iterations=iters or 10 ** 6, record_rounded_cost=False,
+                       materialize_plan=False, collect_iter_log=True)
+r = pot.aspot_solve(inst, cfg, iter_log_cap=100000)
+print(json.dumps({"status": int(r.status), "iterations": r.iterations, "cost": r.cost, "gap": r.feasibility_gap,
+                  "sweeps": r.sweeps, "log": r.iter_log.tolist()}))
+""" % ROOT
+
+_cache = {}
+
+
+def run(env_extra, *args):
+    key = (tuple(sorted(env_extra.items())), args)
+    if key not in _cache:
+        env = dict(os.environ)
+        env.update(env_extra)
+        r = subprocess.run([sys.executable, "-c", SNIPPET] + [str(a) for a in args], env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        d["log"] = np.array(d["log"])
+        _cache[key] = d
+    return _cache[key]
+
+
+VARIANTS = [{"POTGPU_K1PP": "0"}, {"POTGPU_ONE_SIDED": "0"}]
+
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_c3_converged_solve_matches_unfused(env):
+    args = (3, 16384, 0, 1e-2)
+    a, b = run({}, *args), run(env, *args)
+    assert a["status"] == b["status"] == 0  # Converged
+    assert abs(a["iterations"] - b["iterations"]) <= 0.01 * b["iterations"]
+    assert abs(a["cost"] - b["cost"]) <= 1e-4 * abs(b["cost"])
+    assert a["gap"] <= 1e-5
+    # the same decisions (block of z_hat, z_best, block of z_check') on the common prefix
+    k = min(len(a["log"]), len(b["log"]), 200)
+    assert np.array_equal(a["log"][:k, 2:5], b["log"][:k, 2:5])
+    # phi(z_check), phi(z_hat): fp32 summation-order noise only; E_t (an l1
+    # norm of marginal residuals, cancellation-prone) to the fp32 bar
+    np.testing.assert_allclose(a["log"][:k, 6:8], b["log"][:k, 6:8], rtol=1e-5)
+    np.testing.assert_allclose(a["log"][:k, 5], b["log"][:k, 5], rtol=1e-4)
+
+
+def test_c3_sweeps_per_iteration():
+    a = run({}, 3, 16384, 0, 1e-2)
+    b = run({"POTGPU_K1PP": "0"}, 3, 16384, 0, 1e-2)
+    lg = a["log"]
+    # z_check' one-sided (block u or v from z_hat) on almost every iteration at C3
+    one = np.sum((lg[:, 4] != 2) & (lg[:, 3] == 0))
+    assert one >= 0.9 * len(lg)
+    # every such iteration spares the next z_bar's sweep
+    assert a["sweeps"] <= b["sweeps"] - one + 2
+    assert a["sweeps"] <= 2.05 * a["iterations"] + 2
+
+
+def test_c4_prefix_matches_unfused():
+    """C4 exercises the block-w stash too (z_check''s block is w in ~1/3 of its iterations)."""
+    a = run({}, 4, 65536, 60, 1e-3)
+    b = run({"POTGPU_K1PP": "0"}, 4, 65536, 60, 1e-3)
+    assert a["iterations"] == b["iterations"] == 60
+    assert np.array_equal(a["log"][:, 2:5], b["log"][:, 2:5])
+    assert np.any(a["log"][:, 4] == 2) and np.any(a["log"][:, 4] != 2)
+    np.testing.assert_allclose(a["log"][:, 6:8], b["log"][:, 6:8], rtol=1e-5)
+    np.testing.assert_allclose(a["log"][:, 5], b["log"][:, 5], rtol=1e-4)
+    assert abs(a["cost"] - b["cost"]) <= 1e-4 * abs(b["cost"])
+    assert a["sweeps"] < b["sweeps"]
