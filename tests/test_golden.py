@@ -52,3 +52,16 @@ def test_oracle_reference_kats():
         C, _, _, _ = scalar(e["c0"])
         rc = binding.sweep(C, e["gamma"], np.array([e["u"]]), np.array([e["v"]]), e["w"])[0]
         assert rc != 0, e["cite"]
+
+
+def test_headline_fixtures_match_their_instances():
+    """tests/golden/headline.json (the oracle's answers at n = 65536, read by
+    the GPU parity tests instead of a 9-minute oracle run): every entry's
+    digest is the digest of the instance the recipe builds today."""
+    from tests import headline_golden
+    from paper_2601_17196_b200 import pot
+    inst = pot.config_instance(4)
+    a = headline_golden.load("c4_aspot_prefix", inst.X, inst.Y, inst.r, inst.c, [inst.s])
+    assert a.iterations == 3 and a.log.shape == (3, 9) and a.scale > 0
+    t = headline_golden.load("c4_tuned_prefix", inst.X, inst.Y, inst.r, inst.c, [inst.s])
+    assert t.iterations == 1 and [int(x) for x in t.trace[:, 0]] == [0, 1]

@@ -8,7 +8,9 @@ pinned to the CPU oracle (points mode, all host threads) by a 20-iteration
 prefix with identical decisions; the fp32 solve is then compared with the
 anchor at convergence on north_star's fp32 bars (objective 1e-4, violation
 1e-5) plus the iteration count. configs[3] (n = 65536) gets a 3-iteration
-ASPOT prefix against the oracle in points mode.
+ASPOT prefix against the oracle in points mode (the oracle's answer is a
+committed fixture, tests/golden/headline.json; $POTGPU_LIVE_ORACLE=1 runs the
+oracle itself, ~9 min).
 
 Measured on B200 (profiles/c3_anchor.py, profiles/r02/c3_anchor.jsonl): both
 C3 solves converge in 2360 iterations; one decision differs (iteration 2, a
@@ -20,6 +22,7 @@ import numpy as np
 import pytest
 
 from oracle import binding
+from tests import headline_golden
 from paper_2601_17196_b200 import pot
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -91,8 +94,12 @@ def test_c4_aspot_prefix_matches_oracle(ctx):
     c = pot.SolverConfig(epsilon=1e-3, log_every=10 ** 9, max_iterations=3, collect_iter_log=True,
                          materialize_plan=False, record_rounded_cost=False)
     g = pot.aspot_solve(inst, c, ctx=ctx, iter_log_cap=10)
-    o = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=1e-3,
-                      max_iterations=3, skip_plan=True)
+    if headline_golden.live():  # ~9 min on 16 cores
+        o = binding.solve(0, inst.r, inst.c, inst.s, X=inst.X, Y=inst.Y, scale=inst.cost_scale, epsilon=1e-3,
+                          max_iterations=3, skip_plan=True)
+    else:  # the same call's result, committed (tests/golden/make_headline_golden.py)
+        o = headline_golden.load("c4_aspot_prefix", inst.X, inst.Y, inst.r, inst.c, [inst.s])
+        assert o.scale == inst.cost_scale
     assert g.iterations == o.iterations == 3
     assert g.gamma == o.gamma and g.tolerance == o.tolerance
     diff = np.flatnonzero((g.iter_log[:, 1:5] != o.log[:, 1:5]).any(axis=1))

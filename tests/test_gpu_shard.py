@@ -136,20 +136,41 @@ def test_sharded_sinkhorn_matches_oracle(kind, shards, nccl):
 
 @pytest.mark.parametrize("kind", [pot.SolverKind.Aspot, pot.SolverKind.TunedSinkhorn])
 def test_sharded_fp32_points_matches_unsharded(ctx, kind):
-    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one,
-    on north_star's fp32 objective bar. The fp32 column sums are
-    reassociated by sharding; measured on B200 for seeds 1-4
-    (tools/shard_meas.py, profiles/r02/shard_meas.jsonl): the same stopping
-    iteration and rounded costs within 5.3e-5 relative (2 and 4 shards)."""
+    """configs[2] shape at n = 2048 (fp32, on-the-fly cost), 4 shards vs one.
+    The fp32 column sums are reassociated by sharding, and the unsharded
+    default also takes the one-sided / K1'' passes the sharded path does not.
+    Late in the solve the greedy Greenkhorn block choice (solvers.hpp:54-69)
+    cycles through near-ties of its rho-scores; fp32 noise can delay one choice
+    by an iteration, after which two solves stay one iteration out of phase:
+    E_t and the rounded cost oscillate with that phase (E_t by ~20 %, the cost
+    by ~0.3 %), the dual objective does not. Measured on B200
+    (tools/k1pp_small.py, tools/k1pp_logs.py, profiles/r02/k1pp_small_2048.jsonl):
+    the default stops at 1851, the sharded, unfused and fp64 oracle solves at
+    1846; phi agrees to 7e-7 at EVERY iteration across all of them; solves
+    that stay in phase agree in cost to 5e-5 (profiles/r02/shard_meas.jsonl).
+    So: iteration counts within 2 %, phi at equal iteration counts to 1e-6,
+    the cost to the fp32 bar when the stops coincide and to 5e-3 otherwise."""
     inst = pot.config_instance(3, n=2048)
     p = 4.0 if kind == pot.SolverKind.TunedSinkhorn else 1.0
-    cfg = pot.SolverConfig(epsilon=1e-2, tuning_exponent_p=p, log_every=10 ** 9, materialize_plan=False)
-    a = pot.solve(inst, kind, cfg, ctx=ctx)
-    b = pot.solve(inst, kind, cfg, ctx=sctx(4))
+
+    def cfg(cap=10 ** 6):
+        return pot.SolverConfig(epsilon=1e-2, tuning_exponent_p=p, log_every=10 ** 9, materialize_plan=False,
+                                max_iterations=cap)
+    a = pot.solve(inst, kind, cfg(), ctx=ctx)
+    b = pot.solve(inst, kind, cfg(), ctx=sctx(4))
     assert a.status == b.status == pot.SolveStatus.Converged
     assert abs(a.iterations - b.iterations) <= max(2, 0.02 * a.iterations)
-    assert abs(a.cost - b.cost) <= TOL_F32_OBJ * abs(a.cost)
     assert b.feasibility_gap <= TOL_F32_VIOL and abs(b.plan.mass - inst.s) <= TOL_F32_VIOL
+    if a.iterations == b.iterations:
+        assert abs(a.cost - b.cost) <= TOL_F32_OBJ * abs(a.cost)
+    else:  # the iterate of the earlier stop, on both paths
+        k = min(a.iterations, b.iterations)
+        a = pot.solve(inst, kind, cfg(k), ctx=ctx)
+        b = pot.solve(inst, kind, cfg(k), ctx=sctx(4))
+        assert a.iterations == b.iterations == k
+        assert abs(a.cost - b.cost) <= 5e-3 * abs(a.cost)
+    if kind == pot.SolverKind.Aspot:
+        assert abs(a.phi - b.phi) <= 1e-6 * abs(a.phi)
 
 
 def test_sharded_fp32_aspot_prefix_trajectory(ctx):
