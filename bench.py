@@ -281,6 +281,14 @@ def main():
     sweeps_per_it = (s1 - s0) / max(done, 1)
     # roofline of the dominant kernel (the on-the-fly sweep): MUFU ex2 bound
     ms_sweep, elems, _ = sess.time_sweep(20)
+    # the other n^2 pass of an iteration: the one-sided z_check' pass fused with
+    # the next z_bar (K1''), for both Greenkhorn blocks (single GPU only)
+    ms_one = None
+    if world == 1:
+        try:
+            ms_one = {"u": sess.time_one_sided(0, 10), "v": sess.time_one_sided(1, 10)}
+        except pot.PotError:
+            ms_one = None
     clocks = clk.summary()
     sess.close()
 
@@ -355,6 +363,14 @@ def main():
                 "traffic": traffic("sweep_points"), "kernel": "sweep_pts2_f32 (points, 2 rows x 16 columns per warp step)", "ms_per_launch": ms_sweep,
                 "per_unit": "1 MUFU.EX2 per plan entry; n^2 entries per launch",
                 "peak_source": f"16 ex2/clk/SM x {nsm} SMs x median SM clock {sm_mhz} MHz under load"}
+    one_sided = None
+    if ms_one:
+        one_sided = {"bound": "mufu", "peak": mufu_peak, "unit": "Gex2/s", "traffic": traffic("sweep_pts1"),
+                     "kernel": "sweep_pts1_f32 (one-sided z_check' pass fused with the next z_bar, K1'')",
+                     "per_unit": "1 MUFU.EX2 per plan entry; n^2 entries per launch",
+                     "ms_per_launch": ms_one,
+                     "achieved": {b: elems / (ms * 1e-3) / 1e9 for b, ms in ms_one.items()},
+                     "frac": {b: elems / (ms * 1e-3) / 1e9 / mufu_peak for b, ms in ms_one.items()}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         w = workload_points(args, product=False)
@@ -369,7 +385,7 @@ def main():
                         "note": "one public-API call (aspot_solve, max_iterations=K) from host buffers: upload, setup, "
                                 "K iterations, rounding, download"},
                 "gpu_launches": k1 - k0, "sweeps_per_iteration": sweeps_per_it,
-                "roofline": roofline, "roofline_stored": stored, "time_to_eps": tte, "tuned_sinkhorn_time_to_eps": tuned,
+                "roofline": roofline, "roofline_one_sided": one_sided, "roofline_stored": stored, "time_to_eps": tte, "tuned_sinkhorn_time_to_eps": tuned,
                 "cpu_baseline": cpu}
         print(json.dumps(line))
     if dist is not None:

@@ -221,6 +221,13 @@ int potgpu_session_destroy(potgpu_session* s);
  * on the session stream), with the algorithmic elements (n^2 exponentials)
  * and HBM bytes (stored cost only) of one launch. */
 int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep, double* elements, double* bytes);
+/* Roofline probe of the accelerated solver's one-sided pass (fp32 on-the-fly
+ * cost: z_check' when its Greenkhorn block is u (block = 0) or v (block = 1),
+ * fused with the next z_bar when the session runs K1''; reference points:
+ * solvers.hpp:345 and :337). Average device time of one launch at the
+ * current z_check (n^2 exponentials). The session cannot iterate afterwards.
+ * POTGPU_ERR_UNSUPPORTED for any other solver or cost representation. */
+int potgpu_session_time_one_sided(potgpu_session* s, int reps, int block, double* ms_per_pass);
 /* The accelerated solver's state after the last accepted iteration, for
  * the reference's AspotObserver (solvers.hpp:188-204, 364-367): point
  * which = 0 z_best, 1 z_check, 2 z_hat, 3 z_grave (u, v: n doubles; w: 1;

@@ -515,6 +515,10 @@ struct Session {
   // average device time (ms) of one hot-path sweep launch; algorithmic
   // elements and HBM bytes that launch must touch
   virtual double time_sweep(int reps, double* elems, double* bytes) = 0;
+  // average device time (ms) of one one-sided pass (block 0 = u, 1 = v) at the current z_check
+  virtual double time_one_sided(int, int) {
+    throw Error(POTGPU_ERR_UNSUPPORTED, "the one-sided pass exists for fp32 on-the-fly ASPOT only");
+  }
   virtual void stats(int64_t* attempts, int64_t* sweeps) = 0;
   // for drivers that consume the plan themselves (registration): the
   // rounding of the stopping iterate, the point its implicit plan is built
@@ -825,6 +829,7 @@ struct AspotSession : Session {
 
   void iterate(int64_t k, double* ms, int64_t* iters, int* finished) override {
     AspotCtl& h = *ws.host_ctl;
+    if (probed) throw Error(POTGPU_INVALID_ARGUMENT, "time_one_sided clobbered the pass buffers: no iterate() after it");
     if (trivial || (!h.g_active && !h.paused)) {
       if (ms) *ms = 0.0;
       if (iters) *iters = 0;
@@ -910,6 +915,41 @@ struct AspotSession : Session {
     if (elems) *elems = double(rows) * n;
     if (bytes) *bytes = double(rows) * n * stream_bytes_per_elem(P);
     return double(f) / reps;
+  }
+
+  // Roofline probe of the one-sided pass (sweep_pts1_f32, with the K1''
+  // accumulation when the session runs it): z_check' := z_check, source :=
+  // z_check. Each timed launch follows an untimed full sweep of z_check, which
+  // leaves the row-segment maxima the pass shifts by (the pass overwrites
+  // them). The stash and partial buffers are clobbered: no iterate() after.
+  bool probed = false;
+  double time_one_sided(int reps, int block) override {
+    if (trivial || !one_sided || (block != 0 && block != 1))
+      throw Error(POTGPU_ERR_UNSUPPORTED, "the one-sided pass exists for fp32 on-the-fly ASPOT only (block 0 or 1)");
+    probed = true;
+    const Slot ZC = ws.slot(S_ZC);
+    DevBuf<int> blk;
+    blk.alloc(1);
+    PG_CK(cudaMemcpyAsync(blk.p, &block, sizeof(int), cudaMemcpyHostToDevice, cx.stream));
+    OneSidedArgs o{ws.row(R_CHECK), ws.col(R_CHECK), ZC.v(), blk.p};
+    if (k1pp) {
+      o.u2 = ZC.u(); o.v2 = ZC.v(); o.w2 = ZC.w();
+      o.kbar_row = ws.row(R_CHECK); o.kbar_col = ws.col(R_CHECK);
+      o.rowp2 = ws.rowp2.p; o.colp2 = ws.colp2.p; o.maxp2 = ws.maxp2.p;
+      o.bad = ws.stash_bad.p;
+    }
+    double total = 0.0;
+    for (int k = 0; k <= reps; ++k) {  // k = 0: warm
+      launch_local_sweeps(cx, P, ws, ZC, gamma);
+      PG_CK(cudaEventRecord(ev0, cx.stream));
+      launch_one_sided(cx, P, ws, ZC, nullptr, o);
+      PG_CK(cudaEventRecord(ev1, cx.stream));
+      PG_CK(cudaEventSynchronize(ev1));
+      float f = 0.f;
+      PG_CK(cudaEventElapsedTime(&f, ev0, ev1));
+      if (k > 0) total += double(f);
+    }
+    return total / reps;
   }
 
   void finish(potgpu_summary* sm, potgpu_outputs* out) override {
@@ -1567,6 +1607,14 @@ int potgpu_session_time_sweep(potgpu_session* s, int reps, double* ms_per_sweep,
     if (!s || reps < 1) throw Error(POTGPU_INVALID_ARGUMENT, "null session or reps < 1");
     const double ms = reinterpret_cast<Session*>(s)->time_sweep(reps, elements, bytes);
     if (ms_per_sweep) *ms_per_sweep = ms;
+  });
+}
+
+int potgpu_session_time_one_sided(potgpu_session* s, int reps, int block, double* ms_per_pass) {
+  return guarded([&] {
+    if (!s || reps < 1) throw Error(POTGPU_INVALID_ARGUMENT, "null session or reps < 1");
+    const double ms = reinterpret_cast<Session*>(s)->time_one_sided(reps, block);
+    if (ms_per_pass) *ms_per_pass = ms;
   });
 }
 

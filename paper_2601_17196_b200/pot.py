@@ -164,7 +164,7 @@ EXPORTED_SYMBOLS = (
     "potgpu_abi_version", "potgpu_last_error", "potgpu_config_default", "potgpu_create", "potgpu_destroy",
     "potgpu_solve", "potgpu_dual_eval", "potgpu_round_pot", "potgpu_comm_unique_id", "potgpu_comm_init",
     "potgpu_make_synthetic", "potgpu_make_config", "potgpu_session_begin", "potgpu_session_iterate",
-    "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep",
+    "potgpu_session_finish", "potgpu_session_destroy", "potgpu_ctx_stream", "potgpu_session_time_sweep", "potgpu_session_time_one_sided",
     "potgpu_session_stats", "potgpu_solve_batched", "potgpu_comm_init_local", "potgpu_comm_info",
     "potgpu_release_cached_memory", "potgpu_reg_config_default", "potgpu_register_point_clouds", "potgpu_fit_rigid",
     "potgpu_kmeans_quantize", "potgpu_round_balanced", "potgpu_dual_matrix", "potgpu_session_read_state",
@@ -198,6 +198,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.potgpu_ctx_stream.argtypes = [ctypes.c_void_p]
     lib.potgpu_ctx_stream.restype = ctypes.c_void_p
     lib.potgpu_session_time_sweep.argtypes = [ctypes.c_void_p, ctypes.c_int, dp, dp, dp]
+    lib.potgpu_session_time_one_sided.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, dp]
     lib.potgpu_solve_batched.argtypes = [ctypes.c_void_p, ctypes.c_int, P(_Problem), ctypes.c_int64, P(_Config),
                                          P(_Summary), P(_Outputs), ctypes.c_int]
     lib.potgpu_session_stats.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_int64)]
@@ -665,6 +666,13 @@ class Session:
         ms, el, by = np.zeros(1), np.zeros(1), np.zeros(1)
         _check(self.lib.potgpu_session_time_sweep(self._h, int(reps), _dp(ms), _dp(el), _dp(by)))
         return float(ms[0]), float(el[0]), float(by[0])
+
+    def time_one_sided(self, block: int, reps: int = 10) -> float:
+        """ms per launch of the one-sided pass (block 0 = u, 1 = v; fused with
+        the next z_bar under K1'') at the current z_check. No iterate() after."""
+        ms = np.zeros(1)
+        _check(self.lib.potgpu_session_time_one_sided(self._h, int(reps), int(block), _dp(ms)))
+        return float(ms[0])
 
     def carry_stats(self):
         """(carried, exact): CTAs of the fp32 points sweep that used a carried

@@ -24,6 +24,11 @@ $NCU $FULL -k "regex:sweep_pts" -o $OUT/sweep_points -f \
   python tools/profile_sweep.py --config 3 > $OUT/ncu_points.log 2>&1; echo "points rc=$?"
 $NCU $FULL -k "regex:sweep_f32" -o $OUT/sweep_stored -f \
   python tools/profile_sweep.py --config 3 --stored > $OUT/ncu_stored.log 2>&1; echo "stored rc=$?"
+# the fused one-sided pass (z_check' + the next z_bar, K1''): launches inside the loop; the
+# summariser keeps the longest (the gated early-exit launches are a few us)
+$NCU --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:sweep_pts1" --launch-skip 4 --launch-count 6 -o $OUT/sweep_pts1 -f \
+  python bench.py --steps 6 --warmup 6 --no-tte --no-cpu > $OUT/ncu_pts1.log 2>&1; echo "pts1 rc=$?"
 $NCU --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k "regex:k_point_eval" --launch-skip 20 --launch-count 1 -o $OUT/point_eval -f \
   python bench.py --steps 3 --warmup 3 --no-tte --no-cpu > $OUT/ncu_eval.log 2>&1; echo "eval rc=$?"

@@ -38,7 +38,10 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "ns"
 def summarize(rep):
     raw = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, data = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    # several launches in one report: keep the longest (gated early-exit launches are a few us)
+    di = hdr.index("gpu__time_duration.sum")
+    data = max(rows[2:], key=lambda r: float(r[di].replace(",", "")) * UNIT_SCALE.get(units[di], 1) if len(r) > di and r[di] else 0.0)
     out = {"kernel": data[hdr.index("Kernel Name")]}
     for key, m in METRICS.items():
         if m in hdr:
@@ -56,7 +59,7 @@ def main():
     src, dst = sys.argv[1], sys.argv[2]
     os.makedirs(dst, exist_ok=True)
     res = {}
-    for name in ("sweep_points", "sweep_stored", "point_eval"):
+    for name in ("sweep_points", "sweep_pts1", "sweep_stored", "point_eval"):
         rep = os.path.join(src, name + ".ncu-rep")
         if os.path.exists(rep):
             res[name] = summarize(rep)

@@ -220,3 +220,28 @@ def test_aspot_fp32_dense_matches_oracle(ctx):
     assert g.status == o.status
     assert abs(g.cost - o.cost) <= TOL_F32_OBJ * abs(o.cost)
     assert g.feasibility_gap <= TOL_F32_VIOL
+
+
+def test_one_sided_probe(ctx):
+    """potgpu_session_time_one_sided (the bench's roofline probe of the
+    one-sided pass): both blocks time a real launch, about one full sweep's
+    time; the probed session refuses to iterate; other cost representations
+    are unsupported."""
+    inst = pot.config_instance(3, n=4096)
+    cfg = pot.SolverConfig(epsilon=1e-2, log_every=10 ** 9, record_rounded_cost=False, materialize_plan=False)
+    s = pot.Session(pot.SolverKind.Aspot, inst, cfg, ctx=ctx)
+    s.iterate(5)
+    sw = s.time_sweep(5)[0]
+    for block in (0, 1):
+        ms = s.time_one_sided(block, 5)
+        assert 0.3 * sw < ms < 3.0 * sw, (block, ms, sw)
+    with pytest.raises(pot.PotError):
+        s.iterate(1)
+    with pytest.raises(pot.PotError):
+        s.time_one_sided(2, 1)
+    s.close()
+    dense = pot.Session(pot.SolverKind.Aspot, pot.config_instance(1, n=200), cfg, ctx=ctx)
+    dense.iterate(2)
+    with pytest.raises(pot.PotError):
+        dense.time_one_sided(0, 1)
+    dense.close()
