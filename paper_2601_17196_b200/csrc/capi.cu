@@ -1214,7 +1214,7 @@ static void bc_solve_batched(Context& base, const potgpu_problem* problems, int6
   const BcLayout lay = layout_of(cs);
   const size_t smem = lay.bytes();
   if (smem > kSmemMax) throw Error(POTGPU_ERR_UNSUPPORTED, "cluster too small for n");
-  PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  raise_dyn_smem(k_batch_aspot, size_t(int(smem)));
   if (cs > 8) PG_CK(cudaFuncSetAttribute(k_batch_aspot, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute at[1];

@@ -180,6 +180,25 @@ inline bool graph_loop_enabled() {
   return on;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is one process-wide value per
+// kernel (and device), while sessions of different sizes are prepared
+// concurrently (batched workers): the limit is only ever RAISED, under a
+// lock, so a concurrent smaller session cannot lower it below what another
+// session is about to launch with.
+template <typename K>
+inline void raise_dyn_smem(K kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  PG_CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& v = cur[{dev, reinterpret_cast<const void*>(kernel)}];
+  if (bytes > v) {
+    PG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    v = bytes;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};

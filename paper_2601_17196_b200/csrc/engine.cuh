@@ -204,19 +204,16 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
     const size_t sm_est = sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)));
     switch (pts_pairs()) {
       case 2:
-        PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sweep_pts2_smem(int(kMaxRowsPerCta)))));
+        raise_dyn_smem(sweep_pts2_f32<1>, size_t(int(sweep_pts2_smem(int(kMaxRowsPerCta)))));
         PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2_f32<1>, kThreads,
                                                             sweep_pts2_smem(int(std::min<int64_t>(n, kMaxRowsPerCta)))));
         break;
       case 5:
-        PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sweep_pts_smem(int(kMaxRowsPerCta)))));
+        raise_dyn_smem(sweep_ptsR_f32<4>, size_t(int(sweep_pts_smem(int(kMaxRowsPerCta)))));
         PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_ptsR_f32<4>, kThreads, sm_est));
         break;
       case 3:
-        PG_CK(cudaFuncSetAttribute(sweep_pts2s_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sweep_pts_smem(int(kMaxRowsPerCtaS)))));
+        raise_dyn_smem(sweep_pts2s_f32, size_t(int(sweep_pts_smem(int(kMaxRowsPerCtaS)))));
         PG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_pts2s_f32, kThreads,
                                                             sweep_pts_smem(int(std::min<int64_t>(n, kMaxRowsPerCtaS)))));
         break;
@@ -233,7 +230,7 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   ws.pfmt = P.dtype == POTGPU_F64 ? PF_F64 : PF_F32_SCALED;
   const int64_t tc_cap = int64_t(cx.num_sms) * 4;
   if (use_tc) {
-    PG_CK(cudaFuncSetAttribute(sweep_tc_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sweep_tc_smem())));
+    raise_dyn_smem(sweep_tc_f32, size_t(int(sweep_tc_smem())));
   }
   ws.g = use_tc ? choose_grid_tc(n, n, tc_cap) : choose_grid(n, n, cx.num_sms, occ, ws.strip, max_rows);
   int64_t max_rb = ws.g.grid.y;
@@ -259,19 +256,24 @@ inline void prepare_workspace(Context& cx, const DevProblem& P, Workspace& ws, i
   for (const ShardGrid& sh : ws.shards) ws.pts_cs = std::min(ws.pts_cs, pts_cluster(sh.g.grid.x));
   ws.sweep_smem = P.dtype == POTGPU_F64 ? 0 : std::max(sweep_pts2_smem(max_rpc, ws.pts_cs > 1), sweep_f32_smem(max_rpc));
   if (P.dtype != POTGPU_F64) {
-    PG_CK(cudaFuncSetAttribute(sweep_f32<SrcDenseF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2s_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts1_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(std::max(ws.sweep_smem, sweep_pts1_smem(max_rpc)))));
+    raise_dyn_smem(sweep_f32<SrcDenseF32>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts2_f32<1>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts2s_f32, size_t(int(ws.sweep_smem)));
+    {
+      const int sm1 = int(std::max(ws.sweep_smem, sweep_pts1_smem(max_rpc)));
+      raise_dyn_smem(sweep_pts1_f32<0>, size_t(sm1));
+      raise_dyn_smem(sweep_pts1_f32<1>, size_t(sm1));
+      raise_dyn_smem(sweep_pts1_f32<2>, size_t(sm1));
+      raise_dyn_smem(sweep_pts1_f32<3>, size_t(sm1));
+    }
     ws.one_smem = std::max(ws.sweep_smem, sweep_pts1_smem(max_rpc));
-    PG_CK(cudaFuncSetAttribute(sweep_ptsR_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts2_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
-    PG_CK(cudaFuncSetAttribute(sweep_pts_f32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_ptsR_f32<4>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts2_f32<2>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts2_f32<4>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts2_f32<8>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts_f32<4>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts_f32<6>, size_t(int(ws.sweep_smem)));
+    raise_dyn_smem(sweep_pts_f32<8>, size_t(int(ws.sweep_smem)));
   }
   ws.nstrips = ws.g.grid.x / ws.pts_cs;
   if (carry_supported(P) && ws.pts_cs == 1) {
@@ -513,7 +515,12 @@ inline void launch_one_sided(Context& cx, const DevProblem& P, Workspace& ws, Sl
   a.gate = gate;
   a.gamma = 0.0;
   SrcPointsDotF32 s{P.XD4.p, P.YS4.p};
-  launch_k(sweep_pts1_f32, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o);
+  switch (pts1_two()) {
+    case 1: launch_k(sweep_pts1_f32<1>, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o); break;
+    case 2: launch_k(sweep_pts1_f32<2>, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o); break;
+    case 3: launch_k(sweep_pts1_f32<3>, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o); break;
+    default: launch_k(sweep_pts1_f32<0>, dim3(g.grid), dim3(kThreads), ws.one_smem, cx.stream, s, a, o); break;
+  }
 }
 
 // Where an attempt's deferred decisions find their partials (aspot_kernels.cuh Pending).

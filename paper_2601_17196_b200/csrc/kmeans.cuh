@@ -116,7 +116,7 @@ inline int kmeans_quantize(Context& cx, const double* pts_h, int64_t n, int k, u
   PG_CK(cudaMemcpyAsync(pts.p, pts_h, size_t(3 * n) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));
   const int ablocks = int(std::min<int64_t>(ceil_div(n, 256), int64_t(cx.num_sms) * 8));
   const size_t csmem = size_t(3 * k) * sizeof(double);
-  if (csmem > 48 * 1024) PG_CK(cudaFuncSetAttribute(k_km_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csmem)));
+  if (csmem > 48 * 1024) raise_dyn_smem(k_km_assign, size_t(int(csmem)));
   std::vector<double> R(static_cast<size_t>(4 * k));
   auto cluster_sums = [&]() {
     PG_CK(cudaMemcpyAsync(Cd.p, C.data(), size_t(3 * k) * sizeof(double), cudaMemcpyHostToDevice, cx.stream));

@@ -441,6 +441,21 @@ __device__ __forceinline__ float tree_sum2(const float2 (&t)[KP]) {
   return m[0].x + m[0].y;
 }
 
+// sum_q (t_q . g_q) over a lane's KP column pairs as two FFMA2 chains
+// (KP + 2 operations instead of the 2 KP of a product array + sum tree).
+template <int KP>
+__device__ __forceinline__ float wsum2(const float2 (&t)[KP], const float2 (&g)[KP]) {
+  static_assert(KP % 2 == 0, "pairs in two chains");
+  float2 a0 = __fmul2_rn(t[0], g[0]), a1 = __fmul2_rn(t[1], g[1]);
+#pragma unroll
+  for (int q = 2; q < KP; q += 2) {
+    a0 = __ffma2_rn(t[q], g[q], a0);
+    a1 = __ffma2_rn(t[q + 1], g[q + 1], a1);
+  }
+  const float2 s = __fadd2_rn(a0, a1);
+  return s.x + s.y;
+}
+
 // KP column pairs per lane (2 KP columns, a 64 KP-column warp strip); KP = 8
 // matches sweep_f32's map. Fewer pairs -> fewer registers -> more resident
 // warps to cover the per-row dependency chain (profiles/pts_variants.sh).
@@ -1447,6 +1462,9 @@ __device__ __forceinline__ float2 encode_sum(double R, double off) {  // (S, M):
   return make_float2(float(R * exp2(-(M + off))), float(M));
 }
 
+// TWO: rows i and i + 8 per warp step, as sweep_pts2_f32 (both rows' dot
+// products share each column operand, two independent MUFU bursts in flight).
+template <int TWO>
 __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 src, SweepArgs a, OneSidedArgs o) {
   pdl_wait();
   constexpr int KP = kPairs;
@@ -1581,7 +1599,68 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
 #pragma unroll
     for (int q = 0; q < KP; ++q) cacc[q] = cacc2[q] = make_float2(0.f, 0.f);
     float sigma = -INFINITY, sigma2 = -INFINITY;
-    for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+    int64_t i = r0 + warp;
+    if constexpr ((TWO & 1) != 0) {
+      for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8
+        const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+        const float ma = s_M[i - r0], mb = s_M[i + kWarps - r0];
+        const bool la = ma != -INFINITY, lb = mb != -INFINITY;  // an empty segment has t = -inf throughout: exact zeros
+        if (!la && !lb) continue;
+        float2 ta[KP], tb[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 B = s_B[q][lane];
+          float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+          float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
+          xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+          xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
+          ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+          tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+        }
+        const float msa = la ? ma : 0.f, msb = lb ? mb : 0.f;
+        const float mAa = ma + da.w, mAb = mb + db.w;
+        const float mAx = fmaxf(mAa, mAb);
+        mmax = fmaxf(mmax, mAx);
+        if (mAx > sigma) {
+          const float sc = ex2f(sigma - mAx);
+#pragma unroll
+          for (int q = 0; q < KP; ++q) cacc[q] = __fmul2_rn(cacc[q], make_float2(sc, sc));
+          sigma = mAx;
+        }
+        const float fa = la ? ex2f(mAa - sigma) : 0.f, fb = lb ? ex2f(mAb - sigma) : 0.f;
+        const float2 Fa = make_float2(fa, fa), Fb = make_float2(fb, fb);
+        float2 Ga = make_float2(0.f, 0.f), Gb = Ga;
+        if (fuse) {
+          const float mA2a = ma + s_A2[i - r0], mA2b = mb + s_A2[i + kWarps - r0];
+          const float mA2x = fmaxf(mA2a, mA2b);
+          mmax2 = fmaxf(mmax2, mA2x);
+          if (mA2x > sigma2) {
+            const float sc = ex2f(sigma2 - mA2x);
+#pragma unroll
+            for (int q = 0; q < KP; ++q) cacc2[q] = __fmul2_rn(cacc2[q], make_float2(sc, sc));
+            sigma2 = mA2x;
+          }
+          const float ga = la ? ex2f(mA2a - sigma2) : 0.f, gb = lb ? ex2f(mA2b - sigma2) : 0.f;
+          Ga = make_float2(ga, ga);
+          Gb = make_float2(gb, gb);
+        }
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 e = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+          const float2 x = make_float2(ex2f(e.x), ex2f(e.y));
+          cacc[q] = __ffma2_rn(x, Fa, cacc[q]);
+          if (fuse) cacc2[q] = __ffma2_rn(x, Ga, cacc2[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < KP; ++q) {
+          const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
+          const float2 x = make_float2(ex2f(e.x), ex2f(e.y));
+          cacc[q] = __ffma2_rn(x, Fb, cacc[q]);
+          if (fuse) cacc2[q] = __ffma2_rn(x, Gb, cacc2[q]);
+        }
+      }
+    }
+    for (; i < r1; i += kWarps) {
       const float4 d = s_R[i - r0];
       const float m = s_M[i - r0];
       if (m == -INFINITY) continue;  // empty segment (warp-uniform)
@@ -1691,7 +1770,56 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
     }
     __syncwarp();
   };
-  for (int64_t i = r0 + warp; i < r1; i += kWarps) {
+  int64_t i = r0 + warp;
+  if constexpr ((TWO & 2) != 0) {
+    for (; i + kWarps < r1; i += 2 * kWarps) {  // rows i and i + 8 (slots slot and slot + 1)
+      const float4 da = s_R[i - r0], db = s_R[i + kWarps - r0];
+      float2 ta[KP], tb[KP];
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 B = s_B[q][lane];
+        float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
+        float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
+        xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
+        xb = __ffma2_rn(make_float2(db.y, db.y), cy[q], xb);
+        ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
+        tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
+      }
+      const float lma = tree_max2<KP>(ta), lmb = tree_max2<KP>(tb);
+      mmax = fmaxf(mmax, fmaxf(lma + da.w, lmb + db.w));
+      const float sma = s_M[i - r0], smb = s_M[i + kWarps - r0];
+      const float ma = exact ? warp_maxf(lma) : (sma == -INFINITY ? -INFINITY : sma + dvmax);
+      const float mb = exact ? warp_maxf(lmb) : (smb == -INFINITY ? -INFINITY : smb + dvmax);
+      const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 e = __fadd2_rn(ta[q], make_float2(-msa, -msa));
+        ta[q] = make_float2(ex2f(e.x), ex2f(e.y));
+      }
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const float2 e = __fadd2_rn(tb[q], make_float2(-msb, -msb));
+        tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
+      }
+      tile[slot * 33 + lane] = tree_sum2<KP>(ta);
+      tile[(slot + 1) * 33 + lane] = tree_sum2<KP>(tb);
+      if (fuse) {
+        mmax2 = fmaxf(mmax2, fmaxf(lma + s_A2[i - r0], lmb + s_A2[i + kWarps - r0]));
+        tile[(kSlotRows + slot) * 33 + lane] = wsum2<KP>(ta, gw);
+        tile[(kSlotRows + slot + 1) * 33 + lane] = wsum2<KP>(tb, gw);
+      }
+      if ((lane & 15) == slot) my_ms = msa;
+      if ((lane & 15) == slot + 1) my_ms = msb;
+      slot += 2;
+      if (slot == kSlotRows) {
+        flush(kSlotRows);
+        slot = 0;
+        ib = i + 2 * kWarps;
+      }
+    }
+    // an odd slot count before the single-row tail: the tail keeps filling the same batch
+  }
+  for (; i < r1; i += kWarps) {
     const float4 d = s_R[i - r0];
     float2 t[KP];
     dots(d, t);
@@ -1771,6 +1899,17 @@ inline int pts_pairs() {
     const char* e = std::getenv("POTGPU_PTS_PAIRS");
     const int k = e ? std::atoi(e) : 0;
     return (k == 2 || k == 3 || k == 4 || k == 5 || k == 6 || k == 8) ? k : 2;  // 2: the two-row 8-pair variant (default); 3: its smem-column form
+  }();
+  return v;
+}
+
+// $POTGPU_PTS1_TWO: two rows per warp step in the one-sided pass
+// (sweep_pts1_f32<TWO>): bit 0 = its block-u loop, bit 1 = its block-v loop.
+inline int pts1_two() {
+  static const int v = [] {
+    const char* e = std::getenv("POTGPU_PTS1_TWO");
+    const int k = e ? std::atoi(e) : 0;
+    return (k >= 0 && k <= 3) ? k : 0;
   }();
   return v;
 }
