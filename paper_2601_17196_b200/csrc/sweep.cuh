@@ -1905,11 +1905,15 @@ inline int pts_pairs() {
 
 // $POTGPU_PTS1_TWO: two rows per warp step in the one-sided pass
 // (sweep_pts1_f32<TWO>): bit 0 = its block-u loop, bit 1 = its block-v loop.
+// Default 3. Measured on B200 (tools/one_sided_times.py,
+// profiles/r02/pts1_two_rows_ab.jsonl): C3 block u 0.1302 -> 0.1204 ms, block v
+// 0.1331 -> 0.1257 ms, 3417 -> 3509 it/s; C4 1.60 -> 1.44 / 1.83 -> 1.68 ms,
+// 283.4 -> 296.5 it/s.
 inline int pts1_two() {
   static const int v = [] {
     const char* e = std::getenv("POTGPU_PTS1_TWO");
-    const int k = e ? std::atoi(e) : 0;
-    return (k >= 0 && k <= 3) ? k : 0;
+    const int k = e ? std::atoi(e) : 3;
+    return (k >= 0 && k <= 3) ? k : 3;
   }();
   return v;
 }

@@ -95,25 +95,28 @@ def test_c4_prefix_matches_unfused():
 
 
 def test_small_n_same_trajectory_as_unfused():
-    """n = 2048 (configs[2] shape): run to convergence the K1'' solve stops 5
-    iterations after the unfused one (1851 vs 1846, the fp64 oracle's count).
-    Late in the solve the greedy block choice cycles through near-ties of its
-    rho-scores; one choice delayed by an iteration leaves two solves one
-    iteration out of phase, and E_t / the rounded cost oscillate with that
-    phase (~20 % / ~0.3 %) while the dual objective does not (measured:
-    profiles/r02/k1pp_small_2048.jsonl, tools/k1pp_logs.py). So: the same
+    """n = 2048 (configs[2] shape): run to convergence the K1'' and the unfused
+    solves can stop a few iterations apart (measured 1851 vs 1846, and 1846 vs
+    1850 after a change of summation order in the one-sided pass; the fp64
+    oracle: 1846). Late in the solve the greedy block choice cycles through
+    near-ties of its rho-scores; one choice delayed by an iteration leaves two
+    solves one iteration out of phase, and E_t / the rounded cost oscillate
+    with that phase (~20 % / ~0.3 %) while the dual objective does not
+    (profiles/r02/k1pp_small_2048.jsonl, tools/k1pp_logs.py). So: the same
     decisions and E_t to the fp32 bar before the first near-tie, phi to 1e-6 at
-    EVERY iteration, iteration counts within 1 %, and the cost at the unfused
-    stop within the phase's 5e-3."""
-    b = run({"POTGPU_K1PP": "0"}, 3, 2048, 0, 1e-2)
-    a = run({}, 3, 2048, b["iterations"], 1e-2)
-    full = run({}, 3, 2048, 0, 1e-2)
-    assert b["status"] == 0 and full["status"] == 0
-    assert abs(full["iterations"] - b["iterations"]) <= 0.01 * b["iterations"]
-    assert a["iterations"] == b["iterations"]
-    assert a["gap"] <= 1e-5 and full["gap"] <= 1e-5
-    k = 900  # before the first fp32 near-tie (iteration 997)
-    assert np.array_equal(a["log"][:k, 2:5], b["log"][:k, 2:5])
-    np.testing.assert_allclose(a["log"][:k, 5], b["log"][:k, 5], rtol=1e-4)
-    np.testing.assert_allclose(a["log"][:, 6:8], b["log"][:, 6:8], rtol=1e-6)  # phi(z_check), phi(z_hat): every iteration
+    EVERY iteration up to the earlier stop, iteration counts within 1 %, and
+    the cost at the earlier stop within the phase's 5e-3."""
+    fa = run({}, 3, 2048, 0, 1e-2)
+    fb = run({"POTGPU_K1PP": "0"}, 3, 2048, 0, 1e-2)
+    assert fa["status"] == 0 and fb["status"] == 0
+    assert abs(fa["iterations"] - fb["iterations"]) <= 0.01 * fb["iterations"]
+    assert fa["gap"] <= 1e-5 and fb["gap"] <= 1e-5
+    k = min(fa["iterations"], fb["iterations"])
+    a = fa if fa["iterations"] == k else run({}, 3, 2048, k, 1e-2)
+    b = fb if fb["iterations"] == k else run({"POTGPU_K1PP": "0"}, 3, 2048, k, 1e-2)
+    assert a["iterations"] == b["iterations"] == k
+    pre = 900  # before the first fp32 near-tie (iteration 997)
+    assert np.array_equal(a["log"][:pre, 2:5], b["log"][:pre, 2:5])
+    np.testing.assert_allclose(a["log"][:pre, 5], b["log"][:pre, 5], rtol=1e-4)
+    np.testing.assert_allclose(a["log"][:k, 6:8], b["log"][:k, 6:8], rtol=1e-6)  # phi(z_check), phi(z_hat): every iteration
     assert abs(a["cost"] - b["cost"]) <= 5e-3 * abs(b["cost"])

@@ -48,6 +48,8 @@ def baseline():
 @pytest.mark.parametrize("env", [
     {"POTGPU_GRAPH_LOOP": "1"},
     {"POTGPU_ONE_SIDED": "0"},
+    {"POTGPU_K1PP": "0"},
+    {"POTGPU_PTS1_TWO": "0"},
     {"POTGPU_PDL": "0"},
     {"POTGPU_EVAL_TPI": "1"},
     {"POTGPU_EVAL_BLOCKS_PER_SM": "1"},
