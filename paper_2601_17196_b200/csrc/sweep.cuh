@@ -1490,19 +1490,39 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
   float2* colp = reinterpret_cast<float2*>(a.colp);
   float2* rowp2 = reinterpret_cast<float2*>(o.rowp2);
   float2* colp2 = reinterpret_cast<float2*>(o.colp2);
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
-    double A = (a.u[i] + w) * kLog2e;
-    if (a.rowshift) A = A + a.rowshift[i];
-    const float4 x2 = src.X2[i];
-    s_R[i - r0] = make_float4(x2.x, x2.y, x2.z, float(A));
-    const float2 pp = rowp[i * ldp + blockIdx.x];  // read before this thread overwrites it
-    s_M[i - r0] = pp.x != 0.f ? pp.y : -INFINITY;
-    if (mode == 0) rowp[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.krow[i], A) : make_float2(0.f, 0.f);
-    if (fuse) {
-      double A2 = (o.u2[i] + w2) * kLog2e;
-      if (a.rowshift) A2 = A2 + a.rowshift[i];
-      s_A2[i - r0] = float(A2);
-      if (mode == 0) rowp2[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.kbar_row[i], A2) : make_float2(0.f, 0.f);
+  // rows in batches of 4 per thread: all of a batch's loads (the source's partial is a scattered
+  // 8-byte read per row) are issued before its stores, which the compiler could not hoist them over
+  for (int64_t ib0 = r0 + threadIdx.x; ib0 < r1; ib0 += 4 * kThreads) {
+    double uu[4], rs[4], u2[4];
+    float4 x2[4];
+    float2 pp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = ib0 + int64_t(k) * kThreads;
+      if (i < r1) {
+        uu[k] = a.u[i];
+        rs[k] = a.rowshift ? a.rowshift[i] : 0.0;
+        x2[k] = src.X2[i];
+        pp[k] = rowp[i * ldp + blockIdx.x];  // read before this thread overwrites it
+        u2[k] = fuse ? o.u2[i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = ib0 + int64_t(k) * kThreads;
+      if (i < r1) {
+        double A = (uu[k] + w) * kLog2e;
+        if (a.rowshift) A = A + rs[k];
+        s_R[i - r0] = make_float4(x2[k].x, x2[k].y, x2[k].z, float(A));
+        s_M[i - r0] = pp[k].x != 0.f ? pp[k].y : -INFINITY;
+        if (mode == 0) rowp[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.krow[i], A) : make_float2(0.f, 0.f);
+        if (fuse) {
+          double A2 = (u2[k] + w2) * kLog2e;
+          if (a.rowshift) A2 = A2 + rs[k];
+          s_A2[i - r0] = float(A2);
+          if (mode == 0) rowp2[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.kbar_row[i], A2) : make_float2(0.f, 0.f);
+        }
+      }
     }
   }
   float2 cx[KP], cy[KP], cz[KP];
