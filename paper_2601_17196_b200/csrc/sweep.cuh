@@ -1485,13 +1485,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
   float* s_M = s_tiles + kWarps * 32 * 33;
   float* s_A2 = s_M + ((a.rows_per_cta + 3) & ~3);
   __shared__ float2 s_B[KP][32];
-  __shared__ float s_dv[4][kWarps];
+  __shared__ float s_dv[5][kWarps];
   float2* rowp = reinterpret_cast<float2*>(a.rowp);
   float2* colp = reinterpret_cast<float2*>(a.colp);
   float2* rowp2 = reinterpret_cast<float2*>(o.rowp2);
   float2* colp2 = reinterpret_cast<float2*>(o.colp2);
   // rows in batches of 4 per thread: all of a batch's loads (the source's partial is a scattered
   // 8-byte read per row) are issued before its stores, which the compiler could not hoist them over
+  float rbnd = -INFINITY;  // max over this thread's rows of (source segment max + row offset): bounds the exponents
   for (int64_t ib0 = r0 + threadIdx.x; ib0 < r1; ib0 += 4 * kThreads) {
     double uu[4], rs[4], u2[4];
     float4 x2[4];
@@ -1514,12 +1515,15 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
         double A = (uu[k] + w) * kLog2e;
         if (a.rowshift) A = A + rs[k];
         s_R[i - r0] = make_float4(x2[k].x, x2[k].y, x2[k].z, float(A));
-        s_M[i - r0] = pp[k].x != 0.f ? pp[k].y : -INFINITY;
+        const float smk = pp[k].x != 0.f ? pp[k].y : -INFINITY;
+        s_M[i - r0] = smk;
+        rbnd = fmaxf(rbnd, smk + float(A));
         if (mode == 0) rowp[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.krow[i], A) : make_float2(0.f, 0.f);
         if (fuse) {
           double A2 = (u2[k] + w2) * kLog2e;
           if (a.rowshift) A2 = A2 + rs[k];
           s_A2[i - r0] = float(A2);
+          rbnd = fmaxf(rbnd, smk + float(A2));
           if (mode == 0) rowp2[i * ldp + blockIdx.x] = blockIdx.x == 0 ? encode_sum(o.kbar_row[i], A2) : make_float2(0.f, 0.f);
         }
       }
@@ -1574,9 +1578,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       emin = -warp_maxf(-emin);
       ebad = __any_sync(0xffffffffu, ebad);
     }
+    rbnd = warp_maxf(rbnd);
     if (lane == 0) {
       s_dv[0][warp] = dmax; s_dv[1][warp] = dmin;
       s_dv[2][warp] = ebad ? NAN : emax; s_dv[3][warp] = emin;
+      s_dv[4][warp] = rbnd;
     }
     for (int c = threadIdx.x; c < kStrip; c += kThreads)  // the known column sums
       if (j0 + c < n) {
@@ -1604,6 +1610,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
     if (!(evmax > -INFINITY)) evmax = 0.f;
   }
   const bool exact = mode == 1 && !(dvmax - dvmin <= kOneSidedSpread);  // CTA-uniform
+  // Block v: the max exponent of a row segment (the reference's overflow test, dual.hpp:85-90) is
+  // bounded by its shift m_i = (source segment max) + dvmax. Far below the threshold the bound
+  // decides the test like the exact value, and the per-row max tree is skipped; a CTA whose bound
+  // comes within a few units of it (or takes the exact shifts anyway) computes the exact maxima.
+  bool need_lm = exact;
+  if (mode == 1) {
+    float bcta = -INFINITY;
+    for (int ww = 0; ww < kWarps; ++ww) bcta = fmaxf(bcta, s_dv[4][ww]);
+    const float ub = bcta + dvmax + (fuse ? fmaxf(evmax, 0.f) : 0.f);
+    if (!(double(ub) * kLn2 <= kMaxExponent - 20.0)) need_lm = true;  // also NaN
+  }
   float mmax = -INFINITY, mmax2 = -INFINITY;
   auto dots = [&](const float4& d, float2 (&t)[KP]) {
 #pragma unroll
@@ -1805,11 +1822,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
         ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
         tb[q] = __ffma2_rn(make_float2(db.z, db.z), cz[q], xb);
       }
-      const float lma = tree_max2<KP>(ta), lmb = tree_max2<KP>(tb);
-      mmax = fmaxf(mmax, fmaxf(lma + da.w, lmb + db.w));
+      float lma = -INFINITY, lmb = -INFINITY;
+      if (need_lm) { lma = tree_max2<KP>(ta); lmb = tree_max2<KP>(tb); }
       const float sma = s_M[i - r0], smb = s_M[i + kWarps - r0];
       const float ma = exact ? warp_maxf(lma) : (sma == -INFINITY ? -INFINITY : sma + dvmax);
       const float mb = exact ? warp_maxf(lmb) : (smb == -INFINITY ? -INFINITY : smb + dvmax);
+      if (!need_lm) { lma = ma; lmb = mb; }  // the shifts bound the segment maxima
+      mmax = fmaxf(mmax, fmaxf(lma + da.w, lmb + db.w));
       const float msa = (ma == -INFINITY) ? 0.f : ma, msb = (mb == -INFINITY) ? 0.f : mb;
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
@@ -1843,10 +1862,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
     const float4 d = s_R[i - r0];
     float2 t[KP];
     dots(d, t);
-    const float lm = tree_max2<KP>(t);
-    mmax = fmaxf(mmax, lm + d.w);
+    float lm = need_lm ? tree_max2<KP>(t) : -INFINITY;
     const float sm = s_M[i - r0];
     const float m = exact ? warp_maxf(lm) : (sm == -INFINITY ? -INFINITY : sm + dvmax);
+    if (!need_lm) lm = m;  // the shift bounds the segment maximum
+    mmax = fmaxf(mmax, lm + d.w);
     const float ms = (m == -INFINITY) ? 0.f : m;
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
