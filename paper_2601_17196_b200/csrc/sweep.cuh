@@ -658,7 +658,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
   const double w = *a.w;
   const bool use_carry = CS == 1 && a.carry != nullptr;
   extern __shared__ float4 s_R[];  // [rows_per_cta]: (2x', A_i) or (2x', s_i), then the row-sum tiles, then (f_i, A_i)
-  __shared__ float2 s_B[KP][32];
+  // column constants B'_j of the strip, two column pairs per 16-byte word (one LDS.128 per two pairs)
+  __shared__ float4 s_B4[KP / 2][32];
+  auto Bof = [&](int q, int l) -> float2 {
+    const float4 v = s_B4[q >> 1][l];
+    return (q & 1) ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
+  };
   __shared__ float s_red[3][kWarps];
   float2* s_FA = reinterpret_cast<float2*>(reinterpret_cast<float*>(s_R + a.rows_per_cta) + kWarps * 32 * 33 +
                                            (CS > 1 ? 2 * a.rows_per_cta : 0));
@@ -692,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
         }
       }
     }
-    if (warp == 0) s_B[q][lane] = make_float2(b[0], b[1]);
+    if (warp == 0) reinterpret_cast<float2*>(&s_B4[q >> 1][lane])[q & 1] = make_float2(b[0], b[1]);
     cx[q] = make_float2(y[0].x, y[1].x);
     cy[q] = make_float2(y[0].y, y[1].y);
     cz[q] = make_float2(y[0].z, y[1].z);
@@ -831,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float2 ta[KP], tb[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const float2 B = s_B[q][lane];
+        const float2 B = Bof(q, lane);
         float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
         float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
         xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
@@ -852,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float2 ta[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const float2 B = s_B[q][lane];
+        const float2 B = Bof(q, lane);
         float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
         xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
         xa = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
@@ -867,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float2 ta[KP], tb[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const float2 B = s_B[q][lane];
+        const float2 B = Bof(q, lane);
         float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
         float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
         xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
@@ -919,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
       float2 ta[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const float2 B = s_B[q][lane];
+        const float2 B = Bof(q, lane);
         float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
         xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
         ta[q] = __ffma2_rn(make_float2(da.z, da.z), cz[q], xa);
@@ -958,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
         float2 t[KP];
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
-          const float2 B = s_B[q][lane];
+          const float2 B = Bof(q, lane);
           float2 x = __ffma2_rn(make_float2(d.x, d.x), cx[q], B);
           x = __ffma2_rn(make_float2(d.y, d.y), cy[q], x);
           t[q] = __ffma2_rn(make_float2(d.z, d.z), cz[q], x);
@@ -1032,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
     if (s_last) {
       for (int k = threadIdx.x; k < kStrip; k += kThreads) {
         const int q = k >> 5, l = k & 31;
-        const float2 b = s_B[q][l];
+        const float2 b = Bof(q, l);
         const int64_t jj = f32_col(j0, l, q, 0);
         if (jj < n) a.carry_b[jj] = b.x;
         if (jj + 1 < n) a.carry_b[jj + 1] = b.y;
@@ -1484,7 +1489,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
   float* s_tiles = reinterpret_cast<float*>(s_R + a.rows_per_cta);
   float* s_M = s_tiles + kWarps * 32 * 33;
   float* s_A2 = s_M + ((a.rows_per_cta + 3) & ~3);
-  __shared__ float2 s_B[KP][32];
+  // column constants B'_j of the strip, two column pairs per 16-byte word (one LDS.128 per two pairs)
+  __shared__ float4 s_B4[KP / 2][32];
+  auto Bof = [&](int q, int l) -> float2 {
+    const float4 v = s_B4[q >> 1][l];
+    return (q & 1) ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
+  };
   __shared__ float s_dv[5][kWarps];
   float2* rowp = reinterpret_cast<float2*>(a.rowp);
   float2* colp = reinterpret_cast<float2*>(a.colp);
@@ -1564,7 +1574,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       }
       b[h] = float(vv);
     }
-    if (warp == 0) s_B[q][lane] = make_float2(b[0], b[1]);
+    if (warp == 0) reinterpret_cast<float2*>(&s_B4[q >> 1][lane])[q & 1] = make_float2(b[0], b[1]);
     cx[q] = make_float2(y[0].x, y[1].x);
     cy[q] = make_float2(y[0].y, y[1].y);
     cz[q] = make_float2(y[0].z, y[1].z);
@@ -1625,7 +1635,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
   auto dots = [&](const float4& d, float2 (&t)[KP]) {
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
-      const float2 B = s_B[q][lane];
+      const float2 B = Bof(q, lane);
       float2 x = __ffma2_rn(make_float2(d.x, d.x), cx[q], B);
       x = __ffma2_rn(make_float2(d.y, d.y), cy[q], x);
       t[q] = __ffma2_rn(make_float2(d.z, d.z), cz[q], x);
@@ -1646,7 +1656,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
         float2 ta[KP], tb[KP];
 #pragma unroll
         for (int q = 0; q < KP; ++q) {
-          const float2 B = s_B[q][lane];
+          const float2 B = Bof(q, lane);
           float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
           float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
           xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
@@ -1814,7 +1824,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts1_f32(SrcPointsDotF32 sr
       float2 ta[KP], tb[KP];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const float2 B = s_B[q][lane];
+        const float2 B = Bof(q, lane);
         float2 xa = __ffma2_rn(make_float2(da.x, da.x), cx[q], B);
         float2 xb = __ffma2_rn(make_float2(db.x, db.x), cx[q], B);
         xa = __ffma2_rn(make_float2(da.y, da.y), cy[q], xa);
