@@ -914,10 +914,19 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_pts2_f32(SrcPointsDotF32 sr
         tb[q] = make_float2(ex2f(e.x), ex2f(e.y));
         cacc[q] = __ffma2_rn(tb[q], Fb, cacc[q]);
       }
-      *tslot = tree_sum2<KP>(ta);
-      next_slot(msa, i);
-      *tslot = tree_sum2<KP>(tb);
-      next_slot(msb, i + kWarps);
+      // both rows' tile slots in one step (the slot count is even here: only two-row steps precede)
+      tslot[0] = tree_sum2<KP>(ta);
+      tslot[33] = tree_sum2<KP>(tb);
+      tslot += 66;
+      if (lane == slot) my_ms = msa;
+      if (lane == slot + 1) my_ms = msb;
+      slot += 2;
+      if (slot == 32) {
+        flush(32);
+        slot = 0;
+        tslot = tile + lane;
+        ib = i + 2 * kWarps;
+      }
     }
     if (i < r1) {  // a last single row
       const float4 da = s_R[i - r0];
